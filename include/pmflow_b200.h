@@ -1,0 +1,138 @@
+/*
+ * pmflow_b200.h -- C ABI of the B200-native supergraph min-cut engine.
+ *
+ * Plain pointers and sizes only (no torch / CUDA types in signatures).  Every
+ * entry point is reentrant per solver handle; distinct handles may be driven
+ * from distinct host threads concurrently (the Python shim calls through
+ * ctypes, which drops the GIL).
+ *
+ * Reference interfaces replaced (paths under /root/reference/pkg/src/pmflow):
+ *
+ *   pmf_solve_composites   supergraph.py:190-207  solve_composite(g, layout)
+ *                          (and, with nseg == 0, solvers.py:188-191
+ *                          maxflow_pushrelabel).  Several composites may be
+ *                          solved in one device batch; the ThreadedBackend
+ *                          default local solver (scheduler.py:141-142) and
+ *                          WorkerServer(solve_fn=...) (rpc.py:92-100) call it.
+ *   pmf_solve_seed_batch   supergraph.py:227-253 build_seed_supergraph +
+ *                          supergraph.py:190-207 solve_composite +
+ *                          supergraph.py:157-187 split, fused on device:
+ *                          SeedProblem planes in, per-(problem, lambda)
+ *                          flows and canonical label masks out.  Also serves
+ *                          parametric.py:180-183 solve_schedule_sequential.
+ *
+ * Status codes map 1:1 onto the reference exception classes (see
+ * paper_1509_06004_b200/_native.py): PMF_ERR_NOCONV -> SolverError
+ * (solvers.py:137-139), PMF_ERR_NONMAX -> NonMaximalFlowError
+ * (solvers.py:156-157,183-184), PMF_ERR_RANGE -> CapacityOverflowError
+ * (grid.py:45-46), PMF_ERR_ARG -> ValueError, PMF_ERR_CUDA -> RuntimeError.
+ */
+#ifndef PMFLOW_B200_H
+#define PMFLOW_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define PMF_OK 0
+#define PMF_ERR_ARG (-1)
+#define PMF_ERR_CUDA (-2)
+#define PMF_ERR_NOCONV (-3)
+#define PMF_ERR_NONMAX (-4)
+#define PMF_ERR_RANGE (-5)
+
+#define PMF_SWAP_AUTO 0
+#define PMF_SWAP_ON 1
+#define PMF_SWAP_OFF 2
+
+typedef struct pmf_solver pmf_solver;
+
+/* Counters and device timings of the last solve on a handle. */
+typedef struct pmf_stats {
+    int64_t cycles;             /* global-relabel / discharge cycles          */
+    int64_t push_tile_passes;   /* 32x32 tiles discharged                     */
+    int64_t bfs_tile_passes;    /* tiles relaxed by the sink-distance BFS     */
+    int64_t label_tile_passes;  /* tiles relaxed by the source-side BFS       */
+    int64_t push_sweeps;        /* push kernel launches                       */
+    int64_t bfs_sweeps;         /* BFS kernel launches (both BFS kinds)       */
+    int64_t full_passes;        /* whole-state passes (init/seed/emit)        */
+    int64_t grids;              /* independent grids solved                   */
+    int64_t tiles;              /* tiles in the batch                         */
+    int64_t pixels;             /* real (unpadded) pixels in the batch        */
+    int32_t edge_bytes;         /* residual storage per pixel: 4 (u8x4) / 16 */
+    int32_t timed;              /* 1 if the ms fields below are valid         */
+    double ms_total;            /* device time of the whole solve             */
+    double ms_build;            /* build / load kernels                       */
+    double ms_push;             /* push-relabel sweeps                        */
+    double ms_bfs;              /* sink-distance BFS sweeps + init            */
+    double ms_labels;           /* source-side BFS + emit                     */
+    double ms_seed;             /* active-tile seeding passes                 */
+    double ms_h2d;              /* host->device copies                        */
+    double ms_d2h;              /* device->host copies                        */
+} pmf_stats;
+
+/* Create / destroy a solver bound to one CUDA device and its own stream. */
+int pmf_solver_create(int32_t device, pmf_solver **out);
+int pmf_solver_destroy(pmf_solver *s);
+
+/* Tuning knobs: "push_iters" (inner smem iterations per tile pass),
+ * "push_sweeps" (push launches per global relabel), "bfs_chunk" (BFS
+ * launches between convergence checks), "timing" (0/1 device timings),
+ * "max_cycles" (non-convergence guard). Returns PMF_ERR_ARG if unknown. */
+int pmf_solver_set(pmf_solver *s, const char *name, int64_t value);
+
+/* Thread-local message describing the last error on this thread. */
+const char *pmf_last_error(void);
+
+/* Statistics of the last solve on this handle (copied into *out). */
+int pmf_solver_stats(const pmf_solver *s, pmf_stats *out);
+
+/*
+ * Solve ncomp independent (composite) grid graphs in one device batch.
+ * Composite c: width[c] x height[c] pixels, row-major; src[c], snk[c] are
+ * (n) arrays, nbr[c] is (4, n) in direction order LEFT, RIGHT, UP, DOWN --
+ * the admitted int64 capacities of GridGraph (grid.py:56-99).  nseg[c]
+ * segments with column offset / width / swapped flag describe the layout
+ * (supergraph.py:39-64); nseg[c] == 0 means layout None.
+ * Outputs: flow_out[c] (int64) and labels_out[c] (n bytes, 1 = source
+ * side; swapped spans carry the complement of the sink side over all rows,
+ * supergraph.py:201-206).
+ */
+int pmf_solve_composites(pmf_solver *s, int32_t ncomp,
+                         const int32_t *width, const int32_t *height,
+                         const int64_t *const *src, const int64_t *const *snk,
+                         const int64_t *const *nbr,
+                         const int32_t *nseg, const int32_t *const *seg_off,
+                         const int32_t *const *seg_w, const uint8_t *const *seg_swapped,
+                         int64_t *flow_out, uint8_t *const *labels_out);
+
+/*
+ * Build and solve the lambda families of nprob SeedProblems
+ * (parametric.py:80-130) sharing one width x height, over nlam lambda
+ * values (strictly increasing, validated by the caller), on device.
+ * Per problem p: unary_base[p], unary_slope[p], sink_base[p] (n int64),
+ * pairwise[p] ((4, n) int64; identical pointers are uploaded once),
+ * fg_idx[p] / bg_idx[p] (seed flat indices, n_fg[p] / n_bg[p] entries).
+ * swap_mode: PMF_SWAP_AUTO decides per problem at lambda[(nlam-1)/2]
+ * (supergraph.py:210-212, 85-92), ON / OFF force it.
+ * Outputs: swapped_out[nprob]; flows_out[nprob*nlam] (problem-major);
+ * labels_out: nprob*nlam*n bytes, each the canonical minimal-source-side
+ * mask of the ORIGINAL (unswapped) lambda graph -- what split() returns.
+ * The caller guarantees admissibility (instantiate's checks,
+ * parametric.py:141-165); the engine re-checks the ranges it relies on.
+ */
+int pmf_solve_seed_batch(pmf_solver *s, int32_t nprob, int32_t width, int32_t height,
+                         const int64_t *const *unary_base, const int64_t *const *unary_slope,
+                         const int64_t *const *sink_base, const int64_t *const *pairwise,
+                         const int64_t *const *fg_idx, const int32_t *n_fg,
+                         const int64_t *const *bg_idx, const int32_t *n_bg,
+                         int32_t nlam, const int64_t *lambdas, int32_t swap_mode,
+                         uint8_t *swapped_out, int64_t *flows_out, uint8_t *labels_out);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* PMFLOW_B200_H */

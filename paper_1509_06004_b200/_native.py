@@ -1,0 +1,219 @@
+"""ctypes binding of libpmflow_b200.so (the C ABI in include/pmflow_b200.h).
+
+The shared library is built in-tree (``python -m paper_1509_06004_b200.build``
+or ``__graft_entry__.build()``).  There is no CPU fallback: if the library or
+a CUDA device is missing, every solver entry point raises
+``NativeUnavailable``.  Status codes map onto the reference's exception
+classes (solvers.py:33-38, grid.py:45-46).
+"""
+
+from __future__ import annotations
+
+import ctypes
+import os
+import threading
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "libpmflow_b200.so")
+
+PMF_OK, PMF_ERR_ARG, PMF_ERR_CUDA, PMF_ERR_NOCONV, PMF_ERR_NONMAX, PMF_ERR_RANGE = 0, -1, -2, -3, -4, -5
+SWAP_MODES = {"auto": 0, "on": 1, "off": 2}
+
+EXPORTS = ("pmf_solver_create", "pmf_solver_destroy", "pmf_solver_set", "pmf_last_error",
+           "pmf_solver_stats", "pmf_solve_composites", "pmf_solve_seed_batch")
+
+
+class NativeUnavailable(RuntimeError):
+    """The CUDA engine cannot run here (library not built or no GPU)."""
+
+
+class PmfStats(ctypes.Structure):
+    _fields_ = [(k, ctypes.c_int64) for k in (
+        "cycles", "push_tile_passes", "bfs_tile_passes", "label_tile_passes", "push_sweeps",
+        "bfs_sweeps", "full_passes", "grids", "tiles", "pixels")] + [
+        ("edge_bytes", ctypes.c_int32), ("timed", ctypes.c_int32)] + [
+        (k, ctypes.c_double) for k in ("ms_total", "ms_build", "ms_push", "ms_bfs", "ms_labels",
+                                       "ms_seed", "ms_h2d", "ms_d2h")]
+
+    def as_dict(self):
+        return {k: getattr(self, k) for k, _ in self._fields_}
+
+
+_lib = None
+_lib_lock = threading.Lock()
+
+
+def load_library(path: str = LIB_PATH):
+    """Load (once) and type the shared library.  Raises NativeUnavailable."""
+    global _lib
+    with _lib_lock:
+        if _lib is not None:
+            return _lib
+        if not os.path.exists(path):
+            raise NativeUnavailable(
+                f"{path} is not built; run __graft_entry__.build() (no CPU fallback exists)")
+        lib = ctypes.CDLL(path)
+        P = ctypes.POINTER
+        i32, i64, u8, vp = ctypes.c_int32, ctypes.c_int64, ctypes.c_uint8, ctypes.c_void_p
+        lib.pmf_solver_create.argtypes = [i32, P(vp)]
+        lib.pmf_solver_destroy.argtypes = [vp]
+        lib.pmf_solver_set.argtypes = [vp, ctypes.c_char_p, i64]
+        lib.pmf_last_error.argtypes = []
+        lib.pmf_last_error.restype = ctypes.c_char_p
+        lib.pmf_solver_stats.argtypes = [vp, P(PmfStats)]
+        lib.pmf_solve_composites.argtypes = [
+            vp, i32, P(i32), P(i32), P(vp), P(vp), P(vp), P(i32), P(vp), P(vp), P(vp),
+            P(i64), P(vp)]
+        lib.pmf_solve_seed_batch.argtypes = [
+            vp, i32, i32, i32, P(vp), P(vp), P(vp), P(vp), P(vp), P(i32), P(vp), P(i32),
+            i32, P(i64), i32, P(u8), P(i64), P(u8)]
+        for name in EXPORTS:
+            if name != "pmf_last_error":
+                getattr(lib, name).restype = ctypes.c_int
+        _lib = lib
+        return lib
+
+
+def _raise_for(rc: int):
+    from .grid import CapacityOverflowError
+    from .solvers import NonMaximalFlowError, SolverError
+    msg = load_library().pmf_last_error().decode(errors="replace")
+    if rc == PMF_ERR_NOCONV:
+        raise SolverError(msg)
+    if rc == PMF_ERR_NONMAX:
+        raise NonMaximalFlowError(msg)
+    if rc == PMF_ERR_RANGE:
+        raise CapacityOverflowError(msg)
+    if rc == PMF_ERR_ARG:
+        raise ValueError(msg)
+    raise RuntimeError(f"pmflow_b200 CUDA failure: {msg}")
+
+
+def _ptrs(arrays, ctype=ctypes.c_void_p):
+    return (ctype * len(arrays))(*[a.ctypes.data for a in arrays])
+
+
+class Solver:
+    """One device + one CUDA stream + its workspaces.  Not thread-safe: use
+    one per host thread (``solver_for_thread``)."""
+
+    def __init__(self, device: int = 0, **knobs):
+        lib = load_library()
+        h = ctypes.c_void_p()
+        rc = lib.pmf_solver_create(int(device), ctypes.byref(h))
+        if rc:
+            raise NativeUnavailable(lib.pmf_last_error().decode(errors="replace"))
+        self._lib, self._h, self.device = lib, h, device
+        for k, v in knobs.items():
+            self.set(k, v)
+
+    def set(self, name: str, value: int):
+        rc = self._lib.pmf_solver_set(self._h, name.encode(), int(value))
+        if rc:
+            _raise_for(rc)
+
+    def stats(self) -> dict:
+        st = PmfStats()
+        self._lib.pmf_solver_stats(self._h, ctypes.byref(st))
+        return st.as_dict()
+
+    def close(self):
+        if self._h:
+            self._lib.pmf_solver_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    # ---------------------------------------------------------------- solves
+    def solve_composites(self, items):
+        """items: [(width, height, src, snk, nbr, segments)] with segments a
+        list of (offset, width, swapped) or None.  Returns [(flow, labels)]."""
+        k = len(items)
+        keep = []
+        widths = np.array([it[0] for it in items], np.int32)
+        heights = np.array([it[1] for it in items], np.int32)
+        srcs, snks, nbrs, nsegs, offs, wids, sws, labs = [], [], [], [], [], [], [], []
+        for (w, h, src, snk, nbr, segs) in items:
+            srcs.append(np.ascontiguousarray(src, np.int64))
+            snks.append(np.ascontiguousarray(snk, np.int64))
+            nbrs.append(np.ascontiguousarray(nbr, np.int64))
+            segs = list(segs or ())
+            nsegs.append(len(segs))
+            offs.append(np.array([s[0] for s in segs] or [0], np.int32))
+            wids.append(np.array([s[1] for s in segs] or [0], np.int32))
+            sws.append(np.array([1 if s[2] else 0 for s in segs] or [0], np.uint8))
+            labs.append(np.empty(w * h, np.uint8))
+        keep += [srcs, snks, nbrs, offs, wids, sws, labs]
+        flows = np.zeros(k, np.int64)
+        nseg = np.array(nsegs, np.int32)
+        P = ctypes.POINTER
+        rc = self._lib.pmf_solve_composites(
+            self._h, k, widths.ctypes.data_as(P(ctypes.c_int32)),
+            heights.ctypes.data_as(P(ctypes.c_int32)), _ptrs(srcs), _ptrs(snks), _ptrs(nbrs),
+            nseg.ctypes.data_as(P(ctypes.c_int32)), _ptrs(offs), _ptrs(wids), _ptrs(sws),
+            flows.ctypes.data_as(P(ctypes.c_int64)), _ptrs(labs))
+        if rc:
+            _raise_for(rc)
+        return [(int(f), l) for f, l in zip(flows, labs)]
+
+    def solve_seed_batch(self, width, height, problems, lambdas, swap_mode="auto"):
+        """problems: objects with unary_base, unary_slope, sink_base, pairwise
+        (int64) and _fg_idx/_bg_idx.  Returns (swapped (P,), flows (P, K),
+        labels (P, K, n) uint8)."""
+        P_, K = len(problems), len(lambdas)
+        n = width * height
+        ub = [np.ascontiguousarray(p.unary_base, np.int64) for p in problems]
+        us = [np.ascontiguousarray(p.unary_slope, np.int64) for p in problems]
+        sb = [np.ascontiguousarray(p.sink_base, np.int64) for p in problems]
+        pw = [np.ascontiguousarray(p.pairwise, np.int64) for p in problems]
+        fg = [np.ascontiguousarray(p._fg_idx, np.int64) for p in problems]
+        bg = [np.ascontiguousarray(p._bg_idx, np.int64) for p in problems]
+        nfg = np.array([a.size for a in fg], np.int32)
+        nbg = np.array([a.size for a in bg], np.int32)
+        fgp = [a if a.size else np.zeros(1, np.int64) for a in fg]
+        bgp = [a if a.size else np.zeros(1, np.int64) for a in bg]
+        lam = np.ascontiguousarray(lambdas, np.int64)
+        swapped = np.zeros(P_, np.uint8)
+        flows = np.zeros(P_ * K, np.int64)
+        labels = np.empty((P_, K, n), np.uint8)
+        Pt = ctypes.POINTER
+        rc = self._lib.pmf_solve_seed_batch(
+            self._h, P_, width, height, _ptrs(ub), _ptrs(us), _ptrs(sb), _ptrs(pw),
+            _ptrs(fgp), nfg.ctypes.data_as(Pt(ctypes.c_int32)), _ptrs(bgp),
+            nbg.ctypes.data_as(Pt(ctypes.c_int32)), K, lam.ctypes.data_as(Pt(ctypes.c_int64)),
+            SWAP_MODES[swap_mode], swapped.ctypes.data_as(Pt(ctypes.c_uint8)),
+            flows.ctypes.data_as(Pt(ctypes.c_int64)), labels.ctypes.data_as(Pt(ctypes.c_uint8)))
+        if rc:
+            _raise_for(rc)
+        return swapped.astype(bool), flows.reshape(P_, K), labels
+
+
+_tls = threading.local()
+_knobs = {}
+
+
+def configure(**knobs):
+    """Set default knobs for solvers created afterwards (and existing ones
+    of the calling thread)."""
+    _knobs.update(knobs)
+    s = getattr(_tls, "solvers", {})
+    for sv in s.values():
+        for k, v in knobs.items():
+            sv.set(k, v)
+
+
+def solver_for_thread(device: int = 0) -> Solver:
+    """The calling thread's solver for ``device`` (created on first use)."""
+    pool = getattr(_tls, "solvers", None)
+    if pool is None:
+        pool = _tls.solvers = {}
+    s = pool.get(device)
+    if s is None:
+        s = pool[device] = Solver(device, **_knobs)
+    return s

@@ -1,0 +1,692 @@
+// engine.cu -- host driver and C ABI of the B200 supergraph min-cut engine.
+//
+// One pmf_solver = one CUDA device + one stream + grow-only device/pinned
+// workspaces.  A solve is a fixed sequence of kernel launches on that
+// stream; the host synchronises only to read worklist lengths (BFS
+// convergence, termination), never per tile.  See DESIGN.md.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <unordered_map>
+#include <vector>
+
+#include "../../include/pmflow_b200.h"
+#include "kernels.cuh"
+
+using namespace pmf;
+
+namespace {
+
+thread_local std::string g_err;
+
+int fail(int code, const char *fmt, ...) {
+    char buf[512];
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(buf, sizeof buf, fmt, ap);
+    va_end(ap);
+    g_err = buf;
+    return code;
+}
+
+#define CK(x)                                                                      \
+    do {                                                                           \
+        cudaError_t e_ = (x);                                                      \
+        if (e_ != cudaSuccess)                                                     \
+            return fail(PMF_ERR_CUDA, "%s failed: %s", #x, cudaGetErrorString(e_)); \
+    } while (0)
+
+struct DevBuf {
+    void *p = nullptr;
+    size_t cap = 0;
+    int ensure(size_t bytes) {
+        if (bytes <= cap) return 0;
+        if (p) cudaFree(p);
+        p = nullptr;
+        cap = 0;
+        size_t want = std::max<size_t>(bytes + bytes / 4, 256);
+        cudaError_t e = cudaMalloc(&p, want);
+        if (e != cudaSuccess) return fail(PMF_ERR_CUDA, "cudaMalloc(%zu): %s", want, cudaGetErrorString(e));
+        cap = want;
+        return 0;
+    }
+    template <class T> T *as() const { return (T *)p; }
+    ~DevBuf() { if (p) cudaFree(p); }
+};
+
+struct HostBuf {
+    void *p = nullptr;
+    size_t cap = 0;
+    int ensure(size_t bytes) {
+        if (bytes <= cap) return 0;
+        if (p) cudaFreeHost(p);
+        p = nullptr;
+        cap = 0;
+        size_t want = std::max<size_t>(bytes + bytes / 4, 256);
+        cudaError_t e = cudaMallocHost(&p, want);
+        if (e != cudaSuccess) return fail(PMF_ERR_CUDA, "cudaMallocHost(%zu): %s", want, cudaGetErrorString(e));
+        cap = want;
+        return 0;
+    }
+    template <class T> T *as() const { return (T *)p; }
+    ~HostBuf() { if (p) cudaFreeHost(p); }
+};
+
+enum Cat { C_BUILD = 0, C_BFS, C_PUSH, C_SEED, C_LAB, C_H2D, C_D2H, C_N };
+
+inline int64_t cdiv(int64_t a, int64_t b) { return (a + b - 1) / b; }
+
+}  // namespace
+
+struct pmf_solver {
+    int device = 0;
+    cudaStream_t st = nullptr;
+    int sms = 148;
+    int grid_push = 0, grid_bfs = 0, grid_full = 0;
+    // knobs
+    int push_iters = 32;
+    int push_sweeps = 16;
+    int bfs_chunk = 8;
+    int timing = 0;
+    int64_t max_cycles = 50000;
+    // device workspace
+    DevBuf d_w, d_h, d_r, d_lab, d_tile_grid, d_grids, d_live, d_act, d_list, d_inq, d_cnt,
+        d_snk, d_drain, d_err, d_stat, d_colswap, d_out, d_in32, d_pw, d_mask, d_off, d_lam,
+        d_swapcnt, d_swapflag;
+    HostBuf h_in32, h_pw, h_mask, h_out, h_small;
+    std::vector<cudaEvent_t> ev_pool;
+    std::vector<std::pair<int, int>> ev_marks;  // (category, event index of start)
+    size_t ev_used = 0;
+    pmf_stats stats{};
+    int edge_bytes = 4;
+
+    // ---------------------------------------------------------------- timing
+    int ev_get(cudaEvent_t *e) {
+        if (ev_used == ev_pool.size()) {
+            cudaEvent_t x;
+            CK(cudaEventCreate(&x));
+            ev_pool.push_back(x);
+        }
+        *e = ev_pool[ev_used++];
+        return 0;
+    }
+    // mark the start of a timed region of category cat
+    void tmark(int cat) {
+        if (!timing) return;
+        cudaEvent_t e;
+        if (ev_get(&e)) return;
+        cudaEventRecord(e, st);
+        ev_marks.push_back({cat, int(ev_used - 1)});
+    }
+};
+
+namespace {
+
+// --------------------------------------------------------------------------
+// batch layout
+// --------------------------------------------------------------------------
+
+struct Layout {
+    std::vector<GridDesc> grids;
+    std::vector<int32_t> tile_grid;
+    int64_t ntiles = 0, out_bytes = 0, pixels = 0;
+    void add(int32_t W, int32_t H, int32_t kind, int32_t colswap_off, int32_t prob, int32_t lam) {
+        GridDesc g{};
+        g.W = W;
+        g.H = H;
+        g.ntx = int32_t(cdiv(W, TW));
+        g.nty = int32_t(cdiv(H, TH));
+        g.tile_base = ntiles;
+        g.out_off = out_bytes;
+        g.kind = kind;
+        g.colswap_off = colswap_off;
+        g.prob = prob;
+        g.lam = lam;
+        int64_t nt = int64_t(g.ntx) * g.nty;
+        for (int64_t i = 0; i < nt; i++) tile_grid.push_back(int32_t(grids.size()));
+        ntiles += nt;
+        out_bytes += int64_t(W) * H;
+        pixels += int64_t(W) * H;
+        grids.push_back(g);
+    }
+};
+
+int setup_state(pmf_solver *s, const Layout &L, int edge_bytes, Ctx *c) {
+    const int64_t T = L.ntiles, P = T * TPIX, G = int64_t(L.grids.size());
+    if (T >= (int64_t(1) << 31) / TPIX * 64) return fail(PMF_ERR_ARG, "batch too large (%lld tiles)", (long long)T);
+    int rc = 0;
+    if ((rc = s->d_w.ensure(P * 4)) || (rc = s->d_h.ensure(P * 4)) ||
+        (rc = s->d_r.ensure(P * size_t(edge_bytes))) || (rc = s->d_lab.ensure(P)) ||
+        (rc = s->d_tile_grid.ensure(T * 4)) || (rc = s->d_grids.ensure(G * sizeof(GridDesc))) ||
+        (rc = s->d_live.ensure(G * 4)) || (rc = s->d_act.ensure(G * 4)) ||
+        (rc = s->d_list.ensure(2 * T * 4)) || (rc = s->d_inq.ensure(2 * T * 4)) ||
+        (rc = s->d_cnt.ensure(64)) || (rc = s->d_snk.ensure(G * 8)) || (rc = s->d_drain.ensure(G * 8)) ||
+        (rc = s->d_err.ensure(64)) || (rc = s->d_stat.ensure(ST_NSTAT * 8)) ||
+        (rc = s->d_out.ensure(std::max<int64_t>(L.out_bytes, 1))))
+        return rc;
+    s->edge_bytes = edge_bytes;
+    CK(cudaMemcpyAsync(s->d_tile_grid.p, L.tile_grid.data(), T * 4, cudaMemcpyHostToDevice, s->st));
+    CK(cudaMemcpyAsync(s->d_grids.p, L.grids.data(), G * sizeof(GridDesc), cudaMemcpyHostToDevice, s->st));
+    std::vector<int32_t> ones(G, 1);
+    CK(cudaMemcpyAsync(s->d_live.p, ones.data(), G * 4, cudaMemcpyHostToDevice, s->st));
+    CK(cudaMemsetAsync(s->d_act.p, 0, G * 4, s->st));
+    CK(cudaMemsetAsync(s->d_snk.p, 0, G * 8, s->st));
+    CK(cudaMemsetAsync(s->d_drain.p, 0, G * 8, s->st));
+    CK(cudaMemsetAsync(s->d_err.p, 0, 64, s->st));
+    CK(cudaMemsetAsync(s->d_stat.p, 0, ST_NSTAT * 8, s->st));
+    // the host vectors above are stack-owned: make the copies land first
+    CK(cudaStreamSynchronize(s->st));
+    Ctx x{};
+    x.w = s->d_w.as<int32_t>();
+    x.h = s->d_h.as<int32_t>();
+    x.r = s->d_r.p;
+    x.lab = s->d_lab.as<uint8_t>();
+    x.tile_grid = s->d_tile_grid.as<int32_t>();
+    x.grids = s->d_grids.as<GridDesc>();
+    x.live = s->d_live.as<int32_t>();
+    x.act = s->d_act.as<int32_t>();
+    x.list0 = s->d_list.as<int32_t>();
+    x.list1 = x.list0 + T;
+    x.inq0 = s->d_inq.as<int32_t>();
+    x.inq1 = x.inq0 + T;
+    x.cnt = s->d_cnt.as<int32_t>();
+    x.snk_sum = s->d_snk.as<int64_t>();
+    x.drain = s->d_drain.as<int64_t>();
+    x.err = s->d_err.as<int32_t>();
+    x.stat = s->d_stat.as<unsigned long long>();
+    x.colswap = s->d_colswap.as<uint8_t>();
+    x.swapflag = s->d_swapflag.as<int32_t>();
+    x.out = s->d_out.as<uint8_t>();
+    x.ntiles = T;
+    *c = x;
+    return 0;
+}
+
+int begin_phase(pmf_solver *s, const Ctx &c) {
+    CK(cudaMemsetAsync(c.cnt, 0, 3 * 4, s->st));
+    CK(cudaMemsetAsync(c.inq0, 0, size_t(2 * c.ntiles) * 4, s->st));
+    return 0;
+}
+
+int read_count(pmf_solver *s, const Ctx &c, int idx, int32_t *out) {
+    int32_t *hp = s->h_small.as<int32_t>();
+    CK(cudaMemcpyAsync(hp, c.cnt + idx, 4, cudaMemcpyDeviceToHost, s->st));
+    CK(cudaStreamSynchronize(s->st));
+    *out = *hp;
+    return 0;
+}
+
+template <class E>
+int run_bfs(pmf_solver *s, const Ctx &c, bool sink, int64_t *sweeps) {
+    int k = 0;
+    for (;;) {
+        for (int j = 0; j < s->bfs_chunk; j++, k++) {
+            if (sink) k_bfs_sink<E><<<s->grid_bfs, NT, 0, s->st>>>(c, k);
+            else k_bfs_src<E><<<s->grid_bfs, NT, 0, s->st>>>(c, k);
+        }
+        CK(cudaGetLastError());
+        *sweeps += s->bfs_chunk;
+        int32_t left = 0;
+        int rc = read_count(s, c, k % 3, &left);
+        if (rc) return rc;
+        if (left == 0) return 0;
+    }
+}
+
+template <class E>
+int run_solve(pmf_solver *s, const Ctx &c, int32_t ngrids) {
+    int rc = 0;
+    int64_t cycle = 0;
+    for (;; cycle++) {
+        if (cycle > s->max_cycles)
+            return fail(PMF_ERR_NOCONV, "push-relabel failed to converge within %lld cycles",
+                        (long long)s->max_cycles);
+        // exact global relabel
+        s->tmark(C_BFS);
+        if ((rc = begin_phase(s, c))) return rc;
+        k_gr_init<<<s->grid_full, NT, 0, s->st>>>(c);
+        s->stats.full_passes++;
+        if ((rc = run_bfs<E>(s, c, true, &s->stats.bfs_sweeps))) return rc;
+        // list active tiles; retire grids without active pixels
+        s->tmark(C_SEED);
+        if ((rc = begin_phase(s, c))) return rc;
+        k_seed_push<<<s->grid_full, NT, 0, s->st>>>(c);
+        k_update_live<<<int(cdiv(ngrids, 256)), 256, 0, s->st>>>(c, ngrids);
+        CK(cudaGetLastError());
+        s->stats.full_passes++;
+        int32_t nact = 0;
+        if ((rc = read_count(s, c, 0, &nact))) return rc;
+        if (nact == 0) break;
+        s->tmark(C_PUSH);
+        for (int k = 0; k < s->push_sweeps; k++)
+            k_push<E><<<s->grid_push, NT, 0, s->st>>>(c, k, s->push_iters);
+        CK(cudaGetLastError());
+        s->stats.push_sweeps += s->push_sweeps;
+    }
+    s->stats.cycles = cycle + 1;
+    // labels: source-side closure, then emit
+    s->tmark(C_LAB);
+    if ((rc = begin_phase(s, c))) return rc;
+    k_lab_seed<<<s->grid_full, NT, 0, s->st>>>(c);
+    s->stats.full_passes++;
+    if ((rc = run_bfs<E>(s, c, false, &s->stats.bfs_sweeps))) return rc;
+    k_emit<<<s->grid_full, NT, 0, s->st>>>(c);
+    s->stats.full_passes++;
+    CK(cudaGetLastError());
+    return 0;
+}
+
+int finish_stats(pmf_solver *s, const Layout &L) {
+    unsigned long long st[ST_NSTAT];
+    int32_t err = 0;
+    CK(cudaMemcpyAsync(st, s->d_stat.p, sizeof st, cudaMemcpyDeviceToHost, s->st));
+    CK(cudaMemcpyAsync(&err, s->d_err.p, 4, cudaMemcpyDeviceToHost, s->st));
+    CK(cudaStreamSynchronize(s->st));
+    s->stats.push_tile_passes = int64_t(st[ST_PUSH]);
+    s->stats.bfs_tile_passes = int64_t(st[ST_BFS]);
+    s->stats.label_tile_passes = int64_t(st[ST_LAB]);
+    s->stats.grids = int64_t(L.grids.size());
+    s->stats.tiles = L.ntiles;
+    s->stats.pixels = L.pixels;
+    s->stats.edge_bytes = s->edge_bytes;
+    if (s->timing && !s->ev_marks.empty()) {
+        double cat[C_N] = {0};
+        for (size_t i = 0; i + 1 < s->ev_marks.size(); i++) {
+            float ms = 0;
+            cudaEventElapsedTime(&ms, s->ev_pool[s->ev_marks[i].second], s->ev_pool[s->ev_marks[i + 1].second]);
+            cat[s->ev_marks[i].first] += ms;
+        }
+        float tot = 0;
+        cudaEventElapsedTime(&tot, s->ev_pool[s->ev_marks.front().second], s->ev_pool[s->ev_marks.back().second]);
+        s->stats.timed = 1;
+        s->stats.ms_total = tot;
+        s->stats.ms_build = cat[C_BUILD];
+        s->stats.ms_bfs = cat[C_BFS];
+        s->stats.ms_push = cat[C_PUSH];
+        s->stats.ms_seed = cat[C_SEED];
+        s->stats.ms_labels = cat[C_LAB];
+        s->stats.ms_h2d = cat[C_H2D];
+        s->stats.ms_d2h = cat[C_D2H];
+    }
+    if (err == 4) return fail(PMF_ERR_NONMAX, "source side touches an unsaturated sink edge");
+    if (err) return fail(PMF_ERR_CUDA, "device error code %d", err);
+    return 0;
+}
+
+void begin_stats(pmf_solver *s) {
+    s->stats = pmf_stats{};
+    s->ev_used = 0;
+    s->ev_marks.clear();
+}
+
+// narrow an int64 plane into int32 staging, clamping into [lo, hi]
+inline void narrow(int32_t *dst, const int64_t *src, int64_t n, int64_t lo, int64_t hi) {
+    for (int64_t i = 0; i < n; i++) {
+        int64_t v = src[i];
+        dst[i] = int32_t(v < lo ? lo : v > hi ? hi : v);
+    }
+}
+
+// largest c(p->q) + c(q->p) over arc pairs of a (4, n) row-major plane set
+int64_t max_pair(const int32_t *nb, int W, int H) {
+    const int64_t n = int64_t(W) * H;
+    int64_t m = 0;
+    for (int y = 0; y < H; y++)
+        for (int x = 0; x < W; x++) {
+            int64_t p = int64_t(y) * W + x;
+            if (x + 1 < W) m = std::max<int64_t>(m, int64_t(nb[1 * n + p]) + nb[0 * n + p + 1]);
+            if (y + 1 < H) m = std::max<int64_t>(m, int64_t(nb[3 * n + p]) + nb[2 * n + p + W]);
+        }
+    return m;
+}
+
+template <class E>
+int grids_for_push(pmf_solver *s) {
+    int occ = 0;
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_push<E>, NT, 0));
+    s->grid_push = std::max(1, occ) * s->sms;
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_bfs_sink<E>, NT, 0));
+    s->grid_bfs = std::max(1, occ) * s->sms;
+    s->grid_full = 8 * s->sms;
+    return 0;
+}
+
+// --------------------------------------------------------------------------
+// composites
+// --------------------------------------------------------------------------
+
+template <class E>
+int solve_composites_t(pmf_solver *s, const Layout &L, int ncomp, const int64_t *plane_off,
+                       int64_t total_px) {
+    int rc = grids_for_push<E>(s);
+    if (rc) return rc;
+    Ctx c;
+    if ((rc = setup_state(s, L, E::kBytes, &c))) return rc;
+    s->tmark(C_H2D);
+    if ((rc = s->d_in32.ensure(size_t(total_px) * 6 * 4)) || (rc = s->d_off.ensure(size_t(ncomp) * 8)))
+        return rc;
+    c.colswap = s->d_colswap.as<uint8_t>();
+    int32_t *din = s->d_in32.as<int32_t>();
+    CK(cudaMemcpyAsync(din, s->h_in32.p, size_t(total_px) * 6 * 4, cudaMemcpyHostToDevice, s->st));
+    CK(cudaMemcpyAsync(s->d_off.p, plane_off, size_t(ncomp) * 8, cudaMemcpyHostToDevice, s->st));
+    s->tmark(C_BUILD);
+    CompArgs a{din, din + total_px, din + 2 * total_px, s->d_off.as<int64_t>()};
+    k_load_comp<E><<<s->grid_full, NT, 0, s->st>>>(c, a);
+    CK(cudaGetLastError());
+    s->stats.full_passes++;
+    if ((rc = run_solve<E>(s, c, int32_t(L.grids.size())))) return rc;
+    return 0;
+}
+
+}  // namespace
+
+// ==========================================================================
+// C ABI
+// ==========================================================================
+
+extern "C" {
+
+const char *pmf_last_error(void) { return g_err.c_str(); }
+
+int pmf_solver_create(int32_t device, pmf_solver **out) {
+    if (!out) return fail(PMF_ERR_ARG, "null output handle");
+    *out = nullptr;
+    int ndev = 0;
+    CK(cudaGetDeviceCount(&ndev));
+    if (device < 0 || device >= ndev) return fail(PMF_ERR_ARG, "device %d out of range (%d devices)", device, ndev);
+    CK(cudaSetDevice(device));
+    pmf_solver *s = new pmf_solver();
+    s->device = device;
+    cudaDeviceProp prop;
+    if (cudaGetDeviceProperties(&prop, device) != cudaSuccess || prop.major < 10) {
+        delete s;
+        return fail(PMF_ERR_CUDA, "device %d is not sm_100-class", device);
+    }
+    s->sms = prop.multiProcessorCount;
+    if (cudaStreamCreateWithFlags(&s->st, cudaStreamNonBlocking) != cudaSuccess) {
+        delete s;
+        return fail(PMF_ERR_CUDA, "cudaStreamCreate failed");
+    }
+    if (s->h_small.ensure(256)) { delete s; return PMF_ERR_CUDA; }
+    *out = s;
+    return 0;
+}
+
+int pmf_solver_destroy(pmf_solver *s) {
+    if (!s) return 0;
+    cudaSetDevice(s->device);
+    cudaStreamSynchronize(s->st);
+    for (auto e : s->ev_pool) cudaEventDestroy(e);
+    cudaStreamDestroy(s->st);
+    delete s;
+    return 0;
+}
+
+int pmf_solver_set(pmf_solver *s, const char *name, int64_t v) {
+    if (!s || !name) return fail(PMF_ERR_ARG, "null argument");
+    std::string k(name);
+    if (k == "push_iters" && v >= 1 && v <= 100000) s->push_iters = int(v);
+    else if (k == "push_sweeps" && v >= 1 && v <= 100000) s->push_sweeps = int(v);
+    else if (k == "bfs_chunk" && v >= 1 && v <= 100000) s->bfs_chunk = int(v);
+    else if (k == "timing") s->timing = v != 0;
+    else if (k == "max_cycles" && v >= 1) s->max_cycles = v;
+    else return fail(PMF_ERR_ARG, "unknown knob or bad value: %s=%lld", name, (long long)v);
+    return 0;
+}
+
+int pmf_solver_stats(const pmf_solver *s, pmf_stats *out) {
+    if (!s || !out) return fail(PMF_ERR_ARG, "null argument");
+    *out = s->stats;
+    return 0;
+}
+
+int pmf_solve_composites(pmf_solver *s, int32_t ncomp, const int32_t *width, const int32_t *height,
+                         const int64_t *const *src, const int64_t *const *snk,
+                         const int64_t *const *nbr, const int32_t *nseg,
+                         const int32_t *const *seg_off, const int32_t *const *seg_w,
+                         const uint8_t *const *seg_swapped, int64_t *flow_out,
+                         uint8_t *const *labels_out) {
+    if (!s || ncomp < 1 || !width || !height || !src || !snk || !nbr || !flow_out || !labels_out)
+        return fail(PMF_ERR_ARG, "bad arguments");
+    CK(cudaSetDevice(s->device));
+    begin_stats(s);
+    Layout L;
+    std::vector<uint8_t> colswap;
+    std::vector<int64_t> plane_off(ncomp);
+    int64_t total_px = 0;
+    for (int c = 0; c < ncomp; c++) {
+        if (width[c] < 1 || height[c] < 1) return fail(PMF_ERR_ARG, "composite %d: bad shape", c);
+        int32_t cs_off = int32_t(colswap.size());
+        colswap.resize(colswap.size() + width[c], 0);
+        int ns = nseg ? nseg[c] : 0;
+        for (int k = 0; k < ns; k++) {
+            int o = seg_off[c][k], w = seg_w[c][k];
+            if (o < 0 || w < 0 || o + w > width[c]) return fail(PMF_ERR_ARG, "composite %d: segment %d outside grid", c, k);
+            if (seg_swapped[c][k])
+                for (int x = o; x < o + w; x++) colswap[cs_off + x] = 1;
+        }
+        L.add(width[c], height[c], 1, cs_off, c, 0);
+        plane_off[c] = total_px;
+        total_px += int64_t(width[c]) * height[c];
+    }
+    // stage inputs as int32: src | snk | nbr (4 planes) per composite
+    int rc = s->h_in32.ensure(size_t(total_px) * 6 * 4);
+    if (rc) return rc;
+    int32_t *hin = s->h_in32.as<int32_t>();
+    int64_t maxpair = 0, maxexcess = 0;
+    for (int c = 0; c < ncomp; c++) {
+        const int64_t n = int64_t(width[c]) * height[c], off = plane_off[c];
+        for (const int64_t *pl : {src[c], snk[c]})
+            for (int64_t i = 0; i < n; i++)
+                if (pl[i] < 0 || pl[i] > CAP_MAX)
+                    return fail(PMF_ERR_RANGE, "composite %d: capacity outside [0, CAP_MAX]", c);
+        for (int64_t i = 0; i < 4 * n; i++)
+            if (nbr[c][i] < 0 || nbr[c][i] > CAP_MAX)
+                return fail(PMF_ERR_RANGE, "composite %d: capacity outside [0, CAP_MAX]", c);
+        narrow(hin + off, src[c], n, 0, CAP_MAX);
+        narrow(hin + total_px + off, snk[c], n, 0, CAP_MAX);
+        narrow(hin + 2 * total_px + 4 * off, nbr[c], 4 * n, 0, CAP_MAX);
+        maxpair = std::max(maxpair, max_pair(hin + 2 * total_px + 4 * off, width[c], height[c]));
+        // bound on any pixel's excess: its positive terminal plus all arc pairs
+        const int32_t *nb = hin + 2 * total_px + 4 * off;
+        for (int64_t p = 0; p < n; p++) {
+            int64_t e = std::max<int64_t>(0, int64_t(hin[off + p]) - hin[total_px + off + p]);
+            for (int d = 0; d < 4; d++) e += 2 * int64_t(nb[d * n + p]);
+            maxexcess = std::max(maxexcess, e);
+        }
+    }
+    if (maxexcess >= (int64_t(1) << 31) - 1)
+        return fail(PMF_ERR_RANGE, "capacities too large for the int32 device state");
+    if (s->d_colswap.ensure(colswap.size() + 1)) return PMF_ERR_CUDA;
+    CK(cudaMemcpyAsync(s->d_colswap.p, colswap.data(), colswap.size(), cudaMemcpyHostToDevice, s->st));
+    if (s->d_swapflag.ensure(64)) return PMF_ERR_CUDA;
+    CK(cudaStreamSynchronize(s->st));
+    rc = maxpair <= 255 ? solve_composites_t<EdgeU8>(s, L, ncomp, plane_off.data(), total_px)
+                        : solve_composites_t<EdgeI32>(s, L, ncomp, plane_off.data(), total_px);
+    if (rc) return rc;
+    // outputs
+    s->tmark(C_D2H);
+    const int64_t G = int64_t(L.grids.size());
+    const size_t lab_bytes = size_t((L.out_bytes + 7) / 8) * 8;
+    if ((rc = s->h_out.ensure(lab_bytes + size_t(G) * 16))) return rc;
+    uint8_t *ho = s->h_out.as<uint8_t>();
+    int64_t *hsnk = (int64_t *)(ho + lab_bytes);
+    int64_t *hdr = hsnk + G;
+    CK(cudaMemcpyAsync(ho, s->d_out.p, L.out_bytes, cudaMemcpyDeviceToHost, s->st));
+    CK(cudaMemcpyAsync(hsnk, s->d_snk.p, G * 8, cudaMemcpyDeviceToHost, s->st));
+    CK(cudaMemcpyAsync(hdr, s->d_drain.p, G * 8, cudaMemcpyDeviceToHost, s->st));
+    s->tmark(C_N);
+    if ((rc = finish_stats(s, L))) return rc;
+    for (int c = 0; c < ncomp; c++) {
+        flow_out[c] = hsnk[c] - hdr[c];
+        memcpy(labels_out[c], ho + L.grids[c].out_off, size_t(width[c]) * height[c]);
+    }
+    return 0;
+}
+
+int pmf_solve_seed_batch(pmf_solver *s, int32_t nprob, int32_t W, int32_t H,
+                         const int64_t *const *ub, const int64_t *const *us,
+                         const int64_t *const *sb, const int64_t *const *pw,
+                         const int64_t *const *fg_idx, const int32_t *n_fg,
+                         const int64_t *const *bg_idx, const int32_t *n_bg, int32_t nlam,
+                         const int64_t *lambdas, int32_t swap_mode, uint8_t *swapped_out,
+                         int64_t *flows_out, uint8_t *labels_out) {
+    if (!s || nprob < 1 || nlam < 1 || W < 1 || H < 1 || !ub || !us || !sb || !pw || !lambdas ||
+        !flows_out || !labels_out || swap_mode < 0 || swap_mode > 2)
+        return fail(PMF_ERR_ARG, "bad arguments");
+    CK(cudaSetDevice(s->device));
+    begin_stats(s);
+    const int64_t n = int64_t(W) * H;
+    for (int j = 0; j < nlam; j++)
+        if (lambdas[j] < 0 || (j && lambdas[j] <= lambdas[j - 1]))
+            return fail(PMF_ERR_ARG, "lambda values must be non-negative and strictly increasing");
+    const int64_t lam_max = lambdas[nlam - 1];
+    // ---- stage planes: base | slope | sink per problem, pairwise deduped
+    int rc;
+    if ((rc = s->h_in32.ensure(size_t(nprob) * n * 3 * 4)) || (rc = s->h_mask.ensure(size_t(nprob) * n)))
+        return rc;
+    int32_t *hb = s->h_in32.as<int32_t>();
+    uint8_t *hm = s->h_mask.as<uint8_t>();
+    std::vector<int64_t> plane_off(nprob), pw_off(nprob);
+    std::unordered_map<const int64_t *, int64_t> pw_seen;
+    std::vector<const int64_t *> pw_list;
+    for (int p = 0; p < nprob; p++) {
+        auto it = pw_seen.find(pw[p]);
+        if (it == pw_seen.end()) {
+            int64_t o = int64_t(pw_list.size()) * 4 * n;
+            pw_seen[pw[p]] = o;
+            pw_list.push_back(pw[p]);
+            pw_off[p] = o;
+        } else {
+            pw_off[p] = it->second;
+        }
+    }
+    if ((rc = s->h_pw.ensure(pw_list.size() * size_t(4 * n) * 4))) return rc;
+    int32_t *hp = s->h_pw.as<int32_t>();
+    int64_t maxpair = 0;
+    for (size_t k = 0; k < pw_list.size(); k++) {
+        const int64_t *src = pw_list[k];
+        for (int64_t i = 0; i < 4 * n; i++)
+            if (src[i] < 0 || src[i] > CAP_MAX)
+                return fail(PMF_ERR_RANGE, "pairwise capacity outside [0, CAP_MAX]");
+        narrow(hp + k * 4 * n, src, 4 * n, 0, CAP_MAX);
+        maxpair = std::max(maxpair, max_pair(hp + k * 4 * n, W, H));
+    }
+    for (int p = 0; p < nprob; p++) {
+        plane_off[p] = int64_t(p) * n;
+        uint8_t *m = hm + p * n;
+        memset(m, 0, size_t(n));
+        for (int32_t i = 0; i < (n_fg ? n_fg[p] : 0); i++) {
+            int64_t q = fg_idx[p][i];
+            if (q < 0 || q >= n) return fail(PMF_ERR_ARG, "fg seed out of range");
+            m[q] = 1;
+        }
+        for (int32_t i = 0; i < (n_bg ? n_bg[p] : 0); i++) {
+            int64_t q = bg_idx[p][i];
+            if (q < 0 || q >= n) return fail(PMF_ERR_ARG, "bg seed out of range");
+            if (m[q] == 1) return fail(PMF_ERR_ARG, "a pixel cannot be both a foreground and background seed");
+            m[q] = 2;
+        }
+        // ranges the device relies on (instantiate's checks are the caller's)
+        for (int64_t q = 0; q < n; q++) {
+            if (m[q] != 1) {
+                int64_t b = ub[p][q], sl = us[p][q];
+                if (b < 0 || sl < 0) return fail(PMF_ERR_RANGE, "problem %d: negative unary term", p);
+                if (sl && lam_max > (CAP_MAX - std::min(b, CAP_MAX)) / sl + 1)
+                    return fail(PMF_ERR_RANGE, "problem %d: unary term exceeds CAP_MAX", p);
+                if (b + lam_max * sl > CAP_MAX)
+                    return fail(PMF_ERR_RANGE, "problem %d: unary term exceeds CAP_MAX", p);
+            }
+            if (m[q] != 2 && (sb[p][q] < 0 || sb[p][q] > CAP_MAX))
+                return fail(PMF_ERR_RANGE, "problem %d: sink term outside [0, CAP_MAX]", p);
+        }
+        narrow(hb + 3 * p * n + 0 * n, ub[p], n, 0, CAP_MAX);
+        narrow(hb + 3 * p * n + 1 * n, us[p], n, 0, CAP_MAX);
+        narrow(hb + 3 * p * n + 2 * n, sb[p], n, 0, CAP_MAX);
+    }
+    // base/slope/sink are staged per problem as [p][3][n]: the kernels read
+    // base[plane_off[p] + q], slope = base + n, sink = base + 2n
+    bool u8 = maxpair <= 255;
+    if (!u8 && CAP_MAX + 8 * maxpair >= (int64_t(1) << 31) - 1)
+        return fail(PMF_ERR_RANGE, "pairwise capacities too large for the int32 device state");
+    // ---- layout: one grid per (problem, lambda), problem-major
+    Layout L;
+    for (int p = 0; p < nprob; p++)
+        for (int j = 0; j < nlam; j++) L.add(W, H, 0, 0, p, j);
+    rc = u8 ? grids_for_push<EdgeU8>(s) : grids_for_push<EdgeI32>(s);
+    if (rc) return rc;
+    if ((rc = s->d_swapflag.ensure(size_t(nprob) * 4)) || (rc = s->d_colswap.ensure(64))) return rc;
+    Ctx c;
+    if ((rc = setup_state(s, L, u8 ? 4 : 16, &c))) return rc;
+    s->tmark(C_H2D);
+    const size_t bytes_b = size_t(nprob) * n * 3 * 4, bytes_pw = pw_list.size() * size_t(4 * n) * 4;
+    if ((rc = s->d_in32.ensure(bytes_b)) || (rc = s->d_pw.ensure(bytes_pw)) ||
+        (rc = s->d_mask.ensure(size_t(nprob) * n)) || (rc = s->d_off.ensure(size_t(nprob) * 16)) ||
+        (rc = s->d_lam.ensure(size_t(nlam) * 8)) || (rc = s->d_swapcnt.ensure(size_t(nprob) * 8)))
+        return rc;
+    CK(cudaMemcpyAsync(s->d_in32.p, hb, bytes_b, cudaMemcpyHostToDevice, s->st));
+    CK(cudaMemcpyAsync(s->d_pw.p, hp, bytes_pw, cudaMemcpyHostToDevice, s->st));
+    CK(cudaMemcpyAsync(s->d_mask.p, hm, size_t(nprob) * n, cudaMemcpyHostToDevice, s->st));
+    // offsets: base plane of problem p at 3*p*n; slope/sink follow at +n/+2n
+    std::vector<int64_t> offs(2 * size_t(nprob));
+    for (int p = 0; p < nprob; p++) { offs[p] = 3 * int64_t(p) * n; offs[nprob + p] = pw_off[p]; }
+    CK(cudaMemcpyAsync(s->d_off.p, offs.data(), offs.size() * 8, cudaMemcpyHostToDevice, s->st));
+    CK(cudaMemcpyAsync(s->d_lam.p, lambdas, size_t(nlam) * 8, cudaMemcpyHostToDevice, s->st));
+    CK(cudaMemsetAsync(s->d_swapcnt.p, 0, size_t(nprob) * 8, s->st));
+    CK(cudaStreamSynchronize(s->st));   // offs is a stack vector
+    s->tmark(C_BUILD);
+    const int32_t *b32 = s->d_in32.as<int32_t>();
+    SeedArgs a{};
+    a.base = b32;
+    a.slope = b32 + n;
+    a.sink = b32 + 2 * n;
+    a.pw = s->d_pw.as<int32_t>();
+    a.plane_off = s->d_off.as<int64_t>();
+    a.pw_off = s->d_off.as<int64_t>() + nprob;
+    a.lambdas = s->d_lam.as<int64_t>();
+    a.nprob = nprob;
+    a.nlam = nlam;
+    a.W = W;
+    a.H = H;
+    a.mid = (nlam - 1) / 2;   // LambdaSchedule.mid_index, parametric.py:65-68
+    a.swap_mode = swap_mode;
+    a.swap_cnt = s->d_swapcnt.as<int32_t>();
+    a.swapped = s->d_swapflag.as<int32_t>();
+    a.mask = s->d_mask.as<uint8_t>();
+    if (swap_mode == PMF_SWAP_AUTO)
+        k_swap_count<<<int(std::min<int64_t>(cdiv(nprob * n, 256), 16 * s->sms)), 256, 0, s->st>>>(a);
+    k_swap_decide<<<int(cdiv(nprob, 128)), 128, 0, s->st>>>(a);
+    if (u8) k_build_seed<EdgeU8><<<s->grid_full, NT, 0, s->st>>>(c, a);
+    else k_build_seed<EdgeI32><<<s->grid_full, NT, 0, s->st>>>(c, a);
+    CK(cudaGetLastError());
+    s->stats.full_passes++;
+    rc = u8 ? run_solve<EdgeU8>(s, c, int32_t(L.grids.size()))
+            : run_solve<EdgeI32>(s, c, int32_t(L.grids.size()));
+    if (rc) return rc;
+    // ---- outputs: labels (problem-major, lambda-minor), flows, swap flags
+    s->tmark(C_D2H);
+    const int64_t G = int64_t(L.grids.size());
+    const size_t lab_bytes = size_t((L.out_bytes + 7) / 8) * 8;
+    if ((rc = s->h_out.ensure(lab_bytes + size_t(G) * 16 + size_t(nprob) * 4 + 64))) return rc;
+    uint8_t *ho = s->h_out.as<uint8_t>();
+    int64_t *hsnk = (int64_t *)(ho + lab_bytes);
+    int64_t *hdr = hsnk + G;
+    int32_t *hsw = (int32_t *)(hdr + G);
+    CK(cudaMemcpyAsync(ho, s->d_out.p, L.out_bytes, cudaMemcpyDeviceToHost, s->st));
+    CK(cudaMemcpyAsync(hsnk, s->d_snk.p, G * 8, cudaMemcpyDeviceToHost, s->st));
+    CK(cudaMemcpyAsync(hdr, s->d_drain.p, G * 8, cudaMemcpyDeviceToHost, s->st));
+    CK(cudaMemcpyAsync(hsw, s->d_swapflag.p, size_t(nprob) * 4, cudaMemcpyDeviceToHost, s->st));
+    s->tmark(C_N);
+    if ((rc = finish_stats(s, L))) return rc;
+    for (int64_t g = 0; g < G; g++) flows_out[g] = hsnk[g] - hdr[g];
+    if (swapped_out)
+        for (int p = 0; p < nprob; p++) swapped_out[p] = uint8_t(hsw[p] != 0);
+    memcpy(labels_out, ho, size_t(L.out_bytes));
+    return 0;
+}
+
+}  // extern "C"

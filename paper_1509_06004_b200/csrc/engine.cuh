@@ -1,0 +1,168 @@
+// engine.cuh -- device data layout and small helpers shared by the kernels.
+//
+// Layout: every independent grid graph of a
+// batch (one lambda-graph, or one whole composite) is cut into 32x32 tiles;
+// tiles of all grids are numbered 0..T-1 and each per-pixel plane is stored
+// tile-major, pixel p = tile*1024 + ly*32 + lx.  Planes:
+//   w  int32  combined terminal state of the reduced network: w > 0 is excess,
+//             w < 0 is the residual capacity of the pixel->sink arc
+//   h  int32  distance label (HINF = cannot reach the sink: frozen)
+//   r  u8x4   residuals of the 4 neighbour arcs packed in one word (EdgeU8)
+//      int4   or four int32 (EdgeI32) when a capacity pair exceeds 255
+//   lab u8    source-side reachability (label BFS)
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace pmf {
+
+constexpr int TW = 32;              // tile width  (one warp across)
+constexpr int TH = 32;              // tile height
+constexpr int TPIX = TW * TH;       // pixels per tile
+constexpr int NT = 256;             // threads per CTA
+constexpr int PPT = TPIX / NT;      // pixels per thread (4)
+constexpr int32_t HINF = 0x3fffffff;
+constexpr int64_t CAP_MAX = int64_t(1) << 30;   // grid.py:19
+
+enum { DL = 0, DR = 1, DU = 2, DD = 3 };         // grid.py:23 order
+__host__ __device__ constexpr int opp(int d) { return d ^ 1; }
+
+// statistics counters (device, unsigned long long)
+enum { ST_PUSH = 0, ST_BFS = 1, ST_LAB = 2, ST_NSTAT = 4 };
+
+struct GridDesc {
+    int32_t W, H, ntx, nty;
+    int64_t tile_base;
+    int64_t out_off;        // offset of this grid's label bytes in the output
+    int32_t kind;           // 0: batch lambda-graph, 1: composite (column spans)
+    int32_t colswap_off;    // composite: offset of its per-column swap flags
+    int32_t prob, lam;      // builder: problem / lambda index
+};
+
+struct Ctx {
+    int32_t *w;
+    int32_t *h;
+    void *r;
+    uint8_t *lab;
+    const int32_t *tile_grid;
+    const GridDesc *grids;
+    int32_t *live;          // per grid: still has work
+    int32_t *act;           // per grid active-pixel count of the last seed pass
+    int32_t *list0, *list1; // double-buffered tile worklists
+    int32_t *inq0, *inq1;   // "already listed" flags per tile, per buffer
+    int32_t *cnt;           // 3 rolling list lengths
+    int64_t *snk_sum;       // per grid sum of (embedded) sink capacities
+    int64_t *drain;         // per grid sum of unused sink residual
+    int32_t *err;           // device error code (0 ok)
+    unsigned long long *stat;
+    const uint8_t *colswap; // composite per-column swapped flags
+    const int32_t *swapflag;// batch: per-problem swap decision (device-made)
+    uint8_t *out;           // label output bytes
+    int64_t ntiles;
+};
+
+// A batch grid embedded swapped reports its sink side (what split() turns
+// into the original graph's minimal source side); everything else needs the
+// source-side BFS.
+__device__ __forceinline__ bool grid_swapped(const Ctx &c, const GridDesc &gd) {
+    return gd.kind == 0 && c.swapflag[gd.prob] != 0;
+}
+
+__device__ __forceinline__ int32_t *list_of(const Ctx &c, int k) { return (k & 1) ? c.list1 : c.list0; }
+__device__ __forceinline__ int32_t *inq_of(const Ctx &c, int k) { return (k & 1) ? c.inq1 : c.inq0; }
+
+// Append tile t to worklist k (once per list, guarded by its inq flag).
+__device__ __forceinline__ void enqueue(const Ctx &c, int k, int32_t t) {
+    if (atomicExch(&inq_of(c, k)[t], 1) == 0) {
+        int idx = atomicAdd(&c.cnt[k % 3], 1);
+        list_of(c, k)[idx] = t;
+    }
+}
+
+struct TileGeo {
+    int32_t g;              // grid id
+    int32_t tx, ty;
+    int32_t nb[4];          // neighbour tile ids per side, -1 if none
+    int32_t x0, y0, W, H;
+};
+
+__device__ __forceinline__ TileGeo tile_geo(const Ctx &c, int32_t t) {
+    TileGeo o;
+    o.g = c.tile_grid[t];
+    const GridDesc &gd = c.grids[o.g];
+    int32_t l = int32_t(t - gd.tile_base);
+    o.tx = l % gd.ntx;
+    o.ty = l / gd.ntx;
+    o.nb[DL] = o.tx > 0 ? t - 1 : -1;
+    o.nb[DR] = o.tx + 1 < gd.ntx ? t + 1 : -1;
+    o.nb[DU] = o.ty > 0 ? t - gd.ntx : -1;
+    o.nb[DD] = o.ty + 1 < gd.nty ? t + gd.ntx : -1;
+    o.x0 = o.tx * TW;
+    o.y0 = o.ty * TH;
+    o.W = gd.W;
+    o.H = gd.H;
+    return o;
+}
+
+// Index, inside the neighbour tile on side s, of the halo pixel facing
+// position j (row for L/R, column for U/D) of this tile.
+__device__ __forceinline__ int halo_index(int s, int j) {
+    switch (s) {
+    case DL: return j * TW + (TW - 1);
+    case DR: return j * TW;
+    case DU: return (TH - 1) * TW + j;
+    default: return j;
+    }
+}
+
+__device__ __forceinline__ bool on_border(int i) {
+    int lx = i & (TW - 1), ly = i / TW;
+    return lx == 0 || lx == TW - 1 || ly == 0 || ly == TH - 1;
+}
+
+// ---- residual storage policies -------------------------------------------
+
+// Four 8-bit residuals in one word: lane d holds r(p -> d-neighbour).
+// Valid when every arc pair satisfies c(p->q) + c(q->p) <= 255, checked on
+// the host; all concurrent updates are word-sized atomics of lane deltas
+// that keep every lane inside [0, 255].
+struct EdgeU8 {
+    using Word = uint32_t;
+    static constexpr int kBytes = 4;
+    __device__ static Word load(const void *R, int64_t p) { return ((const uint32_t *)R)[p]; }
+    __device__ static int lane(Word w, int d) { return int((w >> (8 * d)) & 0xffu); }
+    __device__ static Word pack(int a, int b, int c, int d) {
+        return uint32_t(a) | (uint32_t(b) << 8) | (uint32_t(c) << 16) | (uint32_t(d) << 24);
+    }
+    __device__ static void store(void *R, int64_t p, Word w) { ((uint32_t *)R)[p] = w; }
+    __device__ static void store_delta(void *R, int64_t p, Word nw, Word ow) {
+        if (nw != ow) atomicAdd(((uint32_t *)R) + p, nw - ow);
+    }
+    __device__ static void add(void *R, int64_t p, int d, int v) {
+        atomicAdd(((uint32_t *)R) + p, uint32_t(v) << (8 * d));
+    }
+};
+
+// Four int32 residuals per pixel (16 B, int4-aligned).
+struct EdgeI32 {
+    using Word = int4;
+    static constexpr int kBytes = 16;
+    __device__ static Word load(const void *R, int64_t p) { return ((const int4 *)R)[p]; }
+    __device__ static int lane(Word w, int d) {
+        return d == 0 ? w.x : d == 1 ? w.y : d == 2 ? w.z : w.w;
+    }
+    __device__ static Word pack(int a, int b, int c, int d) { return make_int4(a, b, c, d); }
+    __device__ static void store(void *R, int64_t p, Word w) { ((int4 *)R)[p] = w; }
+    __device__ static void store_delta(void *R, int64_t p, Word nw, Word ow) {
+        int *q = ((int *)R) + 4 * p;
+        if (nw.x != ow.x) atomicAdd(q + 0, nw.x - ow.x);
+        if (nw.y != ow.y) atomicAdd(q + 1, nw.y - ow.y);
+        if (nw.z != ow.z) atomicAdd(q + 2, nw.z - ow.z);
+        if (nw.w != ow.w) atomicAdd(q + 3, nw.w - ow.w);
+    }
+    __device__ static void add(void *R, int64_t p, int d, int v) {
+        atomicAdd(((int *)R) + 4 * p + d, v);
+    }
+};
+
+}  // namespace pmf

@@ -1,0 +1,263 @@
+"""Parametric seed problems and lambda schedules.
+
+Mirror of /root/reference/pkg/src/pmflow/parametric.py: ``LambdaSchedule``
+(:41-77), ``SeedProblem`` (:80-130), ``instantiate`` (:133-166),
+``solve_schedule_sequential`` (:180-183), ``energy`` (:186-188),
+``check_nested`` (:191-201), same errors.
+
+Device path: ``solve_schedule_sequential`` builds every lambda graph on the
+GPU from the problem planes and solves them as one batch (the "batch"
+baseline of the paper without the per-call overhead).  ``check_family``
+reproduces, without materialising any graph, every error ``instantiate``
+would raise for a list of lambdas, in the reference's order, so the device
+builder only ever sees admissible problems.
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from .grid import (CAP_MAX, BorderEdgeError, CapacityOverflowError, CutResult, GridGraph,
+                   NegativeCapacityError, ShapeError, TOTAL_CAP_LIMIT, admit, cut_cost)
+
+DEFAULT_LAMBDA_VALUES = (1, 2, 3, 5, 7, 11, 16, 24, 36, 54,
+                         81, 122, 183, 274, 411, 617, 925, 1388, 2082, 3123)
+HALVED_LAMBDA_VALUES = DEFAULT_LAMBDA_VALUES[::2]
+
+_PRODUCT_LIMIT = 1 << 62
+
+
+class ScheduleError(ValueError):
+    pass
+
+
+class ProblemError(ValueError):
+    pass
+
+
+@dataclass(frozen=True)
+class LambdaSchedule:
+    """Strictly increasing non-negative integer lambda values."""
+
+    values: tuple
+
+    def __post_init__(self):
+        vals = tuple(int(v) for v in self.values)
+        if not vals:
+            raise ScheduleError("schedule must hold at least one value")
+        if vals[0] < 0:
+            raise ScheduleError("lambda values must be non-negative")
+        if any(b <= a for a, b in zip(vals, vals[1:])):
+            raise ScheduleError("lambda values must be strictly increasing")
+        object.__setattr__(self, "values", vals)
+
+    @classmethod
+    def default(cls) -> "LambdaSchedule":
+        return cls(DEFAULT_LAMBDA_VALUES)
+
+    @classmethod
+    def halved(cls) -> "LambdaSchedule":
+        return cls(HALVED_LAMBDA_VALUES)
+
+    @property
+    def mid_index(self) -> int:
+        """ceil(n/2) - 1: the value the family swap decision is taken at."""
+        return (len(self.values) - 1) // 2
+
+    def __len__(self):
+        return len(self.values)
+
+    def __iter__(self):
+        return iter(self.values)
+
+    def __getitem__(self, i):
+        return self.values[i]
+
+
+@dataclass(frozen=True, eq=False)
+class SeedProblem:
+    """Unary/pairwise terms plus foreground/background seed pixels."""
+
+    width: int
+    height: int
+    unary_base: np.ndarray
+    unary_slope: np.ndarray
+    sink_base: np.ndarray
+    pairwise: np.ndarray  # (4, n), LEFT/RIGHT/UP/DOWN rows
+    fg_seeds: frozenset = field(default_factory=frozenset)
+    bg_seeds: frozenset = field(default_factory=frozenset)
+
+    def __post_init__(self):
+        if self.width < 1 or self.height < 1:
+            raise ProblemError(f"bad dimensions {self.width}x{self.height}")
+        n = self.width * self.height
+        set_ = object.__setattr__
+        for name in ("unary_base", "unary_slope", "sink_base"):
+            a = np.asarray(getattr(self, name), dtype=np.int64).reshape(-1)
+            if a.size != n:
+                raise ShapeError(f"{name}: expected {n} entries, got {a.size}")
+            set_(self, name, a)
+        pw = np.asarray(self.pairwise, dtype=np.int64)
+        if pw.size != 4 * n:
+            raise ShapeError(f"pairwise: expected shape (4, {n}), got {pw.shape}")
+        set_(self, "pairwise", pw.reshape(4, n))
+        if self.unary_slope.size and int(self.unary_slope.min()) < 0:
+            raise ProblemError("unary_slope must be non-negative")
+        fg = frozenset(int(i) for i in self.fg_seeds)
+        bg = frozenset(int(i) for i in self.bg_seeds)
+        if fg & bg:
+            raise ProblemError("a pixel cannot be both a foreground and background seed")
+        if any(not 0 <= i < n for i in fg) or any(not 0 <= i < n for i in bg):
+            raise ProblemError("seed set contains an out-of-range pixel index")
+        set_(self, "fg_seeds", fg)
+        set_(self, "bg_seeds", bg)
+        set_(self, "_fg_idx", np.array(sorted(fg), np.int64))
+        set_(self, "_bg_idx", np.array(sorted(bg), np.int64))
+        set_(self, "_stats", None)
+
+    @property
+    def n(self) -> int:
+        return self.width * self.height
+
+    def _family_stats(self):
+        """Lambda-independent reductions used by check_family (cached)."""
+        if self._stats is None:
+            n = self.n
+            nonfg = np.ones(n, bool)
+            nonfg[self._fg_idx] = False
+            nonbg = np.ones(n, bool)
+            nonbg[self._bg_idx] = False
+            b, s = self.unary_base, self.unary_slope
+            sink = self.sink_base[nonbg]
+            pw = self.pairwise
+            arcs = pw.reshape(4, self.height, self.width)
+            st = dict(
+                max_slope=int(s.max(initial=0)),
+                max_base=int(b.max(initial=0)),
+                min_base_nonfg=int(b[nonfg].min(initial=0)),
+                sum_base_nonfg=int(b[nonfg].sum()),
+                sum_slope_nonfg=int(s[nonfg].sum()),
+                max_slope_nonfg=int(s[nonfg].max(initial=0)),
+                max_base_nonfg=int(b[nonfg].max(initial=0)),
+                n_fg=int(self._fg_idx.size), n_bg=int(self._bg_idx.size),
+                min_sink=int(sink.min(initial=0)), max_sink=int(sink.max(initial=0)),
+                sum_sink=int(sink.sum()), sum_sink_fin=int(sink[sink < CAP_MAX].sum()),
+                min_pw=int(pw.min(initial=0)), max_pw=int(pw.max(initial=0)),
+                sum_pw=int(pw.sum()), sum_pw_fin=int(pw[pw < CAP_MAX].sum()),
+                border=[(d, int(row.max(initial=0))) for d, row in (
+                    (0, arcs[0][:, 0]), (1, arcs[1][:, -1]), (2, arcs[2][0, :]),
+                    (3, arcs[3][-1, :]))],
+                nonfg=nonfg,
+            )
+            object.__setattr__(self, "_stats", st)
+        return self._stats
+
+
+def _check_lambda(p: SeedProblem, lam: int) -> None:
+    """Raise exactly what instantiate(p, lam) raises (parametric.py:141-165
+    and admit, grid.py:112-126), or return if the graph is admissible."""
+    lam = int(lam)
+    if lam < 0:
+        raise ScheduleError(f"lambda must be non-negative, got {lam}")
+    st = p._family_stats()
+    if st["max_slope"] and lam > _PRODUCT_LIMIT // st["max_slope"]:
+        raise CapacityOverflowError(f"lambda {lam} overflows the unary term")
+    exact = st["max_base"] + lam * st["max_slope"] > CAP_MAX
+    src_all = None
+    if exact:
+        src_all = p.unary_base + lam * p.unary_slope
+        over = src_all > CAP_MAX
+        if bool(over.any()):
+            raise CapacityOverflowError(
+                f"unary_base + lambda*unary_slope exceeds CAP_MAX at pixel {int(np.argmax(over))} "
+                f"(lambda={lam})")
+    # admit on the instantiated graph: src (fg pixels are CAP_MAX)
+    if st["min_base_nonfg"] < 0:
+        src_nf = p.unary_base[st["nonfg"]] + lam * p.unary_slope[st["nonfg"]]
+        if src_nf.size and int(src_nf.min()) < 0:
+            raise NegativeCapacityError("src_cap has a negative capacity")
+    if st["min_sink"] < 0:
+        raise NegativeCapacityError("snk_cap has a negative capacity")
+    if st["max_sink"] > CAP_MAX:
+        raise CapacityOverflowError("snk_cap exceeds CAP_MAX = 2**30")
+    if st["min_pw"] < 0:
+        raise NegativeCapacityError("nbr_cap has a negative capacity")
+    if st["max_pw"] > CAP_MAX:
+        raise CapacityOverflowError("nbr_cap exceeds CAP_MAX = 2**30")
+    for d, m in st["border"]:
+        if m > 0:
+            raise BorderEdgeError(f"nonzero {('left', 'right', 'up', 'down')[d]} capacity on the "
+                                  "image border")
+    src_sum = st["sum_base_nonfg"] + lam * st["sum_slope_nonfg"] + st["n_fg"] * CAP_MAX
+    total = src_sum + st["sum_sink"] + st["n_bg"] * CAP_MAX + st["sum_pw"]
+    if total >= TOTAL_CAP_LIMIT:
+        raise CapacityOverflowError("total capacity exceeds the 2**62 admission budget")
+    # seed headroom (parametric.py:160-165)
+    if st["max_base_nonfg"] + lam * st["max_slope_nonfg"] < CAP_MAX:
+        src_fin = st["sum_base_nonfg"] + lam * st["sum_slope_nonfg"]
+    else:
+        s_nf = p.unary_base[st["nonfg"]] + lam * p.unary_slope[st["nonfg"]]
+        src_fin = int(s_nf[s_nf < CAP_MAX].sum())
+    finite = src_fin + st["sum_sink_fin"] + st["sum_pw_fin"]
+    if finite >= CAP_MAX:
+        raise CapacityOverflowError(
+            f"finite capacities sum to {finite}, leaving no headroom under CAP_MAX; "
+            "seed pixels could be severed")
+
+
+def check_family(problem: SeedProblem, lambdas) -> None:
+    """Raise the first error instantiate() would raise over ``lambdas`` (in
+    order); the device builder relies on this having passed."""
+    for lam in lambdas:
+        _check_lambda(problem, lam)
+
+
+def instantiate(problem: SeedProblem, lam: int) -> GridGraph:
+    """Host-built admitted graph for one lambda value (API compatibility;
+    the device path never materialises it)."""
+    _check_lambda(problem, lam)
+    src = problem.unary_base + int(lam) * problem.unary_slope
+    snk = problem.sink_base.copy()
+    src[problem._fg_idx] = CAP_MAX
+    snk[problem._bg_idx] = CAP_MAX
+    return admit(GridGraph(problem.width, problem.height, src, snk, problem.pairwise.copy()))
+
+
+@dataclass(frozen=True, eq=False)
+class ParametricResult:
+    """Cuts for one problem at every schedule value, in order."""
+
+    schedule: LambdaSchedule
+    cuts: tuple
+
+    def masks(self):
+        return [c.labels.astype(bool) for c in self.cuts]
+
+
+def solve_schedule_sequential(problem: SeedProblem, schedule: LambdaSchedule,
+                              device: int = 0) -> ParametricResult:
+    """Every lambda of the schedule solved independently (reference
+    parametric.py:180-183), as one device batch of lambda graphs."""
+    from . import _native
+    check_family(problem, schedule.values)
+    _, flows, labels = _native.solver_for_thread(device).solve_seed_batch(
+        problem.width, problem.height, [problem], schedule.values, "off")
+    return ParametricResult(schedule, tuple(CutResult(int(f), l)
+                                            for f, l in zip(flows[0], labels[0])))
+
+
+def energy(problem: SeedProblem, lam: int, labels) -> int:
+    """Segmentation energy of a mask at one lambda (its cut cost)."""
+    return cut_cost(instantiate(problem, lam), labels)
+
+
+def check_nested(result: ParametricResult):
+    """(True, None) if every mask contains its predecessor, else (False, i)
+    for the first schedule index whose mask loses a pixel."""
+    masks = result.masks()
+    for i in range(1, len(masks)):
+        if bool((masks[i - 1] & ~masks[i]).any()):
+            return False, i
+    return True, None

@@ -1,0 +1,292 @@
+"""Supergraphs: many grid problems knitted into one composite, solved on
+the device.
+
+Mirror of /root/reference/pkg/src/pmflow/supergraph.py.  Host helpers keep
+the reference's names and semantics -- ``Segment`` / ``SupergraphLayout``
+(:39-64), ``terminal_balance`` / ``swap_decision`` (:77-92), ``apply_swap``
+(:95-109), ``join`` (:112-154), ``split`` (:157-187),
+``family_swap_decision`` (:210-212), ``build_lambda_supergraph`` (:215-224),
+``build_seed_supergraph`` (:227-253) -- and ``solve_composite`` (:190-207),
+the single solver entry point, runs on the CUDA engine.
+
+``solve_seed_supergraph`` is the fused device path: it takes the seed
+problems themselves, builds every (problem, lambda) graph on the GPU (no
+host composite), solves them in one batch and returns the layout plus the
+per-constituent cuts -- exactly what
+``split(layout, solve_composite(*build_seed_supergraph(...)[:2]), originals)``
+returns, bit for bit.
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+import numpy as np
+
+from .grid import CutResult, GridGraph, admit, cut_cost
+from .parametric import LambdaSchedule, SeedProblem, check_family, instantiate
+
+
+class SupergraphError(ValueError):
+    pass
+
+
+@dataclass(frozen=True)
+class Segment:
+    """A constituent's column span inside a composite."""
+
+    constituent: int
+    offset: int
+    width: int
+    swapped: bool
+
+
+@dataclass(frozen=True)
+class SupergraphLayout:
+    """Column spans, bridge columns and height of a composite."""
+
+    segments: tuple
+    bridge_columns: tuple
+    height: int
+
+    @property
+    def total_width(self) -> int:
+        tail = self.segments[-1]
+        return tail.offset + tail.width
+
+    @property
+    def any_swapped(self) -> bool:
+        return any(s.swapped for s in self.segments)
+
+
+@dataclass(frozen=True)
+class SwapStats:
+    """Sign pattern of src_cap - snk_cap over a graph's pixels."""
+
+    positive_count: int
+    negative_count: int
+    positive_sum: int
+    negative_sum: int  # absolute value
+
+
+def terminal_balance(g: GridGraph) -> SwapStats:
+    diff = g.src_cap - g.snk_cap
+    up, down = diff[diff > 0], diff[diff < 0]
+    return SwapStats(int(up.size), int(down.size), int(up.sum()), int(-down.sum()))
+
+
+def swap_decision(g: GridGraph) -> bool:
+    """Swap iff strictly more pixels lean to the sink than to the source."""
+    st = terminal_balance(g)
+    return st.negative_count > st.positive_count
+
+
+def apply_swap(g: GridGraph) -> GridGraph:
+    """Exchange the terminals and reverse every neighbour arc (involution).
+
+    The arc p -> right neighbour of the swapped graph carries the original
+    right-neighbour -> p capacity, i.e. the LEFT plane shifted one column,
+    and likewise for the other three directions."""
+    H, W = g.height, g.width
+    src = g.nbr_cap.reshape(4, H, W)
+    dst = np.zeros_like(src)
+    dst[0][:, 1:] = src[1][:, :-1]     # L'(y, x) = R(y, x-1)
+    dst[1][:, :-1] = src[0][:, 1:]     # R'(y, x) = L(y, x+1)
+    dst[2][1:, :] = src[3][:-1, :]     # U'(y, x) = D(y-1, x)
+    dst[3][:-1, :] = src[2][1:, :]     # D'(y, x) = U(y+1, x)
+    return admit(GridGraph(W, H, g.snk_cap.copy(), g.src_cap.copy(), dst.reshape(4, -1)))
+
+
+def _plan(widths, heights, pad):
+    """Segment offsets / bridge columns / height of a left-to-right join."""
+    height = max(heights)
+    if not pad and any(h != height for h in heights):
+        raise SupergraphError(f"height mismatch {sorted(set(heights))}; pass pad=True to pad")
+    offsets, bridges, col = [], [], 0
+    for i, w in enumerate(widths):
+        offsets.append(col)
+        col += w
+        if i + 1 < len(widths):
+            bridges.append(col)
+            col += 1
+    return offsets, bridges, height, col
+
+
+def join(graphs, swapped=None, pad=False):
+    """Knit graphs left to right, one zero-capacity bridge column between
+    neighbours; shorter graphs are zero-padded at the bottom when ``pad``.
+    ``swapped`` only records how the caller embedded each constituent."""
+    graphs = list(graphs)
+    if not graphs:
+        raise SupergraphError("join needs at least one graph")
+    flags = [False] * len(graphs) if swapped is None else [bool(s) for s in swapped]
+    if len(flags) != len(graphs):
+        raise SupergraphError("swapped flags must match the graph count")
+    offsets, bridges, height, total_w = _plan([g.width for g in graphs],
+                                              [g.height for g in graphs], pad)
+    planes = np.zeros((6, height, total_w), np.int64)   # src, snk, L, R, U, D
+    for g, off in zip(graphs, offsets):
+        block = np.concatenate([g.src_cap[None], g.snk_cap[None], g.nbr_cap])
+        planes[:, :g.height, off:off + g.width] = block.reshape(6, g.height, g.width)
+    flat = planes.reshape(6, -1)
+    composite = admit(GridGraph(total_w, height, flat[0], flat[1], flat[2:]))
+    segs = tuple(Segment(i, o, g.width, f) for i, (g, o, f) in enumerate(zip(graphs, offsets, flags)))
+    return composite, SupergraphLayout(segs, tuple(bridges), height)
+
+
+def split(layout: SupergraphLayout, composite: CutResult, graphs) -> list:
+    """Per-constituent cuts from a composite cut; swapped spans are
+    complemented, padding rows dropped, flows recomputed by cut_cost and
+    checked to add up to the composite flow."""
+    graphs = list(graphs)
+    if len(graphs) != len(layout.segments):
+        raise SupergraphError("graph count does not match the layout")
+    n = layout.total_width * layout.height
+    if composite.labels.size != n:
+        raise SupergraphError(
+            f"composite labels have {composite.labels.size} entries, layout implies {n}")
+    grid = composite.labels.reshape(layout.height, layout.total_width)
+    parts = []
+    for seg, g in zip(layout.segments, graphs):
+        if g.width != seg.width or g.height > layout.height:
+            raise SupergraphError(f"constituent {seg.constituent} does not fit its segment")
+        span = grid[:g.height, seg.offset:seg.offset + seg.width]
+        lab = np.ascontiguousarray((1 - span) if seg.swapped else span, dtype=np.uint8).reshape(-1)
+        parts.append(CutResult(cut_cost(g, lab), lab))
+    total = sum(p.flow for p in parts)
+    if total != composite.flow:
+        raise SupergraphError(
+            f"decoded flows sum to {total}, composite flow is {composite.flow}; "
+            "the composite labels are not an optimal cut")
+    return parts
+
+
+def _segments_of(layout):
+    if layout is None:
+        return None
+    return [(s.offset, s.width, s.swapped) for s in layout.segments]
+
+
+def solve_composite(g: GridGraph, layout: SupergraphLayout | None = None,
+                    device: int = 0) -> CutResult:
+    """Solve a (possibly composite) graph on the GPU.
+
+    Unswapped spans report the minimal source side; swapped spans report the
+    complement of the sink-reaching set (supergraph.py:201-206), so ``split``
+    lands every constituent on its original canonical cut."""
+    from . import _native
+    admit(g)
+    (flow, labels), = _native.solver_for_thread(device).solve_composites(
+        [(g.width, g.height, g.src_cap, g.snk_cap, g.nbr_cap, _segments_of(layout))])
+    return CutResult(flow, labels)
+
+
+def solve_composites(tasks, device: int = 0) -> list:
+    """Batch form of solve_composite: [(graph, layout)] -> [CutResult], all
+    in one device solve."""
+    from . import _native
+    items = []
+    for g, layout in tasks:
+        admit(g)
+        items.append((g.width, g.height, g.src_cap, g.snk_cap, g.nbr_cap, _segments_of(layout)))
+    return [CutResult(f, l) for f, l in _native.solver_for_thread(device).solve_composites(items)]
+
+
+def family_swap_decision(problem: SeedProblem, schedule: LambdaSchedule) -> bool:
+    """One swap decision per lambda family, taken at mid-schedule."""
+    return swap_decision(instantiate(problem, schedule[schedule.mid_index]))
+
+
+def build_lambda_supergraph(problem: SeedProblem, schedule: LambdaSchedule, swap: bool):
+    """(composite, layout, originals) of one problem's lambda family."""
+    originals = [instantiate(problem, lam) for lam in schedule]
+    embedded = [apply_swap(g) for g in originals] if swap else originals
+    composite, layout = join(embedded, swapped=[swap] * len(originals))
+    return composite, layout, originals
+
+
+def _check_seed_args(problems, swap_mode):
+    problems = list(problems)
+    if not problems:
+        raise SupergraphError("need at least one problem")
+    if swap_mode not in ("auto", "on", "off"):
+        raise SupergraphError(f"unknown swap_mode {swap_mode!r}")
+    return problems
+
+
+def build_seed_supergraph(problems, schedule: LambdaSchedule, swap_mode: str = "auto"):
+    """Host composite of several problems' lambda families (problem-major,
+    lambda-minor), each with its own swap decision."""
+    problems = _check_seed_args(problems, swap_mode)
+    originals, embedded, flags = [], [], []
+    for p in problems:
+        swap = family_swap_decision(p, schedule) if swap_mode == "auto" else swap_mode == "on"
+        for lam in schedule:
+            g = instantiate(p, lam)
+            originals.append(g)
+            embedded.append(apply_swap(g) if swap else g)
+            flags.append(swap)
+    composite, layout = join(embedded, swapped=flags)
+    return composite, layout, originals
+
+
+def seed_layout(problems, schedule: LambdaSchedule, swapped) -> SupergraphLayout:
+    """The layout build_seed_supergraph would produce for these problems."""
+    widths = [p.width for p in problems for _ in schedule]
+    offsets, bridges, height, _ = _plan(widths, [p.height for p in problems for _ in schedule],
+                                        False)
+    flags = [bool(swapped[i]) for i in range(len(problems)) for _ in schedule]
+    segs = tuple(Segment(i, o, w, f) for i, (o, w, f) in enumerate(zip(offsets, widths, flags)))
+    return SupergraphLayout(segs, tuple(bridges), height)
+
+
+@dataclass(frozen=True, eq=False)
+class SeedSupergraphResult:
+    """Device result of one seed supergraph: its layout and the decoded
+    per-constituent cuts (problem-major, lambda-minor)."""
+
+    layout: SupergraphLayout
+    cuts: tuple
+
+    @property
+    def flow(self) -> int:
+        return sum(c.flow for c in self.cuts)
+
+
+def check_seed_supergraph(problems, schedule: LambdaSchedule, swap_mode: str = "auto"):
+    """Raise whatever build_seed_supergraph would raise, in the same order."""
+    problems = _check_seed_args(problems, swap_mode)
+    shapes = {(p.width, p.height) for p in problems}
+    for p in problems:
+        if swap_mode == "auto":
+            check_family(p, (schedule[schedule.mid_index],))
+        check_family(p, schedule.values)
+    if len({h for _, h in shapes}) > 1:
+        raise SupergraphError(f"height mismatch {sorted({h for _, h in shapes})}; "
+                              "pass pad=True to pad")
+    return problems
+
+
+def solve_seed_supergraph(problems, schedule: LambdaSchedule, swap_mode: str = "auto",
+                          device: int = 0) -> SeedSupergraphResult:
+    """Build + solve + decode a seed supergraph entirely on the device."""
+    from . import _native
+    problems = check_seed_supergraph(problems, schedule, swap_mode)
+    shapes = {(p.width, p.height) for p in problems}
+    solver = _native.solver_for_thread(device)
+    if len(shapes) == 1:
+        W, H = shapes.pop()
+        swapped, flows, labels = solver.solve_seed_batch(W, H, problems, schedule.values, swap_mode)
+    else:  # same height, different widths: one device batch per width
+        swapped = np.zeros(len(problems), bool)
+        flows = [None] * len(problems)
+        labels = [None] * len(problems)
+        for (W, H) in sorted(shapes):
+            idx = [i for i, p in enumerate(problems) if (p.width, p.height) == (W, H)]
+            sw, fl, lb = solver.solve_seed_batch(W, H, [problems[i] for i in idx],
+                                                 schedule.values, swap_mode)
+            for k, i in enumerate(idx):
+                swapped[i], flows[i], labels[i] = sw[k], fl[k], lb[k]
+    cuts = tuple(CutResult(int(flows[i][j]), labels[i][j])
+                 for i in range(len(problems)) for j in range(len(schedule)))
+    return SeedSupergraphResult(seed_layout(problems, schedule, swapped), cuts)

@@ -1,0 +1,110 @@
+"""Benchmark inputs: the reference's synthetic seed problems, bit for bit.
+
+Re-derivation of /root/reference/pkg/src/pmflow/harness/synth.py so the GPU
+box (which has no reference checkout) generates the same problems from the
+same ``rng_seed``: one image of random constant rectangles plus clipped
+noise (synth.py:22-41), contrast-gated pairwise weights (:52-64), and one
+seed problem per interior lattice point with the border as background
+(:44-49, :73-100).  ``tests/test_synth.py`` pins the planes against the
+reference generator.
+
+CPMC seed "type B" (BASELINE.json config 3): the same
+foreground seed with the border minus its top row as background -- not in
+the reference; a documented SeedProblem variant.
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+import numpy as np
+
+from .parametric import SeedProblem
+
+INTENSITY_MAX = 255
+L20 = (2, 3, 4, 5, 7, 9, 12, 16, 22, 30, 40, 54, 73, 99, 134, 181, 244, 329, 444, 600)
+C4_LAMBDAS = (1, 2, 3, 5, 7, 11, 16, 24)
+
+
+def draw_image(width, height, rng, regions=4, noise=10):
+    """(image, region map), both (height, width) int64; rng draws in the
+    reference's order: background, then per rectangle w, h, x0, y0, value,
+    then the noise field."""
+    img = np.full((height, width), int(rng.integers(0, INTENSITY_MAX + 1)), np.int64)
+    reg = np.zeros((height, width), np.int64)
+    for rid in range(1, regions + 1):
+        rw = int(rng.integers(max(1, width // 4), max(2, 3 * width // 4)))
+        rh = int(rng.integers(max(1, height // 4), max(2, 3 * height // 4)))
+        x0 = int(rng.integers(0, max(1, width - rw + 1)))
+        y0 = int(rng.integers(0, max(1, height - rh + 1)))
+        img[y0:y0 + rh, x0:x0 + rw] = int(rng.integers(0, INTENSITY_MAX + 1))
+        reg[y0:y0 + rh, x0:x0 + rw] = rid
+    if noise:
+        img = np.clip(img + rng.integers(-noise, noise + 1, (height, width)), 0, INTENSITY_MAX)
+    return img, reg
+
+
+def contrast_weights(img):
+    """(4, n) pairwise capacities: 1 + 63 * (255 - |dI|) // 255 per edge,
+    the same value on both arcs of an edge."""
+    h, w = img.shape
+    out = np.zeros((4, h, w), np.int64)
+    horiz = 1 + ((INTENSITY_MAX - np.abs(np.diff(img, axis=1))) * 63) // INTENSITY_MAX
+    vert = 1 + ((INTENSITY_MAX - np.abs(np.diff(img, axis=0))) * 63) // INTENSITY_MAX
+    out[1][:, :-1] = horiz
+    out[0][:, 1:] = horiz
+    out[3][:-1, :] = vert
+    out[2][1:, :] = vert
+    return out.reshape(4, -1)
+
+
+def lattice(width, height, rows, cols):
+    """Interior seed points, row-major: y_i = (i+1)H/(rows+1), x_j likewise."""
+    return [((j + 1) * width // (cols + 1), (i + 1) * height // (rows + 1))
+            for i in range(rows) for j in range(cols)]
+
+
+def border_pixels(width, height, top=True):
+    grid = np.arange(width * height).reshape(height, width)
+    ring = np.ones((height, width), bool)
+    ring[1:-1, 1:-1] = False
+    if not top:
+        ring[0, :] = False
+    return frozenset(int(p) for p in grid[ring])
+
+
+def seed_problem(img, x, y, pairwise, bg):
+    """Terminal weights from intensity similarity to the seed pixel."""
+    height, width = img.shape
+    dsim = np.abs(img - img[y, x])
+    near = INTENSITY_MAX - dsim
+    idx = y * width + x
+    if idx in bg:
+        raise ValueError(f"seed ({x}, {y}) sits on the border")
+    return SeedProblem(width=width, height=height,
+                       unary_base=(1 + (near * 15) // INTENSITY_MAX).reshape(-1),
+                       unary_slope=(1 + (near * 7) // INTENSITY_MAX).reshape(-1),
+                       sink_base=(1 + (dsim * 63) // INTENSITY_MAX).reshape(-1),
+                       pairwise=pairwise, fg_seeds=frozenset({idx}), bg_seeds=bg)
+
+
+@dataclass
+class SynthBatch:
+    image: np.ndarray
+    regions: np.ndarray
+    coords: list
+    problems: list
+
+
+def generate(width, height, seed_rows=1, seed_cols=1, regions=4, noise=10, rng_seed=0,
+             types=("A",)) -> SynthBatch:
+    """Seed problems of one synthetic image.  types: "A" = reference
+    problem_for_seed (border background); "B" = border minus the top row.
+    Problems are ordered seed-major, type-minor."""
+    rng = np.random.default_rng(rng_seed)
+    img, reg = draw_image(width, height, rng, regions, noise)
+    pw = contrast_weights(img)
+    bgs = {"A": border_pixels(width, height), "B": border_pixels(width, height, top=False)}
+    coords = lattice(width, height, seed_rows, seed_cols)
+    probs = [seed_problem(img, x, y, pw, bgs[t]) for (x, y) in coords for t in types]
+    return SynthBatch(img, reg, coords, probs)

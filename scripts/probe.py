@@ -1,0 +1,52 @@
+"""Ad-hoc device probe: solve synthetic configs and print stats/timings.
+
+    python scripts/probe.py [c1|c2|c3|c4] [--iters K] [--sweeps P] [--reps R]
+"""
+import argparse
+import json
+import os
+import sys
+import time
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+
+from paper_1509_06004_b200 import LambdaSchedule, _native, synth  # noqa: E402
+from paper_1509_06004_b200.parametric import DEFAULT_LAMBDA_VALUES  # noqa: E402
+
+CFG = {
+    "c1": dict(w=160, h=120, rows=1, cols=1, lams=DEFAULT_LAMBDA_VALUES, types=("A",)),
+    "c2": dict(w=500, h=375, rows=1, cols=1, lams=synth.L20, types=("A",)),
+    "c3": dict(w=500, h=375, rows=5, cols=5, lams=synth.L20, types=("A", "B")),
+    "c4": dict(w=1920, h=1080, rows=1, cols=1, lams=synth.C4_LAMBDAS, types=("A",)),
+}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("cfg", nargs="?", default="c2")
+    ap.add_argument("--iters", type=int, default=None)
+    ap.add_argument("--sweeps", type=int, default=None)
+    ap.add_argument("--chunk", type=int, default=None)
+    ap.add_argument("--reps", type=int, default=3)
+    ap.add_argument("--nprob", type=int, default=None, help="problems per device batch")
+    a = ap.parse_args()
+    c = CFG[a.cfg]
+    b = synth.generate(c["w"], c["h"], c["rows"], c["cols"], rng_seed=0, types=c["types"])
+    probs = b.problems if a.nprob is None else b.problems[:a.nprob]
+    s = _native.Solver(0, timing=1)
+    if a.iters: s.set("push_iters", a.iters)
+    if a.sweeps: s.set("push_sweeps", a.sweeps)
+    if a.chunk: s.set("bfs_chunk", a.chunk)
+    for r in range(a.reps):
+        t0 = time.perf_counter()
+        sw, flows, labels = s.solve_seed_batch(c["w"], c["h"], probs, c["lams"], "auto")
+        dt = time.perf_counter() - t0
+        st = s.stats()
+        cuts = flows.size
+        print(json.dumps(dict(cfg=a.cfg, rep=r, wall_ms=round(dt * 1e3, 2), cuts=cuts,
+                              cuts_per_s=round(cuts / dt, 1), flow=int(flows.sum()),
+                              **{k: (round(v, 3) if isinstance(v, float) else v) for k, v in st.items()})))
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,229 @@
+"""Parity of the CUDA engine against the reference (golden vectors) and the
+CPU oracle.  Integer capacities: flows and label masks must be bit-exact."""
+
+import os
+
+import numpy as np
+import pytest
+
+import oracle
+from conftest import (GOLDEN, load_composites, load_kat, load_random, load_seed_supergraphs,
+                      load_synth)
+from paper_1509_06004_b200 import (CAP_MAX, GridGraph, LambdaSchedule, SeedProblem, admit,
+                                   apply_swap, build_seed_supergraph, cut_cost, join,
+                                   maxflow_many, maxflow_pushrelabel, solve_composite,
+                                   solve_composites, solve_schedule_sequential,
+                                   solve_seed_supergraph, split, synth)
+
+pytestmark = pytest.mark.gpu
+
+
+def grid(w, h, s, t, nb):
+    return admit(GridGraph(w, h, np.asarray(s), np.asarray(t), np.asarray(nb)))
+
+
+def test_kat_fixtures(engine):
+    for name, k in load_kat().items():
+        r = maxflow_pushrelabel(grid(k["width"], k["height"], k["src"], k["snk"], k["nbr"]))
+        assert r.flow == k["flow"], name
+        assert r.labels.tolist() == k["labels"], name
+
+
+@pytest.mark.parametrize("name", ["random_8x8_seed101.npz", "random_3x3_seed102.npz"])
+def test_random_sweeps_one_batch(engine, name):
+    """test_acceptance.py:34-60 fixtures, all graphs in ONE device batch."""
+    cases = load_random(name)
+    got = maxflow_many([grid(w, h, s, t, nb) for (w, h, s, t, nb, _, _) in cases])
+    for r, (*_, flow, labels) in zip(got, cases):
+        assert r.flow == flow
+        assert np.array_equal(r.labels, labels)
+
+
+def test_random_sweep_individually(engine):
+    for (w, h, s, t, nb, flow, labels) in load_random("random_8x8_seed101.npz")[:60]:
+        r = maxflow_pushrelabel(grid(w, h, s, t, nb))
+        assert r.flow == flow and np.array_equal(r.labels, labels)
+
+
+def test_composites_with_swapped_spans(engine):
+    """Composite-level labels incl. swapped spans and padded rows
+    (supergraph.py:201-206)."""
+    from paper_1509_06004_b200 import Segment, SupergraphLayout
+    cases = load_composites()
+    tasks = []
+    for (w, h, s, t, nb, rec) in cases:
+        segs = tuple(Segment(i, o, sw_w, bool(f)) for i, (o, sw_w, f) in enumerate(rec["segments"]))
+        tasks.append((grid(w, h, s, t, nb), SupergraphLayout(segs, (), h)))
+    got = solve_composites(tasks)
+    for r, (*_, rec) in zip(got, cases):
+        assert r.flow == rec["flow"]
+        assert r.labels.tolist() == rec["labels"]
+    # and one at a time through the drop-in entry point
+    for (g, lay), (*_, rec) in list(zip(tasks, cases))[:10]:
+        r = solve_composite(g, lay)
+        assert r.flow == rec["flow"] and r.labels.tolist() == rec["labels"]
+
+
+def _problems(case):
+    W, H = case["width"], case["height"]
+    return [SeedProblem(W, H, p["base"], p["slope"], p["sink"], p["pairwise"],
+                        frozenset(p["fg"]), frozenset(p["bg"])) for p in case["problems"]]
+
+
+def test_seed_supergraph_device_builder(engine):
+    for case in load_seed_supergraphs():
+        probs = _problems(case)
+        res = solve_seed_supergraph(probs, LambdaSchedule(case["lambdas"]), case["mode"])
+        assert [s.swapped for s in res.layout.segments] == case["swapped"]
+        assert res.layout.total_width == case["composite_width"]
+        assert [c.flow for c in res.cuts] == case["flows"]
+        assert [c.labels.tolist() for c in res.cuts] == case["labels"]
+
+
+def test_seed_supergraph_host_composite_path(engine):
+    for case in load_seed_supergraphs():
+        probs = _problems(case)
+        comp, layout, originals = build_seed_supergraph(probs, LambdaSchedule(case["lambdas"]),
+                                                        case["mode"])
+        cut = solve_composite(comp, layout)
+        assert cut.flow == case["composite_flow"]
+        assert cut.labels.tolist() == case["composite_labels"]
+        parts = split(layout, cut, originals)
+        assert [p.flow for p in parts] == case["flows"]
+
+
+def test_c1_supergraph(engine):
+    """C1: 160x120, 1 seed, DEFAULT 20-lambda ladder, one supergraph."""
+    g = load_synth("c1_160x120.npz")
+    probs = synth.generate(160, 120, rng_seed=0).problems
+    sched = LambdaSchedule(g["lambdas"])
+    res = solve_seed_supergraph(probs, sched, "auto")
+    assert res.flow == 27814225
+    for c, flow, lab in zip(res.cuts, g["flows"], g["labels"]):
+        assert c.flow == flow
+        assert np.array_equal(c.labels, lab)
+    comp, layout, originals = build_seed_supergraph(probs, sched, "auto")
+    cut = solve_composite(comp, layout)
+    assert cut.flow == 27814225
+    parts = split(layout, cut, originals)
+    for p, flow, lab in zip(parts, g["flows"], g["labels"]):
+        assert p.flow == flow and np.array_equal(p.labels, lab)
+
+
+def test_c1_swapped_family_matches(engine):
+    """Forcing the s-t swap must not change any decoded cut."""
+    g = load_synth("c1_160x120.npz")
+    probs = synth.generate(160, 120, rng_seed=0).problems
+    res = solve_seed_supergraph(probs, LambdaSchedule(g["lambdas"]), "on")
+    assert all(s.swapped for s in res.layout.segments)
+    for c, flow, lab in zip(res.cuts, g["flows"], g["labels"]):
+        assert c.flow == flow and np.array_equal(c.labels, lab)
+
+
+@pytest.mark.skipif(not os.path.exists(os.path.join(GOLDEN, "c2_500x375.npz")),
+                    reason="C2 fixture not generated")
+def test_c2_sequential_and_supergraph(engine):
+    """C2: 500x375, L20 ladder: per-lambda reference cuts."""
+    g = load_synth("c2_500x375.npz")
+    p = synth.generate(500, 375, rng_seed=0).problems[0]
+    sched = LambdaSchedule(g["lambdas"])
+    res = solve_seed_supergraph([p], sched, "auto")
+    assert res.flow == 90475333
+    for c, flow, lab in zip(res.cuts, g["flows"], g["labels"]):
+        assert c.flow == flow and np.array_equal(c.labels, lab)
+    seq = solve_schedule_sequential(p, sched)
+    assert [c.flow for c in seq.cuts] == g["flows"]
+
+
+def test_repeated_runs_bit_identical(engine):
+    probs = synth.generate(160, 120, rng_seed=3).problems
+    sched = LambdaSchedule.default()
+    a = solve_seed_supergraph(probs, sched)
+    b = solve_seed_supergraph(probs, sched)
+    assert [c.flow for c in a.cuts] == [c.flow for c in b.cuts]
+    assert all(x.labels.tobytes() == y.labels.tobytes() for x, y in zip(a.cuts, b.cuts))
+
+
+def test_edge_shapes_vs_oracle(engine):
+    """1xN, Nx1, tiles straddling 32-px boundaries, CAP_MAX seeds."""
+    rng = np.random.default_rng(5)
+    graphs = []
+    for (w, h) in [(1, 1), (1, 40), (40, 1), (31, 33), (33, 31), (64, 64), (65, 3), (3, 97)]:
+        n = w * h
+        nb = rng.integers(0, 12, (4, h, w))
+        nb[0][:, 0] = 0
+        nb[1][:, -1] = 0
+        nb[2][0, :] = 0
+        nb[3][-1, :] = 0
+        src = rng.integers(0, 15, n)
+        snk = rng.integers(0, 15, n)
+        src[rng.integers(0, n)] = CAP_MAX
+        graphs.append(grid(w, h, src, snk, nb.reshape(4, -1)))
+    got = maxflow_many(graphs)
+    for g, r in zip(graphs, got):
+        f, lab, _ = oracle.solve(g.width, g.height, g.src_cap, g.snk_cap, g.nbr_cap)
+        assert r.flow == f and np.array_equal(r.labels, lab)
+        assert cut_cost(g, r.labels) == r.flow
+
+
+def test_wide_capacities_int32_edges(engine):
+    """Arc pairs above 255 select the int32 residual layout."""
+    rng = np.random.default_rng(9)
+    graphs = []
+    for _ in range(20):
+        w, h = int(rng.integers(2, 40)), int(rng.integers(2, 40))
+        n = w * h
+        nb = rng.integers(0, 5000, (4, h, w))
+        nb[0][:, 0] = 0
+        nb[1][:, -1] = 0
+        nb[2][0, :] = 0
+        nb[3][-1, :] = 0
+        graphs.append(grid(w, h, rng.integers(0, 20000, n), rng.integers(0, 20000, n),
+                           nb.reshape(4, -1)))
+    got = maxflow_many(graphs)
+    for g, r in zip(graphs, got):
+        f, lab, _ = oracle.solve(g.width, g.height, g.src_cap, g.snk_cap, g.nbr_cap)
+        assert r.flow == f and np.array_equal(r.labels, lab)
+
+
+def test_random_composites_vs_oracle(engine):
+    rng = np.random.default_rng(77)
+    tasks, ref = [], []
+    for _ in range(12):
+        k = int(rng.integers(1, 5))
+        h = int(rng.integers(5, 45))
+        graphs = []
+        for _ in range(k):
+            w = int(rng.integers(5, 45))
+            nb = rng.integers(0, 30, (4, h, w))
+            nb[0][:, 0] = 0
+            nb[1][:, -1] = 0
+            nb[2][0, :] = 0
+            nb[3][-1, :] = 0
+            graphs.append(grid(w, h, rng.integers(0, 60, w * h), rng.integers(0, 60, w * h),
+                               nb.reshape(4, -1)))
+        flags = [bool(rng.integers(0, 2)) for _ in graphs]
+        comp, lay = join([apply_swap(g) if f else g for g, f in zip(graphs, flags)], swapped=flags)
+        tasks.append((comp, lay))
+        ref.append(oracle.solve(comp.width, comp.height, comp.src_cap, comp.snk_cap, comp.nbr_cap,
+                                [(s.offset, s.width, s.swapped) for s in lay.segments]))
+    for r, (f, lab, _) in zip(solve_composites(tasks), ref):
+        assert r.flow == f and np.array_equal(r.labels, lab)
+
+
+def test_large_grid_properties(engine):
+    """C4-shaped single lambda (1920x1080): certificate checks that do not
+    need the reference -- the labels' cut cost equals the flow, and the
+    masks are nested along the schedule."""
+    p = synth.generate(1920, 1080, rng_seed=0).problems[0]
+    sched = LambdaSchedule((1, 7, 24))
+    res = solve_seed_supergraph([p], sched)
+    want = {1: 20920322, 7: 44135775, 24: 44904079}   # SURVEY.md Appendix A (scipy oracle)
+    prev = None
+    from paper_1509_06004_b200 import instantiate
+    for lam, c in zip(sched, res.cuts):
+        assert c.flow == want[lam]
+        assert cut_cost(instantiate(p, lam), c.labels) == c.flow
+        if prev is not None:
+            assert not (prev & ~c.labels.astype(bool)).any()
+        prev = c.labels.astype(bool)
