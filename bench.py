@@ -1,0 +1,377 @@
+"""Benchmark: lambda-graph min-cuts/sec of the supergraph path on B200.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config c2]
+                    [--impl b200|reference] [--no-cpu-baseline] [--no-cpmc]
+
+One step = one pass of the hot path over one batch: the seed supergraph of
+BASELINE.json config 2 (synthetic 500x375 image, 1 seed, 20-lambda ladder,
+integer capacities) built, solved and decoded on one GPU = 20 lambda-cuts.
+Under torchrun (N > 1) every rank solves its own supergraph per step (weak
+scaling, independent supergraphs, no data-path collective); ranks only
+meet in barriers and a max-reduction of their times.
+
+value : whole-job lambda-cuts/s with the seed planes already resident in
+        HBM (pmf_seed_run), device time from CUDA events on the engine's
+        stream, L2 flushed (256 MiB memset) between steps, max over ranks.
+e2e   : the same metric through the public API (solve_seed_supergraph)
+        from host SeedProblem objects: conversion + H2D + solve + D2H of
+        every label mask + CutResult construction, wall clock per step.
+--impl reference : the reference solver's algorithm (oracle/, a C
+        restatement of pmflow's push-relabel) on the host cores, same
+        config, same metric.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "lambda-graph min-cuts/sec"
+UNIT = "lambda-cuts/s"
+CONFIGS = {
+    "c1": dict(w=160, h=120, rows=1, cols=1, types=("A",), lams="default",
+               desc="C1: synthetic 160x120, 1 seed, DEFAULT 20-lambda ladder, one supergraph"),
+    "c2": dict(w=500, h=375, rows=1, cols=1, types=("A",), lams="L20",
+               desc="C2: synthetic 500x375 (VOC-sized), 1 seed, 20-lambda ladder L20, "
+                    "one supergraph (20 lambda-graphs) per GPU per step"),
+    "c4": dict(w=1920, h=1080, rows=1, cols=1, types=("A",), lams="C4",
+               desc="C4: synthetic 1920x1080, 1 seed, 8 lambdas per supergraph"),
+}
+BYTES_PER_PIXEL_PASS = {4: 24, 16: 48}   # load+store of w, h and the residual word(s)
+
+
+# ----------------------------------------------------------------- helpers
+
+def dist_env():
+    return (int(os.environ.get("RANK", 0)), int(os.environ.get("LOCAL_RANK", 0)),
+            int(os.environ.get("WORLD_SIZE", 1)))
+
+
+def shard(n_units: int, rank: int, world: int):
+    """Contiguous block of unit indices owned by ``rank`` (independent
+    supergraphs; no exchange between ranks)."""
+    base, extra = divmod(n_units, world)
+    start = rank * base + min(rank, extra)
+    return list(range(start, start + base + (1 if rank < extra else 0)))
+
+
+def reduce_max(value: float, device=None) -> float:
+    import torch
+    import torch.distributed as dist
+    if not (dist.is_available() and dist.is_initialized()):
+        return value
+    t = torch.tensor([value], dtype=torch.float64, device=device)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def barrier(device=None):
+    import torch.distributed as dist
+    if dist.is_available() and dist.is_initialized():
+        if device is not None and dist.get_backend() == "nccl":
+            dist.barrier(device_ids=[device])
+        else:
+            dist.barrier()
+
+
+def lambdas_for(name):
+    from paper_1509_06004_b200 import synth
+    from paper_1509_06004_b200.parametric import DEFAULT_LAMBDA_VALUES
+    return {"default": DEFAULT_LAMBDA_VALUES, "L20": synth.L20, "C4": synth.C4_LAMBDAS}[name]
+
+
+def measured_peaks():
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(path):
+        with open(path) as f:
+            d = json.load(f)
+        return float(d["hbm_gbs"]), "measured"
+    return 6650.0, "fallback"
+
+
+def committed_traffic():
+    """Per-launch DRAM bytes of k_push from the committed ncu capture."""
+    path = os.path.join(ROOT, "profiles", "push_traffic.json")
+    if not os.path.exists(path):
+        return None
+    with open(path) as f:
+        d = json.load(f)
+    return d.get("dram_bytes_per_launch")
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index, self.rows, self.proc = index, [], None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self._t = threading.Thread(target=self._read, daemon=True)
+            self._t.start()
+        except OSError:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) == 6:
+                self.rows.append(parts)
+
+    def __exit__(self, *exc):
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        names = ("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap")
+        reasons = sorted({names[i] for r in self.rows for i in range(4) if r[2 + i] == "Active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
+                "samples": len(self.rows)}
+
+
+# ------------------------------------------------------------- CPU baseline
+
+def cpu_solve_config(cfg, rng_seed, threads):
+    """The reference's solver (C restatement in oracle/) on every lambda graph
+    of one supergraph, per lambda as solve_schedule_sequential does; returns
+    (n_cuts, seconds, total_flow)."""
+    import oracle
+    from paper_1509_06004_b200 import synth
+    lams = lambdas_for(cfg["lams"])
+    batch = synth.generate(cfg["w"], cfg["h"], cfg["rows"], cfg["cols"], rng_seed=rng_seed,
+                           types=cfg["types"])
+    jobs = []
+    for p in batch.problems:
+        for lam in lams:
+            s, t, nb = oracle.instantiate(p.unary_base, p.unary_slope, p.sink_base, p.pairwise,
+                                          p.fg_seeds, p.bg_seeds, lam)
+            jobs.append((cfg["w"], cfg["h"], s, t, nb))
+    t0 = time.perf_counter()
+    res = oracle.solve_many(jobs, threads=threads)
+    dt = time.perf_counter() - t0
+    return len(jobs), dt, sum(r[0] for r in res)
+
+
+def run_reference(args, cfg):
+    rank, _, world = dist_env()
+    if rank != 0:
+        return
+    import oracle
+    oracle.build()
+    threads = os.cpu_count() or 1
+    for _ in range(args.warmup):
+        cpu_solve_config(cfg, 0, threads)
+    tot_cuts, tot_s = 0, 0.0
+    for _ in range(args.steps):
+        n, dt, _ = cpu_solve_config(cfg, 0, threads)
+        tot_cuts += n
+        tot_s += dt
+    value = tot_cuts / tot_s
+    sample = (f"{cfg['desc']}: all lambda-graphs of one supergraph per step, solved with the "
+              f"reference push-relabel restated in C (oracle/pmflow_oracle.c), per lambda as "
+              f"solve_schedule_sequential, {threads} host threads")
+    print(json.dumps({
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * tot_s / args.steps,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "int32",
+        "data": "synthetic", "config": {"workload": cfg["desc"]},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "port",
+                         "sample": sample},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }), flush=True)
+
+
+# ---------------------------------------------------------------- GPU arm
+
+def run_b200(args, cfg):
+    import torch
+    import torch.distributed as dist
+
+    from paper_1509_06004_b200 import LambdaSchedule, _native, solve_seed_supergraph, synth
+    from paper_1509_06004_b200.supergraph import check_seed_supergraph
+
+    rank, local, world = dist_env()
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    dev = local
+    sched = LambdaSchedule(lambdas_for(cfg["lams"]))
+    # weak scaling: rank r owns its own image (rng_seed = r)
+    batch = synth.generate(cfg["w"], cfg["h"], cfg["rows"], cfg["cols"], rng_seed=rank,
+                           types=cfg["types"])
+    problems = check_seed_supergraph(batch.problems, sched, "auto")
+    cuts_per_step = len(problems) * len(sched)
+
+    solver = _native.solver_for_thread(dev)
+    solver.set("timing", 1)
+    stream = torch.cuda.ExternalStream(solver.stream_handle(), device=dev)
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+    solver.seed_stage(cfg["w"], cfg["h"], problems, sched.values, "auto")
+    for _ in range(args.warmup):
+        solver.seed_run()
+    _, ref_flows, _ = solver.seed_fetch(labels=False)
+
+    # ---- device-resident timed region
+    barrier(dev)
+    torch.cuda.synchronize()
+    steps_ms, stats = [], []
+    with ClockSampler(dev) as clk:
+        for _ in range(args.steps):
+            with torch.cuda.stream(stream):
+                flush.zero_()                      # L2 flush, outside the timed events
+                e0 = torch.cuda.Event(enable_timing=True)
+                e1 = torch.cuda.Event(enable_timing=True)
+                e0.record(stream)
+            solver.seed_run()
+            with torch.cuda.stream(stream):
+                e1.record(stream)
+            e1.synchronize()
+            steps_ms.append(e0.elapsed_time(e1))
+            stats.append(solver.stats())
+    torch.cuda.synchronize()
+    barrier(dev)
+    _, flows, _ = solver.seed_fetch(labels=False)
+    assert (flows == ref_flows).all(), "flows changed between runs"
+    dev_s = sum(steps_ms) / 1e3
+    dev_s_max = reduce_max(dev_s, torch.device("cuda", dev))
+    value = world * cuts_per_step * args.steps / dev_s_max
+
+    # roofline of the dominant kernel (push-relabel sweep)
+    push_ms = sum(s["ms_push"] for s in stats)
+    push_launches = sum(s["push_sweeps"] for s in stats)
+    tile_passes = sum(s["push_tile_passes"] for s in stats)
+    edge_bytes = stats[-1]["edge_bytes"]
+    bpp = BYTES_PER_PIXEL_PASS[edge_bytes]
+    alg_bytes_per_launch = tile_passes * 1024 * bpp / max(push_launches, 1)
+    avg_launch_s = push_ms / 1e3 / max(push_launches, 1)
+    achieved = alg_bytes_per_launch / avg_launch_s / 1e9 if avg_launch_s else 0.0
+    peak, peak_kind = measured_peaks()
+    traffic = committed_traffic()
+    total_ms = sum(s["ms_total"] for s in stats)
+    share = {k: round(sum(s[k] for s in stats) / total_ms, 4) for k in
+             ("ms_push", "ms_bfs", "ms_seed", "ms_labels", "ms_build")} if total_ms else {}
+
+    # ---- end to end through the public API (host SeedProblems in, CutResults out)
+    e2e_s, h2d, d2h = 0.0, 0, 0
+    barrier(dev)
+    for i in range(args.warmup + args.steps):
+        t0 = time.perf_counter()
+        res = solve_seed_supergraph(problems, sched, "auto", device=dev)
+        dt = time.perf_counter() - t0
+        if i >= args.warmup:
+            e2e_s += dt
+            st = solver.stats()
+            h2d += st["h2d_bytes"]
+            d2h += st["d2h_bytes"]
+    assert [c.flow for c in res.cuts] == [int(f) for f in ref_flows.reshape(-1)]
+    e2e_s_max = reduce_max(e2e_s, torch.device("cuda", dev))
+    e2e_value = world * cuts_per_step * args.steps / e2e_s_max
+
+    # ---- CPMC image (C3) device time, reported beside the headline
+    cpmc = None
+    if args.cpmc and rank == 0:
+        c3 = synth.generate(500, 375, 5, 5, rng_seed=0, types=("A", "B"))
+        c3p = check_seed_supergraph(c3.problems, sched, "auto")
+        s3 = _native.Solver(dev)
+        s3.seed_stage(500, 375, c3p, sched.values, "auto")
+        s3.seed_run()
+        s3.seed_run()
+        st3 = s3.stats()
+        cpmc = {"ms_per_image": round(st3["ms_device"], 3), "lambda_cuts": len(c3p) * len(sched),
+                "lambda_cuts_per_s": round(len(c3p) * len(sched) / st3["ms_device"] * 1e3, 1),
+                "image": "500x375, 25 seeds x 2 types x 20 lambdas, one device batch"}
+        s3.close()
+
+    # ---- CPU baseline (rank 0, N == 1 only)
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        import oracle
+        oracle.build()
+        threads = os.cpu_count() or 1
+        n, dt, flow = cpu_solve_config(cfg, 0, threads)
+        assert flow == int(ref_flows.sum()), "oracle and engine disagree on the C2 flow"
+        cpu = {"value": n / dt, "unit": UNIT, "cores": threads, "kind": "port",
+               "sample": f"{n} lambda-graphs of the rank-0 supergraph ({cfg['desc'].split(':')[0]}), "
+                         "reference push-relabel restated in C (oracle/pmflow_oracle.c), "
+                         f"per lambda, {threads} threads; took {dt:.2f} s"}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": 1e3 * dev_s_max / args.steps, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "int32", "data": "synthetic",
+            "config": {"workload": cfg["desc"], "lambda_cuts_per_step_per_gpu": cuts_per_step,
+                       "image": f"{cfg['w']}x{cfg['h']}", "rng_seed": "rank",
+                       "l2": "flushed between steps (256 MiB memset, outside the timed events)",
+                       "parallelism": f"{world} GPU(s), independent supergraphs, no collectives"},
+            "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": h2d // args.steps,
+                    "d2h_bytes_per_step": d2h // args.steps},
+            "roofline": {"bound": "hbm", "kernel": "k_push (push-relabel tile sweep)",
+                         "achieved": achieved, "peak": peak, "unit": "GB/s",
+                         "frac": achieved / peak, "traffic": traffic, "peak_kind": peak_kind,
+                         "bytes_per_pixel_pass": bpp,
+                         "pixel_passes_per_s": tile_passes * 1024 / (push_ms / 1e3) if push_ms else 0,
+                         "avg_launch_us": avg_launch_s * 1e6,
+                         "time_share": share},
+            "cpu_baseline": cpu,
+            "clocks": clk.summary(),
+            "gpu_launches": int(sum(s["launches"] for s in stats)),
+            "solver": {k: stats[-1][k] for k in ("cycles", "push_sweeps", "push_tile_passes",
+                                                  "bfs_sweeps", "bfs_tile_passes", "tiles",
+                                                  "edge_bytes")},
+            "cpmc": cpmc,
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", default="c2", choices=sorted(CONFIGS))
+    ap.add_argument("--impl", default="b200", choices=("b200", "reference"))
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-cpmc", dest="cpmc", action="store_false")
+    args = ap.parse_args()
+    if args.warmup < 3 and args.impl == "b200":
+        print("warning: fewer than 3 warm-up steps", file=sys.stderr)
+    cfg = CONFIGS[args.config]
+    if args.impl == "reference":
+        run_reference(args, cfg)
+    else:
+        run_b200(args, cfg)
+
+
+if __name__ == "__main__":
+    main()

@@ -71,6 +71,10 @@ typedef struct pmf_stats {
     double ms_seed;             /* active-tile seeding passes                 */
     double ms_h2d;              /* host->device copies                        */
     double ms_d2h;              /* device->host copies                        */
+    double ms_device;           /* device time of the last run (always on)    */
+    int64_t launches;           /* kernels launched by the last run           */
+    int64_t h2d_bytes;          /* host->device bytes of the last stage       */
+    int64_t d2h_bytes;          /* device->host bytes of the last fetch       */
 } pmf_stats;
 
 /* Create / destroy a solver bound to one CUDA device and its own stream. */
@@ -82,6 +86,10 @@ int pmf_solver_destroy(pmf_solver *s);
  * launches between convergence checks), "timing" (0/1 device timings),
  * "max_cycles" (non-convergence guard). Returns PMF_ERR_ARG if unknown. */
 int pmf_solver_set(pmf_solver *s, const char *name, int64_t value);
+
+/* The solver's CUDA stream (a cudaStream_t) for callers that record their
+ * own events or order their own work against the engine. */
+int pmf_solver_stream(const pmf_solver *s, void **stream_out);
 
 /* Thread-local message describing the last error on this thread. */
 const char *pmf_last_error(void);
@@ -130,6 +138,24 @@ int pmf_solve_seed_batch(pmf_solver *s, int32_t nprob, int32_t width, int32_t he
                          const int64_t *const *bg_idx, const int32_t *n_bg,
                          int32_t nlam, const int64_t *lambdas, int32_t swap_mode,
                          uint8_t *swapped_out, int64_t *flows_out, uint8_t *labels_out);
+
+/*
+ * pmf_solve_seed_batch in three steps, for callers that keep inputs resident
+ * on the device across solves (benchmarks, repeated schedules):
+ *   pmf_seed_stage  validate + convert the planes and copy them to the device
+ *                   (same arguments as pmf_solve_seed_batch minus outputs);
+ *   pmf_seed_run    build + solve the staged batch; results stay on device;
+ *   pmf_seed_fetch  copy swapped flags, flows and (if labels_out != NULL)
+ *                   label masks of the last run to the host.
+ */
+int pmf_seed_stage(pmf_solver *s, int32_t nprob, int32_t width, int32_t height,
+                   const int64_t *const *unary_base, const int64_t *const *unary_slope,
+                   const int64_t *const *sink_base, const int64_t *const *pairwise,
+                   const int64_t *const *fg_idx, const int32_t *n_fg,
+                   const int64_t *const *bg_idx, const int32_t *n_bg,
+                   int32_t nlam, const int64_t *lambdas, int32_t swap_mode);
+int pmf_seed_run(pmf_solver *s);
+int pmf_seed_fetch(pmf_solver *s, uint8_t *swapped_out, int64_t *flows_out, uint8_t *labels_out);
 
 #ifdef __cplusplus
 }

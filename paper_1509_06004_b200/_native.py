@@ -22,7 +22,8 @@ PMF_OK, PMF_ERR_ARG, PMF_ERR_CUDA, PMF_ERR_NOCONV, PMF_ERR_NONMAX, PMF_ERR_RANGE
 SWAP_MODES = {"auto": 0, "on": 1, "off": 2}
 
 EXPORTS = ("pmf_solver_create", "pmf_solver_destroy", "pmf_solver_set", "pmf_last_error",
-           "pmf_solver_stats", "pmf_solve_composites", "pmf_solve_seed_batch")
+           "pmf_solver_stats", "pmf_solver_stream", "pmf_solve_composites", "pmf_solve_seed_batch",
+           "pmf_seed_stage", "pmf_seed_run", "pmf_seed_fetch")
 
 
 class NativeUnavailable(RuntimeError):
@@ -35,7 +36,8 @@ class PmfStats(ctypes.Structure):
         "bfs_sweeps", "full_passes", "grids", "tiles", "pixels")] + [
         ("edge_bytes", ctypes.c_int32), ("timed", ctypes.c_int32)] + [
         (k, ctypes.c_double) for k in ("ms_total", "ms_build", "ms_push", "ms_bfs", "ms_labels",
-                                       "ms_seed", "ms_h2d", "ms_d2h")]
+                                       "ms_seed", "ms_h2d", "ms_d2h", "ms_device")] + [
+        (k, ctypes.c_int64) for k in ("launches", "h2d_bytes", "d2h_bytes")]
 
     def as_dict(self):
         return {k: getattr(self, k) for k, _ in self._fields_}
@@ -69,6 +71,12 @@ def load_library(path: str = LIB_PATH):
         lib.pmf_solve_seed_batch.argtypes = [
             vp, i32, i32, i32, P(vp), P(vp), P(vp), P(vp), P(vp), P(i32), P(vp), P(i32),
             i32, P(i64), i32, P(u8), P(i64), P(u8)]
+        lib.pmf_seed_stage.argtypes = [
+            vp, i32, i32, i32, P(vp), P(vp), P(vp), P(vp), P(vp), P(i32), P(vp), P(i32),
+            i32, P(i64), i32]
+        lib.pmf_seed_run.argtypes = [vp]
+        lib.pmf_seed_fetch.argtypes = [vp, P(u8), P(i64), P(u8)]
+        lib.pmf_solver_stream.argtypes = [vp, P(vp)]
         for name in EXPORTS:
             if name != "pmf_last_error":
                 getattr(lib, name).restype = ctypes.c_int
@@ -162,12 +170,14 @@ class Solver:
             _raise_for(rc)
         return [(int(f), l) for f, l in zip(flows, labs)]
 
-    def solve_seed_batch(self, width, height, problems, lambdas, swap_mode="auto"):
-        """problems: objects with unary_base, unary_slope, sink_base, pairwise
-        (int64) and _fg_idx/_bg_idx.  Returns (swapped (P,), flows (P, K),
-        labels (P, K, n) uint8)."""
-        P_, K = len(problems), len(lambdas)
-        n = width * height
+    def stream_handle(self) -> int:
+        """The solver's cudaStream_t as an integer (torch.cuda.ExternalStream)."""
+        out = ctypes.c_void_p()
+        self._lib.pmf_solver_stream(self._h, ctypes.byref(out))
+        return int(out.value or 0)
+
+    def seed_stage(self, width, height, problems, lambdas, swap_mode="auto"):
+        """Validate/convert seed problems and copy them to the device."""
         ub = [np.ascontiguousarray(p.unary_base, np.int64) for p in problems]
         us = [np.ascontiguousarray(p.unary_slope, np.int64) for p in problems]
         sb = [np.ascontiguousarray(p.sink_base, np.int64) for p in problems]
@@ -179,19 +189,44 @@ class Solver:
         fgp = [a if a.size else np.zeros(1, np.int64) for a in fg]
         bgp = [a if a.size else np.zeros(1, np.int64) for a in bg]
         lam = np.ascontiguousarray(lambdas, np.int64)
-        swapped = np.zeros(P_, np.uint8)
-        flows = np.zeros(P_ * K, np.int64)
-        labels = np.empty((P_, K, n), np.uint8)
         Pt = ctypes.POINTER
-        rc = self._lib.pmf_solve_seed_batch(
-            self._h, P_, width, height, _ptrs(ub), _ptrs(us), _ptrs(sb), _ptrs(pw),
+        rc = self._lib.pmf_seed_stage(
+            self._h, len(problems), width, height, _ptrs(ub), _ptrs(us), _ptrs(sb), _ptrs(pw),
             _ptrs(fgp), nfg.ctypes.data_as(Pt(ctypes.c_int32)), _ptrs(bgp),
-            nbg.ctypes.data_as(Pt(ctypes.c_int32)), K, lam.ctypes.data_as(Pt(ctypes.c_int64)),
-            SWAP_MODES[swap_mode], swapped.ctypes.data_as(Pt(ctypes.c_uint8)),
-            flows.ctypes.data_as(Pt(ctypes.c_int64)), labels.ctypes.data_as(Pt(ctypes.c_uint8)))
+            nbg.ctypes.data_as(Pt(ctypes.c_int32)), lam.size,
+            lam.ctypes.data_as(Pt(ctypes.c_int64)), SWAP_MODES[swap_mode])
         if rc:
             _raise_for(rc)
-        return swapped.astype(bool), flows.reshape(P_, K), labels
+        self._staged = (width * height, len(problems), lam.size)
+
+    def seed_run(self):
+        """Build + solve the staged batch; results stay on the device."""
+        rc = self._lib.pmf_seed_run(self._h)
+        if rc:
+            _raise_for(rc)
+
+    def seed_fetch(self, labels=True):
+        """(swapped (P,), flows (P, K), labels (P, K, n) uint8 or None)."""
+        n, P_, K = self._staged
+        Pt = ctypes.POINTER
+        swapped = np.zeros(P_, np.uint8)
+        flows = np.zeros(P_ * K, np.int64)
+        lab = np.empty((P_, K, n), np.uint8) if labels else None
+        rc = self._lib.pmf_seed_fetch(
+            self._h, swapped.ctypes.data_as(Pt(ctypes.c_uint8)),
+            flows.ctypes.data_as(Pt(ctypes.c_int64)),
+            lab.ctypes.data_as(Pt(ctypes.c_uint8)) if labels else None)
+        if rc:
+            _raise_for(rc)
+        return swapped.astype(bool), flows.reshape(P_, K), lab
+
+    def solve_seed_batch(self, width, height, problems, lambdas, swap_mode="auto"):
+        """problems: objects with unary_base, unary_slope, sink_base, pairwise
+        (int64) and _fg_idx/_bg_idx.  Returns (swapped (P,), flows (P, K),
+        labels (P, K, n) uint8)."""
+        self.seed_stage(width, height, problems, lambdas, swap_mode)
+        self.seed_run()
+        return self.seed_fetch(True)
 
 
 _tls = threading.local()

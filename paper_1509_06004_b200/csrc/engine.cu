@@ -80,6 +80,47 @@ enum Cat { C_BUILD = 0, C_BFS, C_PUSH, C_SEED, C_LAB, C_H2D, C_D2H, C_N };
 
 inline int64_t cdiv(int64_t a, int64_t b) { return (a + b - 1) / b; }
 
+
+struct Layout {
+    std::vector<GridDesc> grids;
+    std::vector<int32_t> tile_grid;
+    int64_t ntiles = 0, out_bytes = 0, pixels = 0;
+    void clear() {
+        grids.clear();
+        tile_grid.clear();
+        ntiles = out_bytes = pixels = 0;
+    }
+    void add(int32_t W, int32_t H, int32_t kind, int32_t colswap_off, int32_t prob, int32_t lam) {
+        GridDesc g{};
+        g.W = W;
+        g.H = H;
+        g.ntx = int32_t(cdiv(W, TW));
+        g.nty = int32_t(cdiv(H, TH));
+        g.tile_base = ntiles;
+        g.out_off = out_bytes;
+        g.kind = kind;
+        g.colswap_off = colswap_off;
+        g.prob = prob;
+        g.lam = lam;
+        int64_t nt = int64_t(g.ntx) * g.nty;
+        tile_grid.insert(tile_grid.end(), size_t(nt), int32_t(grids.size()));
+        ntiles += nt;
+        out_bytes += int64_t(W) * H;
+        pixels += int64_t(W) * H;
+        grids.push_back(g);
+    }
+};
+
+// A staged seed batch: converted planes resident on the device, ready to be
+// built and solved any number of times (pmf_seed_run).
+struct SeedStage {
+    bool valid = false;
+    int32_t nprob = 0, nlam = 0, W = 0, H = 0, swap_mode = 0;
+    bool u8 = true;
+    std::vector<int64_t> offs;      // [plane_off(nprob) | pw_off(nprob)]
+    std::vector<int64_t> lambdas;
+};
+
 }  // namespace
 
 struct pmf_solver {
@@ -98,13 +139,19 @@ struct pmf_solver {
         d_snk, d_drain, d_err, d_stat, d_colswap, d_out, d_in32, d_pw, d_mask, d_off, d_lam,
         d_swapcnt, d_swapflag;
     HostBuf h_in32, h_pw, h_mask, h_out, h_small;
+    Layout lay;
+    std::vector<int32_t> ones;
+    std::vector<uint8_t> colswap;
+    std::vector<int64_t> comp_off;
+    SeedStage stage;
+    Ctx ctx{};
     std::vector<cudaEvent_t> ev_pool;
     std::vector<std::pair<int, int>> ev_marks;  // (category, event index of start)
     size_t ev_used = 0;
+    cudaEvent_t ev_run[2] = {nullptr, nullptr};
     pmf_stats stats{};
     int edge_bytes = 4;
 
-    // ---------------------------------------------------------------- timing
     int ev_get(cudaEvent_t *e) {
         if (ev_used == ev_pool.size()) {
             cudaEvent_t x;
@@ -114,7 +161,7 @@ struct pmf_solver {
         *e = ev_pool[ev_used++];
         return 0;
     }
-    // mark the start of a timed region of category cat
+    // mark the start of a timed region of category cat (timing mode only)
     void tmark(int cat) {
         if (!timing) return;
         cudaEvent_t e;
@@ -124,40 +171,19 @@ struct pmf_solver {
     }
 };
 
+// every kernel launch of a run goes through LAUNCH (counted in stats.launches)
+#define LAUNCH(s, ...)           \
+    do {                         \
+        __VA_ARGS__;             \
+        (s)->stats.launches++;   \
+    } while (0)
+
 namespace {
 
-// --------------------------------------------------------------------------
-// batch layout
-// --------------------------------------------------------------------------
-
-struct Layout {
-    std::vector<GridDesc> grids;
-    std::vector<int32_t> tile_grid;
-    int64_t ntiles = 0, out_bytes = 0, pixels = 0;
-    void add(int32_t W, int32_t H, int32_t kind, int32_t colswap_off, int32_t prob, int32_t lam) {
-        GridDesc g{};
-        g.W = W;
-        g.H = H;
-        g.ntx = int32_t(cdiv(W, TW));
-        g.nty = int32_t(cdiv(H, TH));
-        g.tile_base = ntiles;
-        g.out_off = out_bytes;
-        g.kind = kind;
-        g.colswap_off = colswap_off;
-        g.prob = prob;
-        g.lam = lam;
-        int64_t nt = int64_t(g.ntx) * g.nty;
-        for (int64_t i = 0; i < nt; i++) tile_grid.push_back(int32_t(grids.size()));
-        ntiles += nt;
-        out_bytes += int64_t(W) * H;
-        pixels += int64_t(W) * H;
-        grids.push_back(g);
-    }
-};
-
-int setup_state(pmf_solver *s, const Layout &L, int edge_bytes, Ctx *c) {
+int setup_state(pmf_solver *s, int edge_bytes) {
+    const Layout &L = s->lay;
     const int64_t T = L.ntiles, P = T * TPIX, G = int64_t(L.grids.size());
-    if (T >= (int64_t(1) << 31) / TPIX * 64) return fail(PMF_ERR_ARG, "batch too large (%lld tiles)", (long long)T);
+    if (T >= (int64_t(1) << 31) / 2) return fail(PMF_ERR_ARG, "batch too large (%lld tiles)", (long long)T);
     int rc = 0;
     if ((rc = s->d_w.ensure(P * 4)) || (rc = s->d_h.ensure(P * 4)) ||
         (rc = s->d_r.ensure(P * size_t(edge_bytes))) || (rc = s->d_lab.ensure(P)) ||
@@ -166,21 +192,22 @@ int setup_state(pmf_solver *s, const Layout &L, int edge_bytes, Ctx *c) {
         (rc = s->d_list.ensure(2 * T * 4)) || (rc = s->d_inq.ensure(2 * T * 4)) ||
         (rc = s->d_cnt.ensure(64)) || (rc = s->d_snk.ensure(G * 8)) || (rc = s->d_drain.ensure(G * 8)) ||
         (rc = s->d_err.ensure(64)) || (rc = s->d_stat.ensure(ST_NSTAT * 8)) ||
-        (rc = s->d_out.ensure(std::max<int64_t>(L.out_bytes, 1))))
+        (rc = s->d_out.ensure(std::max<int64_t>(L.out_bytes, 1))) || (rc = s->d_colswap.ensure(64)) ||
+        (rc = s->d_swapflag.ensure(64)))
         return rc;
     s->edge_bytes = edge_bytes;
+    // host sources live in the solver (s->lay, s->ones) until the next setup
     CK(cudaMemcpyAsync(s->d_tile_grid.p, L.tile_grid.data(), T * 4, cudaMemcpyHostToDevice, s->st));
     CK(cudaMemcpyAsync(s->d_grids.p, L.grids.data(), G * sizeof(GridDesc), cudaMemcpyHostToDevice, s->st));
-    std::vector<int32_t> ones(G, 1);
-    CK(cudaMemcpyAsync(s->d_live.p, ones.data(), G * 4, cudaMemcpyHostToDevice, s->st));
+    s->ones.assign(size_t(G), 1);
+    CK(cudaMemcpyAsync(s->d_live.p, s->ones.data(), G * 4, cudaMemcpyHostToDevice, s->st));
     CK(cudaMemsetAsync(s->d_act.p, 0, G * 4, s->st));
     CK(cudaMemsetAsync(s->d_snk.p, 0, G * 8, s->st));
     CK(cudaMemsetAsync(s->d_drain.p, 0, G * 8, s->st));
     CK(cudaMemsetAsync(s->d_err.p, 0, 64, s->st));
     CK(cudaMemsetAsync(s->d_stat.p, 0, ST_NSTAT * 8, s->st));
-    // the host vectors above are stack-owned: make the copies land first
-    CK(cudaStreamSynchronize(s->st));
-    Ctx x{};
+    Ctx &x = s->ctx;
+    x = Ctx{};
     x.w = s->d_w.as<int32_t>();
     x.h = s->d_h.as<int32_t>();
     x.r = s->d_r.p;
@@ -202,7 +229,6 @@ int setup_state(pmf_solver *s, const Layout &L, int edge_bytes, Ctx *c) {
     x.swapflag = s->d_swapflag.as<int32_t>();
     x.out = s->d_out.as<uint8_t>();
     x.ntiles = T;
-    *c = x;
     return 0;
 }
 
@@ -225,8 +251,8 @@ int run_bfs(pmf_solver *s, const Ctx &c, bool sink, int64_t *sweeps) {
     int k = 0;
     for (;;) {
         for (int j = 0; j < s->bfs_chunk; j++, k++) {
-            if (sink) k_bfs_sink<E><<<s->grid_bfs, NT, 0, s->st>>>(c, k);
-            else k_bfs_src<E><<<s->grid_bfs, NT, 0, s->st>>>(c, k);
+            if (sink) LAUNCH(s, (k_bfs_sink<E><<<s->grid_bfs, NT, 0, s->st>>>(c, k)));
+            else LAUNCH(s, (k_bfs_src<E><<<s->grid_bfs, NT, 0, s->st>>>(c, k)));
         }
         CK(cudaGetLastError());
         *sweeps += s->bfs_chunk;
@@ -248,14 +274,14 @@ int run_solve(pmf_solver *s, const Ctx &c, int32_t ngrids) {
         // exact global relabel
         s->tmark(C_BFS);
         if ((rc = begin_phase(s, c))) return rc;
-        k_gr_init<<<s->grid_full, NT, 0, s->st>>>(c);
+        LAUNCH(s, (k_gr_init<<<s->grid_full, NT, 0, s->st>>>(c)));
         s->stats.full_passes++;
         if ((rc = run_bfs<E>(s, c, true, &s->stats.bfs_sweeps))) return rc;
         // list active tiles; retire grids without active pixels
         s->tmark(C_SEED);
         if ((rc = begin_phase(s, c))) return rc;
-        k_seed_push<<<s->grid_full, NT, 0, s->st>>>(c);
-        k_update_live<<<int(cdiv(ngrids, 256)), 256, 0, s->st>>>(c, ngrids);
+        LAUNCH(s, (k_seed_push<<<s->grid_full, NT, 0, s->st>>>(c)));
+        LAUNCH(s, (k_update_live<<<int(cdiv(ngrids, 256)), 256, 0, s->st>>>(c, ngrids)));
         CK(cudaGetLastError());
         s->stats.full_passes++;
         int32_t nact = 0;
@@ -263,7 +289,7 @@ int run_solve(pmf_solver *s, const Ctx &c, int32_t ngrids) {
         if (nact == 0) break;
         s->tmark(C_PUSH);
         for (int k = 0; k < s->push_sweeps; k++)
-            k_push<E><<<s->grid_push, NT, 0, s->st>>>(c, k, s->push_iters);
+            LAUNCH(s, (k_push<E><<<s->grid_push, NT, 0, s->st>>>(c, k, s->push_iters)));
         CK(cudaGetLastError());
         s->stats.push_sweeps += s->push_sweeps;
     }
@@ -271,21 +297,34 @@ int run_solve(pmf_solver *s, const Ctx &c, int32_t ngrids) {
     // labels: source-side closure, then emit
     s->tmark(C_LAB);
     if ((rc = begin_phase(s, c))) return rc;
-    k_lab_seed<<<s->grid_full, NT, 0, s->st>>>(c);
+    LAUNCH(s, (k_lab_seed<<<s->grid_full, NT, 0, s->st>>>(c)));
     s->stats.full_passes++;
     if ((rc = run_bfs<E>(s, c, false, &s->stats.bfs_sweeps))) return rc;
-    k_emit<<<s->grid_full, NT, 0, s->st>>>(c);
+    LAUNCH(s, (k_emit<<<s->grid_full, NT, 0, s->st>>>(c)));
     s->stats.full_passes++;
     CK(cudaGetLastError());
     return 0;
 }
 
-int finish_stats(pmf_solver *s, const Layout &L) {
+// Device-side run bracket: always-on events around the whole run give
+// ms_device; timing mode adds per-phase marks.
+int run_begin(pmf_solver *s) {
+    s->stats = pmf_stats{};
+    s->ev_used = 0;
+    s->ev_marks.clear();
+    CK(cudaEventRecord(s->ev_run[0], s->st));
+    return 0;
+}
+
+int run_end(pmf_solver *s) {
+    s->tmark(C_N);
+    CK(cudaEventRecord(s->ev_run[1], s->st));
     unsigned long long st[ST_NSTAT];
     int32_t err = 0;
     CK(cudaMemcpyAsync(st, s->d_stat.p, sizeof st, cudaMemcpyDeviceToHost, s->st));
     CK(cudaMemcpyAsync(&err, s->d_err.p, 4, cudaMemcpyDeviceToHost, s->st));
     CK(cudaStreamSynchronize(s->st));
+    const Layout &L = s->lay;
     s->stats.push_tile_passes = int64_t(st[ST_PUSH]);
     s->stats.bfs_tile_passes = int64_t(st[ST_BFS]);
     s->stats.label_tile_passes = int64_t(st[ST_LAB]);
@@ -293,6 +332,9 @@ int finish_stats(pmf_solver *s, const Layout &L) {
     s->stats.tiles = L.ntiles;
     s->stats.pixels = L.pixels;
     s->stats.edge_bytes = s->edge_bytes;
+    float dev = 0;
+    cudaEventElapsedTime(&dev, s->ev_run[0], s->ev_run[1]);
+    s->stats.ms_device = dev;
     if (s->timing && !s->ev_marks.empty()) {
         double cat[C_N] = {0};
         for (size_t i = 0; i + 1 < s->ev_marks.size(); i++) {
@@ -317,12 +359,6 @@ int finish_stats(pmf_solver *s, const Layout &L) {
     return 0;
 }
 
-void begin_stats(pmf_solver *s) {
-    s->stats = pmf_stats{};
-    s->ev_used = 0;
-    s->ev_marks.clear();
-}
-
 // narrow an int64 plane into int32 staging, clamping into [lo, hi]
 inline void narrow(int32_t *dst, const int64_t *src, int64_t n, int64_t lo, int64_t hi) {
     for (int64_t i = 0; i < n; i++) {
@@ -345,7 +381,7 @@ int64_t max_pair(const int32_t *nb, int W, int H) {
 }
 
 template <class E>
-int grids_for_push(pmf_solver *s) {
+int grids_for(pmf_solver *s) {
     int occ = 0;
     CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_push<E>, NT, 0));
     s->grid_push = std::max(1, occ) * s->sms;
@@ -356,30 +392,200 @@ int grids_for_push(pmf_solver *s) {
 }
 
 // --------------------------------------------------------------------------
+// seed batches: stage (host convert + H2D) / run (device only) / fetch (D2H)
+// --------------------------------------------------------------------------
+
+template <class E>
+int seed_run_t(pmf_solver *s) {
+    SeedStage &S = s->stage;
+    int rc = grids_for<E>(s);
+    if (rc) return rc;
+    if ((rc = setup_state(s, E::kBytes))) return rc;
+    if ((rc = s->d_swapflag.ensure(size_t(S.nprob) * 4))) return rc;
+    s->ctx.swapflag = s->d_swapflag.as<int32_t>();
+    const Ctx &c = s->ctx;
+    const int64_t n = int64_t(S.W) * S.H;
+    s->tmark(C_BUILD);
+    CK(cudaMemsetAsync(s->d_swapcnt.p, 0, size_t(S.nprob) * 8, s->st));
+    const int32_t *b32 = s->d_in32.as<int32_t>();
+    SeedArgs a{};
+    a.base = b32;
+    a.slope = b32 + n;
+    a.sink = b32 + 2 * n;
+    a.pw = s->d_pw.as<int32_t>();
+    a.plane_off = s->d_off.as<int64_t>();
+    a.pw_off = s->d_off.as<int64_t>() + S.nprob;
+    a.lambdas = s->d_lam.as<int64_t>();
+    a.nprob = S.nprob;
+    a.nlam = S.nlam;
+    a.W = S.W;
+    a.H = S.H;
+    a.mid = (S.nlam - 1) / 2;   // LambdaSchedule.mid_index, parametric.py:65-68
+    a.swap_mode = S.swap_mode;
+    a.swap_cnt = s->d_swapcnt.as<int32_t>();
+    a.swapped = s->d_swapflag.as<int32_t>();
+    a.mask = s->d_mask.as<uint8_t>();
+    if (S.swap_mode == PMF_SWAP_AUTO)
+        LAUNCH(s, (k_swap_count<<<int(std::min<int64_t>(cdiv(S.nprob * n, 256), 16 * s->sms)), 256, 0, s->st>>>(a)));
+    LAUNCH(s, (k_swap_decide<<<int(cdiv(S.nprob, 128)), 128, 0, s->st>>>(a)));
+    LAUNCH(s, (k_build_seed<E><<<s->grid_full, NT, 0, s->st>>>(c, a)));
+    CK(cudaGetLastError());
+    s->stats.full_passes++;
+    return run_solve<E>(s, c, int32_t(s->lay.grids.size()));
+}
+
+int seed_stage(pmf_solver *s, int32_t nprob, int32_t W, int32_t H, const int64_t *const *ub,
+               const int64_t *const *us, const int64_t *const *sb, const int64_t *const *pw,
+               const int64_t *const *fg_idx, const int32_t *n_fg, const int64_t *const *bg_idx,
+               const int32_t *n_bg, int32_t nlam, const int64_t *lambdas, int32_t swap_mode) {
+    SeedStage &S = s->stage;
+    S.valid = false;
+    if (nprob < 1 || nlam < 1 || W < 1 || H < 1 || !ub || !us || !sb || !pw || !lambdas ||
+        swap_mode < 0 || swap_mode > 2)
+        return fail(PMF_ERR_ARG, "bad arguments");
+    const int64_t n = int64_t(W) * H;
+    for (int j = 0; j < nlam; j++)
+        if (lambdas[j] < 0 || (j && lambdas[j] <= lambdas[j - 1]))
+            return fail(PMF_ERR_ARG, "lambda values must be non-negative and strictly increasing");
+    const int64_t lam_max = lambdas[nlam - 1];
+    int rc;
+    // the previous run may still read the staging buffers
+    CK(cudaStreamSynchronize(s->st));
+    if ((rc = s->h_in32.ensure(size_t(nprob) * n * 3 * 4)) || (rc = s->h_mask.ensure(size_t(nprob) * n)))
+        return rc;
+    int32_t *hb = s->h_in32.as<int32_t>();
+    uint8_t *hm = s->h_mask.as<uint8_t>();
+    S.offs.assign(2 * size_t(nprob), 0);
+    std::unordered_map<const int64_t *, int64_t> pw_seen;
+    std::vector<const int64_t *> pw_list;
+    for (int p = 0; p < nprob; p++) {
+        auto it = pw_seen.find(pw[p]);
+        if (it == pw_seen.end()) {
+            int64_t o = int64_t(pw_list.size()) * 4 * n;
+            pw_seen[pw[p]] = o;
+            pw_list.push_back(pw[p]);
+            S.offs[nprob + p] = o;
+        } else {
+            S.offs[nprob + p] = it->second;
+        }
+    }
+    if ((rc = s->h_pw.ensure(pw_list.size() * size_t(4 * n) * 4))) return rc;
+    int32_t *hp = s->h_pw.as<int32_t>();
+    int64_t maxpair = 0;
+    for (size_t k = 0; k < pw_list.size(); k++) {
+        const int64_t *src = pw_list[k];
+        for (int64_t i = 0; i < 4 * n; i++)
+            if (src[i] < 0 || src[i] > CAP_MAX)
+                return fail(PMF_ERR_RANGE, "pairwise capacity outside [0, CAP_MAX]");
+        narrow(hp + k * 4 * n, src, 4 * n, 0, CAP_MAX);
+        maxpair = std::max(maxpair, max_pair(hp + k * 4 * n, W, H));
+    }
+    for (int p = 0; p < nprob; p++) {
+        S.offs[p] = 3 * int64_t(p) * n;   // base of problem p; slope +n, sink +2n
+        uint8_t *m = hm + p * n;
+        memset(m, 0, size_t(n));
+        for (int32_t i = 0; i < (n_fg ? n_fg[p] : 0); i++) {
+            int64_t q = fg_idx[p][i];
+            if (q < 0 || q >= n) return fail(PMF_ERR_ARG, "fg seed out of range");
+            m[q] = 1;
+        }
+        for (int32_t i = 0; i < (n_bg ? n_bg[p] : 0); i++) {
+            int64_t q = bg_idx[p][i];
+            if (q < 0 || q >= n) return fail(PMF_ERR_ARG, "bg seed out of range");
+            if (m[q] == 1) return fail(PMF_ERR_ARG, "a pixel cannot be both a foreground and background seed");
+            m[q] = 2;
+        }
+        // ranges the device relies on (instantiate's own checks are the caller's)
+        for (int64_t q = 0; q < n; q++) {
+            if (m[q] != 1) {
+                int64_t b = ub[p][q], sl = us[p][q];
+                if (b < 0 || sl < 0) return fail(PMF_ERR_RANGE, "problem %d: negative unary term", p);
+                if (b > CAP_MAX || (sl && lam_max > (CAP_MAX - b) / sl))
+                    return fail(PMF_ERR_RANGE, "problem %d: unary term exceeds CAP_MAX", p);
+            }
+            if (m[q] != 2 && (sb[p][q] < 0 || sb[p][q] > CAP_MAX))
+                return fail(PMF_ERR_RANGE, "problem %d: sink term outside [0, CAP_MAX]", p);
+        }
+        narrow(hb + 3 * p * n + 0 * n, ub[p], n, 0, CAP_MAX);
+        narrow(hb + 3 * p * n + 1 * n, us[p], n, 0, CAP_MAX);
+        narrow(hb + 3 * p * n + 2 * n, sb[p], n, 0, CAP_MAX);
+    }
+    S.u8 = maxpair <= 255;
+    if (!S.u8 && CAP_MAX + 8 * maxpair >= (int64_t(1) << 31) - 1)
+        return fail(PMF_ERR_RANGE, "pairwise capacities too large for the int32 device state");
+    S.lambdas.assign(lambdas, lambdas + nlam);
+    const size_t bytes_b = size_t(nprob) * n * 3 * 4, bytes_pw = pw_list.size() * size_t(4 * n) * 4;
+    if ((rc = s->d_in32.ensure(bytes_b)) || (rc = s->d_pw.ensure(bytes_pw)) ||
+        (rc = s->d_mask.ensure(size_t(nprob) * n)) || (rc = s->d_off.ensure(size_t(nprob) * 16)) ||
+        (rc = s->d_lam.ensure(size_t(nlam) * 8)) || (rc = s->d_swapcnt.ensure(size_t(nprob) * 8)))
+        return rc;
+    CK(cudaMemcpyAsync(s->d_in32.p, hb, bytes_b, cudaMemcpyHostToDevice, s->st));
+    CK(cudaMemcpyAsync(s->d_pw.p, hp, bytes_pw, cudaMemcpyHostToDevice, s->st));
+    CK(cudaMemcpyAsync(s->d_mask.p, hm, size_t(nprob) * n, cudaMemcpyHostToDevice, s->st));
+    CK(cudaMemcpyAsync(s->d_off.p, S.offs.data(), S.offs.size() * 8, cudaMemcpyHostToDevice, s->st));
+    CK(cudaMemcpyAsync(s->d_lam.p, S.lambdas.data(), size_t(nlam) * 8, cudaMemcpyHostToDevice, s->st));
+    s->lay.clear();
+    for (int p = 0; p < nprob; p++)
+        for (int j = 0; j < nlam; j++) s->lay.add(W, H, 0, 0, p, j);
+    S.nprob = nprob;
+    S.nlam = nlam;
+    S.W = W;
+    S.H = H;
+    S.swap_mode = swap_mode;
+    S.valid = true;
+    s->stats.h2d_bytes = int64_t(bytes_b + bytes_pw) + int64_t(nprob) * n + int64_t(nlam) * 8;
+    return 0;
+}
+
+int seed_fetch(pmf_solver *s, uint8_t *swapped_out, int64_t *flows_out, uint8_t *labels_out) {
+    const SeedStage &S = s->stage;
+    const Layout &L = s->lay;
+    const int64_t G = int64_t(L.grids.size());
+    const size_t lab_bytes = size_t((L.out_bytes + 7) / 8) * 8;
+    int rc;
+    if ((rc = s->h_out.ensure(lab_bytes + size_t(G) * 16 + size_t(S.nprob) * 4 + 64))) return rc;
+    uint8_t *ho = s->h_out.as<uint8_t>();
+    int64_t *hsnk = (int64_t *)(ho + lab_bytes);
+    int64_t *hdr = hsnk + G;
+    int32_t *hsw = (int32_t *)(hdr + G);
+    if (labels_out) CK(cudaMemcpyAsync(ho, s->d_out.p, L.out_bytes, cudaMemcpyDeviceToHost, s->st));
+    CK(cudaMemcpyAsync(hsnk, s->d_snk.p, G * 8, cudaMemcpyDeviceToHost, s->st));
+    CK(cudaMemcpyAsync(hdr, s->d_drain.p, G * 8, cudaMemcpyDeviceToHost, s->st));
+    CK(cudaMemcpyAsync(hsw, s->d_swapflag.p, size_t(S.nprob) * 4, cudaMemcpyDeviceToHost, s->st));
+    CK(cudaStreamSynchronize(s->st));
+    for (int64_t g = 0; g < G; g++) flows_out[g] = hsnk[g] - hdr[g];
+    if (swapped_out)
+        for (int p = 0; p < S.nprob; p++) swapped_out[p] = uint8_t(hsw[p] != 0);
+    if (labels_out) memcpy(labels_out, ho, size_t(L.out_bytes));
+    s->stats.d2h_bytes = (labels_out ? L.out_bytes : 0) + G * 16 + int64_t(S.nprob) * 4;
+    return 0;
+}
+
+// --------------------------------------------------------------------------
 // composites
 // --------------------------------------------------------------------------
 
 template <class E>
-int solve_composites_t(pmf_solver *s, const Layout &L, int ncomp, const int64_t *plane_off,
-                       int64_t total_px) {
-    int rc = grids_for_push<E>(s);
+int comp_run_t(pmf_solver *s, int ncomp, int64_t total_px) {
+    int rc = grids_for<E>(s);
     if (rc) return rc;
-    Ctx c;
-    if ((rc = setup_state(s, L, E::kBytes, &c))) return rc;
+    if ((rc = setup_state(s, E::kBytes))) return rc;
+    if ((rc = s->d_colswap.ensure(s->colswap.size() + 1))) return rc;
+    s->ctx.colswap = s->d_colswap.as<uint8_t>();
+    CK(cudaMemcpyAsync(s->d_colswap.p, s->colswap.data(), s->colswap.size(), cudaMemcpyHostToDevice, s->st));
+    const Ctx &c = s->ctx;
     s->tmark(C_H2D);
     if ((rc = s->d_in32.ensure(size_t(total_px) * 6 * 4)) || (rc = s->d_off.ensure(size_t(ncomp) * 8)))
         return rc;
-    c.colswap = s->d_colswap.as<uint8_t>();
     int32_t *din = s->d_in32.as<int32_t>();
     CK(cudaMemcpyAsync(din, s->h_in32.p, size_t(total_px) * 6 * 4, cudaMemcpyHostToDevice, s->st));
-    CK(cudaMemcpyAsync(s->d_off.p, plane_off, size_t(ncomp) * 8, cudaMemcpyHostToDevice, s->st));
+    CK(cudaMemcpyAsync(s->d_off.p, s->comp_off.data(), size_t(ncomp) * 8, cudaMemcpyHostToDevice, s->st));
     s->tmark(C_BUILD);
     CompArgs a{din, din + total_px, din + 2 * total_px, s->d_off.as<int64_t>()};
-    k_load_comp<E><<<s->grid_full, NT, 0, s->st>>>(c, a);
+    LAUNCH(s, (k_load_comp<E><<<s->grid_full, NT, 0, s->st>>>(c, a)));
     CK(cudaGetLastError());
     s->stats.full_passes++;
-    if ((rc = run_solve<E>(s, c, int32_t(L.grids.size())))) return rc;
-    return 0;
+    return run_solve<E>(s, c, int32_t(s->lay.grids.size()));
 }
 
 }  // namespace
@@ -399,19 +605,18 @@ int pmf_solver_create(int32_t device, pmf_solver **out) {
     CK(cudaGetDeviceCount(&ndev));
     if (device < 0 || device >= ndev) return fail(PMF_ERR_ARG, "device %d out of range (%d devices)", device, ndev);
     CK(cudaSetDevice(device));
+    cudaDeviceProp prop;
+    CK(cudaGetDeviceProperties(&prop, device));
+    if (prop.major < 10) return fail(PMF_ERR_CUDA, "device %d is sm_%d%d, not sm_100-class", device, prop.major, prop.minor);
     pmf_solver *s = new pmf_solver();
     s->device = device;
-    cudaDeviceProp prop;
-    if (cudaGetDeviceProperties(&prop, device) != cudaSuccess || prop.major < 10) {
-        delete s;
-        return fail(PMF_ERR_CUDA, "device %d is not sm_100-class", device);
-    }
     s->sms = prop.multiProcessorCount;
-    if (cudaStreamCreateWithFlags(&s->st, cudaStreamNonBlocking) != cudaSuccess) {
-        delete s;
-        return fail(PMF_ERR_CUDA, "cudaStreamCreate failed");
+    if (cudaStreamCreateWithFlags(&s->st, cudaStreamNonBlocking) != cudaSuccess ||
+        cudaEventCreate(&s->ev_run[0]) != cudaSuccess || cudaEventCreate(&s->ev_run[1]) != cudaSuccess ||
+        s->h_small.ensure(256)) {
+        pmf_solver_destroy(s);
+        return fail(PMF_ERR_CUDA, "stream/event/pinned allocation failed");
     }
-    if (s->h_small.ensure(256)) { delete s; return PMF_ERR_CUDA; }
     *out = s;
     return 0;
 }
@@ -419,9 +624,11 @@ int pmf_solver_create(int32_t device, pmf_solver **out) {
 int pmf_solver_destroy(pmf_solver *s) {
     if (!s) return 0;
     cudaSetDevice(s->device);
-    cudaStreamSynchronize(s->st);
+    if (s->st) cudaStreamSynchronize(s->st);
     for (auto e : s->ev_pool) cudaEventDestroy(e);
-    cudaStreamDestroy(s->st);
+    for (auto e : s->ev_run)
+        if (e) cudaEventDestroy(e);
+    if (s->st) cudaStreamDestroy(s->st);
     delete s;
     return 0;
 }
@@ -435,6 +642,12 @@ int pmf_solver_set(pmf_solver *s, const char *name, int64_t v) {
     else if (k == "timing") s->timing = v != 0;
     else if (k == "max_cycles" && v >= 1) s->max_cycles = v;
     else return fail(PMF_ERR_ARG, "unknown knob or bad value: %s=%lld", name, (long long)v);
+    return 0;
+}
+
+int pmf_solver_stream(const pmf_solver *s, void **stream_out) {
+    if (!s || !stream_out) return fail(PMF_ERR_ARG, "null argument");
+    *stream_out = (void *)s->st;
     return 0;
 }
 
@@ -453,33 +666,34 @@ int pmf_solve_composites(pmf_solver *s, int32_t ncomp, const int32_t *width, con
     if (!s || ncomp < 1 || !width || !height || !src || !snk || !nbr || !flow_out || !labels_out)
         return fail(PMF_ERR_ARG, "bad arguments");
     CK(cudaSetDevice(s->device));
-    begin_stats(s);
-    Layout L;
-    std::vector<uint8_t> colswap;
-    std::vector<int64_t> plane_off(ncomp);
+    CK(cudaStreamSynchronize(s->st));   // staging buffers are reused below
+    s->lay.clear();
+    s->colswap.clear();
+    s->comp_off.assign(size_t(ncomp), 0);
     int64_t total_px = 0;
     for (int c = 0; c < ncomp; c++) {
         if (width[c] < 1 || height[c] < 1) return fail(PMF_ERR_ARG, "composite %d: bad shape", c);
-        int32_t cs_off = int32_t(colswap.size());
-        colswap.resize(colswap.size() + width[c], 0);
+        int32_t cs_off = int32_t(s->colswap.size());
+        s->colswap.resize(s->colswap.size() + width[c], 0);
         int ns = nseg ? nseg[c] : 0;
         for (int k = 0; k < ns; k++) {
             int o = seg_off[c][k], w = seg_w[c][k];
-            if (o < 0 || w < 0 || o + w > width[c]) return fail(PMF_ERR_ARG, "composite %d: segment %d outside grid", c, k);
+            if (o < 0 || w < 0 || o + w > width[c])
+                return fail(PMF_ERR_ARG, "composite %d: segment %d outside the grid", c, k);
             if (seg_swapped[c][k])
-                for (int x = o; x < o + w; x++) colswap[cs_off + x] = 1;
+                for (int x = o; x < o + w; x++) s->colswap[cs_off + x] = 1;
         }
-        L.add(width[c], height[c], 1, cs_off, c, 0);
-        plane_off[c] = total_px;
+        s->lay.add(width[c], height[c], 1, cs_off, c, 0);
+        s->comp_off[c] = total_px;
         total_px += int64_t(width[c]) * height[c];
     }
-    // stage inputs as int32: src | snk | nbr (4 planes) per composite
+    // stage inputs as int32: src | snk | nbr (4 planes per composite)
     int rc = s->h_in32.ensure(size_t(total_px) * 6 * 4);
     if (rc) return rc;
     int32_t *hin = s->h_in32.as<int32_t>();
     int64_t maxpair = 0, maxexcess = 0;
     for (int c = 0; c < ncomp; c++) {
-        const int64_t n = int64_t(width[c]) * height[c], off = plane_off[c];
+        const int64_t n = int64_t(width[c]) * height[c], off = s->comp_off[c];
         for (const int64_t *pl : {src[c], snk[c]})
             for (int64_t i = 0; i < n; i++)
                 if (pl[i] < 0 || pl[i] > CAP_MAX)
@@ -489,10 +703,10 @@ int pmf_solve_composites(pmf_solver *s, int32_t ncomp, const int32_t *width, con
                 return fail(PMF_ERR_RANGE, "composite %d: capacity outside [0, CAP_MAX]", c);
         narrow(hin + off, src[c], n, 0, CAP_MAX);
         narrow(hin + total_px + off, snk[c], n, 0, CAP_MAX);
-        narrow(hin + 2 * total_px + 4 * off, nbr[c], 4 * n, 0, CAP_MAX);
-        maxpair = std::max(maxpair, max_pair(hin + 2 * total_px + 4 * off, width[c], height[c]));
-        // bound on any pixel's excess: its positive terminal plus all arc pairs
         const int32_t *nb = hin + 2 * total_px + 4 * off;
+        narrow(hin + 2 * total_px + 4 * off, nbr[c], 4 * n, 0, CAP_MAX);
+        maxpair = std::max(maxpair, max_pair(nb, width[c], height[c]));
+        // bound on any pixel's excess: its positive terminal plus all arc pairs
         for (int64_t p = 0; p < n; p++) {
             int64_t e = std::max<int64_t>(0, int64_t(hin[off + p]) - hin[total_px + off + p]);
             for (int d = 0; d < 4; d++) e += 2 * int64_t(nb[d * n + p]);
@@ -501,15 +715,12 @@ int pmf_solve_composites(pmf_solver *s, int32_t ncomp, const int32_t *width, con
     }
     if (maxexcess >= (int64_t(1) << 31) - 1)
         return fail(PMF_ERR_RANGE, "capacities too large for the int32 device state");
-    if (s->d_colswap.ensure(colswap.size() + 1)) return PMF_ERR_CUDA;
-    CK(cudaMemcpyAsync(s->d_colswap.p, colswap.data(), colswap.size(), cudaMemcpyHostToDevice, s->st));
-    if (s->d_swapflag.ensure(64)) return PMF_ERR_CUDA;
-    CK(cudaStreamSynchronize(s->st));
-    rc = maxpair <= 255 ? solve_composites_t<EdgeU8>(s, L, ncomp, plane_off.data(), total_px)
-                        : solve_composites_t<EdgeI32>(s, L, ncomp, plane_off.data(), total_px);
+    if ((rc = run_begin(s))) return rc;
+    rc = maxpair <= 255 ? comp_run_t<EdgeU8>(s, ncomp, total_px) : comp_run_t<EdgeI32>(s, ncomp, total_px);
     if (rc) return rc;
     // outputs
     s->tmark(C_D2H);
+    const Layout &L = s->lay;
     const int64_t G = int64_t(L.grids.size());
     const size_t lab_bytes = size_t((L.out_bytes + 7) / 8) * 8;
     if ((rc = s->h_out.ensure(lab_bytes + size_t(G) * 16))) return rc;
@@ -519,13 +730,43 @@ int pmf_solve_composites(pmf_solver *s, int32_t ncomp, const int32_t *width, con
     CK(cudaMemcpyAsync(ho, s->d_out.p, L.out_bytes, cudaMemcpyDeviceToHost, s->st));
     CK(cudaMemcpyAsync(hsnk, s->d_snk.p, G * 8, cudaMemcpyDeviceToHost, s->st));
     CK(cudaMemcpyAsync(hdr, s->d_drain.p, G * 8, cudaMemcpyDeviceToHost, s->st));
-    s->tmark(C_N);
-    if ((rc = finish_stats(s, L))) return rc;
+    if ((rc = run_end(s))) return rc;
     for (int c = 0; c < ncomp; c++) {
         flow_out[c] = hsnk[c] - hdr[c];
         memcpy(labels_out[c], ho + L.grids[c].out_off, size_t(width[c]) * height[c]);
     }
+    s->stats.h2d_bytes = total_px * 6 * 4;
+    s->stats.d2h_bytes = L.out_bytes + G * 16;
     return 0;
+}
+
+int pmf_seed_stage(pmf_solver *s, int32_t nprob, int32_t W, int32_t H, const int64_t *const *ub,
+                   const int64_t *const *us, const int64_t *const *sb, const int64_t *const *pw,
+                   const int64_t *const *fg_idx, const int32_t *n_fg,
+                   const int64_t *const *bg_idx, const int32_t *n_bg, int32_t nlam,
+                   const int64_t *lambdas, int32_t swap_mode) {
+    if (!s) return fail(PMF_ERR_ARG, "null solver");
+    CK(cudaSetDevice(s->device));
+    return seed_stage(s, nprob, W, H, ub, us, sb, pw, fg_idx, n_fg, bg_idx, n_bg, nlam, lambdas, swap_mode);
+}
+
+int pmf_seed_run(pmf_solver *s) {
+    if (!s || !s->stage.valid) return fail(PMF_ERR_ARG, "no staged seed batch");
+    CK(cudaSetDevice(s->device));
+    int64_t h2d = s->stats.h2d_bytes;
+    int rc = run_begin(s);
+    if (rc) return rc;
+    rc = s->stage.u8 ? seed_run_t<EdgeU8>(s) : seed_run_t<EdgeI32>(s);
+    if (rc) return rc;
+    rc = run_end(s);
+    s->stats.h2d_bytes = h2d;
+    return rc;
+}
+
+int pmf_seed_fetch(pmf_solver *s, uint8_t *swapped_out, int64_t *flows_out, uint8_t *labels_out) {
+    if (!s || !s->stage.valid || !flows_out) return fail(PMF_ERR_ARG, "bad arguments");
+    CK(cudaSetDevice(s->device));
+    return seed_fetch(s, swapped_out, flows_out, labels_out);
 }
 
 int pmf_solve_seed_batch(pmf_solver *s, int32_t nprob, int32_t W, int32_t H,
@@ -535,158 +776,12 @@ int pmf_solve_seed_batch(pmf_solver *s, int32_t nprob, int32_t W, int32_t H,
                          const int64_t *const *bg_idx, const int32_t *n_bg, int32_t nlam,
                          const int64_t *lambdas, int32_t swap_mode, uint8_t *swapped_out,
                          int64_t *flows_out, uint8_t *labels_out) {
-    if (!s || nprob < 1 || nlam < 1 || W < 1 || H < 1 || !ub || !us || !sb || !pw || !lambdas ||
-        !flows_out || !labels_out || swap_mode < 0 || swap_mode > 2)
-        return fail(PMF_ERR_ARG, "bad arguments");
-    CK(cudaSetDevice(s->device));
-    begin_stats(s);
-    const int64_t n = int64_t(W) * H;
-    for (int j = 0; j < nlam; j++)
-        if (lambdas[j] < 0 || (j && lambdas[j] <= lambdas[j - 1]))
-            return fail(PMF_ERR_ARG, "lambda values must be non-negative and strictly increasing");
-    const int64_t lam_max = lambdas[nlam - 1];
-    // ---- stage planes: base | slope | sink per problem, pairwise deduped
-    int rc;
-    if ((rc = s->h_in32.ensure(size_t(nprob) * n * 3 * 4)) || (rc = s->h_mask.ensure(size_t(nprob) * n)))
-        return rc;
-    int32_t *hb = s->h_in32.as<int32_t>();
-    uint8_t *hm = s->h_mask.as<uint8_t>();
-    std::vector<int64_t> plane_off(nprob), pw_off(nprob);
-    std::unordered_map<const int64_t *, int64_t> pw_seen;
-    std::vector<const int64_t *> pw_list;
-    for (int p = 0; p < nprob; p++) {
-        auto it = pw_seen.find(pw[p]);
-        if (it == pw_seen.end()) {
-            int64_t o = int64_t(pw_list.size()) * 4 * n;
-            pw_seen[pw[p]] = o;
-            pw_list.push_back(pw[p]);
-            pw_off[p] = o;
-        } else {
-            pw_off[p] = it->second;
-        }
-    }
-    if ((rc = s->h_pw.ensure(pw_list.size() * size_t(4 * n) * 4))) return rc;
-    int32_t *hp = s->h_pw.as<int32_t>();
-    int64_t maxpair = 0;
-    for (size_t k = 0; k < pw_list.size(); k++) {
-        const int64_t *src = pw_list[k];
-        for (int64_t i = 0; i < 4 * n; i++)
-            if (src[i] < 0 || src[i] > CAP_MAX)
-                return fail(PMF_ERR_RANGE, "pairwise capacity outside [0, CAP_MAX]");
-        narrow(hp + k * 4 * n, src, 4 * n, 0, CAP_MAX);
-        maxpair = std::max(maxpair, max_pair(hp + k * 4 * n, W, H));
-    }
-    for (int p = 0; p < nprob; p++) {
-        plane_off[p] = int64_t(p) * n;
-        uint8_t *m = hm + p * n;
-        memset(m, 0, size_t(n));
-        for (int32_t i = 0; i < (n_fg ? n_fg[p] : 0); i++) {
-            int64_t q = fg_idx[p][i];
-            if (q < 0 || q >= n) return fail(PMF_ERR_ARG, "fg seed out of range");
-            m[q] = 1;
-        }
-        for (int32_t i = 0; i < (n_bg ? n_bg[p] : 0); i++) {
-            int64_t q = bg_idx[p][i];
-            if (q < 0 || q >= n) return fail(PMF_ERR_ARG, "bg seed out of range");
-            if (m[q] == 1) return fail(PMF_ERR_ARG, "a pixel cannot be both a foreground and background seed");
-            m[q] = 2;
-        }
-        // ranges the device relies on (instantiate's checks are the caller's)
-        for (int64_t q = 0; q < n; q++) {
-            if (m[q] != 1) {
-                int64_t b = ub[p][q], sl = us[p][q];
-                if (b < 0 || sl < 0) return fail(PMF_ERR_RANGE, "problem %d: negative unary term", p);
-                if (sl && lam_max > (CAP_MAX - std::min(b, CAP_MAX)) / sl + 1)
-                    return fail(PMF_ERR_RANGE, "problem %d: unary term exceeds CAP_MAX", p);
-                if (b + lam_max * sl > CAP_MAX)
-                    return fail(PMF_ERR_RANGE, "problem %d: unary term exceeds CAP_MAX", p);
-            }
-            if (m[q] != 2 && (sb[p][q] < 0 || sb[p][q] > CAP_MAX))
-                return fail(PMF_ERR_RANGE, "problem %d: sink term outside [0, CAP_MAX]", p);
-        }
-        narrow(hb + 3 * p * n + 0 * n, ub[p], n, 0, CAP_MAX);
-        narrow(hb + 3 * p * n + 1 * n, us[p], n, 0, CAP_MAX);
-        narrow(hb + 3 * p * n + 2 * n, sb[p], n, 0, CAP_MAX);
-    }
-    // base/slope/sink are staged per problem as [p][3][n]: the kernels read
-    // base[plane_off[p] + q], slope = base + n, sink = base + 2n
-    bool u8 = maxpair <= 255;
-    if (!u8 && CAP_MAX + 8 * maxpair >= (int64_t(1) << 31) - 1)
-        return fail(PMF_ERR_RANGE, "pairwise capacities too large for the int32 device state");
-    // ---- layout: one grid per (problem, lambda), problem-major
-    Layout L;
-    for (int p = 0; p < nprob; p++)
-        for (int j = 0; j < nlam; j++) L.add(W, H, 0, 0, p, j);
-    rc = u8 ? grids_for_push<EdgeU8>(s) : grids_for_push<EdgeI32>(s);
+    if (!flows_out || !labels_out) return fail(PMF_ERR_ARG, "bad arguments");
+    int rc = pmf_seed_stage(s, nprob, W, H, ub, us, sb, pw, fg_idx, n_fg, bg_idx, n_bg, nlam, lambdas,
+                            swap_mode);
     if (rc) return rc;
-    if ((rc = s->d_swapflag.ensure(size_t(nprob) * 4)) || (rc = s->d_colswap.ensure(64))) return rc;
-    Ctx c;
-    if ((rc = setup_state(s, L, u8 ? 4 : 16, &c))) return rc;
-    s->tmark(C_H2D);
-    const size_t bytes_b = size_t(nprob) * n * 3 * 4, bytes_pw = pw_list.size() * size_t(4 * n) * 4;
-    if ((rc = s->d_in32.ensure(bytes_b)) || (rc = s->d_pw.ensure(bytes_pw)) ||
-        (rc = s->d_mask.ensure(size_t(nprob) * n)) || (rc = s->d_off.ensure(size_t(nprob) * 16)) ||
-        (rc = s->d_lam.ensure(size_t(nlam) * 8)) || (rc = s->d_swapcnt.ensure(size_t(nprob) * 8)))
-        return rc;
-    CK(cudaMemcpyAsync(s->d_in32.p, hb, bytes_b, cudaMemcpyHostToDevice, s->st));
-    CK(cudaMemcpyAsync(s->d_pw.p, hp, bytes_pw, cudaMemcpyHostToDevice, s->st));
-    CK(cudaMemcpyAsync(s->d_mask.p, hm, size_t(nprob) * n, cudaMemcpyHostToDevice, s->st));
-    // offsets: base plane of problem p at 3*p*n; slope/sink follow at +n/+2n
-    std::vector<int64_t> offs(2 * size_t(nprob));
-    for (int p = 0; p < nprob; p++) { offs[p] = 3 * int64_t(p) * n; offs[nprob + p] = pw_off[p]; }
-    CK(cudaMemcpyAsync(s->d_off.p, offs.data(), offs.size() * 8, cudaMemcpyHostToDevice, s->st));
-    CK(cudaMemcpyAsync(s->d_lam.p, lambdas, size_t(nlam) * 8, cudaMemcpyHostToDevice, s->st));
-    CK(cudaMemsetAsync(s->d_swapcnt.p, 0, size_t(nprob) * 8, s->st));
-    CK(cudaStreamSynchronize(s->st));   // offs is a stack vector
-    s->tmark(C_BUILD);
-    const int32_t *b32 = s->d_in32.as<int32_t>();
-    SeedArgs a{};
-    a.base = b32;
-    a.slope = b32 + n;
-    a.sink = b32 + 2 * n;
-    a.pw = s->d_pw.as<int32_t>();
-    a.plane_off = s->d_off.as<int64_t>();
-    a.pw_off = s->d_off.as<int64_t>() + nprob;
-    a.lambdas = s->d_lam.as<int64_t>();
-    a.nprob = nprob;
-    a.nlam = nlam;
-    a.W = W;
-    a.H = H;
-    a.mid = (nlam - 1) / 2;   // LambdaSchedule.mid_index, parametric.py:65-68
-    a.swap_mode = swap_mode;
-    a.swap_cnt = s->d_swapcnt.as<int32_t>();
-    a.swapped = s->d_swapflag.as<int32_t>();
-    a.mask = s->d_mask.as<uint8_t>();
-    if (swap_mode == PMF_SWAP_AUTO)
-        k_swap_count<<<int(std::min<int64_t>(cdiv(nprob * n, 256), 16 * s->sms)), 256, 0, s->st>>>(a);
-    k_swap_decide<<<int(cdiv(nprob, 128)), 128, 0, s->st>>>(a);
-    if (u8) k_build_seed<EdgeU8><<<s->grid_full, NT, 0, s->st>>>(c, a);
-    else k_build_seed<EdgeI32><<<s->grid_full, NT, 0, s->st>>>(c, a);
-    CK(cudaGetLastError());
-    s->stats.full_passes++;
-    rc = u8 ? run_solve<EdgeU8>(s, c, int32_t(L.grids.size()))
-            : run_solve<EdgeI32>(s, c, int32_t(L.grids.size()));
-    if (rc) return rc;
-    // ---- outputs: labels (problem-major, lambda-minor), flows, swap flags
-    s->tmark(C_D2H);
-    const int64_t G = int64_t(L.grids.size());
-    const size_t lab_bytes = size_t((L.out_bytes + 7) / 8) * 8;
-    if ((rc = s->h_out.ensure(lab_bytes + size_t(G) * 16 + size_t(nprob) * 4 + 64))) return rc;
-    uint8_t *ho = s->h_out.as<uint8_t>();
-    int64_t *hsnk = (int64_t *)(ho + lab_bytes);
-    int64_t *hdr = hsnk + G;
-    int32_t *hsw = (int32_t *)(hdr + G);
-    CK(cudaMemcpyAsync(ho, s->d_out.p, L.out_bytes, cudaMemcpyDeviceToHost, s->st));
-    CK(cudaMemcpyAsync(hsnk, s->d_snk.p, G * 8, cudaMemcpyDeviceToHost, s->st));
-    CK(cudaMemcpyAsync(hdr, s->d_drain.p, G * 8, cudaMemcpyDeviceToHost, s->st));
-    CK(cudaMemcpyAsync(hsw, s->d_swapflag.p, size_t(nprob) * 4, cudaMemcpyDeviceToHost, s->st));
-    s->tmark(C_N);
-    if ((rc = finish_stats(s, L))) return rc;
-    for (int64_t g = 0; g < G; g++) flows_out[g] = hsnk[g] - hdr[g];
-    if (swapped_out)
-        for (int p = 0; p < nprob; p++) swapped_out[p] = uint8_t(hsw[p] != 0);
-    memcpy(labels_out, ho, size_t(L.out_bytes));
-    return 0;
+    if ((rc = pmf_seed_run(s))) return rc;
+    return pmf_seed_fetch(s, swapped_out, flows_out, labels_out);
 }
 
 }  // extern "C"
