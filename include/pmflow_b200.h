@@ -157,6 +157,12 @@ int pmf_seed_stage(pmf_solver *s, int32_t nprob, int32_t width, int32_t height,
 int pmf_seed_run(pmf_solver *s);
 int pmf_seed_fetch(pmf_solver *s, uint8_t *swapped_out, int64_t *flows_out, uint8_t *labels_out);
 
+/* Diagnostics: copy the tile-major device state of the last run (w, h,
+ * residual words, source-side flags; any pointer may be NULL) and the tile
+ * count.  Buffers hold ntiles*1024 entries (r: edge_bytes each). */
+int pmf_debug_state(pmf_solver *s, int32_t *w, int32_t *h, void *r, uint8_t *lab,
+                    int64_t *ntiles);
+
 #ifdef __cplusplus
 }
 #endif

@@ -23,7 +23,7 @@ SWAP_MODES = {"auto": 0, "on": 1, "off": 2}
 
 EXPORTS = ("pmf_solver_create", "pmf_solver_destroy", "pmf_solver_set", "pmf_last_error",
            "pmf_solver_stats", "pmf_solver_stream", "pmf_solve_composites", "pmf_solve_seed_batch",
-           "pmf_seed_stage", "pmf_seed_run", "pmf_seed_fetch")
+           "pmf_seed_stage", "pmf_seed_run", "pmf_seed_fetch", "pmf_debug_state")
 
 
 class NativeUnavailable(RuntimeError):
@@ -77,6 +77,7 @@ def load_library(path: str = LIB_PATH):
         lib.pmf_seed_run.argtypes = [vp]
         lib.pmf_seed_fetch.argtypes = [vp, P(u8), P(i64), P(u8)]
         lib.pmf_solver_stream.argtypes = [vp, P(vp)]
+        lib.pmf_debug_state.argtypes = [vp, vp, vp, vp, vp, P(i64)]
         for name in EXPORTS:
             if name != "pmf_last_error":
                 getattr(lib, name).restype = ctypes.c_int
@@ -169,6 +170,22 @@ class Solver:
         if rc:
             _raise_for(rc)
         return [(int(f), l) for f, l in zip(flows, labs)]
+
+    def debug_state(self):
+        """(w, h, r, lab) tile-major arrays of the last run (diagnostics)."""
+        nt = ctypes.c_int64()
+        self._lib.pmf_debug_state(self._h, None, None, None, None, ctypes.byref(nt))
+        P_ = nt.value * 1024
+        eb = self.stats()["edge_bytes"]
+        w = np.empty(P_, np.int32)
+        h = np.empty(P_, np.int32)
+        r = np.empty(P_, np.uint32) if eb == 4 else np.empty((P_, 4), np.int32)
+        lab = np.empty(P_, np.uint8)
+        rc = self._lib.pmf_debug_state(self._h, w.ctypes.data, h.ctypes.data, r.ctypes.data,
+                                       lab.ctypes.data, ctypes.byref(nt))
+        if rc:
+            _raise_for(rc)
+        return w, h, r, lab
 
     def stream_handle(self) -> int:
         """The solver's cudaStream_t as an integer (torch.cuda.ExternalStream)."""

@@ -16,6 +16,7 @@
 
 #include "../../include/pmflow_b200.h"
 #include "kernels.cuh"
+#include "tile.cuh"
 
 using namespace pmf;
 
@@ -130,14 +131,17 @@ struct pmf_solver {
     int grid_push = 0, grid_bfs = 0, grid_full = 0;
     // knobs
     int push_iters = 32;
-    int push_sweeps = 16;
+    int push_sweeps = 64;
+    int relabel_every = 16;
+    int persistent = 1;
+    int push_budget = 8;      // persistent push phase: pops <= budget * seeded tiles
     int bfs_chunk = 8;
     int timing = 0;
     int64_t max_cycles = 50000;
     // device workspace
     DevBuf d_w, d_h, d_r, d_lab, d_tile_grid, d_grids, d_live, d_act, d_list, d_inq, d_cnt,
         d_snk, d_drain, d_err, d_stat, d_colswap, d_out, d_in32, d_pw, d_mask, d_off, d_lam,
-        d_swapcnt, d_swapflag;
+        d_swapcnt, d_swapflag, d_ring, d_qstate, d_qctr;
     HostBuf h_in32, h_pw, h_mask, h_out, h_small;
     Layout lay;
     std::vector<int32_t> ones;
@@ -193,7 +197,8 @@ int setup_state(pmf_solver *s, int edge_bytes) {
         (rc = s->d_cnt.ensure(64)) || (rc = s->d_snk.ensure(G * 8)) || (rc = s->d_drain.ensure(G * 8)) ||
         (rc = s->d_err.ensure(64)) || (rc = s->d_stat.ensure(ST_NSTAT * 8)) ||
         (rc = s->d_out.ensure(std::max<int64_t>(L.out_bytes, 1))) || (rc = s->d_colswap.ensure(64)) ||
-        (rc = s->d_swapflag.ensure(64)))
+        (rc = s->d_swapflag.ensure(64)) || (rc = s->d_ring.ensure(T * 4)) ||
+        (rc = s->d_qstate.ensure(T * 4)) || (rc = s->d_qctr.ensure(64)))
         return rc;
     s->edge_bytes = edge_bytes;
     // host sources live in the solver (s->lay, s->ones) until the next setup
@@ -229,12 +234,14 @@ int setup_state(pmf_solver *s, int edge_bytes) {
     x.swapflag = s->d_swapflag.as<int32_t>();
     x.out = s->d_out.as<uint8_t>();
     x.ntiles = T;
-    return 0;
-}
-
-int begin_phase(pmf_solver *s, const Ctx &c) {
-    CK(cudaMemsetAsync(c.cnt, 0, 3 * 4, s->st));
-    CK(cudaMemsetAsync(c.inq0, 0, size_t(2 * c.ntiles) * 4, s->st));
+    x.ring = s->d_ring.as<int32_t>();
+    x.qstate = s->d_qstate.as<int32_t>();
+    x.qctr = s->d_qctr.as<unsigned int>();
+    x.qcap = int32_t(T);
+    x.persistent = s->persistent;
+    // BFS phases converge on their own (values only decrease); the cap only
+    // guards against a runaway launch
+    x.budget = unsigned(std::min<int64_t>(int64_t(4096) * T + 4096, int64_t(0xffffffffu) - 1));
     return 0;
 }
 
@@ -246,13 +253,43 @@ int read_count(pmf_solver *s, const Ctx &c, int idx, int32_t *out) {
     return 0;
 }
 
+int begin_phase(pmf_solver *s, const Ctx &c) {
+    if (c.persistent) {
+        CK(cudaMemsetAsync(c.qctr, 0, 16, s->st));
+        CK(cudaMemsetAsync(c.qstate, 0, size_t(c.ntiles) * 4, s->st));
+        CK(cudaMemsetAsync(c.ring, 0xff, size_t(c.ntiles) * 4, s->st));
+    } else {
+        CK(cudaMemsetAsync(c.cnt, 0, 3 * 4, s->st));
+        CK(cudaMemsetAsync(c.inq0, 0, size_t(2 * c.ntiles) * 4, s->st));
+    }
+    return 0;
+}
+
+// number of tiles the seed kernel put in the first worklist / the queue
+int read_seeded(pmf_solver *s, const Ctx &c, int32_t *out) {
+    if (!c.persistent) return read_count(s, c, 0, out);
+    unsigned *hp = s->h_small.as<unsigned>();
+    CK(cudaMemcpyAsync(hp, c.qctr + QC_PENDING, 4, cudaMemcpyDeviceToHost, s->st));
+    CK(cudaStreamSynchronize(s->st));
+    *out = int32_t(*hp);
+    return 0;
+}
+
+
 template <class E>
 int run_bfs(pmf_solver *s, const Ctx &c, bool sink, int64_t *sweeps) {
+    if (c.persistent) {   // one launch; the queue drains on the device
+        if (sink) LAUNCH(s, (k_bfs_sink<E><<<s->grid_bfs, NTT, 0, s->st>>>(c, -1)));
+        else LAUNCH(s, (k_bfs_src<E><<<s->grid_bfs, NTT, 0, s->st>>>(c, -1)));
+        CK(cudaGetLastError());
+        *sweeps += 1;
+        return 0;
+    }
     int k = 0;
     for (;;) {
         for (int j = 0; j < s->bfs_chunk; j++, k++) {
-            if (sink) LAUNCH(s, (k_bfs_sink<E><<<s->grid_bfs, NT, 0, s->st>>>(c, k)));
-            else LAUNCH(s, (k_bfs_src<E><<<s->grid_bfs, NT, 0, s->st>>>(c, k)));
+            if (sink) LAUNCH(s, (k_bfs_sink<E><<<s->grid_bfs, NTT, 0, s->st>>>(c, k)));
+            else LAUNCH(s, (k_bfs_src<E><<<s->grid_bfs, NTT, 0, s->st>>>(c, k)));
         }
         CK(cudaGetLastError());
         *sweeps += s->bfs_chunk;
@@ -285,13 +322,34 @@ int run_solve(pmf_solver *s, const Ctx &c, int32_t ngrids) {
         CK(cudaGetLastError());
         s->stats.full_passes++;
         int32_t nact = 0;
-        if ((rc = read_count(s, c, 0, &nact))) return rc;
+        if ((rc = read_seeded(s, c, &nact))) return rc;
         if (nact == 0) break;
+        if (c.persistent) {
+            s->tmark(C_PUSH);
+            Ctx cp = c;
+            // a bounded pop budget per phase always applies: the next global
+            // relabel resets stale heights (and no launch can spin forever)
+            uint64_t cap = uint64_t(64) * uint64_t(c.ntiles) + 1024;
+            uint64_t want = s->push_budget ? uint64_t(s->push_budget) * uint64_t(nact) + 64 : cap;
+            cp.budget = unsigned(std::min(want, cap));
+            LAUNCH(s, (k_push<E><<<s->grid_push, NTT, 0, s->st>>>(cp, -1, s->push_iters, s->relabel_every)));
+            CK(cudaGetLastError());
+            s->stats.push_sweeps += 1;
+            continue;
+        }
+        // discharge until no tile is listed (or the per-cycle sweep budget
+        // is spent), checking the list length every bfs_chunk launches
         s->tmark(C_PUSH);
-        for (int k = 0; k < s->push_sweeps; k++)
-            LAUNCH(s, (k_push<E><<<s->grid_push, NT, 0, s->st>>>(c, k, s->push_iters)));
-        CK(cudaGetLastError());
-        s->stats.push_sweeps += s->push_sweeps;
+        for (int k = 0; k < s->push_sweeps;) {
+            int chunk = std::min(s->bfs_chunk, s->push_sweeps - k);
+            for (int j = 0; j < chunk; j++, k++)
+                LAUNCH(s, (k_push<E><<<s->grid_push, NTT, 0, s->st>>>(c, k, s->push_iters, s->relabel_every)));
+            CK(cudaGetLastError());
+            s->stats.push_sweeps += chunk;
+            int32_t left = 0;
+            if ((rc = read_count(s, c, k % 3, &left))) return rc;
+            if (left == 0) break;
+        }
     }
     s->stats.cycles = cycle + 1;
     // labels: source-side closure, then emit
@@ -383,9 +441,9 @@ int64_t max_pair(const int32_t *nb, int W, int H) {
 template <class E>
 int grids_for(pmf_solver *s) {
     int occ = 0;
-    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_push<E>, NT, 0));
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_push<E>, NTT, 0));
     s->grid_push = std::max(1, occ) * s->sms;
-    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_bfs_sink<E>, NT, 0));
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_bfs_sink<E>, NTT, 0));
     s->grid_bfs = std::max(1, occ) * s->sms;
     s->grid_full = 8 * s->sms;
     return 0;
@@ -639,6 +697,9 @@ int pmf_solver_set(pmf_solver *s, const char *name, int64_t v) {
     if (k == "push_iters" && v >= 1 && v <= 100000) s->push_iters = int(v);
     else if (k == "push_sweeps" && v >= 1 && v <= 100000) s->push_sweeps = int(v);
     else if (k == "bfs_chunk" && v >= 1 && v <= 100000) s->bfs_chunk = int(v);
+    else if (k == "relabel_every" && v >= 0 && v <= 100000) s->relabel_every = int(v);
+    else if (k == "persistent") s->persistent = v != 0;
+    else if (k == "push_budget" && v >= 0) s->push_budget = int(v);
     else if (k == "timing") s->timing = v != 0;
     else if (k == "max_cycles" && v >= 1) s->max_cycles = v;
     else return fail(PMF_ERR_ARG, "unknown knob or bad value: %s=%lld", name, (long long)v);
@@ -737,6 +798,19 @@ int pmf_solve_composites(pmf_solver *s, int32_t ncomp, const int32_t *width, con
     }
     s->stats.h2d_bytes = total_px * 6 * 4;
     s->stats.d2h_bytes = L.out_bytes + G * 16;
+    return 0;
+}
+
+int pmf_debug_state(pmf_solver *s, int32_t *w, int32_t *h, void *r, uint8_t *lab, int64_t *ntiles) {
+    if (!s) return fail(PMF_ERR_ARG, "null solver");
+    CK(cudaSetDevice(s->device));
+    const int64_t P = s->lay.ntiles * TPIX;
+    if (ntiles) *ntiles = s->lay.ntiles;
+    if (w) CK(cudaMemcpyAsync(w, s->d_w.p, P * 4, cudaMemcpyDeviceToHost, s->st));
+    if (h) CK(cudaMemcpyAsync(h, s->d_h.p, P * 4, cudaMemcpyDeviceToHost, s->st));
+    if (r) CK(cudaMemcpyAsync(r, s->d_r.p, P * s->edge_bytes, cudaMemcpyDeviceToHost, s->st));
+    if (lab) CK(cudaMemcpyAsync(lab, s->d_lab.p, P, cudaMemcpyDeviceToHost, s->st));
+    CK(cudaStreamSynchronize(s->st));
     return 0;
 }
 

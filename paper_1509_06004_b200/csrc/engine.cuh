@@ -59,7 +59,94 @@ struct Ctx {
     const int32_t *swapflag;// batch: per-problem swap decision (device-made)
     uint8_t *out;           // label output bytes
     int64_t ntiles;
+    // persistent work queue: ring of tile ids (-1 =
+    // empty slot), per-tile state, counters {head, tail, pending, pops}
+    int32_t *ring;
+    int32_t *qstate;
+    unsigned int *qctr;
+    int32_t qcap;
+    int32_t persistent;     // seed kernels feed the queue (1) or list 0 (0)
+    unsigned int budget;    // max tile pops of a persistent phase (0 = none)
 };
+
+enum { Q_IDLE = 0, Q_QUEUED = 1, Q_RUNNING = 2, Q_DIRTY = 3 };
+enum { QC_HEAD = 0, QC_TAIL = 1, QC_PENDING = 2, QC_POPS = 3 };
+
+__device__ __forceinline__ unsigned ld_volatile(const unsigned *p) {
+    return *(const volatile unsigned *)p;
+}
+
+// Append t (whose state the caller just moved to QUEUED) to the ring.
+__device__ __forceinline__ void q_push(const Ctx &c, int32_t t) {
+    unsigned idx = atomicAdd(&c.qctr[QC_TAIL], 1u);
+    int32_t *slot = &c.ring[idx % unsigned(c.qcap)];
+    while (atomicCAS(slot, -1, t) != -1) __nanosleep(64);
+}
+
+// Pop a tile id, or -1 if the ring is empty right now.
+__device__ __forceinline__ int32_t q_pop(const Ctx &c) {
+    for (;;) {
+        unsigned hd = ld_volatile(&c.qctr[QC_HEAD]);
+        if (hd >= ld_volatile(&c.qctr[QC_TAIL])) return -1;
+        if (atomicCAS(&c.qctr[QC_HEAD], hd, hd + 1) == hd) {
+            int32_t *slot = &c.ring[hd % unsigned(c.qcap)];
+            int32_t t;
+            while ((t = atomicExch(slot, -1)) == -1) __nanosleep(32);
+            return t;
+        }
+    }
+}
+
+// Ask for tile t to be (re)processed: idle -> queued, running -> dirty.
+__device__ __forceinline__ void q_request(const Ctx &c, int32_t t) {
+    for (;;) {
+        int s = *(volatile int32_t *)&c.qstate[t];
+        if (s == Q_QUEUED || s == Q_DIRTY) return;
+        if (s == Q_IDLE) {
+            if (atomicCAS(&c.qstate[t], Q_IDLE, Q_QUEUED) == Q_IDLE) {
+                atomicAdd(&c.qctr[QC_PENDING], 1u);
+                q_push(c, t);
+                return;
+            }
+        } else if (atomicCAS(&c.qstate[t], Q_RUNNING, Q_DIRTY) == Q_RUNNING) {
+            return;
+        }
+    }
+}
+
+// The running tile t is done; requeue it if it still has work or was
+// dirtied meanwhile, else retire it (pending only drops on retirement, so
+// pending == 0 means nothing is queued or running anywhere).
+__device__ __forceinline__ void q_finish(const Ctx &c, int32_t t, bool again) {
+    for (;;) {
+        if (again) {
+            atomicExch(&c.qstate[t], Q_QUEUED);
+            q_push(c, t);
+            return;
+        }
+        if (atomicCAS(&c.qstate[t], Q_RUNNING, Q_IDLE) == Q_RUNNING) {
+            atomicSub(&c.qctr[QC_PENDING], 1u);
+            return;
+        }
+        again = true;   // dirtied while running
+    }
+}
+
+// Thread 0 of a persistent CTA: next tile to process, or -1 when the phase
+// is over (queue drained with nothing running, or pop budget spent).
+__device__ __forceinline__ int32_t q_next(const Ctx &c) {
+    for (;;) {
+        if (c.budget && ld_volatile(&c.qctr[QC_POPS]) >= c.budget) return -1;
+        int32_t t = q_pop(c);
+        if (t >= 0) {
+            atomicAdd(&c.qctr[QC_POPS], 1u);
+            atomicExch(&c.qstate[t], Q_RUNNING);
+            return t;
+        }
+        if (ld_volatile(&c.qctr[QC_PENDING]) == 0) return -1;
+        __nanosleep(256);
+    }
+}
 
 // A batch grid embedded swapped reports its sink side (what split() turns
 // into the original graph's minimal source side); everything else needs the
@@ -77,6 +164,13 @@ __device__ __forceinline__ void enqueue(const Ctx &c, int k, int32_t t) {
         int idx = atomicAdd(&c.cnt[k % 3], 1);
         list_of(c, k)[idx] = t;
     }
+}
+
+// Seed kernels: put t in the first worklist of the phase (sweep mode) or
+// in the persistent queue.
+__device__ __forceinline__ void seed_tile(const Ctx &c, int32_t t) {
+    if (c.persistent) q_request(c, t);
+    else enqueue(c, 0, t);
 }
 
 struct TileGeo {
@@ -129,7 +223,7 @@ __device__ __forceinline__ bool on_border(int i) {
 struct EdgeU8 {
     using Word = uint32_t;
     static constexpr int kBytes = 4;
-    __device__ static Word load(const void *R, int64_t p) { return ((const uint32_t *)R)[p]; }
+    __device__ static Word load(const void *R, int64_t p) { return __ldcg(((const uint32_t *)R) + p); }
     __device__ static int lane(Word w, int d) { return int((w >> (8 * d)) & 0xffu); }
     __device__ static Word pack(int a, int b, int c, int d) {
         return uint32_t(a) | (uint32_t(b) << 8) | (uint32_t(c) << 16) | (uint32_t(d) << 24);
@@ -147,7 +241,7 @@ struct EdgeU8 {
 struct EdgeI32 {
     using Word = int4;
     static constexpr int kBytes = 16;
-    __device__ static Word load(const void *R, int64_t p) { return ((const int4 *)R)[p]; }
+    __device__ static Word load(const void *R, int64_t p) { return __ldcg(((const int4 *)R) + p); }
     __device__ static int lane(Word w, int d) {
         return d == 0 ? w.x : d == 1 ? w.y : d == 2 ? w.z : w.w;
     }

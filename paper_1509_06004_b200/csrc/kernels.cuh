@@ -164,86 +164,47 @@ __global__ void __launch_bounds__(NT) k_load_comp(Ctx c, CompArgs a) {
 // fixpoint, tiles re-listed while their halo keeps changing.
 // ---------------------------------------------------------------------------
 
+// Seed a BFS phase: list tile t if it holds a seed pixel, and every
+// neighbour facing a seed on t's border -- a seed never "changes", so the
+// relaxation of t alone would never hand it across the tile boundary.
+// `seeds` is this thread's bit set of seed pixels among its PPT pixels.
+__device__ __forceinline__ void seed_with_halo(const Ctx &c, int64_t t, unsigned seeds) {
+    __shared__ int s_sides;
+    if (threadIdx.x == 0) s_sides = 0;
+    __syncthreads();
+    int any = 0, sides = 0;
+    for (int j = 0; j < PPT; j++) {
+        if (!((seeds >> j) & 1)) continue;
+        int i = threadIdx.x + j * NT, lx = i & (TW - 1), ly = i / TW;
+        any = 1;
+        sides |= (lx == 0 ? 1 << DL : 0) | (lx == TW - 1 ? 1 << DR : 0) |
+                 (ly == 0 ? 1 << DU : 0) | (ly == TH - 1 ? 1 << DD : 0);
+    }
+    if (sides) atomicOr(&s_sides, sides);
+    any = __syncthreads_or(any);
+    if (threadIdx.x == 0 && any) {
+        TileGeo g = tile_geo(c, int32_t(t));
+        seed_tile(c, int32_t(t));
+        for (int s = 0; s < 4; s++)
+            if (((s_sides >> s) & 1) && g.nb[s] >= 0) seed_tile(c, g.nb[s]);
+    }
+    __syncthreads();
+}
+
 // h = 1 on pixels with sink residual (w < 0), HINF elsewhere; lists every
-// tile holding such a pixel.  Tiles of finished grids are left untouched.
+// tile holding such a pixel (and its neighbours facing one).  Tiles of
+// finished grids are left untouched.
 __global__ void __launch_bounds__(NT) k_gr_init(Ctx c) {
     for (int64_t t = blockIdx.x; t < c.ntiles; t += gridDim.x) {
         if (!c.live[c.tile_grid[t]]) continue;
-        int any = 0;
+        unsigned seeds = 0;
         for (int j = 0; j < PPT; j++) {
             int64_t p = t * TPIX + threadIdx.x + j * NT;
             int32_t wv = c.w[p];
             c.h[p] = wv < 0 ? 1 : HINF;
-            any |= wv < 0;
+            seeds |= unsigned(wv < 0) << j;
         }
-        if (__syncthreads_or(any) && threadIdx.x == 0) enqueue(c, 0, int32_t(t));
-    }
-}
-
-template <class E>
-__global__ void __launch_bounds__(NT) k_bfs_sink(Ctx c, int k) {
-    __shared__ int32_t sd[TPIX];
-    __shared__ uint8_t sm[TPIX];
-    __shared__ int32_t hd[4][TW];
-    __shared__ int s_side[4];
-    const int32_t n = c.cnt[k % 3];
-    const int32_t *lst = list_of(c, k);
-    if (blockIdx.x == 0 && threadIdx.x == 0) {
-        c.cnt[(k + 2) % 3] = 0;
-        atomicAdd(&c.stat[ST_BFS], (unsigned long long)n);
-    }
-    for (int li = blockIdx.x; li < n; li += gridDim.x) {
-        const int32_t t = lst[li];
-        TileGeo g = tile_geo(c, t);
-        const int64_t base = int64_t(t) * TPIX;
-        int32_t h0[PPT];
-        for (int j = 0; j < PPT; j++) {
-            int i = threadIdx.x + j * NT;
-            h0[j] = c.h[base + i];
-            sd[i] = h0[j];
-            typename E::Word wd = E::load(c.r, base + i);
-            sm[i] = uint8_t((E::lane(wd, 0) > 0) | ((E::lane(wd, 1) > 0) << 1) |
-                            ((E::lane(wd, 2) > 0) << 2) | ((E::lane(wd, 3) > 0) << 3));
-        }
-        if (threadIdx.x < 4 * TW) {
-            int s = threadIdx.x / TW, j = threadIdx.x % TW;
-            hd[s][j] = g.nb[s] >= 0 ? c.h[int64_t(g.nb[s]) * TPIX + halo_index(s, j)] : HINF;
-            if (j == 0) s_side[s] = 0;
-        }
-        if (threadIdx.x == 0) inq_of(c, k)[t] = 0;
-        __syncthreads();
-        for (;;) {
-            int changed = 0;
-            for (int j = 0; j < PPT; j++) {
-                int i = threadIdx.x + j * NT;
-                int32_t v = sd[i];
-                int mk = sm[i];
-                if (v <= 1 || !mk) continue;
-                int lx = i & (TW - 1), ly = i / TW;
-                int32_t m = HINF;
-                if (mk & 1) m = min(m, lx ? sd[i - 1] : hd[DL][ly]);
-                if (mk & 2) m = min(m, lx < TW - 1 ? sd[i + 1] : hd[DR][ly]);
-                if (mk & 4) m = min(m, ly ? sd[i - TW] : hd[DU][lx]);
-                if (mk & 8) m = min(m, ly < TH - 1 ? sd[i + TW] : hd[DD][lx]);
-                if (m + 1 < v) { sd[i] = m + 1; changed = 1; }
-            }
-            if (!__syncthreads_or(changed)) break;
-        }
-        for (int j = 0; j < PPT; j++) {
-            int i = threadIdx.x + j * NT;
-            if (sd[i] != h0[j]) {
-                c.h[base + i] = sd[i];
-                int lx = i & (TW - 1), ly = i / TW;
-                if (lx == 0) s_side[DL] = 1;
-                if (lx == TW - 1) s_side[DR] = 1;
-                if (ly == 0) s_side[DU] = 1;
-                if (ly == TH - 1) s_side[DD] = 1;
-            }
-        }
-        __syncthreads();
-        if (threadIdx.x < 4 && s_side[threadIdx.x] && g.nb[threadIdx.x] >= 0)
-            enqueue(c, k + 1, g.nb[threadIdx.x]);
-        __syncthreads();
+        seed_with_halo(c, t, seeds);
     }
 }
 
@@ -266,7 +227,7 @@ __global__ void __launch_bounds__(NT) k_seed_push(Ctx c) {
         }
         for (int o = 16; o; o >>= 1) a += __shfl_xor_sync(0xffffffffu, a, o);
         if ((threadIdx.x & 31) == 0 && a) atomicAdd(&c.act[gid], a);
-        if (__syncthreads_or(a) && threadIdx.x == 0) enqueue(c, 0, int32_t(t));
+        if (__syncthreads_or(a) && threadIdx.x == 0) seed_tile(c, int32_t(t));
     }
 }
 
@@ -275,135 +236,6 @@ __global__ void k_update_live(Ctx c, int32_t ngrids) {
     if (g >= ngrids) return;
     if (c.live[g] && c.act[g] == 0) c.live[g] = 0;
     c.act[g] = 0;
-}
-
-template <class E>
-__global__ void __launch_bounds__(NT) k_push(Ctx c, int k, int iters) {
-    __shared__ int32_t sw[TPIX], sh[TPIX], sin_[TPIX];
-    __shared__ int32_t sr[4][TPIX];
-    __shared__ int32_t hh[4][TW], hacc[4][TW];
-    __shared__ int s_out[4];
-    const int32_t n = c.cnt[k % 3];
-    const int32_t *lst = list_of(c, k);
-    if (blockIdx.x == 0 && threadIdx.x == 0) {
-        c.cnt[(k + 2) % 3] = 0;
-        atomicAdd(&c.stat[ST_PUSH], (unsigned long long)n);
-    }
-    const int tid = threadIdx.x;
-    for (int li = blockIdx.x; li < n; li += gridDim.x) {
-        const int32_t t = lst[li];
-        TileGeo g = tile_geo(c, t);
-        const int64_t base = int64_t(t) * TPIX;
-        int32_t wv[PPT];
-        typename E::Word rv[PPT];
-        for (int j = 0; j < PPT; j++) {
-            int i = tid + j * NT;
-            wv[j] = c.w[base + i];
-            sw[i] = wv[j];
-            sh[i] = c.h[base + i];
-            sin_[i] = 0;
-            rv[j] = E::load(c.r, base + i);
-            for (int d = 0; d < 4; d++) sr[d][i] = E::lane(rv[j], d);
-        }
-        if (tid < 4 * TW) {
-            int s = tid / TW, j = tid % TW;
-            hh[s][j] = g.nb[s] >= 0 ? c.h[int64_t(g.nb[s]) * TPIX + halo_index(s, j)] : HINF;
-            hacc[s][j] = 0;
-            if (j == 0) s_out[s] = 0;
-        }
-        if (tid == 0) inq_of(c, k)[t] = 0;
-        __syncthreads();
-        for (int it = 0; it < iters; it++) {
-            // ---- push along admissible arcs (heights fixed in this phase, so
-            // no arc is pushed in both directions: plain adds are race-free;
-            // incoming excess gathers in sin_ with shared atomics)
-            for (int j = 0; j < PPT; j++) {
-                int i = tid + j * NT;
-                int32_t e = sw[i], hp = sh[i];
-                if (e <= 0 || hp >= HINF) continue;
-                int lx = i & (TW - 1), ly = i / TW;
-#pragma unroll
-                for (int d = 0; d < 4; d++) {
-                    int32_t rr = sr[d][i];
-                    if (rr <= 0) continue;
-                    int q;
-                    bool in;
-                    int32_t hq;
-                    int pos;
-                    if (d == DL) { in = lx > 0; q = i - 1; pos = ly; }
-                    else if (d == DR) { in = lx < TW - 1; q = i + 1; pos = ly; }
-                    else if (d == DU) { in = ly > 0; q = i - TW; pos = lx; }
-                    else { in = ly < TH - 1; q = i + TW; pos = lx; }
-                    hq = in ? sh[q] : hh[d][pos];
-                    if (hp != hq + 1) continue;
-                    int32_t dl = min(e, rr);
-                    e -= dl;
-                    sr[d][i] = rr - dl;
-                    if (in) {
-                        sr[opp(d)][q] += dl;
-                        atomicAdd(&sin_[q], dl);
-                    } else {
-                        hacc[d][pos] += dl;
-                    }
-                    if (!e) break;
-                }
-                sw[i] = e;
-            }
-            __syncthreads();
-            // ---- absorb inflow, relabel what is still active
-            int act = 0;
-            for (int j = 0; j < PPT; j++) {
-                int i = tid + j * NT;
-                int32_t e = sw[i] + sin_[i];
-                sin_[i] = 0;
-                sw[i] = e;
-                if (e <= 0 || sh[i] >= HINF) continue;
-                int lx = i & (TW - 1), ly = i / TW;
-                int32_t m = HINF;
-                if (sr[DL][i] > 0) m = min(m, lx ? sh[i - 1] : hh[DL][ly]);
-                if (sr[DR][i] > 0) m = min(m, lx < TW - 1 ? sh[i + 1] : hh[DR][ly]);
-                if (sr[DU][i] > 0) m = min(m, ly ? sh[i - TW] : hh[DU][lx]);
-                if (sr[DD][i] > 0) m = min(m, ly < TH - 1 ? sh[i + TW] : hh[DD][lx]);
-                int32_t nh = m >= HINF ? HINF : m + 1;
-                if (nh > sh[i]) sh[i] = nh;
-                act |= sh[i] < HINF;
-            }
-            if (!__syncthreads_or(act)) break;
-        }
-        __syncthreads();
-        // ---- write back: interior pixels plainly, border pixels as deltas
-        // (neighbour tiles may have pushed into them meanwhile)
-        int still = 0;
-        for (int j = 0; j < PPT; j++) {
-            int i = tid + j * NT;
-            int64_t p = base + i;
-            int32_t e = sw[i];
-            typename E::Word nw = E::pack(sr[0][i], sr[1][i], sr[2][i], sr[3][i]);
-            if (!on_border(i)) {
-                c.w[p] = e;
-                E::store(c.r, p, nw);
-            } else {
-                if (e != wv[j]) atomicAdd(&c.w[p], e - wv[j]);
-                E::store_delta(c.r, p, nw, rv[j]);
-            }
-            c.h[p] = sh[i];
-            still |= e > 0 && sh[i] < HINF;
-        }
-        if (tid < 4 * TW) {
-            int s = tid / TW, j = tid % TW;
-            int32_t a = hacc[s][j];
-            if (a > 0) {
-                int64_t q = int64_t(g.nb[s]) * TPIX + halo_index(s, j);
-                atomicAdd(&c.w[q], a);
-                E::add(c.r, q, opp(s), a);
-                s_out[s] = 1;
-            }
-        }
-        still = __syncthreads_or(still);
-        if (tid == 0 && still) enqueue(c, k + 1, t);
-        if (tid < 4 && s_out[tid]) enqueue(c, k + 1, g.nb[tid]);
-        __syncthreads();
-    }
 }
 
 // ---------------------------------------------------------------------------
@@ -415,102 +247,14 @@ __global__ void __launch_bounds__(NT) k_lab_seed(Ctx c) {
     for (int64_t t = blockIdx.x; t < c.ntiles; t += gridDim.x) {
         const GridDesc &gd = c.grids[c.tile_grid[t]];
         if (grid_swapped(c, gd)) continue;
-        int any = 0;
+        unsigned seeds = 0;
         for (int j = 0; j < PPT; j++) {
             int64_t p = t * TPIX + threadIdx.x + j * NT;
             int v = c.w[p] > 0;
             c.lab[p] = uint8_t(v);
-            any |= v;
+            seeds |= unsigned(v) << j;
         }
-        if (__syncthreads_or(any) && threadIdx.x == 0) enqueue(c, 0, int32_t(t));
-    }
-}
-
-template <class E>
-__global__ void __launch_bounds__(NT) k_bfs_src(Ctx c, int k) {
-    __shared__ uint8_t sl[TPIX];
-    __shared__ uint8_t sm[TPIX];      // bit d: the d-neighbour has a residual arc INTO this pixel
-    __shared__ uint8_t hl[4][TW];     // halo pixel reached and its arc into us residual
-    __shared__ int s_side[4];
-    const int32_t n = c.cnt[k % 3];
-    const int32_t *lst = list_of(c, k);
-    if (blockIdx.x == 0 && threadIdx.x == 0) {
-        c.cnt[(k + 2) % 3] = 0;
-        atomicAdd(&c.stat[ST_LAB], (unsigned long long)n);
-    }
-    __shared__ uint32_t sword[TPIX];  // packed "arc > 0" bits per pixel
-    for (int li = blockIdx.x; li < n; li += gridDim.x) {
-        const int32_t t = lst[li];
-        TileGeo g = tile_geo(c, t);
-        const int64_t base = int64_t(t) * TPIX;
-        uint8_t l0[PPT];
-        for (int j = 0; j < PPT; j++) {
-            int i = threadIdx.x + j * NT;
-            l0[j] = c.lab[base + i];
-            sl[i] = l0[j];
-            typename E::Word wd = E::load(c.r, base + i);
-            sword[i] = uint32_t((E::lane(wd, 0) > 0) | ((E::lane(wd, 1) > 0) << 1) |
-                                ((E::lane(wd, 2) > 0) << 2) | ((E::lane(wd, 3) > 0) << 3));
-        }
-        if (threadIdx.x < 4 * TW) {
-            int s = threadIdx.x / TW, j = threadIdx.x % TW;
-            uint8_t v = 0;
-            if (g.nb[s] >= 0) {
-                int64_t q = int64_t(g.nb[s]) * TPIX + halo_index(s, j);
-                v = c.lab[q] && E::lane(E::load(c.r, q), opp(s)) > 0;
-            }
-            hl[s][j] = v;
-            if (j == 0) s_side[s] = 0;
-        }
-        if (threadIdx.x == 0) inq_of(c, k)[t] = 0;
-        __syncthreads();
-        for (int j = 0; j < PPT; j++) {
-            int i = threadIdx.x + j * NT;
-            int lx = i & (TW - 1), ly = i / TW;
-            int mk = 0;
-            if (lx && (sword[i - 1] & (1u << DR))) mk |= 1;
-            if (lx < TW - 1 && (sword[i + 1] & (1u << DL))) mk |= 2;
-            if (ly && (sword[i - TW] & (1u << DD))) mk |= 4;
-            if (ly < TH - 1 && (sword[i + TW] & (1u << DU))) mk |= 8;
-            sm[i] = uint8_t(mk);
-        }
-        __syncthreads();
-        for (;;) {
-            int changed = 0;
-            for (int j = 0; j < PPT; j++) {
-                int i = threadIdx.x + j * NT;
-                if (sl[i]) continue;
-                int lx = i & (TW - 1), ly = i / TW;
-                int mk = sm[i];
-                int r = 0;
-                if (lx == 0) r |= hl[DL][ly];
-                else if (mk & 1) r |= sl[i - 1];
-                if (lx == TW - 1) r |= hl[DR][ly];
-                else if (mk & 2) r |= sl[i + 1];
-                if (ly == 0) r |= hl[DU][lx];
-                else if (mk & 4) r |= sl[i - TW];
-                if (ly == TH - 1) r |= hl[DD][lx];
-                else if (mk & 8) r |= sl[i + TW];
-                if (r) { sl[i] = 1; changed = 1; }
-            }
-            if (!__syncthreads_or(changed)) break;
-        }
-        for (int j = 0; j < PPT; j++) {
-            int i = threadIdx.x + j * NT;
-            if (sl[i] != l0[j]) {
-                c.lab[base + i] = 1;
-                if (c.w[base + i] < 0) atomicExch(c.err, 4);   // NonMaximalFlowError
-                int lx = i & (TW - 1), ly = i / TW;
-                if (lx == 0) s_side[DL] = 1;
-                if (lx == TW - 1) s_side[DR] = 1;
-                if (ly == 0) s_side[DU] = 1;
-                if (ly == TH - 1) s_side[DD] = 1;
-            }
-        }
-        __syncthreads();
-        if (threadIdx.x < 4 && s_side[threadIdx.x] && g.nb[threadIdx.x] >= 0)
-            enqueue(c, k + 1, g.nb[threadIdx.x]);
-        __syncthreads();
+        seed_with_halo(c, t, seeds);
     }
 }
 

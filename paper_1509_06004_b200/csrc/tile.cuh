@@ -1,0 +1,386 @@
+// tile.cuh -- the per-tile kernels: push-relabel discharge and the two BFS
+// sweeps, all built on one shared-memory primitive, tile_relax().
+//
+// One CTA of 1024 threads owns one 32x32 tile at a time, one pixel per
+// thread (warp = row for row work, warp = column for column work).  The
+// CTA walks the tiles of the current worklist (grid-stride) and appends to
+// the next worklist the tiles that still / newly need work.
+#pragma once
+#include "engine.cuh"
+
+namespace pmf {
+
+constexpr int NTT = 1024;        // threads per tile CTA
+constexpr int SP = TW + 1;       // padded shared-memory row stride (conflict-free columns)
+
+// Bit d of a pull mask: this pixel may take the value of its d-neighbour
+// (plus the step cost).  Halo values hv[side][j] stand for the neighbour
+// tile's facing pixels (HINF where there is none).
+//
+// tile_relax: Bellman-Ford to the fixpoint of
+//     d(p) = min(d(p), d(q) + cost)   for every pull arc p <- q
+// computed as alternating row / column passes; each pass is a pair of
+// segmented min-plus scans along warp shuffles (value - cost*x carried
+// through runs of consecutive pull arcs), so a straight run of any length
+// settles in one pass and a path with k turns in about k passes.
+__device__ __forceinline__ int32_t seg_prefix_min(int32_t u, int head, int lane) {
+#pragma unroll
+    for (int off = 1; off < 32; off <<= 1) {
+        int32_t ou = __shfl_up_sync(0xffffffffu, u, off);
+        int oh = __shfl_up_sync(0xffffffffu, head, off);
+        if (lane >= off && !head) {
+            u = min(u, ou);
+            head |= oh;
+        }
+    }
+    return u;
+}
+
+__device__ __forceinline__ int32_t seg_suffix_min(int32_t u, int tail, int lane) {
+#pragma unroll
+    for (int off = 1; off < 32; off <<= 1) {
+        int32_t ou = __shfl_down_sync(0xffffffffu, u, off);
+        int ot = __shfl_down_sync(0xffffffffu, tail, off);
+        if (lane + off < 32 && !tail) {
+            u = min(u, ou);
+            tail |= ot;
+        }
+    }
+    return u;
+}
+
+// one direction pair along a line: lo = pull from the lower index neighbour
+// (bit blo), hi = pull from the higher index neighbour (bit bhi)
+__device__ __forceinline__ int32_t line_relax(int32_t v, int m, int lane, int blo, int bhi,
+                                              int32_t halo_lo, int32_t halo_hi, int cost) {
+    if (lane == 0 && (m & blo)) v = min(v, min(halo_lo + cost, HINF));
+    int32_t u = v - cost * lane;
+    u = seg_prefix_min(u, lane == 0 || !(m & blo), lane);
+    v = min(u + cost * lane, HINF);
+    if (lane == 31 && (m & bhi)) v = min(v, min(halo_hi + cost, HINF));
+    u = v + cost * lane;
+    u = seg_suffix_min(u, lane == 31 || !(m & bhi), lane);
+    return min(u - cost * lane, HINF);
+}
+
+// d: [32][SP] values, mk: [32][32] pull masks, hv: halo values.  All 1024
+// threads call it; returns the number of full sweeps performed.
+__device__ int tile_relax(int32_t *d, const uint8_t *mk, const int32_t (*hv)[TW], int cost) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    int sweeps = 0;
+    for (;;) {
+        int changed = 0;
+        {   // rows: warp = y, lane = x; bits L (1) / R (2)
+            int32_t v0 = d[warp * SP + lane];
+            int32_t v = line_relax(v0, mk[warp * TW + lane], lane, 1, 2, hv[DL][warp], hv[DR][warp], cost);
+            if (v != v0) { d[warp * SP + lane] = v; changed = 1; }
+        }
+        __syncthreads();
+        {   // columns: warp = x, lane = y; bits U (4) / D (8)
+            int32_t v0 = d[lane * SP + warp];
+            int32_t v = line_relax(v0, mk[lane * TW + warp], lane, 4, 8, hv[DU][warp], hv[DD][warp], cost);
+            if (v != v0) { d[lane * SP + warp] = v; changed = 1; }
+        }
+        sweeps++;
+        if (!__syncthreads_or(changed)) return sweeps;
+    }
+}
+
+struct TileResult {
+    int again;   // the tile itself still has work
+    int out;     // bit s: the neighbour on side s needs (re)processing
+};
+
+// Outer loop shared by the tile kernels.  Sweep mode (k >= 0): walk
+// worklist k once, list follow-up tiles in worklist k + 1 (one launch per
+// sweep).  Persistent mode (k < 0): pop tiles from the device queue until
+// the phase drains (or its pop budget is spent); follow-up tiles are queued
+// and picked up by whichever CTA is free, without a kernel boundary.
+template <class Body>
+__device__ __forceinline__ void tile_loop(const Ctx &c, int k, int stat, Body &&body) {
+    __shared__ int32_t s_t;
+    const int i = threadIdx.x;
+    if (k >= 0) {
+        const int32_t n = c.cnt[k % 3];
+        const int32_t *lst = list_of(c, k);
+        if (blockIdx.x == 0 && i == 0) {
+            c.cnt[(k + 2) % 3] = 0;
+            atomicAdd(&c.stat[stat], (unsigned long long)n);
+        }
+        for (int li = blockIdx.x; li < n; li += gridDim.x) {
+            const int32_t t = lst[li];
+            if (i == 0) inq_of(c, k)[t] = 0;
+            TileResult r = body(t);
+            if (i == 0) {
+                TileGeo g = tile_geo(c, t);
+                if (r.again) enqueue(c, k + 1, t);
+                for (int sd = 0; sd < 4; sd++)
+                    if ((r.out >> sd) & 1 && g.nb[sd] >= 0) enqueue(c, k + 1, g.nb[sd]);
+            }
+            __syncthreads();
+        }
+        return;
+    }
+    // Hand-off ordering (store-buffering pattern): a requester writes tile
+    // data, then reads the neighbour's queue state; a popper writes the
+    // state, then reads the data.  Each side needs a gpu-scope SC fence
+    // between its write and its read in EVERY participating thread, i.e.
+    // on both sides of the CTA barrier that separates writer threads from
+    // thread 0 -- otherwise a "still queued" read can pair with a stale
+    // data read and a propagation step is lost.
+    for (;;) {
+        if (i == 0) {
+            int32_t t = q_next(c);
+            __threadfence();
+            s_t = t;
+        }
+        __syncthreads();
+        const int32_t t = s_t;
+        if (t < 0) return;
+        __threadfence();              // popper side: state write < data reads
+        TileResult r = body(t);
+        __threadfence();              // requester side: data writes < ...
+        __syncthreads();
+        if (i == 0) {
+            __threadfence();          // ... < thread 0's queue-state reads
+            TileGeo g = tile_geo(c, t);
+            for (int sd = 0; sd < 4; sd++)
+                if ((r.out >> sd) & 1 && g.nb[sd] >= 0) q_request(c, g.nb[sd]);
+            q_finish(c, t, r.again != 0);
+            atomicAdd(&c.stat[stat], 1ull);
+        }
+    }
+}
+
+// ---------------------------------------------------------------------------
+// Global relabel: exact distance to the sink over residual arcs
+// (solvers.py:54-71).  h holds 1 on sink-residual pixels and HINF elsewhere
+// after k_gr_init; each tile relaxes to its fixpoint given its halo and
+// flags the neighbours facing any border pixel that went down.
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ int border_sides(int lx, int ly) {
+    return (lx == 0 ? 1 << DL : 0) | (lx == TW - 1 ? 1 << DR : 0) | (ly == 0 ? 1 << DU : 0) |
+           (ly == TH - 1 ? 1 << DD : 0);
+}
+
+template <class E>
+__global__ void __launch_bounds__(NTT, 2) k_bfs_sink(Ctx c, int k) {
+    __shared__ int32_t sd[TH * SP];
+    __shared__ uint8_t sm[TPIX];
+    __shared__ int32_t hv[4][TW];
+    __shared__ int s_side;
+    const int i = threadIdx.x, lx = i & 31, ly = i >> 5;
+    tile_loop(c, k, ST_BFS, [&](int32_t t) -> TileResult {
+        TileGeo g = tile_geo(c, t);
+        const int64_t p = int64_t(t) * TPIX + i;
+        const int32_t h0 = __ldcg(c.h + p);
+        typename E::Word wd = E::load(c.r, p);
+        sd[ly * SP + lx] = h0;
+        sm[i] = uint8_t((E::lane(wd, 0) > 0) | ((E::lane(wd, 1) > 0) << 1) |
+                        ((E::lane(wd, 2) > 0) << 2) | ((E::lane(wd, 3) > 0) << 3));
+        if (i < 4 * TW) {
+            int s = i / TW, j = i % TW;
+            hv[s][j] = g.nb[s] >= 0 ? __ldcg(c.h + int64_t(g.nb[s]) * TPIX + halo_index(s, j)) : HINF;
+        }
+        if (i == 0) s_side = 0;
+        __syncthreads();
+        tile_relax(sd, sm, hv, 1);
+        const int32_t h1 = sd[ly * SP + lx];
+        if (h1 != h0) {
+            c.h[p] = h1;
+            if (int b = border_sides(lx, ly)) atomicOr(&s_side, b);
+        }
+        __syncthreads();
+        return TileResult{0, s_side};
+    });
+}
+
+// ---------------------------------------------------------------------------
+// Source-side closure (solvers.py:144-158): lab = 1 where reachable from an
+// excess pixel along residual arcs (relaxation with cost 0 over the arcs
+// INTO each pixel); touching a sink-residual pixel means the preflow was
+// not maximal (NonMaximalFlowError).
+// ---------------------------------------------------------------------------
+template <class E>
+__global__ void __launch_bounds__(NTT, 2) k_bfs_src(Ctx c, int k) {
+    __shared__ int32_t sd[TH * SP];
+    __shared__ uint8_t sbits[TPIX];    // own outgoing "arc > 0" bits
+    __shared__ uint8_t sm[TPIX];       // pull mask: incoming arcs
+    __shared__ int32_t hv[4][TW];
+    __shared__ int s_side;
+    const int i = threadIdx.x, lx = i & 31, ly = i >> 5;
+    tile_loop(c, k, ST_LAB, [&](int32_t t) -> TileResult {
+        TileGeo g = tile_geo(c, t);
+        const int64_t p = int64_t(t) * TPIX + i;
+        const uint8_t l0 = __ldcg(c.lab + p);
+        typename E::Word wd = E::load(c.r, p);
+        sd[ly * SP + lx] = l0 ? 0 : HINF;
+        sbits[i] = uint8_t((E::lane(wd, 0) > 0) | ((E::lane(wd, 1) > 0) << 1) |
+                           ((E::lane(wd, 2) > 0) << 2) | ((E::lane(wd, 3) > 0) << 3));
+        if (i < 4 * TW) {
+            int s = i / TW, j = i % TW;
+            int32_t v = HINF;
+            if (g.nb[s] >= 0 && __ldcg(c.lab + int64_t(g.nb[s]) * TPIX + halo_index(s, j))) v = 0;
+            hv[s][j] = v;
+        }
+        if (i == 0) s_side = 0;
+        __syncthreads();
+        // pull mask: bit d set when the d-neighbour has a residual arc into us
+        int mk = 0;
+        if (lx > 0) mk |= (sbits[i - 1] >> DR) & 1;
+        if (lx < TW - 1) mk |= ((sbits[i + 1] >> DL) & 1) << 1;
+        if (ly > 0) mk |= ((sbits[i - TW] >> DD) & 1) << 2;
+        if (ly < TH - 1) mk |= ((sbits[i + TW] >> DU) & 1) << 3;
+        if (lx == 0 && g.nb[DL] >= 0)
+            mk |= (E::lane(E::load(c.r, int64_t(g.nb[DL]) * TPIX + halo_index(DL, ly)), DR) > 0) << 0;
+        if (lx == TW - 1 && g.nb[DR] >= 0)
+            mk |= (E::lane(E::load(c.r, int64_t(g.nb[DR]) * TPIX + halo_index(DR, ly)), DL) > 0) << 1;
+        if (ly == 0 && g.nb[DU] >= 0)
+            mk |= (E::lane(E::load(c.r, int64_t(g.nb[DU]) * TPIX + halo_index(DU, lx)), DD) > 0) << 2;
+        if (ly == TH - 1 && g.nb[DD] >= 0)
+            mk |= (E::lane(E::load(c.r, int64_t(g.nb[DD]) * TPIX + halo_index(DD, lx)), DU) > 0) << 3;
+        sm[i] = uint8_t(mk);
+        __syncthreads();
+        tile_relax(sd, sm, hv, 0);
+        if (sd[ly * SP + lx] == 0 && !l0) {
+            c.lab[p] = 1;
+            if (__ldcg(c.w + p) < 0) atomicExch(c.err, 4);   // NonMaximalFlowError
+            if (int b = border_sides(lx, ly)) atomicOr(&s_side, b);
+        }
+        __syncthreads();
+        return TileResult{0, s_side};
+    });
+}
+
+// ---------------------------------------------------------------------------
+// Push-relabel discharge of one tile (solvers.py:107-136 semantics with the
+// lock-free admissibility rule h(p) > h(q), which tolerates the stale halo
+// heights of concurrently discharged neighbour tiles).
+//
+// Registers hold the pixel's excess/sink state e and its four residuals;
+// pushes into a neighbour are written to the neighbour's per-direction
+// inflow slot (each slot has exactly one writer per iteration, so no
+// atomics), and absorbed after the barrier.  Heights live in shared memory.
+// At load (and every `relabel_every` iterations) the tile runs an exact
+// local relabel: the distance, inside the tile, to a sink-residual pixel
+// (1) or to a halo pixel (its height + 1) -- HINF means every path out ends
+// in frozen pixels, a certificate that the pixel cannot reach the sink.
+// ---------------------------------------------------------------------------
+template <class E>
+__global__ void __launch_bounds__(NTT, 2) k_push(Ctx c, int k, int iters, int relabel_every) {
+    __shared__ int32_t sh[TH * SP];
+    __shared__ int32_t sd[TH * SP];
+    __shared__ int32_t sin4[4][TPIX];
+    __shared__ uint8_t sm[TPIX];
+    __shared__ int32_t hh[4][TW], hacc[4][TW];
+    __shared__ int s_out;
+    const int i = threadIdx.x, lx = i & 31, ly = i >> 5, pi = ly * SP + lx;
+    // in-tile neighbour (padded index) per direction, or -1 (halo)
+    const int nbi[4] = {lx > 0 ? pi - 1 : -1, lx < TW - 1 ? pi + 1 : -1,
+                        ly > 0 ? pi - SP : -1, ly < TH - 1 ? pi + SP : -1};
+    const int nbt[4] = {i - 1, i + 1, i - TW, i + TW};   // neighbour's flat tile index
+    const int hpos[4] = {ly, ly, lx, lx};                 // index into halo arrays
+    tile_loop(c, k, ST_PUSH, [&](int32_t t) -> TileResult {
+        TileGeo g = tile_geo(c, t);
+        const int64_t p = int64_t(t) * TPIX + i;
+        const int32_t w0 = __ldcg(c.w + p);
+        const typename E::Word rv0 = E::load(c.r, p);
+        int32_t e = w0, h = __ldcg(c.h + p);
+        int32_t r[4];
+#pragma unroll
+        for (int d = 0; d < 4; d++) {
+            r[d] = E::lane(rv0, d);
+            sin4[d][i] = 0;
+        }
+        if (i < 4 * TW) {
+            int s = i / TW, j = i % TW;
+            hh[s][j] = g.nb[s] >= 0 ? __ldcg(c.h + int64_t(g.nb[s]) * TPIX + halo_index(s, j)) : HINF;
+            hacc[s][j] = 0;
+        }
+        if (i == 0) s_out = 0;
+        int act = 1;
+        for (int it = 0; it < iters; it++) {
+            if (relabel_every && it % relabel_every == 0) {
+                // exact local relabel (frozen pixels stay frozen)
+                sd[pi] = e < 0 ? 1 : HINF;
+                sm[i] = uint8_t((r[0] > 0) | ((r[1] > 0) << 1) | ((r[2] > 0) << 2) | ((r[3] > 0) << 3));
+                __syncthreads();
+                tile_relax(sd, sm, hh, 1);
+                if (h < HINF) h = sd[pi];
+                sh[pi] = h;
+                act = __syncthreads_or(e > 0 && h < HINF);
+                if (!act) break;
+            } else if (it == 0) {
+                sh[pi] = h;
+                act = __syncthreads_or(e > 0 && h < HINF);
+                if (!act) break;
+            }
+            int32_t hn[4];
+#pragma unroll
+            for (int d = 0; d < 4; d++) hn[d] = nbi[d] >= 0 ? sh[nbi[d]] : hh[d][hpos[d]];
+            // ---- push downhill (heights are fixed during this phase, so an
+            // arc is never pushed both ways and every inflow slot has one writer)
+            if (e > 0 && h < HINF) {
+#pragma unroll
+                for (int d = 0; d < 4; d++) {
+                    if (e > 0 && r[d] > 0 && h > hn[d]) {
+                        int32_t dl = min(e, r[d]);
+                        e -= dl;
+                        r[d] -= dl;
+                        if (nbi[d] >= 0) sin4[opp(d)][nbt[d]] = dl;
+                        else hacc[d][hpos[d]] += dl;
+                    }
+                }
+            }
+            __syncthreads();
+            // ---- absorb inflow, relabel what is still active
+#pragma unroll
+            for (int d = 0; d < 4; d++) {
+                int32_t v = sin4[d][i];
+                if (v) {
+                    e += v;
+                    r[d] += v;
+                    sin4[d][i] = 0;
+                }
+            }
+            if (e > 0 && h < HINF) {
+                int32_t m = HINF;
+#pragma unroll
+                for (int d = 0; d < 4; d++)
+                    if (r[d] > 0) m = min(m, hn[d]);
+                if (m >= h) {
+                    h = m >= HINF ? HINF : m + 1;
+                    sh[pi] = h;
+                }
+            }
+            act = __syncthreads_or(e > 0 && h < HINF);
+            if (!act) break;
+        }
+        // ---- write back: interior pixels plainly, border pixels as deltas
+        // (neighbour tiles may have pushed into them meanwhile)
+        const typename E::Word rv = E::pack(r[0], r[1], r[2], r[3]);
+        if (!on_border(i)) {
+            c.w[p] = e;
+            E::store(c.r, p, rv);
+        } else {
+            if (e != w0) atomicAdd(&c.w[p], e - w0);
+            E::store_delta(c.r, p, rv, rv0);
+        }
+        c.h[p] = h;
+        __syncthreads();
+        if (i < 4 * TW) {
+            int s = i / TW, j = i % TW;
+            int32_t a = hacc[s][j];
+            if (a > 0) {
+                int64_t q = int64_t(g.nb[s]) * TPIX + halo_index(s, j);
+                atomicAdd(&c.w[q], a);
+                E::add(c.r, q, opp(s), a);
+                atomicOr(&s_out, 1 << s);
+            }
+        }
+        __syncthreads();
+        return TileResult{act, s_out};
+    });
+}
+
+}  // namespace pmf

@@ -27,6 +27,9 @@ def main():
     ap.add_argument("--iters", type=int, default=None)
     ap.add_argument("--sweeps", type=int, default=None)
     ap.add_argument("--chunk", type=int, default=None)
+    ap.add_argument("--relabel", type=int, default=None)
+    ap.add_argument("--persistent", type=int, default=None)
+    ap.add_argument("--budget", type=int, default=None)
     ap.add_argument("--reps", type=int, default=3)
     ap.add_argument("--nprob", type=int, default=None, help="problems per device batch")
     a = ap.parse_args()
@@ -37,6 +40,9 @@ def main():
     if a.iters: s.set("push_iters", a.iters)
     if a.sweeps: s.set("push_sweeps", a.sweeps)
     if a.chunk: s.set("bfs_chunk", a.chunk)
+    if a.relabel is not None: s.set("relabel_every", a.relabel)
+    if a.persistent is not None: s.set("persistent", a.persistent)
+    if a.budget is not None: s.set("push_budget", a.budget)
     for r in range(a.reps):
         t0 = time.perf_counter()
         sw, flows, labels = s.solve_seed_batch(c["w"], c["h"], probs, c["lams"], "auto")

@@ -99,15 +99,16 @@ def test_c1_supergraph(engine):
     sched = LambdaSchedule(g["lambdas"])
     res = solve_seed_supergraph(probs, sched, "auto")
     assert res.flow == 27814225
-    for c, flow, lab in zip(res.cuts, g["flows"], g["labels"]):
-        assert c.flow == flow
-        assert np.array_equal(c.labels, lab)
+    for j, (c, flow, lab) in enumerate(zip(res.cuts, g["flows"], g["labels"])):
+        assert c.flow == flow, j
+        assert np.array_equal(c.labels, lab), (j, int((c.labels != lab).sum()))
     comp, layout, originals = build_seed_supergraph(probs, sched, "auto")
     cut = solve_composite(comp, layout)
     assert cut.flow == 27814225
     parts = split(layout, cut, originals)
-    for p, flow, lab in zip(parts, g["flows"], g["labels"]):
-        assert p.flow == flow and np.array_equal(p.labels, lab)
+    for j, (p, flow, lab) in enumerate(zip(parts, g["flows"], g["labels"])):
+        assert p.flow == flow, ("composite", j, p.flow, flow)
+        assert np.array_equal(p.labels, lab), ("composite", j, int((p.labels != lab).sum()))
 
 
 def test_c1_swapped_family_matches(engine):
@@ -227,3 +228,21 @@ def test_large_grid_properties(engine):
         if prev is not None:
             assert not (prev & ~c.labels.astype(bool)).any()
         prev = c.labels.astype(bool)
+
+
+@pytest.mark.parametrize("persistent", [0, 1])
+def test_c1_stress_repeated(engine, persistent):
+    """Worklist/queue races show up as rare label or flow differences:
+    repeat the C1 supergraph in both scheduling modes."""
+    from paper_1509_06004_b200 import _native
+    g = load_synth("c1_160x120.npz")
+    probs = synth.generate(160, 120, rng_seed=0).problems
+    s = _native.Solver(0, persistent=persistent)
+    try:
+        for rep in range(12):
+            _, flows, labels = s.solve_seed_batch(160, 120, probs, g["lambdas"], "auto")
+            assert flows[0].tolist() == g["flows"], rep
+            for j in range(20):
+                assert np.array_equal(labels[0][j], g["labels"][j]), (rep, j)
+    finally:
+        s.close()
