@@ -75,6 +75,7 @@ typedef struct pmf_stats {
     int64_t launches;           /* kernels launched by the last run           */
     int64_t h2d_bytes;          /* host->device bytes of the last stage       */
     int64_t d2h_bytes;          /* device->host bytes of the last fetch       */
+    int64_t graph_builds;       /* solve graphs (re)built by the last run     */
 } pmf_stats;
 
 /* Create / destroy a solver bound to one CUDA device and its own stream. */
@@ -82,8 +83,12 @@ int pmf_solver_create(int32_t device, pmf_solver **out);
 int pmf_solver_destroy(pmf_solver *s);
 
 /* Tuning knobs: "push_iters" (inner smem iterations per tile pass),
- * "push_sweeps" (push launches per global relabel), "bfs_chunk" (BFS
- * launches between convergence checks), "timing" (0/1 device timings),
+ * "relabel_every" (exact local relabel period inside a tile pass),
+ * "push_budget" (persistent discharge: tile pops per seeded tile),
+ * "push_sweeps" (sweep-mode discharge launches per cycle), "bfs_chunk"
+ * (host-driven mode: launches between convergence checks), "persistent" /
+ * "persistent_bfs" (phase scheduling), "graph" (0: host-driven loop, 1:
+ * whole solve as one CUDA graph), "timing" (0/1 event timings),
  * "max_cycles" (non-convergence guard). Returns PMF_ERR_ARG if unknown. */
 int pmf_solver_set(pmf_solver *s, const char *name, int64_t value);
 

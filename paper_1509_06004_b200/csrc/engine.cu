@@ -130,18 +130,19 @@ struct pmf_solver {
     int sms = 148;
     int grid_push = 0, grid_bfs = 0, grid_full = 0;
     // knobs
-    int push_iters = 32;
+    int push_iters = 16;
     int push_sweeps = 64;
-    int relabel_every = 16;
-    int persistent = 1;
-    int push_budget = 8;      // persistent push phase: pops <= budget * seeded tiles
+    int relabel_every = 8;
+    int persistent = 1;       // discharge phase as one persistent launch
+    int persistent_bfs = 0;   // BFS phases as one persistent launch
+    int push_budget = 2;      // persistent push phase: pops <= budget * seeded tiles
     int bfs_chunk = 8;
     int timing = 0;
     int64_t max_cycles = 50000;
     // device workspace
     DevBuf d_w, d_h, d_r, d_lab, d_tile_grid, d_grids, d_live, d_act, d_list, d_inq, d_cnt,
         d_snk, d_drain, d_err, d_stat, d_colswap, d_out, d_in32, d_pw, d_mask, d_off, d_lam,
-        d_swapcnt, d_swapflag, d_ring, d_qstate, d_qctr;
+        d_swapcnt, d_swapflag, d_ring, d_qstate, d_qctr, d_ctl;
     HostBuf h_in32, h_pw, h_mask, h_out, h_small;
     Layout lay;
     std::vector<int32_t> ones;
@@ -155,6 +156,9 @@ struct pmf_solver {
     cudaEvent_t ev_run[2] = {nullptr, nullptr};
     pmf_stats stats{};
     int edge_bytes = 4;
+    int use_graph = 1;                 // whole solve as one CUDA graph
+    cudaGraphExec_t gexec = nullptr;   // cached instantiated solve graph
+    unsigned char gkey[512] = {0};     // GraphKey it was built for
 
     int ev_get(cudaEvent_t *e) {
         if (ev_used == ev_pool.size()) {
@@ -198,7 +202,8 @@ int setup_state(pmf_solver *s, int edge_bytes) {
         (rc = s->d_err.ensure(64)) || (rc = s->d_stat.ensure(ST_NSTAT * 8)) ||
         (rc = s->d_out.ensure(std::max<int64_t>(L.out_bytes, 1))) || (rc = s->d_colswap.ensure(64)) ||
         (rc = s->d_swapflag.ensure(64)) || (rc = s->d_ring.ensure(T * 4)) ||
-        (rc = s->d_qstate.ensure(T * 4)) || (rc = s->d_qctr.ensure(64)))
+        (rc = s->d_qstate.ensure(T * 4)) || (rc = s->d_qctr.ensure(64)) ||
+        (rc = s->d_ctl.ensure(sizeof(Ctl))))
         return rc;
     s->edge_bytes = edge_bytes;
     // host sources live in the solver (s->lay, s->ones) until the next setup
@@ -239,6 +244,8 @@ int setup_state(pmf_solver *s, int edge_bytes) {
     x.qctr = s->d_qctr.as<unsigned int>();
     x.qcap = int32_t(T);
     x.persistent = s->persistent;
+    x.ctl = s->d_ctl.as<Ctl>();
+    x.budget_dev = 0;
     // BFS phases converge on their own (values only decrease); the cap only
     // guards against a runaway launch
     x.budget = unsigned(std::min<int64_t>(int64_t(4096) * T + 4096, int64_t(0xffffffffu) - 1));
@@ -253,46 +260,58 @@ int read_count(pmf_solver *s, const Ctx &c, int idx, int32_t *out) {
     return 0;
 }
 
-int begin_phase(pmf_solver *s, const Ctx &c) {
-    if (c.persistent) {
-        CK(cudaMemsetAsync(c.qctr, 0, 16, s->st));
-        CK(cudaMemsetAsync(c.qstate, 0, size_t(c.ntiles) * 4, s->st));
-        CK(cudaMemsetAsync(c.ring, 0xff, size_t(c.ntiles) * 4, s->st));
-    } else {
-        CK(cudaMemsetAsync(c.cnt, 0, 3 * 4, s->st));
-        CK(cudaMemsetAsync(c.inq0, 0, size_t(2 * c.ntiles) * 4, s->st));
-    }
-    return 0;
-}
-
-// number of tiles the seed kernel put in the first worklist / the queue
-int read_seeded(pmf_solver *s, const Ctx &c, int32_t *out) {
-    if (!c.persistent) return read_count(s, c, 0, out);
-    unsigned *hp = s->h_small.as<unsigned>();
-    CK(cudaMemcpyAsync(hp, c.qctr + QC_PENDING, 4, cudaMemcpyDeviceToHost, s->st));
+int read_ctl(pmf_solver *s, const Ctx &c, Ctl *out) {
+    Ctl *hp = s->h_small.as<Ctl>();
+    CK(cudaMemcpyAsync(hp, c.ctl, sizeof(Ctl), cudaMemcpyDeviceToHost, s->st));
     CK(cudaStreamSynchronize(s->st));
-    *out = int32_t(*hp);
+    *out = *hp;
     return 0;
 }
 
+inline LaunchCtl lctl(int stat, cudaGraphConditionalHandle h = 0, int has = 0, int max_k = 0) {
+    LaunchCtl l;
+    l.stat = stat;
+    l.cond = h;
+    l.has_cond = has;
+    l.max_k = max_k;
+    return l;
+}
 
+// Per-phase scheduling contexts: the BFS phases and the discharge phase can
+// each run as launch-per-sweep worklists or as one persistent launch.
+struct PhaseCtx {
+    Ctx base, bfs, push, pq;   // pq: persistent discharge with device budget
+};
+
+PhaseCtx phase_ctx(pmf_solver *s, const Ctx &c0) {
+    PhaseCtx p;
+    p.base = c0;
+    p.bfs = c0;
+    p.bfs.persistent = s->persistent_bfs;
+    p.push = c0;
+    p.push.persistent = s->persistent;
+    p.pq = p.push;
+    p.pq.budget_dev = 1;
+    return p;
+}
+
+// ---- host-driven loop (graph = 0): the host reads worklist lengths and the
+// control block between phases
 template <class E>
-int run_bfs(pmf_solver *s, const Ctx &c, bool sink, int64_t *sweeps) {
+int host_bfs(pmf_solver *s, const Ctx &c, bool sink) {
     if (c.persistent) {   // one launch; the queue drains on the device
-        if (sink) LAUNCH(s, (k_bfs_sink<E><<<s->grid_bfs, NTT, 0, s->st>>>(c, -1)));
-        else LAUNCH(s, (k_bfs_src<E><<<s->grid_bfs, NTT, 0, s->st>>>(c, -1)));
+        if (sink) LAUNCH(s, (k_bfs_sink<E><<<s->grid_bfs, NTT, 0, s->st>>>(c, K_PERSISTENT, lctl(ST_BFS))));
+        else LAUNCH(s, (k_bfs_src<E><<<s->grid_bfs, NTT, 0, s->st>>>(c, K_PERSISTENT, lctl(ST_LAB))));
         CK(cudaGetLastError());
-        *sweeps += 1;
         return 0;
     }
     int k = 0;
     for (;;) {
         for (int j = 0; j < s->bfs_chunk; j++, k++) {
-            if (sink) LAUNCH(s, (k_bfs_sink<E><<<s->grid_bfs, NTT, 0, s->st>>>(c, k)));
-            else LAUNCH(s, (k_bfs_src<E><<<s->grid_bfs, NTT, 0, s->st>>>(c, k)));
+            if (sink) LAUNCH(s, (k_bfs_sink<E><<<s->grid_bfs, NTT, 0, s->st>>>(c, k, lctl(ST_BFS))));
+            else LAUNCH(s, (k_bfs_src<E><<<s->grid_bfs, NTT, 0, s->st>>>(c, k, lctl(ST_LAB))));
         }
         CK(cudaGetLastError());
-        *sweeps += s->bfs_chunk;
         int32_t left = 0;
         int rc = read_count(s, c, k % 3, &left);
         if (rc) return rc;
@@ -301,67 +320,219 @@ int run_bfs(pmf_solver *s, const Ctx &c, bool sink, int64_t *sweeps) {
 }
 
 template <class E>
-int run_solve(pmf_solver *s, const Ctx &c, int32_t ngrids) {
+int host_solve(pmf_solver *s, const Ctx &c0, int32_t ngrids) {
+    PhaseCtx P = phase_ctx(s, c0);
     int rc = 0;
-    int64_t cycle = 0;
-    for (;; cycle++) {
-        if (cycle > s->max_cycles)
-            return fail(PMF_ERR_NOCONV, "push-relabel failed to converge within %lld cycles",
-                        (long long)s->max_cycles);
+    for (;;) {
         // exact global relabel
         s->tmark(C_BFS);
-        if ((rc = begin_phase(s, c))) return rc;
-        LAUNCH(s, (k_gr_init<<<s->grid_full, NT, 0, s->st>>>(c)));
+        LAUNCH(s, (k_phase_begin<<<s->grid_full, 256, 0, s->st>>>(P.bfs, P.bfs.persistent, 0, 0)));
+        LAUNCH(s, (k_gr_init<<<s->grid_full, NT, 0, s->st>>>(P.bfs)));
         s->stats.full_passes++;
-        if ((rc = run_bfs<E>(s, c, true, &s->stats.bfs_sweeps))) return rc;
+        if ((rc = host_bfs<E>(s, P.bfs, true))) return rc;
         // list active tiles; retire grids without active pixels
         s->tmark(C_SEED);
-        if ((rc = begin_phase(s, c))) return rc;
-        LAUNCH(s, (k_seed_push<<<s->grid_full, NT, 0, s->st>>>(c)));
-        LAUNCH(s, (k_update_live<<<int(cdiv(ngrids, 256)), 256, 0, s->st>>>(c, ngrids)));
+        LAUNCH(s, (k_phase_begin<<<s->grid_full, 256, 0, s->st>>>(P.push, P.push.persistent, 0, 0)));
+        LAUNCH(s, (k_seed_push<<<s->grid_full, NT, 0, s->st>>>(P.push)));
+        LAUNCH(s, (k_cycle_ctl<<<1, 1024, 0, s->st>>>(P.push, ngrids, P.push.persistent,
+                                                      unsigned(s->push_budget), s->max_cycles, 0, 0)));
         CK(cudaGetLastError());
         s->stats.full_passes++;
-        int32_t nact = 0;
-        if ((rc = read_seeded(s, c, &nact))) return rc;
-        if (nact == 0) break;
-        if (c.persistent) {
-            s->tmark(C_PUSH);
-            Ctx cp = c;
-            // a bounded pop budget per phase always applies: the next global
-            // relabel resets stale heights (and no launch can spin forever)
-            uint64_t cap = uint64_t(64) * uint64_t(c.ntiles) + 1024;
-            uint64_t want = s->push_budget ? uint64_t(s->push_budget) * uint64_t(nact) + 64 : cap;
-            cp.budget = unsigned(std::min(want, cap));
-            LAUNCH(s, (k_push<E><<<s->grid_push, NTT, 0, s->st>>>(cp, -1, s->push_iters, s->relabel_every)));
+        Ctl ctl;
+        if ((rc = read_ctl(s, c0, &ctl))) return rc;
+        if (ctl.noconv)
+            return fail(PMF_ERR_NOCONV, "push-relabel failed to converge within %lld cycles",
+                        (long long)s->max_cycles);
+        if (ctl.nact == 0) break;
+        s->tmark(C_PUSH);
+        if (P.push.persistent) {
+            LAUNCH(s, (k_push<E><<<s->grid_push, NTT, 0, s->st>>>(P.pq, K_PERSISTENT, s->push_iters,
+                                                                  s->relabel_every, lctl(ST_PUSH))));
             CK(cudaGetLastError());
-            s->stats.push_sweeps += 1;
             continue;
         }
-        // discharge until no tile is listed (or the per-cycle sweep budget
-        // is spent), checking the list length every bfs_chunk launches
-        s->tmark(C_PUSH);
+        // discharge until no tile is listed (or the per-cycle sweep cap)
         for (int k = 0; k < s->push_sweeps;) {
             int chunk = std::min(s->bfs_chunk, s->push_sweeps - k);
             for (int j = 0; j < chunk; j++, k++)
-                LAUNCH(s, (k_push<E><<<s->grid_push, NTT, 0, s->st>>>(c, k, s->push_iters, s->relabel_every)));
+                LAUNCH(s, (k_push<E><<<s->grid_push, NTT, 0, s->st>>>(P.push, k, s->push_iters,
+                                                                      s->relabel_every, lctl(ST_PUSH))));
             CK(cudaGetLastError());
-            s->stats.push_sweeps += chunk;
             int32_t left = 0;
-            if ((rc = read_count(s, c, k % 3, &left))) return rc;
+            if ((rc = read_count(s, P.push, k % 3, &left))) return rc;
             if (left == 0) break;
         }
     }
-    s->stats.cycles = cycle + 1;
     // labels: source-side closure, then emit
     s->tmark(C_LAB);
-    if ((rc = begin_phase(s, c))) return rc;
-    LAUNCH(s, (k_lab_seed<<<s->grid_full, NT, 0, s->st>>>(c)));
+    LAUNCH(s, (k_phase_begin<<<s->grid_full, 256, 0, s->st>>>(P.bfs, P.bfs.persistent, 0, 0)));
+    LAUNCH(s, (k_lab_seed<<<s->grid_full, NT, 0, s->st>>>(P.bfs)));
     s->stats.full_passes++;
-    if ((rc = run_bfs<E>(s, c, false, &s->stats.bfs_sweeps))) return rc;
-    LAUNCH(s, (k_emit<<<s->grid_full, NT, 0, s->st>>>(c)));
+    if ((rc = host_bfs<E>(s, P.bfs, false))) return rc;
+    LAUNCH(s, (k_emit<<<s->grid_full, NT, 0, s->st>>>(P.base)));
     s->stats.full_passes++;
     CK(cudaGetLastError());
     return 0;
+}
+
+// ---- graph-driven loop (graph = 1): the whole solve is one CUDA graph with
+// conditional while nodes; loop decisions are taken on the device
+// (k_cycle_ctl, last CTA of every sweep) and the host never synchronises
+// mid-solve.
+template <class F, class... Args>
+int add_kernel(cudaGraph_t g, cudaGraphNode_t *prev, dim3 grid, dim3 block, F func, Args... args) {
+    void *ptrs[] = {(void *)&args...};
+    cudaKernelNodeParams kp{};
+    kp.func = (void *)func;
+    kp.gridDim = grid;
+    kp.blockDim = block;
+    kp.kernelParams = ptrs;
+    cudaGraphNode_t n;
+    CK(cudaGraphAddKernelNode(&n, g, *prev ? prev : nullptr, *prev ? 1 : 0, &kp));
+    *prev = n;
+    return 0;
+}
+
+// appends a while node to g (after *prev); returns its body graph
+int add_while(cudaGraph_t g, cudaGraphNode_t *prev, cudaGraphConditionalHandle h, cudaGraph_t *body) {
+    cudaGraphNodeParams p{};
+    p.type = cudaGraphNodeTypeConditional;
+    p.conditional.handle = h;
+    p.conditional.type = cudaGraphCondTypeWhile;
+    p.conditional.size = 1;
+    cudaGraphNode_t n;
+    CK(cudaGraphAddNode(&n, g, *prev ? prev : nullptr, *prev ? 1 : 0, &p));
+    *body = p.conditional.phGraph_out[0];
+    *prev = n;
+    return 0;
+}
+
+template <class E>
+int build_graph(pmf_solver *s, const Ctx &c0, int32_t ngrids, cudaGraph_t *out) {
+    PhaseCtx P = phase_ctx(s, c0);
+    cudaGraph_t g;
+    CK(cudaGraphCreate(&g, 0));
+    *out = g;
+    cudaGraphNode_t prev = nullptr;
+    int rc;
+    const dim3 gfull(s->grid_full), gbfs(s->grid_bfs), gpush(s->grid_push);
+    cudaGraphConditionalHandle h_cycle;
+    CK(cudaGraphConditionalHandleCreate(&h_cycle, g, 1, cudaGraphCondAssignDefault));
+    cudaGraph_t cyc;
+    if ((rc = add_while(g, &prev, h_cycle, &cyc))) return rc;
+    {   // ---- one cycle: exact global relabel, seeding, discharge
+        cudaGraphNode_t q = nullptr;
+        cudaGraphConditionalHandle h_bfs = 0, h_push = 0;
+        if (!P.bfs.persistent) CK(cudaGraphConditionalHandleCreate(&h_bfs, cyc, 0, 0));
+        if ((rc = add_kernel(cyc, &q, gfull, dim3(256), k_phase_begin, P.bfs, int(P.bfs.persistent), h_bfs,
+                             int(!P.bfs.persistent))))
+            return rc;
+        if ((rc = add_kernel(cyc, &q, gfull, dim3(NT), k_gr_init, P.bfs))) return rc;
+        if (P.bfs.persistent) {
+            if ((rc = add_kernel(cyc, &q, gbfs, dim3(NTT), k_bfs_sink<E>, P.bfs, int(K_PERSISTENT), lctl(ST_BFS))))
+                return rc;
+        } else {
+            cudaGraph_t body;
+            if ((rc = add_while(cyc, &q, h_bfs, &body))) return rc;
+            cudaGraphNode_t b = nullptr;
+            if ((rc = add_kernel(body, &b, gbfs, dim3(NTT), k_bfs_sink<E>, P.bfs, int(K_DEVICE),
+                                 lctl(ST_BFS, h_bfs, 1))))
+                return rc;
+        }
+        if (!P.push.persistent) CK(cudaGraphConditionalHandleCreate(&h_push, cyc, 0, 0));
+        if ((rc = add_kernel(cyc, &q, gfull, dim3(256), k_phase_begin, P.push, int(P.push.persistent), h_push,
+                             int(!P.push.persistent))))
+            return rc;
+        if ((rc = add_kernel(cyc, &q, gfull, dim3(NT), k_seed_push, P.push))) return rc;
+        if ((rc = add_kernel(cyc, &q, dim3(1), dim3(1024), k_cycle_ctl, P.push, ngrids, int(P.push.persistent),
+                             unsigned(s->push_budget), int64_t(s->max_cycles), h_cycle, 1)))
+            return rc;
+        if (P.push.persistent) {
+            if ((rc = add_kernel(cyc, &q, gpush, dim3(NTT), k_push<E>, P.pq, int(K_PERSISTENT), s->push_iters,
+                                 s->relabel_every, lctl(ST_PUSH))))
+                return rc;
+        } else {
+            // k_phase_begin armed h_push = 1; an empty list ends the loop
+            // after its first (idle) sweep
+            cudaGraph_t body;
+            if ((rc = add_while(cyc, &q, h_push, &body))) return rc;
+            cudaGraphNode_t b = nullptr;
+            if ((rc = add_kernel(body, &b, gpush, dim3(NTT), k_push<E>, P.push, int(K_DEVICE), s->push_iters,
+                                 s->relabel_every, lctl(ST_PUSH, h_push, 1, s->push_sweeps))))
+                return rc;
+        }
+    }
+    // ---- labels
+    cudaGraphConditionalHandle h_lab = 0;
+    if (!P.bfs.persistent) CK(cudaGraphConditionalHandleCreate(&h_lab, g, 0, 0));
+    if ((rc = add_kernel(g, &prev, gfull, dim3(256), k_phase_begin, P.bfs, int(P.bfs.persistent), h_lab,
+                         int(!P.bfs.persistent))))
+        return rc;
+    if ((rc = add_kernel(g, &prev, gfull, dim3(NT), k_lab_seed, P.bfs))) return rc;
+    if (P.bfs.persistent) {
+        if ((rc = add_kernel(g, &prev, gbfs, dim3(NTT), k_bfs_src<E>, P.bfs, int(K_PERSISTENT), lctl(ST_LAB))))
+            return rc;
+    } else {
+        cudaGraph_t body;
+        if ((rc = add_while(g, &prev, h_lab, &body))) return rc;
+        cudaGraphNode_t b = nullptr;
+        if ((rc = add_kernel(body, &b, gbfs, dim3(NTT), k_bfs_src<E>, P.bfs, int(K_DEVICE), lctl(ST_LAB, h_lab, 1))))
+            return rc;
+    }
+    if ((rc = add_kernel(g, &prev, gfull, dim3(NT), k_emit, P.base))) return rc;
+    return 0;
+}
+
+// knobs + context a cached graph was built for
+struct GraphKey {
+    Ctx ctx;
+    int32_t ngrids, edge, p_push, p_bfs, iters, relabel, budget, sweeps;
+    int64_t maxc;
+    int32_t gfull, gbfs, gpush;
+};
+
+template <class E>
+int graph_solve(pmf_solver *s, const Ctx &c0, int32_t ngrids) {
+    static_assert(sizeof(GraphKey) <= sizeof(pmf_solver::gkey), "graph key buffer too small");
+    GraphKey key;
+    memset(&key, 0, sizeof key);
+    key.ctx = c0;
+    key.ngrids = ngrids;
+    key.edge = E::kBytes;
+    key.p_push = s->persistent;
+    key.p_bfs = s->persistent_bfs;
+    key.iters = s->push_iters;
+    key.relabel = s->relabel_every;
+    key.budget = s->push_budget;
+    key.sweeps = s->push_sweeps;
+    key.maxc = s->max_cycles;
+    key.gfull = s->grid_full;
+    key.gbfs = s->grid_bfs;
+    key.gpush = s->grid_push;
+    if (!s->gexec || memcmp(&key, s->gkey, sizeof key) != 0) {
+        if (s->gexec) cudaGraphExecDestroy(s->gexec);
+        s->gexec = nullptr;
+        cudaGraph_t g = nullptr;
+        int rc = build_graph<E>(s, c0, ngrids, &g);
+        if (rc) {
+            if (g) cudaGraphDestroy(g);
+            return rc;
+        }
+        cudaError_t e = cudaGraphInstantiate(&s->gexec, g, 0);
+        cudaGraphDestroy(g);
+        if (e != cudaSuccess) return fail(PMF_ERR_CUDA, "cudaGraphInstantiate: %s", cudaGetErrorString(e));
+        memcpy(s->gkey, &key, sizeof key);
+        s->stats.graph_builds++;
+    }
+    CK(cudaGraphLaunch(s->gexec, s->st));
+    s->stats.launches++;
+    return 0;
+}
+
+template <class E>
+int run_solve(pmf_solver *s, const Ctx &c0, int32_t ngrids) {
+    CK(cudaMemsetAsync(c0.ctl, 0, sizeof(Ctl), s->st));
+    return s->use_graph ? graph_solve<E>(s, c0, ngrids) : host_solve<E>(s, c0, ngrids);
 }
 
 // Device-side run bracket: always-on events around the whole run give
@@ -379,17 +550,26 @@ int run_end(pmf_solver *s) {
     CK(cudaEventRecord(s->ev_run[1], s->st));
     unsigned long long st[ST_NSTAT];
     int32_t err = 0;
+    Ctl ctl;
     CK(cudaMemcpyAsync(st, s->d_stat.p, sizeof st, cudaMemcpyDeviceToHost, s->st));
     CK(cudaMemcpyAsync(&err, s->d_err.p, 4, cudaMemcpyDeviceToHost, s->st));
+    CK(cudaMemcpyAsync(&ctl, s->d_ctl.p, sizeof ctl, cudaMemcpyDeviceToHost, s->st));
     CK(cudaStreamSynchronize(s->st));
     const Layout &L = s->lay;
     s->stats.push_tile_passes = int64_t(st[ST_PUSH]);
     s->stats.bfs_tile_passes = int64_t(st[ST_BFS]);
     s->stats.label_tile_passes = int64_t(st[ST_LAB]);
+    s->stats.push_sweeps = int64_t(st[ST_PUSH_L]);
+    s->stats.bfs_sweeps = int64_t(st[ST_BFS_L] + st[ST_LAB_L]);
+    s->stats.cycles = ctl.cycle;
     s->stats.grids = int64_t(L.grids.size());
     s->stats.tiles = L.ntiles;
     s->stats.pixels = L.pixels;
     s->stats.edge_bytes = s->edge_bytes;
+    // device-clock spans of the tile kernels (always on, graph or not)
+    s->stats.ms_push = double(st[ST_PUSH_NS]) * 1e-6;
+    s->stats.ms_bfs = double(st[ST_BFS_NS]) * 1e-6;
+    s->stats.ms_labels = double(st[ST_LAB_NS]) * 1e-6;
     float dev = 0;
     cudaEventElapsedTime(&dev, s->ev_run[0], s->ev_run[1]);
     s->stats.ms_device = dev;
@@ -400,18 +580,16 @@ int run_end(pmf_solver *s) {
             cudaEventElapsedTime(&ms, s->ev_pool[s->ev_marks[i].second], s->ev_pool[s->ev_marks[i + 1].second]);
             cat[s->ev_marks[i].first] += ms;
         }
-        float tot = 0;
-        cudaEventElapsedTime(&tot, s->ev_pool[s->ev_marks.front().second], s->ev_pool[s->ev_marks.back().second]);
         s->stats.timed = 1;
-        s->stats.ms_total = tot;
+        s->stats.ms_total = dev;
         s->stats.ms_build = cat[C_BUILD];
-        s->stats.ms_bfs = cat[C_BFS];
-        s->stats.ms_push = cat[C_PUSH];
         s->stats.ms_seed = cat[C_SEED];
-        s->stats.ms_labels = cat[C_LAB];
         s->stats.ms_h2d = cat[C_H2D];
         s->stats.ms_d2h = cat[C_D2H];
     }
+    if (ctl.noconv)
+        return fail(PMF_ERR_NOCONV, "push-relabel failed to converge within %lld cycles",
+                    (long long)s->max_cycles);
     if (err == 4) return fail(PMF_ERR_NONMAX, "source side touches an unsaturated sink edge");
     if (err) return fail(PMF_ERR_CUDA, "device error code %d", err);
     return 0;
@@ -684,6 +862,7 @@ int pmf_solver_destroy(pmf_solver *s) {
     cudaSetDevice(s->device);
     if (s->st) cudaStreamSynchronize(s->st);
     for (auto e : s->ev_pool) cudaEventDestroy(e);
+    if (s->gexec) cudaGraphExecDestroy(s->gexec);
     for (auto e : s->ev_run)
         if (e) cudaEventDestroy(e);
     if (s->st) cudaStreamDestroy(s->st);
@@ -699,6 +878,8 @@ int pmf_solver_set(pmf_solver *s, const char *name, int64_t v) {
     else if (k == "bfs_chunk" && v >= 1 && v <= 100000) s->bfs_chunk = int(v);
     else if (k == "relabel_every" && v >= 0 && v <= 100000) s->relabel_every = int(v);
     else if (k == "persistent") s->persistent = v != 0;
+    else if (k == "graph") s->use_graph = v != 0;
+    else if (k == "persistent_bfs") s->persistent_bfs = v != 0;
     else if (k == "push_budget" && v >= 0) s->push_budget = int(v);
     else if (k == "timing") s->timing = v != 0;
     else if (k == "max_cycles" && v >= 1) s->max_cycles = v;

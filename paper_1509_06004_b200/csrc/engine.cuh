@@ -27,8 +27,37 @@ constexpr int64_t CAP_MAX = int64_t(1) << 30;   // grid.py:19
 enum { DL = 0, DR = 1, DU = 2, DD = 3 };         // grid.py:23 order
 __host__ __device__ constexpr int opp(int d) { return d ^ 1; }
 
-// statistics counters (device, unsigned long long)
-enum { ST_PUSH = 0, ST_BFS = 1, ST_LAB = 2, ST_NSTAT = 4 };
+// statistics counters (device, unsigned long long): tile passes per kernel
+// kind, launches and their device-clock spans (ns, %globaltimer)
+enum {
+    ST_PUSH = 0, ST_BFS = 1, ST_LAB = 2,
+    ST_PUSH_NS = 3, ST_BFS_NS = 4, ST_LAB_NS = 5,
+    ST_PUSH_L = 6, ST_BFS_L = 7, ST_LAB_L = 8,
+    ST_NSTAT = 16
+};
+
+// sweep index convention of the list-driven tile kernels
+constexpr int K_PERSISTENT = -1;   // one launch drains the device queue
+constexpr int K_DEVICE = -2;       // sweep index lives in Ctl (graph-driven loop)
+
+// Device-side control block of a solve (graph-driven mode keeps all loop
+// state here; the host never reads it mid-solve).
+struct Ctl {
+    int32_t k;              // sweep index of the current list phase
+    uint32_t done;          // CTAs finished in the current launch
+    int32_t cycle;          // global relabel cycles so far
+    uint32_t budget;        // pop budget of the next persistent discharge
+    int32_t nact;           // tiles seeded for discharge this cycle
+    int32_t noconv;         // non-convergence guard tripped
+    unsigned long long t0;  // earliest CTA start of the current launch (ns)
+    unsigned long long t1;  // latest CTA end of the current launch (ns)
+};
+
+__device__ __forceinline__ unsigned long long gtimer() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
 
 struct GridDesc {
     int32_t W, H, ntx, nty;
@@ -67,6 +96,8 @@ struct Ctx {
     int32_t qcap;
     int32_t persistent;     // seed kernels feed the queue (1) or list 0 (0)
     unsigned int budget;    // max tile pops of a persistent phase (0 = none)
+    Ctl *ctl;               // device control block
+    int32_t budget_dev;     // persistent discharge reads its budget from ctl
 };
 
 enum { Q_IDLE = 0, Q_QUEUED = 1, Q_RUNNING = 2, Q_DIRTY = 3 };
@@ -135,8 +166,11 @@ __device__ __forceinline__ void q_finish(const Ctx &c, int32_t t, bool again) {
 // Thread 0 of a persistent CTA: next tile to process, or -1 when the phase
 // is over (queue drained with nothing running, or pop budget spent).
 __device__ __forceinline__ int32_t q_next(const Ctx &c) {
+    // device budget: 0 means "no discharge this cycle"; host budget 0: no cap
+    const unsigned budget = c.budget_dev ? *(volatile unsigned *)&c.ctl->budget : c.budget;
+    if (c.budget_dev && budget == 0) return -1;
     for (;;) {
-        if (c.budget && ld_volatile(&c.qctr[QC_POPS]) >= c.budget) return -1;
+        if (budget && ld_volatile(&c.qctr[QC_POPS]) >= budget) return -1;
         int32_t t = q_pop(c);
         if (t >= 0) {
             atomicAdd(&c.qctr[QC_POPS], 1u);

@@ -231,11 +231,59 @@ __global__ void __launch_bounds__(NT) k_seed_push(Ctx c) {
     }
 }
 
-__global__ void k_update_live(Ctx c, int32_t ngrids) {
-    int g = blockIdx.x * blockDim.x + threadIdx.x;
-    if (g >= ngrids) return;
-    if (c.live[g] && c.act[g] == 0) c.live[g] = 0;
-    c.act[g] = 0;
+// Reset the worklist (sweep mode) or queue (persistent mode) state for a
+// new phase and, in graph mode, arm the conditional of the loop that
+// follows.  Replaces host memsets so the whole solve can run as one graph.
+__global__ void k_phase_begin(Ctx c, int persistent, cudaGraphConditionalHandle cond, int has_cond) {
+    const int64_t tid = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
+    const int64_t stride = int64_t(gridDim.x) * blockDim.x;
+    for (int64_t t = tid; t < c.ntiles; t += stride) {
+        if (persistent) {
+            c.qstate[t] = Q_IDLE;
+            c.ring[t] = -1;
+        } else {
+            c.inq0[t] = 0;
+            c.inq1[t] = 0;
+        }
+    }
+    if (tid == 0) {
+        c.cnt[0] = c.cnt[1] = c.cnt[2] = 0;
+        for (int q = 0; q < 4; q++) c.qctr[q] = 0;
+        c.ctl->k = 0;
+        c.ctl->done = 0;
+        c.ctl->t0 = ~0ull;
+        c.ctl->t1 = 0;
+        if (has_cond) cudaGraphSetConditional(cond, 1u);
+    }
+}
+
+// End of a seeding pass (one CTA): retire grids without active pixels,
+// record how many tiles were seeded, size the next discharge's pop budget,
+// count the cycle and decide (graph mode: via the cycle loop's conditional)
+// whether another discharge + global relabel round is needed.
+__global__ void __launch_bounds__(1024) k_cycle_ctl(Ctx c, int32_t ngrids, int persistent,
+                                                    unsigned budget_factor, int64_t max_cycles,
+                                                    cudaGraphConditionalHandle cond, int has_cond) {
+    for (int g = threadIdx.x; g < ngrids; g += blockDim.x) {
+        if (c.live[g] && c.act[g] == 0) c.live[g] = 0;
+        c.act[g] = 0;
+    }
+    if (threadIdx.x == 0) {
+        Ctl *ctl = c.ctl;
+        int32_t nact = persistent ? int32_t(c.qctr[QC_PENDING]) : c.cnt[0];
+        int32_t cyc = ++ctl->cycle;
+        int stop = nact == 0;
+        if (!stop && cyc > max_cycles) {
+            ctl->noconv = 1;
+            stop = 1;
+        }
+        ctl->nact = nact;
+        // pop budget of the discharge that follows (0 = run none)
+        uint64_t cap = uint64_t(64) * uint64_t(c.ntiles) + 1024;
+        uint64_t want = budget_factor ? uint64_t(budget_factor) * uint64_t(nact) + 64 : cap;
+        ctl->budget = stop ? 0u : unsigned(want < cap ? want : cap);
+        if (has_cond) cudaGraphSetConditional(cond, stop ? 0u : 1u);
+    }
 }
 
 // ---------------------------------------------------------------------------

@@ -91,21 +91,76 @@ struct TileResult {
     int out;     // bit s: the neighbour on side s needs (re)processing
 };
 
-// Outer loop shared by the tile kernels.  Sweep mode (k >= 0): walk
-// worklist k once, list follow-up tiles in worklist k + 1 (one launch per
-// sweep).  Persistent mode (k < 0): pop tiles from the device queue until
-// the phase drains (or its pop budget is spent); follow-up tiles are queued
-// and picked up by whichever CTA is free, without a kernel boundary.
+// Per-launch bookkeeping shared by all CTAs of a tile kernel: device-clock
+// span of the launch (earliest CTA start .. latest CTA end, %globaltimer) and,
+// in graph-driven mode, the advance of the sweep index plus the decision
+// whether the enclosing conditional while node runs another sweep.
+struct LaunchCtl {
+    int stat;                         // ST_PUSH / ST_BFS / ST_LAB
+    cudaGraphConditionalHandle cond;  // loop condition to set (graph mode)
+    int has_cond;
+    int max_k;                        // stop the loop after this many sweeps (0 = no cap)
+};
+
+__device__ __forceinline__ void launch_enter(const Ctx &c) {
+    if (threadIdx.x == 0) atomicMin(&c.ctl->t0, gtimer());
+}
+
+// Called by thread 0 of each of the `parts` participating CTAs when it
+// leaves the kernel (sweep mode: only CTAs that received a tile take part,
+// the rest exit without touching the control block).  k_next is the sweep
+// index that follows (K_DEVICE mode) or -1.
+__device__ __forceinline__ void launch_exit(const Ctx &c, const LaunchCtl &lc, int k_next,
+                                            unsigned parts) {
+    atomicMax(&c.ctl->t1, gtimer());
+    __threadfence();
+    if (atomicAdd(&c.ctl->done, 1u) != parts - 1) return;
+    // last CTA of the launch
+    __threadfence();
+    Ctl *ctl = c.ctl;
+    unsigned long long t0 = *(volatile unsigned long long *)&ctl->t0;
+    unsigned long long t1 = *(volatile unsigned long long *)&ctl->t1;
+    atomicAdd(&c.stat[ST_PUSH_NS + lc.stat], t1 > t0 ? t1 - t0 : 0ull);
+    atomicAdd(&c.stat[ST_PUSH_L + lc.stat], 1ull);
+    ctl->t0 = ~0ull;
+    ctl->t1 = 0;
+    ctl->done = 0;
+    if (k_next >= 0) {
+        int next = *(volatile int32_t *)&c.cnt[k_next % 3];
+        ctl->k = k_next;
+        if (lc.has_cond)
+            cudaGraphSetConditional(lc.cond, (next > 0 && (lc.max_k == 0 || k_next < lc.max_k)) ? 1u : 0u);
+    }
+}
+
+// Outer loop shared by the tile kernels.
+//  * sweep mode (k >= 0, or K_DEVICE with k read from the control block):
+//    walk worklist k once, list follow-up tiles in worklist k + 1;
+//  * persistent mode (K_PERSISTENT): pop tiles from the device queue until
+//    the phase drains (or its pop budget is spent); follow-up tiles are
+//    queued and picked up by whichever CTA is free, with no kernel boundary.
 template <class Body>
-__device__ __forceinline__ void tile_loop(const Ctx &c, int k, int stat, Body &&body) {
-    __shared__ int32_t s_t;
+__device__ __forceinline__ void tile_loop(const Ctx &c, int k, const LaunchCtl &lc, Body &&body) {
+    __shared__ int32_t s_t, s_n;
     const int i = threadIdx.x;
-    if (k >= 0) {
-        const int32_t n = c.cnt[k % 3];
+    if (k != K_PERSISTENT) {
+        if (i == 0) {
+            if (k == K_DEVICE) k = *(volatile int32_t *)&c.ctl->k;
+            s_t = k;
+            s_n = *(volatile int32_t *)&c.cnt[k % 3];
+        }
+        __syncthreads();
+        k = s_t;
+        const int32_t n = s_n;
+        // CTAs without a tile leave at once; the others (or block 0 when
+        // the list is empty) do the launch bookkeeping
+        const unsigned parts = unsigned(max(1, min(n, int32_t(gridDim.x))));
+        if (blockIdx.x >= parts) return;
+        launch_enter(c);
         const int32_t *lst = list_of(c, k);
         if (blockIdx.x == 0 && i == 0) {
             c.cnt[(k + 2) % 3] = 0;
-            atomicAdd(&c.stat[stat], (unsigned long long)n);
+            atomicAdd(&c.stat[lc.stat], (unsigned long long)n);
         }
         for (int li = blockIdx.x; li < n; li += gridDim.x) {
             const int32_t t = lst[li];
@@ -119,15 +174,16 @@ __device__ __forceinline__ void tile_loop(const Ctx &c, int k, int stat, Body &&
             }
             __syncthreads();
         }
+        if (i == 0) launch_exit(c, lc, k + 1, parts);
         return;
     }
+    launch_enter(c);
     // Hand-off ordering (store-buffering pattern): a requester writes tile
     // data, then reads the neighbour's queue state; a popper writes the
     // state, then reads the data.  Each side needs a gpu-scope SC fence
-    // between its write and its read in EVERY participating thread, i.e.
-    // on both sides of the CTA barrier that separates writer threads from
-    // thread 0 -- otherwise a "still queued" read can pair with a stale
-    // data read and a propagation step is lost.
+    // between its write and its read in every participating thread, i.e.
+    // on both sides of the CTA barrier that separates the data threads from
+    // thread 0.
     for (;;) {
         if (i == 0) {
             int32_t t = q_next(c);
@@ -136,7 +192,7 @@ __device__ __forceinline__ void tile_loop(const Ctx &c, int k, int stat, Body &&
         }
         __syncthreads();
         const int32_t t = s_t;
-        if (t < 0) return;
+        if (t < 0) break;
         __threadfence();              // popper side: state write < data reads
         TileResult r = body(t);
         __threadfence();              // requester side: data writes < ...
@@ -147,9 +203,10 @@ __device__ __forceinline__ void tile_loop(const Ctx &c, int k, int stat, Body &&
             for (int sd = 0; sd < 4; sd++)
                 if ((r.out >> sd) & 1 && g.nb[sd] >= 0) q_request(c, g.nb[sd]);
             q_finish(c, t, r.again != 0);
-            atomicAdd(&c.stat[stat], 1ull);
+            atomicAdd(&c.stat[lc.stat], 1ull);
         }
     }
+    if (i == 0) launch_exit(c, lc, -1, gridDim.x);
 }
 
 // ---------------------------------------------------------------------------
@@ -164,13 +221,13 @@ __device__ __forceinline__ int border_sides(int lx, int ly) {
 }
 
 template <class E>
-__global__ void __launch_bounds__(NTT, 2) k_bfs_sink(Ctx c, int k) {
+__global__ void __launch_bounds__(NTT, 2) k_bfs_sink(Ctx c, int k, LaunchCtl lc) {
     __shared__ int32_t sd[TH * SP];
     __shared__ uint8_t sm[TPIX];
     __shared__ int32_t hv[4][TW];
     __shared__ int s_side;
     const int i = threadIdx.x, lx = i & 31, ly = i >> 5;
-    tile_loop(c, k, ST_BFS, [&](int32_t t) -> TileResult {
+    tile_loop(c, k, lc, [&](int32_t t) -> TileResult {
         TileGeo g = tile_geo(c, t);
         const int64_t p = int64_t(t) * TPIX + i;
         const int32_t h0 = __ldcg(c.h + p);
@@ -202,14 +259,14 @@ __global__ void __launch_bounds__(NTT, 2) k_bfs_sink(Ctx c, int k) {
 // not maximal (NonMaximalFlowError).
 // ---------------------------------------------------------------------------
 template <class E>
-__global__ void __launch_bounds__(NTT, 2) k_bfs_src(Ctx c, int k) {
+__global__ void __launch_bounds__(NTT, 2) k_bfs_src(Ctx c, int k, LaunchCtl lc) {
     __shared__ int32_t sd[TH * SP];
     __shared__ uint8_t sbits[TPIX];    // own outgoing "arc > 0" bits
     __shared__ uint8_t sm[TPIX];       // pull mask: incoming arcs
     __shared__ int32_t hv[4][TW];
     __shared__ int s_side;
     const int i = threadIdx.x, lx = i & 31, ly = i >> 5;
-    tile_loop(c, k, ST_LAB, [&](int32_t t) -> TileResult {
+    tile_loop(c, k, lc, [&](int32_t t) -> TileResult {
         TileGeo g = tile_geo(c, t);
         const int64_t p = int64_t(t) * TPIX + i;
         const uint8_t l0 = __ldcg(c.lab + p);
@@ -267,7 +324,7 @@ __global__ void __launch_bounds__(NTT, 2) k_bfs_src(Ctx c, int k) {
 // in frozen pixels, a certificate that the pixel cannot reach the sink.
 // ---------------------------------------------------------------------------
 template <class E>
-__global__ void __launch_bounds__(NTT, 2) k_push(Ctx c, int k, int iters, int relabel_every) {
+__global__ void __launch_bounds__(NTT, 2) k_push(Ctx c, int k, int iters, int relabel_every, LaunchCtl lc) {
     __shared__ int32_t sh[TH * SP];
     __shared__ int32_t sd[TH * SP];
     __shared__ int32_t sin4[4][TPIX];
@@ -280,7 +337,7 @@ __global__ void __launch_bounds__(NTT, 2) k_push(Ctx c, int k, int iters, int re
                         ly > 0 ? pi - SP : -1, ly < TH - 1 ? pi + SP : -1};
     const int nbt[4] = {i - 1, i + 1, i - TW, i + TW};   // neighbour's flat tile index
     const int hpos[4] = {ly, ly, lx, lx};                 // index into halo arrays
-    tile_loop(c, k, ST_PUSH, [&](int32_t t) -> TileResult {
+    tile_loop(c, k, lc, [&](int32_t t) -> TileResult {
         TileGeo g = tile_geo(c, t);
         const int64_t p = int64_t(t) * TPIX + i;
         const int32_t w0 = __ldcg(c.w + p);

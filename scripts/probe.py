@@ -30,28 +30,35 @@ def main():
     ap.add_argument("--relabel", type=int, default=None)
     ap.add_argument("--persistent", type=int, default=None)
     ap.add_argument("--budget", type=int, default=None)
+    ap.add_argument("--pbfs", type=int, default=None)
+    ap.add_argument("--graph", type=int, default=None)
     ap.add_argument("--reps", type=int, default=3)
     ap.add_argument("--nprob", type=int, default=None, help="problems per device batch")
     a = ap.parse_args()
     c = CFG[a.cfg]
     b = synth.generate(c["w"], c["h"], c["rows"], c["cols"], rng_seed=0, types=c["types"])
     probs = b.problems if a.nprob is None else b.problems[:a.nprob]
-    s = _native.Solver(0, timing=1)
+    s = _native.Solver(0)
     if a.iters: s.set("push_iters", a.iters)
     if a.sweeps: s.set("push_sweeps", a.sweeps)
     if a.chunk: s.set("bfs_chunk", a.chunk)
     if a.relabel is not None: s.set("relabel_every", a.relabel)
     if a.persistent is not None: s.set("persistent", a.persistent)
     if a.budget is not None: s.set("push_budget", a.budget)
+    if a.pbfs is not None: s.set("persistent_bfs", a.pbfs)
+    if a.graph is not None: s.set("graph", a.graph)
     for r in range(a.reps):
         t0 = time.perf_counter()
         sw, flows, labels = s.solve_seed_batch(c["w"], c["h"], probs, c["lams"], "auto")
         dt = time.perf_counter() - t0
         st = s.stats()
         cuts = flows.size
-        print(json.dumps(dict(cfg=a.cfg, rep=r, wall_ms=round(dt * 1e3, 2), cuts=cuts,
-                              cuts_per_s=round(cuts / dt, 1), flow=int(flows.sum()),
-                              **{k: (round(v, 3) if isinstance(v, float) else v) for k, v in st.items()})))
+        keep = ("cycles", "push_tile_passes", "bfs_tile_passes", "label_tile_passes", "push_sweeps",
+                "bfs_sweeps", "ms_device", "ms_push", "ms_bfs", "ms_labels", "launches", "graph_builds")
+        print(json.dumps(dict(cfg=a.cfg, args=" ".join(sys.argv[2:]), rep=r,
+                              wall_ms=round(dt * 1e3, 2), cuts_per_s=round(cuts / dt, 1),
+                              flow=int(flows.sum()),
+                              **{k: (round(st[k], 3) if isinstance(st[k], float) else st[k]) for k in keep})))
 
 
 if __name__ == "__main__":
