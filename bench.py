@@ -342,7 +342,7 @@ def run_b200(args, cfg):
                          "time_share": share},
             "cpu_baseline": cpu,
             "clocks": clk.summary(),
-            "gpu_launches": int(sum(s["launches"] for s in stats)),
+            "gpu_launches": int(sum(s["kernels"] for s in stats)),
             "solver": {k: stats[-1][k] for k in ("cycles", "push_sweeps", "push_tile_passes",
                                                   "bfs_sweeps", "bfs_tile_passes", "tiles",
                                                   "edge_bytes")},

@@ -72,10 +72,11 @@ typedef struct pmf_stats {
     double ms_h2d;              /* host->device copies                        */
     double ms_d2h;              /* device->host copies                        */
     double ms_device;           /* device time of the last run (always on)    */
-    int64_t launches;           /* kernels launched by the last run           */
+    int64_t launches;           /* host-side launches (kernels + graphs)      */
     int64_t h2d_bytes;          /* host->device bytes of the last stage       */
     int64_t d2h_bytes;          /* device->host bytes of the last fetch       */
     int64_t graph_builds;       /* solve graphs (re)built by the last run     */
+    int64_t kernels;            /* kernels executed on the device by the run  */
 } pmf_stats;
 
 /* Create / destroy a solver bound to one CUDA device and its own stream. */
@@ -161,6 +162,11 @@ int pmf_seed_stage(pmf_solver *s, int32_t nprob, int32_t width, int32_t height,
                    int32_t nlam, const int64_t *lambdas, int32_t swap_mode);
 int pmf_seed_run(pmf_solver *s);
 int pmf_seed_fetch(pmf_solver *s, uint8_t *swapped_out, int64_t *flows_out, uint8_t *labels_out);
+
+/* Diagnostics: the first (up to *n, at most 64) tile-kernel launches of the
+ * last run: kind (0 discharge, 1 sink BFS, 2 label BFS), device span in us,
+ * tile passes.  *n is updated to the number returned. */
+int pmf_debug_trace(pmf_solver *s, int32_t *kind, double *us, int64_t *tiles, int32_t *n);
 
 /* Diagnostics: copy the tile-major device state of the last run (w, h,
  * residual words, source-side flags; any pointer may be NULL) and the tile

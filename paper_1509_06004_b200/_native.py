@@ -16,14 +16,15 @@ import threading
 import numpy as np
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libpmflow_b200.so")
+LIB_PATH = os.environ.get("PMF_LIB") or os.path.join(HERE, "libpmflow_b200.so")
 
 PMF_OK, PMF_ERR_ARG, PMF_ERR_CUDA, PMF_ERR_NOCONV, PMF_ERR_NONMAX, PMF_ERR_RANGE = 0, -1, -2, -3, -4, -5
 SWAP_MODES = {"auto": 0, "on": 1, "off": 2}
 
 EXPORTS = ("pmf_solver_create", "pmf_solver_destroy", "pmf_solver_set", "pmf_last_error",
            "pmf_solver_stats", "pmf_solver_stream", "pmf_solve_composites", "pmf_solve_seed_batch",
-           "pmf_seed_stage", "pmf_seed_run", "pmf_seed_fetch", "pmf_debug_state")
+           "pmf_seed_stage", "pmf_seed_run", "pmf_seed_fetch", "pmf_debug_state",
+           "pmf_debug_trace")
 
 
 class NativeUnavailable(RuntimeError):
@@ -37,7 +38,8 @@ class PmfStats(ctypes.Structure):
         ("edge_bytes", ctypes.c_int32), ("timed", ctypes.c_int32)] + [
         (k, ctypes.c_double) for k in ("ms_total", "ms_build", "ms_push", "ms_bfs", "ms_labels",
                                        "ms_seed", "ms_h2d", "ms_d2h", "ms_device")] + [
-        (k, ctypes.c_int64) for k in ("launches", "h2d_bytes", "d2h_bytes", "graph_builds")]
+        (k, ctypes.c_int64) for k in ("launches", "h2d_bytes", "d2h_bytes", "graph_builds",
+                                       "kernels")]
 
     def as_dict(self):
         return {k: getattr(self, k) for k, _ in self._fields_}
@@ -78,6 +80,7 @@ def load_library(path: str = LIB_PATH):
         lib.pmf_seed_fetch.argtypes = [vp, P(u8), P(i64), P(u8)]
         lib.pmf_solver_stream.argtypes = [vp, P(vp)]
         lib.pmf_debug_state.argtypes = [vp, vp, vp, vp, vp, P(i64)]
+        lib.pmf_debug_trace.argtypes = [vp, vp, vp, vp, P(i32)]
         for name in EXPORTS:
             if name != "pmf_last_error":
                 getattr(lib, name).restype = ctypes.c_int
@@ -186,6 +189,17 @@ class Solver:
         if rc:
             _raise_for(rc)
         return w, h, r, lab
+
+    def trace(self):
+        """[(kind, us, tile_passes)] of the first tile-kernel launches of the
+        last run (kind: 0 discharge, 1 sink BFS, 2 label BFS)."""
+        n = ctypes.c_int32(64)
+        kind = np.zeros(64, np.int32)
+        us = np.zeros(64, np.float64)
+        tiles = np.zeros(64, np.int64)
+        self._lib.pmf_debug_trace(self._h, kind.ctypes.data, us.ctypes.data, tiles.ctypes.data,
+                                  ctypes.byref(n))
+        return [(int(kind[i]), round(float(us[i]), 1), int(tiles[i])) for i in range(n.value)]
 
     def stream_handle(self) -> int:
         """The solver's cudaStream_t as an integer (torch.cuda.ExternalStream)."""

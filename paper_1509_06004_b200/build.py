@@ -15,7 +15,7 @@ OUT = os.path.join(HERE, "libpmflow_b200.so")
 SOURCES = ["engine.cu"]
 DEPS = SOURCES + ["engine.cuh", "kernels.cuh"]
 NVCC_FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
-              "-Xcompiler", "-fPIC,-O2", "-shared", "--expt-relaxed-constexpr"]
+              "-Xcompiler", "-fPIC,-O2,-fopenmp", "-shared", "--expt-relaxed-constexpr", "-lgomp"]
 
 
 def nvcc():

@@ -7,16 +7,22 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <atomic>
+#include <condition_variable>
 #include <cstdarg>
 #include <cstdio>
 #include <cstring>
+#include <functional>
+#include <mutex>
 #include <string>
+#include <thread>
 #include <unordered_map>
 #include <vector>
 
 #include "../../include/pmflow_b200.h"
 #include "kernels.cuh"
 #include "tile.cuh"
+#include "warp.cuh"
 
 using namespace pmf;
 
@@ -81,6 +87,43 @@ enum Cat { C_BUILD = 0, C_BFS, C_PUSH, C_SEED, C_LAB, C_H2D, C_D2H, C_N };
 
 inline int64_t cdiv(int64_t a, int64_t b) { return (a + b - 1) / b; }
 
+// Host-side parallel loops (OpenMP) for the conversion / validation of the
+// input planes and the copy-out of label masks: the host side of the e2e
+// path is memory-bound int64 -> int32 narrowing that one thread cannot
+// keep up with.
+struct Pool {
+    int threads = 1;
+    // fn(i) for i in [0, n)
+    template <class F>
+    void run(int64_t n, F &&fn) {
+        if (n <= 0) return;
+        const int nt = int(std::min<int64_t>(threads, n));
+#pragma omp parallel for schedule(dynamic, 1) num_threads(nt)
+        for (int64_t i = 0; i < n; i++) fn(i);
+    }
+};
+
+// first error raised by a parallel task (others keep running, result dropped)
+struct TaskErr {
+    std::atomic<int> code{0};
+    std::mutex mu;
+    std::string msg;
+    void set(int c, const std::string &m) {
+        int z = 0;
+        if (code.compare_exchange_strong(z, c)) {
+            std::lock_guard<std::mutex> g(mu);
+            msg = m;
+        }
+    }
+    int raise() {
+        if (!code.load()) return 0;
+        std::lock_guard<std::mutex> g(mu);
+        return fail(code.load(), "%s", msg.c_str());
+    }
+};
+
+constexpr int64_t kChunk = 1 << 16;   // elements per host task
+
 
 struct Layout {
     std::vector<GridDesc> grids;
@@ -133,6 +176,9 @@ struct pmf_solver {
     int push_iters = 16;
     int push_sweeps = 64;
     int relabel_every = 8;
+    int warp = 0;             // 1: warp-per-tile kernels (0: 1024-thread CTA per tile)
+    int grid_wpush = 0, grid_wbfs = 0;
+    size_t smem_w = 0;
     int persistent = 1;       // discharge phase as one persistent launch
     int persistent_bfs = 0;   // BFS phases as one persistent launch
     int push_budget = 2;      // persistent push phase: pops <= budget * seeded tiles
@@ -156,6 +202,7 @@ struct pmf_solver {
     cudaEvent_t ev_run[2] = {nullptr, nullptr};
     pmf_stats stats{};
     int edge_bytes = 4;
+    Pool *pool = nullptr;
     int use_graph = 1;                 // whole solve as one CUDA graph
     cudaGraphExec_t gexec = nullptr;   // cached instantiated solve graph
     unsigned char gkey[512] = {0};     // GraphKey it was built for
@@ -295,22 +342,40 @@ PhaseCtx phase_ctx(pmf_solver *s, const Ctx &c0) {
     return p;
 }
 
+// ---- tile-kernel launchers: warp-per-tile kernels (default) or the
+// 1024-thread-CTA kernels
+template <class E>
+void launch_bfs(pmf_solver *s, const Ctx &c, bool sink, int k) {
+    if (s->warp) {
+        if (sink) LAUNCH(s, (k_wbfs_sink<E><<<s->grid_wbfs, WPB * 32, s->smem_w, s->st>>>(c, k, lctl(ST_BFS))));
+        else LAUNCH(s, (k_wbfs_src<E><<<s->grid_wbfs, WPB * 32, s->smem_w, s->st>>>(c, k, lctl(ST_LAB))));
+    } else {
+        if (sink) LAUNCH(s, (k_bfs_sink<E><<<s->grid_bfs, NTT, 0, s->st>>>(c, k, lctl(ST_BFS))));
+        else LAUNCH(s, (k_bfs_src<E><<<s->grid_bfs, NTT, 0, s->st>>>(c, k, lctl(ST_LAB))));
+    }
+}
+
+template <class E>
+void launch_push(pmf_solver *s, const Ctx &c, int k) {
+    if (s->warp)
+        LAUNCH(s, (k_wpush<E><<<s->grid_wpush, WPB * 32, s->smem_w, s->st>>>(c, k, s->push_iters, s->relabel_every,
+                                                                            lctl(ST_PUSH))));
+    else
+        LAUNCH(s, (k_push<E><<<s->grid_push, NTT, 0, s->st>>>(c, k, s->push_iters, s->relabel_every, lctl(ST_PUSH))));
+}
+
 // ---- host-driven loop (graph = 0): the host reads worklist lengths and the
 // control block between phases
 template <class E>
 int host_bfs(pmf_solver *s, const Ctx &c, bool sink) {
     if (c.persistent) {   // one launch; the queue drains on the device
-        if (sink) LAUNCH(s, (k_bfs_sink<E><<<s->grid_bfs, NTT, 0, s->st>>>(c, K_PERSISTENT, lctl(ST_BFS))));
-        else LAUNCH(s, (k_bfs_src<E><<<s->grid_bfs, NTT, 0, s->st>>>(c, K_PERSISTENT, lctl(ST_LAB))));
+        launch_bfs<E>(s, c, sink, K_PERSISTENT);
         CK(cudaGetLastError());
         return 0;
     }
     int k = 0;
     for (;;) {
-        for (int j = 0; j < s->bfs_chunk; j++, k++) {
-            if (sink) LAUNCH(s, (k_bfs_sink<E><<<s->grid_bfs, NTT, 0, s->st>>>(c, k, lctl(ST_BFS))));
-            else LAUNCH(s, (k_bfs_src<E><<<s->grid_bfs, NTT, 0, s->st>>>(c, k, lctl(ST_LAB))));
-        }
+        for (int j = 0; j < s->bfs_chunk; j++, k++) launch_bfs<E>(s, c, sink, k);
         CK(cudaGetLastError());
         int32_t left = 0;
         int rc = read_count(s, c, k % 3, &left);
@@ -346,17 +411,14 @@ int host_solve(pmf_solver *s, const Ctx &c0, int32_t ngrids) {
         if (ctl.nact == 0) break;
         s->tmark(C_PUSH);
         if (P.push.persistent) {
-            LAUNCH(s, (k_push<E><<<s->grid_push, NTT, 0, s->st>>>(P.pq, K_PERSISTENT, s->push_iters,
-                                                                  s->relabel_every, lctl(ST_PUSH))));
+            launch_push<E>(s, P.pq, K_PERSISTENT);
             CK(cudaGetLastError());
             continue;
         }
         // discharge until no tile is listed (or the per-cycle sweep cap)
         for (int k = 0; k < s->push_sweeps;) {
             int chunk = std::min(s->bfs_chunk, s->push_sweeps - k);
-            for (int j = 0; j < chunk; j++, k++)
-                LAUNCH(s, (k_push<E><<<s->grid_push, NTT, 0, s->st>>>(P.push, k, s->push_iters,
-                                                                      s->relabel_every, lctl(ST_PUSH))));
+            for (int j = 0; j < chunk; j++, k++) launch_push<E>(s, P.push, k);
             CK(cudaGetLastError());
             int32_t left = 0;
             if ((rc = read_count(s, P.push, k % 3, &left))) return rc;
@@ -379,6 +441,22 @@ int host_solve(pmf_solver *s, const Ctx &c0, int32_t ngrids) {
 // conditional while nodes; loop decisions are taken on the device
 // (k_cycle_ctl, last CTA of every sweep) and the host never synchronises
 // mid-solve.
+template <class F, class... Args>
+int add_kernel_smem(cudaGraph_t g, cudaGraphNode_t *prev, dim3 grid, dim3 block, size_t smem, F func,
+                    Args... args) {
+    void *ptrs[] = {(void *)&args...};
+    cudaKernelNodeParams kp{};
+    kp.func = (void *)func;
+    kp.gridDim = grid;
+    kp.blockDim = block;
+    kp.sharedMemBytes = unsigned(smem);
+    kp.kernelParams = ptrs;
+    cudaGraphNode_t n;
+    CK(cudaGraphAddKernelNode(&n, g, *prev ? prev : nullptr, *prev ? 1 : 0, &kp));
+    *prev = n;
+    return 0;
+}
+
 template <class F, class... Args>
 int add_kernel(cudaGraph_t g, cudaGraphNode_t *prev, dim3 grid, dim3 block, F func, Args... args) {
     void *ptrs[] = {(void *)&args...};
@@ -408,6 +486,26 @@ int add_while(cudaGraph_t g, cudaGraphNode_t *prev, cudaGraphConditionalHandle h
 }
 
 template <class E>
+int add_bfs_node(pmf_solver *s, cudaGraph_t g, cudaGraphNode_t *prev, bool sink, const Ctx &c, int k,
+                 LaunchCtl lc) {
+    if (s->warp) {
+        if (sink)
+            return add_kernel_smem(g, prev, dim3(s->grid_wbfs), dim3(WPB * 32), s->smem_w, k_wbfs_sink<E>, c, k, lc);
+        return add_kernel_smem(g, prev, dim3(s->grid_wbfs), dim3(WPB * 32), s->smem_w, k_wbfs_src<E>, c, k, lc);
+    }
+    if (sink) return add_kernel(g, prev, dim3(s->grid_bfs), dim3(NTT), k_bfs_sink<E>, c, k, lc);
+    return add_kernel(g, prev, dim3(s->grid_bfs), dim3(NTT), k_bfs_src<E>, c, k, lc);
+}
+
+template <class E>
+int add_push_node(pmf_solver *s, cudaGraph_t g, cudaGraphNode_t *prev, const Ctx &c, int k, LaunchCtl lc) {
+    if (s->warp)
+        return add_kernel_smem(g, prev, dim3(s->grid_wpush), dim3(WPB * 32), s->smem_w, k_wpush<E>, c, k,
+                               s->push_iters, s->relabel_every, lc);
+    return add_kernel(g, prev, dim3(s->grid_push), dim3(NTT), k_push<E>, c, k, s->push_iters, s->relabel_every, lc);
+}
+
+template <class E>
 int build_graph(pmf_solver *s, const Ctx &c0, int32_t ngrids, cudaGraph_t *out) {
     PhaseCtx P = phase_ctx(s, c0);
     cudaGraph_t g;
@@ -429,15 +527,12 @@ int build_graph(pmf_solver *s, const Ctx &c0, int32_t ngrids, cudaGraph_t *out) 
             return rc;
         if ((rc = add_kernel(cyc, &q, gfull, dim3(NT), k_gr_init, P.bfs))) return rc;
         if (P.bfs.persistent) {
-            if ((rc = add_kernel(cyc, &q, gbfs, dim3(NTT), k_bfs_sink<E>, P.bfs, int(K_PERSISTENT), lctl(ST_BFS))))
-                return rc;
+            if ((rc = add_bfs_node<E>(s, cyc, &q, true, P.bfs, K_PERSISTENT, lctl(ST_BFS)))) return rc;
         } else {
             cudaGraph_t body;
             if ((rc = add_while(cyc, &q, h_bfs, &body))) return rc;
             cudaGraphNode_t b = nullptr;
-            if ((rc = add_kernel(body, &b, gbfs, dim3(NTT), k_bfs_sink<E>, P.bfs, int(K_DEVICE),
-                                 lctl(ST_BFS, h_bfs, 1))))
-                return rc;
+            if ((rc = add_bfs_node<E>(s, body, &b, true, P.bfs, K_DEVICE, lctl(ST_BFS, h_bfs, 1)))) return rc;
         }
         if (!P.push.persistent) CK(cudaGraphConditionalHandleCreate(&h_push, cyc, 0, 0));
         if ((rc = add_kernel(cyc, &q, gfull, dim3(256), k_phase_begin, P.push, int(P.push.persistent), h_push,
@@ -448,17 +543,14 @@ int build_graph(pmf_solver *s, const Ctx &c0, int32_t ngrids, cudaGraph_t *out) 
                              unsigned(s->push_budget), int64_t(s->max_cycles), h_cycle, 1)))
             return rc;
         if (P.push.persistent) {
-            if ((rc = add_kernel(cyc, &q, gpush, dim3(NTT), k_push<E>, P.pq, int(K_PERSISTENT), s->push_iters,
-                                 s->relabel_every, lctl(ST_PUSH))))
-                return rc;
+            if ((rc = add_push_node<E>(s, cyc, &q, P.pq, K_PERSISTENT, lctl(ST_PUSH)))) return rc;
         } else {
             // k_phase_begin armed h_push = 1; an empty list ends the loop
             // after its first (idle) sweep
             cudaGraph_t body;
             if ((rc = add_while(cyc, &q, h_push, &body))) return rc;
             cudaGraphNode_t b = nullptr;
-            if ((rc = add_kernel(body, &b, gpush, dim3(NTT), k_push<E>, P.push, int(K_DEVICE), s->push_iters,
-                                 s->relabel_every, lctl(ST_PUSH, h_push, 1, s->push_sweeps))))
+            if ((rc = add_push_node<E>(s, body, &b, P.push, K_DEVICE, lctl(ST_PUSH, h_push, 1, s->push_sweeps))))
                 return rc;
         }
     }
@@ -470,14 +562,12 @@ int build_graph(pmf_solver *s, const Ctx &c0, int32_t ngrids, cudaGraph_t *out) 
         return rc;
     if ((rc = add_kernel(g, &prev, gfull, dim3(NT), k_lab_seed, P.bfs))) return rc;
     if (P.bfs.persistent) {
-        if ((rc = add_kernel(g, &prev, gbfs, dim3(NTT), k_bfs_src<E>, P.bfs, int(K_PERSISTENT), lctl(ST_LAB))))
-            return rc;
+        if ((rc = add_bfs_node<E>(s, g, &prev, false, P.bfs, K_PERSISTENT, lctl(ST_LAB)))) return rc;
     } else {
         cudaGraph_t body;
         if ((rc = add_while(g, &prev, h_lab, &body))) return rc;
         cudaGraphNode_t b = nullptr;
-        if ((rc = add_kernel(body, &b, gbfs, dim3(NTT), k_bfs_src<E>, P.bfs, int(K_DEVICE), lctl(ST_LAB, h_lab, 1))))
-            return rc;
+        if ((rc = add_bfs_node<E>(s, body, &b, false, P.bfs, K_DEVICE, lctl(ST_LAB, h_lab, 1)))) return rc;
     }
     if ((rc = add_kernel(g, &prev, gfull, dim3(NT), k_emit, P.base))) return rc;
     return 0;
@@ -486,7 +576,7 @@ int build_graph(pmf_solver *s, const Ctx &c0, int32_t ngrids, cudaGraph_t *out) 
 // knobs + context a cached graph was built for
 struct GraphKey {
     Ctx ctx;
-    int32_t ngrids, edge, p_push, p_bfs, iters, relabel, budget, sweeps;
+    int32_t ngrids, edge, p_push, p_bfs, iters, relabel, budget, sweeps, warp;
     int64_t maxc;
     int32_t gfull, gbfs, gpush;
 };
@@ -505,6 +595,7 @@ int graph_solve(pmf_solver *s, const Ctx &c0, int32_t ngrids) {
     key.relabel = s->relabel_every;
     key.budget = s->push_budget;
     key.sweeps = s->push_sweeps;
+    key.warp = s->warp;
     key.maxc = s->max_cycles;
     key.gfull = s->grid_full;
     key.gbfs = s->grid_bfs;
@@ -562,6 +653,15 @@ int run_end(pmf_solver *s) {
     s->stats.push_sweeps = int64_t(st[ST_PUSH_L]);
     s->stats.bfs_sweeps = int64_t(st[ST_BFS_L] + st[ST_LAB_L]);
     s->stats.cycles = ctl.cycle;
+    // kernels executed on the device: the counted tile-kernel launches plus
+    // the fixed per-cycle kernels (2 x phase_begin, gr_init, seed_push,
+    // cycle_ctl), the label tail (phase_begin, lab_seed, emit) and the
+    // build kernels (host-launched, counted in stats.launches)
+    if (s->use_graph)
+        s->stats.kernels = int64_t(st[ST_PUSH_L] + st[ST_BFS_L] + st[ST_LAB_L]) + 5 * int64_t(ctl.cycle) + 3 +
+                           (s->stats.launches - 1);
+    else
+        s->stats.kernels = s->stats.launches;
     s->stats.grids = int64_t(L.grids.size());
     s->stats.tiles = L.ntiles;
     s->stats.pixels = L.pixels;
@@ -623,6 +723,14 @@ int grids_for(pmf_solver *s) {
     s->grid_push = std::max(1, occ) * s->sms;
     CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_bfs_sink<E>, NTT, 0));
     s->grid_bfs = std::max(1, occ) * s->sms;
+    s->smem_w = WPB * sizeof(WarpTile<E>);
+    CK(cudaFuncSetAttribute(k_wpush<E>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(s->smem_w)));
+    CK(cudaFuncSetAttribute(k_wbfs_sink<E>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(s->smem_w)));
+    CK(cudaFuncSetAttribute(k_wbfs_src<E>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(s->smem_w)));
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_wpush<E>, WPB * 32, s->smem_w));
+    s->grid_wpush = std::max(1, occ) * s->sms;
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_wbfs_sink<E>, WPB * 32, s->smem_w));
+    s->grid_wbfs = std::max(1, occ) * s->sms;
     s->grid_full = 8 * s->sms;
     return 0;
 }
@@ -707,15 +815,8 @@ int seed_stage(pmf_solver *s, int32_t nprob, int32_t W, int32_t H, const int64_t
     }
     if ((rc = s->h_pw.ensure(pw_list.size() * size_t(4 * n) * 4))) return rc;
     int32_t *hp = s->h_pw.as<int32_t>();
-    int64_t maxpair = 0;
-    for (size_t k = 0; k < pw_list.size(); k++) {
-        const int64_t *src = pw_list[k];
-        for (int64_t i = 0; i < 4 * n; i++)
-            if (src[i] < 0 || src[i] > CAP_MAX)
-                return fail(PMF_ERR_RANGE, "pairwise capacity outside [0, CAP_MAX]");
-        narrow(hp + k * 4 * n, src, 4 * n, 0, CAP_MAX);
-        maxpair = std::max(maxpair, max_pair(hp + k * 4 * n, W, H));
-    }
+    TaskErr terr;
+    // masks first (seed index lists are short)
     for (int p = 0; p < nprob; p++) {
         S.offs[p] = 3 * int64_t(p) * n;   // base of problem p; slope +n, sink +2n
         uint8_t *m = hm + p * n;
@@ -731,21 +832,53 @@ int seed_stage(pmf_solver *s, int32_t nprob, int32_t W, int32_t H, const int64_t
             if (m[q] == 1) return fail(PMF_ERR_ARG, "a pixel cannot be both a foreground and background seed");
             m[q] = 2;
         }
-        // ranges the device relies on (instantiate's own checks are the caller's)
-        for (int64_t q = 0; q < n; q++) {
+    }
+    // pairwise planes: range check + narrow, chunked
+    const int64_t pw_chunks = cdiv(4 * n, kChunk);
+    s->pool->run(int64_t(pw_list.size()) * pw_chunks, [&](int64_t task) {
+        const int64_t k = task / pw_chunks, lo = (task % pw_chunks) * kChunk, hi = std::min(4 * n, lo + kChunk);
+        const int64_t *src = pw_list[k];
+        for (int64_t i = lo; i < hi; i++)
+            if (src[i] < 0 || src[i] > CAP_MAX) {
+                terr.set(PMF_ERR_RANGE, "pairwise capacity outside [0, CAP_MAX]");
+                return;
+            }
+        narrow(hp + k * 4 * n + lo, src + lo, hi - lo, 0, CAP_MAX);
+    });
+    if ((rc = terr.raise())) return rc;
+    std::vector<int64_t> mp(pw_list.size(), 0);
+    s->pool->run(int64_t(pw_list.size()), [&](int64_t k) { mp[k] = max_pair(hp + k * 4 * n, W, H); });
+    int64_t maxpair = 0;
+    for (int64_t v : mp) maxpair = std::max(maxpair, v);
+    // unary / sink planes: ranges the device relies on (instantiate's own
+    // checks are the caller's), then narrow
+    const int64_t pl_chunks = cdiv(n, kChunk);
+    s->pool->run(int64_t(nprob) * pl_chunks, [&](int64_t task) {
+        const int p = int(task / pl_chunks);
+        const int64_t lo = (task % pl_chunks) * kChunk, hi = std::min(n, lo + kChunk);
+        const uint8_t *m = hm + p * n;
+        for (int64_t q = lo; q < hi; q++) {
             if (m[q] != 1) {
                 int64_t b = ub[p][q], sl = us[p][q];
-                if (b < 0 || sl < 0) return fail(PMF_ERR_RANGE, "problem %d: negative unary term", p);
-                if (b > CAP_MAX || (sl && lam_max > (CAP_MAX - b) / sl))
-                    return fail(PMF_ERR_RANGE, "problem %d: unary term exceeds CAP_MAX", p);
+                if (b < 0 || sl < 0) {
+                    terr.set(PMF_ERR_RANGE, "negative unary term");
+                    return;
+                }
+                if (b > CAP_MAX || (sl && lam_max > (CAP_MAX - b) / sl)) {
+                    terr.set(PMF_ERR_RANGE, "unary term exceeds CAP_MAX");
+                    return;
+                }
             }
-            if (m[q] != 2 && (sb[p][q] < 0 || sb[p][q] > CAP_MAX))
-                return fail(PMF_ERR_RANGE, "problem %d: sink term outside [0, CAP_MAX]", p);
+            if (m[q] != 2 && (sb[p][q] < 0 || sb[p][q] > CAP_MAX)) {
+                terr.set(PMF_ERR_RANGE, "sink term outside [0, CAP_MAX]");
+                return;
+            }
         }
-        narrow(hb + 3 * p * n + 0 * n, ub[p], n, 0, CAP_MAX);
-        narrow(hb + 3 * p * n + 1 * n, us[p], n, 0, CAP_MAX);
-        narrow(hb + 3 * p * n + 2 * n, sb[p], n, 0, CAP_MAX);
-    }
+        narrow(hb + 3 * p * n + 0 * n + lo, ub[p] + lo, hi - lo, 0, CAP_MAX);
+        narrow(hb + 3 * p * n + 1 * n + lo, us[p] + lo, hi - lo, 0, CAP_MAX);
+        narrow(hb + 3 * p * n + 2 * n + lo, sb[p] + lo, hi - lo, 0, CAP_MAX);
+    });
+    if ((rc = terr.raise())) return rc;
     S.u8 = maxpair <= 255;
     if (!S.u8 && CAP_MAX + 8 * maxpair >= (int64_t(1) << 31) - 1)
         return fail(PMF_ERR_RANGE, "pairwise capacities too large for the int32 device state");
@@ -792,7 +925,13 @@ int seed_fetch(pmf_solver *s, uint8_t *swapped_out, int64_t *flows_out, uint8_t 
     for (int64_t g = 0; g < G; g++) flows_out[g] = hsnk[g] - hdr[g];
     if (swapped_out)
         for (int p = 0; p < S.nprob; p++) swapped_out[p] = uint8_t(hsw[p] != 0);
-    if (labels_out) memcpy(labels_out, ho, size_t(L.out_bytes));
+    if (labels_out) {
+        const int64_t chunks = cdiv(L.out_bytes, int64_t(4) << 20);
+        s->pool->run(chunks, [&](int64_t i) {
+            const int64_t lo = i * (int64_t(4) << 20), hi = std::min(L.out_bytes, lo + (int64_t(4) << 20));
+            memcpy(labels_out + lo, ho + lo, size_t(hi - lo));
+        });
+    }
     s->stats.d2h_bytes = (labels_out ? L.out_bytes : 0) + G * 16 + int64_t(S.nprob) * 4;
     return 0;
 }
@@ -847,9 +986,14 @@ int pmf_solver_create(int32_t device, pmf_solver **out) {
     pmf_solver *s = new pmf_solver();
     s->device = device;
     s->sms = prop.multiProcessorCount;
+    {
+        unsigned hc = std::thread::hardware_concurrency();
+        s->pool = new Pool();
+        s->pool->threads = int(std::max(1u, std::min(hc ? hc : 1u, 16u)));
+    }
     if (cudaStreamCreateWithFlags(&s->st, cudaStreamNonBlocking) != cudaSuccess ||
         cudaEventCreate(&s->ev_run[0]) != cudaSuccess || cudaEventCreate(&s->ev_run[1]) != cudaSuccess ||
-        s->h_small.ensure(256)) {
+        s->h_small.ensure(sizeof(Ctl) + 256)) {
         pmf_solver_destroy(s);
         return fail(PMF_ERR_CUDA, "stream/event/pinned allocation failed");
     }
@@ -863,6 +1007,7 @@ int pmf_solver_destroy(pmf_solver *s) {
     if (s->st) cudaStreamSynchronize(s->st);
     for (auto e : s->ev_pool) cudaEventDestroy(e);
     if (s->gexec) cudaGraphExecDestroy(s->gexec);
+    delete s->pool;
     for (auto e : s->ev_run)
         if (e) cudaEventDestroy(e);
     if (s->st) cudaStreamDestroy(s->st);
@@ -878,6 +1023,7 @@ int pmf_solver_set(pmf_solver *s, const char *name, int64_t v) {
     else if (k == "bfs_chunk" && v >= 1 && v <= 100000) s->bfs_chunk = int(v);
     else if (k == "relabel_every" && v >= 0 && v <= 100000) s->relabel_every = int(v);
     else if (k == "persistent") s->persistent = v != 0;
+    else if (k == "warp") s->warp = v != 0;
     else if (k == "graph") s->use_graph = v != 0;
     else if (k == "persistent_bfs") s->persistent_bfs = v != 0;
     else if (k == "push_budget" && v >= 0) s->push_budget = int(v);
@@ -933,27 +1079,45 @@ int pmf_solve_composites(pmf_solver *s, int32_t ncomp, const int32_t *width, con
     int rc = s->h_in32.ensure(size_t(total_px) * 6 * 4);
     if (rc) return rc;
     int32_t *hin = s->h_in32.as<int32_t>();
-    int64_t maxpair = 0, maxexcess = 0;
-    for (int c = 0; c < ncomp; c++) {
+    TaskErr terr;
+    // range check + narrow every plane, chunked over all composites
+    std::vector<int64_t> chunk_base(ncomp + 1, 0);
+    for (int c = 0; c < ncomp; c++)
+        chunk_base[c + 1] = chunk_base[c] + cdiv(int64_t(width[c]) * height[c] * 6, kChunk);
+    s->pool->run(chunk_base[ncomp], [&](int64_t task) {
+        int c = int(std::upper_bound(chunk_base.begin(), chunk_base.end(), task) - chunk_base.begin()) - 1;
         const int64_t n = int64_t(width[c]) * height[c], off = s->comp_off[c];
-        for (const int64_t *pl : {src[c], snk[c]})
-            for (int64_t i = 0; i < n; i++)
-                if (pl[i] < 0 || pl[i] > CAP_MAX)
-                    return fail(PMF_ERR_RANGE, "composite %d: capacity outside [0, CAP_MAX]", c);
-        for (int64_t i = 0; i < 4 * n; i++)
-            if (nbr[c][i] < 0 || nbr[c][i] > CAP_MAX)
-                return fail(PMF_ERR_RANGE, "composite %d: capacity outside [0, CAP_MAX]", c);
-        narrow(hin + off, src[c], n, 0, CAP_MAX);
-        narrow(hin + total_px + off, snk[c], n, 0, CAP_MAX);
+        const int64_t lo = (task - chunk_base[c]) * kChunk, hi = std::min(6 * n, lo + kChunk);
+        for (int64_t i = lo; i < hi; i++) {   // element i of [src | snk | nbr(4n)]
+            const int64_t v = i < n ? src[c][i] : i < 2 * n ? snk[c][i - n] : nbr[c][i - 2 * n];
+            if (v < 0 || v > CAP_MAX) {
+                terr.set(PMF_ERR_RANGE, "composite capacity outside [0, CAP_MAX]");
+                return;
+            }
+            int32_t *dst = i < n ? hin + off + i : i < 2 * n ? hin + total_px + off + (i - n)
+                                                             : hin + 2 * total_px + 4 * off + (i - 2 * n);
+            *dst = int32_t(v);
+        }
+    });
+    if ((rc = terr.raise())) return rc;
+    std::vector<int64_t> mp(ncomp, 0), mx(ncomp, 0);
+    s->pool->run(ncomp, [&](int64_t c) {
+        const int64_t n = int64_t(width[c]) * height[c], off = s->comp_off[c];
         const int32_t *nb = hin + 2 * total_px + 4 * off;
-        narrow(hin + 2 * total_px + 4 * off, nbr[c], 4 * n, 0, CAP_MAX);
-        maxpair = std::max(maxpair, max_pair(nb, width[c], height[c]));
+        mp[c] = max_pair(nb, width[c], height[c]);
         // bound on any pixel's excess: its positive terminal plus all arc pairs
+        int64_t m = 0;
         for (int64_t p = 0; p < n; p++) {
             int64_t e = std::max<int64_t>(0, int64_t(hin[off + p]) - hin[total_px + off + p]);
             for (int d = 0; d < 4; d++) e += 2 * int64_t(nb[d * n + p]);
-            maxexcess = std::max(maxexcess, e);
+            m = std::max(m, e);
         }
+        mx[c] = m;
+    });
+    int64_t maxpair = 0, maxexcess = 0;
+    for (int c = 0; c < ncomp; c++) {
+        maxpair = std::max(maxpair, mp[c]);
+        maxexcess = std::max(maxexcess, mx[c]);
     }
     if (maxexcess >= (int64_t(1) << 31) - 1)
         return fail(PMF_ERR_RANGE, "capacities too large for the int32 device state");
@@ -979,6 +1143,22 @@ int pmf_solve_composites(pmf_solver *s, int32_t ncomp, const int32_t *width, con
     }
     s->stats.h2d_bytes = total_px * 6 * 4;
     s->stats.d2h_bytes = L.out_bytes + G * 16;
+    return 0;
+}
+
+int pmf_debug_trace(pmf_solver *s, int32_t *kind, double *us, int64_t *tiles, int32_t *n) {
+    if (!s || !n) return fail(PMF_ERR_ARG, "null argument");
+    CK(cudaSetDevice(s->device));
+    Ctl ctl;
+    CK(cudaMemcpyAsync(&ctl, s->d_ctl.p, sizeof ctl, cudaMemcpyDeviceToHost, s->st));
+    CK(cudaStreamSynchronize(s->st));
+    int m = std::min(*n, ctl.ntrace);
+    for (int i = 0; i < m; i++) {
+        if (kind) kind[i] = ctl.trace_kind[i];
+        if (us) us[i] = double(ctl.trace_ns[i]) * 1e-3;
+        if (tiles) tiles[i] = int64_t(ctl.trace_tiles[i] & 0xffffffffull);
+    }
+    *n = m;
     return 0;
 }
 

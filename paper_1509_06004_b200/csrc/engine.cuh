@@ -51,7 +51,13 @@ struct Ctl {
     int32_t noconv;         // non-convergence guard tripped
     unsigned long long t0;  // earliest CTA start of the current launch (ns)
     unsigned long long t1;  // latest CTA end of the current launch (ns)
+    // trace of the first kTrace tile-kernel launches: kind, span (ns), tile passes
+    int32_t ntrace;
+    int32_t trace_kind[64];
+    unsigned long long trace_ns[64];
+    unsigned long long trace_tiles[64];
 };
+constexpr int kTrace = 64;
 
 __device__ __forceinline__ unsigned long long gtimer() {
     unsigned long long t;

@@ -122,6 +122,19 @@ __device__ __forceinline__ void launch_exit(const Ctx &c, const LaunchCtl &lc, i
     unsigned long long t1 = *(volatile unsigned long long *)&ctl->t1;
     atomicAdd(&c.stat[ST_PUSH_NS + lc.stat], t1 > t0 ? t1 - t0 : 0ull);
     atomicAdd(&c.stat[ST_PUSH_L + lc.stat], 1ull);
+    {   // launch trace (diagnostics): tiles = passes counted so far minus the previous entry
+        int ix = ctl->ntrace;
+        if (ix < kTrace) {
+            unsigned long long tot = *(volatile unsigned long long *)&c.stat[lc.stat];
+            unsigned long long prev = 0;
+            for (int j = ix - 1; j >= 0; j--)
+                if (ctl->trace_kind[j] == lc.stat) { prev = ctl->trace_tiles[j] >> 32; break; }
+            ctl->trace_kind[ix] = lc.stat;
+            ctl->trace_ns[ix] = t1 > t0 ? t1 - t0 : 0ull;
+            ctl->trace_tiles[ix] = (tot << 32) | ((tot - prev) & 0xffffffffull);
+            ctl->ntrace = ix + 1;
+        }
+    }
     ctl->t0 = ~0ull;
     ctl->t1 = 0;
     ctl->done = 0;
@@ -331,6 +344,7 @@ __global__ void __launch_bounds__(NTT, 2) k_push(Ctx c, int k, int iters, int re
     __shared__ uint8_t sm[TPIX];
     __shared__ int32_t hh[4][TW], hacc[4][TW];
     __shared__ int s_out;
+    __shared__ int s_rowin[TH];   // row received inflow this iteration
     const int i = threadIdx.x, lx = i & 31, ly = i >> 5, pi = ly * SP + lx;
     // in-tile neighbour (padded index) per direction, or -1 (halo)
     const int nbi[4] = {lx > 0 ? pi - 1 : -1, lx < TW - 1 ? pi + 1 : -1,
@@ -355,6 +369,7 @@ __global__ void __launch_bounds__(NTT, 2) k_push(Ctx c, int k, int iters, int re
             hacc[s][j] = 0;
         }
         if (i == 0) s_out = 0;
+        if (i < TH) s_rowin[i] = 0;
         int act = 1;
         for (int it = 0; it < iters; it++) {
             if (relabel_every && it % relabel_every == 0) {
@@ -372,35 +387,57 @@ __global__ void __launch_bounds__(NTT, 2) k_push(Ctx c, int k, int iters, int re
                 act = __syncthreads_or(e > 0 && h < HINF);
                 if (!act) break;
             }
+            // warp == tile row: rows without an active pixel skip the push
+            // work, rows nobody pushed into skip the merge (barriers stay)
+            const bool mine = e > 0 && h < HINF;
             int32_t hn[4];
+            if (__any_sync(0xffffffffu, mine)) {
 #pragma unroll
-            for (int d = 0; d < 4; d++) hn[d] = nbi[d] >= 0 ? sh[nbi[d]] : hh[d][hpos[d]];
-            // ---- push downhill (heights are fixed during this phase, so an
-            // arc is never pushed both ways and every inflow slot has one writer)
-            if (e > 0 && h < HINF) {
+                for (int d = 0; d < 4; d++) hn[d] = nbi[d] >= 0 ? sh[nbi[d]] : hh[d][hpos[d]];
+                // ---- push downhill (heights are fixed during this phase, so
+                // an arc is never pushed both ways and every inflow slot has
+                // one writer)
+                if (mine) {
+                    int pushed = 0;
 #pragma unroll
-                for (int d = 0; d < 4; d++) {
-                    if (e > 0 && r[d] > 0 && h > hn[d]) {
-                        int32_t dl = min(e, r[d]);
-                        e -= dl;
-                        r[d] -= dl;
-                        if (nbi[d] >= 0) sin4[opp(d)][nbt[d]] = dl;
-                        else hacc[d][hpos[d]] += dl;
+                    for (int d = 0; d < 4; d++) {
+                        if (e > 0 && r[d] > 0 && h > hn[d]) {
+                            int32_t dl = min(e, r[d]);
+                            e -= dl;
+                            r[d] -= dl;
+                            if (nbi[d] >= 0) {
+                                sin4[opp(d)][nbt[d]] = dl;
+                                pushed |= 1 << d;
+                            } else {
+                                hacc[d][hpos[d]] += dl;
+                            }
+                        }
                     }
+                    if (pushed & ((1 << DL) | (1 << DR))) s_rowin[ly] = 1;
+                    if (pushed & (1 << DU)) s_rowin[ly - 1] = 1;
+                    if (pushed & (1 << DD)) s_rowin[ly + 1] = 1;
                 }
             }
             __syncthreads();
             // ---- absorb inflow, relabel what is still active
+            if (s_rowin[ly]) {
 #pragma unroll
-            for (int d = 0; d < 4; d++) {
-                int32_t v = sin4[d][i];
-                if (v) {
-                    e += v;
-                    r[d] += v;
-                    sin4[d][i] = 0;
+                for (int d = 0; d < 4; d++) {
+                    int32_t v = sin4[d][i];
+                    if (v) {
+                        e += v;
+                        r[d] += v;
+                        sin4[d][i] = 0;
+                    }
                 }
+                __syncwarp();
+                if (lx == 0) s_rowin[ly] = 0;
             }
             if (e > 0 && h < HINF) {
+                if (!mine) {   // became active by inflow this iteration
+#pragma unroll
+                    for (int d = 0; d < 4; d++) hn[d] = nbi[d] >= 0 ? sh[nbi[d]] : hh[d][hpos[d]];
+                }
                 int32_t m = HINF;
 #pragma unroll
                 for (int d = 0; d < 4; d++)

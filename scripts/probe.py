@@ -32,6 +32,8 @@ def main():
     ap.add_argument("--budget", type=int, default=None)
     ap.add_argument("--pbfs", type=int, default=None)
     ap.add_argument("--graph", type=int, default=None)
+    ap.add_argument("--warp", type=int, default=None)
+    ap.add_argument("--trace", action="store_true")
     ap.add_argument("--reps", type=int, default=3)
     ap.add_argument("--nprob", type=int, default=None, help="problems per device batch")
     a = ap.parse_args()
@@ -47,16 +49,28 @@ def main():
     if a.budget is not None: s.set("push_budget", a.budget)
     if a.pbfs is not None: s.set("persistent_bfs", a.pbfs)
     if a.graph is not None: s.set("graph", a.graph)
+    if a.warp is not None: s.set("warp", a.warp)
     for r in range(a.reps):
         t0 = time.perf_counter()
-        sw, flows, labels = s.solve_seed_batch(c["w"], c["h"], probs, c["lams"], "auto")
-        dt = time.perf_counter() - t0
+        s.seed_stage(c["w"], c["h"], probs, c["lams"], "auto")
+        t1 = time.perf_counter()
+        s.seed_run()
+        t2 = time.perf_counter()
+        sw, flows, labels = s.seed_fetch(True)
+        t3 = time.perf_counter()
+        dt = t3 - t0
         st = s.stats()
         cuts = flows.size
+        if a.trace and r == a.reps - 1:
+            tr = s.trace()
+            print("trace push (us, tiles):", [(u, t) for k, u, t in tr if k == 0])
+            print("trace bfs  (us, tiles):", [(u, t) for k, u, t in tr if k == 1][:30])
         keep = ("cycles", "push_tile_passes", "bfs_tile_passes", "label_tile_passes", "push_sweeps",
                 "bfs_sweeps", "ms_device", "ms_push", "ms_bfs", "ms_labels", "launches", "graph_builds")
         print(json.dumps(dict(cfg=a.cfg, args=" ".join(sys.argv[2:]), rep=r,
-                              wall_ms=round(dt * 1e3, 2), cuts_per_s=round(cuts / dt, 1),
+                              wall_ms=round(dt * 1e3, 2), stage_ms=round((t1 - t0) * 1e3, 2),
+                              run_ms=round((t2 - t1) * 1e3, 2), fetch_ms=round((t3 - t2) * 1e3, 2),
+                              cuts_per_s=round(cuts / dt, 1),
                               flow=int(flows.sum()),
                               **{k: (round(st[k], 3) if isinstance(st[k], float) else st[k]) for k in keep})))
 
