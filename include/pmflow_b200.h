@@ -77,6 +77,7 @@ typedef struct pmf_stats {
     int64_t d2h_bytes;          /* device->host bytes of the last fetch       */
     int64_t graph_builds;       /* solve graphs (re)built by the last run     */
     int64_t kernels;            /* kernels executed on the device by the run  */
+    int64_t steps;              /* warm-start steps (lambdas per chain)       */
 } pmf_stats;
 
 /* Create / destroy a solver bound to one CUDA device and its own stream. */
@@ -89,7 +90,9 @@ int pmf_solver_destroy(pmf_solver *s);
  * "push_sweeps" (sweep-mode discharge launches per cycle), "bfs_chunk"
  * (host-driven mode: launches between convergence checks), "persistent" /
  * "persistent_bfs" (phase scheduling), "graph" (0: host-driven loop, 1:
- * whole solve as one CUDA graph), "timing" (0/1 event timings),
+ * whole solve as one CUDA graph), "chain" (warm-start chain length; 0:
+ * auto), "warm_grids" (auto chains target about this many grids),
+ * "timing" (0/1 event timings),
  * "max_cycles" (non-convergence guard). Returns PMF_ERR_ARG if unknown. */
 int pmf_solver_set(pmf_solver *s, const char *name, int64_t value);
 

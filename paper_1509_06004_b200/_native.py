@@ -39,7 +39,7 @@ class PmfStats(ctypes.Structure):
         (k, ctypes.c_double) for k in ("ms_total", "ms_build", "ms_push", "ms_bfs", "ms_labels",
                                        "ms_seed", "ms_h2d", "ms_d2h", "ms_device")] + [
         (k, ctypes.c_int64) for k in ("launches", "h2d_bytes", "d2h_bytes", "graph_builds",
-                                       "kernels")]
+                                       "kernels", "steps")]
 
     def as_dict(self):
         return {k: getattr(self, k) for k, _ in self._fields_}

@@ -134,7 +134,8 @@ struct Layout {
         tile_grid.clear();
         ntiles = out_bytes = pixels = 0;
     }
-    void add(int32_t W, int32_t H, int32_t kind, int32_t colswap_off, int32_t prob, int32_t lam) {
+    void add(int32_t W, int32_t H, int32_t kind, int32_t colswap_off, int32_t prob, int32_t lam,
+             int32_t lam_end) {
         GridDesc g{};
         g.W = W;
         g.H = H;
@@ -146,6 +147,7 @@ struct Layout {
         g.colswap_off = colswap_off;
         g.prob = prob;
         g.lam = lam;
+        g.lam_end = lam_end;
         int64_t nt = int64_t(g.ntx) * g.nty;
         tile_grid.insert(tile_grid.end(), size_t(nt), int32_t(grids.size()));
         ntiles += nt;
@@ -163,6 +165,8 @@ struct SeedStage {
     bool u8 = true;
     std::vector<int64_t> offs;      // [plane_off(nprob) | pw_off(nprob)]
     std::vector<int64_t> lambdas;
+    std::vector<int64_t> slope_sum; // per problem: sum of unary_slope over non-fg pixels
+    int32_t chain = 1;              // lambdas per warm-start chain
 };
 
 }  // namespace
@@ -182,16 +186,18 @@ struct pmf_solver {
     int persistent = 1;       // discharge phase as one persistent launch
     int persistent_bfs = 0;   // BFS phases as one persistent launch
     int push_budget = 2;      // persistent push phase: pops <= budget * seeded tiles
+    int chain = 0;            // warm-start chain length (0: auto from warm_grids)
+    int warm_grids = 200;     // auto chains: aim for about this many grids per batch
     int bfs_chunk = 8;
     int timing = 0;
     int64_t max_cycles = 50000;
     // device workspace
     DevBuf d_w, d_h, d_r, d_lab, d_tile_grid, d_grids, d_live, d_act, d_list, d_inq, d_cnt,
         d_snk, d_drain, d_err, d_stat, d_colswap, d_out, d_in32, d_pw, d_mask, d_off, d_lam,
-        d_swapcnt, d_swapflag, d_ring, d_qstate, d_qctr, d_ctl;
+        d_swapcnt, d_swapflag, d_ring, d_qstate, d_qctr, d_ctl, d_curlam, d_flows, d_slopesum;
     HostBuf h_in32, h_pw, h_mask, h_out, h_small;
     Layout lay;
-    std::vector<int32_t> ones;
+    std::vector<int32_t> ones, curlam0;
     std::vector<uint8_t> colswap;
     std::vector<int64_t> comp_off;
     SeedStage stage;
@@ -205,7 +211,7 @@ struct pmf_solver {
     Pool *pool = nullptr;
     int use_graph = 1;                 // whole solve as one CUDA graph
     cudaGraphExec_t gexec = nullptr;   // cached instantiated solve graph
-    unsigned char gkey[512] = {0};     // GraphKey it was built for
+    unsigned char gkey[1024] = {0};    // GraphKey it was built for
 
     int ev_get(cudaEvent_t *e) {
         if (ev_used == ev_pool.size()) {
@@ -250,7 +256,7 @@ int setup_state(pmf_solver *s, int edge_bytes) {
         (rc = s->d_out.ensure(std::max<int64_t>(L.out_bytes, 1))) || (rc = s->d_colswap.ensure(64)) ||
         (rc = s->d_swapflag.ensure(64)) || (rc = s->d_ring.ensure(T * 4)) ||
         (rc = s->d_qstate.ensure(T * 4)) || (rc = s->d_qctr.ensure(64)) ||
-        (rc = s->d_ctl.ensure(sizeof(Ctl))))
+        (rc = s->d_ctl.ensure(sizeof(Ctl))) || (rc = s->d_curlam.ensure(G * 4)))
         return rc;
     s->edge_bytes = edge_bytes;
     // host sources live in the solver (s->lay, s->ones) until the next setup
@@ -258,6 +264,9 @@ int setup_state(pmf_solver *s, int edge_bytes) {
     CK(cudaMemcpyAsync(s->d_grids.p, L.grids.data(), G * sizeof(GridDesc), cudaMemcpyHostToDevice, s->st));
     s->ones.assign(size_t(G), 1);
     CK(cudaMemcpyAsync(s->d_live.p, s->ones.data(), G * 4, cudaMemcpyHostToDevice, s->st));
+    s->curlam0.resize(size_t(G));
+    for (int64_t g = 0; g < G; g++) s->curlam0[g] = L.grids[g].lam;
+    CK(cudaMemcpyAsync(s->d_curlam.p, s->curlam0.data(), G * 4, cudaMemcpyHostToDevice, s->st));
     CK(cudaMemsetAsync(s->d_act.p, 0, G * 4, s->st));
     CK(cudaMemsetAsync(s->d_snk.p, 0, G * 8, s->st));
     CK(cudaMemsetAsync(s->d_drain.p, 0, G * 8, s->st));
@@ -293,6 +302,9 @@ int setup_state(pmf_solver *s, int edge_bytes) {
     x.persistent = s->persistent;
     x.ctl = s->d_ctl.as<Ctl>();
     x.budget_dev = 0;
+    x.cur_lam = s->d_curlam.as<int32_t>();
+    x.flows = s->d_flows.as<int64_t>();
+    x.nlam = s->stage.nlam;
     // BFS phases converge on their own (values only decrease); the cap only
     // guards against a runaway launch
     x.budget = unsigned(std::min<int64_t>(int64_t(4096) * T + 4096, int64_t(0xffffffffu) - 1));
@@ -506,16 +518,24 @@ int add_push_node(pmf_solver *s, cudaGraph_t g, cudaGraphNode_t *prev, const Ctx
 }
 
 template <class E>
-int build_graph(pmf_solver *s, const Ctx &c0, int32_t ngrids, cudaGraph_t *out) {
+int build_graph(pmf_solver *s, const Ctx &c0, int32_t ngrids, const SeedArgs *sa, const int64_t *slope_sum,
+                cudaGraph_t *out) {
     PhaseCtx P = phase_ctx(s, c0);
-    cudaGraph_t g;
-    CK(cudaGraphCreate(&g, 0));
-    *out = g;
-    cudaGraphNode_t prev = nullptr;
+    cudaGraph_t root;
+    CK(cudaGraphCreate(&root, 0));
+    *out = root;
     int rc;
-    const dim3 gfull(s->grid_full), gbfs(s->grid_bfs), gpush(s->grid_push);
+    const dim3 gfull(s->grid_full);
+    // warm-start steps: one iteration per lambda of the longest chain
+    cudaGraphConditionalHandle h_step;
+    CK(cudaGraphConditionalHandleCreate(&h_step, root, 1, cudaGraphCondAssignDefault));
+    cudaGraphNode_t rprev = nullptr;
+    cudaGraph_t g;
+    if ((rc = add_while(root, &rprev, h_step, &g))) return rc;
+    cudaGraphNode_t prev = nullptr;
     cudaGraphConditionalHandle h_cycle;
-    CK(cudaGraphConditionalHandleCreate(&h_cycle, g, 1, cudaGraphCondAssignDefault));
+    CK(cudaGraphConditionalHandleCreate(&h_cycle, g, 0, 0));
+    if ((rc = add_kernel(g, &prev, dim3(1), dim3(1), k_arm, h_cycle))) return rc;
     cudaGraph_t cyc;
     if ((rc = add_while(g, &prev, h_cycle, &cyc))) return rc;
     {   // ---- one cycle: exact global relabel, seeding, discharge
@@ -570,6 +590,13 @@ int build_graph(pmf_solver *s, const Ctx &c0, int32_t ngrids, cudaGraph_t *out) 
         if ((rc = add_bfs_node<E>(s, body, &b, false, P.bfs, K_DEVICE, lctl(ST_LAB, h_lab, 1)))) return rc;
     }
     if ((rc = add_kernel(g, &prev, gfull, dim3(NT), k_emit, P.base))) return rc;
+    if ((rc = add_kernel(g, &prev, dim3(std::max(1, int(cdiv(ngrids, 256)))), dim3(256), k_finalize, P.base, ngrids)))
+        return rc;
+    SeedArgs none{};
+    if (sa && (rc = add_kernel(g, &prev, gfull, dim3(NT), k_advance_tiles, P.base, *sa))) return rc;
+    if ((rc = add_kernel(g, &prev, dim3(1), dim3(1024), k_advance_grids, P.base, sa ? *sa : none, slope_sum, ngrids,
+                         h_step, 1)))
+        return rc;
     return 0;
 }
 
@@ -579,10 +606,13 @@ struct GraphKey {
     int32_t ngrids, edge, p_push, p_bfs, iters, relabel, budget, sweeps, warp;
     int64_t maxc;
     int32_t gfull, gbfs, gpush;
+    SeedArgs sa;
+    const int64_t *slope_sum;
+    int32_t has_sa;
 };
 
 template <class E>
-int graph_solve(pmf_solver *s, const Ctx &c0, int32_t ngrids) {
+int graph_solve(pmf_solver *s, const Ctx &c0, int32_t ngrids, const SeedArgs *sa, const int64_t *slope_sum) {
     static_assert(sizeof(GraphKey) <= sizeof(pmf_solver::gkey), "graph key buffer too small");
     GraphKey key;
     memset(&key, 0, sizeof key);
@@ -600,11 +630,14 @@ int graph_solve(pmf_solver *s, const Ctx &c0, int32_t ngrids) {
     key.gfull = s->grid_full;
     key.gbfs = s->grid_bfs;
     key.gpush = s->grid_push;
+    if (sa) key.sa = *sa;
+    key.slope_sum = slope_sum;
+    key.has_sa = sa != nullptr;
     if (!s->gexec || memcmp(&key, s->gkey, sizeof key) != 0) {
         if (s->gexec) cudaGraphExecDestroy(s->gexec);
         s->gexec = nullptr;
         cudaGraph_t g = nullptr;
-        int rc = build_graph<E>(s, c0, ngrids, &g);
+        int rc = build_graph<E>(s, c0, ngrids, sa, slope_sum, &g);
         if (rc) {
             if (g) cudaGraphDestroy(g);
             return rc;
@@ -621,9 +654,24 @@ int graph_solve(pmf_solver *s, const Ctx &c0, int32_t ngrids) {
 }
 
 template <class E>
-int run_solve(pmf_solver *s, const Ctx &c0, int32_t ngrids) {
+int run_solve(pmf_solver *s, const Ctx &c0, int32_t ngrids, const SeedArgs *sa = nullptr,
+              const int64_t *slope_sum = nullptr) {
     CK(cudaMemsetAsync(c0.ctl, 0, sizeof(Ctl), s->st));
-    return s->use_graph ? graph_solve<E>(s, c0, ngrids) : host_solve<E>(s, c0, ngrids);
+    if (s->use_graph) return graph_solve<E>(s, c0, ngrids, sa, slope_sum);
+    const int gfin = std::max(1, int(cdiv(ngrids, 256)));
+    for (;;) {   // warm-start steps
+        int rc = host_solve<E>(s, c0, ngrids);
+        if (rc) return rc;
+        LAUNCH(s, (k_finalize<<<gfin, 256, 0, s->st>>>(c0, ngrids)));
+        if (!sa) break;
+        LAUNCH(s, (k_advance_tiles<<<s->grid_full, NT, 0, s->st>>>(c0, *sa)));
+        LAUNCH(s, (k_advance_grids<<<1, 1024, 0, s->st>>>(c0, *sa, slope_sum, ngrids, 0, 0)));
+        CK(cudaGetLastError());
+        Ctl ctl;
+        if ((rc = read_ctl(s, c0, &ctl))) return rc;
+        if (ctl.noconv || !ctl.more) break;
+    }
+    return 0;
 }
 
 // Device-side run bracket: always-on events around the whole run give
@@ -652,14 +700,15 @@ int run_end(pmf_solver *s) {
     s->stats.label_tile_passes = int64_t(st[ST_LAB]);
     s->stats.push_sweeps = int64_t(st[ST_PUSH_L]);
     s->stats.bfs_sweeps = int64_t(st[ST_BFS_L] + st[ST_LAB_L]);
-    s->stats.cycles = ctl.cycle;
+    s->stats.cycles = ctl.cycles_total;
+    s->stats.steps = std::max(1, ctl.steps);
     // kernels executed on the device: the counted tile-kernel launches plus
     // the fixed per-cycle kernels (2 x phase_begin, gr_init, seed_push,
     // cycle_ctl), the label tail (phase_begin, lab_seed, emit) and the
     // build kernels (host-launched, counted in stats.launches)
     if (s->use_graph)
-        s->stats.kernels = int64_t(st[ST_PUSH_L] + st[ST_BFS_L] + st[ST_LAB_L]) + 5 * int64_t(ctl.cycle) + 3 +
-                           (s->stats.launches - 1);
+        s->stats.kernels = int64_t(st[ST_PUSH_L] + st[ST_BFS_L] + st[ST_LAB_L]) + 5 * int64_t(ctl.cycles_total) +
+                           7 * int64_t(std::max(1, ctl.steps)) + (s->stats.launches - 1);
     else
         s->stats.kernels = s->stats.launches;
     s->stats.grids = int64_t(L.grids.size());
@@ -775,7 +824,9 @@ int seed_run_t(pmf_solver *s) {
     LAUNCH(s, (k_build_seed<E><<<s->grid_full, NT, 0, s->st>>>(c, a)));
     CK(cudaGetLastError());
     s->stats.full_passes++;
-    return run_solve<E>(s, c, int32_t(s->lay.grids.size()));
+    const bool chains = S.chain > 1;
+    return run_solve<E>(s, c, int32_t(s->lay.grids.size()), chains ? &a : nullptr,
+                        chains ? s->d_slopesum.as<int64_t>() : nullptr);
 }
 
 int seed_stage(pmf_solver *s, int32_t nprob, int32_t W, int32_t H, const int64_t *const *ub,
@@ -893,9 +944,32 @@ int seed_stage(pmf_solver *s, int32_t nprob, int32_t W, int32_t H, const int64_t
     CK(cudaMemcpyAsync(s->d_mask.p, hm, size_t(nprob) * n, cudaMemcpyHostToDevice, s->st));
     CK(cudaMemcpyAsync(s->d_off.p, S.offs.data(), S.offs.size() * 8, cudaMemcpyHostToDevice, s->st));
     CK(cudaMemcpyAsync(s->d_lam.p, S.lambdas.data(), size_t(nlam) * 8, cudaMemcpyHostToDevice, s->st));
+    // warm-start chains: nlam lambdas split into chains of S.chain
+    // consecutive values; each chain is one grid solved step by step
+    int32_t chain = s->chain;
+    if (chain <= 0) {
+        const int64_t per_problem = std::max<int64_t>(1, cdiv(s->warm_grids, nprob));
+        chain = int32_t(cdiv(nlam, std::min<int64_t>(per_problem, nlam)));
+    }
+    chain = std::max(1, std::min(chain, nlam));
+    S.chain = chain;
     s->lay.clear();
     for (int p = 0; p < nprob; p++)
-        for (int j = 0; j < nlam; j++) s->lay.add(W, H, 0, 0, p, j);
+        for (int j = 0; j < nlam; j += chain) s->lay.add(W, H, 0, 0, p, j, std::min(nlam, j + chain));
+    s->lay.out_bytes = int64_t(nprob) * nlam * n;   // one label plane per (problem, lambda)
+    // sums of unary_slope over non-fg pixels (sink capacity growth of swapped grids)
+    S.slope_sum.assign(size_t(nprob), 0);
+    s->pool->run(nprob, [&](int64_t p) {
+        const uint8_t *m = hm + p * n;
+        const int32_t *sl = hb + 3 * p * n + n;
+        int64_t acc = 0;
+        for (int64_t q = 0; q < n; q++)
+            if (m[q] != 1) acc += sl[q];
+        S.slope_sum[p] = acc;
+    });
+    if ((rc = s->d_slopesum.ensure(size_t(nprob) * 8)) || (rc = s->d_flows.ensure(size_t(nprob) * nlam * 8)))
+        return rc;
+    CK(cudaMemcpyAsync(s->d_slopesum.p, S.slope_sum.data(), size_t(nprob) * 8, cudaMemcpyHostToDevice, s->st));
     S.nprob = nprob;
     S.nlam = nlam;
     S.W = W;
@@ -909,30 +983,30 @@ int seed_stage(pmf_solver *s, int32_t nprob, int32_t W, int32_t H, const int64_t
 int seed_fetch(pmf_solver *s, uint8_t *swapped_out, int64_t *flows_out, uint8_t *labels_out) {
     const SeedStage &S = s->stage;
     const Layout &L = s->lay;
-    const int64_t G = int64_t(L.grids.size());
-    const size_t lab_bytes = size_t((L.out_bytes + 7) / 8) * 8;
+    const int64_t nf = int64_t(S.nprob) * S.nlam;
+    const int64_t out_bytes = nf * int64_t(S.W) * S.H;
+    const size_t lab_bytes = size_t((out_bytes + 7) / 8) * 8;
     int rc;
-    if ((rc = s->h_out.ensure(lab_bytes + size_t(G) * 16 + size_t(S.nprob) * 4 + 64))) return rc;
+    if ((rc = s->h_out.ensure(lab_bytes + size_t(nf) * 8 + size_t(S.nprob) * 4 + 64))) return rc;
     uint8_t *ho = s->h_out.as<uint8_t>();
-    int64_t *hsnk = (int64_t *)(ho + lab_bytes);
-    int64_t *hdr = hsnk + G;
-    int32_t *hsw = (int32_t *)(hdr + G);
-    if (labels_out) CK(cudaMemcpyAsync(ho, s->d_out.p, L.out_bytes, cudaMemcpyDeviceToHost, s->st));
-    CK(cudaMemcpyAsync(hsnk, s->d_snk.p, G * 8, cudaMemcpyDeviceToHost, s->st));
-    CK(cudaMemcpyAsync(hdr, s->d_drain.p, G * 8, cudaMemcpyDeviceToHost, s->st));
+    int64_t *hfl = (int64_t *)(ho + lab_bytes);
+    int32_t *hsw = (int32_t *)(hfl + nf);
+    if (labels_out) CK(cudaMemcpyAsync(ho, s->d_out.p, out_bytes, cudaMemcpyDeviceToHost, s->st));
+    CK(cudaMemcpyAsync(hfl, s->d_flows.p, nf * 8, cudaMemcpyDeviceToHost, s->st));
     CK(cudaMemcpyAsync(hsw, s->d_swapflag.p, size_t(S.nprob) * 4, cudaMemcpyDeviceToHost, s->st));
     CK(cudaStreamSynchronize(s->st));
-    for (int64_t g = 0; g < G; g++) flows_out[g] = hsnk[g] - hdr[g];
+    memcpy(flows_out, hfl, size_t(nf) * 8);
     if (swapped_out)
         for (int p = 0; p < S.nprob; p++) swapped_out[p] = uint8_t(hsw[p] != 0);
     if (labels_out) {
-        const int64_t chunks = cdiv(L.out_bytes, int64_t(4) << 20);
+        const int64_t chunks = cdiv(out_bytes, int64_t(4) << 20);
         s->pool->run(chunks, [&](int64_t i) {
-            const int64_t lo = i * (int64_t(4) << 20), hi = std::min(L.out_bytes, lo + (int64_t(4) << 20));
+            const int64_t lo = i * (int64_t(4) << 20), hi = std::min(out_bytes, lo + (int64_t(4) << 20));
             memcpy(labels_out + lo, ho + lo, size_t(hi - lo));
         });
     }
-    s->stats.d2h_bytes = (labels_out ? L.out_bytes : 0) + G * 16 + int64_t(S.nprob) * 4;
+    s->stats.d2h_bytes = (labels_out ? out_bytes : 0) + nf * 8 + int64_t(S.nprob) * 4;
+    (void)L;
     return 0;
 }
 
@@ -1024,6 +1098,8 @@ int pmf_solver_set(pmf_solver *s, const char *name, int64_t v) {
     else if (k == "relabel_every" && v >= 0 && v <= 100000) s->relabel_every = int(v);
     else if (k == "persistent") s->persistent = v != 0;
     else if (k == "warp") s->warp = v != 0;
+    else if (k == "chain" && v >= 0 && v <= 1000000) s->chain = int(v);
+    else if (k == "warm_grids" && v >= 1) s->warm_grids = int(v);
     else if (k == "graph") s->use_graph = v != 0;
     else if (k == "persistent_bfs") s->persistent_bfs = v != 0;
     else if (k == "push_budget" && v >= 0) s->push_budget = int(v);
@@ -1071,7 +1147,7 @@ int pmf_solve_composites(pmf_solver *s, int32_t ncomp, const int32_t *width, con
             if (seg_swapped[c][k])
                 for (int x = o; x < o + w; x++) s->colswap[cs_off + x] = 1;
         }
-        s->lay.add(width[c], height[c], 1, cs_off, c, 0);
+        s->lay.add(width[c], height[c], 1, cs_off, c, 0, 1);
         s->comp_off[c] = total_px;
         total_px += int64_t(width[c]) * height[c];
     }
@@ -1121,6 +1197,7 @@ int pmf_solve_composites(pmf_solver *s, int32_t ncomp, const int32_t *width, con
     }
     if (maxexcess >= (int64_t(1) << 31) - 1)
         return fail(PMF_ERR_RANGE, "capacities too large for the int32 device state");
+    if ((rc = s->d_flows.ensure(size_t(ncomp) * 8))) return rc;
     if ((rc = run_begin(s))) return rc;
     rc = maxpair <= 255 ? comp_run_t<EdgeU8>(s, ncomp, total_px) : comp_run_t<EdgeI32>(s, ncomp, total_px);
     if (rc) return rc;
@@ -1134,11 +1211,11 @@ int pmf_solve_composites(pmf_solver *s, int32_t ncomp, const int32_t *width, con
     int64_t *hsnk = (int64_t *)(ho + lab_bytes);
     int64_t *hdr = hsnk + G;
     CK(cudaMemcpyAsync(ho, s->d_out.p, L.out_bytes, cudaMemcpyDeviceToHost, s->st));
-    CK(cudaMemcpyAsync(hsnk, s->d_snk.p, G * 8, cudaMemcpyDeviceToHost, s->st));
-    CK(cudaMemcpyAsync(hdr, s->d_drain.p, G * 8, cudaMemcpyDeviceToHost, s->st));
+    CK(cudaMemcpyAsync(hsnk, s->d_flows.p, G * 8, cudaMemcpyDeviceToHost, s->st));
+    (void)hdr;
     if ((rc = run_end(s))) return rc;
     for (int c = 0; c < ncomp; c++) {
-        flow_out[c] = hsnk[c] - hdr[c];
+        flow_out[c] = hsnk[c];
         memcpy(labels_out[c], ho + L.grids[c].out_off, size_t(width[c]) * height[c]);
     }
     s->stats.h2d_bytes = total_px * 6 * 4;

@@ -49,6 +49,9 @@ struct Ctl {
     uint32_t budget;        // pop budget of the next persistent discharge
     int32_t nact;           // tiles seeded for discharge this cycle
     int32_t noconv;         // non-convergence guard tripped
+    int32_t cycles_total;   // cycles over all warm-start steps
+    int32_t steps;          // warm-start steps run
+    int32_t more;           // another warm-start step follows
     unsigned long long t0;  // earliest CTA start of the current launch (ns)
     unsigned long long t1;  // latest CTA end of the current launch (ns)
     // trace of the first kTrace tile-kernel launches: kind, span (ns), tile passes
@@ -71,7 +74,8 @@ struct GridDesc {
     int64_t out_off;        // offset of this grid's label bytes in the output
     int32_t kind;           // 0: batch lambda-graph, 1: composite (column spans)
     int32_t colswap_off;    // composite: offset of its per-column swap flags
-    int32_t prob, lam;      // builder: problem / lambda index
+    int32_t prob, lam;      // builder: problem / first lambda index of the grid's chain
+    int32_t lam_end;        // one past the last lambda index of the chain (warm start)
 };
 
 struct Ctx {
@@ -104,6 +108,9 @@ struct Ctx {
     unsigned int budget;    // max tile pops of a persistent phase (0 = none)
     Ctl *ctl;               // device control block
     int32_t budget_dev;     // persistent discharge reads its budget from ctl
+    int32_t *cur_lam;       // per grid: lambda index being solved (warm-start chains)
+    int64_t *flows;         // per (problem, lambda) [seed batch] or per grid [composites]
+    int32_t nlam;           // lambdas per problem (seed batch)
 };
 
 enum { Q_IDLE = 0, Q_QUEUED = 1, Q_RUNNING = 2, Q_DIRTY = 3 };

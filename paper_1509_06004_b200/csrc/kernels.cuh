@@ -272,6 +272,7 @@ __global__ void __launch_bounds__(1024) k_cycle_ctl(Ctx c, int32_t ngrids, int p
         Ctl *ctl = c.ctl;
         int32_t nact = persistent ? int32_t(c.qctr[QC_PENDING]) : c.cnt[0];
         int32_t cyc = ++ctl->cycle;
+        ctl->cycles_total++;
         int stop = nact == 0;
         if (!stop && cyc > max_cycles) {
             ctl->noconv = 1;
@@ -330,10 +331,82 @@ __global__ void __launch_bounds__(NT) k_emit(Ctx c) {
             } else {
                 v = grid_swapped(c, gd) ? uint8_t(c.h[p] < HINF) : c.lab[p];
             }
-            c.out[gd.out_off + int64_t(y) * g.W + x] = v;
+            const int64_t off = gd.kind == 1 ? gd.out_off
+                                             : (int64_t(gd.prob) * c.nlam + c.cur_lam[g.g]) * (int64_t(g.W) * g.H);
+            c.out[off + int64_t(y) * g.W + x] = v;
         }
         int64_t s = block_sum64(drain, red);
         if (threadIdx.x == 0 && s) atomicAdd((unsigned long long *)&c.drain[g.g], (unsigned long long)s);
+    }
+}
+
+}  // namespace pmf
+
+namespace pmf {
+
+// Arm a conditional node (graph mode): 1 before the loop it controls.
+__global__ void k_arm(cudaGraphConditionalHandle h) { cudaGraphSetConditional(h, 1u); }
+
+// Per-grid results of a solved step: flow = sum of (embedded) sink
+// capacities minus the sink residual left unused (solvers.py:140, reduced
+// network), stored at the grid's (problem, lambda) slot.
+__global__ void k_finalize(Ctx c, int32_t ngrids) {
+    for (int g = blockIdx.x * blockDim.x + threadIdx.x; g < ngrids; g += gridDim.x * blockDim.x) {
+        const GridDesc &gd = c.grids[g];
+        const int64_t idx = gd.kind == 1 ? g : int64_t(gd.prob) * c.nlam + c.cur_lam[g];
+        c.flows[idx] = c.snk_sum[g] - c.drain[g];
+        c.drain[g] = 0;
+    }
+}
+
+// Warm start along the nested schedule: the maximum
+// preflow of lambda_i stays a valid preflow of lambda_{i+1} -- only the
+// terminal capacities grow (source arcs of unswapped grids, sink arcs of
+// swapped ones, parametric.py:147) -- so the next solve starts from it.
+// Non-fg pixels gain (lambda_{i+1} - lambda_i) * slope of source (w +=) or,
+// embedded swapped, of sink capacity (w -=).
+__global__ void __launch_bounds__(NT) k_advance_tiles(Ctx c, SeedArgs a) {
+    const int64_t n = int64_t(a.W) * a.H;
+    for (int64_t t = blockIdx.x; t < c.ntiles; t += gridDim.x) {
+        TileGeo g = tile_geo(c, int32_t(t));
+        const GridDesc &gd = c.grids[g.g];
+        const int cur = c.cur_lam[g.g];
+        if (cur + 1 >= gd.lam_end) continue;
+        const int64_t dl = a.lambdas[cur + 1] - a.lambdas[cur];
+        const int sign = c.swapflag[gd.prob] ? -1 : 1;
+        const int64_t po = a.plane_off[gd.prob];
+        for (int j = 0; j < PPT; j++) {
+            int i = threadIdx.x + j * NT;
+            int x = g.x0 + (i & (TW - 1)), y = g.y0 + i / TW;
+            if (x >= g.W || y >= g.H) continue;
+            const int64_t q = int64_t(y) * a.W + x;
+            if (a.mask[int64_t(gd.prob) * n + q] == 1) continue;   // fg seed: CAP_MAX either way
+            c.w[t * TPIX + i] += int32_t(sign * dl * int64_t(a.slope[po + q]));
+        }
+    }
+}
+
+// One CTA: advance every grid with a next lambda (cur_lam, live, embedded
+// sink-capacity sum) and tell the step loop whether another step runs.
+__global__ void __launch_bounds__(1024) k_advance_grids(Ctx c, SeedArgs a, const int64_t *slope_sum,
+                                                        int32_t ngrids, cudaGraphConditionalHandle cond,
+                                                        int has_cond) {
+    int any = 0;
+    for (int g = threadIdx.x; g < ngrids && a.nprob > 0; g += blockDim.x) {
+        const GridDesc &gd = c.grids[g];
+        const int cur = c.cur_lam[g];
+        if (cur + 1 >= gd.lam_end) continue;
+        if (c.swapflag[gd.prob]) c.snk_sum[g] += (a.lambdas[cur + 1] - a.lambdas[cur]) * slope_sum[gd.prob];
+        c.cur_lam[g] = cur + 1;
+        c.live[g] = 1;
+        any = 1;
+    }
+    any = __syncthreads_or(any);
+    if (threadIdx.x == 0) {
+        c.ctl->cycle = 0;   // the non-convergence guard counts cycles per step
+        c.ctl->steps++;
+        c.ctl->more = any;
+        if (has_cond) cudaGraphSetConditional(cond, any ? 1u : 0u);
     }
 }
 

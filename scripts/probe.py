@@ -34,6 +34,8 @@ def main():
     ap.add_argument("--graph", type=int, default=None)
     ap.add_argument("--warp", type=int, default=None)
     ap.add_argument("--trace", action="store_true")
+    ap.add_argument("--chain", type=int, default=None)
+    ap.add_argument("--check", action="store_true", help="compare flows with a chain=1 solve")
     ap.add_argument("--reps", type=int, default=3)
     ap.add_argument("--nprob", type=int, default=None, help="problems per device batch")
     a = ap.parse_args()
@@ -50,6 +52,12 @@ def main():
     if a.pbfs is not None: s.set("persistent_bfs", a.pbfs)
     if a.graph is not None: s.set("graph", a.graph)
     if a.warp is not None: s.set("warp", a.warp)
+    if a.chain is not None: s.set("chain", a.chain)
+    ref = None
+    if a.check:
+        r0 = _native.Solver(0, chain=1)
+        ref = r0.solve_seed_batch(c["w"], c["h"], probs, c["lams"], "auto")
+        r0.close()
     for r in range(a.reps):
         t0 = time.perf_counter()
         s.seed_stage(c["w"], c["h"], probs, c["lams"], "auto")
@@ -65,8 +73,13 @@ def main():
             tr = s.trace()
             print("trace push (us, tiles):", [(u, t) for k, u, t in tr if k == 0])
             print("trace bfs  (us, tiles):", [(u, t) for k, u, t in tr if k == 1][:30])
+        if ref is not None:
+            import numpy as np
+            ok = bool((ref[1] == flows).all()) and bool(np.array_equal(ref[2], labels))
+            print("check vs chain=1:", "OK" if ok else "MISMATCH")
         keep = ("cycles", "push_tile_passes", "bfs_tile_passes", "label_tile_passes", "push_sweeps",
-                "bfs_sweeps", "ms_device", "ms_push", "ms_bfs", "ms_labels", "launches", "graph_builds")
+                "bfs_sweeps", "ms_device", "ms_push", "ms_bfs", "ms_labels", "launches", "graph_builds",
+                "steps", "grids")
         print(json.dumps(dict(cfg=a.cfg, args=" ".join(sys.argv[2:]), rep=r,
                               wall_ms=round(dt * 1e3, 2), stage_ms=round((t1 - t0) * 1e3, 2),
                               run_ms=round((t2 - t1) * 1e3, 2), fetch_ms=round((t3 - t2) * 1e3, 2),

@@ -246,3 +246,30 @@ def test_c1_stress_repeated(engine, persistent):
                 assert np.array_equal(labels[0][j], g["labels"][j]), (rep, j)
     finally:
         s.close()
+
+
+@pytest.mark.parametrize("chain", [2, 3, 5])
+def test_warm_start_chains_match_reference(engine, chain):
+    """Warm start along the nested schedule (each grid solves `chain`
+    consecutive lambdas, reusing the previous maximum preflow) must give the
+    reference's cuts, swapped families included."""
+    from paper_1509_06004_b200 import _native
+    s = _native.Solver(0, chain=chain)
+    try:
+        for case in load_seed_supergraphs():
+            probs = _problems(case)
+            sw, flows, labels = s.solve_seed_batch(case["width"], case["height"], probs,
+                                                   case["lambdas"], case["mode"])
+            assert [bool(x) for x in sw for _ in case["lambdas"]] == case["swapped"]
+            assert flows.reshape(-1).tolist() == case["flows"]
+            assert [l.tolist() for l in labels.reshape(len(case["flows"]), -1)] == case["labels"]
+        g = load_synth("c1_160x120.npz")
+        probs = synth.generate(160, 120, rng_seed=0).problems
+        for mode in ("auto", "on"):
+            _, flows, labels = s.solve_seed_batch(160, 120, probs, g["lambdas"], mode)
+            assert flows[0].tolist() == g["flows"]
+            for j in range(20):
+                assert np.array_equal(labels[0][j], g["labels"][j]), (mode, j)
+        assert s.stats()["steps"] == chain
+    finally:
+        s.close()
