@@ -43,9 +43,19 @@ CONFIGS = {
     "c2": dict(w=500, h=375, rows=1, cols=1, types=("A",), lams="L20",
                desc="C2: synthetic 500x375 (VOC-sized), 1 seed, 20-lambda ladder L20, "
                     "one supergraph (20 lambda-graphs) per GPU per step"),
+    "c3": dict(w=500, h=375, rows=5, cols=5, types=("A", "B"), lams="L20",
+               desc="C3: one CPMC-style image per GPU per step -- synthetic 500x375, 25 seeds x "
+                    "2 seed types x 20 lambdas = 1000 lambda-graphs in one device batch "
+                    "(warm-start chains along the schedule)"),
     "c4": dict(w=1920, h=1080, rows=1, cols=1, types=("A",), lams="C4",
                desc="C4: synthetic 1920x1080, 1 seed, 8 lambdas per supergraph"),
+    "c5": dict(w=500, h=375, rows=5, cols=5, types=("A", "B"), lams="L20", images=2,
+               desc="C5: batch throughput -- 2 synthetic CPMC images (500x375, 25 seeds x 2 types "
+                    "x 20 lambdas) per GPU per step, images independent across GPUs"),
 }
+# CPU reference sample per step for the big configs (the full C3 image is
+# ~3,400 CPU-s on the reference algorithm): the first problems' lambda graphs
+REF_SAMPLE_PROBLEMS = {"c3": 2, "c5": 2, "c4": 1}
 BYTES_PER_PIXEL_PASS = {4: 24, 16: 48}   # load+store of w, h and the residual word(s)
 
 
@@ -158,17 +168,17 @@ class ClockSampler:
 
 # ------------------------------------------------------------- CPU baseline
 
-def cpu_solve_config(cfg, rng_seed, threads):
+def cpu_solve_config(cfg, rng_seed, threads, max_problems=None):
     """The reference's solver (C restatement in oracle/) on every lambda graph
-    of one supergraph, per lambda as solve_schedule_sequential does; returns
-    (n_cuts, seconds, total_flow)."""
+    of one supergraph (or of the first ``max_problems`` problems), per lambda
+    as solve_schedule_sequential does; returns (n_cuts, seconds, total_flow)."""
     import oracle
     from paper_1509_06004_b200 import synth
     lams = lambdas_for(cfg["lams"])
     batch = synth.generate(cfg["w"], cfg["h"], cfg["rows"], cfg["cols"], rng_seed=rng_seed,
                            types=cfg["types"])
     jobs = []
-    for p in batch.problems:
+    for p in batch.problems[:max_problems]:
         for lam in lams:
             s, t, nb = oracle.instantiate(p.unary_base, p.unary_slope, p.sink_base, p.pairwise,
                                           p.fg_seeds, p.bg_seeds, lam)
@@ -186,15 +196,18 @@ def run_reference(args, cfg):
     import oracle
     oracle.build()
     threads = os.cpu_count() or 1
+    mp = REF_SAMPLE_PROBLEMS.get(args.config)
     for _ in range(args.warmup):
-        cpu_solve_config(cfg, 0, threads)
+        cpu_solve_config(cfg, 0, threads, mp)
     tot_cuts, tot_s = 0, 0.0
     for _ in range(args.steps):
-        n, dt, _ = cpu_solve_config(cfg, 0, threads)
+        n, dt, _ = cpu_solve_config(cfg, 0, threads, mp)
         tot_cuts += n
         tot_s += dt
     value = tot_cuts / tot_s
-    sample = (f"{cfg['desc']}: all lambda-graphs of one supergraph per step, solved with the "
+    what = (f"the lambda-graphs of the first {mp} seed problems" if mp else
+            "all lambda-graphs of one supergraph")
+    sample = (f"{cfg['desc']}: {what} per step ({tot_cuts // args.steps} graphs), solved with the "
               f"reference push-relabel restated in C (oracle/pmflow_oracle.c), per lambda as "
               f"solve_schedule_sequential, {threads} host threads")
     print(json.dumps({
@@ -218,15 +231,22 @@ def run_b200(args, cfg):
     from paper_1509_06004_b200.supergraph import check_seed_supergraph
 
     rank, local, world = dist_env()
-    torch.cuda.set_device(local)
+    ndev = torch.cuda.device_count()
+    dev = local % ndev          # one GPU per rank (shared only when testing N > #GPUs)
+    torch.cuda.set_device(dev)
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-    dev = local
+        if ndev >= world:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", dev))
+        else:   # NCCL cannot put two ranks on one GPU: plumbing-only test mode
+            dist.init_process_group("gloo")
     sched = LambdaSchedule(lambdas_for(cfg["lams"]))
-    # weak scaling: rank r owns its own image (rng_seed = r)
-    batch = synth.generate(cfg["w"], cfg["h"], cfg["rows"], cfg["cols"], rng_seed=rank,
-                           types=cfg["types"])
-    problems = check_seed_supergraph(batch.problems, sched, "auto")
+    # weak scaling: rank r owns its own images (rng_seed = r * images + i)
+    nimg = cfg.get("images", 1)
+    problems = []
+    for i in range(nimg):
+        batch = synth.generate(cfg["w"], cfg["h"], cfg["rows"], cfg["cols"],
+                               rng_seed=rank * nimg + i, types=cfg["types"])
+        problems += check_seed_supergraph(batch.problems, sched, "auto")
     cuts_per_step = len(problems) * len(sched)
 
     solver = _native.solver_for_thread(dev)
@@ -295,7 +315,7 @@ def run_b200(args, cfg):
 
     # ---- CPMC image (C3) device time, reported beside the headline
     cpmc = None
-    if args.cpmc and rank == 0:
+    if args.cpmc and rank == 0 and args.config not in ("c3", "c5"):
         c3 = synth.generate(500, 375, 5, 5, rng_seed=0, types=("A", "B"))
         c3p = check_seed_supergraph(c3.problems, sched, "auto")
         s3 = _native.Solver(dev)
@@ -314,10 +334,15 @@ def run_b200(args, cfg):
         import oracle
         oracle.build()
         threads = os.cpu_count() or 1
-        n, dt, flow = cpu_solve_config(cfg, 0, threads)
-        assert flow == int(ref_flows.sum()), "oracle and engine disagree on the C2 flow"
+        mp = REF_SAMPLE_PROBLEMS.get(args.config)
+        n, dt, flow = cpu_solve_config(cfg, 0, threads, mp)
+        if mp is None:
+            assert flow == int(ref_flows.sum()), "oracle and engine disagree on the flow"
+        else:
+            assert flow == int(ref_flows.reshape(-1)[:n].sum()), "oracle and engine disagree"
         cpu = {"value": n / dt, "unit": UNIT, "cores": threads, "kind": "port",
-               "sample": f"{n} lambda-graphs of the rank-0 supergraph ({cfg['desc'].split(':')[0]}), "
+               "sample": f"{n} lambda-graphs of the rank-0 batch ({cfg['desc'].split(':')[0]}"
+                         f"{', first %d problems' % mp if mp else ''}), "
                          "reference push-relabel restated in C (oracle/pmflow_oracle.c), "
                          f"per lambda, {threads} threads; took {dt:.2f} s"}
 
@@ -343,11 +368,14 @@ def run_b200(args, cfg):
             "cpu_baseline": cpu,
             "clocks": clk.summary(),
             "gpu_launches": int(sum(s["kernels"] for s in stats)),
-            "solver": {k: stats[-1][k] for k in ("cycles", "push_sweeps", "push_tile_passes",
+            "solver": {k: stats[-1][k] for k in ("cycles", "steps", "push_sweeps", "push_tile_passes",
                                                   "bfs_sweeps", "bfs_tile_passes", "tiles",
-                                                  "edge_bytes")},
+                                                  "edge_bytes", "grids")},
             "cpmc": cpmc,
         }
+        if args.config in ("c3", "c5"):
+            line["ms_per_image"] = 1e3 * dev_s_max / args.steps / nimg
+            line["e2e"]["ms_per_image"] = 1e3 * e2e_s_max / args.steps / nimg
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()

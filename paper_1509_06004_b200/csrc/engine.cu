@@ -187,6 +187,7 @@ struct pmf_solver {
     int persistent_bfs = 0;   // BFS phases as one persistent launch
     int push_budget = 2;      // persistent push phase: pops <= budget * seeded tiles
     int chain = 0;            // warm-start chain length (0: auto from warm_grids)
+    int relax_cap = 0;        // sweep cap of the discharge's local relabel (0: to the fixpoint)
     int warm_grids = 200;     // auto chains: aim for about this many grids per batch
     int bfs_chunk = 8;
     int timing = 0;
@@ -373,7 +374,8 @@ void launch_push(pmf_solver *s, const Ctx &c, int k) {
         LAUNCH(s, (k_wpush<E><<<s->grid_wpush, WPB * 32, s->smem_w, s->st>>>(c, k, s->push_iters, s->relabel_every,
                                                                             lctl(ST_PUSH))));
     else
-        LAUNCH(s, (k_push<E><<<s->grid_push, NTT, 0, s->st>>>(c, k, s->push_iters, s->relabel_every, lctl(ST_PUSH))));
+        LAUNCH(s, (k_push<E><<<s->grid_push, NTT, 0, s->st>>>(c, k, s->push_iters, s->relabel_every, s->relax_cap,
+                                                              lctl(ST_PUSH))));
 }
 
 // ---- host-driven loop (graph = 0): the host reads worklist lengths and the
@@ -514,7 +516,8 @@ int add_push_node(pmf_solver *s, cudaGraph_t g, cudaGraphNode_t *prev, const Ctx
     if (s->warp)
         return add_kernel_smem(g, prev, dim3(s->grid_wpush), dim3(WPB * 32), s->smem_w, k_wpush<E>, c, k,
                                s->push_iters, s->relabel_every, lc);
-    return add_kernel(g, prev, dim3(s->grid_push), dim3(NTT), k_push<E>, c, k, s->push_iters, s->relabel_every, lc);
+    return add_kernel(g, prev, dim3(s->grid_push), dim3(NTT), k_push<E>, c, k, s->push_iters, s->relabel_every,
+                      s->relax_cap, lc);
 }
 
 template <class E>
@@ -603,7 +606,7 @@ int build_graph(pmf_solver *s, const Ctx &c0, int32_t ngrids, const SeedArgs *sa
 // knobs + context a cached graph was built for
 struct GraphKey {
     Ctx ctx;
-    int32_t ngrids, edge, p_push, p_bfs, iters, relabel, budget, sweeps, warp;
+    int32_t ngrids, edge, p_push, p_bfs, iters, relabel, budget, sweeps, warp, relax_cap;
     int64_t maxc;
     int32_t gfull, gbfs, gpush;
     SeedArgs sa;
@@ -626,6 +629,7 @@ int graph_solve(pmf_solver *s, const Ctx &c0, int32_t ngrids, const SeedArgs *sa
     key.budget = s->push_budget;
     key.sweeps = s->push_sweeps;
     key.warp = s->warp;
+    key.relax_cap = s->relax_cap;
     key.maxc = s->max_cycles;
     key.gfull = s->grid_full;
     key.gbfs = s->grid_bfs;
@@ -1099,6 +1103,7 @@ int pmf_solver_set(pmf_solver *s, const char *name, int64_t v) {
     else if (k == "persistent") s->persistent = v != 0;
     else if (k == "warp") s->warp = v != 0;
     else if (k == "chain" && v >= 0 && v <= 1000000) s->chain = int(v);
+    else if (k == "relax_cap" && v >= 0 && v <= 1000) s->relax_cap = int(v);
     else if (k == "warm_grids" && v >= 1) s->warm_grids = int(v);
     else if (k == "graph") s->use_graph = v != 0;
     else if (k == "persistent_bfs") s->persistent_bfs = v != 0;

@@ -64,8 +64,11 @@ __device__ __forceinline__ int32_t line_relax(int32_t v, int m, int lane, int bl
 }
 
 // d: [32][SP] values, mk: [32][32] pull masks, hv: halo values.  All 1024
-// threads call it; returns the number of full sweeps performed.
-__device__ int tile_relax(int32_t *d, const uint8_t *mk, const int32_t (*hv)[TW], int cost) {
+// threads call it.  Runs to the fixpoint (returns 1) or stops after
+// max_sweeps sweeps (> 0; returns 0 if it had not converged) -- a capped
+// relax only gives upper bounds and its HINF values are not certificates.
+__device__ int tile_relax(int32_t *d, const uint8_t *mk, const int32_t (*hv)[TW], int cost,
+                          int max_sweeps = 0) {
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     int sweeps = 0;
     for (;;) {
@@ -82,7 +85,8 @@ __device__ int tile_relax(int32_t *d, const uint8_t *mk, const int32_t (*hv)[TW]
             if (v != v0) { d[lane * SP + warp] = v; changed = 1; }
         }
         sweeps++;
-        if (!__syncthreads_or(changed)) return sweeps;
+        if (!__syncthreads_or(changed)) return 1;
+        if (max_sweeps && sweeps >= max_sweeps) return 0;
     }
 }
 
@@ -337,7 +341,8 @@ __global__ void __launch_bounds__(NTT, 2) k_bfs_src(Ctx c, int k, LaunchCtl lc) 
 // in frozen pixels, a certificate that the pixel cannot reach the sink.
 // ---------------------------------------------------------------------------
 template <class E>
-__global__ void __launch_bounds__(NTT, 2) k_push(Ctx c, int k, int iters, int relabel_every, LaunchCtl lc) {
+__global__ void __launch_bounds__(NTT, 2) k_push(Ctx c, int k, int iters, int relabel_every, int relax_cap,
+                                                 LaunchCtl lc) {
     __shared__ int32_t sh[TH * SP];
     __shared__ int32_t sd[TH * SP];
     __shared__ int32_t sin4[4][TPIX];
@@ -377,8 +382,10 @@ __global__ void __launch_bounds__(NTT, 2) k_push(Ctx c, int k, int iters, int re
                 sd[pi] = e < 0 ? 1 : HINF;
                 sm[i] = uint8_t((r[0] > 0) | ((r[1] > 0) << 1) | ((r[2] > 0) << 2) | ((r[3] > 0) << 3));
                 __syncthreads();
-                tile_relax(sd, sm, hh, 1);
-                if (h < HINF) h = sd[pi];
+                const int conv = tile_relax(sd, sm, hh, 1, relax_cap);
+                // frozen pixels stay frozen; an unconverged relax may not
+                // freeze anyone (keep the old height where it found nothing)
+                if (h < HINF && (conv || sd[pi] < HINF)) h = sd[pi];
                 sh[pi] = h;
                 act = __syncthreads_or(e > 0 && h < HINF);
                 if (!act) break;

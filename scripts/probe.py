@@ -35,6 +35,7 @@ def main():
     ap.add_argument("--warp", type=int, default=None)
     ap.add_argument("--trace", action="store_true")
     ap.add_argument("--chain", type=int, default=None)
+    ap.add_argument("--cap", type=int, default=None)
     ap.add_argument("--check", action="store_true", help="compare flows with a chain=1 solve")
     ap.add_argument("--reps", type=int, default=3)
     ap.add_argument("--nprob", type=int, default=None, help="problems per device batch")
@@ -53,6 +54,7 @@ def main():
     if a.graph is not None: s.set("graph", a.graph)
     if a.warp is not None: s.set("warp", a.warp)
     if a.chain is not None: s.set("chain", a.chain)
+    if a.cap is not None: s.set("relax_cap", a.cap)
     ref = None
     if a.check:
         r0 = _native.Solver(0, chain=1)
