@@ -91,7 +91,9 @@ int pmf_solver_destroy(pmf_solver *s);
  * (host-driven mode: launches between convergence checks), "persistent" /
  * "persistent_bfs" (phase scheduling), "graph" (0: host-driven loop, 1:
  * whole solve as one CUDA graph), "chain" (warm-start chain length; 0:
- * auto), "warm_grids" (auto chains target about this many grids),
+ * auto: whole ladder per problem from "warm_min_problems" problems on),
+ * "push_budget_warm" (discharge budget of warm-start batches),
+ * "warp" (bit mask: warp-per-tile discharge 1 / sink BFS 2 / label BFS 4),
  * "timing" (0/1 event timings),
  * "max_cycles" (non-convergence guard). Returns PMF_ERR_ARG if unknown. */
 int pmf_solver_set(pmf_solver *s, const char *name, int64_t value);

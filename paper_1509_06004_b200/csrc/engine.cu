@@ -180,15 +180,23 @@ struct pmf_solver {
     int push_iters = 16;
     int push_sweeps = 64;
     int relabel_every = 8;
-    int warp = 0;             // 1: warp-per-tile kernels (0: 1024-thread CTA per tile)
+    // warp-per-tile kernels instead of 1024-thread CTAs, per kernel kind:
+    // bit 0 discharge, bit 1 sink BFS, bit 2 label BFS; -1: auto (label BFS
+    // always, sink BFS when the batch has >= warp_bfs_tiles tiles)
+    int warp = 4;
+    int warp_bfs_tiles = 20000;
+    int warp_eff = 0;         // resolved bits for the current batch
+    int warm_active = 0;      // the current run uses warm-start chains
     int grid_wpush = 0, grid_wbfs = 0;
     size_t smem_w = 0;
     int persistent = 1;       // discharge phase as one persistent launch
     int persistent_bfs = 0;   // BFS phases as one persistent launch
     int push_budget = 2;      // persistent push phase: pops <= budget * seeded tiles
-    int chain = 0;            // warm-start chain length (0: auto from warm_grids)
+    int chain = 0;            // warm-start chain length (0: auto, see warm_min_problems)
     int relax_cap = 0;        // sweep cap of the discharge's local relabel (0: to the fixpoint)
-    int warm_grids = 200;     // auto chains: aim for about this many grids per batch
+    int warm_min_problems = 8;  // auto: one chain per problem (whole ladder) from this many problems
+    int push_budget_warm = 4;   // discharge budget factor when the batch runs warm-start chains
+    int verify = 1;             // seed batches: device cut_cost == flow certificate per cut
     int bfs_chunk = 8;
     int timing = 0;
     int64_t max_cycles = 50000;
@@ -260,6 +268,7 @@ int setup_state(pmf_solver *s, int edge_bytes) {
         (rc = s->d_ctl.ensure(sizeof(Ctl))) || (rc = s->d_curlam.ensure(G * 4)))
         return rc;
     s->edge_bytes = edge_bytes;
+    s->warp_eff = s->warp >= 0 ? s->warp : (4 | (T >= s->warp_bfs_tiles ? 2 : 0));
     // host sources live in the solver (s->lay, s->ones) until the next setup
     CK(cudaMemcpyAsync(s->d_tile_grid.p, L.tile_grid.data(), T * 4, cudaMemcpyHostToDevice, s->st));
     CK(cudaMemcpyAsync(s->d_grids.p, L.grids.data(), G * sizeof(GridDesc), cudaMemcpyHostToDevice, s->st));
@@ -328,6 +337,12 @@ int read_ctl(pmf_solver *s, const Ctx &c, Ctl *out) {
     return 0;
 }
 
+// discharge pop budget per seeded tile (warm-start steps start closer to
+// the answer and profit from longer discharges between global relabels)
+inline int budget_factor(const pmf_solver *s) {
+    return s->warm_active ? s->push_budget_warm : s->push_budget;
+}
+
 inline LaunchCtl lctl(int stat, cudaGraphConditionalHandle h = 0, int has = 0, int max_k = 0) {
     LaunchCtl l;
     l.stat = stat;
@@ -359,7 +374,7 @@ PhaseCtx phase_ctx(pmf_solver *s, const Ctx &c0) {
 // 1024-thread-CTA kernels
 template <class E>
 void launch_bfs(pmf_solver *s, const Ctx &c, bool sink, int k) {
-    if (s->warp) {
+    if (s->warp_eff & (sink ? 2 : 4)) {
         if (sink) LAUNCH(s, (k_wbfs_sink<E><<<s->grid_wbfs, WPB * 32, s->smem_w, s->st>>>(c, k, lctl(ST_BFS))));
         else LAUNCH(s, (k_wbfs_src<E><<<s->grid_wbfs, WPB * 32, s->smem_w, s->st>>>(c, k, lctl(ST_LAB))));
     } else {
@@ -370,7 +385,7 @@ void launch_bfs(pmf_solver *s, const Ctx &c, bool sink, int k) {
 
 template <class E>
 void launch_push(pmf_solver *s, const Ctx &c, int k) {
-    if (s->warp)
+    if (s->warp_eff & 1)
         LAUNCH(s, (k_wpush<E><<<s->grid_wpush, WPB * 32, s->smem_w, s->st>>>(c, k, s->push_iters, s->relabel_every,
                                                                             lctl(ST_PUSH))));
     else
@@ -414,7 +429,7 @@ int host_solve(pmf_solver *s, const Ctx &c0, int32_t ngrids) {
         LAUNCH(s, (k_phase_begin<<<s->grid_full, 256, 0, s->st>>>(P.push, P.push.persistent, 0, 0)));
         LAUNCH(s, (k_seed_push<<<s->grid_full, NT, 0, s->st>>>(P.push)));
         LAUNCH(s, (k_cycle_ctl<<<1, 1024, 0, s->st>>>(P.push, ngrids, P.push.persistent,
-                                                      unsigned(s->push_budget), s->max_cycles, 0, 0)));
+                                                      unsigned(budget_factor(s)), s->max_cycles, 0, 0)));
         CK(cudaGetLastError());
         s->stats.full_passes++;
         Ctl ctl;
@@ -502,7 +517,7 @@ int add_while(cudaGraph_t g, cudaGraphNode_t *prev, cudaGraphConditionalHandle h
 template <class E>
 int add_bfs_node(pmf_solver *s, cudaGraph_t g, cudaGraphNode_t *prev, bool sink, const Ctx &c, int k,
                  LaunchCtl lc) {
-    if (s->warp) {
+    if (s->warp_eff & (sink ? 2 : 4)) {
         if (sink)
             return add_kernel_smem(g, prev, dim3(s->grid_wbfs), dim3(WPB * 32), s->smem_w, k_wbfs_sink<E>, c, k, lc);
         return add_kernel_smem(g, prev, dim3(s->grid_wbfs), dim3(WPB * 32), s->smem_w, k_wbfs_src<E>, c, k, lc);
@@ -513,7 +528,7 @@ int add_bfs_node(pmf_solver *s, cudaGraph_t g, cudaGraphNode_t *prev, bool sink,
 
 template <class E>
 int add_push_node(pmf_solver *s, cudaGraph_t g, cudaGraphNode_t *prev, const Ctx &c, int k, LaunchCtl lc) {
-    if (s->warp)
+    if (s->warp_eff & 1)
         return add_kernel_smem(g, prev, dim3(s->grid_wpush), dim3(WPB * 32), s->smem_w, k_wpush<E>, c, k,
                                s->push_iters, s->relabel_every, lc);
     return add_kernel(g, prev, dim3(s->grid_push), dim3(NTT), k_push<E>, c, k, s->push_iters, s->relabel_every,
@@ -563,7 +578,7 @@ int build_graph(pmf_solver *s, const Ctx &c0, int32_t ngrids, const SeedArgs *sa
             return rc;
         if ((rc = add_kernel(cyc, &q, gfull, dim3(NT), k_seed_push, P.push))) return rc;
         if ((rc = add_kernel(cyc, &q, dim3(1), dim3(1024), k_cycle_ctl, P.push, ngrids, int(P.push.persistent),
-                             unsigned(s->push_budget), int64_t(s->max_cycles), h_cycle, 1)))
+                             unsigned(budget_factor(s)), int64_t(s->max_cycles), h_cycle, 1)))
             return rc;
         if (P.push.persistent) {
             if ((rc = add_push_node<E>(s, cyc, &q, P.pq, K_PERSISTENT, lctl(ST_PUSH)))) return rc;
@@ -626,9 +641,9 @@ int graph_solve(pmf_solver *s, const Ctx &c0, int32_t ngrids, const SeedArgs *sa
     key.p_bfs = s->persistent_bfs;
     key.iters = s->push_iters;
     key.relabel = s->relabel_every;
-    key.budget = s->push_budget;
+    key.budget = budget_factor(s);
     key.sweeps = s->push_sweeps;
-    key.warp = s->warp;
+    key.warp = s->warp_eff;
     key.relax_cap = s->relax_cap;
     key.maxc = s->max_cycles;
     key.gfull = s->grid_full;
@@ -744,6 +759,7 @@ int run_end(pmf_solver *s) {
         return fail(PMF_ERR_NOCONV, "push-relabel failed to converge within %lld cycles",
                     (long long)s->max_cycles);
     if (err == 4) return fail(PMF_ERR_NONMAX, "source side touches an unsaturated sink edge");
+    if (err == 5) return fail(PMF_ERR_NONMAX, "a cut's cost differs from its flow (integrity check)");
     if (err) return fail(PMF_ERR_CUDA, "device error code %d", err);
     return 0;
 }
@@ -829,8 +845,15 @@ int seed_run_t(pmf_solver *s) {
     CK(cudaGetLastError());
     s->stats.full_passes++;
     const bool chains = S.chain > 1;
-    return run_solve<E>(s, c, int32_t(s->lay.grids.size()), chains ? &a : nullptr,
-                        chains ? s->d_slopesum.as<int64_t>() : nullptr);
+    s->warm_active = chains;
+    int rc2 = run_solve<E>(s, c, int32_t(s->lay.grids.size()), chains ? &a : nullptr,
+                           chains ? s->d_slopesum.as<int64_t>() : nullptr);
+    if (rc2) return rc2;
+    if (s->verify) {
+        LAUNCH(s, (k_verify<<<int(std::min<int64_t>(int64_t(S.nprob) * S.nlam, 8 * s->sms)), NT, 0, s->st>>>(c, a)));
+        CK(cudaGetLastError());
+    }
+    return 0;
 }
 
 int seed_stage(pmf_solver *s, int32_t nprob, int32_t W, int32_t H, const int64_t *const *ub,
@@ -950,11 +973,11 @@ int seed_stage(pmf_solver *s, int32_t nprob, int32_t W, int32_t H, const int64_t
     CK(cudaMemcpyAsync(s->d_lam.p, S.lambdas.data(), size_t(nlam) * 8, cudaMemcpyHostToDevice, s->st));
     // warm-start chains: nlam lambdas split into chains of S.chain
     // consecutive values; each chain is one grid solved step by step
+    // auto: enough problems keep the GPU busy with one grid per problem, so
+    // each solves its whole ladder warm; few problems are latency-bound and
+    // solve every lambda cold and in parallel
     int32_t chain = s->chain;
-    if (chain <= 0) {
-        const int64_t per_problem = std::max<int64_t>(1, cdiv(s->warm_grids, nprob));
-        chain = int32_t(cdiv(nlam, std::min<int64_t>(per_problem, nlam)));
-    }
+    if (chain <= 0) chain = nprob >= s->warm_min_problems ? nlam : 1;
     chain = std::max(1, std::min(chain, nlam));
     S.chain = chain;
     s->lay.clear();
@@ -1020,6 +1043,7 @@ int seed_fetch(pmf_solver *s, uint8_t *swapped_out, int64_t *flows_out, uint8_t 
 
 template <class E>
 int comp_run_t(pmf_solver *s, int ncomp, int64_t total_px) {
+    s->warm_active = 0;
     int rc = grids_for<E>(s);
     if (rc) return rc;
     if ((rc = setup_state(s, E::kBytes))) return rc;
@@ -1101,10 +1125,13 @@ int pmf_solver_set(pmf_solver *s, const char *name, int64_t v) {
     else if (k == "bfs_chunk" && v >= 1 && v <= 100000) s->bfs_chunk = int(v);
     else if (k == "relabel_every" && v >= 0 && v <= 100000) s->relabel_every = int(v);
     else if (k == "persistent") s->persistent = v != 0;
-    else if (k == "warp") s->warp = v != 0;
+    else if (k == "warp" && v >= -1 && v <= 7) s->warp = int(v);
+    else if (k == "warp_bfs_tiles" && v >= 0) s->warp_bfs_tiles = int(v);
     else if (k == "chain" && v >= 0 && v <= 1000000) s->chain = int(v);
     else if (k == "relax_cap" && v >= 0 && v <= 1000) s->relax_cap = int(v);
-    else if (k == "warm_grids" && v >= 1) s->warm_grids = int(v);
+    else if (k == "warm_min_problems" && v >= 1) s->warm_min_problems = int(v);
+    else if (k == "push_budget_warm" && v >= 0) s->push_budget_warm = int(v);
+    else if (k == "verify") s->verify = v != 0;
     else if (k == "graph") s->use_graph = v != 0;
     else if (k == "persistent_bfs") s->persistent_bfs = v != 0;
     else if (k == "push_budget" && v >= 0) s->push_budget = int(v);

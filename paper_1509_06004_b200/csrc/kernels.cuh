@@ -386,6 +386,39 @@ __global__ void __launch_bounds__(NT) k_advance_tiles(Ctx c, SeedArgs a) {
     }
 }
 
+// Integrity certificate per (problem, lambda) (grid.py:159-178 cut_cost;
+// the reference checks it in split(), supergraph.py:181-186, and in the RPC
+// client, rpc.py:328-331): the cut cost of the emitted mask of the ORIGINAL
+// graph must equal the flow.  One CTA per (problem, lambda) plane.
+__global__ void __launch_bounds__(NT) k_verify(Ctx c, SeedArgs a) {
+    __shared__ int64_t red[NT / 32];
+    const int64_t n = int64_t(a.W) * a.H;
+    for (int64_t plane = blockIdx.x; plane < int64_t(a.nprob) * a.nlam; plane += gridDim.x) {
+        const int p = int(plane / a.nlam), j = int(plane % a.nlam);
+        const int64_t lam = a.lambdas[j];
+        const uint8_t *lab = c.out + plane * n;
+        const int64_t po = a.plane_off[p];
+        const int32_t *pw = a.pw + a.pw_off[p];
+        int64_t cost = 0;
+        for (int64_t q = threadIdx.x; q < n; q += NT) {
+            const uint8_t m = a.mask[int64_t(p) * n + q];
+            const int x = int(q % a.W), y = int(q / a.W);
+            if (lab[q]) {
+                cost += m == 2 ? CAP_MAX : int64_t(a.sink[po + q]);
+                // arcs leaving the source side (off-grid counts as source side)
+                if (x > 0 && !lab[q - 1]) cost += pw[0 * n + q];
+                if (x + 1 < a.W && !lab[q + 1]) cost += pw[1 * n + q];
+                if (y > 0 && !lab[q - a.W]) cost += pw[2 * n + q];
+                if (y + 1 < a.H && !lab[q + a.W]) cost += pw[3 * n + q];
+            } else {
+                cost += m == 1 ? CAP_MAX : int64_t(a.base[po + q]) + lam * int64_t(a.slope[po + q]);
+            }
+        }
+        const int64_t tot = block_sum64(cost, red);
+        if (threadIdx.x == 0 && tot != c.flows[plane]) atomicExch(c.err, 5);
+    }
+}
+
 // One CTA: advance every grid with a next lambda (cur_lam, live, embedded
 // sink-capacity sum) and tell the step loop whether another step runs.
 __global__ void __launch_bounds__(1024) k_advance_grids(Ctx c, SeedArgs a, const int64_t *slope_sum,

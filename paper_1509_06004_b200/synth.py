@@ -88,6 +88,17 @@ def seed_problem(img, x, y, pairwise, bg):
                        pairwise=pairwise, fg_seeds=frozenset({idx}), bg_seeds=bg)
 
 
+def quantize_weights(values, scale: int = 1 << 16) -> np.ndarray:
+    """Real-valued weights to integer capacities, round half up at ``scale``
+    (harness/synth.py:139-151); negative weights are rejected."""
+    if scale < 1:
+        raise ValueError("scale must be positive")
+    q = np.floor(np.asarray(values, np.float64) * scale + 0.5).astype(np.int64)
+    if q.size and int(q.min()) < 0:
+        raise ValueError("weights must be non-negative")
+    return q
+
+
 @dataclass
 class SynthBatch:
     image: np.ndarray

@@ -260,3 +260,26 @@ def test_run_dynamic_retries_once_then_aborts():
             run_dynamic([Task(id=i) for i in range(5)], [WorkerHandle(0), WorkerHandle(1)], backend)
     finally:
         backend.close()
+
+
+# ------------------------------------------------------------- synth
+
+def test_quantize_weights_rounds_half_up():
+    """harness/synth.py:139-151 semantics (test_harness.py:78-84)."""
+    from paper_1509_06004_b200.synth import quantize_weights
+    assert quantize_weights([0.0, 0.125, 0.375, 1.0], scale=4).tolist() == [0, 1, 2, 4]
+    with pytest.raises(ValueError):
+        quantize_weights([-0.1])
+    with pytest.raises(ValueError):
+        quantize_weights([1.0], scale=0)
+
+
+def test_synth_type_b_and_lattice():
+    from paper_1509_06004_b200 import synth
+    b = synth.generate(24, 20, 2, 3, rng_seed=1, types=("A", "B"))
+    assert len(b.problems) == 12 and b.coords == synth.lattice(24, 20, 2, 3)
+    a, bb = b.problems[0], b.problems[1]
+    assert a.fg_seeds == bb.fg_seeds
+    top = set(range(24))
+    assert bb.bg_seeds == a.bg_seeds - top
+    assert np.array_equal(a.unary_base, bb.unary_base)
