@@ -168,10 +168,13 @@ int pmf_seed_stage(pmf_solver *s, int32_t nprob, int32_t width, int32_t height,
 int pmf_seed_run(pmf_solver *s);
 int pmf_seed_fetch(pmf_solver *s, uint8_t *swapped_out, int64_t *flows_out, uint8_t *labels_out);
 
-/* Diagnostics: the first (up to *n, at most 64) tile-kernel launches of the
- * last run: kind (0 discharge, 1 sink BFS, 2 label BFS), device span in us,
- * tile passes.  *n is updated to the number returned. */
-int pmf_debug_trace(pmf_solver *s, int32_t *kind, double *us, int64_t *tiles, int32_t *n);
+/* Diagnostics: the first (up to *n, at most 256) tile-kernel launches of the
+ * last run: kind (0 discharge, 1 sink BFS, 2 label BFS; 4-6 one sweep of a
+ * multi-sweep launch of kind 0-2), device span in us,
+ * start in us after the first traced launch, tile passes.  *n is updated to
+ * the number returned. */
+int pmf_debug_trace(pmf_solver *s, int32_t *kind, double *us, double *start_us, int64_t *tiles,
+                    int32_t *n);
 
 /* Diagnostics: copy the tile-major device state of the last run (w, h,
  * residual words, source-side flags; any pointer may be NULL) and the tile

@@ -80,7 +80,7 @@ def load_library(path: str = LIB_PATH):
         lib.pmf_seed_fetch.argtypes = [vp, P(u8), P(i64), P(u8)]
         lib.pmf_solver_stream.argtypes = [vp, P(vp)]
         lib.pmf_debug_state.argtypes = [vp, vp, vp, vp, vp, P(i64)]
-        lib.pmf_debug_trace.argtypes = [vp, vp, vp, vp, P(i32)]
+        lib.pmf_debug_trace.argtypes = [vp, vp, vp, vp, vp, P(i32)]
         for name in EXPORTS:
             if name != "pmf_last_error":
                 getattr(lib, name).restype = ctypes.c_int
@@ -191,15 +191,18 @@ class Solver:
         return w, h, r, lab
 
     def trace(self):
-        """[(kind, us, tile_passes)] of the first tile-kernel launches of the
-        last run (kind: 0 discharge, 1 sink BFS, 2 label BFS)."""
-        n = ctypes.c_int32(64)
-        kind = np.zeros(64, np.int32)
-        us = np.zeros(64, np.float64)
-        tiles = np.zeros(64, np.int64)
-        self._lib.pmf_debug_trace(self._h, kind.ctypes.data, us.ctypes.data, tiles.ctypes.data,
-                                  ctypes.byref(n))
-        return [(int(kind[i]), round(float(us[i]), 1), int(tiles[i])) for i in range(n.value)]
+        """[(kind, us, tile_passes, start_us)] of the first tile-kernel launches
+        of the last run (kind: 0 discharge, 1 sink BFS, 2 label BFS; start_us
+        relative to the first traced launch)."""
+        n = ctypes.c_int32(256)
+        kind = np.zeros(256, np.int32)
+        us = np.zeros(256, np.float64)
+        t0 = np.zeros(256, np.float64)
+        tiles = np.zeros(256, np.int64)
+        self._lib.pmf_debug_trace(self._h, kind.ctypes.data, us.ctypes.data, t0.ctypes.data,
+                                  tiles.ctypes.data, ctypes.byref(n))
+        return [(int(kind[i]), round(float(us[i]), 1), int(tiles[i]), round(float(t0[i]), 1))
+                for i in range(n.value)]
 
     def stream_handle(self) -> int:
         """The solver's cudaStream_t as an integer (torch.cuda.ExternalStream)."""

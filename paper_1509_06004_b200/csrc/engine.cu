@@ -191,6 +191,7 @@ struct pmf_solver {
     size_t smem_w = 0;
     int persistent = 1;       // discharge phase as one persistent launch
     int persistent_bfs = 0;   // BFS phases as one persistent launch
+    int bfs_multi = 1;        // BFS phases as one cooperative launch (grid barriers between sweeps)
     int push_budget = 2;      // persistent push phase: pops <= budget * seeded tiles
     int chain = 0;            // warm-start chain length (0: auto, see warm_min_problems)
     int relax_cap = 0;        // sweep cap of the discharge's local relabel (0: to the fixpoint)
@@ -372,8 +373,36 @@ PhaseCtx phase_ctx(pmf_solver *s, const Ctx &c0) {
 
 // ---- tile-kernel launchers: warp-per-tile kernels (default) or the
 // 1024-thread-CTA kernels
+// cooperative launch (every CTA co-resident) for the K_MULTI kernels
+template <class... KArgs, class... Args>
+cudaError_t launch_coop(void (*f)(KArgs...), int grid, int block, size_t smem, cudaStream_t st, Args... args) {
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(grid);
+    cfg.blockDim = dim3(block);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeCooperative;
+    at[0].val.cooperative = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, f, args...);
+}
+
 template <class E>
 void launch_bfs(pmf_solver *s, const Ctx &c, bool sink, int k) {
+    if (k == K_MULTI) {
+        const LaunchCtl lc = lctl(sink ? ST_BFS : ST_LAB);
+        cudaError_t e;
+        if (s->warp_eff & (sink ? 2 : 4))
+            e = launch_coop(sink ? k_wbfs_sink<E> : k_wbfs_src<E>, s->grid_wbfs, WPB * 32, s->smem_w, s->st, c, k,
+                            lc);
+        else
+            e = launch_coop(sink ? k_bfs_sink<E> : k_bfs_src<E>, s->grid_bfs, NTT, 0, s->st, c, k, lc);
+        (void)e;   // surfaced by the caller's cudaGetLastError
+        s->stats.launches++;
+        return;
+    }
     if (s->warp_eff & (sink ? 2 : 4)) {
         if (sink) LAUNCH(s, (k_wbfs_sink<E><<<s->grid_wbfs, WPB * 32, s->smem_w, s->st>>>(c, k, lctl(ST_BFS))));
         else LAUNCH(s, (k_wbfs_src<E><<<s->grid_wbfs, WPB * 32, s->smem_w, s->st>>>(c, k, lctl(ST_LAB))));
@@ -399,6 +428,11 @@ template <class E>
 int host_bfs(pmf_solver *s, const Ctx &c, bool sink) {
     if (c.persistent) {   // one launch; the queue drains on the device
         launch_bfs<E>(s, c, sink, K_PERSISTENT);
+        CK(cudaGetLastError());
+        return 0;
+    }
+    if (s->bfs_multi) {   // one cooperative launch runs every sweep
+        launch_bfs<E>(s, c, sink, K_MULTI);
         CK(cudaGetLastError());
         return 0;
     }
@@ -515,8 +549,8 @@ int add_while(cudaGraph_t g, cudaGraphNode_t *prev, cudaGraphConditionalHandle h
 }
 
 template <class E>
-int add_bfs_node(pmf_solver *s, cudaGraph_t g, cudaGraphNode_t *prev, bool sink, const Ctx &c, int k,
-                 LaunchCtl lc) {
+int add_bfs_node_raw(pmf_solver *s, cudaGraph_t g, cudaGraphNode_t *prev, bool sink, const Ctx &c, int k,
+                     LaunchCtl lc) {
     if (s->warp_eff & (sink ? 2 : 4)) {
         if (sink)
             return add_kernel_smem(g, prev, dim3(s->grid_wbfs), dim3(WPB * 32), s->smem_w, k_wbfs_sink<E>, c, k, lc);
@@ -524,6 +558,17 @@ int add_bfs_node(pmf_solver *s, cudaGraph_t g, cudaGraphNode_t *prev, bool sink,
     }
     if (sink) return add_kernel(g, prev, dim3(s->grid_bfs), dim3(NTT), k_bfs_sink<E>, c, k, lc);
     return add_kernel(g, prev, dim3(s->grid_bfs), dim3(NTT), k_bfs_src<E>, c, k, lc);
+}
+
+template <class E>
+int add_bfs_node(pmf_solver *s, cudaGraph_t g, cudaGraphNode_t *prev, bool sink, const Ctx &c, int k,
+                 LaunchCtl lc) {
+    int rc = add_bfs_node_raw<E>(s, g, prev, sink, c, k, lc);
+    if (rc || k != K_MULTI) return rc;
+    cudaLaunchAttributeValue v{};
+    v.cooperative = 1;
+    CK(cudaGraphKernelNodeSetAttribute(*prev, cudaLaunchAttributeCooperative, &v));
+    return 0;
 }
 
 template <class E>
@@ -559,13 +604,16 @@ int build_graph(pmf_solver *s, const Ctx &c0, int32_t ngrids, const SeedArgs *sa
     {   // ---- one cycle: exact global relabel, seeding, discharge
         cudaGraphNode_t q = nullptr;
         cudaGraphConditionalHandle h_bfs = 0, h_push = 0;
-        if (!P.bfs.persistent) CK(cudaGraphConditionalHandleCreate(&h_bfs, cyc, 0, 0));
+        const bool bfs_loop = !P.bfs.persistent && !s->bfs_multi;
+        if (bfs_loop) CK(cudaGraphConditionalHandleCreate(&h_bfs, cyc, 0, 0));
         if ((rc = add_kernel(cyc, &q, gfull, dim3(256), k_phase_begin, P.bfs, int(P.bfs.persistent), h_bfs,
-                             int(!P.bfs.persistent))))
+                             int(bfs_loop))))
             return rc;
         if ((rc = add_kernel(cyc, &q, gfull, dim3(NT), k_gr_init, P.bfs))) return rc;
         if (P.bfs.persistent) {
             if ((rc = add_bfs_node<E>(s, cyc, &q, true, P.bfs, K_PERSISTENT, lctl(ST_BFS)))) return rc;
+        } else if (s->bfs_multi) {
+            if ((rc = add_bfs_node<E>(s, cyc, &q, true, P.bfs, K_MULTI, lctl(ST_BFS)))) return rc;
         } else {
             cudaGraph_t body;
             if ((rc = add_while(cyc, &q, h_bfs, &body))) return rc;
@@ -594,13 +642,16 @@ int build_graph(pmf_solver *s, const Ctx &c0, int32_t ngrids, const SeedArgs *sa
     }
     // ---- labels
     cudaGraphConditionalHandle h_lab = 0;
-    if (!P.bfs.persistent) CK(cudaGraphConditionalHandleCreate(&h_lab, g, 0, 0));
+    const bool lab_loop = !P.bfs.persistent && !s->bfs_multi;
+    if (lab_loop) CK(cudaGraphConditionalHandleCreate(&h_lab, g, 0, 0));
     if ((rc = add_kernel(g, &prev, gfull, dim3(256), k_phase_begin, P.bfs, int(P.bfs.persistent), h_lab,
-                         int(!P.bfs.persistent))))
+                         int(lab_loop))))
         return rc;
     if ((rc = add_kernel(g, &prev, gfull, dim3(NT), k_lab_seed, P.bfs))) return rc;
     if (P.bfs.persistent) {
         if ((rc = add_bfs_node<E>(s, g, &prev, false, P.bfs, K_PERSISTENT, lctl(ST_LAB)))) return rc;
+    } else if (s->bfs_multi) {
+        if ((rc = add_bfs_node<E>(s, g, &prev, false, P.bfs, K_MULTI, lctl(ST_LAB)))) return rc;
     } else {
         cudaGraph_t body;
         if ((rc = add_while(g, &prev, h_lab, &body))) return rc;
@@ -621,7 +672,7 @@ int build_graph(pmf_solver *s, const Ctx &c0, int32_t ngrids, const SeedArgs *sa
 // knobs + context a cached graph was built for
 struct GraphKey {
     Ctx ctx;
-    int32_t ngrids, edge, p_push, p_bfs, iters, relabel, budget, sweeps, warp, relax_cap;
+    int32_t ngrids, edge, p_push, p_bfs, iters, relabel, budget, sweeps, warp, relax_cap, multi;
     int64_t maxc;
     int32_t gfull, gbfs, gpush;
     SeedArgs sa;
@@ -645,6 +696,7 @@ int graph_solve(pmf_solver *s, const Ctx &c0, int32_t ngrids, const SeedArgs *sa
     key.sweeps = s->push_sweeps;
     key.warp = s->warp_eff;
     key.relax_cap = s->relax_cap;
+    key.multi = s->bfs_multi;
     key.maxc = s->max_cycles;
     key.gfull = s->grid_full;
     key.gbfs = s->grid_bfs;
@@ -790,8 +842,12 @@ int grids_for(pmf_solver *s) {
     int occ = 0;
     CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_push<E>, NTT, 0));
     s->grid_push = std::max(1, occ) * s->sms;
+    // BFS grids are co-resident (cooperative K_MULTI launches): the smaller
+    // occupancy of the sink and label kernels
+    int occ2 = 0;
     CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_bfs_sink<E>, NTT, 0));
-    s->grid_bfs = std::max(1, occ) * s->sms;
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ2, k_bfs_src<E>, NTT, 0));
+    s->grid_bfs = std::max(1, std::min(occ, occ2)) * s->sms;
     s->smem_w = WPB * sizeof(WarpTile<E>);
     CK(cudaFuncSetAttribute(k_wpush<E>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(s->smem_w)));
     CK(cudaFuncSetAttribute(k_wbfs_sink<E>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(s->smem_w)));
@@ -799,7 +855,8 @@ int grids_for(pmf_solver *s) {
     CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_wpush<E>, WPB * 32, s->smem_w));
     s->grid_wpush = std::max(1, occ) * s->sms;
     CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_wbfs_sink<E>, WPB * 32, s->smem_w));
-    s->grid_wbfs = std::max(1, occ) * s->sms;
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ2, k_wbfs_src<E>, WPB * 32, s->smem_w));
+    s->grid_wbfs = std::max(1, std::min(occ, occ2)) * s->sms;
     s->grid_full = 8 * s->sms;
     return 0;
 }
@@ -1134,6 +1191,7 @@ int pmf_solver_set(pmf_solver *s, const char *name, int64_t v) {
     else if (k == "verify") s->verify = v != 0;
     else if (k == "graph") s->use_graph = v != 0;
     else if (k == "persistent_bfs") s->persistent_bfs = v != 0;
+    else if (k == "bfs_multi") s->bfs_multi = v != 0;
     else if (k == "push_budget" && v >= 0) s->push_budget = int(v);
     else if (k == "timing") s->timing = v != 0;
     else if (k == "max_cycles" && v >= 1) s->max_cycles = v;
@@ -1255,7 +1313,8 @@ int pmf_solve_composites(pmf_solver *s, int32_t ncomp, const int32_t *width, con
     return 0;
 }
 
-int pmf_debug_trace(pmf_solver *s, int32_t *kind, double *us, int64_t *tiles, int32_t *n) {
+int pmf_debug_trace(pmf_solver *s, int32_t *kind, double *us, double *start_us, int64_t *tiles,
+                    int32_t *n) {
     if (!s || !n) return fail(PMF_ERR_ARG, "null argument");
     CK(cudaSetDevice(s->device));
     Ctl ctl;
@@ -1265,6 +1324,7 @@ int pmf_debug_trace(pmf_solver *s, int32_t *kind, double *us, int64_t *tiles, in
     for (int i = 0; i < m; i++) {
         if (kind) kind[i] = ctl.trace_kind[i];
         if (us) us[i] = double(ctl.trace_ns[i]) * 1e-3;
+        if (start_us) start_us[i] = double(ctl.trace_t0[i] - ctl.trace_t0[0]) * 1e-3;
         if (tiles) tiles[i] = int64_t(ctl.trace_tiles[i] & 0xffffffffull);
     }
     *n = m;

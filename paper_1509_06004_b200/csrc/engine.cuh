@@ -39,6 +39,7 @@ enum {
 // sweep index convention of the list-driven tile kernels
 constexpr int K_PERSISTENT = -1;   // one launch drains the device queue
 constexpr int K_DEVICE = -2;       // sweep index lives in Ctl (graph-driven loop)
+constexpr int K_MULTI = -3;        // one cooperative launch runs every sweep (grid barriers)
 
 // Device-side control block of a solve (graph-driven mode keeps all loop
 // state here; the host never reads it mid-solve).
@@ -54,13 +55,35 @@ struct Ctl {
     int32_t more;           // another warm-start step follows
     unsigned long long t0;  // earliest CTA start of the current launch (ns)
     unsigned long long t1;  // latest CTA end of the current launch (ns)
+    uint32_t bar_count;     // grid barrier (K_MULTI): arrivals so far in the launch
+    uint32_t bar_pad;
     // trace of the first kTrace tile-kernel launches: kind, span (ns), tile passes
     int32_t ntrace;
-    int32_t trace_kind[64];
-    unsigned long long trace_ns[64];
-    unsigned long long trace_tiles[64];
+    int32_t trace_kind[256];
+    unsigned long long trace_ns[256];
+    unsigned long long trace_tiles[256];
+    unsigned long long trace_t0[256];  // absolute start of the launch (ns)
 };
-constexpr int kTrace = 64;
+constexpr int kTrace = 256;
+
+// Grid-wide barrier for cooperative launches (every CTA co-resident): a
+// monotonic arrival counter; barrier `round` (0, 1, ...) of the launch
+// completes when it reaches (round + 1) * gridDim.x.  The last CTA to leave
+// the launch resets it (launch_exit).  Release/acquire at gpu scope orders
+// each CTA's tile writes before the other CTAs' reads in the next sweep.
+__device__ __forceinline__ void grid_sync(Ctl *ctl, int round) {
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        const uint32_t target = uint32_t(round + 1) * gridDim.x;
+        uint32_t *ctr = &ctl->bar_count;
+        asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(ctr) : "memory");
+        uint32_t v;
+        do {
+            asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(ctr) : "memory");
+        } while (v < target);
+    }
+    __syncthreads();
+}
 
 __device__ __forceinline__ unsigned long long gtimer() {
     unsigned long long t;

@@ -19,48 +19,42 @@ constexpr int SP = TW + 1;       // padded shared-memory row stride (conflict-fr
 //
 // tile_relax: Bellman-Ford to the fixpoint of
 //     d(p) = min(d(p), d(q) + cost)   for every pull arc p <- q
-// computed as alternating row / column passes; each pass is a pair of
-// segmented min-plus scans along warp shuffles (value - cost*x carried
-// through runs of consecutive pull arcs), so a straight run of any length
-// settles in one pass and a path with k turns in about k passes.
-__device__ __forceinline__ int32_t seg_prefix_min(int32_t u, int head, int lane) {
-#pragma unroll
-    for (int off = 1; off < 32; off <<= 1) {
-        int32_t ou = __shfl_up_sync(0xffffffffu, u, off);
-        int oh = __shfl_up_sync(0xffffffffu, head, off);
-        if (lane >= off && !head) {
-            u = min(u, ou);
-            head |= oh;
-        }
-    }
-    return u;
+// computed as alternating row / column passes.  A pass is two segmented
+// min-plus scans along warp shuffles -- rightward (value - cost*x carried
+// through runs of consecutive pull-from-left arcs) and leftward -- so a
+// straight run of any length settles in one pass and a path with k turns in
+// about k passes.  The two scans are independent (a shortest path never
+// reverses inside one line), so they run interleaved from the same input,
+// and their segment bounds depend only on the masks: computed once per call
+// with ballots, each scan step is a single shuffle.
+// segment bounds of a line scan, packed: bits 0-4 first lane of my
+// rightward segment, bits 5-9 last lane of my leftward segment
+__device__ __forceinline__ unsigned line_seg(int m, int lane, int blo, int bhi) {
+    const unsigned heads = __ballot_sync(0xffffffffu, lane == 0 || !(m & blo));
+    const unsigned tails = __ballot_sync(0xffffffffu, lane == 31 || !(m & bhi));
+    const unsigned lo = 31 - __clz(heads & (0xffffffffu >> (31 - lane)));
+    const unsigned hi = __ffs(tails & (0xffffffffu << lane)) - 1;
+    return lo | (hi << 5);
 }
 
-__device__ __forceinline__ int32_t seg_suffix_min(int32_t u, int tail, int lane) {
+// one line, both directions: lo = pull from the lower index neighbour (bit
+// blo; lane 0 from *halo_lo), hi = pull from the higher one (bit bhi; lane
+// 31 from *halo_hi)
+__device__ __forceinline__ int32_t line_relax(int32_t v, int m, int lane, unsigned seg, int blo, int bhi,
+                                              const int32_t *halo_lo, const int32_t *halo_hi, int cost) {
+    int32_t a = v, b = v;
+    if (lane == 0 && (m & blo)) a = min(a, *halo_lo + cost);
+    if (lane == 31 && (m & bhi)) b = min(b, *halo_hi + cost);
+    const int lo = seg & 31, hi = (seg >> 5) & 31;
+    int32_t ua = a - cost * lane, ub = b + cost * lane;
 #pragma unroll
     for (int off = 1; off < 32; off <<= 1) {
-        int32_t ou = __shfl_down_sync(0xffffffffu, u, off);
-        int ot = __shfl_down_sync(0xffffffffu, tail, off);
-        if (lane + off < 32 && !tail) {
-            u = min(u, ou);
-            tail |= ot;
-        }
+        const int32_t oa = __shfl_up_sync(0xffffffffu, ua, off);
+        const int32_t ob = __shfl_down_sync(0xffffffffu, ub, off);
+        if (lane - off >= lo) ua = min(ua, oa);
+        if (lane + off <= hi) ub = min(ub, ob);
     }
-    return u;
-}
-
-// one direction pair along a line: lo = pull from the lower index neighbour
-// (bit blo), hi = pull from the higher index neighbour (bit bhi)
-__device__ __forceinline__ int32_t line_relax(int32_t v, int m, int lane, int blo, int bhi,
-                                              int32_t halo_lo, int32_t halo_hi, int cost) {
-    if (lane == 0 && (m & blo)) v = min(v, min(halo_lo + cost, HINF));
-    int32_t u = v - cost * lane;
-    u = seg_prefix_min(u, lane == 0 || !(m & blo), lane);
-    v = min(u + cost * lane, HINF);
-    if (lane == 31 && (m & bhi)) v = min(v, min(halo_hi + cost, HINF));
-    u = v + cost * lane;
-    u = seg_suffix_min(u, lane == 31 || !(m & bhi), lane);
-    return min(u - cost * lane, HINF);
+    return min(min(ua + cost * lane, ub - cost * lane), HINF);
 }
 
 // d: [32][SP] values, mk: [32][32] pull masks, hv: halo values.  All 1024
@@ -70,18 +64,28 @@ __device__ __forceinline__ int32_t line_relax(int32_t v, int m, int lane, int bl
 __device__ int tile_relax(int32_t *d, const uint8_t *mk, const int32_t (*hv)[TW], int cost,
                           int max_sweeps = 0) {
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    // rows: warp = y, lane = x; bits L (1) / R (2).  columns: warp = x,
+    // lane = y; bits U (4) / D (8).  Masks and segment bounds of both
+    // passes packed in one register (bits 0-3 row mask, 4-7 column mask,
+    // 8-17 row segments, 18-27 column segments).
+    unsigned pk;
+    {
+        const int mr = mk[warp * TW + lane], mc = mk[lane * TW + warp];
+        pk = unsigned(mr) | (unsigned(mc) << 4) | (line_seg(mr, lane, 1, 2) << 8) | (line_seg(mc, lane, 4, 8) << 18);
+    }
     int sweeps = 0;
     for (;;) {
         int changed = 0;
-        {   // rows: warp = y, lane = x; bits L (1) / R (2)
-            int32_t v0 = d[warp * SP + lane];
-            int32_t v = line_relax(v0, mk[warp * TW + lane], lane, 1, 2, hv[DL][warp], hv[DR][warp], cost);
+        {
+            const int32_t v0 = d[warp * SP + lane];
+            const int32_t v = line_relax(v0, pk & 15, lane, pk >> 8, 1, 2, &hv[DL][warp], &hv[DR][warp], cost);
             if (v != v0) { d[warp * SP + lane] = v; changed = 1; }
         }
         __syncthreads();
-        {   // columns: warp = x, lane = y; bits U (4) / D (8)
-            int32_t v0 = d[lane * SP + warp];
-            int32_t v = line_relax(v0, mk[lane * TW + warp], lane, 4, 8, hv[DU][warp], hv[DD][warp], cost);
+        {
+            const int32_t v0 = d[lane * SP + warp];
+            const int32_t v = line_relax(v0, (pk >> 4) & 15, lane, pk >> 18, 4, 8, &hv[DU][warp], &hv[DD][warp],
+                                         cost);
             if (v != v0) { d[lane * SP + warp] = v; changed = 1; }
         }
         sweeps++;
@@ -90,10 +94,36 @@ __device__ int tile_relax(int32_t *d, const uint8_t *mk, const int32_t (*hv)[TW]
     }
 }
 
+// diagnostics: K_MULTI sweeps as trace entries of kind 4 + stat (start
+// stamp, listed tiles; the span is filled in by the next entry)
+__device__ __forceinline__ void trace_sweep(Ctl *ctl, int stat, int32_t n) {
+    const int ix = ctl->ntrace;
+    if (ix >= kTrace) return;
+    const unsigned long long now = gtimer();
+    ctl->trace_kind[ix] = 4 + stat;
+    ctl->trace_t0[ix] = now;
+    ctl->trace_ns[ix] = 0;
+    ctl->trace_tiles[ix] = (unsigned long long)(uint32_t)n;
+    if (ix > 0 && ctl->trace_kind[ix - 1] == 4 + stat) ctl->trace_ns[ix - 1] = now - ctl->trace_t0[ix - 1];
+    ctl->ntrace = ix + 1;
+}
+
 struct TileResult {
     int again;   // the tile itself still has work
     int out;     // bit s: the neighbour on side s needs (re)processing
 };
+
+// Follow-up tiles of a processed tile into worklist k, one candidate per
+// thread j = 0..4 (0: the tile itself, 1..4: the neighbour on side j - 1)
+// so that the enqueue atomics overlap instead of running back to back.
+__device__ __forceinline__ void enqueue_follow(const Ctx &c, int k, int32_t t, const TileResult &r, int j) {
+    if (j == 0) {
+        if (r.again) enqueue(c, k, t);
+    } else if ((r.out >> (j - 1)) & 1) {
+        const TileGeo g = tile_geo(c, t);
+        if (g.nb[j - 1] >= 0) enqueue(c, k, g.nb[j - 1]);
+    }
+}
 
 // Per-launch bookkeeping shared by all CTAs of a tile kernel: device-clock
 // span of the launch (earliest CTA start .. latest CTA end, %globaltimer) and,
@@ -135,6 +165,7 @@ __device__ __forceinline__ void launch_exit(const Ctx &c, const LaunchCtl &lc, i
                 if (ctl->trace_kind[j] == lc.stat) { prev = ctl->trace_tiles[j] >> 32; break; }
             ctl->trace_kind[ix] = lc.stat;
             ctl->trace_ns[ix] = t1 > t0 ? t1 - t0 : 0ull;
+            ctl->trace_t0[ix] = t0;
             ctl->trace_tiles[ix] = (tot << 32) | ((tot - prev) & 0xffffffffull);
             ctl->ntrace = ix + 1;
         }
@@ -142,6 +173,7 @@ __device__ __forceinline__ void launch_exit(const Ctx &c, const LaunchCtl &lc, i
     ctl->t0 = ~0ull;
     ctl->t1 = 0;
     ctl->done = 0;
+    ctl->bar_count = 0;   // every CTA has passed its last grid barrier
     if (k_next >= 0) {
         int next = *(volatile int32_t *)&c.cnt[k_next % 3];
         ctl->k = k_next;
@@ -156,10 +188,68 @@ __device__ __forceinline__ void launch_exit(const Ctx &c, const LaunchCtl &lc, i
 //  * persistent mode (K_PERSISTENT): pop tiles from the device queue until
 //    the phase drains (or its pop budget is spent); follow-up tiles are
 //    queued and picked up by whichever CTA is free, with no kernel boundary.
+// Persistent-queue hand-off of a processed tile, by the lanes of one warp:
+// lanes 1..4 request the flagged neighbours concurrently, then lane 0
+// retires or requeues the tile (after the requests, so the pending count
+// never touches zero while follow-up work is being registered).
+__device__ __forceinline__ void q_follow(const Ctx &c, int32_t t, const TileResult &r, int lane, int stat) {
+    if (lane >= 1 && lane <= 4 && ((r.out >> (lane - 1)) & 1)) {
+        __threadfence();              // ... < this lane's queue-state reads
+        const TileGeo g = tile_geo(c, t);
+        if (g.nb[lane - 1] >= 0) q_request(c, g.nb[lane - 1]);
+        __threadfence();
+    }
+    __syncwarp();
+    if (lane == 0) {
+        __threadfence();
+        q_finish(c, t, r.again != 0);
+        atomicAdd(&c.stat[stat], 1ull);
+    }
+}
+
 template <class Body>
 __device__ __forceinline__ void tile_loop(const Ctx &c, int k, const LaunchCtl &lc, Body &&body) {
     __shared__ int32_t s_t, s_n;
     const int i = threadIdx.x;
+    if (k == K_MULTI) {
+        // every sweep of the phase in one cooperative launch: the same
+        // worklist discipline as sweep mode, a grid barrier in place of the
+        // kernel boundary
+        launch_enter(c);
+        if (i == 0) s_t = *(volatile int32_t *)&c.ctl->k;
+        __syncthreads();
+        int kk = s_t, sweeps = 0;
+        for (;;) {
+            if (i == 0) s_n = *(volatile int32_t *)&c.cnt[kk % 3];
+            __syncthreads();
+            const int32_t n = s_n;
+            if (n == 0) break;
+            const int32_t *lst = list_of(c, kk);
+            if (blockIdx.x == 0 && i == 0) {
+                c.cnt[(kk + 2) % 3] = 0;
+                atomicAdd(&c.stat[lc.stat], (unsigned long long)n);
+                trace_sweep(c.ctl, lc.stat, n);
+            }
+            for (int li = blockIdx.x; li < n; li += gridDim.x) {
+                const int32_t t = __ldcg(lst + li);
+                if (i == 0) inq_of(c, kk)[t] = 0;
+                TileResult r = body(t);
+                if (i < 5) enqueue_follow(c, kk + 1, t, r, i);
+                __syncthreads();
+            }
+            grid_sync(c.ctl, sweeps);
+            kk++;
+            sweeps++;
+        }
+        if (i == 0) {
+            if (blockIdx.x == 0) {
+                c.ctl->k = kk;
+                if (sweeps > 1) atomicAdd(&c.stat[ST_PUSH_L + lc.stat], (unsigned long long)(sweeps - 1));
+            }
+            launch_exit(c, lc, -1, gridDim.x);
+        }
+        return;
+    }
     if (k != K_PERSISTENT) {
         if (i == 0) {
             if (k == K_DEVICE) k = *(volatile int32_t *)&c.ctl->k;
@@ -183,12 +273,7 @@ __device__ __forceinline__ void tile_loop(const Ctx &c, int k, const LaunchCtl &
             const int32_t t = lst[li];
             if (i == 0) inq_of(c, k)[t] = 0;
             TileResult r = body(t);
-            if (i == 0) {
-                TileGeo g = tile_geo(c, t);
-                if (r.again) enqueue(c, k + 1, t);
-                for (int sd = 0; sd < 4; sd++)
-                    if ((r.out >> sd) & 1 && g.nb[sd] >= 0) enqueue(c, k + 1, g.nb[sd]);
-            }
+            if (i < 5) enqueue_follow(c, k + 1, t, r, i);
             __syncthreads();
         }
         if (i == 0) launch_exit(c, lc, k + 1, parts);
@@ -214,14 +299,7 @@ __device__ __forceinline__ void tile_loop(const Ctx &c, int k, const LaunchCtl &
         TileResult r = body(t);
         __threadfence();              // requester side: data writes < ...
         __syncthreads();
-        if (i == 0) {
-            __threadfence();          // ... < thread 0's queue-state reads
-            TileGeo g = tile_geo(c, t);
-            for (int sd = 0; sd < 4; sd++)
-                if ((r.out >> sd) & 1 && g.nb[sd] >= 0) q_request(c, g.nb[sd]);
-            q_finish(c, t, r.again != 0);
-            atomicAdd(&c.stat[lc.stat], 1ull);
-        }
+        if (i < 32) q_follow(c, t, r, i, lc.stat);
     }
     if (i == 0) launch_exit(c, lc, -1, gridDim.x);
 }

@@ -215,6 +215,38 @@ __device__ __forceinline__ void warp_loop(const Ctx &c, int k, const LaunchCtl &
     const int lane = threadIdx.x & 31;
     const int gw = blockIdx.x * WPB + (threadIdx.x >> 5);
     const int nw = gridDim.x * WPB;
+    if (k == K_MULTI) {   // as in tile_loop: all sweeps, grid barriers between them
+        if (lane == 0) atomicMin(&c.ctl->t0, gtimer());
+        int kk = *(volatile int32_t *)&c.ctl->k, sweeps = 0;
+        for (;;) {
+            const int32_t n = *(volatile int32_t *)&c.cnt[kk % 3];
+            if (n == 0) break;
+            const int32_t *lst = list_of(c, kk);
+            __syncthreads();   // every warp has read n before block 0 resets a list
+            if (gw == 0 && lane == 0) {
+                c.cnt[(kk + 2) % 3] = 0;
+                atomicAdd(&c.stat[lc.stat], (unsigned long long)n);
+            }
+            for (int li = gw; li < n; li += nw) {
+                const int32_t t = __ldcg(lst + li);
+                if (lane == 0) inq_of(c, kk)[t] = 0;
+                TileResult r = body(t);
+                if (lane < 5) enqueue_follow(c, kk + 1, t, r, lane);
+                __syncwarp();
+            }
+            grid_sync(c.ctl, sweeps);
+            kk++;
+            sweeps++;
+        }
+        if (threadIdx.x == 0) {
+            if (blockIdx.x == 0) {
+                c.ctl->k = kk;
+                if (sweeps > 1) atomicAdd(&c.stat[ST_PUSH_L + lc.stat], (unsigned long long)(sweeps - 1));
+            }
+            launch_exit(c, lc, -1, gridDim.x);
+        }
+        return;
+    }
     if (k != K_PERSISTENT) {
         if (k == K_DEVICE) k = *(volatile int32_t *)&c.ctl->k;
         const int32_t n = *(volatile int32_t *)&c.cnt[k % 3];
@@ -230,12 +262,7 @@ __device__ __forceinline__ void warp_loop(const Ctx &c, int k, const LaunchCtl &
             const int32_t t = lst[li];
             if (lane == 0) inq_of(c, k)[t] = 0;
             TileResult r = body(t);
-            if (lane == 0) {
-                TileGeo g = tile_geo(c, t);
-                if (r.again) enqueue(c, k + 1, t);
-                for (int sd = 0; sd < 4; sd++)
-                    if ((r.out >> sd) & 1 && g.nb[sd] >= 0) enqueue(c, k + 1, g.nb[sd]);
-            }
+            if (lane < 5) enqueue_follow(c, k + 1, t, r, lane);
             __syncwarp();
         }
         if (lane == 0) launch_exit(c, lc, k + 1, parts);
@@ -256,14 +283,7 @@ __device__ __forceinline__ void warp_loop(const Ctx &c, int k, const LaunchCtl &
         TileResult r = body(t);
         __threadfence();
         __syncwarp();
-        if (lane == 0) {
-            __threadfence();
-            TileGeo g = tile_geo(c, t);
-            for (int sd = 0; sd < 4; sd++)
-                if ((r.out >> sd) & 1 && g.nb[sd] >= 0) q_request(c, g.nb[sd]);
-            q_finish(c, t, r.again != 0);
-            atomicAdd(&c.stat[lc.stat], 1ull);
-        }
+        q_follow(c, t, r, lane, lc.stat);
         __syncwarp();
     }
     if (lane == 0) launch_exit(c, lc, -1, unsigned(nw));

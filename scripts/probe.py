@@ -36,6 +36,7 @@ def main():
     ap.add_argument("--trace", action="store_true")
     ap.add_argument("--chain", type=int, default=None)
     ap.add_argument("--cap", type=int, default=None)
+    ap.add_argument("--multi", type=int, default=None)
     ap.add_argument("--check", action="store_true", help="compare flows with a chain=1 solve")
     ap.add_argument("--reps", type=int, default=3)
     ap.add_argument("--nprob", type=int, default=None, help="problems per device batch")
@@ -55,11 +56,13 @@ def main():
     if a.warp is not None: s.set("warp", a.warp)
     if a.chain is not None: s.set("chain", a.chain)
     if a.cap is not None: s.set("relax_cap", a.cap)
+    if a.multi is not None: s.set("bfs_multi", a.multi)
     ref = None
     if a.check:
         r0 = _native.Solver(0, chain=1)
         ref = r0.solve_seed_batch(c["w"], c["h"], probs, c["lams"], "auto")
         r0.close()
+    devs = []
     for r in range(a.reps):
         t0 = time.perf_counter()
         s.seed_stage(c["w"], c["h"], probs, c["lams"], "auto")
@@ -70,11 +73,16 @@ def main():
         t3 = time.perf_counter()
         dt = t3 - t0
         st = s.stats()
+        devs.append(st["ms_device"])
         cuts = flows.size
         if a.trace and r == a.reps - 1:
             tr = s.trace()
-            print("trace push (us, tiles):", [(u, t) for k, u, t in tr if k == 0])
-            print("trace bfs  (us, tiles):", [(u, t) for k, u, t in tr if k == 1][:30])
+            print("trace push (us, tiles):", [(u, t) for k, u, t, _ in tr if k == 0])
+            print("trace bfs  (us, tiles):", [(u, t) for k, u, t, _ in tr if k == 1][:30])
+            print("timeline (kind, start_us, span_us, gap_us):")
+            for i, (k, u, t, st0) in enumerate(tr):
+                gap = st0 - (tr[i - 1][3] + tr[i - 1][1]) if i else 0.0
+                print(f"  {k} {st0:9.1f} {u:8.1f} {gap:7.1f} tiles={t}")
         if ref is not None:
             import numpy as np
             ok = bool((ref[1] == flows).all()) and bool(np.array_equal(ref[2], labels))
@@ -87,6 +95,7 @@ def main():
                               run_ms=round((t2 - t1) * 1e3, 2), fetch_ms=round((t3 - t2) * 1e3, 2),
                               cuts_per_s=round(cuts / dt, 1),
                               flow=int(flows.sum()),
+                              med_dev_ms=round(sorted(devs[1:] or devs)[len(devs[1:] or devs) // 2], 3),
                               **{k: (round(st[k], 3) if isinstance(st[k], float) else st[k]) for k in keep})))
 
 
