@@ -13,7 +13,6 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 OUT = os.path.join(HERE, "libpmflow_b200.so")
 SOURCES = ["engine.cu"]
-DEPS = SOURCES + ["engine.cuh", "kernels.cuh"]
 NVCC_FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
               "-Xcompiler", "-fPIC,-O2,-fopenmp", "-shared", "--expt-relaxed-constexpr", "-lgomp"]
 
@@ -30,7 +29,8 @@ def stale() -> bool:
         return True
     t = os.path.getmtime(OUT)
     hdr = os.path.join(HERE, "..", "include", "pmflow_b200.h")
-    return any(os.path.getmtime(p) > t for p in [os.path.join(CSRC, d) for d in DEPS] + [hdr])
+    deps = [os.path.join(CSRC, f) for f in os.listdir(CSRC) if f.endswith((".cu", ".cuh", ".h"))]
+    return any(os.path.getmtime(p) > t for p in deps + [hdr, os.path.abspath(__file__)])
 
 
 def build(force: bool = False, verbose: bool = False) -> str:
