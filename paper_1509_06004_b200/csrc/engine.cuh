@@ -137,7 +137,7 @@ struct Ctx {
 };
 
 enum { Q_IDLE = 0, Q_QUEUED = 1, Q_RUNNING = 2, Q_DIRTY = 3 };
-enum { QC_HEAD = 0, QC_TAIL = 1, QC_PENDING = 2, QC_POPS = 3 };
+enum { QC_HEAD = 0, QC_TAIL = 1, QC_PENDING = 2 };   // HEAD = tickets taken = pops
 
 __device__ __forceinline__ unsigned ld_volatile(const unsigned *p) {
     return *(const volatile unsigned *)p;
@@ -148,20 +148,6 @@ __device__ __forceinline__ void q_push(const Ctx &c, int32_t t) {
     unsigned idx = atomicAdd(&c.qctr[QC_TAIL], 1u);
     int32_t *slot = &c.ring[idx % unsigned(c.qcap)];
     while (atomicCAS(slot, -1, t) != -1) __nanosleep(64);
-}
-
-// Pop a tile id, or -1 if the ring is empty right now.
-__device__ __forceinline__ int32_t q_pop(const Ctx &c) {
-    for (;;) {
-        unsigned hd = ld_volatile(&c.qctr[QC_HEAD]);
-        if (hd >= ld_volatile(&c.qctr[QC_TAIL])) return -1;
-        if (atomicCAS(&c.qctr[QC_HEAD], hd, hd + 1) == hd) {
-            int32_t *slot = &c.ring[hd % unsigned(c.qcap)];
-            int32_t t;
-            while ((t = atomicExch(slot, -1)) == -1) __nanosleep(32);
-            return t;
-        }
-    }
 }
 
 // Ask for tile t to be (re)processed: idle -> queued, running -> dirty.
@@ -200,21 +186,30 @@ __device__ __forceinline__ void q_finish(const Ctx &c, int32_t t, bool again) {
 }
 
 // Thread 0 of a persistent CTA: next tile to process, or -1 when the phase
-// is over (queue drained with nothing running, or pop budget spent).
+// is over (nothing queued or running) or its pop budget is spent.  Poppers
+// take a ticket (ring position) with one fetch-add -- no CAS retry loop on
+// a contended head -- and wait for a tile to land in that slot.  Any waiter
+// on a slot may take any tile that lands there, so tickets that alias a
+// slot (more waiters than ring slots) only reorder work.  Tickets taken
+// after the phase drained are discarded by the next k_phase_begin.
 __device__ __forceinline__ int32_t q_next(const Ctx &c) {
     // device budget: 0 means "no discharge this cycle"; host budget 0: no cap
     const unsigned budget = c.budget_dev ? *(volatile unsigned *)&c.ctl->budget : c.budget;
     if (c.budget_dev && budget == 0) return -1;
+    if (budget && ld_volatile(&c.qctr[QC_HEAD]) >= budget) return -1;
+    const unsigned hd = atomicAdd(&c.qctr[QC_HEAD], 1u);
+    if (budget && hd >= budget) return -1;
+    int32_t *slot = &c.ring[hd % unsigned(c.qcap)];
     for (;;) {
-        if (budget && ld_volatile(&c.qctr[QC_POPS]) >= budget) return -1;
-        int32_t t = q_pop(c);
-        if (t >= 0) {
-            atomicAdd(&c.qctr[QC_POPS], 1u);
-            atomicExch(&c.qstate[t], Q_RUNNING);
-            return t;
+        if (*(volatile int32_t *)slot != -1) {
+            const int32_t t = atomicExch(slot, -1);
+            if (t >= 0) {
+                atomicExch(&c.qstate[t], Q_RUNNING);
+                return t;
+            }
         }
         if (ld_volatile(&c.qctr[QC_PENDING]) == 0) return -1;
-        __nanosleep(256);
+        __nanosleep(64);
     }
 }
 

@@ -409,76 +409,92 @@ __global__ void __launch_bounds__(NTT, 2) k_bfs_src(Ctx c, int k, LaunchCtl lc) 
 // lock-free admissibility rule h(p) > h(q), which tolerates the stale halo
 // heights of concurrently discharged neighbour tiles).
 //
-// Registers hold the pixel's excess/sink state e and its four residuals;
-// pushes into a neighbour are written to the neighbour's per-direction
-// inflow slot (each slot has exactly one writer per iteration, so no
-// atomics), and absorbed after the barrier.  Heights live in shared memory.
+// Registers hold the pixel's excess/sink state e and its four residuals.
+// Heights and inflow live in shared memory on a ring-padded 34x34 frame:
+// the ring holds the neighbour tiles' facing pixels, so every neighbour
+// access is one unconditional load at a fixed offset.  A push into the
+// d-neighbour adds to that neighbour's inflow slot for direction opp(d)
+// (one writer per slot per iteration -- no atomics); in-tile slots are
+// absorbed (and zeroed) by their owner after the barrier, ring slots
+// accumulate over the pass and leave as one global atomic per halo pixel.
 // At load (and every `relabel_every` iterations) the tile runs an exact
 // local relabel: the distance, inside the tile, to a sink-residual pixel
 // (1) or to a halo pixel (its height + 1) -- HINF means every path out ends
 // in frozen pixels, a certificate that the pixel cannot reach the sink.
 // ---------------------------------------------------------------------------
+constexpr int RW = TW + 2;             // ring-padded row stride
+constexpr int RPIX = RW * (TH + 2);    // ring-padded frame size
+
+__device__ __forceinline__ int ring_index(int s, int j) {
+    switch (s) {
+    case DL: return (j + 1) * RW;
+    case DR: return (j + 1) * RW + TW + 1;
+    case DU: return j + 1;
+    default: return (TH + 1) * RW + j + 1;
+    }
+}
+
 template <class E>
 __global__ void __launch_bounds__(NTT, 2) k_push(Ctx c, int k, int iters, int relabel_every, int relax_cap,
                                                  LaunchCtl lc) {
-    __shared__ int32_t sh[TH * SP];
-    __shared__ int32_t sd[TH * SP];
-    __shared__ int32_t sin4[4][TPIX];
+    __shared__ int32_t sh[RPIX];        // heights (ring: neighbour tiles)
+    __shared__ int32_t sin[4][RPIX];    // sin[d][q]: flow pushed into q by its d-neighbour
+    __shared__ int32_t sd[TH * SP];     // local relabel distances
     __shared__ uint8_t sm[TPIX];
-    __shared__ int32_t hh[4][TW], hacc[4][TW];
+    __shared__ int32_t hh[4][TW];       // halo heights for tile_relax
     __shared__ int s_out;
-    __shared__ int s_rowin[TH];   // row received inflow this iteration
+    __shared__ int s_rowin[TH + 2];     // ring-frame row received inflow this iteration
+    constexpr int OFF[4] = {-1, 1, -RW, RW};
     const int i = threadIdx.x, lx = i & 31, ly = i >> 5, pi = ly * SP + lx;
-    // in-tile neighbour (padded index) per direction, or -1 (halo)
-    const int nbi[4] = {lx > 0 ? pi - 1 : -1, lx < TW - 1 ? pi + 1 : -1,
-                        ly > 0 ? pi - SP : -1, ly < TH - 1 ? pi + SP : -1};
-    const int nbt[4] = {i - 1, i + 1, i - TW, i + TW};   // neighbour's flat tile index
-    const int hpos[4] = {ly, ly, lx, lx};                 // index into halo arrays
+    const int q = (ly + 1) * RW + lx + 1;
+    // inflow slots are zero at every pass boundary (absorbed / drained)
+    for (int j = i; j < 4 * RPIX; j += NTT) (&sin[0][0])[j] = 0;
+    if (i < TH + 2) s_rowin[i] = 0;
     tile_loop(c, k, lc, [&](int32_t t) -> TileResult {
-        TileGeo g = tile_geo(c, t);
         const int64_t p = int64_t(t) * TPIX + i;
         const int32_t w0 = __ldcg(c.w + p);
         const typename E::Word rv0 = E::load(c.r, p);
         int32_t e = w0, h = __ldcg(c.h + p);
         int32_t r[4];
 #pragma unroll
-        for (int d = 0; d < 4; d++) {
-            r[d] = E::lane(rv0, d);
-            sin4[d][i] = 0;
-        }
+        for (int d = 0; d < 4; d++) r[d] = E::lane(rv0, d);
         if (i < 4 * TW) {
-            int s = i / TW, j = i % TW;
-            hh[s][j] = g.nb[s] >= 0 ? __ldcg(c.h + int64_t(g.nb[s]) * TPIX + halo_index(s, j)) : HINF;
-            hacc[s][j] = 0;
+            const int s = i / TW, j = i % TW;
+            const int32_t nb = tile_geo(c, t).nb[s];
+            const int32_t v = nb >= 0 ? __ldcg(c.h + int64_t(nb) * TPIX + halo_index(s, j)) : HINF;
+            hh[s][j] = v;
+            sh[ring_index(s, j)] = v;
         }
         if (i == 0) s_out = 0;
-        if (i < TH) s_rowin[i] = 0;
         int act = 1;
+        int until_relabel = 0;
         for (int it = 0; it < iters; it++) {
-            if (relabel_every && it % relabel_every == 0) {
+            if (relabel_every && until_relabel == 0) {
+                until_relabel = relabel_every;
                 // exact local relabel (frozen pixels stay frozen)
                 sd[pi] = e < 0 ? 1 : HINF;
                 sm[i] = uint8_t((r[0] > 0) | ((r[1] > 0) << 1) | ((r[2] > 0) << 2) | ((r[3] > 0) << 3));
                 __syncthreads();
                 const int conv = tile_relax(sd, sm, hh, 1, relax_cap);
-                // frozen pixels stay frozen; an unconverged relax may not
-                // freeze anyone (keep the old height where it found nothing)
+                // an unconverged relax may not freeze anyone (keep the old
+                // height where it found nothing)
                 if (h < HINF && (conv || sd[pi] < HINF)) h = sd[pi];
-                sh[pi] = h;
+                sh[q] = h;
                 act = __syncthreads_or(e > 0 && h < HINF);
                 if (!act) break;
             } else if (it == 0) {
-                sh[pi] = h;
+                sh[q] = h;
                 act = __syncthreads_or(e > 0 && h < HINF);
                 if (!act) break;
             }
+            until_relabel--;
             // warp == tile row: rows without an active pixel skip the push
             // work, rows nobody pushed into skip the merge (barriers stay)
             const bool mine = e > 0 && h < HINF;
             int32_t hn[4];
             if (__any_sync(0xffffffffu, mine)) {
 #pragma unroll
-                for (int d = 0; d < 4; d++) hn[d] = nbi[d] >= 0 ? sh[nbi[d]] : hh[d][hpos[d]];
+                for (int d = 0; d < 4; d++) hn[d] = sh[q + OFF[d]];
                 // ---- push downhill (heights are fixed during this phase, so
                 // an arc is never pushed both ways and every inflow slot has
                 // one writer)
@@ -487,41 +503,37 @@ __global__ void __launch_bounds__(NTT, 2) k_push(Ctx c, int k, int iters, int re
 #pragma unroll
                     for (int d = 0; d < 4; d++) {
                         if (e > 0 && r[d] > 0 && h > hn[d]) {
-                            int32_t dl = min(e, r[d]);
+                            const int32_t dl = min(e, r[d]);
                             e -= dl;
                             r[d] -= dl;
-                            if (nbi[d] >= 0) {
-                                sin4[opp(d)][nbt[d]] = dl;
-                                pushed |= 1 << d;
-                            } else {
-                                hacc[d][hpos[d]] += dl;
-                            }
+                            sin[opp(d)][q + OFF[d]] += dl;
+                            pushed |= 1 << d;
                         }
                     }
-                    if (pushed & ((1 << DL) | (1 << DR))) s_rowin[ly] = 1;
-                    if (pushed & (1 << DU)) s_rowin[ly - 1] = 1;
-                    if (pushed & (1 << DD)) s_rowin[ly + 1] = 1;
+                    if (pushed & ((1 << DL) | (1 << DR))) s_rowin[ly + 1] = 1;
+                    if (pushed & (1 << DU)) s_rowin[ly] = 1;
+                    if (pushed & (1 << DD)) s_rowin[ly + 2] = 1;
                 }
             }
             __syncthreads();
             // ---- absorb inflow, relabel what is still active
-            if (s_rowin[ly]) {
+            if (s_rowin[ly + 1]) {
 #pragma unroll
                 for (int d = 0; d < 4; d++) {
-                    int32_t v = sin4[d][i];
+                    const int32_t v = sin[d][q];
                     if (v) {
                         e += v;
                         r[d] += v;
-                        sin4[d][i] = 0;
+                        sin[d][q] = 0;
                     }
                 }
                 __syncwarp();
-                if (lx == 0) s_rowin[ly] = 0;
+                if (lx == 0) s_rowin[ly + 1] = 0;
             }
             if (e > 0 && h < HINF) {
                 if (!mine) {   // became active by inflow this iteration
 #pragma unroll
-                    for (int d = 0; d < 4; d++) hn[d] = nbi[d] >= 0 ? sh[nbi[d]] : hh[d][hpos[d]];
+                    for (int d = 0; d < 4; d++) hn[d] = sh[q + OFF[d]];
                 }
                 int32_t m = HINF;
 #pragma unroll
@@ -529,7 +541,7 @@ __global__ void __launch_bounds__(NTT, 2) k_push(Ctx c, int k, int iters, int re
                     if (r[d] > 0) m = min(m, hn[d]);
                 if (m >= h) {
                     h = m >= HINF ? HINF : m + 1;
-                    sh[pi] = h;
+                    sh[q] = h;
                 }
             }
             act = __syncthreads_or(e > 0 && h < HINF);
@@ -546,14 +558,17 @@ __global__ void __launch_bounds__(NTT, 2) k_push(Ctx c, int k, int iters, int re
             E::store_delta(c.r, p, rv, rv0);
         }
         c.h[p] = h;
+        if (i < 2) s_rowin[i * (TH + 1)] = 0;   // ring rows are never absorbed
         __syncthreads();
         if (i < 4 * TW) {
-            int s = i / TW, j = i % TW;
-            int32_t a = hacc[s][j];
+            const int s = i / TW, j = i % TW;
+            int32_t *slot = &sin[opp(s)][ring_index(s, j)];
+            const int32_t a = *slot;
             if (a > 0) {
-                int64_t q = int64_t(g.nb[s]) * TPIX + halo_index(s, j);
-                atomicAdd(&c.w[q], a);
-                E::add(c.r, q, opp(s), a);
+                *slot = 0;
+                const int64_t qn = int64_t(tile_geo(c, t).nb[s]) * TPIX + halo_index(s, j);
+                atomicAdd(&c.w[qn], a);
+                E::add(c.r, qn, opp(s), a);
                 atomicOr(&s_out, 1 << s);
             }
         }

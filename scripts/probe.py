@@ -40,10 +40,14 @@ def main():
     ap.add_argument("--check", action="store_true", help="compare flows with a chain=1 solve")
     ap.add_argument("--reps", type=int, default=3)
     ap.add_argument("--nprob", type=int, default=None, help="problems per device batch")
+    ap.add_argument("--images", type=int, default=1, help="images per device batch (rng_seed 0..)")
     a = ap.parse_args()
     c = CFG[a.cfg]
-    b = synth.generate(c["w"], c["h"], c["rows"], c["cols"], rng_seed=0, types=c["types"])
-    probs = b.problems if a.nprob is None else b.problems[:a.nprob]
+    probs = []
+    for i in range(a.images):
+        b = synth.generate(c["w"], c["h"], c["rows"], c["cols"], rng_seed=i, types=c["types"])
+        probs += b.problems
+    probs = probs if a.nprob is None else probs[:a.nprob]
     s = _native.Solver(0)
     if a.iters: s.set("push_iters", a.iters)
     if a.sweeps: s.set("push_sweeps", a.sweeps)
