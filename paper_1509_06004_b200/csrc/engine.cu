@@ -128,10 +128,12 @@ constexpr int64_t kChunk = 1 << 16;   // elements per host task
 struct Layout {
     std::vector<GridDesc> grids;
     std::vector<int32_t> tile_grid;
+    std::vector<int4> tile_nb;      // neighbour tile per side (L, R, U, D), -1 if none
     int64_t ntiles = 0, out_bytes = 0, pixels = 0;
     void clear() {
         grids.clear();
         tile_grid.clear();
+        tile_nb.clear();
         ntiles = out_bytes = pixels = 0;
     }
     void add(int32_t W, int32_t H, int32_t kind, int32_t colswap_off, int32_t prob, int32_t lam,
@@ -150,6 +152,12 @@ struct Layout {
         g.lam_end = lam_end;
         int64_t nt = int64_t(g.ntx) * g.nty;
         tile_grid.insert(tile_grid.end(), size_t(nt), int32_t(grids.size()));
+        for (int32_t ty = 0; ty < g.nty; ty++)
+            for (int32_t tx = 0; tx < g.ntx; tx++) {
+                const int32_t t = int32_t(ntiles + int64_t(ty) * g.ntx + tx);
+                tile_nb.push_back(make_int4(tx > 0 ? t - 1 : -1, tx + 1 < g.ntx ? t + 1 : -1,
+                                            ty > 0 ? t - g.ntx : -1, ty + 1 < g.nty ? t + g.ntx : -1));
+            }
         ntiles += nt;
         out_bytes += int64_t(W) * H;
         pixels += int64_t(W) * H;
@@ -202,7 +210,7 @@ struct pmf_solver {
     int timing = 0;
     int64_t max_cycles = 50000;
     // device workspace
-    DevBuf d_w, d_h, d_r, d_lab, d_tile_grid, d_grids, d_live, d_act, d_list, d_inq, d_cnt,
+    DevBuf d_w, d_h, d_r, d_lab, d_tile_grid, d_tnb, d_grids, d_live, d_act, d_list, d_inq, d_cnt,
         d_snk, d_drain, d_err, d_stat, d_colswap, d_out, d_in32, d_pw, d_mask, d_off, d_lam,
         d_swapcnt, d_swapflag, d_ring, d_qstate, d_qctr, d_ctl, d_curlam, d_flows, d_slopesum;
     HostBuf h_in32, h_pw, h_mask, h_out, h_small;
@@ -258,7 +266,7 @@ int setup_state(pmf_solver *s, int edge_bytes) {
     int rc = 0;
     if ((rc = s->d_w.ensure(P * 4)) || (rc = s->d_h.ensure(P * 4)) ||
         (rc = s->d_r.ensure(P * size_t(edge_bytes))) || (rc = s->d_lab.ensure(P)) ||
-        (rc = s->d_tile_grid.ensure(T * 4)) || (rc = s->d_grids.ensure(G * sizeof(GridDesc))) ||
+        (rc = s->d_tile_grid.ensure(T * 4)) || (rc = s->d_tnb.ensure(T * 16)) || (rc = s->d_grids.ensure(G * sizeof(GridDesc))) ||
         (rc = s->d_live.ensure(G * 4)) || (rc = s->d_act.ensure(G * 4)) ||
         (rc = s->d_list.ensure(2 * T * 4)) || (rc = s->d_inq.ensure(2 * T * 4)) ||
         (rc = s->d_cnt.ensure(64)) || (rc = s->d_snk.ensure(G * 8)) || (rc = s->d_drain.ensure(G * 8)) ||
@@ -272,6 +280,7 @@ int setup_state(pmf_solver *s, int edge_bytes) {
     s->warp_eff = s->warp >= 0 ? s->warp : (4 | (T >= s->warp_bfs_tiles ? 2 : 0));
     // host sources live in the solver (s->lay, s->ones) until the next setup
     CK(cudaMemcpyAsync(s->d_tile_grid.p, L.tile_grid.data(), T * 4, cudaMemcpyHostToDevice, s->st));
+    CK(cudaMemcpyAsync(s->d_tnb.p, L.tile_nb.data(), T * 16, cudaMemcpyHostToDevice, s->st));
     CK(cudaMemcpyAsync(s->d_grids.p, L.grids.data(), G * sizeof(GridDesc), cudaMemcpyHostToDevice, s->st));
     s->ones.assign(size_t(G), 1);
     CK(cudaMemcpyAsync(s->d_live.p, s->ones.data(), G * 4, cudaMemcpyHostToDevice, s->st));
@@ -290,6 +299,7 @@ int setup_state(pmf_solver *s, int edge_bytes) {
     x.r = s->d_r.p;
     x.lab = s->d_lab.as<uint8_t>();
     x.tile_grid = s->d_tile_grid.as<int32_t>();
+    x.tnb = s->d_tnb.as<int4>();
     x.grids = s->d_grids.as<GridDesc>();
     x.live = s->d_live.as<int32_t>();
     x.act = s->d_act.as<int32_t>();

@@ -107,6 +107,7 @@ struct Ctx {
     void *r;
     uint8_t *lab;
     const int32_t *tile_grid;
+    const int4 *tnb;        // per tile: neighbour tile per side (L, R, U, D), -1 if none
     const GridDesc *grids;
     int32_t *live;          // per grid: still has work
     int32_t *act;           // per grid active-pixel count of the last seed pass
@@ -137,7 +138,7 @@ struct Ctx {
 };
 
 enum { Q_IDLE = 0, Q_QUEUED = 1, Q_RUNNING = 2, Q_DIRTY = 3 };
-enum { QC_HEAD = 0, QC_TAIL = 1, QC_PENDING = 2 };   // HEAD = tickets taken = pops
+enum { QC_HEAD = 0, QC_TAIL = 1, QC_PENDING = 2, QC_CONT = 3 };   // HEAD: tickets taken; CONT: continuations
 
 __device__ __forceinline__ unsigned ld_volatile(const unsigned *p) {
     return *(const volatile unsigned *)p;
@@ -196,9 +197,9 @@ __device__ __forceinline__ int32_t q_next(const Ctx &c) {
     // device budget: 0 means "no discharge this cycle"; host budget 0: no cap
     const unsigned budget = c.budget_dev ? *(volatile unsigned *)&c.ctl->budget : c.budget;
     if (c.budget_dev && budget == 0) return -1;
-    if (budget && ld_volatile(&c.qctr[QC_HEAD]) >= budget) return -1;
+    if (budget && ld_volatile(&c.qctr[QC_HEAD]) + ld_volatile(&c.qctr[QC_CONT]) >= budget) return -1;
     const unsigned hd = atomicAdd(&c.qctr[QC_HEAD], 1u);
-    if (budget && hd >= budget) return -1;
+    if (budget && hd + ld_volatile(&c.qctr[QC_CONT]) >= budget) return -1;
     int32_t *slot = &c.ring[hd % unsigned(c.qcap)];
     for (;;) {
         if (*(volatile int32_t *)slot != -1) {
@@ -211,6 +212,19 @@ __device__ __forceinline__ int32_t q_next(const Ctx &c) {
         if (ld_volatile(&c.qctr[QC_PENDING]) == 0) return -1;
         __nanosleep(64);
     }
+}
+
+// Continuation: the CTA that just finished a tile takes an idle neighbour
+// it activated straight away (IDLE -> RUNNING), skipping the ring hand-off
+// -- the common case in the latency-bound tail, where excess walks from tile
+// to tile.  Counts against the pop budget like a pop.
+__device__ __forceinline__ bool q_claim(const Ctx &c, int32_t t) {
+    const unsigned budget = c.budget_dev ? *(volatile unsigned *)&c.ctl->budget : c.budget;
+    if (budget && ld_volatile(&c.qctr[QC_HEAD]) + ld_volatile(&c.qctr[QC_CONT]) >= budget) return false;
+    if (atomicCAS(&c.qstate[t], Q_IDLE, Q_RUNNING) != Q_IDLE) return false;
+    atomicAdd(&c.qctr[QC_PENDING], 1u);
+    atomicAdd(&c.qctr[QC_CONT], 1u);
+    return true;
 }
 
 // A batch grid embedded swapped reports its sink side (what split() turns
@@ -261,6 +275,20 @@ __device__ __forceinline__ TileGeo tile_geo(const Ctx &c, int32_t t) {
     o.W = gd.W;
     o.H = gd.H;
     return o;
+}
+
+// Neighbour tile on side s (one load from the precomputed table).
+__device__ __forceinline__ int32_t tile_nb(const Ctx &c, int32_t t, int s) {
+    const int *nb = reinterpret_cast<const int *>(c.tnb + t);
+    return __ldg(nb + s);
+}
+
+struct TileNb {
+    int32_t nb[4];
+};
+__device__ __forceinline__ TileNb tile_nbs(const Ctx &c, int32_t t) {
+    const int4 v = __ldg(c.tnb + t);
+    return TileNb{{v.x, v.y, v.z, v.w}};
 }
 
 // Index, inside the neighbour tile on side s, of the halo pixel facing

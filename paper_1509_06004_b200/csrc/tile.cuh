@@ -120,8 +120,8 @@ __device__ __forceinline__ void enqueue_follow(const Ctx &c, int k, int32_t t, c
     if (j == 0) {
         if (r.again) enqueue(c, k, t);
     } else if ((r.out >> (j - 1)) & 1) {
-        const TileGeo g = tile_geo(c, t);
-        if (g.nb[j - 1] >= 0) enqueue(c, k, g.nb[j - 1]);
+        const int32_t nb = tile_nb(c, t, j - 1);
+        if (nb >= 0) enqueue(c, k, nb);
     }
 }
 
@@ -192,11 +192,19 @@ __device__ __forceinline__ void launch_exit(const Ctx &c, const LaunchCtl &lc, i
 // lanes 1..4 request the flagged neighbours concurrently, then lane 0
 // retires or requeues the tile (after the requests, so the pending count
 // never touches zero while follow-up work is being registered).
-__device__ __forceinline__ void q_follow(const Ctx &c, int32_t t, const TileResult &r, int lane, int stat) {
-    if (lane >= 1 && lane <= 4 && ((r.out >> (lane - 1)) & 1)) {
+__device__ __forceinline__ void q_follow(const Ctx &c, int32_t t, const TileResult &r, int lane, int stat,
+                                         int32_t *cont = nullptr) {
+    // continuation candidate (cont != nullptr): the lowest flagged side,
+    // when the tile itself is done
+    const unsigned flags = unsigned(r.out) & 15u;
+    const int want = (cont && !r.again && flags) ? __ffs(flags) : 0;
+    if (lane >= 1 && lane <= 4 && ((flags >> (lane - 1)) & 1)) {
         __threadfence();              // ... < this lane's queue-state reads
-        const TileGeo g = tile_geo(c, t);
-        if (g.nb[lane - 1] >= 0) q_request(c, g.nb[lane - 1]);
+        const int32_t nb = tile_nb(c, t, lane - 1);
+        if (nb >= 0) {
+            if (lane == want && q_claim(c, nb)) *cont = nb;
+            else q_request(c, nb);
+        }
         __threadfence();
     }
     __syncwarp();
@@ -286,9 +294,13 @@ __device__ __forceinline__ void tile_loop(const Ctx &c, int k, const LaunchCtl &
     // between its write and its read in every participating thread, i.e.
     // on both sides of the CTA barrier that separates the data threads from
     // thread 0.
+    __shared__ int32_t s_cont;
+    if (i == 0) s_cont = -1;
     for (;;) {
         if (i == 0) {
-            int32_t t = q_next(c);
+            int32_t t = s_cont;
+            s_cont = -1;
+            if (t < 0) t = q_next(c);
             __threadfence();
             s_t = t;
         }
@@ -299,7 +311,7 @@ __device__ __forceinline__ void tile_loop(const Ctx &c, int k, const LaunchCtl &
         TileResult r = body(t);
         __threadfence();              // requester side: data writes < ...
         __syncthreads();
-        if (i < 32) q_follow(c, t, r, i, lc.stat);
+        if (i < 32) q_follow(c, t, r, i, lc.stat, &s_cont);
     }
     if (i == 0) launch_exit(c, lc, -1, gridDim.x);
 }
@@ -323,7 +335,7 @@ __global__ void __launch_bounds__(NTT, 2) k_bfs_sink(Ctx c, int k, LaunchCtl lc)
     __shared__ int s_side;
     const int i = threadIdx.x, lx = i & 31, ly = i >> 5;
     tile_loop(c, k, lc, [&](int32_t t) -> TileResult {
-        TileGeo g = tile_geo(c, t);
+        const TileNb g = tile_nbs(c, t);
         const int64_t p = int64_t(t) * TPIX + i;
         const int32_t h0 = __ldcg(c.h + p);
         typename E::Word wd = E::load(c.r, p);
@@ -362,7 +374,7 @@ __global__ void __launch_bounds__(NTT, 2) k_bfs_src(Ctx c, int k, LaunchCtl lc) 
     __shared__ int s_side;
     const int i = threadIdx.x, lx = i & 31, ly = i >> 5;
     tile_loop(c, k, lc, [&](int32_t t) -> TileResult {
-        TileGeo g = tile_geo(c, t);
+        const TileNb g = tile_nbs(c, t);
         const int64_t p = int64_t(t) * TPIX + i;
         const uint8_t l0 = __ldcg(c.lab + p);
         typename E::Word wd = E::load(c.r, p);
@@ -460,7 +472,7 @@ __global__ void __launch_bounds__(NTT, 2) k_push(Ctx c, int k, int iters, int re
         for (int d = 0; d < 4; d++) r[d] = E::lane(rv0, d);
         if (i < 4 * TW) {
             const int s = i / TW, j = i % TW;
-            const int32_t nb = tile_geo(c, t).nb[s];
+            const int32_t nb = tile_nb(c, t, s);
             const int32_t v = nb >= 0 ? __ldcg(c.h + int64_t(nb) * TPIX + halo_index(s, j)) : HINF;
             hh[s][j] = v;
             sh[ring_index(s, j)] = v;
@@ -566,7 +578,7 @@ __global__ void __launch_bounds__(NTT, 2) k_push(Ctx c, int k, int iters, int re
             const int32_t a = *slot;
             if (a > 0) {
                 *slot = 0;
-                const int64_t qn = int64_t(tile_geo(c, t).nb[s]) * TPIX + halo_index(s, j);
+                const int64_t qn = int64_t(tile_nb(c, t, s)) * TPIX + halo_index(s, j);
                 atomicAdd(&c.w[qn], a);
                 E::add(c.r, qn, opp(s), a);
                 atomicOr(&s_out, 1 << s);

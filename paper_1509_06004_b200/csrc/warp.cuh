@@ -65,7 +65,7 @@ __device__ __forceinline__ int32_t warp_min(int32_t v) {
 // coalesced 128 B line per plane)
 // ---------------------------------------------------------------------------
 template <class E>
-__device__ __forceinline__ void wt_load(const Ctx &c, int32_t t, WarpTile<E> &T, const TileGeo &g, int lane,
+__device__ __forceinline__ void wt_load(const Ctx &c, int32_t t, WarpTile<E> &T, const TileNb &g, int lane,
                                         bool want_w, bool want_h) {
     const int64_t base = int64_t(t) * TPIX;
 #pragma unroll 4
@@ -298,7 +298,7 @@ __global__ void __launch_bounds__(WPB * 32) k_wbfs_sink(Ctx c, int k, LaunchCtl 
     WarpTile<E> &T = reinterpret_cast<WarpTile<E> *>(smem_raw)[threadIdx.x >> 5];
     const int lane = threadIdx.x & 31;
     warp_loop(c, k, lc, [&](int32_t t) -> TileResult {
-        TileGeo g = tile_geo(c, t);
+        const TileNb g = tile_nbs(c, t);
         const int64_t base = int64_t(t) * TPIX;
         wt_load<E>(c, t, T, g, lane, true, false);
         uint32_t m[4];
@@ -331,7 +331,7 @@ __global__ void __launch_bounds__(WPB * 32) k_wbfs_src(Ctx c, int k, LaunchCtl l
     WarpTile<E> &T = reinterpret_cast<WarpTile<E> *>(smem_raw)[threadIdx.x >> 5];
     const int lane = threadIdx.x & 31;
     warp_loop(c, k, lc, [&](int32_t t) -> TileResult {
-        TileGeo g = tile_geo(c, t);
+        const TileNb g = tile_nbs(c, t);
         const int64_t base = int64_t(t) * TPIX;
         wt_load<E>(c, t, T, g, lane, true, false);
         uint32_t m[4];   // own arcs: bit x of m[d] = r_d(x, y) > 0
@@ -425,7 +425,7 @@ __global__ void __launch_bounds__(WPB * 32) k_wpush(Ctx c, int k, int rounds, in
     WarpTile<E> &T = reinterpret_cast<WarpTile<E> *>(smem_raw)[threadIdx.x >> 5];
     const int lane = threadIdx.x & 31;
     warp_loop(c, k, lc, [&](int32_t t) -> TileResult {
-        TileGeo g = tile_geo(c, t);
+        const TileNb g = tile_nbs(c, t);
         const int64_t base = int64_t(t) * TPIX;
         wt_load<E>(c, t, T, g, lane, true, true);
         // snapshots of the border pixels for delta write-back: lane x keeps
