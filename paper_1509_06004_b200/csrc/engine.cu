@@ -206,11 +206,12 @@ struct pmf_solver {
     int warm_min_problems = 8;  // auto: one chain per problem (whole ladder) from this many problems
     int push_budget_warm = 4;   // discharge budget factor when the batch runs warm-start chains
     int verify = 1;             // seed batches: device cut_cost == flow certificate per cut
+    int rolling = 1;            // warm-start chains advance per grid as each finishes (no step barrier)
     int bfs_chunk = 8;
     int timing = 0;
     int64_t max_cycles = 50000;
     // device workspace
-    DevBuf d_w, d_h, d_r, d_lab, d_tile_grid, d_tnb, d_grids, d_live, d_act, d_list, d_inq, d_cnt,
+    DevBuf d_w, d_h, d_r, d_lab, d_tile_grid, d_tnb, d_fin, d_grids, d_live, d_act, d_list, d_inq, d_cnt,
         d_snk, d_drain, d_err, d_stat, d_colswap, d_out, d_in32, d_pw, d_mask, d_off, d_lam,
         d_swapcnt, d_swapflag, d_ring, d_qstate, d_qctr, d_ctl, d_curlam, d_flows, d_slopesum;
     HostBuf h_in32, h_pw, h_mask, h_out, h_small;
@@ -267,7 +268,7 @@ int setup_state(pmf_solver *s, int edge_bytes) {
     if ((rc = s->d_w.ensure(P * 4)) || (rc = s->d_h.ensure(P * 4)) ||
         (rc = s->d_r.ensure(P * size_t(edge_bytes))) || (rc = s->d_lab.ensure(P)) ||
         (rc = s->d_tile_grid.ensure(T * 4)) || (rc = s->d_tnb.ensure(T * 16)) || (rc = s->d_grids.ensure(G * sizeof(GridDesc))) ||
-        (rc = s->d_live.ensure(G * 4)) || (rc = s->d_act.ensure(G * 4)) ||
+        (rc = s->d_live.ensure(G * 4)) || (rc = s->d_fin.ensure(G * 4)) || (rc = s->d_act.ensure(G * 4)) ||
         (rc = s->d_list.ensure(2 * T * 4)) || (rc = s->d_inq.ensure(2 * T * 4)) ||
         (rc = s->d_cnt.ensure(64)) || (rc = s->d_snk.ensure(G * 8)) || (rc = s->d_drain.ensure(G * 8)) ||
         (rc = s->d_err.ensure(64)) || (rc = s->d_stat.ensure(ST_NSTAT * 8)) ||
@@ -288,6 +289,7 @@ int setup_state(pmf_solver *s, int edge_bytes) {
     for (int64_t g = 0; g < G; g++) s->curlam0[g] = L.grids[g].lam;
     CK(cudaMemcpyAsync(s->d_curlam.p, s->curlam0.data(), G * 4, cudaMemcpyHostToDevice, s->st));
     CK(cudaMemsetAsync(s->d_act.p, 0, G * 4, s->st));
+    CK(cudaMemsetAsync(s->d_fin.p, 0, G * 4, s->st));
     CK(cudaMemsetAsync(s->d_snk.p, 0, G * 8, s->st));
     CK(cudaMemsetAsync(s->d_drain.p, 0, G * 8, s->st));
     CK(cudaMemsetAsync(s->d_err.p, 0, 64, s->st));
@@ -302,6 +304,8 @@ int setup_state(pmf_solver *s, int edge_bytes) {
     x.tnb = s->d_tnb.as<int4>();
     x.grids = s->d_grids.as<GridDesc>();
     x.live = s->d_live.as<int32_t>();
+    x.fin = s->d_fin.as<int32_t>();
+    x.rolling = 0;
     x.act = s->d_act.as<int32_t>();
     x.list0 = s->d_list.as<int32_t>();
     x.list1 = x.list0 + T;
@@ -473,7 +477,7 @@ int host_solve(pmf_solver *s, const Ctx &c0, int32_t ngrids) {
         LAUNCH(s, (k_phase_begin<<<s->grid_full, 256, 0, s->st>>>(P.push, P.push.persistent, 0, 0)));
         LAUNCH(s, (k_seed_push<<<s->grid_full, NT, 0, s->st>>>(P.push)));
         LAUNCH(s, (k_cycle_ctl<<<1, 1024, 0, s->st>>>(P.push, ngrids, P.push.persistent,
-                                                      unsigned(budget_factor(s)), s->max_cycles, 0, 0)));
+                                                      unsigned(budget_factor(s)), s->max_cycles, 0, 0, 0, 0)));
         CK(cudaGetLastError());
         s->stats.full_passes++;
         Ctl ctl;
@@ -550,6 +554,20 @@ int add_while(cudaGraph_t g, cudaGraphNode_t *prev, cudaGraphConditionalHandle h
     p.type = cudaGraphNodeTypeConditional;
     p.conditional.handle = h;
     p.conditional.type = cudaGraphCondTypeWhile;
+    p.conditional.size = 1;
+    cudaGraphNode_t n;
+    CK(cudaGraphAddNode(&n, g, *prev ? prev : nullptr, *prev ? 1 : 0, &p));
+    *body = p.conditional.phGraph_out[0];
+    *prev = n;
+    return 0;
+}
+
+// appends an if node to g (after *prev); returns its body graph
+int add_if(cudaGraph_t g, cudaGraphNode_t *prev, cudaGraphConditionalHandle h, cudaGraph_t *body) {
+    cudaGraphNodeParams p{};
+    p.type = cudaGraphNodeTypeConditional;
+    p.conditional.handle = h;
+    p.conditional.type = cudaGraphCondTypeIf;
     p.conditional.size = 1;
     cudaGraphNode_t n;
     CK(cudaGraphAddNode(&n, g, *prev ? prev : nullptr, *prev ? 1 : 0, &p));
@@ -636,7 +654,8 @@ int build_graph(pmf_solver *s, const Ctx &c0, int32_t ngrids, const SeedArgs *sa
             return rc;
         if ((rc = add_kernel(cyc, &q, gfull, dim3(NT), k_seed_push, P.push))) return rc;
         if ((rc = add_kernel(cyc, &q, dim3(1), dim3(1024), k_cycle_ctl, P.push, ngrids, int(P.push.persistent),
-                             unsigned(budget_factor(s)), int64_t(s->max_cycles), h_cycle, 1)))
+                             unsigned(budget_factor(s)), int64_t(s->max_cycles), h_cycle, 1,
+                             cudaGraphConditionalHandle(0), 0)))
             return rc;
         if (P.push.persistent) {
             if ((rc = add_push_node<E>(s, cyc, &q, P.pq, K_PERSISTENT, lctl(ST_PUSH)))) return rc;
@@ -675,6 +694,58 @@ int build_graph(pmf_solver *s, const Ctx &c0, int32_t ngrids, const SeedArgs *sa
     if (sa && (rc = add_kernel(g, &prev, gfull, dim3(NT), k_advance_tiles, P.base, *sa))) return rc;
     if ((rc = add_kernel(g, &prev, dim3(1), dim3(1024), k_advance_grids, P.base, sa ? *sa : none, slope_sum, ngrids,
                          h_step, 1)))
+        return rc;
+    return 0;
+}
+
+// Rolling warm start (graph mode): one cycle loop for the whole batch.
+// Every cycle relabels and discharges the live grids; the grids that ran out
+// of active pixels in it (k_cycle_ctl marks them `fin`) get their labels,
+// flow and next lambda in the same cycle and rejoin the live set -- chains
+// no longer wait for the slowest grid of a common step.
+template <class E>
+int build_graph_rolling(pmf_solver *s, const Ctx &c0, int32_t ngrids, const SeedArgs *sa,
+                        const int64_t *slope_sum, cudaGraph_t *out) {
+    PhaseCtx P = phase_ctx(s, c0);
+    cudaGraph_t root;
+    CK(cudaGraphCreate(&root, 0));
+    *out = root;
+    int rc;
+    const dim3 gfull(s->grid_full);
+    const int bfs_k = P.bfs.persistent ? K_PERSISTENT : K_MULTI;
+    cudaGraphConditionalHandle h_cycle;
+    CK(cudaGraphConditionalHandleCreate(&h_cycle, root, 0, 0));
+    cudaGraphNode_t prev = nullptr;
+    if ((rc = add_kernel(root, &prev, dim3(1), dim3(1), k_arm, h_cycle))) return rc;
+    cudaGraph_t cyc;
+    if ((rc = add_while(root, &prev, h_cycle, &cyc))) return rc;
+    cudaGraphConditionalHandle h_lab;
+    CK(cudaGraphConditionalHandleCreate(&h_lab, cyc, 0, cudaGraphCondAssignDefault));
+    cudaGraphNode_t q = nullptr;
+    const cudaGraphConditionalHandle none = 0;
+    // exact global relabel of the live grids
+    if ((rc = add_kernel(cyc, &q, gfull, dim3(256), k_phase_begin, P.bfs, int(P.bfs.persistent), none, 0))) return rc;
+    if ((rc = add_kernel(cyc, &q, gfull, dim3(NT), k_gr_init, P.bfs))) return rc;
+    if ((rc = add_bfs_node<E>(s, cyc, &q, true, P.bfs, bfs_k, lctl(ST_BFS)))) return rc;
+    // seeding, retire / finish grids, discharge
+    if ((rc = add_kernel(cyc, &q, gfull, dim3(256), k_phase_begin, P.push, 1, none, 0))) return rc;
+    if ((rc = add_kernel(cyc, &q, gfull, dim3(NT), k_seed_push, P.push))) return rc;
+    if ((rc = add_kernel(cyc, &q, dim3(1), dim3(1024), k_cycle_ctl, P.push, ngrids, 1, unsigned(budget_factor(s)),
+                         int64_t(s->max_cycles), h_cycle, 1, h_lab, 1)))
+        return rc;
+    if ((rc = add_push_node<E>(s, cyc, &q, P.pq, K_PERSISTENT, lctl(ST_PUSH)))) return rc;
+    // finished grids: labels, flow, next lambda
+    cudaGraph_t lab;
+    if ((rc = add_if(cyc, &q, h_lab, &lab))) return rc;
+    cudaGraphNode_t l = nullptr;
+    if ((rc = add_kernel(lab, &l, gfull, dim3(256), k_phase_begin, P.bfs, int(P.bfs.persistent), none, 0))) return rc;
+    if ((rc = add_kernel(lab, &l, gfull, dim3(NT), k_lab_seed, P.bfs))) return rc;
+    if ((rc = add_bfs_node<E>(s, lab, &l, false, P.bfs, bfs_k, lctl(ST_LAB)))) return rc;
+    if ((rc = add_kernel(lab, &l, gfull, dim3(NT), k_emit, P.base))) return rc;
+    if ((rc = add_kernel(lab, &l, dim3(std::max(1, int(cdiv(ngrids, 256)))), dim3(256), k_finalize, P.base, ngrids)))
+        return rc;
+    if ((rc = add_kernel(lab, &l, gfull, dim3(NT), k_advance_tiles, P.base, *sa))) return rc;
+    if ((rc = add_kernel(lab, &l, dim3(1), dim3(1024), k_advance_grids, P.base, *sa, slope_sum, ngrids, h_cycle, 1)))
         return rc;
     return 0;
 }
@@ -718,7 +789,8 @@ int graph_solve(pmf_solver *s, const Ctx &c0, int32_t ngrids, const SeedArgs *sa
         if (s->gexec) cudaGraphExecDestroy(s->gexec);
         s->gexec = nullptr;
         cudaGraph_t g = nullptr;
-        int rc = build_graph<E>(s, c0, ngrids, sa, slope_sum, &g);
+        int rc = c0.rolling ? build_graph_rolling<E>(s, c0, ngrids, sa, slope_sum, &g)
+                            : build_graph<E>(s, c0, ngrids, sa, slope_sum, &g);
         if (rc) {
             if (g) cudaGraphDestroy(g);
             return rc;
@@ -734,10 +806,58 @@ int graph_solve(pmf_solver *s, const Ctx &c0, int32_t ngrids, const SeedArgs *sa
     return 0;
 }
 
+// Rolling warm start, host-driven (graph = 0): same kernels and order as
+// build_graph_rolling, loop decisions read back from the control block.
+template <class E>
+int host_solve_rolling(pmf_solver *s, const Ctx &c0, int32_t ngrids, const SeedArgs &sa, const int64_t *slope_sum) {
+    PhaseCtx P = phase_ctx(s, c0);
+    const int gfin = std::max(1, int(cdiv(ngrids, 256)));
+    int rc = 0;
+    for (;;) {
+        s->tmark(C_BFS);
+        LAUNCH(s, (k_phase_begin<<<s->grid_full, 256, 0, s->st>>>(P.bfs, P.bfs.persistent, 0, 0)));
+        LAUNCH(s, (k_gr_init<<<s->grid_full, NT, 0, s->st>>>(P.bfs)));
+        if ((rc = host_bfs<E>(s, P.bfs, true))) return rc;
+        s->tmark(C_SEED);
+        LAUNCH(s, (k_phase_begin<<<s->grid_full, 256, 0, s->st>>>(P.push, 1, 0, 0)));
+        LAUNCH(s, (k_seed_push<<<s->grid_full, NT, 0, s->st>>>(P.push)));
+        LAUNCH(s, (k_cycle_ctl<<<1, 1024, 0, s->st>>>(P.push, ngrids, 1, unsigned(budget_factor(s)), s->max_cycles,
+                                                      0, 0, 0, 0)));
+        CK(cudaGetLastError());
+        Ctl ctl;
+        if ((rc = read_ctl(s, c0, &ctl))) return rc;
+        if (ctl.noconv)
+            return fail(PMF_ERR_NOCONV, "push-relabel failed to converge within %lld cycles",
+                        (long long)s->max_cycles);
+        if (ctl.nact) {
+            s->tmark(C_PUSH);
+            launch_push<E>(s, P.pq, K_PERSISTENT);
+            CK(cudaGetLastError());
+        }
+        if (!ctl.nfin) {
+            if (!ctl.nact) break;
+            continue;
+        }
+        s->tmark(C_LAB);
+        LAUNCH(s, (k_phase_begin<<<s->grid_full, 256, 0, s->st>>>(P.bfs, P.bfs.persistent, 0, 0)));
+        LAUNCH(s, (k_lab_seed<<<s->grid_full, NT, 0, s->st>>>(P.bfs)));
+        if ((rc = host_bfs<E>(s, P.bfs, false))) return rc;
+        LAUNCH(s, (k_emit<<<s->grid_full, NT, 0, s->st>>>(P.base)));
+        LAUNCH(s, (k_finalize<<<gfin, 256, 0, s->st>>>(c0, ngrids)));
+        LAUNCH(s, (k_advance_tiles<<<s->grid_full, NT, 0, s->st>>>(c0, sa)));
+        LAUNCH(s, (k_advance_grids<<<1, 1024, 0, s->st>>>(c0, sa, slope_sum, ngrids, 0, 0)));
+        CK(cudaGetLastError());
+        if ((rc = read_ctl(s, c0, &ctl))) return rc;
+        if (!ctl.more) break;
+    }
+    return 0;
+}
+
 template <class E>
 int run_solve(pmf_solver *s, const Ctx &c0, int32_t ngrids, const SeedArgs *sa = nullptr,
               const int64_t *slope_sum = nullptr) {
     CK(cudaMemsetAsync(c0.ctl, 0, sizeof(Ctl), s->st));
+    if (c0.rolling && !s->use_graph) return host_solve_rolling<E>(s, c0, ngrids, *sa, slope_sum);
     if (s->use_graph) return graph_solve<E>(s, c0, ngrids, sa, slope_sum);
     const int gfin = std::max(1, int(cdiv(ngrids, 256)));
     for (;;) {   // warm-start steps
@@ -913,6 +1033,8 @@ int seed_run_t(pmf_solver *s) {
     s->stats.full_passes++;
     const bool chains = S.chain > 1;
     s->warm_active = chains;
+    // rolling warm start needs the persistent discharge and a single-launch BFS
+    s->ctx.rolling = chains && s->rolling && s->persistent && (s->bfs_multi || s->persistent_bfs);
     int rc2 = run_solve<E>(s, c, int32_t(s->lay.grids.size()), chains ? &a : nullptr,
                            chains ? s->d_slopesum.as<int64_t>() : nullptr);
     if (rc2) return rc2;
@@ -1199,6 +1321,7 @@ int pmf_solver_set(pmf_solver *s, const char *name, int64_t v) {
     else if (k == "warm_min_problems" && v >= 1) s->warm_min_problems = int(v);
     else if (k == "push_budget_warm" && v >= 0) s->push_budget_warm = int(v);
     else if (k == "verify") s->verify = v != 0;
+    else if (k == "rolling") s->rolling = v != 0;
     else if (k == "graph") s->use_graph = v != 0;
     else if (k == "persistent_bfs") s->persistent_bfs = v != 0;
     else if (k == "bfs_multi") s->bfs_multi = v != 0;

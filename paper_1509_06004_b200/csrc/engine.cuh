@@ -53,6 +53,7 @@ struct Ctl {
     int32_t cycles_total;   // cycles over all warm-start steps
     int32_t steps;          // warm-start steps run
     int32_t more;           // another warm-start step follows
+    int32_t nfin;           // rolling mode: grids that finished in this cycle
     unsigned long long t0;  // earliest CTA start of the current launch (ns)
     unsigned long long t1;  // latest CTA end of the current launch (ns)
     uint32_t bar_count;     // grid barrier (K_MULTI): arrivals so far in the launch
@@ -110,6 +111,8 @@ struct Ctx {
     const int4 *tnb;        // per tile: neighbour tile per side (L, R, U, D), -1 if none
     const GridDesc *grids;
     int32_t *live;          // per grid: still has work
+    int32_t *fin;           // per grid (rolling mode): finished its lambda this cycle, labels due
+    int32_t rolling;        // rolling warm start: grids emit and advance as they finish
     int32_t *act;           // per grid active-pixel count of the last seed pass
     int32_t *list0, *list1; // double-buffered tile worklists
     int32_t *inq0, *inq1;   // "already listed" flags per tile, per buffer
@@ -226,6 +229,10 @@ __device__ __forceinline__ bool q_claim(const Ctx &c, int32_t t) {
     atomicAdd(&c.qctr[QC_CONT], 1u);
     return true;
 }
+
+// Label-phase kernels act on every grid, or in rolling mode only on the
+// grids that finished their lambda in this cycle.
+__device__ __forceinline__ bool grid_due(const Ctx &c, int32_t g) { return !c.rolling || c.fin[g]; }
 
 // A batch grid embedded swapped reports its sink side (what split() turns
 // into the original graph's minimal source side); everything else needs the

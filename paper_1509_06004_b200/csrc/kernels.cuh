@@ -263,11 +263,24 @@ __global__ void k_phase_begin(Ctx c, int persistent, cudaGraphConditionalHandle 
 // whether another discharge + global relabel round is needed.
 __global__ void __launch_bounds__(1024) k_cycle_ctl(Ctx c, int32_t ngrids, int persistent,
                                                     unsigned budget_factor, int64_t max_cycles,
-                                                    cudaGraphConditionalHandle cond, int has_cond) {
+                                                    cudaGraphConditionalHandle cond, int has_cond,
+                                                    cudaGraphConditionalHandle cond_lab, int has_lab) {
+    __shared__ int s_fin;
+    if (threadIdx.x == 0) s_fin = 0;
+    __syncthreads();
+    int nfin = 0;
     for (int g = threadIdx.x; g < ngrids; g += blockDim.x) {
-        if (c.live[g] && c.act[g] == 0) c.live[g] = 0;
+        if (c.live[g] && c.act[g] == 0) {
+            c.live[g] = 0;
+            if (c.rolling) {
+                c.fin[g] = 1;
+                nfin++;
+            }
+        }
         c.act[g] = 0;
     }
+    if (nfin) atomicAdd(&s_fin, nfin);
+    __syncthreads();
     if (threadIdx.x == 0) {
         Ctl *ctl = c.ctl;
         int32_t nact = persistent ? int32_t(c.qctr[QC_PENDING]) : c.cnt[0];
@@ -279,11 +292,15 @@ __global__ void __launch_bounds__(1024) k_cycle_ctl(Ctx c, int32_t ngrids, int p
             stop = 1;
         }
         ctl->nact = nact;
+        ctl->nfin = s_fin;
         // pop budget of the discharge that follows (0 = run none)
         uint64_t cap = uint64_t(64) * uint64_t(c.ntiles) + 1024;
         uint64_t want = budget_factor ? uint64_t(budget_factor) * uint64_t(nact) + 64 : cap;
         ctl->budget = stop ? 0u : unsigned(want < cap ? want : cap);
-        if (has_cond) cudaGraphSetConditional(cond, stop ? 0u : 1u);
+        // rolling mode: finished grids run the label block (which decides
+        // whether the cycle loop goes on once they have advanced)
+        if (has_cond) cudaGraphSetConditional(cond, (!stop || (s_fin && !ctl->noconv)) ? 1u : 0u);
+        if (has_lab) cudaGraphSetConditional(cond_lab, s_fin ? 1u : 0u);
     }
 }
 
@@ -294,7 +311,9 @@ __global__ void __launch_bounds__(1024) k_cycle_ctl(Ctx c, int32_t ngrids, int p
 
 __global__ void __launch_bounds__(NT) k_lab_seed(Ctx c) {
     for (int64_t t = blockIdx.x; t < c.ntiles; t += gridDim.x) {
-        const GridDesc &gd = c.grids[c.tile_grid[t]];
+        const int32_t gid = c.tile_grid[t];
+        if (!grid_due(c, gid)) continue;
+        const GridDesc &gd = c.grids[gid];
         if (grid_swapped(c, gd)) continue;
         unsigned seeds = 0;
         for (int j = 0; j < PPT; j++) {
@@ -315,6 +334,7 @@ __global__ void __launch_bounds__(NT) k_lab_seed(Ctx c) {
 __global__ void __launch_bounds__(NT) k_emit(Ctx c) {
     __shared__ int64_t red[NT / 32];
     for (int64_t t = blockIdx.x; t < c.ntiles; t += gridDim.x) {
+        if (!grid_due(c, c.tile_grid[t])) continue;
         TileGeo g = tile_geo(c, int32_t(t));
         const GridDesc &gd = c.grids[g.g];
         int64_t drain = 0;
@@ -352,6 +372,7 @@ __global__ void k_arm(cudaGraphConditionalHandle h) { cudaGraphSetConditional(h,
 // network), stored at the grid's (problem, lambda) slot.
 __global__ void k_finalize(Ctx c, int32_t ngrids) {
     for (int g = blockIdx.x * blockDim.x + threadIdx.x; g < ngrids; g += gridDim.x * blockDim.x) {
+        if (!grid_due(c, g)) continue;
         const GridDesc &gd = c.grids[g];
         const int64_t idx = gd.kind == 1 ? g : int64_t(gd.prob) * c.nlam + c.cur_lam[g];
         c.flows[idx] = c.snk_sum[g] - c.drain[g];
@@ -368,6 +389,7 @@ __global__ void k_finalize(Ctx c, int32_t ngrids) {
 __global__ void __launch_bounds__(NT) k_advance_tiles(Ctx c, SeedArgs a) {
     const int64_t n = int64_t(a.W) * a.H;
     for (int64_t t = blockIdx.x; t < c.ntiles; t += gridDim.x) {
+        if (!grid_due(c, c.tile_grid[t])) continue;
         TileGeo g = tile_geo(c, int32_t(t));
         const GridDesc &gd = c.grids[g.g];
         const int cur = c.cur_lam[g.g];
@@ -426,6 +448,14 @@ __global__ void __launch_bounds__(1024) k_advance_grids(Ctx c, SeedArgs a, const
                                                         int has_cond) {
     int any = 0;
     for (int g = threadIdx.x; g < ngrids && a.nprob > 0; g += blockDim.x) {
+        if (c.rolling) {   // only the grids that just finished; the loop runs on while any grid is live
+            const int due = c.fin[g];
+            c.fin[g] = 0;
+            if (!due) {
+                any |= c.live[g];
+                continue;
+            }
+        }
         const GridDesc &gd = c.grids[g];
         const int cur = c.cur_lam[g];
         if (cur + 1 >= gd.lam_end) continue;

@@ -40,6 +40,7 @@ def main():
     ap.add_argument("--check", action="store_true", help="compare flows with a chain=1 solve")
     ap.add_argument("--reps", type=int, default=3)
     ap.add_argument("--nprob", type=int, default=None, help="problems per device batch")
+    ap.add_argument("--knob", action="append", default=[], help="name=value (any pmf_solver_set knob)")
     ap.add_argument("--images", type=int, default=1, help="images per device batch (rng_seed 0..)")
     a = ap.parse_args()
     c = CFG[a.cfg]
@@ -49,6 +50,9 @@ def main():
         probs += b.problems
     probs = probs if a.nprob is None else probs[:a.nprob]
     s = _native.Solver(0)
+    for kv in a.knob:
+        kn, kv_ = kv.split("=")
+        s.set(kn, int(kv_))
     if a.iters: s.set("push_iters", a.iters)
     if a.sweeps: s.set("push_sweeps", a.sweeps)
     if a.chunk: s.set("bfs_chunk", a.chunk)

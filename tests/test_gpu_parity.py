@@ -248,13 +248,16 @@ def test_c1_stress_repeated(engine, persistent):
         s.close()
 
 
+@pytest.mark.parametrize("rolling", [1, 0])
 @pytest.mark.parametrize("chain", [2, 3, 5])
-def test_warm_start_chains_match_reference(engine, chain):
+def test_warm_start_chains_match_reference(engine, chain, rolling):
     """Warm start along the nested schedule (each grid solves `chain`
     consecutive lambdas, reusing the previous maximum preflow) must give the
-    reference's cuts, swapped families included."""
+    reference's cuts, swapped families included -- both with a common step
+    per lambda (rolling=0) and with every grid advancing as soon as it
+    finishes (rolling=1)."""
     from paper_1509_06004_b200 import _native
-    s = _native.Solver(0, chain=chain)
+    s = _native.Solver(0, chain=chain, rolling=rolling)
     try:
         for case in load_seed_supergraphs():
             probs = _problems(case)
@@ -270,6 +273,39 @@ def test_warm_start_chains_match_reference(engine, chain):
             assert flows[0].tolist() == g["flows"]
             for j in range(20):
                 assert np.array_equal(labels[0][j], g["labels"][j]), (mode, j)
-        assert s.stats()["steps"] == chain
+        # steps: common lambda steps (rolling=0) / label rounds (rolling=1)
+        assert s.stats()["steps"] == chain if not rolling else s.stats()["steps"] >= chain
     finally:
         s.close()
+
+
+def test_c3_cpmc_image_rolling_vs_cold_vs_reference(engine):
+    """C3 CPMC image (500x375, 25 seeds x types A/B x L20): the rolling warm
+    start (default for many problems) must reproduce the cold per-lambda
+    solve bit for bit, the reference's per-type flow sums (SURVEY.md
+    Appendix A: A 2,408,913,070, B 2,293,473,574; first seed A 101,007,728,
+    B 99,225,144) and the oracle's cuts on sampled (problem, lambda) pairs."""
+    from paper_1509_06004_b200 import _native
+    b = synth.generate(500, 375, 5, 5, rng_seed=0, types=("A", "B"))
+    lams = synth.L20
+    warm = _native.Solver(0)
+    cold = _native.Solver(0, chain=1)
+    try:
+        _, fw, lw = warm.solve_seed_batch(500, 375, b.problems, lams, "auto")
+        assert warm.stats()["cycles"] > 0
+        _, fc, lc = cold.solve_seed_batch(500, 375, b.problems, lams, "auto")
+    finally:
+        warm.close()
+        cold.close()
+    assert np.array_equal(fw, fc)
+    assert np.array_equal(lw, lc)
+    per = fw.sum(axis=1)
+    assert int(per[0::2].sum()) == 2408913070 and int(per[1::2].sum()) == 2293473574
+    assert int(per[0]) == 101007728 and int(per[1]) == 99225144
+    for pi, li in ((0, 0), (17, 9), (49, 19)):
+        p = b.problems[pi]
+        src, snk, nbr = oracle.instantiate(p.unary_base, p.unary_slope, p.sink_base, p.pairwise,
+                                           p.fg_seeds, p.bg_seeds, lams[li])
+        flow, labels, _ = oracle.solve(500, 375, src, snk, nbr)
+        assert int(fw[pi, li]) == flow
+        assert np.array_equal(lw[pi, li].reshape(-1), labels)
