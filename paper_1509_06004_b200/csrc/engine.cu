@@ -211,7 +211,7 @@ struct pmf_solver {
     int timing = 0;
     int64_t max_cycles = 50000;
     // device workspace
-    DevBuf d_w, d_h, d_r, d_lab, d_tile_grid, d_tnb, d_fin, d_grids, d_live, d_act, d_list, d_inq, d_cnt,
+    DevBuf d_w, d_h, d_r, d_lab, d_tile_grid, d_tnb, d_fin, d_gpend, d_grids, d_live, d_act, d_list, d_inq, d_cnt,
         d_snk, d_drain, d_err, d_stat, d_colswap, d_out, d_in32, d_pw, d_mask, d_off, d_lam,
         d_swapcnt, d_swapflag, d_ring, d_qstate, d_qctr, d_ctl, d_curlam, d_flows, d_slopesum;
     HostBuf h_in32, h_pw, h_mask, h_out, h_small;
@@ -268,7 +268,7 @@ int setup_state(pmf_solver *s, int edge_bytes) {
     if ((rc = s->d_w.ensure(P * 4)) || (rc = s->d_h.ensure(P * 4)) ||
         (rc = s->d_r.ensure(P * size_t(edge_bytes))) || (rc = s->d_lab.ensure(P)) ||
         (rc = s->d_tile_grid.ensure(T * 4)) || (rc = s->d_tnb.ensure(T * 16)) || (rc = s->d_grids.ensure(G * sizeof(GridDesc))) ||
-        (rc = s->d_live.ensure(G * 4)) || (rc = s->d_fin.ensure(G * 4)) || (rc = s->d_act.ensure(G * 4)) ||
+        (rc = s->d_live.ensure(G * 4)) || (rc = s->d_fin.ensure(G * 4)) || (rc = s->d_gpend.ensure(G * 4)) || (rc = s->d_act.ensure(G * 4)) ||
         (rc = s->d_list.ensure(2 * T * 4)) || (rc = s->d_inq.ensure(2 * T * 4)) ||
         (rc = s->d_cnt.ensure(64)) || (rc = s->d_snk.ensure(G * 8)) || (rc = s->d_drain.ensure(G * 8)) ||
         (rc = s->d_err.ensure(64)) || (rc = s->d_stat.ensure(ST_NSTAT * 8)) ||
@@ -290,6 +290,7 @@ int setup_state(pmf_solver *s, int edge_bytes) {
     CK(cudaMemcpyAsync(s->d_curlam.p, s->curlam0.data(), G * 4, cudaMemcpyHostToDevice, s->st));
     CK(cudaMemsetAsync(s->d_act.p, 0, G * 4, s->st));
     CK(cudaMemsetAsync(s->d_fin.p, 0, G * 4, s->st));
+    CK(cudaMemsetAsync(s->d_gpend.p, 0, G * 4, s->st));
     CK(cudaMemsetAsync(s->d_snk.p, 0, G * 8, s->st));
     CK(cudaMemsetAsync(s->d_drain.p, 0, G * 8, s->st));
     CK(cudaMemsetAsync(s->d_err.p, 0, 64, s->st));
@@ -305,6 +306,8 @@ int setup_state(pmf_solver *s, int edge_bytes) {
     x.grids = s->d_grids.as<GridDesc>();
     x.live = s->d_live.as<int32_t>();
     x.fin = s->d_fin.as<int32_t>();
+    x.gpend = s->d_gpend.as<int32_t>();
+    x.ngrids = int32_t(G);
     x.rolling = 0;
     x.act = s->d_act.as<int32_t>();
     x.list0 = s->d_list.as<int32_t>();
@@ -734,6 +737,7 @@ int build_graph_rolling(pmf_solver *s, const Ctx &c0, int32_t ngrids, const Seed
                          int64_t(s->max_cycles), h_cycle, 1, h_lab, 1)))
         return rc;
     if ((rc = add_push_node<E>(s, cyc, &q, P.pq, K_PERSISTENT, lctl(ST_PUSH)))) return rc;
+    if ((rc = add_kernel(cyc, &q, dim3(1), dim3(1024), k_push_done, P.base, ngrids, h_cycle, 1, h_lab, 1))) return rc;
     // finished grids: labels, flow, next lambda
     cudaGraph_t lab;
     if ((rc = add_if(cyc, &q, h_lab, &lab))) return rc;
@@ -832,7 +836,9 @@ int host_solve_rolling(pmf_solver *s, const Ctx &c0, int32_t ngrids, const SeedA
         if (ctl.nact) {
             s->tmark(C_PUSH);
             launch_push<E>(s, P.pq, K_PERSISTENT);
+            LAUNCH(s, (k_push_done<<<1, 1024, 0, s->st>>>(c0, ngrids, 0, 0, 0, 0)));
             CK(cudaGetLastError());
+            if ((rc = read_ctl(s, c0, &ctl))) return rc;
         }
         if (!ctl.nfin) {
             if (!ctl.nact) break;

@@ -112,6 +112,8 @@ struct Ctx {
     const GridDesc *grids;
     int32_t *live;          // per grid: still has work
     int32_t *fin;           // per grid (rolling mode): finished its lambda this cycle, labels due
+    int32_t *gpend;         // per grid: its tiles queued or running in the current persistent phase
+    int32_t ngrids;
     int32_t rolling;        // rolling warm start: grids emit and advance as they finish
     int32_t *act;           // per grid active-pixel count of the last seed pass
     int32_t *list0, *list1; // double-buffered tile worklists
@@ -162,6 +164,7 @@ __device__ __forceinline__ void q_request(const Ctx &c, int32_t t) {
         if (s == Q_IDLE) {
             if (atomicCAS(&c.qstate[t], Q_IDLE, Q_QUEUED) == Q_IDLE) {
                 atomicAdd(&c.qctr[QC_PENDING], 1u);
+                atomicAdd(&c.gpend[c.tile_grid[t]], 1);
                 q_push(c, t);
                 return;
             }
@@ -182,6 +185,7 @@ __device__ __forceinline__ void q_finish(const Ctx &c, int32_t t, bool again) {
             return;
         }
         if (atomicCAS(&c.qstate[t], Q_RUNNING, Q_IDLE) == Q_RUNNING) {
+            atomicSub(&c.gpend[c.tile_grid[t]], 1);
             atomicSub(&c.qctr[QC_PENDING], 1u);
             return;
         }
@@ -226,6 +230,7 @@ __device__ __forceinline__ bool q_claim(const Ctx &c, int32_t t) {
     if (budget && ld_volatile(&c.qctr[QC_HEAD]) + ld_volatile(&c.qctr[QC_CONT]) >= budget) return false;
     if (atomicCAS(&c.qstate[t], Q_IDLE, Q_RUNNING) != Q_IDLE) return false;
     atomicAdd(&c.qctr[QC_PENDING], 1u);
+    atomicAdd(&c.gpend[c.tile_grid[t]], 1);
     atomicAdd(&c.qctr[QC_CONT], 1u);
     return true;
 }

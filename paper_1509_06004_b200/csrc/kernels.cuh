@@ -246,6 +246,8 @@ __global__ void k_phase_begin(Ctx c, int persistent, cudaGraphConditionalHandle 
             c.inq1[t] = 0;
         }
     }
+    if (persistent)
+        for (int64_t g = tid; g < c.ngrids; g += stride) c.gpend[g] = 0;
     if (tid == 0) {
         c.cnt[0] = c.cnt[1] = c.cnt[2] = 0;
         for (int q = 0; q < 4; q++) c.qctr[q] = 0;
@@ -301,6 +303,36 @@ __global__ void __launch_bounds__(1024) k_cycle_ctl(Ctx c, int32_t ngrids, int p
         // whether the cycle loop goes on once they have advanced)
         if (has_cond) cudaGraphSetConditional(cond, (!stop || (s_fin && !ctl->noconv)) ? 1u : 0u);
         if (has_lab) cudaGraphSetConditional(cond_lab, s_fin ? 1u : 0u);
+    }
+}
+
+// Rolling mode, after a discharge: a live grid none of whose tiles is still
+// queued or running has no active pixel left -- every pixel with excess is
+// frozen, and frozen heights are exact certificates (global relabel, or a
+// local relabel whose every exit was frozen) -- so its preflow is maximum
+// and it finishes now instead of after one more global relabel.  Swapped
+// grids report their sink side, which needs that exact relabel: they take
+// the regular path.
+__global__ void __launch_bounds__(1024) k_push_done(Ctx c, int32_t ngrids, cudaGraphConditionalHandle cond,
+                                                    int has_cond, cudaGraphConditionalHandle cond_lab,
+                                                    int has_lab) {
+    __shared__ int s_fin;
+    if (threadIdx.x == 0) s_fin = 0;
+    __syncthreads();
+    int nfin = 0;
+    for (int g = threadIdx.x; g < ngrids; g += blockDim.x) {
+        if (c.live[g] && c.gpend[g] == 0 && !grid_swapped(c, c.grids[g])) {
+            c.live[g] = 0;
+            c.fin[g] = 1;
+            nfin++;
+        }
+    }
+    if (nfin) atomicAdd(&s_fin, nfin);
+    __syncthreads();
+    if (threadIdx.x == 0 && s_fin && !c.ctl->noconv) {
+        c.ctl->nfin += s_fin;
+        if (has_cond) cudaGraphSetConditional(cond, 1u);
+        if (has_lab) cudaGraphSetConditional(cond_lab, 1u);
     }
 }
 
