@@ -49,8 +49,8 @@ CONFIGS = {
                     "(warm-start chains along the schedule)"),
     "c4": dict(w=1920, h=1080, rows=1, cols=1, types=("A",), lams="C4",
                desc="C4: synthetic 1920x1080, 1 seed, 8 lambdas per supergraph"),
-    "c5": dict(w=500, h=375, rows=5, cols=5, types=("A", "B"), lams="L20", images=2,
-               desc="C5: batch throughput -- 2 synthetic CPMC images (500x375, 25 seeds x 2 types "
+    "c5": dict(w=500, h=375, rows=5, cols=5, types=("A", "B"), lams="L20", images=8,
+               desc="C5: batch throughput -- 8 synthetic CPMC images (500x375, 25 seeds x 2 types "
                     "x 20 lambdas) per GPU per step, images independent across GPUs"),
 }
 # CPU reference sample per step for the big configs (the full C3 image is

@@ -207,6 +207,7 @@ struct pmf_solver {
     int push_budget_warm = 4;   // discharge budget factor when the batch runs warm-start chains
     int verify = 1;             // seed batches: device cut_cost == flow certificate per cut
     int rolling = 1;            // warm-start chains advance per grid as each finishes (no step barrier)
+    int push_minb = 2;          // CTA discharge: min CTAs per SM of its launch bounds (1 or 2)
     int bfs_chunk = 8;
     int timing = 0;
     int64_t max_cycles = 50000;
@@ -429,13 +430,20 @@ void launch_bfs(pmf_solver *s, const Ctx &c, bool sink, int k) {
     }
 }
 
+// CTA discharge kernel: 2 CTAs per SM at 32 registers (default) or one CTA
+// per SM at 64 registers (knob push_minb = 1)
+template <class E>
+auto push_kernel(const pmf_solver *s) -> decltype(&k_push<E, 2>) {
+    return s->push_minb == 1 ? &k_push<E, 1> : &k_push<E, 2>;
+}
+
 template <class E>
 void launch_push(pmf_solver *s, const Ctx &c, int k) {
     if (s->warp_eff & 1)
         LAUNCH(s, (k_wpush<E><<<s->grid_wpush, WPB * 32, s->smem_w, s->st>>>(c, k, s->push_iters, s->relabel_every,
                                                                             lctl(ST_PUSH))));
     else
-        LAUNCH(s, (k_push<E><<<s->grid_push, NTT, 0, s->st>>>(c, k, s->push_iters, s->relabel_every, s->relax_cap,
+        LAUNCH(s, (push_kernel<E>(s)<<<s->grid_push, NTT, 0, s->st>>>(c, k, s->push_iters, s->relabel_every, s->relax_cap,
                                                               lctl(ST_PUSH))));
 }
 
@@ -607,7 +615,7 @@ int add_push_node(pmf_solver *s, cudaGraph_t g, cudaGraphNode_t *prev, const Ctx
     if (s->warp_eff & 1)
         return add_kernel_smem(g, prev, dim3(s->grid_wpush), dim3(WPB * 32), s->smem_w, k_wpush<E>, c, k,
                                s->push_iters, s->relabel_every, lc);
-    return add_kernel(g, prev, dim3(s->grid_push), dim3(NTT), k_push<E>, c, k, s->push_iters, s->relabel_every,
+    return add_kernel(g, prev, dim3(s->grid_push), dim3(NTT), push_kernel<E>(s), c, k, s->push_iters, s->relabel_every,
                       s->relax_cap, lc);
 }
 
@@ -757,7 +765,7 @@ int build_graph_rolling(pmf_solver *s, const Ctx &c0, int32_t ngrids, const Seed
 // knobs + context a cached graph was built for
 struct GraphKey {
     Ctx ctx;
-    int32_t ngrids, edge, p_push, p_bfs, iters, relabel, budget, sweeps, warp, relax_cap, multi;
+    int32_t ngrids, edge, p_push, p_bfs, iters, relabel, budget, sweeps, warp, relax_cap, multi, minb;
     int64_t maxc;
     int32_t gfull, gbfs, gpush;
     SeedArgs sa;
@@ -782,6 +790,7 @@ int graph_solve(pmf_solver *s, const Ctx &c0, int32_t ngrids, const SeedArgs *sa
     key.warp = s->warp_eff;
     key.relax_cap = s->relax_cap;
     key.multi = s->bfs_multi;
+    key.minb = s->push_minb;
     key.maxc = s->max_cycles;
     key.gfull = s->grid_full;
     key.gbfs = s->grid_bfs;
@@ -976,7 +985,7 @@ int64_t max_pair(const int32_t *nb, int W, int H) {
 template <class E>
 int grids_for(pmf_solver *s) {
     int occ = 0;
-    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_push<E>, NTT, 0));
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, push_kernel<E>(s), NTT, 0));
     s->grid_push = std::max(1, occ) * s->sms;
     // BFS grids are co-resident (cooperative K_MULTI launches): the smaller
     // occupancy of the sink and label kernels
@@ -1328,6 +1337,7 @@ int pmf_solver_set(pmf_solver *s, const char *name, int64_t v) {
     else if (k == "push_budget_warm" && v >= 0) s->push_budget_warm = int(v);
     else if (k == "verify") s->verify = v != 0;
     else if (k == "rolling") s->rolling = v != 0;
+    else if (k == "push_minb" && (v == 1 || v == 2)) s->push_minb = int(v);
     else if (k == "graph") s->use_graph = v != 0;
     else if (k == "persistent_bfs") s->persistent_bfs = v != 0;
     else if (k == "bfs_multi") s->bfs_multi = v != 0;

@@ -446,9 +446,9 @@ __device__ __forceinline__ int ring_index(int s, int j) {
     }
 }
 
-template <class E>
-__global__ void __launch_bounds__(NTT, 2) k_push(Ctx c, int k, int iters, int relabel_every, int relax_cap,
-                                                 LaunchCtl lc) {
+template <class E, int MINB>
+__global__ void __launch_bounds__(NTT, MINB) k_push(Ctx c, int k, int iters, int relabel_every, int relax_cap,
+                                                    LaunchCtl lc) {
     __shared__ int32_t sh[RPIX];        // heights (ring: neighbour tiles)
     __shared__ int32_t sin[4][RPIX];    // sin[d][q]: flow pushed into q by its d-neighbour
     __shared__ int32_t sd[TH * SP];     // local relabel distances
