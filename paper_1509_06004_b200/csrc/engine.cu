@@ -11,6 +11,7 @@
 #include <condition_variable>
 #include <cstdarg>
 #include <cstdio>
+#include <sys/mman.h>
 #include <cstring>
 #include <functional>
 #include <mutex>
@@ -213,7 +214,7 @@ struct pmf_solver {
     int64_t max_cycles = 50000;
     // device workspace
     DevBuf d_w, d_h, d_r, d_lab, d_tile_grid, d_tnb, d_fin, d_gpend, d_grids, d_live, d_act, d_list, d_inq, d_cnt,
-        d_snk, d_drain, d_err, d_stat, d_colswap, d_out, d_in32, d_pw, d_mask, d_off, d_lam,
+        d_snk, d_drain, d_err, d_stat, d_colswap, d_out, d_bits, d_in32, d_pw, d_mask, d_off, d_lam,
         d_swapcnt, d_swapflag, d_ring, d_qstate, d_qctr, d_ctl, d_curlam, d_flows, d_slopesum;
     HostBuf h_in32, h_pw, h_mask, h_out, h_small;
     Layout lay;
@@ -1100,7 +1101,6 @@ int seed_stage(pmf_solver *s, int32_t nprob, int32_t W, int32_t H, const int64_t
     TaskErr terr;
     // masks first (seed index lists are short)
     for (int p = 0; p < nprob; p++) {
-        S.offs[p] = 3 * int64_t(p) * n;   // base of problem p; slope +n, sink +2n
         uint8_t *m = hm + p * n;
         memset(m, 0, size_t(n));
         for (int32_t i = 0; i < (n_fg ? n_fg[p] : 0); i++) {
@@ -1132,47 +1132,90 @@ int seed_stage(pmf_solver *s, int32_t nprob, int32_t W, int32_t H, const int64_t
     s->pool->run(int64_t(pw_list.size()), [&](int64_t k) { mp[k] = max_pair(hp + k * 4 * n, W, H); });
     int64_t maxpair = 0;
     for (int64_t v : mp) maxpair = std::max(maxpair, v);
-    // unary / sink planes: ranges the device relies on (instantiate's own
-    // checks are the caller's), then narrow
+    // unary / sink planes.  Problems whose three planes equal those of the
+    // previous problem (e.g. the two seed types of one CPMC seed) share one
+    // staged copy.  Every problem is range-checked against its own masks
+    // (ranges the device relies on; instantiate's own checks are the
+    // caller's); only the distinct planes are narrowed and copied, in groups
+    // whose H2D overlaps the conversion of the next group.
+    std::vector<uint8_t> same(size_t(nprob), 0);
+    s->pool->run(nprob, [&](int64_t p) {
+        if (p == 0) return;
+        const size_t nb = size_t(n) * 8;
+        same[p] = (ub[p] == ub[p - 1] || !memcmp(ub[p], ub[p - 1], nb)) &&
+                  (us[p] == us[p - 1] || !memcmp(us[p], us[p - 1], nb)) &&
+                  (sb[p] == sb[p - 1] || !memcmp(sb[p], sb[p - 1], nb));
+    });
+    std::vector<int32_t> uniq;   // problems whose planes are staged
+    std::vector<int32_t> staged_as(static_cast<size_t>(nprob), 0);
+    for (int p = 0; p < nprob; p++) {
+        if (!same[p]) uniq.push_back(p);
+        staged_as[p] = uniq.back();
+        S.offs[p] = 3 * int64_t(uniq.size() - 1) * n;   // base of problem p; slope +n, sink +2n
+    }
+    // range check of pixel q of problem p (seed masks exempt fg unary / bg sink terms)
+    auto check = [&](int p, int64_t q, uint8_t m) -> bool {
+        if (m != 1) {
+            const int64_t b = ub[p][q], sl = us[p][q];
+            if (b < 0 || sl < 0) {
+                terr.set(PMF_ERR_RANGE, "negative unary term");
+                return false;
+            }
+            if (b > CAP_MAX || (sl && lam_max > (CAP_MAX - b) / sl)) {
+                terr.set(PMF_ERR_RANGE, "unary term exceeds CAP_MAX");
+                return false;
+            }
+        }
+        if (m != 2 && (sb[p][q] < 0 || sb[p][q] > CAP_MAX)) {
+            terr.set(PMF_ERR_RANGE, "sink term outside [0, CAP_MAX]");
+            return false;
+        }
+        return true;
+    };
+    // problems sharing planes: only the pixels where their seed masks differ
+    // from the staged problem's need their own check
     const int64_t pl_chunks = cdiv(n, kChunk);
     s->pool->run(int64_t(nprob) * pl_chunks, [&](int64_t task) {
         const int p = int(task / pl_chunks);
+        if (!same[p]) return;
         const int64_t lo = (task % pl_chunks) * kChunk, hi = std::min(n, lo + kChunk);
-        const uint8_t *m = hm + p * n;
-        for (int64_t q = lo; q < hi; q++) {
-            if (m[q] != 1) {
-                int64_t b = ub[p][q], sl = us[p][q];
-                if (b < 0 || sl < 0) {
-                    terr.set(PMF_ERR_RANGE, "negative unary term");
-                    return;
-                }
-                if (b > CAP_MAX || (sl && lam_max > (CAP_MAX - b) / sl)) {
-                    terr.set(PMF_ERR_RANGE, "unary term exceeds CAP_MAX");
-                    return;
-                }
-            }
-            if (m[q] != 2 && (sb[p][q] < 0 || sb[p][q] > CAP_MAX)) {
-                terr.set(PMF_ERR_RANGE, "sink term outside [0, CAP_MAX]");
-                return;
-            }
-        }
-        narrow(hb + 3 * p * n + 0 * n + lo, ub[p] + lo, hi - lo, 0, CAP_MAX);
-        narrow(hb + 3 * p * n + 1 * n + lo, us[p] + lo, hi - lo, 0, CAP_MAX);
-        narrow(hb + 3 * p * n + 2 * n + lo, sb[p] + lo, hi - lo, 0, CAP_MAX);
+        const uint8_t *m = hm + p * n, *mr = hm + int64_t(staged_as[p]) * n;
+        for (int64_t q = lo; q < hi; q++)
+            if (m[q] != mr[q] && !check(p, q, m[q])) return;
     });
     if ((rc = terr.raise())) return rc;
     S.u8 = maxpair <= 255;
     if (!S.u8 && CAP_MAX + 8 * maxpair >= (int64_t(1) << 31) - 1)
         return fail(PMF_ERR_RANGE, "pairwise capacities too large for the int32 device state");
     S.lambdas.assign(lambdas, lambdas + nlam);
-    const size_t bytes_b = size_t(nprob) * n * 3 * 4, bytes_pw = pw_list.size() * size_t(4 * n) * 4;
+    const int64_t nu = int64_t(uniq.size());
+    const size_t bytes_b = size_t(nu) * n * 3 * 4, bytes_pw = pw_list.size() * size_t(4 * n) * 4;
     if ((rc = s->d_in32.ensure(bytes_b)) || (rc = s->d_pw.ensure(bytes_pw)) ||
         (rc = s->d_mask.ensure(size_t(nprob) * n)) || (rc = s->d_off.ensure(size_t(nprob) * 16)) ||
         (rc = s->d_lam.ensure(size_t(nlam) * 8)) || (rc = s->d_swapcnt.ensure(size_t(nprob) * 8)))
         return rc;
-    CK(cudaMemcpyAsync(s->d_in32.p, hb, bytes_b, cudaMemcpyHostToDevice, s->st));
     CK(cudaMemcpyAsync(s->d_pw.p, hp, bytes_pw, cudaMemcpyHostToDevice, s->st));
     CK(cudaMemcpyAsync(s->d_mask.p, hm, size_t(nprob) * n, cudaMemcpyHostToDevice, s->st));
+    // distinct planes: check + narrow in one pass, group by group, each
+    // group's H2D overlapping the conversion of the next
+    const int64_t group = std::max<int64_t>(1, cdiv(nu, 8));
+    for (int64_t g0 = 0; g0 < nu; g0 += group) {
+        const int64_t g1 = std::min(nu, g0 + group);
+        s->pool->run((g1 - g0) * pl_chunks, [&](int64_t task) {
+            const int64_t u = g0 + task / pl_chunks;
+            const int p = uniq[size_t(u)];
+            const int64_t lo = (task % pl_chunks) * kChunk, hi = std::min(n, lo + kChunk);
+            const uint8_t *m = hm + p * n;
+            for (int64_t q = lo; q < hi; q++)
+                if (!check(p, q, m[q])) return;
+            narrow(hb + 3 * u * n + 0 * n + lo, ub[p] + lo, hi - lo, 0, CAP_MAX);
+            narrow(hb + 3 * u * n + 1 * n + lo, us[p] + lo, hi - lo, 0, CAP_MAX);
+            narrow(hb + 3 * u * n + 2 * n + lo, sb[p] + lo, hi - lo, 0, CAP_MAX);
+        });
+        if ((rc = terr.raise())) return rc;
+        CK(cudaMemcpyAsync(s->d_in32.as<int32_t>() + 3 * g0 * n, hb + 3 * g0 * n, size_t(g1 - g0) * 3 * n * 4,
+                           cudaMemcpyHostToDevice, s->st));
+    }
     CK(cudaMemcpyAsync(s->d_off.p, S.offs.data(), S.offs.size() * 8, cudaMemcpyHostToDevice, s->st));
     CK(cudaMemcpyAsync(s->d_lam.p, S.lambdas.data(), size_t(nlam) * 8, cudaMemcpyHostToDevice, s->st));
     // warm-start chains: nlam lambdas split into chains of S.chain
@@ -1192,7 +1235,7 @@ int seed_stage(pmf_solver *s, int32_t nprob, int32_t W, int32_t H, const int64_t
     S.slope_sum.assign(size_t(nprob), 0);
     s->pool->run(nprob, [&](int64_t p) {
         const uint8_t *m = hm + p * n;
-        const int32_t *sl = hb + 3 * p * n + n;
+        const int32_t *sl = hb + S.offs[p] + n;
         int64_t acc = 0;
         for (int64_t q = 0; q < n; q++)
             if (m[q] != 1) acc += sl[q];
@@ -1211,18 +1254,39 @@ int seed_stage(pmf_solver *s, int32_t nprob, int32_t W, int32_t H, const int64_t
     return 0;
 }
 
+// 8 output bytes (bit j -> byte j, 0/1) per input byte
+struct UnpackLut {
+    uint64_t v[256];
+    UnpackLut() {
+        for (int b = 0; b < 256; b++) {
+            uint64_t w = 0;
+            for (int j = 0; j < 8; j++) w |= uint64_t((b >> j) & 1) << (8 * j);
+            v[b] = w;
+        }
+    }
+};
+
 int seed_fetch(pmf_solver *s, uint8_t *swapped_out, int64_t *flows_out, uint8_t *labels_out) {
+    static const UnpackLut lut;
     const SeedStage &S = s->stage;
-    const Layout &L = s->lay;
     const int64_t nf = int64_t(S.nprob) * S.nlam;
     const int64_t out_bytes = nf * int64_t(S.W) * S.H;
-    const size_t lab_bytes = size_t((out_bytes + 7) / 8) * 8;
+    // labels travel as bits (k_pack_bits) and are unpacked on the host
+    const int64_t nwords = cdiv(out_bytes, 32), bit_bytes = nwords * 4;
+    const size_t lab_bytes = size_t(cdiv(bit_bytes, 64) * 64);
     int rc;
     if ((rc = s->h_out.ensure(lab_bytes + size_t(nf) * 8 + size_t(S.nprob) * 4 + 64))) return rc;
     uint8_t *ho = s->h_out.as<uint8_t>();
     int64_t *hfl = (int64_t *)(ho + lab_bytes);
     int32_t *hsw = (int32_t *)(hfl + nf);
-    if (labels_out) CK(cudaMemcpyAsync(ho, s->d_out.p, out_bytes, cudaMemcpyDeviceToHost, s->st));
+    if (labels_out) {
+        if ((rc = s->d_bits.ensure(size_t(bit_bytes)))) return rc;
+        const int grid = int(std::min<int64_t>(cdiv(out_bytes, 128 * 8), 16 * s->sms));
+        LAUNCH(s, (k_pack_bits<<<std::max(grid, 1), 256, 0, s->st>>>(s->d_out.as<uint8_t>(), s->d_bits.as<uint32_t>(),
+                                                                     out_bytes)));
+        CK(cudaGetLastError());
+        CK(cudaMemcpyAsync(ho, s->d_bits.p, size_t(bit_bytes), cudaMemcpyDeviceToHost, s->st));
+    }
     CK(cudaMemcpyAsync(hfl, s->d_flows.p, nf * 8, cudaMemcpyDeviceToHost, s->st));
     CK(cudaMemcpyAsync(hsw, s->d_swapflag.p, size_t(S.nprob) * 4, cudaMemcpyDeviceToHost, s->st));
     CK(cudaStreamSynchronize(s->st));
@@ -1230,14 +1294,26 @@ int seed_fetch(pmf_solver *s, uint8_t *swapped_out, int64_t *flows_out, uint8_t 
     if (swapped_out)
         for (int p = 0; p < S.nprob; p++) swapped_out[p] = uint8_t(hsw[p] != 0);
     if (labels_out) {
-        const int64_t chunks = cdiv(out_bytes, int64_t(4) << 20);
+        // large outputs are fresh memory: ask for huge pages so first touch
+        // costs one fault per 2 MiB instead of per 4 KiB
+        if (out_bytes >= (int64_t(64) << 20)) {
+            const uintptr_t a = (reinterpret_cast<uintptr_t>(labels_out) + 0x1fffff) & ~uintptr_t(0x1fffff);
+            const uintptr_t e = (reinterpret_cast<uintptr_t>(labels_out) + uintptr_t(out_bytes)) & ~uintptr_t(0x1fffff);
+            if (e > a) madvise(reinterpret_cast<void *>(a), e - a, MADV_HUGEPAGE);
+        }
+        // parallel unpack straight into the caller's buffer (64 KiB of bits per task)
+        const int64_t per = int64_t(64) << 10, full = out_bytes / 8, chunks = cdiv(full, per);
         s->pool->run(chunks, [&](int64_t i) {
-            const int64_t lo = i * (int64_t(4) << 20), hi = std::min(out_bytes, lo + (int64_t(4) << 20));
-            memcpy(labels_out + lo, ho + lo, size_t(hi - lo));
+            const int64_t lo = i * per, hi = std::min(full, lo + per);
+            uint64_t *dst = reinterpret_cast<uint64_t *>(labels_out) + lo;
+            for (int64_t k = lo; k < hi; k++) {
+                const uint64_t v = lut.v[ho[k]];
+                memcpy(dst + (k - lo), &v, 8);
+            }
         });
+        for (int64_t i = full * 8; i < out_bytes; i++) labels_out[i] = uint8_t((ho[i >> 3] >> (i & 7)) & 1);
     }
-    s->stats.d2h_bytes = (labels_out ? out_bytes : 0) + nf * 8 + int64_t(S.nprob) * 4;
-    (void)L;
+    s->stats.d2h_bytes = (labels_out ? bit_bytes : 0) + nf * 8 + int64_t(S.nprob) * 4;
     return 0;
 }
 

@@ -396,6 +396,41 @@ __global__ void __launch_bounds__(NT) k_emit(Ctx c) {
 
 namespace pmf {
 
+// Label bytes (0/1) -> bit array for the D2H (8x fewer bytes over the host
+// link): bit j of word w is byte 32*w + j.  Each warp packs 128 bytes per
+// step (uchar4 per lane, four ballots).
+__global__ void k_pack_bits(const uint8_t *__restrict__ bytes, uint32_t *__restrict__ bits, int64_t n) {
+    const int lane = threadIdx.x & 31;
+    const int64_t warp = (blockIdx.x * int64_t(blockDim.x) + threadIdx.x) >> 5;
+    const int64_t nwarps = (int64_t(gridDim.x) * blockDim.x) >> 5;
+    for (int64_t base = warp * 128; base < n; base += nwarps * 128) {
+        const int64_t i = base + 4 * lane;
+        uchar4 v = make_uchar4(0, 0, 0, 0);
+        if (i + 3 < n) {
+            v = *reinterpret_cast<const uchar4 *>(bytes + i);
+        } else {
+            if (i < n) v.x = bytes[i];
+            if (i + 1 < n) v.y = bytes[i + 1];
+            if (i + 2 < n) v.z = bytes[i + 2];
+        }
+        // byte base + 4*lane + k sits in word base/32 + (4*lane + k)/32, bit (4*lane + k) % 32
+        const unsigned b0 = __ballot_sync(0xffffffffu, v.x != 0), b1 = __ballot_sync(0xffffffffu, v.y != 0),
+                       b2 = __ballot_sync(0xffffffffu, v.z != 0), b3 = __ballot_sync(0xffffffffu, v.w != 0);
+        if (lane < 4) {
+            // word lane covers lanes 8*lane .. 8*lane + 7 (4 bytes each)
+            uint32_t w = 0;
+#pragma unroll
+            for (int l = 0; l < 8; l++) {
+                const int src = 8 * lane + l;
+                w |= (((b0 >> src) & 1u) << (4 * l)) | (((b1 >> src) & 1u) << (4 * l + 1)) |
+                     (((b2 >> src) & 1u) << (4 * l + 2)) | (((b3 >> src) & 1u) << (4 * l + 3));
+            }
+            const int64_t wi = base / 32 + lane;
+            if (wi * 32 < n) bits[wi] = w;
+        }
+    }
+}
+
 // Arm a conditional node (graph mode): 1 before the loop it controls.
 __global__ void k_arm(cudaGraphConditionalHandle h) { cudaGraphSetConditional(h, 1u); }
 

@@ -73,18 +73,24 @@ def border_pixels(width, height, top=True):
     return frozenset(int(p) for p in grid[ring])
 
 
-def seed_problem(img, x, y, pairwise, bg):
-    """Terminal weights from intensity similarity to the seed pixel."""
-    height, width = img.shape
+def seed_terms(img, x, y):
+    """(unary_base, unary_slope, sink_base) from intensity similarity to the
+    seed pixel."""
     dsim = np.abs(img - img[y, x])
     near = INTENSITY_MAX - dsim
+    return ((1 + (near * 15) // INTENSITY_MAX).reshape(-1), (1 + (near * 7) // INTENSITY_MAX).reshape(-1),
+            (1 + (dsim * 63) // INTENSITY_MAX).reshape(-1))
+
+
+def seed_problem(img, x, y, pairwise, bg, terms=None):
+    """Terminal weights from intensity similarity to the seed pixel (the
+    seed types of one seed share ``terms``: same arrays, staged once)."""
+    height, width = img.shape
     idx = y * width + x
     if idx in bg:
         raise ValueError(f"seed ({x}, {y}) sits on the border")
-    return SeedProblem(width=width, height=height,
-                       unary_base=(1 + (near * 15) // INTENSITY_MAX).reshape(-1),
-                       unary_slope=(1 + (near * 7) // INTENSITY_MAX).reshape(-1),
-                       sink_base=(1 + (dsim * 63) // INTENSITY_MAX).reshape(-1),
+    base, slope, sink = terms if terms is not None else seed_terms(img, x, y)
+    return SeedProblem(width=width, height=height, unary_base=base, unary_slope=slope, sink_base=sink,
                        pairwise=pairwise, fg_seeds=frozenset({idx}), bg_seeds=bg)
 
 
@@ -117,5 +123,8 @@ def generate(width, height, seed_rows=1, seed_cols=1, regions=4, noise=10, rng_s
     pw = contrast_weights(img)
     bgs = {"A": border_pixels(width, height), "B": border_pixels(width, height, top=False)}
     coords = lattice(width, height, seed_rows, seed_cols)
-    probs = [seed_problem(img, x, y, pw, bgs[t]) for (x, y) in coords for t in types]
+    probs = []
+    for (x, y) in coords:
+        terms = seed_terms(img, x, y)
+        probs += [seed_problem(img, x, y, pw, bgs[t], terms) for t in types]
     return SynthBatch(img, reg, coords, probs)

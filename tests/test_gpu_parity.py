@@ -309,3 +309,42 @@ def test_c3_cpmc_image_rolling_vs_cold_vs_reference(engine):
         flow, labels, _ = oracle.solve(500, 375, src, snk, nbr)
         assert int(fw[pi, li]) == flow
         assert np.array_equal(lw[pi, li].reshape(-1), labels)
+
+
+def test_staging_shares_equal_planes_but_checks_each_mask(engine):
+    """Problems with equal unary/sink planes are staged once (pointer-equal
+    or content-equal arrays); results stay per problem, and each problem's
+    range check still uses its own seed masks."""
+    from paper_1509_06004_b200 import _native
+    from paper_1509_06004_b200.grid import CapacityOverflowError
+    b = synth.generate(64, 48, 1, 2, rng_seed=3, types=("A", "B"))
+    a0, b0 = b.problems[0], b.problems[1]
+    assert a0.unary_base.ctypes.data == b0.unary_base.ctypes.data   # generator shares the seed terms
+    # a content-equal copy with the other seed type must give the same cuts as b0
+    c0 = SeedProblem(64, 48, a0.unary_base.copy(), a0.unary_slope.copy(), a0.sink_base.copy(),
+                     a0.pairwise, a0.fg_seeds, b0.bg_seeds)
+    lams = [1, 4, 9]
+    s = _native.Solver(0)
+    try:
+        _, f1, l1 = s.solve_seed_batch(64, 48, [a0, b0, b.problems[2]], lams, "auto")
+        _, f2, l2 = s.solve_seed_batch(64, 48, [a0, c0, b.problems[2]], lams, "auto")
+        assert np.array_equal(f1, f2) and np.array_equal(l1, l2)
+        for pi, p in enumerate((a0, b0)):
+            for li, lam in enumerate(lams):
+                src, snk, nbr = oracle.instantiate(p.unary_base, p.unary_slope, p.sink_base, p.pairwise,
+                                                   p.fg_seeds, p.bg_seeds, lam)
+                flow, labels, _ = oracle.solve(64, 48, src, snk, nbr)
+                assert int(f1[pi, li]) == flow and np.array_equal(l1[pi, li], labels)
+        # pixel 0 is a bg seed of type A only: an out-of-range sink term there
+        # is exempt for A but must be rejected for the plane-sharing B problem
+        sink = a0.sink_base.copy()
+        sink[0] = CAP_MAX + 1
+        pa = SeedProblem(64, 48, a0.unary_base, a0.unary_slope, sink, a0.pairwise, a0.fg_seeds,
+                         a0.bg_seeds)
+        pb = SeedProblem(64, 48, a0.unary_base, a0.unary_slope, sink, a0.pairwise, a0.fg_seeds,
+                         b0.bg_seeds - {0})
+        s.solve_seed_batch(64, 48, [pa], lams, "off")
+        with pytest.raises(CapacityOverflowError):
+            s.solve_seed_batch(64, 48, [pa, pb], lams, "off")
+    finally:
+        s.close()
