@@ -57,6 +57,15 @@ CONFIGS = {
 # ~3,400 CPU-s on the reference algorithm): the first problems' lambda graphs
 REF_SAMPLE_PROBLEMS = {"c3": 2, "c5": 2, "c4": 1}
 BYTES_PER_PIXEL_PASS = {4: 24, 16: 48}   # load+store of w, h and the residual word(s)
+# algorithmic bytes per pixel of one tile pass of each kind of the
+# asynchronous solver, by residual word size 4 / 16:
+#   push  load+store w, h, r          bfs   load h, r; store h
+#   lab   load lab, r; store lab      binit load w; store h
+#   seed  load w, h                   linit load w; store lab
+#   emit  load w, lab|h, mask, slope; store out, w, h (next lambda's init)
+ASYNC_BYTES = {"push_tile_passes": (24, 48), "bfs_tile_passes": (12, 24), "label_tile_passes": (6, 18),
+               "binit_tile_passes": (8, 8), "seed_tile_passes": (8, 8), "linit_tile_passes": (5, 5),
+               "emit_tile_passes": (22, 22)}
 
 
 # ----------------------------------------------------------------- helpers
@@ -108,14 +117,15 @@ def measured_peaks():
     return 6650.0, "fallback"
 
 
-def committed_traffic():
-    """Per-launch DRAM bytes of k_push from the committed ncu capture."""
-    path = os.path.join(ROOT, "profiles", "push_traffic.json")
+def committed_traffic(kernel, config):
+    """Per-launch DRAM bytes (ncu dram__bytes_read + write) of `kernel` on
+    `config` from the committed capture in profiles/traffic.json, or None."""
+    path = os.path.join(ROOT, "profiles", "traffic.json")
     if not os.path.exists(path):
         return None
     with open(path) as f:
         d = json.load(f)
-    return d.get("dram_bytes_per_launch")
+    return d.get(kernel, {}).get("per_config", {}).get(config, {}).get("dram_bytes_per_launch")
 
 
 class ClockSampler:
@@ -282,20 +292,42 @@ def run_b200(args, cfg):
     dev_s_max = reduce_max(dev_s, torch.device("cuda", dev))
     value = world * cuts_per_step * args.steps / dev_s_max
 
-    # roofline of the dominant kernel (push-relabel sweep)
-    push_ms = sum(s["ms_push"] for s in stats)
-    push_launches = sum(s["push_sweeps"] for s in stats)
-    tile_passes = sum(s["push_tile_passes"] for s in stats)
-    edge_bytes = stats[-1]["edge_bytes"]
-    bpp = BYTES_PER_PIXEL_PASS[edge_bytes]
-    alg_bytes_per_launch = tile_passes * 1024 * bpp / max(push_launches, 1)
-    avg_launch_s = push_ms / 1e3 / max(push_launches, 1)
-    achieved = alg_bytes_per_launch / avg_launch_s / 1e9 if avg_launch_s else 0.0
+    # roofline of the dominant kernel: the asynchronous solve kernel (every
+    # phase of every grid, one launch per step) or, step-synchronous, the
+    # push-relabel discharge
     peak, peak_kind = measured_peaks()
-    traffic = committed_traffic()
+    edge_bytes = stats[-1]["edge_bytes"]
     total_ms = sum(s["ms_device"] for s in stats)
-    share = {k: round(sum(s[k] for s in stats) / total_ms, 4) for k in
-             ("ms_push", "ms_bfs", "ms_labels")} if total_ms else {}
+    if stats[-1]["async_mode"]:
+        col = 0 if edge_bytes == 4 else 1
+        kern_ms = sum(s["ms_async"] for s in stats)
+        alg_bytes = sum(s[k] * 1024 * v[col] for s in stats for k, v in ASYNC_BYTES.items())
+        achieved = alg_bytes / args.steps / (kern_ms / 1e3 / args.steps) / 1e9 if kern_ms else 0.0
+        roofline = {"bound": "hbm", "kernel": "k_async (asynchronous solve: relabel, discharge, labels, "
+                                              "emit of every grid in one persistent launch)",
+                    "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
+                    "traffic": committed_traffic("k_async", args.config), "peak_kind": peak_kind,
+                    "bytes_per_pixel_pass": {k.replace("_tile_passes", ""): v[col] for k, v in ASYNC_BYTES.items()},
+                    "tile_passes_per_step": {k.replace("_tile_passes", ""): stats[-1][k] for k in ASYNC_BYTES},
+                    "avg_launch_us": kern_ms * 1e3 / args.steps,
+                    "time_share": {"k_async": round(kern_ms / total_ms, 4) if total_ms else None}}
+    else:
+        push_ms = sum(s["ms_push"] for s in stats)
+        push_launches = sum(s["push_sweeps"] for s in stats)
+        tile_passes = sum(s["push_tile_passes"] for s in stats)
+        bpp = BYTES_PER_PIXEL_PASS[edge_bytes]
+        alg_bytes_per_launch = tile_passes * 1024 * bpp / max(push_launches, 1)
+        avg_launch_s = push_ms / 1e3 / max(push_launches, 1)
+        achieved = alg_bytes_per_launch / avg_launch_s / 1e9 if avg_launch_s else 0.0
+        share = {k: round(sum(s[k] for s in stats) / total_ms, 4) for k in
+                 ("ms_push", "ms_bfs", "ms_labels")} if total_ms else {}
+        roofline = {"bound": "hbm", "kernel": "k_push (push-relabel tile discharge)",
+                    "achieved": achieved, "peak": peak, "unit": "GB/s",
+                    "frac": achieved / peak, "traffic": committed_traffic("k_push", args.config), "peak_kind": peak_kind,
+                    "bytes_per_pixel_pass": bpp,
+                    "pixel_passes_per_s": tile_passes * 1024 / (push_ms / 1e3) if push_ms else 0,
+                    "avg_launch_us": avg_launch_s * 1e6,
+                    "time_share": share}
 
     # ---- end to end through the public API (host SeedProblems in, CutResults out)
     e2e_s, h2d, d2h = 0.0, 0, 0
@@ -359,18 +391,13 @@ def run_b200(args, cfg):
                        "parallelism": f"{world} GPU(s), independent supergraphs, no collectives"},
             "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": h2d // args.steps,
                     "d2h_bytes_per_step": d2h // args.steps},
-            "roofline": {"bound": "hbm", "kernel": "k_push (push-relabel tile sweep)",
-                         "achieved": achieved, "peak": peak, "unit": "GB/s",
-                         "frac": achieved / peak, "traffic": traffic, "peak_kind": peak_kind,
-                         "bytes_per_pixel_pass": bpp,
-                         "pixel_passes_per_s": tile_passes * 1024 / (push_ms / 1e3) if push_ms else 0,
-                         "avg_launch_us": avg_launch_s * 1e6,
-                         "time_share": share},
+            "roofline": roofline,
             "cpu_baseline": cpu,
             "clocks": clk.summary(),
             "gpu_launches": int(sum(s["kernels"] for s in stats)),
-            "solver": {k: stats[-1][k] for k in ("cycles", "steps", "push_sweeps", "push_tile_passes",
-                                                  "bfs_sweeps", "bfs_tile_passes", "tiles",
+            "solver": {k: stats[-1][k] for k in ("async_mode", "cycles", "steps", "push_sweeps",
+                                                  "push_tile_passes", "bfs_sweeps", "bfs_tile_passes",
+                                                  "label_tile_passes", "scan_tile_passes", "tiles",
                                                   "edge_bytes", "grids")},
             "cpmc": cpmc,
         }

@@ -77,7 +77,15 @@ typedef struct pmf_stats {
     int64_t d2h_bytes;          /* device->host bytes of the last fetch       */
     int64_t graph_builds;       /* solve graphs (re)built by the last run     */
     int64_t kernels;            /* kernels executed on the device by the run  */
-    int64_t steps;              /* warm-start steps (lambdas per chain)       */
+    int64_t steps;              /* warm-start steps (lambdas per chain); async: lambda-graphs finished */
+    int64_t scan_tile_passes;   /* async: init / seed / label-init / emit tile passes */
+    double ms_async;            /* async: span of the persistent solve kernel (device clock) */
+    int32_t async_mode;         /* 1: the last run used the asynchronous solver */
+    int32_t reserved;
+    int64_t binit_tile_passes;  /* async scan phases, tiles each: relabel init, */
+    int64_t seed_tile_passes;   /*   active-tile seeding, label init,           */
+    int64_t linit_tile_passes;  /*   emit (+ warm-start advance)                */
+    int64_t emit_tile_passes;
 } pmf_stats;
 
 /* Create / destroy a solver bound to one CUDA device and its own stream. */
@@ -175,6 +183,11 @@ int pmf_seed_fetch(pmf_solver *s, uint8_t *swapped_out, int64_t *flows_out, uint
  * the number returned. */
 int pmf_debug_trace(pmf_solver *s, int32_t *kind, double *us, double *start_us, int64_t *tiles,
                     int32_t *n);
+
+/* Diagnostics: CTA-busy milliseconds of the last asynchronous run, summed
+ * over CTAs: per phase kind (BINIT, BFS, SEED, PUSH, LINIT, LAB, EMIT, -),
+ * queue wait, hand-off, grid transitions; out16 holds 16 doubles. */
+int pmf_debug_busy(pmf_solver *s, double *out16);
 
 /* Diagnostics: copy the tile-major device state of the last run (w, h,
  * residual words, source-side flags; any pointer may be NULL) and the tile

@@ -24,7 +24,7 @@ SWAP_MODES = {"auto": 0, "on": 1, "off": 2}
 EXPORTS = ("pmf_solver_create", "pmf_solver_destroy", "pmf_solver_set", "pmf_last_error",
            "pmf_solver_stats", "pmf_solver_stream", "pmf_solve_composites", "pmf_solve_seed_batch",
            "pmf_seed_stage", "pmf_seed_run", "pmf_seed_fetch", "pmf_debug_state",
-           "pmf_debug_trace")
+           "pmf_debug_trace", "pmf_debug_busy")
 
 
 class NativeUnavailable(RuntimeError):
@@ -39,7 +39,10 @@ class PmfStats(ctypes.Structure):
         (k, ctypes.c_double) for k in ("ms_total", "ms_build", "ms_push", "ms_bfs", "ms_labels",
                                        "ms_seed", "ms_h2d", "ms_d2h", "ms_device")] + [
         (k, ctypes.c_int64) for k in ("launches", "h2d_bytes", "d2h_bytes", "graph_builds",
-                                       "kernels", "steps")]
+                                       "kernels", "steps", "scan_tile_passes")] + [
+        ("ms_async", ctypes.c_double), ("async_mode", ctypes.c_int32), ("reserved", ctypes.c_int32)] + [
+        (k, ctypes.c_int64) for k in ("binit_tile_passes", "seed_tile_passes", "linit_tile_passes",
+                                       "emit_tile_passes")]
 
     def as_dict(self):
         return {k: getattr(self, k) for k, _ in self._fields_}
@@ -81,6 +84,7 @@ def load_library(path: str = LIB_PATH):
         lib.pmf_solver_stream.argtypes = [vp, P(vp)]
         lib.pmf_debug_state.argtypes = [vp, vp, vp, vp, vp, P(i64)]
         lib.pmf_debug_trace.argtypes = [vp, vp, vp, vp, vp, P(i32)]
+        lib.pmf_debug_busy.argtypes = [vp, P(ctypes.c_double)]
         for name in EXPORTS:
             if name != "pmf_last_error":
                 getattr(lib, name).restype = ctypes.c_int
@@ -203,6 +207,13 @@ class Solver:
                                   tiles.ctypes.data, ctypes.byref(n))
         return [(int(kind[i]), round(float(us[i]), 1), int(tiles[i]), round(float(t0[i]), 1))
                 for i in range(n.value)]
+
+    def busy(self):
+        """Async runs: CTA-busy ms per phase kind, summed over CTAs."""
+        out = np.zeros(16, np.float64)
+        self._lib.pmf_debug_busy(self._h, out.ctypes.data_as(ctypes.POINTER(ctypes.c_double)))
+        names = ("binit", "bfs", "seed", "push", "linit", "lab", "emit", "-", "wait", "handoff", "transition")
+        return {k: round(float(v), 2) for k, v in zip(names, out) if k != "-"}
 
     def stream_handle(self) -> int:
         """The solver's cudaStream_t as an integer (torch.cuda.ExternalStream)."""

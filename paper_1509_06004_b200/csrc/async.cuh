@@ -1,0 +1,478 @@
+// async.cuh -- one persistent kernel solves a whole seed batch.
+//
+// Every grid (a warm-start chain of lambda-graphs, or one cold lambda-graph)
+// walks its own phase machine
+//
+//   BINIT -> BFS -> SEED -+-> PUSH -> BINIT ...           (next relabel cycle)
+//                         +-> LINIT -> LAB -> EMIT -+-> BFS  (next lambda; EMIT ran its BINIT)
+//                                                   +-> done
+//
+// and the tiles of all grids share one work queue (engine.cuh q_*): a CTA
+// pops a tile, runs the body of its grid's current phase, requests the
+// neighbours it touched, and the CTA that retires the last tile of a grid's
+// phase performs that grid's transition (decides the next phase, enqueues
+// its tiles).  No grid ever waits for another one at a phase boundary, so
+// the latency-bound tails of one grid overlap the dense work of the others.
+//
+// Phase bodies (one CTA of 1024 threads, one 32x32 tile):
+//   BINIT  h = 1 on sink-residual pixels, HINF elsewhere; flag BFS seeds   (k_gr_init)
+//   BFS    exact distance to the sink, tile-local fixpoint                 (bfs_sink_tile)
+//   SEED   count active pixels (w > 0, h < HINF); flag active tiles       (k_seed_push)
+//   PUSH   discharge under a per-grid pop budget                           (push_tile)
+//   LINIT  lab = (w > 0); flag label seeds                                 (k_lab_seed)
+//   LAB    residual closure of the excess pixels                           (bfs_src_tile)
+//   EMIT   label bytes, unused sink residual, warm-start advance of w      (k_emit, k_advance_tiles)
+// The reference semantics of each body are documented at the kernels named.
+#pragma once
+#include "kernels.cuh"
+#include "tile.cuh"
+
+namespace pmf {
+
+enum { PH_BINIT = 0, PH_BFS, PH_SEED, PH_PUSH, PH_LINIT, PH_LAB, PH_EMIT, PH_DONE };
+// scan phases (BINIT, SEED, LINIT, EMIT) run as tasks of SCAN_GROUP
+// consecutive tiles, queued by their first tile
+constexpr int SCAN_GROUP = 8;
+__host__ __device__ constexpr bool scan_phase(int ph) {
+    return ph == PH_BINIT || ph == PH_SEED || ph == PH_LINIT || ph == PH_EMIT;
+}
+// extra pass counters (Ctx::stat) of the scan phases
+enum { ST_BINIT = 9, ST_SEED = 10, ST_LINIT = 11, ST_EMIT = 12, ST_LAMS = 13, ST_ASYNC_NS = 14 };
+// CTA-busy nanoseconds per phase kind (ST_BUSY + PH_*), then queue wait,
+// hand-off (requests + retire) and grid transitions
+constexpr int ST_BUSY = 16;
+enum { BUSY_WAIT = 8, BUSY_FOLLOW = 9, BUSY_TRANS = 10, BUSY_N = 11 };
+
+struct GridRun {
+    int32_t phase;
+    int32_t pops;      // discharge tile passes in the current PUSH phase
+    int32_t budget;    // ... and their cap
+    int32_t act;       // active pixels found by the current SEED phase
+    int32_t cut;       // the current PUSH phase hit its budget
+    int32_t cycles;    // relabel cycles of the current lambda
+    int64_t drain;     // unused sink residual (EMIT)
+};
+
+struct AsyncArgs {
+    SeedArgs sa;
+    const int64_t *slope_sum;
+    GridRun *gr;
+    uint8_t *tflag;    // per tile: listed for the next flagged phase
+    int iters, relabel_every, relax_cap;
+    unsigned budget_factor;
+    int32_t max_cycles;
+    int32_t cont;      // continuation hand-off between neighbouring tiles
+};
+
+// ---- scan phases: one task = up to SCAN_GROUP consecutive tiles of a grid,
+// all processed at once (SCAN_GROUP pixels per thread, loads issued
+// together), with per-tile flags / counts gathered in shared memory.
+struct ScanShared {
+    int any[SCAN_GROUP];     // tile has a flagged pixel / active-pixel count
+    int sides[SCAN_GROUP];   // border sides of flagged pixels
+};
+__shared__ ScanShared s_scan;
+
+__device__ __forceinline__ void scan_reset() {
+    if (threadIdx.x < SCAN_GROUP) s_scan.any[threadIdx.x] = 0, s_scan.sides[threadIdx.x] = 0;
+    __syncthreads();
+}
+
+// thread k < ntl: flag tile t0 + k for the next flagged phase when it holds a
+// flagged pixel, plus each neighbour facing a flagged border pixel (a seed
+// never changes, so the tile alone would never hand it across the border;
+// seed_with_halo() of the worklist kernels)
+__device__ __forceinline__ void scan_flag(const Ctx &c, const AsyncArgs &A, int32_t t0, int ntl) {
+    __syncthreads();
+    const int k = threadIdx.x;
+    if (k < ntl && s_scan.any[k]) {
+        const int32_t t = t0 + k;
+        A.tflag[t] = 1;
+        for (int s = 0; s < 4; s++)
+            if ((s_scan.sides[k] >> s) & 1) {
+                const int32_t nb = tile_nb(c, t, s);
+                if (nb >= 0) A.tflag[nb] = 1;
+            }
+    }
+}
+
+// per-pixel flag contribution of pixel i of tile k (warp-aggregated)
+__device__ __forceinline__ void scan_mark(int k, int flagged) {
+    const int i = threadIdx.x;
+    const unsigned b = __ballot_sync(0xffffffffu, flagged);
+    if (!b) return;
+    const int sides = flagged ? border_sides(i & 31, i >> 5) : 0;
+    const int orr = __reduce_or_sync(0xffffffffu, sides);
+    if ((i & 31) == 0) {
+        atomicOr(&s_scan.any[k], 1);
+        if (orr) atomicOr(&s_scan.sides[k], orr);
+    }
+}
+
+// BINIT (k_gr_init): h = 1 on sink-residual pixels, HINF elsewhere
+__device__ __forceinline__ void binit_group(const Ctx &c, const AsyncArgs &A, int32_t t0, int ntl) {
+    const int i = threadIdx.x;
+    scan_reset();
+    int32_t wv[SCAN_GROUP];
+#pragma unroll
+    for (int k = 0; k < SCAN_GROUP; k++) wv[k] = k < ntl ? __ldcg(c.w + int64_t(t0 + k) * TPIX + i) : 0;
+#pragma unroll
+    for (int k = 0; k < SCAN_GROUP; k++)
+        if (k < ntl) {
+            c.h[int64_t(t0 + k) * TPIX + i] = wv[k] < 0 ? 1 : HINF;
+            scan_mark(k, wv[k] < 0);
+        }
+    scan_flag(c, A, t0, ntl);
+}
+
+// SEED (k_seed_push): count active pixels (w > 0, h < HINF) per tile
+__device__ __forceinline__ void seed_group(const Ctx &c, const AsyncArgs &A, int32_t t0, int ntl, int32_t g) {
+    const int i = threadIdx.x;
+    scan_reset();
+    int a[SCAN_GROUP];
+#pragma unroll
+    for (int k = 0; k < SCAN_GROUP; k++) {
+        const int64_t p = int64_t(t0 + k) * TPIX + i;
+        a[k] = k < ntl && __ldcg(c.w + p) > 0 && __ldcg(c.h + p) < HINF;
+    }
+#pragma unroll
+    for (int k = 0; k < SCAN_GROUP; k++) {
+        const int v = __reduce_add_sync(0xffffffffu, a[k]);
+        if ((i & 31) == 0 && v) atomicAdd(&s_scan.any[k], v);
+    }
+    __syncthreads();
+    if (i < ntl && s_scan.any[i]) {
+        atomicAdd(&A.gr[g].act, s_scan.any[i]);
+        A.tflag[t0 + i] = 1;
+    }
+}
+
+// LINIT (k_lab_seed): lab = (w > 0), label BFS seeds (swapped grids report
+// the sink side and run no label BFS: nothing to flag)
+__device__ __forceinline__ void linit_group(const Ctx &c, const AsyncArgs &A, int32_t t0, int ntl, bool swapped) {
+    const int i = threadIdx.x;
+    scan_reset();
+    int v[SCAN_GROUP];
+#pragma unroll
+    for (int k = 0; k < SCAN_GROUP; k++) v[k] = k < ntl && __ldcg(c.w + int64_t(t0 + k) * TPIX + i) > 0;
+#pragma unroll
+    for (int k = 0; k < SCAN_GROUP; k++)
+        if (k < ntl) {
+            c.lab[int64_t(t0 + k) * TPIX + i] = uint8_t(v[k]);
+            if (!swapped) scan_mark(k, v[k]);
+        }
+    if (!swapped) scan_flag(c, A, t0, ntl);
+}
+
+// EMIT (k_emit + k_advance_tiles): label bytes (swapped grids: sink side
+// {h < HINF} of the final exact relabel; else the source-side closure),
+// unused sink residual, and -- when the chain has a next lambda -- the
+// warm-start advance of w followed by that lambda's BINIT
+__device__ __forceinline__ void emit_group(const Ctx &c, const AsyncArgs &A, int32_t t0, int ntl, int32_t g) {
+    __shared__ int64_t red[NTT / 32];
+    const SeedArgs &a = A.sa;
+    const GridDesc &gd = c.grids[g];
+    const int i = threadIdx.x;
+    const int cur = __ldcg(c.cur_lam + g);   // advanced by other CTAs' transitions
+    const bool next = cur + 1 < gd.lam_end;
+    const bool swapped = grid_swapped(c, gd);
+    const int64_t n = int64_t(gd.W) * gd.H;
+    const int64_t dl = next ? a.lambdas[cur + 1] - a.lambdas[cur] : 0;
+    const int sign = c.swapflag[gd.prob] ? -1 : 1;
+    uint8_t *out = c.out + (int64_t(gd.prob) * c.nlam + cur) * n;
+    const uint8_t *mask = a.mask + int64_t(gd.prob) * n;
+    const int32_t *slope = a.slope + a.plane_off[gd.prob];
+    if (next) scan_reset();
+    int64_t drain = 0;
+    const int32_t l0 = int32_t(t0 - gd.tile_base);
+#pragma unroll 2
+    for (int k = 0; k < SCAN_GROUP; k++) {
+        if (k >= ntl) break;
+        const int32_t l = l0 + k;
+        const int x = (l % gd.ntx) * TW + (i & 31), y = (l / gd.ntx) * TH + (i >> 5);
+        const int64_t p = int64_t(t0 + k) * TPIX + i;
+        int32_t wv = __ldcg(c.w + p);
+        if (x < gd.W && y < gd.H) {
+            if (wv < 0) drain -= wv;
+            const int64_t q = int64_t(y) * gd.W + x;
+            out[q] = swapped ? uint8_t(__ldcg(c.h + p) < HINF) : __ldcg(c.lab + p);
+            if (next && mask[q] != 1) {   // fg seed: CAP_MAX either way
+                wv += int32_t(sign * dl * int64_t(slope[q]));
+                c.w[p] = wv;
+            }
+        }
+        if (next) {   // the next lambda's BINIT, fused
+            c.h[p] = wv < 0 ? 1 : HINF;
+            scan_mark(k, wv < 0);
+        }
+    }
+    const int64_t s = block_sum64(drain, red);
+    if (i == 0 && s) atomicAdd((unsigned long long *)&A.gr[g].drain, (unsigned long long)s);
+    if (next) scan_flag(c, A, t0, ntl);
+}
+
+// Whole CTA, after the last tile of grid g's phase `ph` retired (nothing of
+// g is queued or running): pick the next phase and enqueue its tiles.  A
+// flagged phase with no flagged tile is empty and falls through at once.
+// The phase (and a discharge's budget) is published before any of its tiles
+// is queued; poppers read it after their pop (fences on both sides).
+__device__ void grid_transition(const Ctx &c, const AsyncArgs &A, int32_t g, int ph) {
+    __shared__ int s_next, s_cnt;
+    const GridDesc &gd = c.grids[g];
+    GridRun &R = A.gr[g];
+    const int64_t t0 = gd.tile_base;
+    const int32_t nt = gd.ntx * gd.nty;
+    for (;;) {
+        if (threadIdx.x == 0) {
+            int next = PH_DONE;
+            const bool swapped = grid_swapped(c, gd);
+            switch (ph) {
+            case PH_BINIT: next = PH_BFS; break;
+            case PH_BFS:
+                R.act = 0;
+                next = PH_SEED;
+                break;
+            case PH_SEED:
+                if (__ldcg(&R.act) == 0) {
+                    next = PH_LINIT;
+                } else if ((R.cycles = __ldcg(&R.cycles) + 1) > A.max_cycles) {
+                    c.ctl->noconv = 1;
+                } else {
+                    next = PH_PUSH;
+                    R.pops = 0;
+                    R.cut = 0;
+                    atomicAdd(&c.ctl->cycles_total, 1);
+                }
+                break;
+            case PH_PUSH:
+                // even a drained discharge needs a confirming exact relabel:
+                // the lock-free rule h(p) > h(q) against a halo height read at
+                // pass start can push into a pixel frozen meanwhile, giving it
+                // a residual path out, so HINF marks alone certify nothing
+                next = PH_BINIT;
+                break;
+            case PH_LINIT: next = swapped ? PH_EMIT : PH_LAB; break;
+            case PH_LAB: next = PH_EMIT; break;
+            case PH_EMIT: {
+                const int cur = __ldcg(c.cur_lam + g);
+                const int64_t snk = int64_t(__ldcg((const unsigned long long *)(c.snk_sum + g)));
+                c.flows[int64_t(gd.prob) * c.nlam + cur] =
+                    snk - int64_t(__ldcg((const unsigned long long *)&R.drain));
+                R.drain = 0;
+                atomicAdd(&c.stat[ST_LAMS], 1ull);
+                if (cur + 1 < gd.lam_end) {
+                    if (swapped)
+                        c.snk_sum[g] = snk + (A.sa.lambdas[cur + 1] - A.sa.lambdas[cur]) * A.slope_sum[gd.prob];
+                    c.cur_lam[g] = cur + 1;
+                    R.cycles = 0;
+                    next = PH_BFS;   // EMIT ran the next lambda's BINIT
+                }
+                break;
+            }
+            default: break;
+            }
+            s_next = next;
+            s_cnt = 0;
+        }
+        __syncthreads();
+        const int next = s_next;
+        if (next == PH_DONE) {
+            if (threadIdx.x == 0) {
+                R.phase = PH_DONE;
+                __threadfence();
+            }
+            __syncthreads();
+            return;
+        }
+        const bool all = scan_phase(next);
+        // count the tasks the phase will run
+        int mine = 0;
+        for (int32_t j = threadIdx.x; j < nt; j += blockDim.x)
+            mine += all ? j % SCAN_GROUP == 0 : __ldcg(&A.tflag[t0 + j]) != 0;
+        if (mine) atomicAdd(&s_cnt, mine);
+        __syncthreads();
+        const int cnt = s_cnt;
+        if (cnt == 0) {   // empty flagged phase: go on to the one after it
+            ph = next;
+            __syncthreads();
+            continue;
+        }
+        if (threadIdx.x == 0) {
+            if (next == PH_PUSH)   // pop budget: factor x seeded tiles (k_cycle_ctl)
+                R.budget = A.budget_factor ? int32_t(A.budget_factor) * cnt + 64 : 0x7fffffff;
+            R.phase = next;
+            // hold the phase open while its tiles are being queued: a tile
+            // popped and retired meanwhile must not see the count reach zero
+            atomicAdd(&c.gpend[g], 1);
+            __threadfence();
+        }
+        __syncthreads();
+        __threadfence();
+        for (int32_t j = threadIdx.x; j < nt; j += blockDim.x) {
+            const int32_t t = int32_t(t0 + j);
+            bool go = all && j % SCAN_GROUP == 0;
+            if (!all && __ldcg(&A.tflag[t])) {
+                A.tflag[t] = 0;
+                go = true;
+            }
+            if (go) q_request(c, t);
+        }
+        __threadfence();
+        __syncthreads();
+        if (threadIdx.x == 0) s_next = atomicSub(&c.gpend[g], 1) == 1;
+        __syncthreads();
+        if (!s_next) return;
+        ph = next;   // every tile of the new phase already finished: next transition
+        __syncthreads();
+    }
+}
+
+// Retire (or requeue) the running tile t.  Returns 0: requeued, 1: retired,
+// 2: retired as the last queued/running tile of its grid's phase.  The
+// global pending count is left to the caller (it drops after a transition
+// has queued the next phase, so it never touches zero in between).
+__device__ __forceinline__ int aq_finish(const Ctx &c, int32_t t, bool again) {
+    for (;;) {
+        if (again) {
+            atomicExch(&c.qstate[t], Q_QUEUED);
+            q_push(c, t);
+            return 0;
+        }
+        if (atomicCAS(&c.qstate[t], Q_RUNNING, Q_IDLE) == Q_RUNNING)
+            return atomicSub(&c.gpend[c.tile_grid[t]], 1) == 1 ? 2 : 1;
+        again = true;   // dirtied while running
+    }
+}
+
+template <class E>
+__global__ void __launch_bounds__(NTT, 2) k_async(Ctx c, AsyncArgs A) {
+    __shared__ int32_t s_t, s_cont;
+    __shared__ int s_fin, s_ok;
+    const int i = threadIdx.x;
+    push_prepare();
+    if (i == 0) {
+        s_cont = -1;
+        atomicMin(&c.ctl->t0, gtimer());
+    }
+    for (;;) {
+        if (i == 0) {
+            const unsigned long long tw = gtimer();
+            int32_t t = s_cont;
+            s_cont = -1;
+            if (t < 0) t = q_next(c);
+            __threadfence();
+            s_t = t;
+            atomicAdd(&c.stat[ST_BUSY + BUSY_WAIT], gtimer() - tw);
+        }
+        __syncthreads();
+        const int32_t t = s_t;
+        if (t < 0) break;
+        __threadfence();   // popper side: state write < data reads
+        const unsigned long long tb = i == 0 ? gtimer() : 0ull;
+        const int32_t g = __ldg(c.tile_grid + t);
+        const int ph = __ldcg(&A.gr[g].phase);
+        TileResult r{0, 0};
+        int stat = -1, npass = 1;
+        if (scan_phase(ph)) {
+            const GridDesc &gd = c.grids[g];
+            const int ntl = int(min(int64_t(SCAN_GROUP), gd.tile_base + int64_t(gd.ntx) * gd.nty - t));
+            switch (ph) {
+            case PH_BINIT: binit_group(c, A, t, ntl); break;
+            case PH_SEED: seed_group(c, A, t, ntl, g); break;
+            case PH_LINIT: linit_group(c, A, t, ntl, grid_swapped(c, gd)); break;
+            default: emit_group(c, A, t, ntl, g); break;
+            }
+            stat = ph == PH_BINIT ? ST_BINIT : ph == PH_SEED ? ST_SEED : ph == PH_LINIT ? ST_LINIT : ST_EMIT;
+            npass = ntl;
+        } else if (ph == PH_BFS) {
+            r = bfs_sink_tile<E>(c, t);
+            stat = ST_BFS;
+        } else if (ph == PH_PUSH) {
+            if (i == 0) {
+                s_ok = atomicAdd(&A.gr[g].pops, 1) < __ldcg(&A.gr[g].budget);
+                if (!s_ok) A.gr[g].cut = 1;   // budget spent: relabel before more discharge
+            }
+            __syncthreads();
+            if (s_ok) {
+                r = push_tile<E>(c, t, A.iters, A.relabel_every, A.relax_cap);
+                stat = ST_PUSH;
+            }
+        } else if (ph == PH_LAB) {
+            r = bfs_src_tile<E>(c, t);
+            stat = ST_LAB;
+        }
+        const unsigned long long tf = i == 0 ? gtimer() : 0ull;
+        if (i == 0) atomicAdd(&c.stat[ST_BUSY + ph], tf - tb);
+        __threadfence();   // requester side: data writes < queue-state reads
+        __syncthreads();
+        if (i < 32) {
+            // neighbours this pass touched (same phase); the lowest one is
+            // taken over directly when the tile itself is done
+            const unsigned flags = unsigned(r.out) & 15u;
+            const int want = (A.cont && !r.again && flags) ? __ffs(flags) : 0;
+            if (i >= 1 && i <= 4 && ((flags >> (i - 1)) & 1)) {
+                __threadfence();
+                const int32_t nb = tile_nb(c, t, i - 1);
+                if (nb >= 0) {
+                    if (i == want && q_claim(c, nb)) s_cont = nb;
+                    else q_request(c, nb);
+                }
+                __threadfence();
+            }
+            __syncwarp();
+            if (i == 0) {
+                __threadfence();
+                s_fin = aq_finish(c, t, r.again != 0);
+                if (stat >= 0) atomicAdd(&c.stat[stat], (unsigned long long)npass);
+            }
+        }
+        __syncthreads();
+        const int fin = s_fin;
+        const unsigned long long tt = i == 0 ? gtimer() : 0ull;
+        if (i == 0) atomicAdd(&c.stat[ST_BUSY + BUSY_FOLLOW], tt - tf);
+        if (fin == 2) {
+            __threadfence();
+            grid_transition(c, A, g, ph);
+            if (i == 0) atomicAdd(&c.stat[ST_BUSY + BUSY_TRANS], gtimer() - tt);
+        }
+        if (i == 0 && fin) {
+            __threadfence();
+            atomicSub(&c.qctr[QC_PENDING], 1u);
+        }
+    }
+    if (i == 0) {
+        atomicMax(&c.ctl->t1, gtimer());
+        __threadfence();
+        if (atomicAdd(&c.ctl->done, 1u) == gridDim.x - 1) {
+            __threadfence();
+            const unsigned long long t0 = *(volatile unsigned long long *)&c.ctl->t0;
+            const unsigned long long t1 = *(volatile unsigned long long *)&c.ctl->t1;
+            c.stat[ST_ASYNC_NS] = t1 > t0 ? t1 - t0 : 0ull;
+        }
+    }
+}
+
+// Start of an asynchronous batch (after k_phase_begin reset the queue):
+// every grid in BINIT with all its tiles queued.
+__global__ void k_async_begin(Ctx c, AsyncArgs A, int32_t ngrids) {
+    const int64_t tid = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
+    const int64_t stride = int64_t(gridDim.x) * blockDim.x;
+    for (int64_t g = tid; g < ngrids; g += stride) {
+        GridRun &R = A.gr[g];
+        R.phase = PH_BINIT;
+        R.pops = R.budget = R.act = R.cut = R.cycles = 0;
+        R.drain = 0;
+    }
+    for (int64_t t = tid; t < c.ntiles; t += stride) A.tflag[t] = 0;
+}
+
+__global__ void k_async_queue_all(Ctx c) {
+    const int64_t tid = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
+    const int64_t stride = int64_t(gridDim.x) * blockDim.x;
+    for (int64_t t = tid; t < c.ntiles; t += stride) {
+        const GridDesc &gd = c.grids[c.tile_grid[t]];
+        if ((t - gd.tile_base) % SCAN_GROUP == 0) q_request(c, int32_t(t));   // BINIT task leaders
+    }
+}
+
+}  // namespace pmf

@@ -24,6 +24,7 @@
 #include "kernels.cuh"
 #include "tile.cuh"
 #include "warp.cuh"
+#include "async.cuh"
 
 using namespace pmf;
 
@@ -209,11 +210,17 @@ struct pmf_solver {
     int verify = 1;             // seed batches: device cut_cost == flow certificate per cut
     int rolling = 1;            // warm-start chains advance per grid as each finishes (no step barrier)
     int push_minb = 2;          // CTA discharge: min CTAs per SM of its launch bounds (1 or 2)
+    int grid_div = 1;           // use 1/grid_div of the GPU's resident CTAs (solvers sharing a GPU)
+    int async_mode = -1;        // seed batches: one persistent kernel, every grid on its own phase machine
+                                // (1), step-synchronous phases (0), or -1: async up to async_max_tiles tiles
+    int async_max_tiles = 12000;
+    int async_cont = 1;
+    double busy_ms[16] = {0};    // async: CTA-busy time per phase kind of the last run (diagnostics)
     int bfs_chunk = 8;
     int timing = 0;
     int64_t max_cycles = 50000;
     // device workspace
-    DevBuf d_w, d_h, d_r, d_lab, d_tile_grid, d_tnb, d_fin, d_gpend, d_grids, d_live, d_act, d_list, d_inq, d_cnt,
+    DevBuf d_w, d_h, d_r, d_lab, d_tile_grid, d_tnb, d_fin, d_gpend, d_gr, d_tflag, d_vacc, d_grids, d_live, d_act, d_list, d_inq, d_cnt,
         d_snk, d_drain, d_err, d_stat, d_colswap, d_out, d_bits, d_in32, d_pw, d_mask, d_off, d_lam,
         d_swapcnt, d_swapflag, d_ring, d_qstate, d_qctr, d_ctl, d_curlam, d_flows, d_slopesum;
     HostBuf h_in32, h_pw, h_mask, h_out, h_small;
@@ -746,7 +753,6 @@ int build_graph_rolling(pmf_solver *s, const Ctx &c0, int32_t ngrids, const Seed
                          int64_t(s->max_cycles), h_cycle, 1, h_lab, 1)))
         return rc;
     if ((rc = add_push_node<E>(s, cyc, &q, P.pq, K_PERSISTENT, lctl(ST_PUSH)))) return rc;
-    if ((rc = add_kernel(cyc, &q, dim3(1), dim3(1024), k_push_done, P.base, ngrids, h_cycle, 1, h_lab, 1))) return rc;
     // finished grids: labels, flow, next lambda
     cudaGraph_t lab;
     if ((rc = add_if(cyc, &q, h_lab, &lab))) return rc;
@@ -846,7 +852,6 @@ int host_solve_rolling(pmf_solver *s, const Ctx &c0, int32_t ngrids, const SeedA
         if (ctl.nact) {
             s->tmark(C_PUSH);
             launch_push<E>(s, P.pq, K_PERSISTENT);
-            LAUNCH(s, (k_push_done<<<1, 1024, 0, s->st>>>(c0, ngrids, 0, 0, 0, 0)));
             CK(cudaGetLastError());
             if ((rc = read_ctl(s, c0, &ctl))) return rc;
         }
@@ -912,13 +917,20 @@ int run_end(pmf_solver *s) {
     CK(cudaMemcpyAsync(&ctl, s->d_ctl.p, sizeof ctl, cudaMemcpyDeviceToHost, s->st));
     CK(cudaStreamSynchronize(s->st));
     const Layout &L = s->lay;
+    s->stats.scan_tile_passes = int64_t(st[ST_BINIT] + st[ST_SEED] + st[ST_LINIT] + st[ST_EMIT]);
+    s->stats.binit_tile_passes = int64_t(st[ST_BINIT]);
+    s->stats.seed_tile_passes = int64_t(st[ST_SEED]);
+    s->stats.linit_tile_passes = int64_t(st[ST_LINIT]);
+    s->stats.emit_tile_passes = int64_t(st[ST_EMIT]);
+    s->stats.ms_async = double(st[ST_ASYNC_NS]) * 1e-6;
+    for (int k = 0; k < BUSY_N; k++) s->busy_ms[k] = double(st[ST_BUSY + k]) * 1e-6;
     s->stats.push_tile_passes = int64_t(st[ST_PUSH]);
     s->stats.bfs_tile_passes = int64_t(st[ST_BFS]);
     s->stats.label_tile_passes = int64_t(st[ST_LAB]);
     s->stats.push_sweeps = int64_t(st[ST_PUSH_L]);
     s->stats.bfs_sweeps = int64_t(st[ST_BFS_L] + st[ST_LAB_L]);
     s->stats.cycles = ctl.cycles_total;
-    s->stats.steps = std::max(1, ctl.steps);
+    s->stats.steps = s->stats.async_mode ? int64_t(st[ST_LAMS]) : std::max(1, ctl.steps);
     // kernels executed on the device: the counted tile-kernel launches plus
     // the fixed per-cycle kernels (2 x phase_begin, gr_init, seed_push,
     // cycle_ctl), the label tail (phase_begin, lab_seed, emit) and the
@@ -1004,12 +1016,65 @@ int grids_for(pmf_solver *s) {
     CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ2, k_wbfs_src<E>, WPB * 32, s->smem_w));
     s->grid_wbfs = std::max(1, std::min(occ, occ2)) * s->sms;
     s->grid_full = 8 * s->sms;
+    if (s->grid_div > 1) {   // a share of the GPU (several solvers running side by side)
+        for (int *gp : {&s->grid_push, &s->grid_bfs, &s->grid_full, &s->grid_wpush, &s->grid_wbfs})
+            *gp = std::max(1, *gp / s->grid_div);
+    }
     return 0;
 }
 
 // --------------------------------------------------------------------------
 // seed batches: stage (host convert + H2D) / run (device only) / fetch (D2H)
 // --------------------------------------------------------------------------
+
+// Integrity certificate of a seed batch (k_verify): cut cost of every
+// emitted mask on the original graph == its flow
+int launch_verify(pmf_solver *s, const Ctx &c, const SeedArgs &a) {
+    const int64_t planes = int64_t(a.nprob) * a.nlam, n = int64_t(a.W) * a.H;
+    const int chunks = int(std::max<int64_t>(1, std::min<int64_t>(cdiv(n, 16384), 1024)));
+    int rc;
+    if ((rc = s->d_vacc.ensure(size_t(planes) * 8))) return rc;
+    CK(cudaMemsetAsync(s->d_vacc.p, 0, size_t(planes) * 8, s->st));
+    unsigned long long *acc = s->d_vacc.as<unsigned long long>();
+    LAUNCH(s, (k_verify<<<int(std::min<int64_t>(planes * chunks, 32 * s->sms)), NT, 0, s->st>>>(c, a, acc, chunks)));
+    LAUNCH(s, (k_verify_check<<<int(std::max<int64_t>(1, std::min<int64_t>(cdiv(planes, 256), 1024))), 256, 0, s->st>>>(
+                   c, planes, acc)));
+    CK(cudaGetLastError());
+    return 0;
+}
+
+// Asynchronous seed batch (async.cuh): queue reset, every grid in BINIT with
+// all its tiles queued, then one persistent launch runs every phase of
+// every grid.
+template <class E>
+int async_solve(pmf_solver *s, const Ctx &c0, const SeedArgs &sa) {
+    const int64_t G = int64_t(s->lay.grids.size()), T = s->lay.ntiles;
+    int rc;
+    if ((rc = s->d_gr.ensure(size_t(G) * sizeof(GridRun))) || (rc = s->d_tflag.ensure(size_t(T)))) return rc;
+    Ctx c = c0;
+    c.persistent = 1;
+    c.budget = 0;       // no global pop budget: discharges are capped per grid
+    c.budget_dev = 0;
+    AsyncArgs A{};
+    A.sa = sa;
+    A.slope_sum = s->d_slopesum.as<int64_t>();
+    A.gr = s->d_gr.as<GridRun>();
+    A.tflag = s->d_tflag.as<uint8_t>();
+    A.iters = s->push_iters;
+    A.relabel_every = s->relabel_every;
+    A.relax_cap = s->relax_cap;
+    A.budget_factor = unsigned(budget_factor(s));
+    A.max_cycles = int32_t(std::min<int64_t>(s->max_cycles, 0x7fffffff));
+    A.cont = s->async_cont;
+    CK(cudaMemsetAsync(c.ctl, 0, sizeof(Ctl), s->st));
+    LAUNCH(s, (k_phase_begin<<<s->grid_full, 256, 0, s->st>>>(c, 1, 0, 0)));
+    LAUNCH(s, (k_async_begin<<<s->grid_full, 256, 0, s->st>>>(c, A, int32_t(G))));
+    LAUNCH(s, (k_async_queue_all<<<s->grid_full, 256, 0, s->st>>>(c)));
+    LAUNCH(s, (k_async<E><<<s->grid_push, NTT, 0, s->st>>>(c, A)));
+    CK(cudaGetLastError());
+    s->stats.async_mode = 1;
+    return 0;
+}
 
 template <class E>
 int seed_run_t(pmf_solver *s) {
@@ -1049,14 +1114,22 @@ int seed_run_t(pmf_solver *s) {
     s->stats.full_passes++;
     const bool chains = S.chain > 1;
     s->warm_active = chains;
+    // asynchronous solver for latency-bound batches; large batches keep the
+    // GPU full with step-synchronous phases, whose wide scan kernels and
+    // multi-sweep relabels cost less per tile than queued tile tasks
+    const bool use_async = s->async_mode == 1 || (s->async_mode < 0 && s->lay.ntiles <= s->async_max_tiles);
+    if (use_async) {
+        if ((rc = async_solve<E>(s, c, a))) return rc;
+        if (s->verify && (rc = launch_verify(s, c, a))) return rc;
+        return 0;
+    }
     // rolling warm start needs the persistent discharge and a single-launch BFS
     s->ctx.rolling = chains && s->rolling && s->persistent && (s->bfs_multi || s->persistent_bfs);
     int rc2 = run_solve<E>(s, c, int32_t(s->lay.grids.size()), chains ? &a : nullptr,
                            chains ? s->d_slopesum.as<int64_t>() : nullptr);
     if (rc2) return rc2;
     if (s->verify) {
-        LAUNCH(s, (k_verify<<<int(std::min<int64_t>(int64_t(S.nprob) * S.nlam, 8 * s->sms)), NT, 0, s->st>>>(c, a)));
-        CK(cudaGetLastError());
+        if ((rc = launch_verify(s, c, a))) return rc;
     }
     return 0;
 }
@@ -1414,6 +1487,10 @@ int pmf_solver_set(pmf_solver *s, const char *name, int64_t v) {
     else if (k == "verify") s->verify = v != 0;
     else if (k == "rolling") s->rolling = v != 0;
     else if (k == "push_minb" && (v == 1 || v == 2)) s->push_minb = int(v);
+    else if (k == "grid_div" && v >= 1 && v <= 64) s->grid_div = int(v);
+    else if (k == "async" && v >= -1 && v <= 1) s->async_mode = int(v);
+    else if (k == "async_max_tiles" && v >= 0) s->async_max_tiles = int(std::min<int64_t>(v, 1 << 30));
+    else if (k == "async_cont") s->async_cont = v != 0;
     else if (k == "graph") s->use_graph = v != 0;
     else if (k == "persistent_bfs") s->persistent_bfs = v != 0;
     else if (k == "bfs_multi") s->bfs_multi = v != 0;
@@ -1535,6 +1612,15 @@ int pmf_solve_composites(pmf_solver *s, int32_t ncomp, const int32_t *width, con
     }
     s->stats.h2d_bytes = total_px * 6 * 4;
     s->stats.d2h_bytes = L.out_bytes + G * 16;
+    return 0;
+}
+
+// CTA-busy milliseconds of the last asynchronous run, summed over CTAs:
+// per phase kind (BINIT, BFS, SEED, PUSH, LINIT, LAB, EMIT, -), queue wait,
+// hand-off, grid transitions, then zeros.
+int pmf_debug_busy(pmf_solver *s, double *out16) {
+    if (!s || !out16) return fail(PMF_ERR_ARG, "null argument");
+    for (int k = 0; k < 16; k++) out16[k] = s->busy_ms[k];
     return 0;
 }
 

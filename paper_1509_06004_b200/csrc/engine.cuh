@@ -33,7 +33,7 @@ enum {
     ST_PUSH = 0, ST_BFS = 1, ST_LAB = 2,
     ST_PUSH_NS = 3, ST_BFS_NS = 4, ST_LAB_NS = 5,
     ST_PUSH_L = 6, ST_BFS_L = 7, ST_LAB_L = 8,
-    ST_NSTAT = 16
+    ST_NSTAT = 40
 };
 
 // sweep index convention of the list-driven tile kernels

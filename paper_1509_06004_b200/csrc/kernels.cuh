@@ -71,7 +71,7 @@ __device__ __forceinline__ int64_t block_sum64(int64_t v, int64_t *red) {
     __syncthreads();
     int64_t s = 0;
     if (threadIdx.x == 0)
-        for (int i = 0; i < NT / 32; i++) s += red[i];
+        for (int i = 0; i < int(blockDim.x >> 5); i++) s += red[i];
     __syncthreads();
     return s;
 }
@@ -306,36 +306,6 @@ __global__ void __launch_bounds__(1024) k_cycle_ctl(Ctx c, int32_t ngrids, int p
     }
 }
 
-// Rolling mode, after a discharge: a live grid none of whose tiles is still
-// queued or running has no active pixel left -- every pixel with excess is
-// frozen, and frozen heights are exact certificates (global relabel, or a
-// local relabel whose every exit was frozen) -- so its preflow is maximum
-// and it finishes now instead of after one more global relabel.  Swapped
-// grids report their sink side, which needs that exact relabel: they take
-// the regular path.
-__global__ void __launch_bounds__(1024) k_push_done(Ctx c, int32_t ngrids, cudaGraphConditionalHandle cond,
-                                                    int has_cond, cudaGraphConditionalHandle cond_lab,
-                                                    int has_lab) {
-    __shared__ int s_fin;
-    if (threadIdx.x == 0) s_fin = 0;
-    __syncthreads();
-    int nfin = 0;
-    for (int g = threadIdx.x; g < ngrids; g += blockDim.x) {
-        if (c.live[g] && c.gpend[g] == 0 && !grid_swapped(c, c.grids[g])) {
-            c.live[g] = 0;
-            c.fin[g] = 1;
-            nfin++;
-        }
-    }
-    if (nfin) atomicAdd(&s_fin, nfin);
-    __syncthreads();
-    if (threadIdx.x == 0 && s_fin && !c.ctl->noconv) {
-        c.ctl->nfin += s_fin;
-        if (has_cond) cudaGraphSetConditional(cond, 1u);
-        if (has_lab) cudaGraphSetConditional(cond_lab, 1u);
-    }
-}
-
 // ---------------------------------------------------------------------------
 // Labels: source-side closure of the excess pixels (solvers.py:144-158),
 // then per-grid label bytes and flows.
@@ -479,17 +449,22 @@ __global__ void __launch_bounds__(NT) k_advance_tiles(Ctx c, SeedArgs a) {
 // the reference checks it in split(), supergraph.py:181-186, and in the RPC
 // client, rpc.py:328-331): the cut cost of the emitted mask of the ORIGINAL
 // graph must equal the flow.  One CTA per (problem, lambda) plane.
-__global__ void __launch_bounds__(NT) k_verify(Ctx c, SeedArgs a) {
+// One CTA per (plane, chunk of pixels); partial cut costs summed per plane
+// into acc (zeroed by the caller), compared with the flows by k_verify_check.
+__global__ void __launch_bounds__(NT) k_verify(Ctx c, SeedArgs a, unsigned long long *acc, int chunks) {
     __shared__ int64_t red[NT / 32];
     const int64_t n = int64_t(a.W) * a.H;
-    for (int64_t plane = blockIdx.x; plane < int64_t(a.nprob) * a.nlam; plane += gridDim.x) {
+    const int64_t per = (n + chunks - 1) / chunks;
+    for (int64_t blk = blockIdx.x; blk < int64_t(a.nprob) * a.nlam * chunks; blk += gridDim.x) {
+        const int64_t plane = blk / chunks;
+        const int64_t lo = (blk % chunks) * per, hi = min(n, lo + per);
         const int p = int(plane / a.nlam), j = int(plane % a.nlam);
         const int64_t lam = a.lambdas[j];
         const uint8_t *lab = c.out + plane * n;
         const int64_t po = a.plane_off[p];
         const int32_t *pw = a.pw + a.pw_off[p];
         int64_t cost = 0;
-        for (int64_t q = threadIdx.x; q < n; q += NT) {
+        for (int64_t q = lo + threadIdx.x; q < hi; q += NT) {
             const uint8_t m = a.mask[int64_t(p) * n + q];
             const int x = int(q % a.W), y = int(q / a.W);
             if (lab[q]) {
@@ -504,8 +479,14 @@ __global__ void __launch_bounds__(NT) k_verify(Ctx c, SeedArgs a) {
             }
         }
         const int64_t tot = block_sum64(cost, red);
-        if (threadIdx.x == 0 && tot != c.flows[plane]) atomicExch(c.err, 5);
+        if (threadIdx.x == 0 && tot) atomicAdd(acc + plane, (unsigned long long)tot);
     }
+}
+
+__global__ void k_verify_check(Ctx c, int64_t nplanes, const unsigned long long *acc) {
+    for (int64_t plane = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; plane < nplanes;
+         plane += int64_t(gridDim.x) * blockDim.x)
+        if (int64_t(acc[plane]) != c.flows[plane]) atomicExch(c.err, 5);
 }
 
 // One CTA: advance every grid with a next lambda (cur_lam, live, embedded

@@ -327,36 +327,43 @@ __device__ __forceinline__ int border_sides(int lx, int ly) {
            (ly == TH - 1 ? 1 << DD : 0);
 }
 
+// Tile-pass scratch in shared memory, shared by the tile bodies below (one
+// body runs at a time in a CTA; kernels allocate only what they reference).
+__shared__ int32_t s_sd[TH * SP];     // tile_relax values
+__shared__ uint8_t s_sm[TPIX];        // tile_relax pull masks
+__shared__ uint8_t s_bits[TPIX];      // label BFS: own outgoing-arc bits
+__shared__ int32_t s_hv[4][TW];       // halo values per side
+__shared__ int s_side;                // sides whose neighbour needs work
+
+template <class E>
+__device__ __forceinline__ TileResult bfs_sink_tile(const Ctx &c, int32_t t) {
+    const int i = threadIdx.x, lx = i & 31, ly = i >> 5;
+    const TileNb g = tile_nbs(c, t);
+    const int64_t p = int64_t(t) * TPIX + i;
+    const int32_t h0 = __ldcg(c.h + p);
+    typename E::Word wd = E::load(c.r, p);
+    s_sd[ly * SP + lx] = h0;
+    s_sm[i] = uint8_t((E::lane(wd, 0) > 0) | ((E::lane(wd, 1) > 0) << 1) | ((E::lane(wd, 2) > 0) << 2) |
+                      ((E::lane(wd, 3) > 0) << 3));
+    if (i < 4 * TW) {
+        int s = i / TW, j = i % TW;
+        s_hv[s][j] = g.nb[s] >= 0 ? __ldcg(c.h + int64_t(g.nb[s]) * TPIX + halo_index(s, j)) : HINF;
+    }
+    if (i == 0) s_side = 0;
+    __syncthreads();
+    tile_relax(s_sd, s_sm, s_hv, 1);
+    const int32_t h1 = s_sd[ly * SP + lx];
+    if (h1 != h0) {
+        c.h[p] = h1;
+        if (int b = border_sides(lx, ly)) atomicOr(&s_side, b);
+    }
+    __syncthreads();
+    return TileResult{0, s_side};
+}
+
 template <class E>
 __global__ void __launch_bounds__(NTT, 2) k_bfs_sink(Ctx c, int k, LaunchCtl lc) {
-    __shared__ int32_t sd[TH * SP];
-    __shared__ uint8_t sm[TPIX];
-    __shared__ int32_t hv[4][TW];
-    __shared__ int s_side;
-    const int i = threadIdx.x, lx = i & 31, ly = i >> 5;
-    tile_loop(c, k, lc, [&](int32_t t) -> TileResult {
-        const TileNb g = tile_nbs(c, t);
-        const int64_t p = int64_t(t) * TPIX + i;
-        const int32_t h0 = __ldcg(c.h + p);
-        typename E::Word wd = E::load(c.r, p);
-        sd[ly * SP + lx] = h0;
-        sm[i] = uint8_t((E::lane(wd, 0) > 0) | ((E::lane(wd, 1) > 0) << 1) |
-                        ((E::lane(wd, 2) > 0) << 2) | ((E::lane(wd, 3) > 0) << 3));
-        if (i < 4 * TW) {
-            int s = i / TW, j = i % TW;
-            hv[s][j] = g.nb[s] >= 0 ? __ldcg(c.h + int64_t(g.nb[s]) * TPIX + halo_index(s, j)) : HINF;
-        }
-        if (i == 0) s_side = 0;
-        __syncthreads();
-        tile_relax(sd, sm, hv, 1);
-        const int32_t h1 = sd[ly * SP + lx];
-        if (h1 != h0) {
-            c.h[p] = h1;
-            if (int b = border_sides(lx, ly)) atomicOr(&s_side, b);
-        }
-        __syncthreads();
-        return TileResult{0, s_side};
-    });
+    tile_loop(c, k, lc, [&](int32_t t) { return bfs_sink_tile<E>(c, t); });
 }
 
 // ---------------------------------------------------------------------------
@@ -366,54 +373,52 @@ __global__ void __launch_bounds__(NTT, 2) k_bfs_sink(Ctx c, int k, LaunchCtl lc)
 // not maximal (NonMaximalFlowError).
 // ---------------------------------------------------------------------------
 template <class E>
-__global__ void __launch_bounds__(NTT, 2) k_bfs_src(Ctx c, int k, LaunchCtl lc) {
-    __shared__ int32_t sd[TH * SP];
-    __shared__ uint8_t sbits[TPIX];    // own outgoing "arc > 0" bits
-    __shared__ uint8_t sm[TPIX];       // pull mask: incoming arcs
-    __shared__ int32_t hv[4][TW];
-    __shared__ int s_side;
+__device__ __forceinline__ TileResult bfs_src_tile(const Ctx &c, int32_t t) {
     const int i = threadIdx.x, lx = i & 31, ly = i >> 5;
-    tile_loop(c, k, lc, [&](int32_t t) -> TileResult {
-        const TileNb g = tile_nbs(c, t);
-        const int64_t p = int64_t(t) * TPIX + i;
-        const uint8_t l0 = __ldcg(c.lab + p);
-        typename E::Word wd = E::load(c.r, p);
-        sd[ly * SP + lx] = l0 ? 0 : HINF;
-        sbits[i] = uint8_t((E::lane(wd, 0) > 0) | ((E::lane(wd, 1) > 0) << 1) |
-                           ((E::lane(wd, 2) > 0) << 2) | ((E::lane(wd, 3) > 0) << 3));
-        if (i < 4 * TW) {
-            int s = i / TW, j = i % TW;
-            int32_t v = HINF;
-            if (g.nb[s] >= 0 && __ldcg(c.lab + int64_t(g.nb[s]) * TPIX + halo_index(s, j))) v = 0;
-            hv[s][j] = v;
-        }
-        if (i == 0) s_side = 0;
-        __syncthreads();
-        // pull mask: bit d set when the d-neighbour has a residual arc into us
-        int mk = 0;
-        if (lx > 0) mk |= (sbits[i - 1] >> DR) & 1;
-        if (lx < TW - 1) mk |= ((sbits[i + 1] >> DL) & 1) << 1;
-        if (ly > 0) mk |= ((sbits[i - TW] >> DD) & 1) << 2;
-        if (ly < TH - 1) mk |= ((sbits[i + TW] >> DU) & 1) << 3;
-        if (lx == 0 && g.nb[DL] >= 0)
-            mk |= (E::lane(E::load(c.r, int64_t(g.nb[DL]) * TPIX + halo_index(DL, ly)), DR) > 0) << 0;
-        if (lx == TW - 1 && g.nb[DR] >= 0)
-            mk |= (E::lane(E::load(c.r, int64_t(g.nb[DR]) * TPIX + halo_index(DR, ly)), DL) > 0) << 1;
-        if (ly == 0 && g.nb[DU] >= 0)
-            mk |= (E::lane(E::load(c.r, int64_t(g.nb[DU]) * TPIX + halo_index(DU, lx)), DD) > 0) << 2;
-        if (ly == TH - 1 && g.nb[DD] >= 0)
-            mk |= (E::lane(E::load(c.r, int64_t(g.nb[DD]) * TPIX + halo_index(DD, lx)), DU) > 0) << 3;
-        sm[i] = uint8_t(mk);
-        __syncthreads();
-        tile_relax(sd, sm, hv, 0);
-        if (sd[ly * SP + lx] == 0 && !l0) {
-            c.lab[p] = 1;
-            if (__ldcg(c.w + p) < 0) atomicExch(c.err, 4);   // NonMaximalFlowError
-            if (int b = border_sides(lx, ly)) atomicOr(&s_side, b);
-        }
-        __syncthreads();
-        return TileResult{0, s_side};
-    });
+    const TileNb g = tile_nbs(c, t);
+    const int64_t p = int64_t(t) * TPIX + i;
+    const uint8_t l0 = __ldcg(c.lab + p);
+    typename E::Word wd = E::load(c.r, p);
+    s_sd[ly * SP + lx] = l0 ? 0 : HINF;
+    s_bits[i] = uint8_t((E::lane(wd, 0) > 0) | ((E::lane(wd, 1) > 0) << 1) | ((E::lane(wd, 2) > 0) << 2) |
+                        ((E::lane(wd, 3) > 0) << 3));
+    if (i < 4 * TW) {
+        int s = i / TW, j = i % TW;
+        int32_t v = HINF;
+        if (g.nb[s] >= 0 && __ldcg(c.lab + int64_t(g.nb[s]) * TPIX + halo_index(s, j))) v = 0;
+        s_hv[s][j] = v;
+    }
+    if (i == 0) s_side = 0;
+    __syncthreads();
+    // pull mask: bit d set when the d-neighbour has a residual arc into us
+    int mk = 0;
+    if (lx > 0) mk |= (s_bits[i - 1] >> DR) & 1;
+    if (lx < TW - 1) mk |= ((s_bits[i + 1] >> DL) & 1) << 1;
+    if (ly > 0) mk |= ((s_bits[i - TW] >> DD) & 1) << 2;
+    if (ly < TH - 1) mk |= ((s_bits[i + TW] >> DU) & 1) << 3;
+    if (lx == 0 && g.nb[DL] >= 0)
+        mk |= (E::lane(E::load(c.r, int64_t(g.nb[DL]) * TPIX + halo_index(DL, ly)), DR) > 0) << 0;
+    if (lx == TW - 1 && g.nb[DR] >= 0)
+        mk |= (E::lane(E::load(c.r, int64_t(g.nb[DR]) * TPIX + halo_index(DR, ly)), DL) > 0) << 1;
+    if (ly == 0 && g.nb[DU] >= 0)
+        mk |= (E::lane(E::load(c.r, int64_t(g.nb[DU]) * TPIX + halo_index(DU, lx)), DD) > 0) << 2;
+    if (ly == TH - 1 && g.nb[DD] >= 0)
+        mk |= (E::lane(E::load(c.r, int64_t(g.nb[DD]) * TPIX + halo_index(DD, lx)), DU) > 0) << 3;
+    s_sm[i] = uint8_t(mk);
+    __syncthreads();
+    tile_relax(s_sd, s_sm, s_hv, 0);
+    if (s_sd[ly * SP + lx] == 0 && !l0) {
+        c.lab[p] = 1;
+        if (__ldcg(c.w + p) < 0) atomicExch(c.err, 4);   // NonMaximalFlowError
+        if (int b = border_sides(lx, ly)) atomicOr(&s_side, b);
+    }
+    __syncthreads();
+    return TileResult{0, s_side};
+}
+
+template <class E>
+__global__ void __launch_bounds__(NTT, 2) k_bfs_src(Ctx c, int k, LaunchCtl lc) {
+    tile_loop(c, k, lc, [&](int32_t t) { return bfs_src_tile<E>(c, t); });
 }
 
 // ---------------------------------------------------------------------------
@@ -446,147 +451,153 @@ __device__ __forceinline__ int ring_index(int s, int j) {
     }
 }
 
-template <class E, int MINB>
-__global__ void __launch_bounds__(NTT, MINB) k_push(Ctx c, int k, int iters, int relabel_every, int relax_cap,
-                                                    LaunchCtl lc) {
-    __shared__ int32_t sh[RPIX];        // heights (ring: neighbour tiles)
-    __shared__ int32_t sin[4][RPIX];    // sin[d][q]: flow pushed into q by its d-neighbour
-    __shared__ int32_t sd[TH * SP];     // local relabel distances
-    __shared__ uint8_t sm[TPIX];
-    __shared__ int32_t hh[4][TW];       // halo heights for tile_relax
-    __shared__ int s_out;
-    __shared__ int s_rowin[TH + 2];     // ring-frame row received inflow this iteration
+__shared__ int32_t s_ph[RPIX];        // discharge heights (ring: neighbour tiles)
+__shared__ int32_t s_in[4][RPIX];     // s_in[d][q]: flow pushed into q by its d-neighbour
+__shared__ int s_rowin[TH + 2];       // ring-frame row received inflow this iteration
+
+// Discharge scratch invariant: inflow slots and row flags are zero at every
+// pass boundary; established once per CTA by push_prepare().
+__device__ __forceinline__ void push_prepare() {
+    for (int j = threadIdx.x; j < 4 * RPIX; j += blockDim.x) (&s_in[0][0])[j] = 0;
+    if (threadIdx.x < TH + 2) s_rowin[threadIdx.x] = 0;
+}
+
+template <class E>
+__device__ __forceinline__ TileResult push_tile(const Ctx &c, int32_t t, int iters, int relabel_every,
+                                                int relax_cap) {
     constexpr int OFF[4] = {-1, 1, -RW, RW};
     const int i = threadIdx.x, lx = i & 31, ly = i >> 5, pi = ly * SP + lx;
     const int q = (ly + 1) * RW + lx + 1;
-    // inflow slots are zero at every pass boundary (absorbed / drained)
-    for (int j = i; j < 4 * RPIX; j += NTT) (&sin[0][0])[j] = 0;
-    if (i < TH + 2) s_rowin[i] = 0;
-    tile_loop(c, k, lc, [&](int32_t t) -> TileResult {
-        const int64_t p = int64_t(t) * TPIX + i;
-        const int32_t w0 = __ldcg(c.w + p);
-        const typename E::Word rv0 = E::load(c.r, p);
-        int32_t e = w0, h = __ldcg(c.h + p);
-        int32_t r[4];
+    const int64_t p = int64_t(t) * TPIX + i;
+    const int32_t w0 = __ldcg(c.w + p);
+    const typename E::Word rv0 = E::load(c.r, p);
+    int32_t e = w0, h = __ldcg(c.h + p);
+    int32_t r[4];
 #pragma unroll
-        for (int d = 0; d < 4; d++) r[d] = E::lane(rv0, d);
-        if (i < 4 * TW) {
-            const int s = i / TW, j = i % TW;
-            const int32_t nb = tile_nb(c, t, s);
-            const int32_t v = nb >= 0 ? __ldcg(c.h + int64_t(nb) * TPIX + halo_index(s, j)) : HINF;
-            hh[s][j] = v;
-            sh[ring_index(s, j)] = v;
-        }
-        if (i == 0) s_out = 0;
-        int act = 1;
-        int until_relabel = 0;
-        for (int it = 0; it < iters; it++) {
-            if (relabel_every && until_relabel == 0) {
-                until_relabel = relabel_every;
-                // exact local relabel (frozen pixels stay frozen)
-                sd[pi] = e < 0 ? 1 : HINF;
-                sm[i] = uint8_t((r[0] > 0) | ((r[1] > 0) << 1) | ((r[2] > 0) << 2) | ((r[3] > 0) << 3));
-                __syncthreads();
-                const int conv = tile_relax(sd, sm, hh, 1, relax_cap);
-                // an unconverged relax may not freeze anyone (keep the old
-                // height where it found nothing)
-                if (h < HINF && (conv || sd[pi] < HINF)) h = sd[pi];
-                sh[q] = h;
-                act = __syncthreads_or(e > 0 && h < HINF);
-                if (!act) break;
-            } else if (it == 0) {
-                sh[q] = h;
-                act = __syncthreads_or(e > 0 && h < HINF);
-                if (!act) break;
-            }
-            until_relabel--;
-            // warp == tile row: rows without an active pixel skip the push
-            // work, rows nobody pushed into skip the merge (barriers stay)
-            const bool mine = e > 0 && h < HINF;
-            int32_t hn[4];
-            if (__any_sync(0xffffffffu, mine)) {
-#pragma unroll
-                for (int d = 0; d < 4; d++) hn[d] = sh[q + OFF[d]];
-                // ---- push downhill (heights are fixed during this phase, so
-                // an arc is never pushed both ways and every inflow slot has
-                // one writer)
-                if (mine) {
-                    int pushed = 0;
-#pragma unroll
-                    for (int d = 0; d < 4; d++) {
-                        if (e > 0 && r[d] > 0 && h > hn[d]) {
-                            const int32_t dl = min(e, r[d]);
-                            e -= dl;
-                            r[d] -= dl;
-                            sin[opp(d)][q + OFF[d]] += dl;
-                            pushed |= 1 << d;
-                        }
-                    }
-                    if (pushed & ((1 << DL) | (1 << DR))) s_rowin[ly + 1] = 1;
-                    if (pushed & (1 << DU)) s_rowin[ly] = 1;
-                    if (pushed & (1 << DD)) s_rowin[ly + 2] = 1;
-                }
-            }
+    for (int d = 0; d < 4; d++) r[d] = E::lane(rv0, d);
+    if (i < 4 * TW) {
+        const int s = i / TW, j = i % TW;
+        const int32_t nb = tile_nb(c, t, s);
+        const int32_t v = nb >= 0 ? __ldcg(c.h + int64_t(nb) * TPIX + halo_index(s, j)) : HINF;
+        s_hv[s][j] = v;
+        s_ph[ring_index(s, j)] = v;
+    }
+    if (i == 0) s_side = 0;
+    int act = 1;
+    int until_relabel = 0;
+    for (int it = 0; it < iters; it++) {
+        if (relabel_every && until_relabel == 0) {
+            until_relabel = relabel_every;
+            // exact local relabel (frozen pixels stay frozen)
+            s_sd[pi] = e < 0 ? 1 : HINF;
+            s_sm[i] = uint8_t((r[0] > 0) | ((r[1] > 0) << 1) | ((r[2] > 0) << 2) | ((r[3] > 0) << 3));
             __syncthreads();
-            // ---- absorb inflow, relabel what is still active
-            if (s_rowin[ly + 1]) {
-#pragma unroll
-                for (int d = 0; d < 4; d++) {
-                    const int32_t v = sin[d][q];
-                    if (v) {
-                        e += v;
-                        r[d] += v;
-                        sin[d][q] = 0;
-                    }
-                }
-                __syncwarp();
-                if (lx == 0) s_rowin[ly + 1] = 0;
-            }
-            if (e > 0 && h < HINF) {
-                if (!mine) {   // became active by inflow this iteration
-#pragma unroll
-                    for (int d = 0; d < 4; d++) hn[d] = sh[q + OFF[d]];
-                }
-                int32_t m = HINF;
-#pragma unroll
-                for (int d = 0; d < 4; d++)
-                    if (r[d] > 0) m = min(m, hn[d]);
-                if (m >= h) {
-                    h = m >= HINF ? HINF : m + 1;
-                    sh[q] = h;
-                }
-            }
+            const int conv = tile_relax(s_sd, s_sm, s_hv, 1, relax_cap);
+            // an unconverged relax may not freeze anyone (keep the old
+            // height where it found nothing)
+            if (h < HINF && (conv || s_sd[pi] < HINF)) h = s_sd[pi];
+            s_ph[q] = h;
+            act = __syncthreads_or(e > 0 && h < HINF);
+            if (!act) break;
+        } else if (it == 0) {
+            s_ph[q] = h;
             act = __syncthreads_or(e > 0 && h < HINF);
             if (!act) break;
         }
-        // ---- write back: interior pixels plainly, border pixels as deltas
-        // (neighbour tiles may have pushed into them meanwhile)
-        const typename E::Word rv = E::pack(r[0], r[1], r[2], r[3]);
-        if (!on_border(i)) {
-            c.w[p] = e;
-            E::store(c.r, p, rv);
-        } else {
-            if (e != w0) atomicAdd(&c.w[p], e - w0);
-            E::store_delta(c.r, p, rv, rv0);
-        }
-        c.h[p] = h;
-        if (i < 2) s_rowin[i * (TH + 1)] = 0;   // ring rows are never absorbed
-        __syncthreads();
-        if (i < 4 * TW) {
-            const int s = i / TW, j = i % TW;
-            int32_t *slot = &sin[opp(s)][ring_index(s, j)];
-            const int32_t a = *slot;
-            if (a > 0) {
-                *slot = 0;
-                const int64_t qn = int64_t(tile_nb(c, t, s)) * TPIX + halo_index(s, j);
-                atomicAdd(&c.w[qn], a);
-                E::add(c.r, qn, opp(s), a);
-                atomicOr(&s_out, 1 << s);
+        until_relabel--;
+        // warp == tile row: rows without an active pixel skip the push
+        // work, rows nobody pushed into skip the merge (barriers stay)
+        const bool mine = e > 0 && h < HINF;
+        int32_t hn[4];
+        if (__any_sync(0xffffffffu, mine)) {
+#pragma unroll
+            for (int d = 0; d < 4; d++) hn[d] = s_ph[q + OFF[d]];
+            // ---- push downhill (heights are fixed during this phase, so
+            // an arc is never pushed both ways and every inflow slot has
+            // one writer)
+            if (mine) {
+                int pushed = 0;
+#pragma unroll
+                for (int d = 0; d < 4; d++) {
+                    if (e > 0 && r[d] > 0 && h > hn[d]) {
+                        const int32_t dl = min(e, r[d]);
+                        e -= dl;
+                        r[d] -= dl;
+                        s_in[opp(d)][q + OFF[d]] += dl;
+                        pushed |= 1 << d;
+                    }
+                }
+                if (pushed & ((1 << DL) | (1 << DR))) s_rowin[ly + 1] = 1;
+                if (pushed & (1 << DU)) s_rowin[ly] = 1;
+                if (pushed & (1 << DD)) s_rowin[ly + 2] = 1;
             }
         }
         __syncthreads();
-        return TileResult{act, s_out};
-    });
+        // ---- absorb inflow, relabel what is still active
+        if (s_rowin[ly + 1]) {
+#pragma unroll
+            for (int d = 0; d < 4; d++) {
+                const int32_t v = s_in[d][q];
+                if (v) {
+                    e += v;
+                    r[d] += v;
+                    s_in[d][q] = 0;
+                }
+            }
+            __syncwarp();
+            if (lx == 0) s_rowin[ly + 1] = 0;
+        }
+        if (e > 0 && h < HINF) {
+            if (!mine) {   // became active by inflow this iteration
+#pragma unroll
+                for (int d = 0; d < 4; d++) hn[d] = s_ph[q + OFF[d]];
+            }
+            int32_t m = HINF;
+#pragma unroll
+            for (int d = 0; d < 4; d++)
+                if (r[d] > 0) m = min(m, hn[d]);
+            if (m >= h) {
+                h = m >= HINF ? HINF : m + 1;
+                s_ph[q] = h;
+            }
+        }
+        act = __syncthreads_or(e > 0 && h < HINF);
+        if (!act) break;
+    }
+    // ---- write back: interior pixels plainly, border pixels as deltas
+    // (neighbour tiles may have pushed into them meanwhile)
+    const typename E::Word rv = E::pack(r[0], r[1], r[2], r[3]);
+    if (!on_border(i)) {
+        c.w[p] = e;
+        E::store(c.r, p, rv);
+    } else {
+        if (e != w0) atomicAdd(&c.w[p], e - w0);
+        E::store_delta(c.r, p, rv, rv0);
+    }
+    c.h[p] = h;
+    if (i < 2) s_rowin[i * (TH + 1)] = 0;   // ring rows are never absorbed
+    __syncthreads();
+    if (i < 4 * TW) {
+        const int s = i / TW, j = i % TW;
+        int32_t *slot = &s_in[opp(s)][ring_index(s, j)];
+        const int32_t a = *slot;
+        if (a > 0) {
+            *slot = 0;
+            const int64_t qn = int64_t(tile_nb(c, t, s)) * TPIX + halo_index(s, j);
+            atomicAdd(&c.w[qn], a);
+            E::add(c.r, qn, opp(s), a);
+            atomicOr(&s_side, 1 << s);
+        }
+    }
+    __syncthreads();
+    return TileResult{act, s_side};
+}
+
+template <class E, int MINB>
+__global__ void __launch_bounds__(NTT, MINB) k_push(Ctx c, int k, int iters, int relabel_every, int relax_cap,
+                                                    LaunchCtl lc) {
+    push_prepare();
+    tile_loop(c, k, lc, [&](int32_t t) { return push_tile<E>(c, t, iters, relabel_every, relax_cap); });
 }
 
 }  // namespace pmf

@@ -10,6 +10,8 @@ rows = list(csv.reader(open(sys.argv[1])))
 hi = [i for i, r in enumerate(rows) if r and r[0] == "ID"][0]
 hdr, data = rows[hi], rows[hi + 1:]
 ki, vi, ui = hdr.index("Kernel Name"), hdr.index("Metric Value"), hdr.index("Metric Unit")
+mi = hdr.index("Metric Name")
+data = [r for r in data if r[mi] == "gpu__time_duration.sum"]
 scale = {"ns": 1e-3, "nsecond": 1e-3, "us": 1.0, "usecond": 1.0, "ms": 1e3, "msecond": 1e3}
 seq = [(r[ki].split("(")[0].replace("void ", "").replace("pmf::", ""),
         float(r[vi].replace(",", "")) * scale[r[ui]]) for r in data]

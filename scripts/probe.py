@@ -91,13 +91,15 @@ def main():
             for i, (k, u, t, st0) in enumerate(tr):
                 gap = st0 - (tr[i - 1][3] + tr[i - 1][1]) if i else 0.0
                 print(f"  {k} {st0:9.1f} {u:8.1f} {gap:7.1f} tiles={t}")
+        if st.get("async_mode") and r == a.reps - 1:
+            print("busy ms (CTA-summed):", s.busy(), "kernel ms", round(st["ms_async"], 3))
         if ref is not None:
             import numpy as np
             ok = bool((ref[1] == flows).all()) and bool(np.array_equal(ref[2], labels))
             print("check vs chain=1:", "OK" if ok else "MISMATCH")
         keep = ("cycles", "push_tile_passes", "bfs_tile_passes", "label_tile_passes", "push_sweeps",
                 "bfs_sweeps", "ms_device", "ms_push", "ms_bfs", "ms_labels", "launches", "graph_builds",
-                "steps", "grids")
+                "steps", "grids", "scan_tile_passes", "ms_async")
         print(json.dumps(dict(cfg=a.cfg, args=" ".join(sys.argv[2:]), rep=r,
                               wall_ms=round(dt * 1e3, 2), stage_ms=round((t1 - t0) * 1e3, 2),
                               run_ms=round((t2 - t1) * 1e3, 2), fetch_ms=round((t3 - t2) * 1e3, 2),

@@ -7,6 +7,6 @@ while read -r args; do
     timeout 120 python scripts/probe.py $c --reps 3 $args | tail -1 | python -c "
 import json,sys
 d=json.loads(sys.stdin.read())
-print(d['cfg'], '[$args]', 'dev', d['med_dev_ms'], 'push', d['ms_push'], 'bfs', d['ms_bfs'], 'cyc', d['cycles'], 'ptp', d['push_tile_passes'], 'btp', d['bfs_tile_passes'], 'bsw', d['bfs_sweeps'])" || echo "$c [$args] FAILED"
+print(d['cfg'], '[$args]', 'dev', d['med_dev_ms'], 'push', d['ms_push'], 'bfs', d['ms_bfs'], 'cyc', d['cycles'], 'ptp', d['push_tile_passes'], 'btp', d['bfs_tile_passes'], 'bsw', d['bfs_sweeps'], 'scan', d.get('scan_tile_passes'), 'lab', d['label_tile_passes'])" || echo "$c [$args] FAILED"
   done
 done < "$1"

@@ -248,16 +248,16 @@ def test_c1_stress_repeated(engine, persistent):
         s.close()
 
 
-@pytest.mark.parametrize("rolling", [1, 0])
+@pytest.mark.parametrize("mode", ["async", "rolling", "steps"])
 @pytest.mark.parametrize("chain", [2, 3, 5])
-def test_warm_start_chains_match_reference(engine, chain, rolling):
+def test_warm_start_chains_match_reference(engine, chain, mode):
     """Warm start along the nested schedule (each grid solves `chain`
     consecutive lambdas, reusing the previous maximum preflow) must give the
     reference's cuts, swapped families included -- both with a common step
     per lambda (rolling=0) and with every grid advancing as soon as it
     finishes (rolling=1)."""
     from paper_1509_06004_b200 import _native
-    s = _native.Solver(0, chain=chain, rolling=rolling)
+    s = _native.Solver(0, chain=chain, **{"async": int(mode == "async")}, rolling=int(mode == "rolling"))
     try:
         for case in load_seed_supergraphs():
             probs = _problems(case)
@@ -273,8 +273,13 @@ def test_warm_start_chains_match_reference(engine, chain, rolling):
             assert flows[0].tolist() == g["flows"]
             for j in range(20):
                 assert np.array_equal(labels[0][j], g["labels"][j]), (mode, j)
-        # steps: common lambda steps (rolling=0) / label rounds (rolling=1)
-        assert s.stats()["steps"] == chain if not rolling else s.stats()["steps"] >= chain
+        # steps: common lambda steps (rolling=0) / label rounds (rolling=1) /
+        # lambda-graphs finished (asynchronous solver)
+        st = s.stats()
+        if mode == "async":
+            assert st["async_mode"] and st["steps"] == 20
+        else:
+            assert st["steps"] == chain if mode == "steps" else st["steps"] >= chain
     finally:
         s.close()
 
