@@ -353,3 +353,28 @@ def test_staging_shares_equal_planes_but_checks_each_mask(engine):
             s.solve_seed_batch(64, 48, [pa, pb], lams, "off")
     finally:
         s.close()
+
+
+def test_async_solver_matches_step_synchronous_under_load(engine):
+    """The asynchronous solver (every grid on its own phase machine in one
+    persistent kernel) against the step-synchronous engine on a loaded batch
+    (4 CPMC images, 200 warm-start chains), repeated: bit-identical flows and
+    masks, integrity check on.  Guards the hand-off / phase-transition races
+    (a drained-discharge early finish once passed small tests and failed
+    here)."""
+    from paper_1509_06004_b200 import _native
+    probs = []
+    for i in range(4):
+        probs += synth.generate(500, 375, 5, 5, rng_seed=i, types=("A", "B")).problems
+    sync = _native.Solver(0, **{"async": 0})
+    asy = _native.Solver(0, **{"async": 1})
+    try:
+        _, fs, ls = sync.solve_seed_batch(500, 375, probs, synth.L20, "auto")
+        for _ in range(2):
+            _, fa, la = asy.solve_seed_batch(500, 375, probs, synth.L20, "auto")
+            assert asy.stats()["async_mode"] == 1
+            assert np.array_equal(fa, fs)
+            assert np.array_equal(la, ls)
+    finally:
+        sync.close()
+        asy.close()
