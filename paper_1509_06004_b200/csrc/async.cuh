@@ -279,7 +279,7 @@ __device__ void grid_transition(const Ctx &c, const AsyncArgs &A, int32_t g, int
         if (next == PH_DONE) {
             if (threadIdx.x == 0) {
                 R.phase = PH_DONE;
-                __threadfence();
+                qfence();
             }
             __syncthreads();
             return;
@@ -304,10 +304,10 @@ __device__ void grid_transition(const Ctx &c, const AsyncArgs &A, int32_t g, int
             // hold the phase open while its tiles are being queued: a tile
             // popped and retired meanwhile must not see the count reach zero
             atomicAdd(&c.gpend[g], 1);
-            __threadfence();
+            qfence();
         }
         __syncthreads();
-        __threadfence();
+        qfence();
         for (int32_t j = threadIdx.x; j < nt; j += blockDim.x) {
             const int32_t t = int32_t(t0 + j);
             bool go = all && j % SCAN_GROUP == 0;
@@ -317,7 +317,7 @@ __device__ void grid_transition(const Ctx &c, const AsyncArgs &A, int32_t g, int
             }
             if (go) q_request(c, t);
         }
-        __threadfence();
+        qfence();
         __syncthreads();
         if (threadIdx.x == 0) s_next = atomicSub(&c.gpend[g], 1) == 1;
         __syncthreads();
@@ -360,14 +360,14 @@ __global__ void __launch_bounds__(NTT, 2) k_async(Ctx c, AsyncArgs A) {
             int32_t t = s_cont;
             s_cont = -1;
             if (t < 0) t = q_next(c);
-            __threadfence();
+            qfence();
             s_t = t;
             atomicAdd(&c.stat[ST_BUSY + BUSY_WAIT], gtimer() - tw);
         }
         __syncthreads();
         const int32_t t = s_t;
         if (t < 0) break;
-        __threadfence();   // popper side: state write < data reads
+        qfence();   // popper side: state write < data reads
         const unsigned long long tb = i == 0 ? gtimer() : 0ull;
         const int32_t g = __ldg(c.tile_grid + t);
         const int ph = __ldcg(&A.gr[g].phase);
@@ -394,7 +394,8 @@ __global__ void __launch_bounds__(NTT, 2) k_async(Ctx c, AsyncArgs A) {
             }
             __syncthreads();
             if (s_ok) {
-                r = push_tile<E>(c, t, A.iters, A.relabel_every, A.relax_cap);
+                r = c.push_mode == 1 ? push_tile1<E>(c, t, A.iters, A.relabel_every, A.relax_cap)
+                                     : push_tile<E>(c, t, A.iters, A.relabel_every, A.relax_cap);
                 stat = ST_PUSH;
             }
         } else if (ph == PH_LAB) {
@@ -403,25 +404,29 @@ __global__ void __launch_bounds__(NTT, 2) k_async(Ctx c, AsyncArgs A) {
         }
         const unsigned long long tf = i == 0 ? gtimer() : 0ull;
         if (i == 0) atomicAdd(&c.stat[ST_BUSY + ph], tf - tb);
-        __threadfence();   // requester side: data writes < queue-state reads
+        qfence();   // requester side: data writes < queue-state reads
         __syncthreads();
         if (i < 32) {
             // neighbours this pass touched (same phase); the lowest one is
             // taken over directly when the tile itself is done
             const unsigned flags = unsigned(r.out) & 15u;
             const int want = (A.cont && !r.again && flags) ? __ffs(flags) : 0;
+            // the neighbours are counted pending before this tile retires
+            // (so its grid's count cannot touch zero meanwhile); their ring
+            // insertion overlaps the retirement
+            int32_t nb = -1;
+            bool push = false;
             if (i >= 1 && i <= 4 && ((flags >> (i - 1)) & 1)) {
-                __threadfence();
-                const int32_t nb = tile_nb(c, t, i - 1);
+                nb = tile_nb(c, t, i - 1);
                 if (nb >= 0) {
                     if (i == want && q_claim(c, nb)) s_cont = nb;
-                    else q_request(c, nb);
+                    else push = q_mark(c, nb);
                 }
-                __threadfence();
+                qfence();
             }
             __syncwarp();
+            if (push) q_push(c, nb);
             if (i == 0) {
-                __threadfence();
                 s_fin = aq_finish(c, t, r.again != 0);
                 if (stat >= 0) atomicAdd(&c.stat[stat], (unsigned long long)npass);
             }
@@ -431,20 +436,20 @@ __global__ void __launch_bounds__(NTT, 2) k_async(Ctx c, AsyncArgs A) {
         const unsigned long long tt = i == 0 ? gtimer() : 0ull;
         if (i == 0) atomicAdd(&c.stat[ST_BUSY + BUSY_FOLLOW], tt - tf);
         if (fin == 2) {
-            __threadfence();
+            qfence();
             grid_transition(c, A, g, ph);
             if (i == 0) atomicAdd(&c.stat[ST_BUSY + BUSY_TRANS], gtimer() - tt);
         }
         if (i == 0 && fin) {
-            __threadfence();
+            qfence();
             atomicSub(&c.qctr[QC_PENDING], 1u);
         }
     }
     if (i == 0) {
         atomicMax(&c.ctl->t1, gtimer());
-        __threadfence();
+        qfence();
         if (atomicAdd(&c.ctl->done, 1u) == gridDim.x - 1) {
-            __threadfence();
+            qfence();
             const unsigned long long t0 = *(volatile unsigned long long *)&c.ctl->t0;
             const unsigned long long t1 = *(volatile unsigned long long *)&c.ctl->t1;
             c.stat[ST_ASYNC_NS] = t1 > t0 ? t1 - t0 : 0ull;

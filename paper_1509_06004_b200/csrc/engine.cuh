@@ -115,6 +115,7 @@ struct Ctx {
     int32_t *gpend;         // per grid: its tiles queued or running in the current persistent phase
     int32_t ngrids;
     int32_t rolling;        // rolling warm start: grids emit and advance as they finish
+    int32_t push_mode;      // discharge body: 0 two barriers per iteration, 1 one (double-buffered inflow)
     int32_t *act;           // per grid active-pixel count of the last seed pass
     int32_t *list0, *list1; // double-buffered tile worklists
     int32_t *inq0, *inq1;   // "already listed" flags per tile, per buffer
@@ -145,6 +146,13 @@ struct Ctx {
 enum { Q_IDLE = 0, Q_QUEUED = 1, Q_RUNNING = 2, Q_DIRTY = 3 };
 enum { QC_HEAD = 0, QC_TAIL = 1, QC_PENDING = 2, QC_CONT = 3 };   // HEAD: tickets taken; CONT: continuations
 
+// Queue hand-off fence.  Every cross-CTA hand-off of a tile goes through a
+// read-modify-write of that tile's queue state (requests CAS it, pops and
+// retirements exchange / CAS it), so the data written before a request is
+// published by release / acquire through the same location; gpu-scope
+// acq_rel fences suffice where sequential consistency would cost more.
+__device__ __forceinline__ void qfence() { asm volatile("fence.acq_rel.gpu;" ::: "memory"); }
+
 __device__ __forceinline__ unsigned ld_volatile(const unsigned *p) {
     return *(const volatile unsigned *)p;
 }
@@ -157,21 +165,28 @@ __device__ __forceinline__ void q_push(const Ctx &c, int32_t t) {
 }
 
 // Ask for tile t to be (re)processed: idle -> queued, running -> dirty.
-__device__ __forceinline__ void q_request(const Ctx &c, int32_t t) {
+// Always an RMW on the state (see qfence).  Split in two so a hand-off can
+// overlap the ring insertion with the retirement of its own tile:
+// q_mark() changes the state and counts the tile as pending (returns true
+// when the caller must q_push it), q_push() inserts it.
+__device__ __forceinline__ bool q_mark(const Ctx &c, int32_t t) {
+    int s = atomicCAS(&c.qstate[t], Q_IDLE, Q_QUEUED);
     for (;;) {
-        int s = *(volatile int32_t *)&c.qstate[t];
-        if (s == Q_QUEUED || s == Q_DIRTY) return;
         if (s == Q_IDLE) {
-            if (atomicCAS(&c.qstate[t], Q_IDLE, Q_QUEUED) == Q_IDLE) {
-                atomicAdd(&c.qctr[QC_PENDING], 1u);
-                atomicAdd(&c.gpend[c.tile_grid[t]], 1);
-                q_push(c, t);
-                return;
-            }
-        } else if (atomicCAS(&c.qstate[t], Q_RUNNING, Q_DIRTY) == Q_RUNNING) {
-            return;
+            atomicAdd(&c.qctr[QC_PENDING], 1u);
+            atomicAdd(&c.gpend[c.tile_grid[t]], 1);
+            return true;
         }
+        if (s == Q_QUEUED || s == Q_DIRTY) return false;
+        // running: mark dirty (it requeues itself when done)
+        const int o = atomicCAS(&c.qstate[t], Q_RUNNING, Q_DIRTY);
+        if (o == Q_RUNNING) return false;
+        s = o == Q_IDLE ? atomicCAS(&c.qstate[t], Q_IDLE, Q_QUEUED) : o;
     }
+}
+
+__device__ __forceinline__ void q_request(const Ctx &c, int32_t t) {
+    if (q_mark(c, t)) q_push(c, t);
 }
 
 // The running tile t is done; requeue it if it still has work or was
