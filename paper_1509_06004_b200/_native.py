@@ -213,7 +213,12 @@ class Solver:
         out = np.zeros(16, np.float64)
         self._lib.pmf_debug_busy(self._h, out.ctypes.data_as(ctypes.POINTER(ctypes.c_double)))
         names = ("binit", "bfs", "seed", "push", "linit", "lab", "emit", "-", "wait", "handoff", "transition")
-        return {k: round(float(v), 2) for k, v in zip(names, out) if k != "-"}
+        d = {k: round(float(v), 2) for k, v in zip(names, out) if k != "-"}
+        d["push_iterations"] = int(out[15])
+        d["relax_ms"] = round(float(out[13]), 2)
+        d["relax_calls"] = int(out[14])
+        d["relax_sweeps"] = int(out[12])
+        return d
 
     def stream_handle(self) -> int:
         """The solver's cudaStream_t as an integer (torch.cuda.ExternalStream)."""

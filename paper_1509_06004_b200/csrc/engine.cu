@@ -926,6 +926,10 @@ int run_end(pmf_solver *s) {
     s->stats.emit_tile_passes = int64_t(st[ST_EMIT]);
     s->stats.ms_async = double(st[ST_ASYNC_NS]) * 1e-6;
     for (int k = 0; k < BUSY_N; k++) s->busy_ms[k] = double(st[ST_BUSY + k]) * 1e-6;
+    s->busy_ms[15] = double(st[ST_PUSH_ITERS]);
+    s->busy_ms[13] = double(st[ST_RELAX_NS]) * 1e-6;
+    s->busy_ms[14] = double(st[ST_RELAX_N]);
+    s->busy_ms[12] = double(st[ST_RELAX_SW]);
     s->stats.push_tile_passes = int64_t(st[ST_PUSH]);
     s->stats.bfs_tile_passes = int64_t(st[ST_BFS]);
     s->stats.label_tile_passes = int64_t(st[ST_LAB]);

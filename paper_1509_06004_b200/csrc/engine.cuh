@@ -33,6 +33,8 @@ enum {
     ST_PUSH = 0, ST_BFS = 1, ST_LAB = 2,
     ST_PUSH_NS = 3, ST_BFS_NS = 4, ST_LAB_NS = 5,
     ST_PUSH_L = 6, ST_BFS_L = 7, ST_LAB_L = 8,
+    ST_PUSH_ITERS = 28,   // discharge iterations executed (diagnostics)
+    ST_RELAX_NS = 29, ST_RELAX_N = 30, ST_RELAX_SW = 31,   // discharge local relabels: time, count, sweeps
     ST_NSTAT = 40
 };
 

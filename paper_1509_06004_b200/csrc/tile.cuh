@@ -58,9 +58,9 @@ __device__ __forceinline__ int32_t line_relax(int32_t v, int m, int lane, unsign
 }
 
 // d: [32][SP] values, mk: [32][32] pull masks, hv: halo values.  All 1024
-// threads call it.  Runs to the fixpoint (returns 1) or stops after
-// max_sweeps sweeps (> 0; returns 0 if it had not converged) -- a capped
-// relax only gives upper bounds and its HINF values are not certificates.
+// threads call it.  Runs to the fixpoint (bit 0 of the result set) or stops
+// after max_sweeps sweeps (> 0; bit 0 clear if it had not converged) -- a
+// capped relax only gives upper bounds.  Bits 1.. hold the sweeps run.
 __device__ int tile_relax(int32_t *d, const uint8_t *mk, const int32_t (*hv)[TW], int cost,
                           int max_sweeps = 0) {
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -89,8 +89,8 @@ __device__ int tile_relax(int32_t *d, const uint8_t *mk, const int32_t (*hv)[TW]
             if (v != v0) { d[lane * SP + warp] = v; changed = 1; }
         }
         sweeps++;
-        if (!__syncthreads_or(changed)) return 1;
-        if (max_sweeps && sweeps >= max_sweeps) return 0;
+        if (!__syncthreads_or(changed)) return 1 | (sweeps << 1);
+        if (max_sweeps && sweeps >= max_sweeps) return sweeps << 1;
     }
 }
 
@@ -487,15 +487,22 @@ __device__ __forceinline__ TileResult push_tile(const Ctx &c, int32_t t, int ite
     }
     if (i == 0) s_side = 0;
     int act = 1;
-    int until_relabel = 0;
+    int until_relabel = 0, its = 0;
     for (int it = 0; it < iters; it++) {
+        its++;
         if (relabel_every && until_relabel == 0) {
             until_relabel = relabel_every;
             // exact local relabel (frozen pixels stay frozen)
             s_sd[pi] = e < 0 ? 1 : HINF;
             s_sm[i] = uint8_t((r[0] > 0) | ((r[1] > 0) << 1) | ((r[2] > 0) << 2) | ((r[3] > 0) << 3));
             __syncthreads();
-            const int conv = tile_relax(s_sd, s_sm, s_hv, 1, relax_cap);
+            const unsigned long long tr0 = i == 0 ? gtimer() : 0ull;
+            const int rr = tile_relax(s_sd, s_sm, s_hv, 1, relax_cap), conv = rr & 1;
+            if (i == 0) {   // diagnostics
+                atomicAdd(&c.stat[ST_RELAX_NS], gtimer() - tr0);
+                atomicAdd(&c.stat[ST_RELAX_N], 1ull);
+                atomicAdd(&c.stat[ST_RELAX_SW], (unsigned long long)(rr >> 1));
+            }
             // an unconverged relax may not freeze anyone (keep the old
             // height where it found nothing)
             if (h < HINF && (conv || s_sd[pi] < HINF)) h = s_sd[pi];
@@ -567,6 +574,7 @@ __device__ __forceinline__ TileResult push_tile(const Ctx &c, int32_t t, int ite
         act = __syncthreads_or(e > 0 && h < HINF);
         if (!act) break;
     }
+    if (i == 0) atomicAdd(&c.stat[ST_PUSH_ITERS], (unsigned long long)its);   // diagnostics
     // ---- write back: interior pixels plainly, border pixels as deltas
     // (neighbour tiles may have pushed into them meanwhile)
     const typename E::Word rv = E::pack(r[0], r[1], r[2], r[3]);
@@ -650,7 +658,7 @@ __device__ __forceinline__ TileResult push_tile1(const Ctx &c, int32_t t, int it
             s_sd[pi] = e < 0 ? 1 : HINF;
             s_sm[i] = uint8_t((r[0] > 0) | ((r[1] > 0) << 1) | ((r[2] > 0) << 2) | ((r[3] > 0) << 3));
             __syncthreads();
-            const int conv = tile_relax(s_sd, s_sm, s_hv, 1, relax_cap);
+            const int conv = tile_relax(s_sd, s_sm, s_hv, 1, relax_cap) & 1;
             if (h < HINF && (conv || s_sd[pi] < HINF)) h = s_sd[pi];
             s_ph[q] = h;
             act = __syncthreads_or(e > 0 && h < HINF);
