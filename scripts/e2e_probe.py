@@ -6,9 +6,10 @@ from paper_1509_06004_b200 import LambdaSchedule, _native, synth, solve_seed_sup
 from paper_1509_06004_b200.supergraph import check_seed_supergraph
 
 imgs = int(sys.argv[1]) if len(sys.argv) > 1 else 1
+rows = int(sys.argv[2]) if len(sys.argv) > 2 else 5      # 1: the C2 single-seed supergraph
 probs = []
 for i in range(imgs):
-    probs += synth.generate(500, 375, 5, 5, rng_seed=i, types=("A", "B")).problems
+    probs += synth.generate(500, 375, rows, rows, rng_seed=i, types=("A", "B") if rows > 1 else ("A",)).problems
 sched = LambdaSchedule(synth.L20)
 s = _native.solver_for_thread(0)
 for rep in range(4):
