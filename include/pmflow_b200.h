@@ -176,6 +176,14 @@ int pmf_seed_stage(pmf_solver *s, int32_t nprob, int32_t width, int32_t height,
 int pmf_seed_run(pmf_solver *s);
 int pmf_seed_fetch(pmf_solver *s, uint8_t *swapped_out, int64_t *flows_out, uint8_t *labels_out);
 
+/* Scores of the last seed run on the device (replaces the per-cut host
+ * loop of harness/bench.py:95-113, `overlap` :36-45): truths[p] is problem
+ * p's 0/1 ground-truth mask (width*height bytes, row-major); for every
+ * (problem, lambda), problem-major: fg_out = |S|, inter_out = |S & G|,
+ * union_out = |S | G| (overlap = inter / union, exact). */
+int pmf_seed_score(pmf_solver *s, const uint8_t *const *truths, int64_t *fg_out, int64_t *inter_out,
+                   int64_t *union_out);
+
 /* Diagnostics: the first (up to *n, at most 256) tile-kernel launches of the
  * last run: kind (0 discharge, 1 sink BFS, 2 label BFS; 4-6 one sweep of a
  * multi-sweep launch of kind 0-2), device span in us,

@@ -24,7 +24,7 @@ SWAP_MODES = {"auto": 0, "on": 1, "off": 2}
 EXPORTS = ("pmf_solver_create", "pmf_solver_destroy", "pmf_solver_set", "pmf_last_error",
            "pmf_solver_stats", "pmf_solver_stream", "pmf_solve_composites", "pmf_solve_seed_batch",
            "pmf_seed_stage", "pmf_seed_run", "pmf_seed_fetch", "pmf_debug_state",
-           "pmf_debug_trace", "pmf_debug_busy")
+           "pmf_debug_trace", "pmf_debug_busy", "pmf_seed_score")
 
 
 class NativeUnavailable(RuntimeError):
@@ -85,6 +85,7 @@ def load_library(path: str = LIB_PATH):
         lib.pmf_debug_state.argtypes = [vp, vp, vp, vp, vp, P(i64)]
         lib.pmf_debug_trace.argtypes = [vp, vp, vp, vp, vp, P(i32)]
         lib.pmf_debug_busy.argtypes = [vp, P(ctypes.c_double)]
+        lib.pmf_seed_score.argtypes = [vp, P(vp), P(i64), P(i64), P(i64)]
         for name in EXPORTS:
             if name != "pmf_last_error":
                 getattr(lib, name).restype = ctypes.c_int
@@ -269,6 +270,24 @@ class Solver:
         if rc:
             _raise_for(rc)
         return swapped.astype(bool), flows.reshape(P_, K), lab
+
+    def seed_score(self, truths):
+        """Device scores of the last seed run against one 0/1 truth mask per
+        problem: (foreground, intersection, union) int64 arrays (P, K)."""
+        n, P_, K = self._staged
+        if len(truths) != P_:
+            raise ValueError(f"need one truth mask per problem ({P_}), got {len(truths)}")
+        keep = [np.ascontiguousarray(np.asarray(t).reshape(-1) != 0, np.uint8) for t in truths]
+        if any(k.size != n for k in keep):
+            raise ValueError("truth mask size differs from the problems' pixel count")
+        fg, inter, uni = (np.zeros(P_ * K, np.int64) for _ in range(3))
+        Pt = ctypes.POINTER
+        rc = self._lib.pmf_seed_score(self._h, _ptrs(keep), fg.ctypes.data_as(Pt(ctypes.c_int64)),
+                                      inter.ctypes.data_as(Pt(ctypes.c_int64)),
+                                      uni.ctypes.data_as(Pt(ctypes.c_int64)))
+        if rc:
+            _raise_for(rc)
+        return fg.reshape(P_, K), inter.reshape(P_, K), uni.reshape(P_, K)
 
     def solve_seed_batch(self, width, height, problems, lambdas, swap_mode="auto"):
         """problems: objects with unary_base, unary_slope, sink_base, pairwise

@@ -221,7 +221,7 @@ struct pmf_solver {
     int timing = 0;
     int64_t max_cycles = 50000;
     // device workspace
-    DevBuf d_w, d_h, d_r, d_lab, d_tile_grid, d_tnb, d_fin, d_gpend, d_gr, d_tflag, d_vacc, d_grids, d_live, d_act, d_list, d_inq, d_cnt,
+    DevBuf d_w, d_h, d_r, d_lab, d_tile_grid, d_tnb, d_fin, d_gpend, d_gr, d_tflag, d_vacc, d_truth, d_score, d_grids, d_live, d_act, d_list, d_inq, d_cnt,
         d_snk, d_drain, d_err, d_stat, d_colswap, d_out, d_bits, d_in32, d_pw, d_mask, d_off, d_lam,
         d_swapcnt, d_swapflag, d_ring, d_qstate, d_qctr, d_ctl, d_curlam, d_flows, d_slopesum;
     HostBuf h_in32, h_pw, h_mask, h_out, h_small;
@@ -1683,6 +1683,50 @@ int pmf_seed_run(pmf_solver *s) {
     rc = run_end(s);
     s->stats.h2d_bytes = h2d;
     return rc;
+}
+
+// Device scoring of the last seed run against ground-truth masks (one n-byte
+// 0/1 mask per problem): per (problem, lambda) foreground count and the
+// exact Jaccard overlap terms |S & G|, |S | G| (harness/bench.py:36-45).
+int pmf_seed_score(pmf_solver *s, const uint8_t *const *truths, int64_t *fg_out, int64_t *inter_out,
+                   int64_t *union_out) {
+    if (!s || !s->stage.valid || !truths || !fg_out || !inter_out || !union_out)
+        return fail(PMF_ERR_ARG, "bad arguments");
+    CK(cudaSetDevice(s->device));
+    const SeedStage &S = s->stage;
+    const int64_t n = int64_t(S.W) * S.H, planes = int64_t(S.nprob) * S.nlam;
+    int rc;
+    if ((rc = s->d_truth.ensure(size_t(S.nprob) * n)) || (rc = s->d_score.ensure(size_t(planes) * 24)) ||
+        (rc = s->h_mask.ensure(size_t(S.nprob) * n)) || (rc = s->h_small.ensure(size_t(planes) * 24 + 64)))
+        return rc;
+    // the previous run may still read the staging masks
+    CK(cudaStreamSynchronize(s->st));
+    uint8_t *hm = s->h_mask.as<uint8_t>();
+    TaskErr terr;
+    s->pool->run(S.nprob, [&](int64_t p) {
+        if (!truths[p]) {
+            terr.set(PMF_ERR_ARG, "a truth mask is missing");
+            return;
+        }
+        memcpy(hm + p * n, truths[p], size_t(n));
+    });
+    if ((rc = terr.raise())) return rc;
+    CK(cudaMemcpyAsync(s->d_truth.p, hm, size_t(S.nprob) * n, cudaMemcpyHostToDevice, s->st));
+    CK(cudaMemsetAsync(s->d_score.p, 0, size_t(planes) * 24, s->st));
+    const int chunks = int(std::max<int64_t>(1, std::min<int64_t>(cdiv(n, 16384), 1024)));
+    LAUNCH(s, (k_score<<<int(std::min<int64_t>(planes * chunks, 32 * s->sms)), NT, 0, s->st>>>(
+                   s->d_out.as<uint8_t>(), s->d_truth.as<uint8_t>(), S.nprob, S.nlam, n, chunks,
+                   s->d_score.as<unsigned long long>())));
+    CK(cudaGetLastError());
+    int64_t *hs = s->h_small.as<int64_t>();
+    CK(cudaMemcpyAsync(hs, s->d_score.p, size_t(planes) * 24, cudaMemcpyDeviceToHost, s->st));
+    CK(cudaStreamSynchronize(s->st));
+    for (int64_t k = 0; k < planes; k++) {
+        fg_out[k] = hs[3 * k];
+        inter_out[k] = hs[3 * k + 1];
+        union_out[k] = hs[3 * k + 2];
+    }
+    return 0;
 }
 
 int pmf_seed_fetch(pmf_solver *s, uint8_t *swapped_out, int64_t *flows_out, uint8_t *labels_out) {

@@ -483,6 +483,37 @@ __global__ void __launch_bounds__(NT) k_verify(Ctx c, SeedArgs a, unsigned long 
     }
 }
 
+// Scores of every emitted mask against its problem's ground-truth mask
+// (harness/bench.py:36-45 overlap, :104-111 foreground): per (problem,
+// lambda) plane the foreground count |S|, |S & G| and |S | G|, summed into
+// acc[3 * plane + {0, 1, 2}] (zeroed by the caller).  One CTA per (plane,
+// pixel chunk), 16 bytes per thread per step.
+__global__ void __launch_bounds__(NT) k_score(const uint8_t *__restrict__ out, const uint8_t *__restrict__ truth,
+                                              int32_t nprob, int32_t nlam, int64_t n, int chunks,
+                                              unsigned long long *acc) {
+    __shared__ int64_t red[NT / 32];
+    const int64_t per = ((n + chunks - 1) / chunks + 15) / 16 * 16;
+    for (int64_t blk = blockIdx.x; blk < int64_t(nprob) * nlam * chunks; blk += gridDim.x) {
+        const int64_t plane = blk / chunks;
+        const int64_t lo = (blk % chunks) * per, hi = min(n, lo + per);
+        const uint8_t *m = out + plane * n;
+        const uint8_t *g = truth + (plane / nlam) * n;
+        int64_t fg = 0, in = 0, un = 0;
+        for (int64_t q = lo + threadIdx.x; q < hi; q += NT) {
+            const int a = m[q] != 0, b = g[q] != 0;
+            fg += a;
+            in += a & b;
+            un += a | b;
+        }
+        const int64_t sf = block_sum64(fg, red), si = block_sum64(in, red), su = block_sum64(un, red);
+        if (threadIdx.x == 0) {
+            if (sf) atomicAdd(acc + 3 * plane + 0, (unsigned long long)sf);
+            if (si) atomicAdd(acc + 3 * plane + 1, (unsigned long long)si);
+            if (su) atomicAdd(acc + 3 * plane + 2, (unsigned long long)su);
+        }
+    }
+}
+
 __global__ void k_verify_check(Ctx c, int64_t nplanes, const unsigned long long *acc) {
     for (int64_t plane = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; plane < nplanes;
          plane += int64_t(gridDim.x) * blockDim.x)

@@ -247,6 +247,7 @@ class SeedSupergraphResult:
 
     layout: SupergraphLayout
     cuts: tuple
+    scores: tuple = ()   # scoring.CutScore per cut when truths were given
 
     @property
     def flow(self) -> int:
@@ -268,16 +269,24 @@ def check_seed_supergraph(problems, schedule: LambdaSchedule, swap_mode: str = "
 
 
 def solve_seed_supergraph(problems, schedule: LambdaSchedule, swap_mode: str = "auto",
-                          device: int = 0) -> SeedSupergraphResult:
-    """Build + solve + decode a seed supergraph entirely on the device."""
+                          device: int = 0, truths=None) -> SeedSupergraphResult:
+    """Build + solve + decode a seed supergraph entirely on the device.
+    With ``truths`` (one 0/1 mask per problem) every cut is also scored on
+    the device (foreground count, exact overlap; harness/bench.py:95-113)."""
     from . import _native
     problems = check_seed_supergraph(problems, schedule, swap_mode)
     shapes = {(p.width, p.height) for p in problems}
     solver = _native.solver_for_thread(device)
+    scores = ()
     if len(shapes) == 1:
         W, H = shapes.pop()
         swapped, flows, labels = solver.solve_seed_batch(W, H, problems, schedule.values, swap_mode)
+        if truths is not None:
+            from .scoring import score_cuts
+            scores = score_cuts(solver, truths)
     else:  # same height, different widths: one device batch per width
+        if truths is not None:
+            raise SupergraphError("device scoring needs problems of one shape")
         swapped = np.zeros(len(problems), bool)
         flows = [None] * len(problems)
         labels = [None] * len(problems)
@@ -289,4 +298,4 @@ def solve_seed_supergraph(problems, schedule: LambdaSchedule, swap_mode: str = "
                 swapped[i], flows[i], labels[i] = sw[k], fl[k], lb[k]
     cuts = tuple(CutResult(int(flows[i][j]), labels[i][j])
                  for i in range(len(problems)) for j in range(len(schedule)))
-    return SeedSupergraphResult(seed_layout(problems, schedule, swapped), cuts)
+    return SeedSupergraphResult(seed_layout(problems, schedule, swapped), cuts, scores)

@@ -105,12 +105,24 @@ def quantize_weights(values, scale: int = 1 << 16) -> np.ndarray:
     return q
 
 
+def truth_mask(region, seed_x, seed_y) -> np.ndarray:
+    """Flat uint8 mask of the region containing the seed
+    (harness/synth.py:102-105)."""
+    return (region == region[seed_y, seed_x]).astype(np.uint8).reshape(-1)
+
+
 @dataclass
 class SynthBatch:
     image: np.ndarray
     regions: np.ndarray
     coords: list
     problems: list
+    types: tuple = ("A",)
+
+    @property
+    def truths(self) -> list:
+        """Ground-truth mask per problem (its seed's region), in problem order."""
+        return [truth_mask(self.regions, x, y) for (x, y) in self.coords for _ in self.types]
 
 
 def generate(width, height, seed_rows=1, seed_cols=1, regions=4, noise=10, rng_seed=0,
@@ -127,4 +139,4 @@ def generate(width, height, seed_rows=1, seed_cols=1, regions=4, noise=10, rng_s
     for (x, y) in coords:
         terms = seed_terms(img, x, y)
         probs += [seed_problem(img, x, y, pw, bgs[t], terms) for t in types]
-    return SynthBatch(img, reg, coords, probs)
+    return SynthBatch(img, reg, coords, probs, tuple(types))

@@ -93,3 +93,21 @@ def engine():
     """The built native engine on cuda:0 (fails loudly if missing)."""
     from paper_1509_06004_b200 import _native
     return _native.solver_for_thread(0)
+
+
+def load_scores():
+    """Reference scores (harness/bench.py:104-111) of a 96x72, 2x2-seed synth
+    batch: per problem flows, foreground counts, exact overlaps."""
+    with open(os.path.join(GOLDEN, "scores_96x72_2x2.json")) as f:
+        return json.load(f)
+
+
+def problem_digest(p):
+    """sha256 of a SeedProblem's planes and seeds (make_golden.problem_digest)."""
+    import hashlib
+    h = hashlib.sha256()
+    for a in (p.unary_base, p.unary_slope, p.sink_base, p.pairwise):
+        h.update(np.ascontiguousarray(a, np.int64).tobytes())
+    h.update(np.array(sorted(p.fg_seeds), np.int64).tobytes())
+    h.update(np.array(sorted(p.bg_seeds), np.int64).tobytes())
+    return h.hexdigest()

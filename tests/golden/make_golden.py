@@ -188,16 +188,43 @@ def synth_config(name, width, height, lambdas, rows=1, cols=1, rng_seed=0, compo
     np.savez_compressed(os.path.join(OUT, name), **rec)
 
 
+def synth_scores(name, width, height, lambdas, rows=1, cols=1, rng_seed=0):
+    """Reference scoring of per-lambda cuts (harness/bench.py:104-111):
+    foreground counts and exact overlaps with the truth masks, per problem."""
+    from pmflow.harness.bench import overlap
+    cfg = BenchConfig(width=width, height=height, seed_rows=rows, seed_cols=cols,
+                      rng_seed=rng_seed)
+    _, problems, truths = generate_batch(cfg)
+    recs = []
+    for p, t in zip(problems, truths):
+        seq = solve_schedule_sequential(p, LambdaSchedule(lambdas))
+        ov = [overlap(c.labels, t) for c in seq.cuts]
+        recs.append(dict(problem_sha256=problem_digest(p),
+                         truth_sha256=hashlib.sha256(np.asarray(t, np.uint8).tobytes()).hexdigest(),
+                         flows=[c.flow for c in seq.cuts],
+                         foreground=[int(c.labels.sum()) for c in seq.cuts],
+                         overlap=[[o.numerator, o.denominator] for o in ov]))
+    with open(os.path.join(OUT, name), "w") as f:
+        json.dump(dict(width=width, height=height, rows=rows, cols=cols, rng_seed=rng_seed,
+                       lambdas=list(lambdas), problems=recs), f)
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--big", action="store_true")
+    ap.add_argument("--only-scores", action="store_true")
     args = ap.parse_args()
+    if args.only_scores:
+        synth_scores("scores_96x72_2x2.json", 96, 72, LambdaSchedule.default().values, rows=2, cols=2,
+                     rng_seed=5)
+        return
     kat()
     random_sweep("random_8x8_seed101.npz", 101, 500, 8, 10)     # test_acceptance.py:34-46
     random_sweep("random_3x3_seed102.npz", 102, 100, 3, 10)     # :49-60
     composite_sweep("composites_swapped", 34, 40)
     seed_supergraph_cases()
     synth_config("c1_160x120.npz", 160, 120, LambdaSchedule.default().values, composite=True)
+    synth_scores("scores_96x72_2x2.json", 96, 72, LambdaSchedule.default().values, rows=2, cols=2, rng_seed=5)
     if args.big:
         synth_config("c2_500x375.npz", 500, 375, L20)
 

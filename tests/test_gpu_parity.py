@@ -378,3 +378,23 @@ def test_async_solver_matches_step_synchronous_under_load(engine):
     finally:
         sync.close()
         asy.close()
+
+
+def test_device_scoring_matches_reference():
+    """Device scoring (pmf_seed_score) of a seed supergraph equals the
+    reference's per-cut foreground counts and exact overlaps
+    (harness/bench.py:104-111), and the host overlap of the returned masks."""
+    from fractions import Fraction
+    from conftest import load_scores
+    from paper_1509_06004_b200.scoring import overlap
+    g = load_scores()
+    b = synth.generate(g["width"], g["height"], g["rows"], g["cols"], rng_seed=g["rng_seed"])
+    res = solve_seed_supergraph(b.problems, LambdaSchedule(g["lambdas"]), "auto", truths=b.truths)
+    K = len(g["lambdas"])
+    assert len(res.scores) == len(b.problems) * K
+    for pi, rec in enumerate(g["problems"]):
+        for j in range(K):
+            cut, sc = res.cuts[pi * K + j], res.scores[pi * K + j]
+            assert cut.flow == rec["flows"][j]
+            assert sc.foreground == rec["foreground"][j] == int(cut.labels.sum())
+            assert sc.overlap == Fraction(*rec["overlap"][j]) == overlap(cut.labels, b.truths[pi])

@@ -283,3 +283,34 @@ def test_synth_type_b_and_lattice():
     top = set(range(24))
     assert bb.bg_seeds == a.bg_seeds - top
     assert np.array_equal(a.unary_base, bb.unary_base)
+
+
+def test_overlap_reference_fixtures():
+    """harness/bench.py:36-45 semantics (test_harness.py:119-130,
+    test_acceptance.py:215-221)."""
+    from fractions import Fraction
+    from paper_1509_06004_b200.scoring import CutScore, overlap, scores_from_counts
+    assert overlap([1, 0, 1], [1, 0, 1]) == Fraction(1)
+    assert overlap([1, 1, 0, 0], [0, 0, 1, 1]) == Fraction(0)
+    assert overlap([1, 1, 0, 0], [1, 1, 1, 1]) == Fraction(1, 2)
+    with pytest.raises(ValueError):
+        overlap([1, 0], [1, 0, 0])
+    with pytest.raises(ValueError):
+        overlap([0, 0], [0, 0])
+    assert scores_from_counts([3], [2], [4]) == (CutScore(3, Fraction(1, 2)),)
+    with pytest.raises(ValueError):
+        scores_from_counts([0], [0], [0])
+
+
+def test_synth_truths_match_reference():
+    """Our generator reproduces the reference's problems and truth masks
+    (harness/synth.py:102-136) for the scored golden batch."""
+    import hashlib
+    from conftest import load_scores, problem_digest
+    from paper_1509_06004_b200 import synth
+    g = load_scores()
+    b = synth.generate(g["width"], g["height"], g["rows"], g["cols"], rng_seed=g["rng_seed"])
+    assert len(b.problems) == len(g["problems"])
+    for p, t, rec in zip(b.problems, b.truths, g["problems"]):
+        assert problem_digest(p) == rec["problem_sha256"]
+        assert hashlib.sha256(np.asarray(t, np.uint8).tobytes()).hexdigest() == rec["truth_sha256"]
