@@ -82,12 +82,16 @@ __device__ __forceinline__ void scan_reset() {
 // flagged pixel, plus each neighbour facing a flagged border pixel (a seed
 // never changes, so the tile alone would never hand it across the border;
 // seed_with_halo() of the worklist kernels)
-__device__ __forceinline__ void scan_flag(const Ctx &c, const AsyncArgs &A, int32_t t0, int ntl) {
+// (bit 4 of sides, when `need_open` is set: the tile also has an unflagged
+// pixel -- a tile whose every pixel is flagged is not listed itself, only
+// the neighbours facing its border)
+__device__ __forceinline__ void scan_flag(const Ctx &c, const AsyncArgs &A, int32_t t0, int ntl,
+                                          bool need_open = false) {
     __syncthreads();
     const int k = threadIdx.x;
     if (k < ntl && s_scan.any[k]) {
         const int32_t t = t0 + k;
-        A.tflag[t] = 1;
+        if (!need_open || (s_scan.sides[k] & 16)) A.tflag[t] = 1;
         for (int s = 0; s < 4; s++)
             if ((s_scan.sides[k] >> s) & 1) {
                 const int32_t nb = tile_nb(c, t, s);
@@ -149,19 +153,32 @@ __device__ __forceinline__ void seed_group(const Ctx &c, const AsyncArgs &A, int
 
 // LINIT (k_lab_seed): lab = (w > 0), label BFS seeds (swapped grids report
 // the sink side and run no label BFS: nothing to flag)
-__device__ __forceinline__ void linit_group(const Ctx &c, const AsyncArgs &A, int32_t t0, int ntl, bool swapped) {
+// Past the first lambda of a chain the previous lambda's source side also
+// seeds the closure: minimal source sides are nested along a monotone
+// schedule (parametric.py:191-201), so S(lambda_i) is inside
+// S(lambda_{i+1}) and adding it changes nothing but the distance the
+// closure has to travel; tiles already fully inside are not relaxed.
+__device__ __forceinline__ void linit_group(const Ctx &c, const AsyncArgs &A, int32_t t0, int ntl, int32_t g,
+                                            bool swapped) {
     const int i = threadIdx.x;
+    const bool nested = __ldcg(c.cur_lam + g) > c.grids[g].lam;
     scan_reset();
     int v[SCAN_GROUP];
 #pragma unroll
-    for (int k = 0; k < SCAN_GROUP; k++) v[k] = k < ntl && __ldcg(c.w + int64_t(t0 + k) * TPIX + i) > 0;
+    for (int k = 0; k < SCAN_GROUP; k++) {
+        const int64_t p = int64_t(t0 + k) * TPIX + i;
+        v[k] = k < ntl && (__ldcg(c.w + p) > 0 || (nested && __ldcg(c.lab + p)));
+    }
 #pragma unroll
     for (int k = 0; k < SCAN_GROUP; k++)
         if (k < ntl) {
             c.lab[int64_t(t0 + k) * TPIX + i] = uint8_t(v[k]);
-            if (!swapped) scan_mark(k, v[k]);
+            if (!swapped) {
+                scan_mark(k, v[k]);
+                if (__any_sync(0xffffffffu, !v[k]) && (i & 31) == 0) atomicOr(&s_scan.sides[k], 16);
+            }
         }
-    if (!swapped) scan_flag(c, A, t0, ntl);
+    if (!swapped) scan_flag(c, A, t0, ntl, true);
 }
 
 // EMIT (k_emit + k_advance_tiles): label bytes (swapped grids: sink side
@@ -379,7 +396,7 @@ __global__ void __launch_bounds__(NTT, 2) k_async(Ctx c, AsyncArgs A) {
             switch (ph) {
             case PH_BINIT: binit_group(c, A, t, ntl); break;
             case PH_SEED: seed_group(c, A, t, ntl, g); break;
-            case PH_LINIT: linit_group(c, A, t, ntl, grid_swapped(c, gd)); break;
+            case PH_LINIT: linit_group(c, A, t, ntl, g, grid_swapped(c, gd)); break;
             default: emit_group(c, A, t, ntl, g); break;
             }
             stat = ph == PH_BINIT ? ST_BINIT : ph == PH_SEED ? ST_SEED : ph == PH_LINIT ? ST_LINIT : ST_EMIT;

@@ -381,6 +381,8 @@ __device__ __forceinline__ TileResult bfs_src_tile(const Ctx &c, int32_t t) {
     const TileNb g = tile_nbs(c, t);
     const int64_t p = int64_t(t) * TPIX + i;
     const uint8_t l0 = __ldcg(c.lab + p);
+    // a tile whose every pixel is already in the closure cannot change
+    if (__syncthreads_and(l0)) return TileResult{0, 0};
     typename E::Word wd = E::load(c.r, p);
     s_sd[ly * SP + lx] = l0 ? 0 : HINF;
     s_bits[i] = uint8_t((E::lane(wd, 0) > 0) | ((E::lane(wd, 1) > 0) << 1) | ((E::lane(wd, 2) > 0) << 2) |
