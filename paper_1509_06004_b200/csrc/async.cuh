@@ -62,6 +62,7 @@ struct AsyncArgs {
     unsigned budget_factor;
     int32_t max_cycles;
     int32_t cont;      // continuation hand-off between neighbouring tiles
+    int32_t prefetch;  // take the next ticket while the queue is deep
 };
 
 // ---- scan phases: one task = up to SCAN_GROUP consecutive tiles of a grid,
@@ -371,12 +372,22 @@ __global__ void __launch_bounds__(NTT, 2) k_async(Ctx c, AsyncArgs A) {
         s_cont = -1;
         atomicMin(&c.ctl->t0, gtimer());
     }
+    // ticket taken ahead while the queue is deep (its tile is then already
+    // queued, so holding it while this CTA works delays nobody)
+    unsigned pre = ~0u;
     for (;;) {
         if (i == 0) {
             const unsigned long long tw = gtimer();
             int32_t t = s_cont;
             s_cont = -1;
-            if (t < 0) t = q_next(c);
+            if (t < 0) {
+                t = pre != ~0u ? q_wait(c, pre) : q_next(c);
+                pre = ~0u;
+            }
+            if (t >= 0 && A.prefetch && pre == ~0u) {   // at most one ticket held
+                const unsigned hd = ld_volatile(&c.qctr[QC_HEAD]), tl = ld_volatile(&c.qctr[QC_TAIL]);
+                if (tl > hd && tl - hd > 2u * gridDim.x) pre = atomicAdd(&c.qctr[QC_HEAD], 1u);
+            }
             qfence();
             s_t = t;
             atomicAdd(&c.stat[ST_BUSY + BUSY_WAIT], gtimer() - tw);

@@ -215,7 +215,7 @@ struct pmf_solver {
     int async_mode = -1;        // seed batches: one persistent kernel, every grid on its own phase machine
                                 // (1), step-synchronous phases (0), or -1: async up to async_max_tiles tiles
     int async_max_tiles = 12000;
-    int async_cont = 1;
+    int async_cont = 1, async_prefetch = 1;
     double busy_ms[16] = {0};    // async: CTA-busy time per phase kind of the last run (diagnostics)
     int bfs_chunk = 8;
     int timing = 0;
@@ -1072,6 +1072,7 @@ int async_solve(pmf_solver *s, const Ctx &c0, const SeedArgs &sa) {
     A.budget_factor = unsigned(budget_factor(s));
     A.max_cycles = int32_t(std::min<int64_t>(s->max_cycles, 0x7fffffff));
     A.cont = s->async_cont;
+    A.prefetch = s->async_prefetch;
     CK(cudaMemsetAsync(c.ctl, 0, sizeof(Ctl), s->st));
     LAUNCH(s, (k_phase_begin<<<s->grid_full, 256, 0, s->st>>>(c, 1, 0, 0)));
     LAUNCH(s, (k_async_begin<<<s->grid_full, 256, 0, s->st>>>(c, A, int32_t(G))));
@@ -1498,6 +1499,7 @@ int pmf_solver_set(pmf_solver *s, const char *name, int64_t v) {
     else if (k == "async" && v >= -1 && v <= 1) s->async_mode = int(v);
     else if (k == "async_max_tiles" && v >= 0) s->async_max_tiles = int(std::min<int64_t>(v, 1 << 30));
     else if (k == "async_cont") s->async_cont = v != 0;
+    else if (k == "async_prefetch") s->async_prefetch = v != 0;
     else if (k == "graph") s->use_graph = v != 0;
     else if (k == "persistent_bfs") s->persistent_bfs = v != 0;
     else if (k == "bfs_multi") s->bfs_multi = v != 0;

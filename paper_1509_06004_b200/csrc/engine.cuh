@@ -217,13 +217,9 @@ __device__ __forceinline__ void q_finish(const Ctx &c, int32_t t, bool again) {
 // on a slot may take any tile that lands there, so tickets that alias a
 // slot (more waiters than ring slots) only reorder work.  Tickets taken
 // after the phase drained are discarded by the next k_phase_begin.
-__device__ __forceinline__ int32_t q_next(const Ctx &c) {
-    // device budget: 0 means "no discharge this cycle"; host budget 0: no cap
-    const unsigned budget = c.budget_dev ? *(volatile unsigned *)&c.ctl->budget : c.budget;
-    if (c.budget_dev && budget == 0) return -1;
-    if (budget && ld_volatile(&c.qctr[QC_HEAD]) + ld_volatile(&c.qctr[QC_CONT]) >= budget) return -1;
-    const unsigned hd = atomicAdd(&c.qctr[QC_HEAD], 1u);
-    if (budget && hd + ld_volatile(&c.qctr[QC_CONT]) >= budget) return -1;
+// Wait for the tile of ticket hd (a ring position), or -1 when the phase is
+// over (nothing queued or running).
+__device__ __forceinline__ int32_t q_wait(const Ctx &c, unsigned hd) {
     int32_t *slot = &c.ring[hd % unsigned(c.qcap)];
     for (;;) {
         if (*(volatile int32_t *)slot != -1) {
@@ -236,6 +232,16 @@ __device__ __forceinline__ int32_t q_next(const Ctx &c) {
         if (ld_volatile(&c.qctr[QC_PENDING]) == 0) return -1;
         __nanosleep(64);
     }
+}
+
+__device__ __forceinline__ int32_t q_next(const Ctx &c) {
+    // device budget: 0 means "no discharge this cycle"; host budget 0: no cap
+    const unsigned budget = c.budget_dev ? *(volatile unsigned *)&c.ctl->budget : c.budget;
+    if (c.budget_dev && budget == 0) return -1;
+    if (budget && ld_volatile(&c.qctr[QC_HEAD]) + ld_volatile(&c.qctr[QC_CONT]) >= budget) return -1;
+    const unsigned hd = atomicAdd(&c.qctr[QC_HEAD], 1u);
+    if (budget && hd + ld_volatile(&c.qctr[QC_CONT]) >= budget) return -1;
+    return q_wait(c, hd);
 }
 
 // Continuation: the CTA that just finished a tile takes an idle neighbour
