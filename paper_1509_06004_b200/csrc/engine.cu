@@ -11,6 +11,7 @@
 #include <condition_variable>
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 #include <sys/mman.h>
 #include <cstring>
 #include <functional>
@@ -1450,6 +1451,11 @@ int pmf_solver_create(int32_t device, pmf_solver **out) {
     s->sms = prop.multiProcessorCount;
     {
         unsigned hc = std::thread::hardware_concurrency();
+        // one process per GPU (torchrun): share the host cores between the local ranks
+        if (const char *lw = getenv("LOCAL_WORLD_SIZE")) {
+            const int n = atoi(lw);
+            if (n > 1) hc = std::max(1u, hc / unsigned(n));
+        }
         s->pool = new Pool();
         s->pool->threads = int(std::max(1u, std::min(hc ? hc : 1u, 16u)));
     }
