@@ -1038,12 +1038,15 @@ int grids_for(pmf_solver *s) {
 // emitted mask on the original graph == its flow
 int launch_verify(pmf_solver *s, const Ctx &c, const SeedArgs &a) {
     const int64_t planes = int64_t(a.nprob) * a.nlam, n = int64_t(a.W) * a.H;
-    const int chunks = int(std::max<int64_t>(1, std::min<int64_t>(cdiv(n, 16384), 1024)));
+    // (problem, chunk) CTAs: ~4 rounds of NT * VPX pixels each
+    const int64_t want = std::max<int64_t>(cdiv(n, int64_t(NT) * VPX * 4), cdiv(4 * s->sms, a.nprob));
+    const int chunks = int(std::max<int64_t>(1, std::min<int64_t>({want, cdiv(n, int64_t(NT) * VPX), 4096})));
     int rc;
     if ((rc = s->d_vacc.ensure(size_t(planes) * 8))) return rc;
     CK(cudaMemsetAsync(s->d_vacc.p, 0, size_t(planes) * 8, s->st));
     unsigned long long *acc = s->d_vacc.as<unsigned long long>();
-    LAUNCH(s, (k_verify<<<int(std::min<int64_t>(planes * chunks, 32 * s->sms)), NT, 0, s->st>>>(c, a, acc, chunks)));
+    LAUNCH(s, (k_verify<<<int(std::min<int64_t>(int64_t(a.nprob) * chunks, 32 * s->sms)), NT, 0, s->st>>>(
+                   c, a, acc, chunks)));
     LAUNCH(s, (k_verify_check<<<int(std::max<int64_t>(1, std::min<int64_t>(cdiv(planes, 256), 1024))), 256, 0, s->st>>>(
                    c, planes, acc)));
     CK(cudaGetLastError());

@@ -449,37 +449,65 @@ __global__ void __launch_bounds__(NT) k_advance_tiles(Ctx c, SeedArgs a) {
 // the reference checks it in split(), supergraph.py:181-186, and in the RPC
 // client, rpc.py:328-331): the cut cost of the emitted mask of the ORIGINAL
 // graph must equal the flow.  One CTA per (problem, lambda) plane.
-// One CTA per (plane, chunk of pixels); partial cut costs summed per plane
-// into acc (zeroed by the caller), compared with the flows by k_verify_check.
+// One CTA per (problem, chunk of pixels): the problem's planes are read
+// once for all its lambdas (the per-plane pass re-read them nlam times and
+// was bandwidth-bound at ~10 ms per 8-image batch); partial cut costs are
+// summed per (problem, lambda) into acc (zeroed by the caller) and compared
+// with the flows by k_verify_check.
+constexpr int VPX = 4;     // pixels per thread per round
+constexpr int VLAM = 24;   // lambdas per pass over the problem's planes (register accumulators)
 __global__ void __launch_bounds__(NT) k_verify(Ctx c, SeedArgs a, unsigned long long *acc, int chunks) {
-    __shared__ int64_t red[NT / 32];
+    __shared__ unsigned long long s_acc[VLAM];
     const int64_t n = int64_t(a.W) * a.H;
     const int64_t per = (n + chunks - 1) / chunks;
-    for (int64_t blk = blockIdx.x; blk < int64_t(a.nprob) * a.nlam * chunks; blk += gridDim.x) {
-        const int64_t plane = blk / chunks;
+    for (int64_t blk = blockIdx.x; blk < int64_t(a.nprob) * chunks; blk += gridDim.x) {
+        const int p = int(blk / chunks);
         const int64_t lo = (blk % chunks) * per, hi = min(n, lo + per);
-        const int p = int(plane / a.nlam), j = int(plane % a.nlam);
-        const int64_t lam = a.lambdas[j];
-        const uint8_t *lab = c.out + plane * n;
         const int64_t po = a.plane_off[p];
         const int32_t *pw = a.pw + a.pw_off[p];
-        int64_t cost = 0;
-        for (int64_t q = lo + threadIdx.x; q < hi; q += NT) {
-            const uint8_t m = a.mask[int64_t(p) * n + q];
-            const int x = int(q % a.W), y = int(q / a.W);
-            if (lab[q]) {
-                cost += m == 2 ? CAP_MAX : int64_t(a.sink[po + q]);
-                // arcs leaving the source side (off-grid counts as source side)
-                if (x > 0 && !lab[q - 1]) cost += pw[0 * n + q];
-                if (x + 1 < a.W && !lab[q + 1]) cost += pw[1 * n + q];
-                if (y > 0 && !lab[q - a.W]) cost += pw[2 * n + q];
-                if (y + 1 < a.H && !lab[q + a.W]) cost += pw[3 * n + q];
-            } else {
-                cost += m == 1 ? CAP_MAX : int64_t(a.base[po + q]) + lam * int64_t(a.slope[po + q]);
+        const uint8_t *mask = a.mask + int64_t(p) * n;
+        for (int j0 = 0; j0 < a.nlam; j0 += VLAM) {
+            int64_t cost[VLAM];
+#pragma unroll
+            for (int jj = 0; jj < VLAM; jj++) cost[jj] = 0;
+            if (threadIdx.x < VLAM) s_acc[threadIdx.x] = 0;
+            for (int64_t q0 = lo; q0 < hi; q0 += int64_t(NT) * VPX) {
+#pragma unroll
+                for (int k = 0; k < VPX; k++) {
+                    const int64_t q = q0 + threadIdx.x + int64_t(k) * NT;
+                    if (q >= hi) continue;
+                    const uint8_t m = mask[q];
+                    const int64_t bs = a.base[po + q], sl = a.slope[po + q], sk = m == 2 ? CAP_MAX : a.sink[po + q];
+                    const int x = int(q % a.W), y = int(q / a.W);
+                    const int32_t a0 = x > 0 ? pw[q] : 0, a1 = x + 1 < a.W ? pw[n + q] : 0;
+                    const int32_t a2 = y > 0 ? pw[2 * n + q] : 0, a3 = y + 1 < a.H ? pw[3 * n + q] : 0;
+                    const uint8_t *lab = c.out + (int64_t(p) * a.nlam + j0) * n + q;
+#pragma unroll
+                    for (int jj = 0; jj < VLAM; jj++) {
+                        if (j0 + jj >= a.nlam) break;
+                        const uint8_t *l = lab + int64_t(jj) * n;
+                        if (*l) {
+                            // arcs leaving the source side (off-grid counts as source side)
+                            cost[jj] += sk + (a0 && !l[-1] ? a0 : 0) + (a1 && !l[1] ? a1 : 0) +
+                                        (a2 && !l[-a.W] ? a2 : 0) + (a3 && !l[a.W] ? a3 : 0);
+                        } else {
+                            cost[jj] += m == 1 ? CAP_MAX : bs + a.lambdas[j0 + jj] * sl;
+                        }
+                    }
+                }
             }
+            __syncthreads();
+#pragma unroll
+            for (int jj = 0; jj < VLAM; jj++) {
+                int64_t v = cost[jj];
+                for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+                if ((threadIdx.x & 31) == 0 && v) atomicAdd(&s_acc[jj], (unsigned long long)v);
+            }
+            __syncthreads();
+            if (threadIdx.x < VLAM && j0 + int(threadIdx.x) < a.nlam && s_acc[threadIdx.x])
+                atomicAdd(acc + int64_t(p) * a.nlam + j0 + threadIdx.x, s_acc[threadIdx.x]);
+            __syncthreads();
         }
-        const int64_t tot = block_sum64(cost, red);
-        if (threadIdx.x == 0 && tot) atomicAdd(acc + plane, (unsigned long long)tot);
     }
 }
 
