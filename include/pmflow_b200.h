@@ -197,6 +197,11 @@ int pmf_debug_trace(pmf_solver *s, int32_t *kind, double *us, double *start_us, 
  * queue wait, hand-off, grid transitions; out16 holds 16 doubles. */
 int pmf_debug_busy(pmf_solver *s, double *out16);
 
+/* Diagnostics: phase timeline of grid g of the last asynchronous run made
+ * with knob phase_log = 1: up to *n entries, phase << 56 | globaltimer ns;
+ * *n is updated to the number returned. */
+int pmf_debug_phases(pmf_solver *s, int64_t g, uint64_t *out, int32_t *n);
+
 /* Diagnostics: copy the tile-major device state of the last run (w, h,
  * residual words, source-side flags; any pointer may be NULL) and the tile
  * count.  Buffers hold ntiles*1024 entries (r: edge_bytes each). */

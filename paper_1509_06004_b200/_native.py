@@ -24,7 +24,7 @@ SWAP_MODES = {"auto": 0, "on": 1, "off": 2}
 EXPORTS = ("pmf_solver_create", "pmf_solver_destroy", "pmf_solver_set", "pmf_last_error",
            "pmf_solver_stats", "pmf_solver_stream", "pmf_solve_composites", "pmf_solve_seed_batch",
            "pmf_seed_stage", "pmf_seed_run", "pmf_seed_fetch", "pmf_debug_state",
-           "pmf_debug_trace", "pmf_debug_busy", "pmf_seed_score")
+           "pmf_debug_trace", "pmf_debug_busy", "pmf_seed_score", "pmf_debug_phases")
 
 
 class NativeUnavailable(RuntimeError):
@@ -85,6 +85,7 @@ def load_library(path: str = LIB_PATH):
         lib.pmf_debug_state.argtypes = [vp, vp, vp, vp, vp, P(i64)]
         lib.pmf_debug_trace.argtypes = [vp, vp, vp, vp, vp, P(i32)]
         lib.pmf_debug_busy.argtypes = [vp, P(ctypes.c_double)]
+        lib.pmf_debug_phases.argtypes = [vp, i64, P(ctypes.c_uint64), P(i32)]
         lib.pmf_seed_score.argtypes = [vp, P(vp), P(i64), P(i64), P(i64)]
         for name in EXPORTS:
             if name != "pmf_last_error":
@@ -220,6 +221,20 @@ class Solver:
         d["relax_calls"] = int(out[14])
         d["relax_sweeps"] = int(out[12])
         return d
+
+    def phases(self, grid: int):
+        """Phase timeline [(phase name, us since the first entry)] of one grid
+        of the last asynchronous run (knob phase_log=1)."""
+        out = np.zeros(128, np.uint64)
+        n = ctypes.c_int32(128)
+        rc = self._lib.pmf_debug_phases(self._h, grid, out.ctypes.data_as(ctypes.POINTER(ctypes.c_uint64)),
+                                        ctypes.byref(n))
+        if rc:
+            _raise_for(rc)
+        names = ("binit", "bfs", "seed", "push", "linit", "lab", "emit", "done")
+        v = out[:n.value]
+        ts = (v & np.uint64((1 << 56) - 1)).astype(np.int64)
+        return [(names[int(x >> np.uint64(56))], round(float(t - ts[0]) / 1e3, 1)) for x, t in zip(v, ts)]
 
     def stream_handle(self) -> int:
         """The solver's cudaStream_t as an integer (torch.cuda.ExternalStream)."""

@@ -63,7 +63,9 @@ struct AsyncArgs {
     int32_t max_cycles;
     int32_t cont;      // continuation hand-off between neighbouring tiles
     int32_t prefetch;  // take the next ticket while the queue is deep
+    unsigned long long *plog;   // diagnostics (nullable): per grid PLOG entries (phase << 56 | globaltimer)
 };
+constexpr int PLOG = 128;
 
 // ---- scan phases: one task = up to SCAN_GROUP consecutive tiles of a grid,
 // all processed at once (SCAN_GROUP pixels per thread, loads issued
@@ -297,6 +299,14 @@ __device__ void grid_transition(const Ctx &c, const AsyncArgs &A, int32_t g, int
         if (next == PH_DONE) {
             if (threadIdx.x == 0) {
                 R.phase = PH_DONE;
+                if (A.plog) {
+                    unsigned long long *lg = A.plog + int64_t(g) * PLOG;
+                    const unsigned long long k = lg[0];
+                    if (k + 1 < PLOG) {
+                        lg[k + 1] = (unsigned long long)PH_DONE << 56 | (gtimer() & ((1ull << 56) - 1));
+                        lg[0] = k + 1;
+                    }
+                }
                 qfence();
             }
             __syncthreads();
@@ -319,6 +329,14 @@ __device__ void grid_transition(const Ctx &c, const AsyncArgs &A, int32_t g, int
             if (next == PH_PUSH)   // pop budget: factor x seeded tiles (k_cycle_ctl)
                 R.budget = A.budget_factor ? int32_t(A.budget_factor) * cnt + 64 : 0x7fffffff;
             R.phase = next;
+            if (A.plog) {   // diagnostics: phase timeline of the grid
+                unsigned long long *lg = A.plog + int64_t(g) * PLOG;
+                const unsigned long long k = lg[0];
+                if (k + 1 < PLOG) {
+                    lg[k + 1] = (unsigned long long)next << 56 | (gtimer() & ((1ull << 56) - 1));
+                    lg[0] = k + 1;
+                }
+            }
             // hold the phase open while its tiles are being queued: a tile
             // popped and retired meanwhile must not see the count reach zero
             atomicAdd(&c.gpend[g], 1);

@@ -217,12 +217,14 @@ struct pmf_solver {
                                 // (1), step-synchronous phases (0), or -1: async up to async_max_tiles tiles
     int async_max_tiles = 12000;
     int async_cont = 1, async_prefetch = 1;
+    int phase_log = 0;          // diagnostics: record every grid's phase timeline (async)
+    int64_t plog_grids = 0;
     double busy_ms[16] = {0};    // async: CTA-busy time per phase kind of the last run (diagnostics)
     int bfs_chunk = 8;
     int timing = 0;
     int64_t max_cycles = 50000;
     // device workspace
-    DevBuf d_w, d_h, d_r, d_lab, d_tile_grid, d_tnb, d_fin, d_gpend, d_gr, d_tflag, d_vacc, d_truth, d_score, d_grids, d_live, d_act, d_list, d_inq, d_cnt,
+    DevBuf d_w, d_h, d_r, d_lab, d_tile_grid, d_tnb, d_fin, d_gpend, d_gr, d_tflag, d_vacc, d_truth, d_score, d_plog, d_grids, d_live, d_act, d_list, d_inq, d_cnt,
         d_snk, d_drain, d_err, d_stat, d_colswap, d_out, d_bits, d_in32, d_pw, d_mask, d_off, d_lam,
         d_swapcnt, d_swapflag, d_ring, d_qstate, d_qctr, d_ctl, d_curlam, d_flows, d_slopesum;
     HostBuf h_in32, h_pw, h_mask, h_out, h_small;
@@ -1077,6 +1079,12 @@ int async_solve(pmf_solver *s, const Ctx &c0, const SeedArgs &sa) {
     A.max_cycles = int32_t(std::min<int64_t>(s->max_cycles, 0x7fffffff));
     A.cont = s->async_cont;
     A.prefetch = s->async_prefetch;
+    if (s->phase_log) {
+        if ((rc = s->d_plog.ensure(size_t(G) * PLOG * 8))) return rc;
+        CK(cudaMemsetAsync(s->d_plog.p, 0, size_t(G) * PLOG * 8, s->st));
+        A.plog = s->d_plog.as<unsigned long long>();
+        s->plog_grids = G;
+    }
     CK(cudaMemsetAsync(c.ctl, 0, sizeof(Ctl), s->st));
     LAUNCH(s, (k_phase_begin<<<s->grid_full, 256, 0, s->st>>>(c, 1, 0, 0)));
     LAUNCH(s, (k_async_begin<<<s->grid_full, 256, 0, s->st>>>(c, A, int32_t(G))));
@@ -1509,6 +1517,7 @@ int pmf_solver_set(pmf_solver *s, const char *name, int64_t v) {
     else if (k == "async_max_tiles" && v >= 0) s->async_max_tiles = int(std::min<int64_t>(v, 1 << 30));
     else if (k == "async_cont") s->async_cont = v != 0;
     else if (k == "async_prefetch") s->async_prefetch = v != 0;
+    else if (k == "phase_log") s->phase_log = v != 0;
     else if (k == "graph") s->use_graph = v != 0;
     else if (k == "persistent_bfs") s->persistent_bfs = v != 0;
     else if (k == "bfs_multi") s->bfs_multi = v != 0;
@@ -1639,6 +1648,19 @@ int pmf_solve_composites(pmf_solver *s, int32_t ncomp, const int32_t *width, con
 int pmf_debug_busy(pmf_solver *s, double *out16) {
     if (!s || !out16) return fail(PMF_ERR_ARG, "null argument");
     for (int k = 0; k < 16; k++) out16[k] = s->busy_ms[k];
+    return 0;
+}
+
+// Phase timeline of grid g of the last asynchronous run with knob
+// phase_log = 1: up to PLOG - 1 entries (phase << 56 | globaltimer ns).
+int pmf_debug_phases(pmf_solver *s, int64_t g, uint64_t *out, int32_t *n) {
+    if (!s || !out || !n) return fail(PMF_ERR_ARG, "null argument");
+    if (g < 0 || g >= s->plog_grids) return fail(PMF_ERR_ARG, "no phase log for grid %lld", (long long)g);
+    uint64_t buf[PLOG];
+    CK(cudaMemcpy(buf, s->d_plog.as<unsigned long long>() + g * PLOG, sizeof buf, cudaMemcpyDeviceToHost));
+    const int k = int(std::min<uint64_t>(buf[0], uint64_t(PLOG - 1)));
+    *n = std::min(*n, k);
+    for (int j = 0; j < *n; j++) out[j] = buf[j + 1];
     return 0;
 }
 
