@@ -398,3 +398,32 @@ def test_device_scoring_matches_reference():
             assert cut.flow == rec["flows"][j]
             assert sc.foreground == rec["foreground"][j] == int(cut.labels.sum())
             assert sc.overlap == Fraction(*rec["overlap"][j]) == overlap(cut.labels, b.truths[pi])
+
+
+def test_run_dynamic_on_gpu_backend():
+    """scheduler.py:253-292 policy over the GPU backend (one executor per
+    device, queued tasks coalesced into device batches): composite tasks and
+    device-built seed-supergraph tasks in one run give the same cuts as the
+    direct calls, which are pinned to the reference elsewhere."""
+    from paper_1509_06004_b200 import GpuBackend, Task, gpu_workers, run_dynamic
+    b = synth.generate(160, 120, 2, 2, rng_seed=1)
+    sched = LambdaSchedule(synth.L20[:6])
+    tasks = []
+    for i, p in enumerate(b.problems):
+        comp, layout, _ = build_seed_supergraph([p], sched, "auto")
+        tasks.append(Task(id=2 * i, graph=comp, layout=layout, duration=comp.n))
+        tasks.append(Task(id=2 * i + 1, problems=(p,), schedule=sched))
+    backend = GpuBackend(max_batch=3)
+    try:
+        schedule, cuts = run_dynamic(tasks, gpu_workers([0], slots=3), backend)
+    finally:
+        backend.close()
+    assert sorted(r.task_id for r in schedule.records) == [t.id for t in tasks]
+    for i, p in enumerate(b.problems):
+        comp, layout, originals = build_seed_supergraph([p], sched, "auto")
+        direct = solve_composite(comp, layout)
+        assert cuts[2 * i].flow == direct.flow and np.array_equal(cuts[2 * i].labels, direct.labels)
+        parts = split(layout, direct, originals)
+        dev = cuts[2 * i + 1]
+        assert [c.flow for c in dev.cuts] == [c.flow for c in parts]
+        assert all(np.array_equal(a.labels, c.labels) for a, c in zip(dev.cuts, parts))
