@@ -60,6 +60,7 @@ struct AsyncArgs {
     uint8_t *tflag;    // per tile: listed for the next flagged phase
     int iters, relabel_every, relax_cap;
     unsigned budget_factor;
+    int32_t budget_add;    // discharge pop budget: factor x seeded tiles + this
     int32_t max_cycles;
     int32_t cont;      // continuation hand-off between neighbouring tiles
     int32_t prefetch;  // take the next ticket while the queue is deep
@@ -327,7 +328,7 @@ __device__ void grid_transition(const Ctx &c, const AsyncArgs &A, int32_t g, int
         }
         if (threadIdx.x == 0) {
             if (next == PH_PUSH)   // pop budget: factor x seeded tiles (k_cycle_ctl)
-                R.budget = A.budget_factor ? int32_t(A.budget_factor) * cnt + 64 : 0x7fffffff;
+                R.budget = A.budget_factor ? int32_t(A.budget_factor) * cnt + A.budget_add : 0x7fffffff;
             R.phase = next;
             if (A.plog) {   // diagnostics: phase timeline of the grid
                 unsigned long long *lg = A.plog + int64_t(g) * PLOG;

@@ -208,6 +208,7 @@ struct pmf_solver {
     int relax_cap = 0;        // sweep cap of the discharge's local relabel (0: to the fixpoint)
     int warm_min_problems = 8;  // auto: one chain per problem (whole ladder) from this many problems
     int push_budget_warm = 4;   // discharge budget factor when the batch runs warm-start chains
+    int push_budget_add = 64;   // asynchronous solver: + this many pops per discharge phase
     int verify = 1;             // seed batches: device cut_cost == flow certificate per cut
     int rolling = 1;            // warm-start chains advance per grid as each finishes (no step barrier)
     int push_minb = 2;          // CTA discharge: min CTAs per SM of its launch bounds (1 or 2)
@@ -1076,6 +1077,7 @@ int async_solve(pmf_solver *s, const Ctx &c0, const SeedArgs &sa) {
     A.relabel_every = s->relabel_every;
     A.relax_cap = s->relax_cap;
     A.budget_factor = unsigned(budget_factor(s));
+    A.budget_add = s->push_budget_add;
     A.max_cycles = int32_t(std::min<int64_t>(s->max_cycles, 0x7fffffff));
     A.cont = s->async_cont;
     A.prefetch = s->async_prefetch;
@@ -1508,6 +1510,7 @@ int pmf_solver_set(pmf_solver *s, const char *name, int64_t v) {
     else if (k == "relax_cap" && v >= 0 && v <= 1000) s->relax_cap = int(v);
     else if (k == "warm_min_problems" && v >= 1) s->warm_min_problems = int(v);
     else if (k == "push_budget_warm" && v >= 0) s->push_budget_warm = int(v);
+    else if (k == "push_budget_add" && v >= 0 && v < (int64_t(1) << 30)) s->push_budget_add = int(v);
     else if (k == "verify") s->verify = v != 0;
     else if (k == "rolling") s->rolling = v != 0;
     else if (k == "push_minb" && (v == 1 || v == 2)) s->push_minb = int(v);
