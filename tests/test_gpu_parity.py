@@ -427,3 +427,42 @@ def test_run_dynamic_on_gpu_backend():
         dev = cuts[2 * i + 1]
         assert [c.flow for c in dev.cuts] == [c.flow for c in parts]
         assert all(np.array_equal(a.labels, c.labels) for a, c in zip(dev.cuts, parts))
+
+
+@pytest.mark.parametrize("mode", [1, 0])
+def test_seed_batches_on_edge_shapes(engine, mode):
+    """Seed batches through the device builder on odd shapes (1xN, Nx1,
+    tiles straddling 32-px boundaries), warm chains and cold grids, both
+    schedulers (mode 1: asynchronous kernel, 0: step-synchronous), against
+    the oracle's restatement of the reference solver per (problem, lambda)."""
+    from paper_1509_06004_b200 import _native
+    rng = np.random.default_rng(11)
+    lams = [1, 3, 8, 20]
+    for (w, h) in [(1, 7), (9, 1), (33, 2), (31, 33), (65, 34)]:
+        n = w * h
+        probs = []
+        for k in range(9):   # >= warm_min_problems: warm-start chains
+            nb = rng.integers(1, 20, (4, h, w))
+            nb[0][:, 0] = 0
+            nb[1][:, -1] = 0
+            nb[2][0, :] = 0
+            nb[3][-1, :] = 0
+            fg = {int(rng.integers(0, n))}
+            bg = {int(x) for x in rng.integers(0, n, 2)} - fg
+            probs.append(SeedProblem(w, h, rng.integers(0, 10, n), rng.integers(0, 4, n),
+                                     rng.integers(0, 25, n), nb.reshape(4, n), fg, bg))
+        for chain in (0, 1):
+            s = _native.Solver(0, chain=chain, **{"async": mode})
+            try:
+                sw, flows, labels = s.solve_seed_batch(w, h, probs, lams, "auto")
+            finally:
+                s.close()
+            for pi, p in enumerate(probs):
+                for li, lam in enumerate(lams):
+                    src, snk, nbr = oracle.instantiate(p.unary_base, p.unary_slope, p.sink_base, p.pairwise,
+                                                       p.fg_seeds, p.bg_seeds, lam)
+                    # swapped families decode to the original graph's cut
+                    # (swap invariance, test_acceptance.py:79-87)
+                    f, lab, _ = oracle.solve(w, h, src, snk, nbr)
+                    assert int(flows[pi, li]) == f, (w, h, chain, pi, lam)
+                    assert np.array_equal(labels[pi, li], lab), (w, h, chain, pi, lam)
