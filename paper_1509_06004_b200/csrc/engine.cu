@@ -213,6 +213,7 @@ struct pmf_solver {
     int rolling = 1;            // warm-start chains advance per grid as each finishes (no step barrier)
     int push_minb = 2;          // CTA discharge: min CTAs per SM of its launch bounds (1 or 2)
     int push_mode = 0;          // discharge body: 0 two CTA barriers per iteration, 1 one
+    int push_flush = 0;         // discharge: hand border inflow over every this many iterations (0 off; queue modes)
     int grid_div = 1;           // use 1/grid_div of the GPU's resident CTAs (solvers sharing a GPU)
     int async_mode = -1;        // seed batches: one persistent kernel, every grid on its own phase machine
                                 // (1), step-synchronous phases (0), or -1: async up to async_max_tiles tiles
@@ -321,6 +322,7 @@ int setup_state(pmf_solver *s, int edge_bytes) {
     x.live = s->d_live.as<int32_t>();
     x.fin = s->d_fin.as<int32_t>();
     x.push_mode = s->push_mode;
+    x.push_flush = s->push_flush;
     x.gpend = s->d_gpend.as<int32_t>();
     x.ngrids = int32_t(G);
     x.rolling = 0;
@@ -1516,6 +1518,7 @@ int pmf_solver_set(pmf_solver *s, const char *name, int64_t v) {
     else if (k == "push_minb" && (v == 1 || v == 2)) s->push_minb = int(v);
     else if (k == "grid_div" && v >= 1 && v <= 64) s->grid_div = int(v);
     else if (k == "push_mode" && (v == 0 || v == 1)) s->push_mode = int(v);
+    else if (k == "push_flush" && v >= 0 && v <= 1024) s->push_flush = int(v);
     else if (k == "async" && v >= -1 && v <= 1) s->async_mode = int(v);
     else if (k == "async_max_tiles" && v >= 0) s->async_max_tiles = int(std::min<int64_t>(v, 1 << 30));
     else if (k == "async_cont") s->async_cont = v != 0;

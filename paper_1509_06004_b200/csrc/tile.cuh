@@ -467,6 +467,55 @@ __device__ __forceinline__ void push_prepare() {
     if (threadIdx.x < 2 * (TH + 2)) (&s_rowin[0][0])[threadIdx.x] = 0;
 }
 
+// Mid-pass hand-off (knob push_flush, queue modes): flow pushed across the
+// tile border so far is applied to the neighbour tiles now and they are
+// requested, so they start while this pass goes on, instead of one pass
+// (up to `iters` iterations) later.  The border pixels' own deltas are
+// written first, so a u8 residual lane never holds the neighbour's
+// increment on top of a decrement not yet applied (each side only ever
+// adds what it may); w0 / rv0 advance so the final write-back adds only
+// what follows.
+__shared__ int s_flush;
+template <class E>
+__device__ __forceinline__ void push_flush(const Ctx &c, int32_t t, int64_t p, int i, int32_t e, int32_t h,
+                                           const int32_t *r, int32_t &w0, typename E::Word &rv0) {
+    int pending = 0;
+    if (i < 4 * TW) {
+        const int s = i / TW, j = i % TW;
+        pending = s_in[0][opp(s)][ring_index(s, j)] > 0;
+    }
+    if (i == 0) s_flush = 0;
+    if (!__syncthreads_or(pending)) return;
+    if (on_border(i)) {
+        const typename E::Word rv = E::pack(r[0], r[1], r[2], r[3]);
+        if (e != w0) atomicAdd(&c.w[p], e - w0);
+        E::store_delta(c.r, p, rv, rv0);
+        c.h[p] = h;
+        w0 = e;
+        rv0 = rv;
+    }
+    __syncthreads();
+    if (i < 4 * TW) {
+        const int s = i / TW, j = i % TW;
+        int32_t *slot = &s_in[0][opp(s)][ring_index(s, j)];
+        const int32_t a = *slot;
+        if (a > 0) {
+            *slot = 0;
+            const int64_t qn = int64_t(tile_nb(c, t, s)) * TPIX + halo_index(s, j);
+            atomicAdd(&c.w[qn], a);
+            E::add(c.r, qn, opp(s), a);
+            atomicOr(&s_flush, 1 << s);
+        }
+    }
+    qfence();   // requester side: data writes < queue-state RMWs
+    __syncthreads();
+    if (i >= 1 && i <= 4 && ((s_flush >> (i - 1)) & 1)) {
+        const int32_t nb = tile_nb(c, t, i - 1);
+        if (nb >= 0) q_request(c, nb);
+    }
+    __syncthreads();
+}
+
 template <class E>
 __device__ __forceinline__ TileResult push_tile(const Ctx &c, int32_t t, int iters, int relabel_every,
                                                 int relax_cap) {
@@ -474,8 +523,8 @@ __device__ __forceinline__ TileResult push_tile(const Ctx &c, int32_t t, int ite
     const int i = threadIdx.x, lx = i & 31, ly = i >> 5, pi = ly * SP + lx;
     const int q = (ly + 1) * RW + lx + 1;
     const int64_t p = int64_t(t) * TPIX + i;
-    const int32_t w0 = __ldcg(c.w + p);
-    const typename E::Word rv0 = E::load(c.r, p);
+    int32_t w0 = __ldcg(c.w + p);
+    typename E::Word rv0 = E::load(c.r, p);
     int32_t e = w0, h = __ldcg(c.h + p);
     int32_t r[4];
 #pragma unroll
@@ -492,6 +541,8 @@ __device__ __forceinline__ TileResult push_tile(const Ctx &c, int32_t t, int ite
     int until_relabel = 0, its = 0;
     for (int it = 0; it < iters; it++) {
         its++;
+        if (c.push_flush && it > 0 && it % c.push_flush == 0 && c.persistent)
+            push_flush<E>(c, t, p, i, e, h, r, w0, rv0);
         if (relabel_every && until_relabel == 0) {
             until_relabel = relabel_every;
             // exact local relabel (frozen pixels stay frozen)

@@ -368,16 +368,18 @@ def test_async_solver_matches_step_synchronous_under_load(engine):
         probs += synth.generate(500, 375, 5, 5, rng_seed=i, types=("A", "B")).problems
     sync = _native.Solver(0, **{"async": 0})
     asy = _native.Solver(0, **{"async": 1})
+    flush = _native.Solver(0, **{"async": 1}, push_flush=8)   # mid-pass hand-off variant
     try:
         _, fs, ls = sync.solve_seed_batch(500, 375, probs, synth.L20, "auto")
-        for _ in range(2):
-            _, fa, la = asy.solve_seed_batch(500, 375, probs, synth.L20, "auto")
-            assert asy.stats()["async_mode"] == 1
+        for s in (asy, asy, flush):
+            _, fa, la = s.solve_seed_batch(500, 375, probs, synth.L20, "auto")
+            assert s.stats()["async_mode"] == 1
             assert np.array_equal(fa, fs)
             assert np.array_equal(la, ls)
     finally:
         sync.close()
         asy.close()
+        flush.close()
 
 
 def test_device_scoring_matches_reference():
