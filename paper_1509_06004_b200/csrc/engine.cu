@@ -947,7 +947,7 @@ int run_end(pmf_solver *s) {
     // the fixed per-cycle kernels (2 x phase_begin, gr_init, seed_push,
     // cycle_ctl), the label tail (phase_begin, lab_seed, emit) and the
     // build kernels (host-launched, counted in stats.launches)
-    if (s->use_graph)
+    if (s->use_graph && !s->stats.async_mode)
         s->stats.kernels = int64_t(st[ST_PUSH_L] + st[ST_BFS_L] + st[ST_LAB_L]) + 5 * int64_t(ctl.cycles_total) +
                            7 * int64_t(std::max(1, ctl.steps)) + (s->stats.launches - 1);
     else
