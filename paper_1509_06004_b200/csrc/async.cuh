@@ -152,6 +152,7 @@ __device__ __forceinline__ void seed_group(const Ctx &c, const AsyncArgs &A, int
     if (i < ntl && s_scan.any[i]) {
         atomicAdd(&A.gr[g].act, s_scan.any[i]);
         A.tflag[t0 + i] = 1;
+        if (c.tfresh) c.tfresh[t0 + i] = 1;   // its heights are this relabel's exact distances
     }
 }
 

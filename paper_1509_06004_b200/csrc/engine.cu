@@ -213,6 +213,7 @@ struct pmf_solver {
     int rolling = 1;            // warm-start chains advance per grid as each finishes (no step barrier)
     int push_minb = 2;          // CTA discharge: min CTAs per SM of its launch bounds (1 or 2)
     int push_mode = 0;          // discharge body: 0 two CTA barriers per iteration, 1 one
+    int fresh_skip = 1;         // first discharge pass after an exact relabel skips its local relabel
     int push_flush = 0;         // discharge: hand border inflow over every this many iterations (0 off; queue modes)
     int grid_div = 1;           // use 1/grid_div of the GPU's resident CTAs (solvers sharing a GPU)
     int async_mode = -1;        // seed batches: one persistent kernel, every grid on its own phase machine
@@ -226,7 +227,7 @@ struct pmf_solver {
     int timing = 0;
     int64_t max_cycles = 50000;
     // device workspace
-    DevBuf d_w, d_h, d_r, d_lab, d_tile_grid, d_tnb, d_fin, d_gpend, d_gr, d_tflag, d_vacc, d_truth, d_score, d_plog, d_grids, d_live, d_act, d_list, d_inq, d_cnt,
+    DevBuf d_w, d_h, d_r, d_lab, d_tile_grid, d_tnb, d_fin, d_gpend, d_gr, d_tflag, d_vacc, d_truth, d_score, d_plog, d_tfresh, d_grids, d_live, d_act, d_list, d_inq, d_cnt,
         d_snk, d_drain, d_err, d_stat, d_colswap, d_out, d_bits, d_in32, d_pw, d_mask, d_off, d_lam,
         d_swapcnt, d_swapflag, d_ring, d_qstate, d_qctr, d_ctl, d_curlam, d_flows, d_slopesum;
     HostBuf h_in32, h_pw, h_mask, h_out, h_small;
@@ -323,6 +324,12 @@ int setup_state(pmf_solver *s, int edge_bytes) {
     x.fin = s->d_fin.as<int32_t>();
     x.push_mode = s->push_mode;
     x.push_flush = s->push_flush;
+    x.tfresh = nullptr;
+    if (s->fresh_skip) {
+        if ((rc = s->d_tfresh.ensure(size_t(T)))) return rc;
+        CK(cudaMemsetAsync(s->d_tfresh.p, 0, size_t(T), s->st));
+        x.tfresh = s->d_tfresh.as<uint8_t>();
+    }
     x.gpend = s->d_gpend.as<int32_t>();
     x.ngrids = int32_t(G);
     x.rolling = 0;
@@ -1519,6 +1526,7 @@ int pmf_solver_set(pmf_solver *s, const char *name, int64_t v) {
     else if (k == "grid_div" && v >= 1 && v <= 64) s->grid_div = int(v);
     else if (k == "push_mode" && (v == 0 || v == 1)) s->push_mode = int(v);
     else if (k == "push_flush" && v >= 0 && v <= 1024) s->push_flush = int(v);
+    else if (k == "fresh_skip") s->fresh_skip = v != 0;
     else if (k == "async" && v >= -1 && v <= 1) s->async_mode = int(v);
     else if (k == "async_max_tiles" && v >= 0) s->async_max_tiles = int(std::min<int64_t>(v, 1 << 30));
     else if (k == "async_cont") s->async_cont = v != 0;

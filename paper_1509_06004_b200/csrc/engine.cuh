@@ -118,6 +118,8 @@ struct Ctx {
     int32_t ngrids;
     int32_t rolling;        // rolling warm start: grids emit and advance as they finish
     int32_t push_mode;      // discharge body: 0 two barriers per iteration, 1 one (double-buffered inflow)
+    uint8_t *tfresh;        // per tile: heights are exact from the last relabel (first discharge
+                            // pass skips its local relabel, a no-op then); nullptr: off
     int32_t push_flush;     // discharge: hand border inflow to the neighbours every this many iterations (0 off)
     int32_t *act;           // per grid active-pixel count of the last seed pass
     int32_t *list0, *list1; // double-buffered tile worklists

@@ -227,7 +227,10 @@ __global__ void __launch_bounds__(NT) k_seed_push(Ctx c) {
         }
         for (int o = 16; o; o >>= 1) a += __shfl_xor_sync(0xffffffffu, a, o);
         if ((threadIdx.x & 31) == 0 && a) atomicAdd(&c.act[gid], a);
-        if (__syncthreads_or(a) && threadIdx.x == 0) seed_tile(c, int32_t(t));
+        if (__syncthreads_or(a) && threadIdx.x == 0) {
+            if (c.tfresh) c.tfresh[t] = 1;   // its heights are this relabel's exact distances
+            seed_tile(c, int32_t(t));
+        }
     }
 }
 

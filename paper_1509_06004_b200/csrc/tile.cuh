@@ -537,8 +537,16 @@ __device__ __forceinline__ TileResult push_tile(const Ctx &c, int32_t t, int ite
         s_ph[ring_index(s, j)] = v;
     }
     if (i == 0) s_side = 0;
+    // first pass after an exact relabel: the local relabel would reproduce
+    // the heights (exact global distances restricted to the tile), skip it
+    bool fresh = false;
+    if (c.tfresh) {
+        fresh = __ldcg(c.tfresh + t) != 0;
+        __syncthreads();   // everyone has read the flag before it is cleared
+        if (fresh && i == 0) c.tfresh[t] = 0;
+    }
     int act = 1;
-    int until_relabel = 0, its = 0;
+    int until_relabel = fresh ? relabel_every : 0, its = 0;
     for (int it = 0; it < iters; it++) {
         its++;
         if (c.push_flush && it > 0 && it % c.push_flush == 0 && c.persistent)
