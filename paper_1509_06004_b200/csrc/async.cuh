@@ -48,7 +48,7 @@ struct GridRun {
     int32_t pops;      // discharge tile passes in the current PUSH phase
     int32_t budget;    // ... and their cap
     int32_t act;       // active pixels found by the current SEED phase
-    int32_t cut;       // the current PUSH phase hit its budget
+    int32_t pad;
     int32_t cycles;    // relabel cycles of the current lambda
     int64_t drain;     // unused sink residual (EMIT)
 };
@@ -262,7 +262,6 @@ __device__ void grid_transition(const Ctx &c, const AsyncArgs &A, int32_t g, int
                 } else {
                     next = PH_PUSH;
                     R.pops = 0;
-                    R.cut = 0;
                     atomicAdd(&c.ctl->cycles_total, 1);
                 }
                 break;
@@ -437,8 +436,8 @@ __global__ void __launch_bounds__(NTT, 2) k_async(Ctx c, AsyncArgs A) {
             stat = ST_BFS;
         } else if (ph == PH_PUSH) {
             if (i == 0) {
+                // budget spent: the tile waits for the relabel that follows
                 s_ok = atomicAdd(&A.gr[g].pops, 1) < __ldcg(&A.gr[g].budget);
-                if (!s_ok) A.gr[g].cut = 1;   // budget spent: relabel before more discharge
             }
             __syncthreads();
             if (s_ok) {
@@ -513,7 +512,7 @@ __global__ void k_async_begin(Ctx c, AsyncArgs A, int32_t ngrids) {
     for (int64_t g = tid; g < ngrids; g += stride) {
         GridRun &R = A.gr[g];
         R.phase = PH_BINIT;
-        R.pops = R.budget = R.act = R.cut = R.cycles = 0;
+        R.pops = R.budget = R.act = R.pad = R.cycles = 0;
         R.drain = 0;
     }
     for (int64_t t = tid; t < c.ntiles; t += stride) A.tflag[t] = 0;
