@@ -125,7 +125,7 @@ struct TaskErr {
     }
 };
 
-constexpr int64_t kChunk = 1 << 16;   // elements per host task
+constexpr int64_t kChunk = 1 << 14;   // elements per host task
 
 
 struct Layout {
@@ -1001,11 +1001,13 @@ inline void narrow(int32_t *dst, const int64_t *src, int64_t n, int64_t lo, int6
     }
 }
 
-// largest c(p->q) + c(q->p) over arc pairs of a (4, n) row-major plane set
-int64_t max_pair(const int32_t *nb, int W, int H) {
+// largest c(p->q) + c(q->p) over the arc pairs leaving rows [y0, y1) of a
+// (4, n) row-major plane set
+int64_t max_pair(const int32_t *nb, int W, int H, int y0 = 0, int y1 = -1) {
     const int64_t n = int64_t(W) * H;
     int64_t m = 0;
-    for (int y = 0; y < H; y++)
+    if (y1 < 0) y1 = H;
+    for (int y = y0; y < y1; y++)
         for (int x = 0; x < W; x++) {
             int64_t p = int64_t(y) * W + x;
             if (x + 1 < W) m = std::max<int64_t>(m, int64_t(nb[1 * n + p]) + nb[0 * n + p + 1]);
@@ -1231,8 +1233,13 @@ int seed_stage(pmf_solver *s, int32_t nprob, int32_t W, int32_t H, const int64_t
         narrow(hp + k * 4 * n + lo, src + lo, hi - lo, 0, CAP_MAX);
     });
     if ((rc = terr.raise())) return rc;
-    std::vector<int64_t> mp(pw_list.size(), 0);
-    s->pool->run(int64_t(pw_list.size()), [&](int64_t k) { mp[k] = max_pair(hp + k * 4 * n, W, H); });
+    const int rows = int(std::max<int64_t>(1, kChunk / W)), row_tasks = int(cdiv(H, rows));
+    std::vector<int64_t> mp(pw_list.size() * size_t(row_tasks), 0);
+    s->pool->run(int64_t(mp.size()), [&](int64_t task) {
+        const int64_t k = task / row_tasks;
+        const int y0 = int(task % row_tasks) * rows;
+        mp[size_t(task)] = max_pair(hp + k * 4 * n, W, H, y0, std::min(H, y0 + rows));
+    });
     int64_t maxpair = 0;
     for (int64_t v : mp) maxpair = std::max(maxpair, v);
     // unary / sink planes.  Problems whose three planes equal those of the
