@@ -467,6 +467,39 @@ __device__ __forceinline__ void push_prepare() {
     if (threadIdx.x < 2 * (TH + 2)) (&s_rowin[0][0])[threadIdx.x] = 0;
 }
 
+// Residuals of one pixel held in registers: EdgeU8 keeps the packed u8x4
+// word (lane arithmetic on the word is exact: every lane stays in [0, 255])
+// -- one register instead of four, which the 32-register discharge needs.
+template <class E>
+struct RegRes;
+template <>
+struct RegRes<EdgeU8> {
+    uint32_t w;
+    __device__ __forceinline__ explicit RegRes(uint32_t word) : w(word) {}
+    __device__ __forceinline__ int get(int d) const { return int((w >> (8 * d)) & 0xffu); }
+    __device__ __forceinline__ bool pos(int d) const { return ((w >> (8 * d)) & 0xffu) != 0u; }
+    __device__ __forceinline__ void add(int d, int v) { w += uint32_t(v) << (8 * d); }
+    __device__ __forceinline__ void sub(int d, int v) { w -= uint32_t(v) << (8 * d); }
+    __device__ __forceinline__ uint8_t mask() const {
+        const uint32_t x = __vcmpne4(w, 0u);   // 0xff per nonzero byte
+        return uint8_t(((x >> 7) & 1u) | ((x >> 14) & 2u) | ((x >> 21) & 4u) | ((x >> 28) & 8u));
+    }
+    __device__ __forceinline__ uint32_t word() const { return w; }
+};
+template <>
+struct RegRes<EdgeI32> {
+    int32_t r[4];
+    __device__ __forceinline__ explicit RegRes(int4 v) : r{v.x, v.y, v.z, v.w} {}
+    __device__ __forceinline__ int get(int d) const { return r[d]; }
+    __device__ __forceinline__ bool pos(int d) const { return r[d] > 0; }
+    __device__ __forceinline__ void add(int d, int v) { r[d] += v; }
+    __device__ __forceinline__ void sub(int d, int v) { r[d] -= v; }
+    __device__ __forceinline__ uint8_t mask() const {
+        return uint8_t((r[0] > 0) | ((r[1] > 0) << 1) | ((r[2] > 0) << 2) | ((r[3] > 0) << 3));
+    }
+    __device__ __forceinline__ int4 word() const { return make_int4(r[0], r[1], r[2], r[3]); }
+};
+
 // Mid-pass hand-off (knob push_flush, queue modes): flow pushed across the
 // tile border so far is applied to the neighbour tiles now and they are
 // requested, so they start while this pass goes on, instead of one pass
@@ -478,7 +511,7 @@ __device__ __forceinline__ void push_prepare() {
 __shared__ int s_flush;
 template <class E>
 __device__ __forceinline__ void push_flush(const Ctx &c, int32_t t, int64_t p, int i, int32_t e, int32_t h,
-                                           const int32_t *r, int32_t &w0, typename E::Word &rv0) {
+                                           const RegRes<E> &R, int32_t &w0, typename E::Word &rv0) {
     int pending = 0;
     if (i < 4 * TW) {
         const int s = i / TW, j = i % TW;
@@ -487,7 +520,7 @@ __device__ __forceinline__ void push_flush(const Ctx &c, int32_t t, int64_t p, i
     if (i == 0) s_flush = 0;
     if (!__syncthreads_or(pending)) return;
     if (on_border(i)) {
-        const typename E::Word rv = E::pack(r[0], r[1], r[2], r[3]);
+        const typename E::Word rv = R.word();
         if (e != w0) atomicAdd(&c.w[p], e - w0);
         E::store_delta(c.r, p, rv, rv0);
         c.h[p] = h;
@@ -526,9 +559,7 @@ __device__ __forceinline__ TileResult push_tile(const Ctx &c, int32_t t, int ite
     int32_t w0 = __ldcg(c.w + p);
     typename E::Word rv0 = E::load(c.r, p);
     int32_t e = w0, h = __ldcg(c.h + p);
-    int32_t r[4];
-#pragma unroll
-    for (int d = 0; d < 4; d++) r[d] = E::lane(rv0, d);
+    RegRes<E> R(rv0);
     if (i < 4 * TW) {
         const int s = i / TW, j = i % TW;
         const int32_t nb = tile_nb(c, t, s);
@@ -550,12 +581,12 @@ __device__ __forceinline__ TileResult push_tile(const Ctx &c, int32_t t, int ite
     for (int it = 0; it < iters; it++) {
         its++;
         if (c.push_flush && it > 0 && it % c.push_flush == 0 && c.persistent)
-            push_flush<E>(c, t, p, i, e, h, r, w0, rv0);
+            push_flush<E>(c, t, p, i, e, h, R, w0, rv0);
         if (relabel_every && until_relabel == 0) {
             until_relabel = relabel_every;
             // exact local relabel (frozen pixels stay frozen)
             s_sd[pi] = e < 0 ? 1 : HINF;
-            s_sm[i] = uint8_t((r[0] > 0) | ((r[1] > 0) << 1) | ((r[2] > 0) << 2) | ((r[3] > 0) << 3));
+            s_sm[i] = R.mask();
             __syncthreads();
             const unsigned long long tr0 = i == 0 ? gtimer() : 0ull;
             const int rr = tile_relax(s_sd, s_sm, s_hv, 1, relax_cap), conv = rr & 1;
@@ -590,10 +621,11 @@ __device__ __forceinline__ TileResult push_tile(const Ctx &c, int32_t t, int ite
                 int pushed = 0;
 #pragma unroll
                 for (int d = 0; d < 4; d++) {
-                    if (e > 0 && r[d] > 0 && h > hn[d]) {
-                        const int32_t dl = min(e, r[d]);
+                    const int rd = R.get(d);
+                    if (e > 0 && rd > 0 && h > hn[d]) {
+                        const int32_t dl = min(e, rd);
                         e -= dl;
-                        r[d] -= dl;
+                        R.sub(d, dl);
                         s_in[0][opp(d)][q + OFF[d]] += dl;
                         pushed |= 1 << d;
                     }
@@ -611,7 +643,7 @@ __device__ __forceinline__ TileResult push_tile(const Ctx &c, int32_t t, int ite
                 const int32_t v = s_in[0][d][q];
                 if (v) {
                     e += v;
-                    r[d] += v;
+                    R.add(d, v);
                     s_in[0][d][q] = 0;
                 }
             }
@@ -626,7 +658,7 @@ __device__ __forceinline__ TileResult push_tile(const Ctx &c, int32_t t, int ite
             int32_t m = HINF;
 #pragma unroll
             for (int d = 0; d < 4; d++)
-                if (r[d] > 0) m = min(m, hn[d]);
+                if (R.pos(d)) m = min(m, hn[d]);
             if (m >= h) {
                 h = m >= HINF ? HINF : m + 1;
                 s_ph[q] = h;
@@ -638,7 +670,7 @@ __device__ __forceinline__ TileResult push_tile(const Ctx &c, int32_t t, int ite
     if (i == 0) atomicAdd(&c.stat[ST_PUSH_ITERS], (unsigned long long)its);   // diagnostics
     // ---- write back: interior pixels plainly, border pixels as deltas
     // (neighbour tiles may have pushed into them meanwhile)
-    const typename E::Word rv = E::pack(r[0], r[1], r[2], r[3]);
+    const typename E::Word rv = R.word();
     if (!on_border(i)) {
         c.w[p] = e;
         E::store(c.r, p, rv);
