@@ -225,8 +225,8 @@ class Solver:
     def phases(self, grid: int):
         """Phase timeline [(phase name, us since the first entry)] of one grid
         of the last asynchronous run (knob phase_log=1)."""
-        out = np.zeros(128, np.uint64)
-        n = ctypes.c_int32(128)
+        out = np.zeros(512, np.uint64)
+        n = ctypes.c_int32(512)
         rc = self._lib.pmf_debug_phases(self._h, grid, out.ctypes.data_as(ctypes.POINTER(ctypes.c_uint64)),
                                         ctypes.byref(n))
         if rc:

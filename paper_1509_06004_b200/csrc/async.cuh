@@ -66,7 +66,7 @@ struct AsyncArgs {
     int32_t prefetch;  // take the next ticket while the queue is deep
     unsigned long long *plog;   // diagnostics (nullable): per grid PLOG entries (phase << 56 | globaltimer)
 };
-constexpr int PLOG = 128;
+constexpr int PLOG = 512;
 
 // ---- scan phases: one task = up to SCAN_GROUP consecutive tiles of a grid,
 // all processed at once (SCAN_GROUP pixels per thread, loads issued
