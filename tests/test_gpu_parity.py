@@ -468,3 +468,24 @@ def test_seed_batches_on_edge_shapes(engine, mode):
                     f, lab, _ = oracle.solve(w, h, src, snk, nbr)
                     assert int(flows[pi, li]) == f, (w, h, chain, pi, lam)
                     assert np.array_equal(labels[pi, li], lab), (w, h, chain, pi, lam)
+
+
+@pytest.mark.parametrize("mode", [1, 0])
+def test_c4_all_lambdas_both_schedulers(engine, mode):
+    """C4 (1920x1080, lambdas 1..24): every per-lambda flow of SURVEY.md
+    Appendix A (scipy-Dinic oracle, reference-confirmed at 1, 7, 24) and the
+    foreground counts, through the asynchronous kernel (mode 1) and the
+    step-synchronous engine (mode 0)."""
+    from paper_1509_06004_b200 import _native
+    p = synth.generate(1920, 1080, rng_seed=0).problems
+    lams = synth.C4_LAMBDAS
+    flows_a = [20920322, 25439507, 29721283, 37249143, 44135775, 44603555, 44719143, 44904079]
+    fg_a = [611418, 986561, 1015195, 1180813, 1180813, 2067603, 2067604, 2067604]
+    s = _native.Solver(0, **{"async": mode})
+    try:
+        _, flows, labels = s.solve_seed_batch(1920, 1080, p, lams, "auto")
+        assert s.stats()["async_mode"] == mode
+    finally:
+        s.close()
+    assert flows[0].tolist() == flows_a
+    assert [int(l.sum()) for l in labels[0]] == fg_a
