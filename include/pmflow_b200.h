@@ -103,7 +103,16 @@ int pmf_solver_destroy(pmf_solver *s);
  * "push_budget_warm" (discharge budget of warm-start batches),
  * "warp" (bit mask: warp-per-tile discharge 1 / sink BFS 2 / label BFS 4),
  * "timing" (0/1 event timings),
- * "max_cycles" (non-convergence guard). Returns PMF_ERR_ARG if unknown. */
+ * "max_cycles" (non-convergence guard),
+ * "async" (seed batches: -1 auto / 0 step-synchronous / 1 asynchronous
+ * single-kernel solver) with "async_max_tiles" (auto threshold),
+ * "async_cont" / "async_prefetch" (queue hand-off options),
+ * "rolling" (step-synchronous warm start without a common step barrier),
+ * "verify" (device cut-cost == flow certificate, default on),
+ * "fresh_skip" (skip the no-op local relabel of a first pass on exact
+ * heights), "push_budget_add", "push_mode", "push_flush", "push_minb",
+ * "grid_div", "relax_cap", "bfs_multi", "phase_log" (diagnostics).
+ * Returns PMF_ERR_ARG if unknown or out of range. */
 int pmf_solver_set(pmf_solver *s, const char *name, int64_t value);
 
 /* The solver's CUDA stream (a cudaStream_t) for callers that record their
