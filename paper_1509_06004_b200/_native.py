@@ -217,6 +217,8 @@ class Solver:
         names = ("binit", "bfs", "seed", "push", "linit", "lab", "emit", "-", "wait", "handoff", "transition")
         d = {k: round(float(v), 2) for k, v in zip(names, out) if k != "-"}
         d["push_iterations"] = int(out[15])
+        d["spec_tries"] = int(out[7])
+        d["spec_spoiled"] = int(out[11])
         d["relax_ms"] = round(float(out[13]), 2)
         d["relax_calls"] = int(out[14])
         d["relax_sweeps"] = int(out[12])

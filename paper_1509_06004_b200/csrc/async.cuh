@@ -37,7 +37,8 @@ __host__ __device__ constexpr bool scan_phase(int ph) {
     return ph == PH_BINIT || ph == PH_SEED || ph == PH_LINIT || ph == PH_EMIT;
 }
 // extra pass counters (Ctx::stat) of the scan phases
-enum { ST_BINIT = 9, ST_SEED = 10, ST_LINIT = 11, ST_EMIT = 12, ST_LAMS = 13, ST_ASYNC_NS = 14 };
+enum { ST_BINIT = 9, ST_SEED = 10, ST_LINIT = 11, ST_EMIT = 12, ST_LAMS = 13, ST_ASYNC_NS = 14,
+       ST_SPEC = 32, ST_SPOILED = 33 };   // speculative label closures tried / spoiled
 // CTA-busy nanoseconds per phase kind (ST_BUSY + PH_*), then queue wait,
 // hand-off (requests + retire) and grid transitions
 constexpr int ST_BUSY = 16;
@@ -48,8 +49,12 @@ struct GridRun {
     int32_t pops;      // discharge tile passes in the current PUSH phase
     int32_t budget;    // ... and their cap
     int32_t act;       // active pixels found by the current SEED phase
-    int32_t pad;
+    int32_t cut;       // the current PUSH phase hit its budget
     int32_t cycles;    // relabel cycles of the current lambda
+    int32_t spec;      // the current label closure is speculative (after a drained discharge)
+    int32_t spoiled;   // ... and reached a sink-residual pixel: not done yet
+    int32_t labok;     // lab holds the previous lambda's source side (nested seeding)
+    int32_t pad;
     int64_t drain;     // unused sink residual (EMIT)
 };
 
@@ -64,6 +69,7 @@ struct AsyncArgs {
     int32_t max_cycles;
     int32_t cont;      // continuation hand-off between neighbouring tiles
     int32_t prefetch;  // take the next ticket while the queue is deep
+    int32_t spec;      // a drained discharge goes straight to a speculative label closure
     unsigned long long *plog;   // diagnostics (nullable): per grid PLOG entries (phase << 56 | globaltimer)
 };
 constexpr int PLOG = 512;
@@ -166,7 +172,7 @@ __device__ __forceinline__ void seed_group(const Ctx &c, const AsyncArgs &A, int
 __device__ __forceinline__ void linit_group(const Ctx &c, const AsyncArgs &A, int32_t t0, int ntl, int32_t g,
                                             bool swapped) {
     const int i = threadIdx.x;
-    const bool nested = __ldcg(c.cur_lam + g) > c.grids[g].lam;
+    const bool nested = __ldcg(c.cur_lam + g) > c.grids[g].lam && __ldcg(&A.gr[g].labok);
     scan_reset();
     int v[SCAN_GROUP];
 #pragma unroll
@@ -262,18 +268,41 @@ __device__ void grid_transition(const Ctx &c, const AsyncArgs &A, int32_t g, int
                 } else {
                     next = PH_PUSH;
                     R.pops = 0;
+                    R.cut = 0;
                     atomicAdd(&c.ctl->cycles_total, 1);
                 }
                 break;
             case PH_PUSH:
-                // even a drained discharge needs a confirming exact relabel:
-                // the lock-free rule h(p) > h(q) against a halo height read at
-                // pass start can push into a pixel frozen meanwhile, giving it
-                // a residual path out, so HINF marks alone certify nothing
-                next = PH_BINIT;
+                // A drained discharge is not a certificate by itself (the
+                // lock-free rule h(p) > h(q) against a halo height read at
+                // pass start can push into a pixel frozen meanwhile, giving
+                // it a residual path out).  The label closure of the excess
+                // pixels IS one (it is source_side, solvers.py:144-158): run
+                // it speculatively -- if it never reaches a sink-residual
+                // pixel the preflow is maximum and the labels are final;
+                // otherwise relabel and discharge on.  Swapped grids need
+                // the sink side of an exact relabel.
+                if (A.spec && !__ldcg(&R.cut) && !swapped) {
+                    R.spec = 1;
+                    R.spoiled = 0;
+                    atomicAdd(&c.stat[ST_SPEC], 1ull);
+                    next = PH_LINIT;
+                } else {
+                    next = PH_BINIT;
+                }
                 break;
             case PH_LINIT: next = swapped ? PH_EMIT : PH_LAB; break;
-            case PH_LAB: next = PH_EMIT; break;
+            case PH_LAB:
+                if (R.spec && __ldcg(&R.spoiled)) {
+                    atomicAdd(&c.stat[ST_SPOILED], 1ull);
+                    R.labok = 0;   // lab now holds a spoiled closure
+                    next = PH_BINIT;
+                } else {
+                    next = PH_EMIT;
+                }
+                R.spec = 0;
+                R.spoiled = 0;
+                break;
             case PH_EMIT: {
                 const int cur = __ldcg(c.cur_lam + g);
                 const int64_t snk = int64_t(__ldcg((const unsigned long long *)(c.snk_sum + g)));
@@ -286,6 +315,7 @@ __device__ void grid_transition(const Ctx &c, const AsyncArgs &A, int32_t g, int
                         c.snk_sum[g] = snk + (A.sa.lambdas[cur + 1] - A.sa.lambdas[cur]) * A.slope_sum[gd.prob];
                     c.cur_lam[g] = cur + 1;
                     R.cycles = 0;
+                    R.labok = 1;     // lab holds this lambda's source side
                     next = PH_BFS;   // EMIT ran the next lambda's BINIT
                 }
                 break;
@@ -438,6 +468,7 @@ __global__ void __launch_bounds__(NTT, 2) k_async(Ctx c, AsyncArgs A) {
             if (i == 0) {
                 // budget spent: the tile waits for the relabel that follows
                 s_ok = atomicAdd(&A.gr[g].pops, 1) < __ldcg(&A.gr[g].budget);
+                if (!s_ok) A.gr[g].cut = 1;
             }
             __syncthreads();
             if (s_ok) {
@@ -446,7 +477,11 @@ __global__ void __launch_bounds__(NTT, 2) k_async(Ctx c, AsyncArgs A) {
                 stat = ST_PUSH;
             }
         } else if (ph == PH_LAB) {
-            r = bfs_src_tile<E>(c, t);
+            // one CTA-uniform decision (the flag changes under our feet)
+            if (i == 0) s_ok = !__ldcg(&A.gr[g].spoiled);
+            __syncthreads();
+            if (s_ok)   // else: a spoiled speculative closure has nothing left to learn
+                r = bfs_src_tile<E>(c, t, __ldcg(&A.gr[g].spec) ? &A.gr[g].spoiled : nullptr);
             stat = ST_LAB;
         }
         const unsigned long long tf = i == 0 ? gtimer() : 0ull;
@@ -512,7 +547,8 @@ __global__ void k_async_begin(Ctx c, AsyncArgs A, int32_t ngrids) {
     for (int64_t g = tid; g < ngrids; g += stride) {
         GridRun &R = A.gr[g];
         R.phase = PH_BINIT;
-        R.pops = R.budget = R.act = R.pad = R.cycles = 0;
+        R.pops = R.budget = R.act = R.cut = R.cycles = 0;
+        R.spec = R.spoiled = R.labok = R.pad = 0;
         R.drain = 0;
     }
     for (int64_t t = tid; t < c.ntiles; t += stride) A.tflag[t] = 0;

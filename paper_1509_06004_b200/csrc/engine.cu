@@ -220,9 +220,11 @@ struct pmf_solver {
                                 // (1), step-synchronous phases (0), or -1: async up to async_max_tiles tiles
     int async_max_tiles = 12000;
     int async_cont = 1, async_prefetch = 1;
+    int async_spec = 1;         // drained discharge -> speculative label closure instead of a confirming relabel
     int phase_log = 0;          // diagnostics: record every grid's phase timeline (async)
     int64_t plog_grids = 0;
-    double busy_ms[16] = {0};    // async: CTA-busy time per phase kind of the last run (diagnostics)
+    double busy_ms[16] = {0};
+    int64_t spec_tries = 0, spec_spoiled = 0;    // async: CTA-busy time per phase kind of the last run (diagnostics)
     int bfs_chunk = 8;
     int timing = 0;
     int64_t max_cycles = 50000;
@@ -943,6 +945,8 @@ int run_end(pmf_solver *s) {
     s->busy_ms[13] = double(st[ST_RELAX_NS]) * 1e-6;
     s->busy_ms[14] = double(st[ST_RELAX_N]);
     s->busy_ms[12] = double(st[ST_RELAX_SW]);
+    s->spec_tries = int64_t(st[ST_SPEC]);
+    s->spec_spoiled = int64_t(st[ST_SPOILED]);
     s->stats.push_tile_passes = int64_t(st[ST_PUSH]);
     s->stats.bfs_tile_passes = int64_t(st[ST_BFS]);
     s->stats.label_tile_passes = int64_t(st[ST_LAB]);
@@ -1092,6 +1096,7 @@ int async_solve(pmf_solver *s, const Ctx &c0, const SeedArgs &sa) {
     A.max_cycles = int32_t(std::min<int64_t>(s->max_cycles, 0x7fffffff));
     A.cont = s->async_cont;
     A.prefetch = s->async_prefetch;
+    A.spec = s->async_spec;
     if (s->phase_log) {
         if ((rc = s->d_plog.ensure(size_t(G) * PLOG * 8))) return rc;
         CK(cudaMemsetAsync(s->d_plog.p, 0, size_t(G) * PLOG * 8, s->st));
@@ -1538,6 +1543,7 @@ int pmf_solver_set(pmf_solver *s, const char *name, int64_t v) {
     else if (k == "async_max_tiles" && v >= 0) s->async_max_tiles = int(std::min<int64_t>(v, 1 << 30));
     else if (k == "async_cont") s->async_cont = v != 0;
     else if (k == "async_prefetch") s->async_prefetch = v != 0;
+    else if (k == "async_spec") s->async_spec = v != 0;
     else if (k == "phase_log") s->phase_log = v != 0;
     else if (k == "graph") s->use_graph = v != 0;
     else if (k == "persistent_bfs") s->persistent_bfs = v != 0;
@@ -1669,6 +1675,8 @@ int pmf_solve_composites(pmf_solver *s, int32_t ncomp, const int32_t *width, con
 int pmf_debug_busy(pmf_solver *s, double *out16) {
     if (!s || !out16) return fail(PMF_ERR_ARG, "null argument");
     for (int k = 0; k < 16; k++) out16[k] = s->busy_ms[k];
+    out16[7] = double(s->spec_tries);     // speculative label closures tried
+    out16[11] = double(s->spec_spoiled);  // ... and spoiled
     return 0;
 }
 

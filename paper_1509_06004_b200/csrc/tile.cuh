@@ -375,8 +375,10 @@ __global__ void __launch_bounds__(NTT, 2) k_bfs_sink(Ctx c, int k, LaunchCtl lc)
 // INTO each pixel); touching a sink-residual pixel means the preflow was
 // not maximal (NonMaximalFlowError).
 // ---------------------------------------------------------------------------
+// spoil != nullptr: a speculative closure (asynchronous solver) -- reaching
+// a sink-residual pixel only marks the attempt spoiled instead of raising
 template <class E>
-__device__ __forceinline__ TileResult bfs_src_tile(const Ctx &c, int32_t t) {
+__device__ __forceinline__ TileResult bfs_src_tile(const Ctx &c, int32_t t, int32_t *spoil = nullptr) {
     const int i = threadIdx.x, lx = i & 31, ly = i >> 5;
     const TileNb g = tile_nbs(c, t);
     const int64_t p = int64_t(t) * TPIX + i;
@@ -414,7 +416,10 @@ __device__ __forceinline__ TileResult bfs_src_tile(const Ctx &c, int32_t t) {
     tile_relax(s_sd, s_sm, s_hv, 0);
     if (s_sd[ly * SP + lx] == 0 && !l0) {
         c.lab[p] = 1;
-        if (__ldcg(c.w + p) < 0) atomicExch(c.err, 4);   // NonMaximalFlowError
+        if (__ldcg(c.w + p) < 0) {
+            if (spoil) *spoil = 1;            // the preflow was not maximum yet
+            else atomicExch(c.err, 4);        // NonMaximalFlowError
+        }
         if (int b = border_sides(lx, ly)) atomicOr(&s_side, b);
     }
     __syncthreads();

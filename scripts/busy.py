@@ -15,4 +15,5 @@ print(cfg, " ".join(args), "dev", d["med_dev_ms"], "| us/pass push", per("push",
       "| iters/push pass", round(b.get("push_iterations", 0) / max(1, d["push_tile_passes"]), 2),
       "relax us/call", round(1e3 * b.get("relax_ms", 0) / max(1, b.get("relax_calls", 0)), 2),
       "relax calls/pass", round(b.get("relax_calls", 0) / max(1, d["push_tile_passes"]), 2),
-      "sweeps/relax", round(b.get("relax_sweeps", 0) / max(1, b.get("relax_calls", 0)), 2))
+      "sweeps/relax", round(b.get("relax_sweeps", 0) / max(1, b.get("relax_calls", 0)), 2),
+      "| spec", b.get("spec_tries"), "spoiled", b.get("spec_spoiled"))
