@@ -229,7 +229,7 @@ struct pmf_solver {
     int timing = 0;
     int64_t max_cycles = 50000;
     // device workspace
-    DevBuf d_w, d_h, d_r, d_lab, d_tile_grid, d_tnb, d_fin, d_gpend, d_gr, d_tflag, d_vacc, d_truth, d_score, d_plog, d_tfresh, d_grids, d_live, d_act, d_list, d_inq, d_cnt,
+    DevBuf d_w, d_h, d_r, d_lab, d_tile_grid, d_tnb, d_fin, d_gpend, d_specg, d_gr, d_tflag, d_vacc, d_truth, d_score, d_plog, d_tfresh, d_grids, d_live, d_act, d_list, d_inq, d_cnt,
         d_snk, d_drain, d_err, d_stat, d_colswap, d_out, d_bits, d_in32, d_pw, d_mask, d_off, d_lam,
         d_swapcnt, d_swapflag, d_ring, d_qstate, d_qctr, d_ctl, d_curlam, d_flows, d_slopesum;
     HostBuf h_in32, h_pw, h_mask, h_out, h_small;
@@ -286,7 +286,7 @@ int setup_state(pmf_solver *s, int edge_bytes) {
     if ((rc = s->d_w.ensure(P * 4)) || (rc = s->d_h.ensure(P * 4)) ||
         (rc = s->d_r.ensure(P * size_t(edge_bytes))) || (rc = s->d_lab.ensure(P)) ||
         (rc = s->d_tile_grid.ensure(T * 4)) || (rc = s->d_tnb.ensure(T * 16)) || (rc = s->d_grids.ensure(G * sizeof(GridDesc))) ||
-        (rc = s->d_live.ensure(G * 4)) || (rc = s->d_fin.ensure(G * 4)) || (rc = s->d_gpend.ensure(G * 4)) || (rc = s->d_act.ensure(G * 4)) ||
+        (rc = s->d_live.ensure(G * 4)) || (rc = s->d_fin.ensure(G * 4)) || (rc = s->d_gpend.ensure(G * 4)) || (rc = s->d_specg.ensure(G * 4)) || (rc = s->d_act.ensure(G * 4)) ||
         (rc = s->d_list.ensure(2 * T * 4)) || (rc = s->d_inq.ensure(2 * T * 4)) ||
         (rc = s->d_cnt.ensure(64)) || (rc = s->d_snk.ensure(G * 8)) || (rc = s->d_drain.ensure(G * 8)) ||
         (rc = s->d_err.ensure(64)) || (rc = s->d_stat.ensure(ST_NSTAT * 8)) ||
@@ -309,6 +309,7 @@ int setup_state(pmf_solver *s, int edge_bytes) {
     CK(cudaMemsetAsync(s->d_act.p, 0, G * 4, s->st));
     CK(cudaMemsetAsync(s->d_fin.p, 0, G * 4, s->st));
     CK(cudaMemsetAsync(s->d_gpend.p, 0, G * 4, s->st));
+    CK(cudaMemsetAsync(s->d_specg.p, 0, G * 4, s->st));
     CK(cudaMemsetAsync(s->d_snk.p, 0, G * 8, s->st));
     CK(cudaMemsetAsync(s->d_drain.p, 0, G * 8, s->st));
     CK(cudaMemsetAsync(s->d_err.p, 0, 64, s->st));
@@ -333,6 +334,7 @@ int setup_state(pmf_solver *s, int edge_bytes) {
         x.tfresh = s->d_tfresh.as<uint8_t>();
     }
     x.gpend = s->d_gpend.as<int32_t>();
+    x.specg = nullptr;   // set by seed_run_t in rolling mode
     x.ngrids = int32_t(G);
     x.rolling = 0;
     x.act = s->d_act.as<int32_t>();
@@ -770,6 +772,8 @@ int build_graph_rolling(pmf_solver *s, const Ctx &c0, int32_t ngrids, const Seed
                          int64_t(s->max_cycles), h_cycle, 1, h_lab, 1)))
         return rc;
     if ((rc = add_push_node<E>(s, cyc, &q, P.pq, K_PERSISTENT, lctl(ST_PUSH)))) return rc;
+    if (c0.specg && (rc = add_kernel(cyc, &q, dim3(1), dim3(1024), k_push_spec, P.base, ngrids, h_cycle, 1, h_lab, 1)))
+        return rc;
     // finished grids: labels, flow, next lambda
     cudaGraph_t lab;
     if ((rc = add_if(cyc, &q, h_lab, &lab))) return rc;
@@ -777,6 +781,7 @@ int build_graph_rolling(pmf_solver *s, const Ctx &c0, int32_t ngrids, const Seed
     if ((rc = add_kernel(lab, &l, gfull, dim3(256), k_phase_begin, P.bfs, int(P.bfs.persistent), none, 0))) return rc;
     if ((rc = add_kernel(lab, &l, gfull, dim3(NT), k_lab_seed, P.bfs))) return rc;
     if ((rc = add_bfs_node<E>(s, lab, &l, false, P.bfs, bfs_k, lctl(ST_LAB)))) return rc;
+    if (c0.specg && (rc = add_kernel(lab, &l, dim3(1), dim3(1024), k_unspoil, P.base, ngrids))) return rc;
     if ((rc = add_kernel(lab, &l, gfull, dim3(NT), k_emit, P.base))) return rc;
     if ((rc = add_kernel(lab, &l, dim3(std::max(1, int(cdiv(ngrids, 256)))), dim3(256), k_finalize, P.base, ngrids)))
         return rc;
@@ -869,6 +874,7 @@ int host_solve_rolling(pmf_solver *s, const Ctx &c0, int32_t ngrids, const SeedA
         if (ctl.nact) {
             s->tmark(C_PUSH);
             launch_push<E>(s, P.pq, K_PERSISTENT);
+            if (c0.specg) LAUNCH(s, (k_push_spec<<<1, 1024, 0, s->st>>>(c0, ngrids, 0, 0, 0, 0)));
             CK(cudaGetLastError());
             if ((rc = read_ctl(s, c0, &ctl))) return rc;
         }
@@ -880,6 +886,7 @@ int host_solve_rolling(pmf_solver *s, const Ctx &c0, int32_t ngrids, const SeedA
         LAUNCH(s, (k_phase_begin<<<s->grid_full, 256, 0, s->st>>>(P.bfs, P.bfs.persistent, 0, 0)));
         LAUNCH(s, (k_lab_seed<<<s->grid_full, NT, 0, s->st>>>(P.bfs)));
         if ((rc = host_bfs<E>(s, P.bfs, false))) return rc;
+        if (c0.specg) LAUNCH(s, (k_unspoil<<<1, 1024, 0, s->st>>>(c0, ngrids)));
         LAUNCH(s, (k_emit<<<s->grid_full, NT, 0, s->st>>>(P.base)));
         LAUNCH(s, (k_finalize<<<gfin, 256, 0, s->st>>>(c0, ngrids)));
         LAUNCH(s, (k_advance_tiles<<<s->grid_full, NT, 0, s->st>>>(c0, sa)));
@@ -947,6 +954,10 @@ int run_end(pmf_solver *s) {
     s->busy_ms[12] = double(st[ST_RELAX_SW]);
     s->spec_tries = int64_t(st[ST_SPEC]);
     s->spec_spoiled = int64_t(st[ST_SPOILED]);
+    if (!s->stats.async_mode) {   // rolling mode's speculative label rounds
+        s->spec_tries = int64_t(st[ST_SPEC_ROLL]);
+        s->spec_spoiled = int64_t(st[ST_SPOIL_ROLL]);
+    }
     s->stats.push_tile_passes = int64_t(st[ST_PUSH]);
     s->stats.bfs_tile_passes = int64_t(st[ST_BFS]);
     s->stats.label_tile_passes = int64_t(st[ST_LAB]);
@@ -1162,6 +1173,7 @@ int seed_run_t(pmf_solver *s) {
     }
     // rolling warm start needs the persistent discharge and a single-launch BFS
     s->ctx.rolling = chains && s->rolling && s->persistent && (s->bfs_multi || s->persistent_bfs);
+    s->ctx.specg = s->ctx.rolling && s->async_spec ? s->d_specg.as<int32_t>() : nullptr;
     int rc2 = run_solve<E>(s, c, int32_t(s->lay.grids.size()), chains ? &a : nullptr,
                            chains ? s->d_slopesum.as<int64_t>() : nullptr);
     if (rc2) return rc2;

@@ -35,6 +35,7 @@ enum {
     ST_PUSH_L = 6, ST_BFS_L = 7, ST_LAB_L = 8,
     ST_PUSH_ITERS = 28,   // discharge iterations executed (diagnostics)
     ST_RELAX_NS = 29, ST_RELAX_N = 30, ST_RELAX_SW = 31,   // discharge local relabels: time, count, sweeps
+    ST_SPEC_ROLL = 34, ST_SPOIL_ROLL = 35,   // rolling mode: speculative label rounds tried / spoiled
     ST_NSTAT = 40
 };
 
@@ -115,6 +116,7 @@ struct Ctx {
     int32_t *live;          // per grid: still has work
     int32_t *fin;           // per grid (rolling mode): finished its lambda this cycle, labels due
     int32_t *gpend;         // per grid: its tiles queued or running in the current persistent phase
+    int32_t *specg;         // rolling mode (nullable): 1 label closure speculative, 2 spoiled
     int32_t ngrids;
     int32_t rolling;        // rolling warm start: grids emit and advance as they finish
     int32_t push_mode;      // discharge body: 0 two barriers per iteration, 1 one (double-buffered inflow)

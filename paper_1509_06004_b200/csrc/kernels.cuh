@@ -309,6 +309,53 @@ __global__ void __launch_bounds__(1024) k_cycle_ctl(Ctx c, int32_t ngrids, int p
     }
 }
 
+// Rolling mode, after a discharge: a live unswapped grid none of whose tiles
+// is still queued or running drained its discharge.  That alone certifies
+// nothing (see async.cuh), but the label closure of its excess pixels does:
+// the grid joins this cycle's label round speculatively (specg = 1); a
+// closure that reaches a sink-residual pixel marks it spoiled (2) and
+// k_unspoil sends it back to relabel and discharge.
+__global__ void __launch_bounds__(1024) k_push_spec(Ctx c, int32_t ngrids, cudaGraphConditionalHandle cond,
+                                                    int has_cond, cudaGraphConditionalHandle cond_lab,
+                                                    int has_lab) {
+    __shared__ int s_fin;
+    if (threadIdx.x == 0) s_fin = 0;
+    __syncthreads();
+    int nfin = 0;
+    for (int g = threadIdx.x; g < ngrids; g += blockDim.x) {
+        if (c.live[g] && c.gpend[g] == 0 && !grid_swapped(c, c.grids[g])) {
+            c.live[g] = 0;
+            c.fin[g] = 1;
+            c.specg[g] = 1;
+            nfin++;
+        }
+    }
+    if (nfin) atomicAdd(&s_fin, nfin);
+    __syncthreads();
+    if (threadIdx.x == 0 && s_fin && !c.ctl->noconv) {
+        c.ctl->nfin += s_fin;
+        atomicAdd(&c.stat[ST_SPEC_ROLL], (unsigned long long)s_fin);
+        if (has_cond) cudaGraphSetConditional(cond, 1u);
+        if (has_lab) cudaGraphSetConditional(cond_lab, 1u);
+    }
+}
+
+// After the label closure of a rolling round: spoiled speculative grids go
+// back to the live set (no labels, no advance); the others finish.
+__global__ void __launch_bounds__(1024) k_unspoil(Ctx c, int32_t ngrids) {
+    int n = 0;
+    for (int g = threadIdx.x; g < ngrids; g += blockDim.x) {
+        const int sp = c.specg[g];
+        if (sp == 2) {
+            c.fin[g] = 0;
+            c.live[g] = 1;
+            n++;
+        }
+        if (sp) c.specg[g] = 0;
+    }
+    if (n) atomicAdd(&c.stat[ST_SPOIL_ROLL], (unsigned long long)n);
+}
+
 // ---------------------------------------------------------------------------
 // Labels: source-side closure of the excess pixels (solvers.py:144-158),
 // then per-grid label bytes and flows.

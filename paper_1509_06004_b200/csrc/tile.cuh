@@ -417,7 +417,7 @@ __device__ __forceinline__ TileResult bfs_src_tile(const Ctx &c, int32_t t, int3
     if (s_sd[ly * SP + lx] == 0 && !l0) {
         c.lab[p] = 1;
         if (__ldcg(c.w + p) < 0) {
-            if (spoil) *spoil = 1;            // the preflow was not maximum yet
+            if (spoil) *spoil = 2;            // the preflow was not maximum yet
             else atomicExch(c.err, 4);        // NonMaximalFlowError
         }
         if (int b = border_sides(lx, ly)) atomicOr(&s_side, b);
@@ -428,7 +428,14 @@ __device__ __forceinline__ TileResult bfs_src_tile(const Ctx &c, int32_t t, int3
 
 template <class E>
 __global__ void __launch_bounds__(NTT, 2) k_bfs_src(Ctx c, int k, LaunchCtl lc) {
-    tile_loop(c, k, lc, [&](int32_t t) { return bfs_src_tile<E>(c, t); });
+    tile_loop(c, k, lc, [&](int32_t t) {
+        int32_t *sp = nullptr;   // rolling mode: a speculative closure only marks its grid spoiled
+        if (c.specg) {
+            const int32_t g = __ldg(c.tile_grid + t);
+            if (__ldcg(c.specg + g)) sp = c.specg + g;
+        }
+        return bfs_src_tile<E>(c, t, sp);
+    });
 }
 
 // ---------------------------------------------------------------------------

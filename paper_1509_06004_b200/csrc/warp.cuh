@@ -387,7 +387,11 @@ __global__ void __launch_bounds__(WPB * 32) k_wbfs_src(Ctx c, int k, LaunchCtl l
         for (uint32_t b = fresh; b; b &= b - 1) {
             const int x = __ffs(b) - 1, p = lane * TW + x;
             c.lab[base + p] = 1;
-            if (T.w[p] < 0) atomicExch(c.err, 4);
+            if (T.w[p] < 0) {
+                const int32_t gid = __ldg(c.tile_grid + t);
+                if (c.specg && __ldcg(c.specg + gid)) c.specg[gid] = 2;   // speculative: spoiled
+                else atomicExch(c.err, 4);
+            }
             out |= (x == 0 ? 1 << DL : 0) | (x == TW - 1 ? 1 << DR : 0);
         }
         if (fresh) out |= (lane == 0 ? 1 << DU : 0) | (lane == 31 ? 1 << DD : 0);
