@@ -3,9 +3,11 @@
 // Every grid (a warm-start chain of lambda-graphs, or one cold lambda-graph)
 // walks its own phase machine
 //
-//   BINIT -> BFS -> SEED -+-> PUSH -> BINIT ...           (next relabel cycle)
-//                         +-> LINIT -> LAB -> EMIT -+-> BFS  (next lambda; EMIT ran its BINIT)
-//                                                   +-> done
+//   BINIT -> BFS -> SEED -+-> PUSH -+-> BINIT ...           (budget spent: relabel cycle)
+//                         |         +-> LINIT               (drained: speculative closure)
+//                         +-> LINIT -> LAB -+-> EMIT -+-> SEED (next lambda, unswapped) / BFS (swapped)
+//                                           |         +-> done
+//                                           +-> BINIT       (speculative closure spoiled)
 //
 // and the tiles of all grids share one work queue (engine.cuh q_*): a CTA
 // pops a tile, runs the body of its grid's current phase, requests the
@@ -70,6 +72,7 @@ struct AsyncArgs {
     int32_t cont;      // continuation hand-off between neighbouring tiles
     int32_t prefetch;  // take the next ticket while the queue is deep
     int32_t spec;      // a drained discharge goes straight to a speculative label closure
+    int32_t keep_h;    // unswapped grids enter the next lambda with their current heights
     unsigned long long *plog;   // diagnostics (nullable): per grid PLOG entries (phase << 56 | globaltimer)
 };
 constexpr int PLOG = 512;
@@ -210,7 +213,11 @@ __device__ __forceinline__ void emit_group(const Ctx &c, const AsyncArgs &A, int
     uint8_t *out = c.out + (int64_t(gd.prob) * c.nlam + cur) * n;
     const uint8_t *mask = a.mask + int64_t(gd.prob) * n;
     const int32_t *slope = a.slope + a.plane_off[gd.prob];
-    if (next) scan_reset();
+    // unswapped grids may keep their heights into the next lambda (knob
+    // adv_keep_h, see the EMIT transition); swapped ones get that lambda's
+    // BINIT fused in here
+    const bool reinit = next && (swapped || !A.keep_h);
+    if (reinit) scan_reset();
     int64_t drain = 0;
     const int32_t l0 = int32_t(t0 - gd.tile_base);
 #pragma unroll 2
@@ -229,14 +236,14 @@ __device__ __forceinline__ void emit_group(const Ctx &c, const AsyncArgs &A, int
                 c.w[p] = wv;
             }
         }
-        if (next) {   // the next lambda's BINIT, fused
+        if (reinit) {   // the next lambda's BINIT, fused
             c.h[p] = wv < 0 ? 1 : HINF;
             scan_mark(k, wv < 0);
         }
     }
     const int64_t s = block_sum64(drain, red);
     if (i == 0 && s) atomicAdd((unsigned long long *)&A.gr[g].drain, (unsigned long long)s);
-    if (next) scan_flag(c, A, t0, ntl);
+    if (reinit) scan_flag(c, A, t0, ntl);
 }
 
 // Whole CTA, after the last tile of grid g's phase `ph` retired (nothing of
@@ -316,7 +323,17 @@ __device__ void grid_transition(const Ctx &c, const AsyncArgs &A, int32_t g, int
                     c.cur_lam[g] = cur + 1;
                     R.cycles = 0;
                     R.labok = 1;     // lab holds this lambda's source side
-                    next = PH_BFS;   // EMIT ran the next lambda's BINIT
+                    if (swapped || !A.keep_h) {
+                        next = PH_BFS;   // EMIT ran the next lambda's BINIT
+                    } else {
+                        // lambda_{i+1} only lowers sink residuals of an
+                        // unswapped grid (w += dl * slope): no residual path
+                        // appears, so lambda_i's exact distances stay a valid
+                        // labelling (lower bounds, HINF exact): seed the
+                        // discharge straight away
+                        R.act = 0;
+                        next = PH_SEED;
+                    }
                 }
                 break;
             }

@@ -221,6 +221,7 @@ struct pmf_solver {
     int async_max_tiles = 12000;
     int async_cont = 1, async_prefetch = 1;
     int async_spec = 1;         // drained discharge -> speculative label closure instead of a confirming relabel
+    int adv_keep_h = 1;         // async: unswapped grids enter the next lambda without a relabel
     int phase_log = 0;          // diagnostics: record every grid's phase timeline (async)
     int64_t plog_grids = 0;
     double busy_ms[16] = {0};
@@ -1108,6 +1109,7 @@ int async_solve(pmf_solver *s, const Ctx &c0, const SeedArgs &sa) {
     A.cont = s->async_cont;
     A.prefetch = s->async_prefetch;
     A.spec = s->async_spec;
+    A.keep_h = s->adv_keep_h;
     if (s->phase_log) {
         if ((rc = s->d_plog.ensure(size_t(G) * PLOG * 8))) return rc;
         CK(cudaMemsetAsync(s->d_plog.p, 0, size_t(G) * PLOG * 8, s->st));
@@ -1556,6 +1558,7 @@ int pmf_solver_set(pmf_solver *s, const char *name, int64_t v) {
     else if (k == "async_cont") s->async_cont = v != 0;
     else if (k == "async_prefetch") s->async_prefetch = v != 0;
     else if (k == "async_spec") s->async_spec = v != 0;
+    else if (k == "adv_keep_h") s->adv_keep_h = v != 0;
     else if (k == "phase_log") s->phase_log = v != 0;
     else if (k == "graph") s->use_graph = v != 0;
     else if (k == "persistent_bfs") s->persistent_bfs = v != 0;
