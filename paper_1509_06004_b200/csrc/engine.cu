@@ -230,7 +230,7 @@ struct pmf_solver {
     int timing = 0;
     int64_t max_cycles = 50000;
     // device workspace
-    DevBuf d_w, d_h, d_r, d_lab, d_tile_grid, d_tnb, d_fin, d_gpend, d_specg, d_gr, d_tflag, d_vacc, d_truth, d_score, d_plog, d_tfresh, d_grids, d_live, d_act, d_list, d_inq, d_cnt,
+    DevBuf d_w, d_h, d_r, d_lab, d_tile_grid, d_tnb, d_fin, d_gpend, d_specg, d_keeph, d_gr, d_tflag, d_vacc, d_truth, d_score, d_plog, d_tfresh, d_grids, d_live, d_act, d_list, d_inq, d_cnt,
         d_snk, d_drain, d_err, d_stat, d_colswap, d_out, d_bits, d_in32, d_pw, d_mask, d_off, d_lam,
         d_swapcnt, d_swapflag, d_ring, d_qstate, d_qctr, d_ctl, d_curlam, d_flows, d_slopesum;
     HostBuf h_in32, h_pw, h_mask, h_out, h_small;
@@ -287,7 +287,7 @@ int setup_state(pmf_solver *s, int edge_bytes) {
     if ((rc = s->d_w.ensure(P * 4)) || (rc = s->d_h.ensure(P * 4)) ||
         (rc = s->d_r.ensure(P * size_t(edge_bytes))) || (rc = s->d_lab.ensure(P)) ||
         (rc = s->d_tile_grid.ensure(T * 4)) || (rc = s->d_tnb.ensure(T * 16)) || (rc = s->d_grids.ensure(G * sizeof(GridDesc))) ||
-        (rc = s->d_live.ensure(G * 4)) || (rc = s->d_fin.ensure(G * 4)) || (rc = s->d_gpend.ensure(G * 4)) || (rc = s->d_specg.ensure(G * 4)) || (rc = s->d_act.ensure(G * 4)) ||
+        (rc = s->d_live.ensure(G * 4)) || (rc = s->d_fin.ensure(G * 4)) || (rc = s->d_gpend.ensure(G * 4)) || (rc = s->d_specg.ensure(G * 4)) || (rc = s->d_keeph.ensure(G * 4)) || (rc = s->d_act.ensure(G * 4)) ||
         (rc = s->d_list.ensure(2 * T * 4)) || (rc = s->d_inq.ensure(2 * T * 4)) ||
         (rc = s->d_cnt.ensure(64)) || (rc = s->d_snk.ensure(G * 8)) || (rc = s->d_drain.ensure(G * 8)) ||
         (rc = s->d_err.ensure(64)) || (rc = s->d_stat.ensure(ST_NSTAT * 8)) ||
@@ -311,6 +311,7 @@ int setup_state(pmf_solver *s, int edge_bytes) {
     CK(cudaMemsetAsync(s->d_fin.p, 0, G * 4, s->st));
     CK(cudaMemsetAsync(s->d_gpend.p, 0, G * 4, s->st));
     CK(cudaMemsetAsync(s->d_specg.p, 0, G * 4, s->st));
+    CK(cudaMemsetAsync(s->d_keeph.p, 0, G * 4, s->st));
     CK(cudaMemsetAsync(s->d_snk.p, 0, G * 8, s->st));
     CK(cudaMemsetAsync(s->d_drain.p, 0, G * 8, s->st));
     CK(cudaMemsetAsync(s->d_err.p, 0, 64, s->st));
@@ -336,6 +337,7 @@ int setup_state(pmf_solver *s, int edge_bytes) {
     }
     x.gpend = s->d_gpend.as<int32_t>();
     x.specg = nullptr;   // set by seed_run_t in rolling mode
+    x.keeph = nullptr;   // set by seed_run_t for warm chains
     x.ngrids = int32_t(G);
     x.rolling = 0;
     x.act = s->d_act.as<int32_t>();
@@ -1176,6 +1178,7 @@ int seed_run_t(pmf_solver *s) {
     // rolling warm start needs the persistent discharge and a single-launch BFS
     s->ctx.rolling = chains && s->rolling && s->persistent && (s->bfs_multi || s->persistent_bfs);
     s->ctx.specg = s->ctx.rolling && s->async_spec ? s->d_specg.as<int32_t>() : nullptr;
+    s->ctx.keeph = chains && s->adv_keep_h ? s->d_keeph.as<int32_t>() : nullptr;
     int rc2 = run_solve<E>(s, c, int32_t(s->lay.grids.size()), chains ? &a : nullptr,
                            chains ? s->d_slopesum.as<int64_t>() : nullptr);
     if (rc2) return rc2;

@@ -117,6 +117,7 @@ struct Ctx {
     int32_t *fin;           // per grid (rolling mode): finished its lambda this cycle, labels due
     int32_t *gpend;         // per grid: its tiles queued or running in the current persistent phase
     int32_t *specg;         // rolling mode (nullable): 1 label closure speculative, 2 spoiled
+    int32_t *keeph;         // warm chains (nullable): grid entered its lambda with valid heights, skip its relabel
     int32_t ngrids;
     int32_t rolling;        // rolling warm start: grids emit and advance as they finish
     int32_t push_mode;      // discharge body: 0 two barriers per iteration, 1 one (double-buffered inflow)

@@ -196,7 +196,8 @@ __device__ __forceinline__ void seed_with_halo(const Ctx &c, int64_t t, unsigned
 // finished grids are left untouched.
 __global__ void __launch_bounds__(NT) k_gr_init(Ctx c) {
     for (int64_t t = blockIdx.x; t < c.ntiles; t += gridDim.x) {
-        if (!c.live[c.tile_grid[t]]) continue;
+        const int32_t g = c.tile_grid[t];
+        if (!c.live[g] || (c.keeph && c.keeph[g])) continue;
         unsigned seeds = 0;
         for (int j = 0; j < PPT; j++) {
             int64_t p = t * TPIX + threadIdx.x + j * NT;
@@ -275,6 +276,7 @@ __global__ void __launch_bounds__(1024) k_cycle_ctl(Ctx c, int32_t ngrids, int p
     __syncthreads();
     int nfin = 0;
     for (int g = threadIdx.x; g < ngrids; g += blockDim.x) {
+        if (c.keeph) c.keeph[g] = 0;   // seeded with its kept heights: relabel from the next cycle on
         if (c.live[g] && c.act[g] == 0) {
             c.live[g] = 0;
             if (c.rolling) {
@@ -619,6 +621,9 @@ __global__ void __launch_bounds__(1024) k_advance_grids(Ctx c, SeedArgs a, const
         if (c.swapflag[gd.prob]) c.snk_sum[g] += (a.lambdas[cur + 1] - a.lambdas[cur]) * slope_sum[gd.prob];
         c.cur_lam[g] = cur + 1;
         c.live[g] = 1;
+        // unswapped: lambda_{i+1} only lowers sink residuals, the exact
+        // heights of lambda_i stay a valid labelling -- skip one relabel
+        if (c.keeph && !c.swapflag[gd.prob]) c.keeph[g] = 1;
         any = 1;
     }
     any = __syncthreads_or(any);
