@@ -217,7 +217,9 @@ __device__ __forceinline__ void emit_group(const Ctx &c, const AsyncArgs &A, int
     // adv_keep_h, see the EMIT transition); swapped ones get that lambda's
     // BINIT fused in here
     const bool reinit = next && (swapped || !A.keep_h);
-    if (reinit) scan_reset();
+    // kept heights: the next lambda's SEED, fused (active = w > 0, h < HINF)
+    const bool seed = next && !reinit;
+    if (reinit || seed) scan_reset();
     int64_t drain = 0;
     const int32_t l0 = int32_t(t0 - gd.tile_base);
 #pragma unroll 2
@@ -240,10 +242,21 @@ __device__ __forceinline__ void emit_group(const Ctx &c, const AsyncArgs &A, int
             c.h[p] = wv < 0 ? 1 : HINF;
             scan_mark(k, wv < 0);
         }
+        if (seed) {
+            const int act = __reduce_add_sync(0xffffffffu, int(wv > 0 && __ldcg(c.h + p) < HINF));
+            if ((i & 31) == 0 && act) atomicAdd(&s_scan.any[k], act);
+        }
     }
     const int64_t s = block_sum64(drain, red);
     if (i == 0 && s) atomicAdd((unsigned long long *)&A.gr[g].drain, (unsigned long long)s);
     if (reinit) scan_flag(c, A, t0, ntl);
+    if (seed) {
+        __syncthreads();
+        if (i < ntl && s_scan.any[i]) {
+            atomicAdd(&A.gr[g].act, s_scan.any[i]);
+            A.tflag[t0 + i] = 1;
+        }
+    }
 }
 
 // Whole CTA, after the last tile of grid g's phase `ph` retired (nothing of
@@ -298,7 +311,10 @@ __device__ void grid_transition(const Ctx &c, const AsyncArgs &A, int32_t g, int
                     next = PH_BINIT;
                 }
                 break;
-            case PH_LINIT: next = swapped ? PH_EMIT : PH_LAB; break;
+            case PH_LINIT:
+                next = swapped ? PH_EMIT : PH_LAB;
+                R.act = 0;   // EMIT may seed the next lambda
+                break;
             case PH_LAB:
                 if (R.spec && __ldcg(&R.spoiled)) {
                     atomicAdd(&c.stat[ST_SPOILED], 1ull);
@@ -306,6 +322,7 @@ __device__ void grid_transition(const Ctx &c, const AsyncArgs &A, int32_t g, int
                     next = PH_BINIT;
                 } else {
                     next = PH_EMIT;
+                    R.act = 0;   // EMIT may seed the next lambda
                 }
                 R.spec = 0;
                 R.spoiled = 0;
@@ -330,9 +347,23 @@ __device__ void grid_transition(const Ctx &c, const AsyncArgs &A, int32_t g, int
                         // unswapped grid (w += dl * slope): no residual path
                         // appears, so lambda_i's exact distances stay a valid
                         // labelling (lower bounds, HINF exact): seed the
-                        // discharge straight away
-                        R.act = 0;
-                        next = PH_SEED;
+                        // discharge straight away (EMIT ran that
+                        // lambda's seeding)
+                        if (__ldcg(&R.act) == 0) {
+                            // kept heights may carry HINF marks of a
+                            // speculative finish, which certify nothing: the
+                            // closure decides (speculative, falls back)
+                            next = PH_LINIT;
+                            R.spec = 1;
+                            R.spoiled = 0;
+                            atomicAdd(&c.stat[ST_SPEC], 1ull);
+                        } else {
+                            next = PH_PUSH;
+                            R.cycles = 1;
+                            R.pops = 0;
+                            R.cut = 0;
+                            atomicAdd(&c.ctl->cycles_total, 1);
+                        }
                     }
                 }
                 break;

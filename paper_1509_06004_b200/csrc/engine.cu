@@ -1111,7 +1111,7 @@ int async_solve(pmf_solver *s, const Ctx &c0, const SeedArgs &sa) {
     A.cont = s->async_cont;
     A.prefetch = s->async_prefetch;
     A.spec = s->async_spec;
-    A.keep_h = s->adv_keep_h;
+    A.keep_h = s->adv_keep_h && s->async_spec;   // kept heights need the speculative closure
     if (s->phase_log) {
         if ((rc = s->d_plog.ensure(size_t(G) * PLOG * 8))) return rc;
         CK(cudaMemsetAsync(s->d_plog.p, 0, size_t(G) * PLOG * 8, s->st));
@@ -1178,7 +1178,8 @@ int seed_run_t(pmf_solver *s) {
     // rolling warm start needs the persistent discharge and a single-launch BFS
     s->ctx.rolling = chains && s->rolling && s->persistent && (s->bfs_multi || s->persistent_bfs);
     s->ctx.specg = s->ctx.rolling && s->async_spec ? s->d_specg.as<int32_t>() : nullptr;
-    s->ctx.keeph = chains && s->adv_keep_h ? s->d_keeph.as<int32_t>() : nullptr;
+    // kept heights need the speculative closure as their safety net
+    s->ctx.keeph = s->ctx.specg && s->adv_keep_h ? s->d_keeph.as<int32_t>() : nullptr;
     int rc2 = run_solve<E>(s, c, int32_t(s->lay.grids.size()), chains ? &a : nullptr,
                            chains ? s->d_slopesum.as<int64_t>() : nullptr);
     if (rc2) return rc2;

@@ -276,11 +276,16 @@ __global__ void __launch_bounds__(1024) k_cycle_ctl(Ctx c, int32_t ngrids, int p
     __syncthreads();
     int nfin = 0;
     for (int g = threadIdx.x; g < ngrids; g += blockDim.x) {
-        if (c.keeph) c.keeph[g] = 0;   // seeded with its kept heights: relabel from the next cycle on
+        // seeded with kept heights (relabel from the next cycle on); their
+        // HINF marks may come from a speculative finish and certify nothing,
+        // so a grid with no active pixel finishes speculatively
+        const bool kept = c.keeph && c.keeph[g];
+        if (kept) c.keeph[g] = 0;
         if (c.live[g] && c.act[g] == 0) {
             c.live[g] = 0;
             if (c.rolling) {
                 c.fin[g] = 1;
+                if (kept) c.specg[g] = 1;
                 nfin++;
             }
         }
