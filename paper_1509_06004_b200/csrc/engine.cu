@@ -207,7 +207,7 @@ struct pmf_solver {
     int chain = 0;            // warm-start chain length (0: auto, see warm_min_problems)
     int relax_cap = 0;        // sweep cap of the discharge's local relabel (0: to the fixpoint)
     int warm_min_problems = 8;  // auto: one chain per problem (whole ladder) from this many problems
-    int push_budget_warm = 4;   // discharge budget factor when the batch runs warm-start chains
+    int push_budget_warm = 3;   // discharge budget factor when the batch runs warm-start chains
     int push_budget_add = 64;   // asynchronous solver: + this many pops per discharge phase
     int verify = 1;             // seed batches: device cut_cost == flow certificate per cut
     int rolling = 1;            // warm-start chains advance per grid as each finishes (no step barrier)
