@@ -34,7 +34,7 @@ namespace pmf {
 enum { PH_BINIT = 0, PH_BFS, PH_SEED, PH_PUSH, PH_LINIT, PH_LAB, PH_EMIT, PH_DONE };
 // scan phases (BINIT, SEED, LINIT, EMIT) run as tasks of SCAN_GROUP
 // consecutive tiles, queued by their first tile
-constexpr int SCAN_GROUP = 8;
+constexpr int SCAN_GROUP = 16;
 __host__ __device__ constexpr bool scan_phase(int ph) {
     return ph == PH_BINIT || ph == PH_SEED || ph == PH_LINIT || ph == PH_EMIT;
 }
