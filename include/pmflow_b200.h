@@ -105,7 +105,8 @@ int pmf_solver_destroy(pmf_solver *s);
  * "timing" (0/1 event timings),
  * "max_cycles" (non-convergence guard),
  * "async" (seed batches: -1 auto / 0 step-synchronous / 1 asynchronous
- * single-kernel solver) with "async_max_tiles" (auto threshold),
+ * single-kernel solver) with "async_max_tiles" / "async_max_grid_tiles"
+ * (auto thresholds: batch tiles, average tiles per grid),
  * "async_cont" / "async_prefetch" (queue hand-off options),
  * "rolling" (step-synchronous warm start without a common step barrier),
  * "verify" (device cut-cost == flow certificate, default on),

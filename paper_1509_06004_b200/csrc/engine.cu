@@ -218,7 +218,8 @@ struct pmf_solver {
     int grid_div = 1;           // use 1/grid_div of the GPU's resident CTAs (solvers sharing a GPU)
     int async_mode = -1;        // seed batches: one persistent kernel, every grid on its own phase machine
                                 // (1), step-synchronous phases (0), or -1: async up to async_max_tiles tiles
-    int async_max_tiles = 12000;
+    int async_max_tiles = 30000;
+    int async_max_grid_tiles = 1024;   // ... and grids of at most this many tiles on average
     int async_cont = 1, async_prefetch = 1;
     int async_spec = 1;         // drained discharge -> speculative label closure instead of a confirming relabel
     int adv_keep_h = 1;         // async: unswapped grids enter the next lambda without a relabel
@@ -1169,7 +1170,10 @@ int seed_run_t(pmf_solver *s) {
     // asynchronous solver for latency-bound batches; large batches keep the
     // GPU full with step-synchronous phases, whose wide scan kernels and
     // multi-sweep relabels cost less per tile than queued tile tasks
-    const bool use_async = s->async_mode == 1 || (s->async_mode < 0 && s->lay.ntiles <= s->async_max_tiles);
+    const int64_t ngr = std::max<int64_t>(1, int64_t(s->lay.grids.size()));
+    const bool use_async = s->async_mode == 1 ||
+                           (s->async_mode < 0 && s->lay.ntiles <= s->async_max_tiles &&
+                            s->lay.ntiles <= int64_t(s->async_max_grid_tiles) * ngr);
     if (use_async) {
         if ((rc = async_solve<E>(s, c, a))) return rc;
         if (s->verify && (rc = launch_verify(s, c, a))) return rc;
@@ -1559,6 +1563,7 @@ int pmf_solver_set(pmf_solver *s, const char *name, int64_t v) {
     else if (k == "fresh_skip") s->fresh_skip = v != 0;
     else if (k == "async" && v >= -1 && v <= 1) s->async_mode = int(v);
     else if (k == "async_max_tiles" && v >= 0) s->async_max_tiles = int(std::min<int64_t>(v, 1 << 30));
+    else if (k == "async_max_grid_tiles" && v >= 0) s->async_max_grid_tiles = int(std::min<int64_t>(v, 1 << 30));
     else if (k == "async_cont") s->async_cont = v != 0;
     else if (k == "async_prefetch") s->async_prefetch = v != 0;
     else if (k == "async_spec") s->async_spec = v != 0;
