@@ -11,6 +11,7 @@ from __future__ import annotations
 
 import ctypes
 import os
+import sys
 import threading
 
 import numpy as np
@@ -113,6 +114,37 @@ def _ptrs(arrays, ctype=ctypes.c_void_p):
     return (ctype * len(arrays))(*[a.ctypes.data for a in arrays])
 
 
+class _LabelBuffers:
+    """Reuse of large label output buffers across calls.  A fresh multi-MB
+    numpy array costs a page fault and a kernel zero-fill per 4 KiB on first
+    touch, which dominated the host side of large batches.  A buffer is
+    handed out again only once nothing but this pool references it: every
+    numpy view of it (the per-cut label arrays) holds a reference to it, so
+    ``sys.getrefcount`` shows when the caller has dropped them all."""
+
+    MIN_BYTES = 16 << 20
+    KEEP = 2          # buffers kept per size
+
+    def __init__(self):
+        self._free = {}
+        self._lock = threading.Lock()
+
+    def take(self, shape):
+        nbytes = int(np.prod(shape))
+        if nbytes < self.MIN_BYTES:
+            return np.empty(shape, np.uint8)
+        with self._lock:
+            bufs = self._free.setdefault(nbytes, [])
+            for b in bufs:
+                # refs: the list entry, the loop variable, getrefcount's argument
+                if sys.getrefcount(b) <= 3:
+                    return b.reshape(shape)
+            b = np.empty(nbytes, np.uint8)
+            if len(bufs) < self.KEEP:
+                bufs.append(b)
+            return b.reshape(shape)
+
+
 class Solver:
     """One device + one CUDA stream + its workspaces.  Not thread-safe: use
     one per host thread (``solver_for_thread``)."""
@@ -124,6 +156,7 @@ class Solver:
         if rc:
             raise NativeUnavailable(lib.pmf_last_error().decode(errors="replace"))
         self._lib, self._h, self.device = lib, h, device
+        self._labels = _LabelBuffers()
         for k, v in knobs.items():
             self.set(k, v)
 
@@ -279,7 +312,7 @@ class Solver:
         Pt = ctypes.POINTER
         swapped = np.zeros(P_, np.uint8)
         flows = np.zeros(P_ * K, np.int64)
-        lab = np.empty((P_, K, n), np.uint8) if labels else None
+        lab = self._labels.take((P_, K, n)) if labels else None
         rc = self._lib.pmf_seed_fetch(
             self._h, swapped.ctypes.data_as(Pt(ctypes.c_uint8)),
             flows.ctypes.data_as(Pt(ctypes.c_int64)),

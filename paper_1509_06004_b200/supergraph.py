@@ -236,8 +236,13 @@ def seed_layout(problems, schedule: LambdaSchedule, swapped) -> SupergraphLayout
     offsets, bridges, height, _ = _plan(widths, [p.height for p in problems for _ in schedule],
                                         False)
     flags = [bool(swapped[i]) for i in range(len(problems)) for _ in schedule]
-    segs = tuple(Segment(i, o, w, f) for i, (o, w, f) in enumerate(zip(offsets, widths, flags)))
-    return SupergraphLayout(segs, tuple(bridges), height)
+    new = object.__new__
+    segs = []
+    for i, (o, w, f) in enumerate(zip(offsets, widths, flags)):
+        seg = new(Segment)                     # frozen dataclass, fields set directly
+        seg.__dict__.update(constituent=i, offset=o, width=w, swapped=f)
+        segs.append(seg)
+    return SupergraphLayout(tuple(segs), tuple(bridges), height)
 
 
 @dataclass(frozen=True, eq=False)
@@ -296,6 +301,7 @@ def solve_seed_supergraph(problems, schedule: LambdaSchedule, swap_mode: str = "
                                                  schedule.values, swap_mode)
             for k, i in enumerate(idx):
                 swapped[i], flows[i], labels[i] = sw[k], fl[k], lb[k]
-    cuts = tuple(CutResult(int(flows[i][j]), labels[i][j])
+    fl = [[int(f) for f in row] for row in flows]
+    cuts = tuple(CutResult._trusted(fl[i][j], labels[i][j])
                  for i in range(len(problems)) for j in range(len(schedule)))
     return SeedSupergraphResult(seed_layout(problems, schedule, swapped), cuts, scores)

@@ -314,3 +314,26 @@ def test_synth_truths_match_reference():
     for p, t, rec in zip(b.problems, b.truths, g["problems"]):
         assert problem_digest(p) == rec["problem_sha256"]
         assert hashlib.sha256(np.asarray(t, np.uint8).tobytes()).hexdigest() == rec["truth_sha256"]
+
+
+def test_label_buffer_pool_never_hands_out_live_memory():
+    """_native._LabelBuffers reuses a label output buffer only once no array
+    (or view of one) returned earlier still references it."""
+    from paper_1509_06004_b200._native import _LabelBuffers
+    pool = _LabelBuffers()
+    pool.MIN_BYTES = 1
+    a = pool.take((2, 3, 4))
+    view = a[1][2]
+    del a
+    b = pool.take((2, 3, 4))
+    assert not np.shares_memory(b, view)      # a view of the first buffer is alive
+    view[:] = 7
+    del b
+    c = pool.take((2, 3, 4))
+    assert not np.shares_memory(c, view)
+    assert (view == 7).all()
+    del view
+    d = pool.take((2, 3, 4))
+    e = pool.take((2, 3, 4))
+    assert not np.shares_memory(d, e)
+    assert pool.take((5,)).shape == (5,)
