@@ -231,10 +231,10 @@ struct pmf_solver {
     int timing = 0;
     int64_t max_cycles = 50000;
     // device workspace
-    DevBuf d_w, d_h, d_r, d_lab, d_tile_grid, d_tnb, d_fin, d_gpend, d_specg, d_keeph, d_gr, d_tflag, d_vacc, d_truth, d_score, d_plog, d_tfresh, d_grids, d_live, d_act, d_list, d_inq, d_cnt,
+    DevBuf d_w, d_h, d_r, d_lab, d_tile_grid, d_tnb, d_fin, d_gpend, d_specg, d_keeph, d_seeds, d_sofs, d_gr, d_tflag, d_vacc, d_truth, d_score, d_plog, d_tfresh, d_grids, d_live, d_act, d_list, d_inq, d_cnt,
         d_snk, d_drain, d_err, d_stat, d_colswap, d_out, d_bits, d_in32, d_pw, d_mask, d_off, d_lam,
         d_swapcnt, d_swapflag, d_ring, d_qstate, d_qctr, d_ctl, d_curlam, d_flows, d_slopesum;
-    HostBuf h_in32, h_pw, h_mask, h_out, h_small;
+    HostBuf h_in32, h_pw, h_mask, h_out, h_small, h_seeds;
     Layout lay;
     std::vector<int32_t> ones, curlam0;
     std::vector<uint8_t> colswap;
@@ -1231,22 +1231,39 @@ int seed_stage(pmf_solver *s, int32_t nprob, int32_t W, int32_t H, const int64_t
     if ((rc = s->h_pw.ensure(pw_list.size() * size_t(4 * n) * 4))) return rc;
     int32_t *hp = s->h_pw.as<int32_t>();
     TaskErr terr;
-    // masks first (seed index lists are short)
-    for (int p = 0; p < nprob; p++) {
+    // seed masks on the host (validation), one task per problem; the device
+    // builds its own copy from the index lists (k_seed_masks), so only the
+    // lists cross the host link
+    TaskErr merr;
+    s->pool->run(nprob, [&](int64_t p) {
         uint8_t *m = hm + p * n;
         memset(m, 0, size_t(n));
         for (int32_t i = 0; i < (n_fg ? n_fg[p] : 0); i++) {
-            int64_t q = fg_idx[p][i];
-            if (q < 0 || q >= n) return fail(PMF_ERR_ARG, "fg seed out of range");
+            const int64_t q = fg_idx[p][i];
+            if (q < 0 || q >= n) return merr.set(PMF_ERR_ARG, "fg seed out of range");
             m[q] = 1;
         }
         for (int32_t i = 0; i < (n_bg ? n_bg[p] : 0); i++) {
-            int64_t q = bg_idx[p][i];
-            if (q < 0 || q >= n) return fail(PMF_ERR_ARG, "bg seed out of range");
-            if (m[q] == 1) return fail(PMF_ERR_ARG, "a pixel cannot be both a foreground and background seed");
+            const int64_t q = bg_idx[p][i];
+            if (q < 0 || q >= n) return merr.set(PMF_ERR_ARG, "bg seed out of range");
+            if (m[q] == 1) return merr.set(PMF_ERR_ARG, "a pixel cannot be both a foreground and background seed");
             m[q] = 2;
         }
+    });
+    if ((rc = merr.raise())) return rc;
+    // index lists for the device: [fg of p0 | bg of p0 | fg of p1 | ...]
+    std::vector<int64_t> sofs(size_t(2 * nprob + 1), 0);
+    for (int p = 0; p < nprob; p++) {
+        sofs[2 * p + 1] = sofs[2 * p] + (n_fg ? n_fg[p] : 0);
+        sofs[2 * p + 2] = sofs[2 * p + 1] + (n_bg ? n_bg[p] : 0);
     }
+    const int64_t nseeds = sofs.back();
+    if ((rc = s->h_seeds.ensure(size_t(nseeds + 1) * 4))) return rc;
+    int32_t *hs = s->h_seeds.as<int32_t>();
+    s->pool->run(nprob, [&](int64_t p) {
+        for (int32_t i = 0; i < (n_fg ? n_fg[p] : 0); i++) hs[sofs[2 * p] + i] = int32_t(fg_idx[p][i]);
+        for (int32_t i = 0; i < (n_bg ? n_bg[p] : 0); i++) hs[sofs[2 * p + 1] + i] = int32_t(bg_idx[p][i]);
+    });
     // pairwise planes: range check + narrow, chunked
     const int64_t pw_chunks = cdiv(4 * n, kChunk);
     s->pool->run(int64_t(pw_list.size()) * pw_chunks, [&](int64_t task) {
@@ -1332,7 +1349,13 @@ int seed_stage(pmf_solver *s, int32_t nprob, int32_t W, int32_t H, const int64_t
         (rc = s->d_lam.ensure(size_t(nlam) * 8)) || (rc = s->d_swapcnt.ensure(size_t(nprob) * 8)))
         return rc;
     CK(cudaMemcpyAsync(s->d_pw.p, hp, bytes_pw, cudaMemcpyHostToDevice, s->st));
-    CK(cudaMemcpyAsync(s->d_mask.p, hm, size_t(nprob) * n, cudaMemcpyHostToDevice, s->st));
+    if ((rc = s->d_seeds.ensure(size_t(nseeds + 1) * 4)) || (rc = s->d_sofs.ensure(sofs.size() * 8))) return rc;
+    CK(cudaMemcpyAsync(s->d_seeds.p, hs, size_t(nseeds) * 4, cudaMemcpyHostToDevice, s->st));
+    CK(cudaMemcpyAsync(s->d_sofs.p, sofs.data(), sofs.size() * 8, cudaMemcpyHostToDevice, s->st));
+    CK(cudaMemsetAsync(s->d_mask.p, 0, size_t(nprob) * n, s->st));
+    LAUNCH(s, (k_seed_masks<<<std::max(1, std::min(nprob, 4 * s->sms)), 256, 0, s->st>>>(
+                   s->d_mask.as<uint8_t>(), s->d_seeds.as<int32_t>(), s->d_sofs.as<int64_t>(), nprob, n)));
+    CK(cudaGetLastError());
     // distinct planes: check + narrow in one pass, group by group, each
     // group's H2D overlapping the conversion of the next
     const int64_t group = std::max<int64_t>(1, cdiv(nu, 8));
@@ -1387,7 +1410,7 @@ int seed_stage(pmf_solver *s, int32_t nprob, int32_t W, int32_t H, const int64_t
     S.H = H;
     S.swap_mode = swap_mode;
     S.valid = true;
-    s->stats.h2d_bytes = int64_t(bytes_b + bytes_pw) + int64_t(nprob) * n + int64_t(nlam) * 8;
+    s->stats.h2d_bytes = int64_t(bytes_b + bytes_pw) + nseeds * 4 + int64_t(sofs.size()) * 8 + int64_t(nlam) * 8;
     return 0;
 }
 

@@ -31,6 +31,18 @@ struct SeedArgs {
     int32_t *swapped;                           // [nprob]
 };
 
+// Seed masks of a batch from its index lists (1 = fg seed, 2 = bg seed;
+// mask zeroed by the caller): seeds[sofs[2p] .. sofs[2p+1]) are problem p's
+// fg pixels, seeds[sofs[2p+1] .. sofs[2p+2]) its bg pixels (disjoint,
+// checked on the host).
+__global__ void k_seed_masks(uint8_t *mask, const int32_t *seeds, const int64_t *sofs, int32_t nprob, int64_t n) {
+    for (int p = blockIdx.x; p < nprob; p += gridDim.x) {
+        uint8_t *m = mask + int64_t(p) * n;
+        for (int64_t j = sofs[2 * p] + threadIdx.x; j < sofs[2 * p + 2]; j += blockDim.x)
+            m[seeds[j]] = j < sofs[2 * p + 1] ? 1 : 2;
+    }
+}
+
 // Terminal balance at the mid-schedule lambda (supergraph.py:77-92, 210-212).
 __global__ void k_swap_count(SeedArgs a) {
     int64_t n = int64_t(a.W) * a.H;
