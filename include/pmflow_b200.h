@@ -109,7 +109,9 @@ int pmf_solver_destroy(pmf_solver *s);
  * (auto thresholds: batch tiles, average tiles per grid),
  * "async_cont" / "async_prefetch" (queue hand-off options),
  * "rolling" (step-synchronous warm start without a common step barrier),
- * "verify" (device cut-cost == flow certificate, default on),
+ * "verify" (device cut-cost == flow certificate, default on; 2 = test hook
+ *   that corrupts one emitted label first, so the check must fail),
+ * "verify_vec" (4-pixel-group certificate kernel for W % 4 == 0, default on),
  * "fresh_skip" (skip the no-op local relabel of a first pass on exact
  * heights), "push_budget_add", "push_mode", "push_flush", "push_minb",
  * "grid_div", "relax_cap", "bfs_multi", "phase_log" (diagnostics).

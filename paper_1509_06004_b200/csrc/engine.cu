@@ -210,6 +210,7 @@ struct pmf_solver {
     int push_budget_warm = 3;   // discharge budget factor when the batch runs warm-start chains
     int push_budget_add = 64;   // asynchronous solver: + this many pops per discharge phase
     int verify = 1;             // seed batches: device cut_cost == flow certificate per cut
+    int verify_vec = 1;         // 4-pixel-group verify kernel when W % 4 == 0
     int rolling = 1;            // warm-start chains advance per grid as each finishes (no step barrier)
     int push_minb = 2;          // CTA discharge: min CTAs per SM of its launch bounds (1 or 2)
     int push_mode = 0;          // discharge body: 0 two CTA barriers per iteration, 1 one
@@ -1069,17 +1070,32 @@ int grids_for(pmf_solver *s) {
 
 // Integrity certificate of a seed batch (k_verify): cut cost of every
 // emitted mask on the original graph == its flow
+template <class E>
 int launch_verify(pmf_solver *s, const Ctx &c, const SeedArgs &a) {
     const int64_t planes = int64_t(a.nprob) * a.nlam, n = int64_t(a.W) * a.H;
     // (problem, chunk) CTAs: ~4 rounds of NT * VPX pixels each
     const int64_t want = std::max<int64_t>(cdiv(n, int64_t(NT) * VPX * 4), cdiv(4 * s->sms, a.nprob));
     const int chunks = int(std::max<int64_t>(1, std::min<int64_t>({want, cdiv(n, int64_t(NT) * VPX), 4096})));
+    if (n >= (int64_t(1) << 31)) return fail(PMF_ERR_ARG, "image too large for the integrity check (%lld pixels)", (long long)n);
     int rc;
     if ((rc = s->d_vacc.ensure(size_t(planes) * 8))) return rc;
     CK(cudaMemsetAsync(s->d_vacc.p, 0, size_t(planes) * 8, s->st));
     unsigned long long *acc = s->d_vacc.as<unsigned long long>();
-    LAUNCH(s, (k_verify<<<int(std::min<int64_t>(int64_t(a.nprob) * chunks, 32 * s->sms)), NT, 0, s->st>>>(
-                   c, a, acc, chunks)));
+    // verify=2 (test hook): flip the label of the centre pixel of (problem 0,
+    // lambda 0) so the check must fail
+    if (s->verify == 2) LAUNCH(s, (k_flip_label<<<1, 1, 0, s->st>>>(c.out, int64_t(a.H / 2) * a.W + a.W / 2)));
+    constexpr bool narrow = std::is_same<E, EdgeU8>::value;
+    if (a.W % 4 == 0 && s->verify_vec) {
+        // 4-pixel groups: ~4 rounds of NT groups per CTA
+        const int64_t n4 = n / 4;
+        const int64_t w4 = std::max<int64_t>(cdiv(n4, int64_t(NT) * 4), cdiv(4 * s->sms, a.nprob));
+        const int ch4 = int(std::max<int64_t>(1, std::min<int64_t>({w4, cdiv(n4, NT), 4096})));
+        LAUNCH(s, (k_verify4<narrow><<<int(std::min<int64_t>(int64_t(a.nprob) * ch4, 32 * s->sms)), NT, 0, s->st>>>(
+                       c, a, acc, ch4)));
+    } else {
+        LAUNCH(s, (k_verify<narrow><<<int(std::min<int64_t>(int64_t(a.nprob) * chunks, 32 * s->sms)), NT, 0, s->st>>>(
+                       c, a, acc, chunks)));
+    }
     LAUNCH(s, (k_verify_check<<<int(std::max<int64_t>(1, std::min<int64_t>(cdiv(planes, 256), 1024))), 256, 0, s->st>>>(
                    c, planes, acc)));
     CK(cudaGetLastError());
@@ -1159,8 +1175,12 @@ int seed_run_t(pmf_solver *s) {
     a.swap_cnt = s->d_swapcnt.as<int32_t>();
     a.swapped = s->d_swapflag.as<int32_t>();
     a.mask = s->d_mask.as<uint8_t>();
-    if (S.swap_mode == PMF_SWAP_AUTO)
-        LAUNCH(s, (k_swap_count<<<int(std::min<int64_t>(cdiv(S.nprob * n, 256), 16 * s->sms)), 256, 0, s->st>>>(a)));
+    if (S.swap_mode == PMF_SWAP_AUTO) {
+        if (n >= (int64_t(1) << 31)) return fail(PMF_ERR_ARG, "image too large (%lld pixels)", (long long)n);
+        const int chunks = int(std::max<int64_t>(1, std::min<int64_t>(cdiv(n, 256 * 4), cdiv(8 * s->sms, S.nprob))));
+        LAUNCH(s, (k_swap_count<<<int(std::min<int64_t>(int64_t(S.nprob) * chunks, 16 * s->sms)), 256, 0, s->st>>>(
+                       a, chunks)));
+    }
     LAUNCH(s, (k_swap_decide<<<int(cdiv(S.nprob, 128)), 128, 0, s->st>>>(a)));
     LAUNCH(s, (k_build_seed<E><<<s->grid_full, NT, 0, s->st>>>(c, a)));
     CK(cudaGetLastError());
@@ -1176,7 +1196,7 @@ int seed_run_t(pmf_solver *s) {
                             s->lay.ntiles <= int64_t(s->async_max_grid_tiles) * ngr);
     if (use_async) {
         if ((rc = async_solve<E>(s, c, a))) return rc;
-        if (s->verify && (rc = launch_verify(s, c, a))) return rc;
+        if (s->verify && (rc = launch_verify<E>(s, c, a))) return rc;
         return 0;
     }
     // rolling warm start needs the persistent discharge and a single-launch BFS
@@ -1188,7 +1208,7 @@ int seed_run_t(pmf_solver *s) {
                            chains ? s->d_slopesum.as<int64_t>() : nullptr);
     if (rc2) return rc2;
     if (s->verify) {
-        if ((rc = launch_verify(s, c, a))) return rc;
+        if ((rc = launch_verify<E>(s, c, a))) return rc;
     }
     return 0;
 }
@@ -1441,7 +1461,7 @@ int seed_fetch(pmf_solver *s, uint8_t *swapped_out, int64_t *flows_out, uint8_t 
     int32_t *hsw = (int32_t *)(hfl + nf);
     if (labels_out) {
         if ((rc = s->d_bits.ensure(size_t(bit_bytes)))) return rc;
-        const int grid = int(std::min<int64_t>(cdiv(out_bytes, 128 * 8), 16 * s->sms));
+        const int grid = int(std::min<int64_t>(cdiv(out_bytes, 32 * 256), 16 * s->sms));
         LAUNCH(s, (k_pack_bits<<<std::max(grid, 1), 256, 0, s->st>>>(s->d_out.as<uint8_t>(), s->d_bits.as<uint32_t>(),
                                                                      out_bytes)));
         CK(cudaGetLastError());
@@ -1577,7 +1597,8 @@ int pmf_solver_set(pmf_solver *s, const char *name, int64_t v) {
     else if (k == "warm_min_problems" && v >= 1) s->warm_min_problems = int(v);
     else if (k == "push_budget_warm" && v >= 0) s->push_budget_warm = int(v);
     else if (k == "push_budget_add" && v >= 0 && v < (int64_t(1) << 30)) s->push_budget_add = int(v);
-    else if (k == "verify") s->verify = v != 0;
+    else if (k == "verify" && v >= 0 && v <= 2) s->verify = int(v);
+    else if (k == "verify_vec") s->verify_vec = v != 0;
     else if (k == "rolling") s->rolling = v != 0;
     else if (k == "push_minb" && (v == 1 || v == 2)) s->push_minb = int(v);
     else if (k == "grid_div" && v >= 1 && v <= 64) s->grid_div = int(v);

@@ -12,6 +12,8 @@
 // (solvers.py:144-158; proof in DESIGN.md), and the sink side
 // (solvers.py:161-174) is {h < HINF} of the final exact relabel.
 #pragma once
+#include <type_traits>
+
 #include "engine.cuh"
 
 namespace pmf {
@@ -44,27 +46,41 @@ __global__ void k_seed_masks(uint8_t *mask, const int32_t *seeds, const int64_t 
 }
 
 // Terminal balance at the mid-schedule lambda (supergraph.py:77-92, 210-212).
-__global__ void k_swap_count(SeedArgs a) {
-    int64_t n = int64_t(a.W) * a.H;
-    int64_t lam = a.lambdas[a.mid];
-    int neg = 0, pos = 0;
-    for (int64_t idx = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; idx < n * a.nprob;
-         idx += int64_t(gridDim.x) * blockDim.x) {
-        int32_t p = int32_t(idx / n);
-        int64_t r = idx - int64_t(p) * n;
-        int64_t q = a.plane_off[p] + r;
-        uint8_t m = a.mask[idx];
-        int64_t src = m == 1 ? CAP_MAX : int64_t(a.base[q]) + lam * int64_t(a.slope[q]);
-        int64_t snk = m == 2 ? CAP_MAX : int64_t(a.sink[q]);
-        int64_t d = src - snk;
-        neg = d < 0;
-        pos = d > 0;
-        // warp-aggregated atomics: at most one per warp and problem
-        unsigned mm = __match_any_sync(__activemask(), p);
-        int nn = __popc(__ballot_sync(mm, neg)), pp = __popc(__ballot_sync(mm, pos));
-        if ((threadIdx.x & 31) == __ffs(mm) - 1) {
-            if (nn) atomicAdd(&a.swap_cnt[2 * p], nn);
-            if (pp) atomicAdd(&a.swap_cnt[2 * p + 1], pp);
+__device__ __forceinline__ int64_t block_sum64(int64_t v, int64_t *red) {
+    for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = v;
+    __syncthreads();
+    int64_t s = 0;
+    if (threadIdx.x == 0)
+        for (int i = 0; i < int(blockDim.x >> 5); i++) s += red[i];
+    __syncthreads();
+    return s;
+}
+
+// One CTA per (problem, pixel chunk): block-reduced counts, two atomics.
+__global__ void __launch_bounds__(256) k_swap_count(SeedArgs a, int chunks) {
+    __shared__ int64_t red[256 / 32];
+    const int32_t n = a.W * a.H;   // < 2^31 (checked by the stage)
+    const int32_t per = int32_t((int64_t(n) + chunks - 1) / chunks);
+    const int64_t lam = a.lambdas[a.mid];
+    for (int64_t blk = blockIdx.x; blk < int64_t(a.nprob) * chunks; blk += gridDim.x) {
+        const int p = int(blk / chunks);
+        const int32_t lo = int32_t(blk % chunks) * per, hi = min(n, lo + per);
+        const int32_t *bp = a.base + a.plane_off[p], *sp = a.slope + a.plane_off[p], *kp = a.sink + a.plane_off[p];
+        const uint8_t *mask = a.mask + int64_t(p) * n;
+        int64_t neg = 0, pos = 0;
+        for (int32_t q = lo + threadIdx.x; q < hi; q += blockDim.x) {
+            const uint8_t m = mask[q];
+            const int64_t src = m == 1 ? CAP_MAX : int64_t(bp[q]) + lam * int64_t(sp[q]);
+            const int64_t snk = m == 2 ? CAP_MAX : int64_t(kp[q]);
+            neg += src < snk;
+            pos += src > snk;
+        }
+        neg = block_sum64(neg, red);
+        pos = block_sum64(pos, red);
+        if (threadIdx.x == 0) {
+            if (neg) atomicAdd(&a.swap_cnt[2 * p], int32_t(neg));
+            if (pos) atomicAdd(&a.swap_cnt[2 * p + 1], int32_t(pos));
         }
     }
 }
@@ -75,17 +91,6 @@ __global__ void k_swap_decide(SeedArgs a) {
     if (a.swap_mode == 1) a.swapped[p] = 1;
     else if (a.swap_mode == 2) a.swapped[p] = 0;
     else a.swapped[p] = a.swap_cnt[2 * p] > a.swap_cnt[2 * p + 1];
-}
-
-__device__ __forceinline__ int64_t block_sum64(int64_t v, int64_t *red) {
-    for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = v;
-    __syncthreads();
-    int64_t s = 0;
-    if (threadIdx.x == 0)
-        for (int i = 0; i < int(blockDim.x >> 5); i++) s += red[i];
-    __syncthreads();
-    return s;
 }
 
 // One CTA per tile: instantiate (problem, lambda), swap if flagged, write
@@ -436,37 +441,24 @@ __global__ void __launch_bounds__(NT) k_emit(Ctx c) {
 namespace pmf {
 
 // Label bytes (0/1) -> bit array for the D2H (8x fewer bytes over the host
-// link): bit j of word w is byte 32*w + j.  Each warp packs 128 bytes per
-// step (uchar4 per lane, four ballots).
+// link): bit j of word w is byte 32*w + j.  One thread per word: two 16-byte
+// loads, and each 4-byte group's low bits gathered by one multiply
+// ((v & 0x01010101) * 0x10204080 puts bytes 0..3 at bits 28..31).
+__device__ __forceinline__ uint32_t gather4(uint32_t v) { return ((v & 0x01010101u) * 0x10204080u) >> 28; }
 __global__ void k_pack_bits(const uint8_t *__restrict__ bytes, uint32_t *__restrict__ bits, int64_t n) {
-    const int lane = threadIdx.x & 31;
-    const int64_t warp = (blockIdx.x * int64_t(blockDim.x) + threadIdx.x) >> 5;
-    const int64_t nwarps = (int64_t(gridDim.x) * blockDim.x) >> 5;
-    for (int64_t base = warp * 128; base < n; base += nwarps * 128) {
-        const int64_t i = base + 4 * lane;
-        uchar4 v = make_uchar4(0, 0, 0, 0);
-        if (i + 3 < n) {
-            v = *reinterpret_cast<const uchar4 *>(bytes + i);
+    const int64_t nw = n / 32;
+    for (int64_t w = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; w < (n + 31) / 32;
+         w += int64_t(gridDim.x) * blockDim.x) {
+        uint32_t out = 0;
+        if (w < nw) {
+            const uint4 u = __ldcs(reinterpret_cast<const uint4 *>(bytes) + 2 * w);
+            const uint4 v = __ldcs(reinterpret_cast<const uint4 *>(bytes) + 2 * w + 1);
+            out = gather4(u.x) | gather4(u.y) << 4 | gather4(u.z) << 8 | gather4(u.w) << 12 |
+                  gather4(v.x) << 16 | gather4(v.y) << 20 | gather4(v.z) << 24 | gather4(v.w) << 28;
         } else {
-            if (i < n) v.x = bytes[i];
-            if (i + 1 < n) v.y = bytes[i + 1];
-            if (i + 2 < n) v.z = bytes[i + 2];
+            for (int64_t i = 32 * w; i < n; i++) out |= uint32_t(bytes[i] != 0) << (i - 32 * w);
         }
-        // byte base + 4*lane + k sits in word base/32 + (4*lane + k)/32, bit (4*lane + k) % 32
-        const unsigned b0 = __ballot_sync(0xffffffffu, v.x != 0), b1 = __ballot_sync(0xffffffffu, v.y != 0),
-                       b2 = __ballot_sync(0xffffffffu, v.z != 0), b3 = __ballot_sync(0xffffffffu, v.w != 0);
-        if (lane < 4) {
-            // word lane covers lanes 8*lane .. 8*lane + 7 (4 bytes each)
-            uint32_t w = 0;
-#pragma unroll
-            for (int l = 0; l < 8; l++) {
-                const int src = 8 * lane + l;
-                w |= (((b0 >> src) & 1u) << (4 * l)) | (((b1 >> src) & 1u) << (4 * l + 1)) |
-                     (((b2 >> src) & 1u) << (4 * l + 2)) | (((b3 >> src) & 1u) << (4 * l + 3));
-            }
-            const int64_t wi = base / 32 + lane;
-            if (wi * 32 < n) bits[wi] = w;
-        }
+        bits[w] = out;
     }
 }
 
@@ -518,50 +510,74 @@ __global__ void __launch_bounds__(NT) k_advance_tiles(Ctx c, SeedArgs a) {
 // the reference checks it in split(), supergraph.py:181-186, and in the RPC
 // client, rpc.py:328-331): the cut cost of the emitted mask of the ORIGINAL
 // graph must equal the flow.  One CTA per (problem, lambda) plane.
-// One CTA per (problem, chunk of pixels): the problem's planes are read
-// once for all its lambdas (the per-plane pass re-read them nlam times and
-// was bandwidth-bound at ~10 ms per 8-image batch); partial cut costs are
-// summed per (problem, lambda) into acc (zeroed by the caller) and compared
-// with the flows by k_verify_check.
-constexpr int VPX = 4;     // pixels per thread per round
-constexpr int VLAM = 24;   // lambdas per pass over the problem's planes (register accumulators)
-__global__ void __launch_bounds__(NT) k_verify(Ctx c, SeedArgs a, unsigned long long *acc, int chunks) {
+// One CTA per (problem, chunk of pixels): a thread loads its VPX pixels'
+// terms once per VLAM lambdas and then issues every label load of the pass
+// unconditionally (no load behind a branch on another load: the pass is
+// latency-bound, so the loads must be in flight together); partial cut
+// costs are summed per (problem, lambda) into acc (zeroed by the caller) and
+// compared with the flows by k_verify_check.  Pixel indices within a plane
+// are 32-bit (launch_verify rejects planes of 2^31 pixels or more).
+constexpr int VPX = 2;     // pixels per thread per round
+constexpr int VLAM = 10;   // lambdas per pass over the problem's planes (register accumulators)
+// NARROW: pairwise capacities <= 255 (EdgeU8 batches), so a source-side
+// pixel's cost (sink <= CAP_MAX = 2^30 plus four arcs) fits 32 bits
+template <bool NARROW>
+__global__ void __launch_bounds__(NT, 3) k_verify(Ctx c, SeedArgs a, unsigned long long *acc, int chunks) {
+    using SS = typename std::conditional<NARROW, int32_t, int64_t>::type;
     __shared__ unsigned long long s_acc[VLAM];
-    const int64_t n = int64_t(a.W) * a.H;
-    const int64_t per = (n + chunks - 1) / chunks;
+    const int32_t n = a.W * a.H;
+    const int32_t per = int32_t((int64_t(n) + chunks - 1) / chunks);
     for (int64_t blk = blockIdx.x; blk < int64_t(a.nprob) * chunks; blk += gridDim.x) {
         const int p = int(blk / chunks);
-        const int64_t lo = (blk % chunks) * per, hi = min(n, lo + per);
-        const int64_t po = a.plane_off[p];
+        const int32_t lo = int32_t(blk % chunks) * per, hi = min(n, lo + per);
+        const int32_t *bp = a.base + a.plane_off[p], *sp = a.slope + a.plane_off[p], *kp = a.sink + a.plane_off[p];
         const int32_t *pw = a.pw + a.pw_off[p];
         const uint8_t *mask = a.mask + int64_t(p) * n;
         for (int j0 = 0; j0 < a.nlam; j0 += VLAM) {
+            const int nj = min(VLAM, a.nlam - j0);
             int64_t cost[VLAM];
 #pragma unroll
             for (int jj = 0; jj < VLAM; jj++) cost[jj] = 0;
             if (threadIdx.x < VLAM) s_acc[threadIdx.x] = 0;
-            for (int64_t q0 = lo; q0 < hi; q0 += int64_t(NT) * VPX) {
+            for (int32_t q0 = lo; q0 < hi; q0 += NT * VPX) {
+                int32_t qq[VPX], a0[VPX], a1[VPX], a2[VPX], a3[VPX], sk[VPX];
+                int64_t bs[VPX], sl[VPX];
 #pragma unroll
                 for (int k = 0; k < VPX; k++) {
-                    const int64_t q = q0 + threadIdx.x + int64_t(k) * NT;
-                    if (q >= hi) continue;
-                    const uint8_t m = mask[q];
-                    const int64_t bs = a.base[po + q], sl = a.slope[po + q], sk = m == 2 ? CAP_MAX : a.sink[po + q];
-                    const int x = int(q % a.W), y = int(q / a.W);
-                    const int32_t a0 = x > 0 ? pw[q] : 0, a1 = x + 1 < a.W ? pw[n + q] : 0;
-                    const int32_t a2 = y > 0 ? pw[2 * n + q] : 0, a3 = y + 1 < a.H ? pw[3 * n + q] : 0;
-                    const uint8_t *lab = c.out + (int64_t(p) * a.nlam + j0) * n + q;
+                    const int32_t q = q0 + threadIdx.x + k * NT;
+                    const bool ok = q < hi;
+                    qq[k] = ok ? q : lo;   // a pixel past the chunk reads a valid label and adds 0
+                    const int32_t x = ok ? q % a.W : 0, y = ok ? q / a.W : 0;
+                    const uint8_t m = ok ? mask[q] : 0;
+                    // m == 1 (fg seed): CAP_MAX when on the sink side; m == 2 (bg
+                    // seed): CAP_MAX when on the source side
+                    bs[k] = !ok ? 0 : m == 1 ? CAP_MAX : bp[q];
+                    sl[k] = !ok || m == 1 ? 0 : sp[q];
+                    sk[k] = !ok ? 0 : m == 2 ? int32_t(CAP_MAX) : kp[q];
+                    a0[k] = ok && x > 0 ? pw[q] : 0;
+                    a1[k] = ok && x + 1 < a.W ? pw[int64_t(n) + q] : 0;
+                    a2[k] = ok && y > 0 ? pw[2 * int64_t(n) + q] : 0;
+                    a3[k] = ok && y + 1 < a.H ? pw[3 * int64_t(n) + q] : 0;
+                }
+                const uint8_t *lab = c.out + (int64_t(p) * a.nlam + j0) * n;
+                // no branches in here: every load of the pass can be in flight at
+                // once (lambdas past nj re-read the last plane and add 0)
 #pragma unroll
-                    for (int jj = 0; jj < VLAM; jj++) {
-                        if (j0 + jj >= a.nlam) break;
-                        const uint8_t *l = lab + int64_t(jj) * n;
-                        if (*l) {
-                            // arcs leaving the source side (off-grid counts as source side)
-                            cost[jj] += sk + (a0 && !l[-1] ? a0 : 0) + (a1 && !l[1] ? a1 : 0) +
-                                        (a2 && !l[-a.W] ? a2 : 0) + (a3 && !l[a.W] ? a3 : 0);
-                        } else {
-                            cost[jj] += m == 1 ? CAP_MAX : bs + a.lambdas[j0 + jj] * sl;
-                        }
+                for (int jj = 0; jj < VLAM; jj++) {
+                    const int j = min(jj, nj - 1);
+                    const uint8_t *l = lab + int64_t(j) * n;
+                    const int64_t lam = a.lambdas[j0 + j];
+#pragma unroll
+                    for (int k = 0; k < VPX; k++) {
+                        const int32_t q = qq[k];
+                        const uint8_t l0 = l[q];
+                        const uint8_t ll = a0[k] ? l[q - 1] : 1, lr = a1[k] ? l[q + 1] : 1;
+                        const uint8_t lu = a2[k] ? l[q - a.W] : 1, ld = a3[k] ? l[q + a.W] : 1;
+                        // arcs leaving the source side (off-grid counts as source side)
+                        const SS src_side = SS(sk[k]) + SS(ll ? 0 : a0[k]) + SS(lr ? 0 : a1[k]) +
+                                            SS(lu ? 0 : a2[k]) + SS(ld ? 0 : a3[k]);
+                        const int64_t v = l0 ? int64_t(src_side) : bs[k] + lam * sl[k];
+                        cost[jj] += jj < nj ? v : 0;
                     }
                 }
             }
@@ -573,7 +589,7 @@ __global__ void __launch_bounds__(NT) k_verify(Ctx c, SeedArgs a, unsigned long 
                 if ((threadIdx.x & 31) == 0 && v) atomicAdd(&s_acc[jj], (unsigned long long)v);
             }
             __syncthreads();
-            if (threadIdx.x < VLAM && j0 + int(threadIdx.x) < a.nlam && s_acc[threadIdx.x])
+            if (threadIdx.x < nj && s_acc[threadIdx.x])
                 atomicAdd(acc + int64_t(p) * a.nlam + j0 + threadIdx.x, s_acc[threadIdx.x]);
             __syncthreads();
         }
@@ -610,6 +626,98 @@ __global__ void __launch_bounds__(NT) k_score(const uint8_t *__restrict__ out, c
         }
     }
 }
+
+// k_verify for images with W % 4 == 0: a thread owns 4 consecutive pixels of
+// one row, so per lambda its labels, the row above and the row below are
+// three 4-byte loads plus two predicated edge bytes (5 loads per 4 pixels
+// instead of 20), and its terms are 16-byte loads.  Every offset (plane_off,
+// pw_off, label planes) is a multiple of n, hence of 4.
+constexpr int VLAM4 = 8;
+template <bool NARROW>
+__global__ void __launch_bounds__(NT, 3) k_verify4(Ctx c, SeedArgs a, unsigned long long *acc, int chunks) {
+    using SS = typename std::conditional<NARROW, int32_t, int64_t>::type;
+    __shared__ unsigned long long s_acc[VLAM4];
+    const int32_t n = a.W * a.H, n4 = n / 4, W = a.W;
+    const int32_t per = int32_t((int64_t(n4) + chunks - 1) / chunks);
+    for (int64_t blk = blockIdx.x; blk < int64_t(a.nprob) * chunks; blk += gridDim.x) {
+        const int p = int(blk / chunks);
+        const int32_t lo = int32_t(blk % chunks) * per, hi = min(n4, lo + per);
+        const int4 *bp = reinterpret_cast<const int4 *>(a.base + a.plane_off[p]);
+        const int4 *sp = reinterpret_cast<const int4 *>(a.slope + a.plane_off[p]);
+        const int4 *kp = reinterpret_cast<const int4 *>(a.sink + a.plane_off[p]);
+        const int4 *pw = reinterpret_cast<const int4 *>(a.pw + a.pw_off[p]);
+        const uint32_t *mask = reinterpret_cast<const uint32_t *>(a.mask + int64_t(p) * n);
+        for (int j0 = 0; j0 < a.nlam; j0 += VLAM4) {
+            const int nj = min(VLAM4, a.nlam - j0);
+            int64_t cost[VLAM4];
+#pragma unroll
+            for (int jj = 0; jj < VLAM4; jj++) cost[jj] = 0;
+            if (threadIdx.x < VLAM4) s_acc[threadIdx.x] = 0;
+            for (int32_t g0 = lo; g0 < hi; g0 += NT) {
+                const int32_t g = g0 + threadIdx.x;
+                const bool ok = g < hi;
+                const int32_t gq = ok ? g : lo, q = 4 * gq;   // a group past the chunk adds 0
+                const int32_t x = q % W, y = q / W;
+                const uint32_t m4 = mask[gq];
+                const int4 B = bp[gq], S = sp[gq], K = kp[gq];
+                int4 A0 = pw[gq], A1 = pw[n4 + gq], A2 = pw[2 * n4 + gq], A3 = pw[3 * n4 + gq];
+                if (x == 0) A0.x = 0;
+                if (x + 4 == W) A1.w = 0;
+                if (y == 0) A2 = make_int4(0, 0, 0, 0);
+                if (y + 1 == a.H) A3 = make_int4(0, 0, 0, 0);
+                if (!ok) A0 = A1 = A2 = A3 = make_int4(0, 0, 0, 0);
+                const int32_t bb[4] = {B.x, B.y, B.z, B.w}, ss[4] = {S.x, S.y, S.z, S.w}, kk[4] = {K.x, K.y, K.z, K.w};
+                const int32_t a0[4] = {A0.x, A0.y, A0.z, A0.w}, a1[4] = {A1.x, A1.y, A1.z, A1.w};
+                const int32_t a2[4] = {A2.x, A2.y, A2.z, A2.w}, a3[4] = {A3.x, A3.y, A3.z, A3.w};
+                int64_t bs[4], sl[4];
+                int32_t sk[4];
+#pragma unroll
+                for (int i = 0; i < 4; i++) {
+                    const uint32_t m = (m4 >> (8 * i)) & 0xffu;
+                    bs[i] = !ok ? 0 : m == 1 ? CAP_MAX : bb[i];
+                    sl[i] = !ok || m == 1 ? 0 : ss[i];
+                    sk[i] = !ok ? 0 : m == 2 ? int32_t(CAP_MAX) : kk[i];
+                }
+                const uint8_t *lab = c.out + (int64_t(p) * a.nlam + j0) * n;
+#pragma unroll
+                for (int jj = 0; jj < VLAM4; jj++) {
+                    const int j = min(jj, nj - 1);
+                    const uint8_t *l = lab + int64_t(j) * n + q;
+                    const int64_t lam = a.lambdas[j0 + j];
+                    const uint32_t L = *reinterpret_cast<const uint32_t *>(l);
+                    // off-grid neighbours count as source side (their arcs are 0 anyway)
+                    const uint32_t U = y > 0 ? *reinterpret_cast<const uint32_t *>(l - W) : 0x01010101u;
+                    const uint32_t D = y + 1 < a.H ? *reinterpret_cast<const uint32_t *>(l + W) : 0x01010101u;
+                    const uint32_t lb = x > 0 ? l[-1] : 1u, rb = x + 4 < W ? l[4] : 1u;
+                    const uint32_t left = (L << 8) | lb, right = (L >> 8) | (rb << 24);
+                    int64_t v = 0;
+#pragma unroll
+                    for (int i = 0; i < 4; i++) {
+                        const int sh = 8 * i;
+                        const SS src_side = SS(sk[i]) + SS((left >> sh) & 1u ? 0 : a0[i]) +
+                                            SS((right >> sh) & 1u ? 0 : a1[i]) + SS((U >> sh) & 1u ? 0 : a2[i]) +
+                                            SS((D >> sh) & 1u ? 0 : a3[i]);
+                        v += (L >> sh) & 1u ? int64_t(src_side) : bs[i] + lam * sl[i];
+                    }
+                    cost[jj] += jj < nj ? v : 0;
+                }
+            }
+            __syncthreads();
+#pragma unroll
+            for (int jj = 0; jj < VLAM4; jj++) {
+                int64_t v = cost[jj];
+                for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+                if ((threadIdx.x & 31) == 0 && v) atomicAdd(&s_acc[jj], (unsigned long long)v);
+            }
+            __syncthreads();
+            if (threadIdx.x < nj && s_acc[threadIdx.x])
+                atomicAdd(acc + int64_t(p) * a.nlam + j0 + threadIdx.x, s_acc[threadIdx.x]);
+            __syncthreads();
+        }
+    }
+}
+
+__global__ void k_flip_label(uint8_t *out, int64_t q) { out[q] ^= 1; }
 
 __global__ void k_verify_check(Ctx c, int64_t nplanes, const unsigned long long *acc) {
     for (int64_t plane = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; plane < nplanes;

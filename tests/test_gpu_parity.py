@@ -440,7 +440,8 @@ def test_seed_batches_on_edge_shapes(engine, mode):
     from paper_1509_06004_b200 import _native
     rng = np.random.default_rng(11)
     lams = [1, 3, 8, 20]
-    for (w, h) in [(1, 7), (9, 1), (33, 2), (31, 33), (65, 34)]:
+    # W % 4 == 0 shapes take the 4-pixel-group certificate kernel
+    for (w, h) in [(1, 7), (9, 1), (33, 2), (31, 33), (65, 34), (4, 5), (8, 1), (36, 3), (64, 33)]:
         n = w * h
         probs = []
         for k in range(9):   # >= warm_min_problems: warm-start chains
@@ -489,3 +490,26 @@ def test_c4_all_lambdas_both_schedulers(engine, mode):
         s.close()
     assert flows[0].tolist() == flows_a
     assert [int(l.sum()) for l in labels[0]] == fg_a
+
+
+@pytest.mark.parametrize("mode,vec", [(0, 1), (1, 1), (1, 0)])
+def test_integrity_check_catches_a_corrupted_cut(engine, mode, vec):
+    """The device certificate (cut cost of every emitted mask == its flow,
+    grid.py:159-178 / supergraph.py:181-186) rejects a batch whose emitted
+    mask was corrupted (knob verify=2 flips one label before the check), in
+    both schedulers and with both certificate kernels (verify_vec: 4-pixel
+    groups, W % 4 == 0 here, or per pixel); the same batch passes with
+    verify=1."""
+    from paper_1509_06004_b200 import _native
+    from paper_1509_06004_b200.solvers import NonMaximalFlowError
+    probs = synth.generate(500, 375, 2, 2, rng_seed=3, types=("A", "B")).problems
+    for verify in (1, 2):
+        s = _native.Solver(0, **{"async": mode}, verify=verify, verify_vec=vec)
+        try:
+            if verify == 1:
+                s.solve_seed_batch(500, 375, probs, synth.L20, "auto")
+            else:
+                with pytest.raises(NonMaximalFlowError, match="integrity"):
+                    s.solve_seed_batch(500, 375, probs, synth.L20, "auto")
+        finally:
+            s.close()
