@@ -181,49 +181,76 @@ __global__ void __launch_bounds__(NT) k_load_comp(Ctx c, CompArgs a) {
 // fixpoint, tiles re-listed while their halo keeps changing.
 // ---------------------------------------------------------------------------
 
-// Seed a BFS phase: list tile t if it holds a seed pixel, and every
-// neighbour facing a seed on t's border -- a seed never "changes", so the
-// relaxation of t alone would never hand it across the tile boundary.
-// `seeds` is this thread's bit set of seed pixels among its PPT pixels.
-__device__ __forceinline__ void seed_with_halo(const Ctx &c, int64_t t, unsigned seeds) {
-    __shared__ int s_sides;
-    if (threadIdx.x == 0) s_sides = 0;
-    __syncthreads();
-    int any = 0, sides = 0;
-    for (int j = 0; j < PPT; j++) {
-        if (!((seeds >> j) & 1)) continue;
-        int i = threadIdx.x + j * NT, lx = i & (TW - 1), ly = i / TW;
-        any = 1;
-        sides |= (lx == 0 ? 1 << DL : 0) | (lx == TW - 1 ? 1 << DR : 0) |
-                 (ly == 0 ? 1 << DU : 0) | (ly == TH - 1 ? 1 << DD : 0);
+// Full-batch scans (relabel / seed / label / emit / advance in the
+// step-synchronous mode) run one WARP per tile: lane l owns column l, and
+// row r of the tile is pixel l + 32 r (TW == 32), so every row is one
+// coalesced 128-byte access and a tile needs no block barrier.  Warps take
+// their grid-stride tiles 32 at a time, testing the per-grid predicate
+// (live, due) lane-parallel, so a skipped tile costs no load round trip of
+// its own (one CTA per tile spent ~100 us a scan on C5, ~70% of whose tiles
+// a rolling step skips).
+static_assert(TW == 32 && TH == 32, "warp-per-tile scans assume 32x32 tiles");
+// rows loaded before any store of the batch (stores may alias the loads, so
+// the compiler cannot hoist the next row's loads above them)
+constexpr int SCAN_ROWS = 8;
+template <class Pred, class F>
+__device__ __forceinline__ void for_tiles(const Ctx &c, Pred pred, F f) {
+    const int lane = threadIdx.x & 31;
+    const int64_t w0 = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+    const int64_t G = (int64_t(gridDim.x) * blockDim.x) >> 5;
+    for (int64_t r = 0; w0 + r * G < c.ntiles; r += 32) {
+        const int64_t t = w0 + (r + lane) * G;
+        unsigned m = __ballot_sync(0xffffffffu, t < c.ntiles && pred(c.tile_grid[t]));
+        while (m) {
+            const int k = __ffs(m) - 1;
+            m &= m - 1;
+            f(w0 + (r + k) * G, lane);
+        }
     }
-    if (sides) atomicOr(&s_sides, sides);
-    any = __syncthreads_or(any);
-    if (threadIdx.x == 0 && any) {
+}
+
+// Seed a BFS phase (warp per tile): list tile t if it holds a seed pixel,
+// and every neighbour facing a seed on t's border -- a seed never
+// "changes", so the relaxation of t alone would never hand it across the
+// tile boundary.  `seeds` bit r = pixel (lane, row r) is a seed.
+__device__ __forceinline__ void seed_with_halo(const Ctx &c, int64_t t, unsigned seeds, int lane) {
+    const unsigned cols = __ballot_sync(0xffffffffu, seeds != 0);
+    const unsigned top = __ballot_sync(0xffffffffu, seeds & 1u), bottom = __ballot_sync(0xffffffffu, seeds >> (TH - 1));
+    if (lane == 0 && cols) {
+        const int sides = (cols & 1u ? 1 << DL : 0) | (cols >> 31 ? 1 << DR : 0) | (top ? 1 << DU : 0) |
+                          (bottom ? 1 << DD : 0);
         TileGeo g = tile_geo(c, int32_t(t));
         seed_tile(c, int32_t(t));
         for (int s = 0; s < 4; s++)
-            if (((s_sides >> s) & 1) && g.nb[s] >= 0) seed_tile(c, g.nb[s]);
+            if (((sides >> s) & 1) && g.nb[s] >= 0) seed_tile(c, g.nb[s]);
     }
-    __syncthreads();
+}
+
+__device__ __forceinline__ int64_t warp_sum64(int64_t v) {
+    for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    return v;
 }
 
 // h = 1 on pixels with sink residual (w < 0), HINF elsewhere; lists every
 // tile holding such a pixel (and its neighbours facing one).  Tiles of
 // finished grids are left untouched.
 __global__ void __launch_bounds__(NT) k_gr_init(Ctx c) {
-    for (int64_t t = blockIdx.x; t < c.ntiles; t += gridDim.x) {
-        const int32_t g = c.tile_grid[t];
-        if (!c.live[g] || (c.keeph && c.keeph[g])) continue;
+    for_tiles(c, [&](int32_t g) { return c.live[g] && !(c.keeph && c.keeph[g]); }, [&](int64_t t, int lane) {
         unsigned seeds = 0;
-        for (int j = 0; j < PPT; j++) {
-            int64_t p = t * TPIX + threadIdx.x + j * NT;
-            int32_t wv = c.w[p];
-            c.h[p] = wv < 0 ? 1 : HINF;
-            seeds |= unsigned(wv < 0) << j;
+        const int64_t p0 = t * TPIX + lane;
+#pragma unroll
+        for (int r0 = 0; r0 < TH; r0 += SCAN_ROWS) {
+            int32_t wv[SCAN_ROWS];   // loads of the batch before its stores (they may alias)
+#pragma unroll
+            for (int k = 0; k < SCAN_ROWS; k++) wv[k] = c.w[p0 + TW * (r0 + k)];
+#pragma unroll
+            for (int k = 0; k < SCAN_ROWS; k++) {
+                c.h[p0 + TW * (r0 + k)] = wv[k] < 0 ? 1 : HINF;
+                seeds |= unsigned(wv[k] < 0) << (r0 + k);
+            }
         }
-        seed_with_halo(c, t, seeds);
-    }
+        seed_with_halo(c, t, seeds, lane);
+    });
 }
 
 // ---------------------------------------------------------------------------
@@ -235,21 +262,20 @@ __global__ void __launch_bounds__(NT) k_gr_init(Ctx c) {
 // Lists every tile of a live grid that holds an active pixel (w > 0,
 // h < HINF); counts active pixels per grid.
 __global__ void __launch_bounds__(NT) k_seed_push(Ctx c) {
-    for (int64_t t = blockIdx.x; t < c.ntiles; t += gridDim.x) {
-        int32_t gid = c.tile_grid[t];
-        if (!c.live[gid]) continue;
+    for_tiles(c, [&](int32_t g) { return c.live[g] != 0; }, [&](int64_t t, int lane) {
         int a = 0;
-        for (int j = 0; j < PPT; j++) {
-            int64_t p = t * TPIX + threadIdx.x + j * NT;
+#pragma unroll 8
+        for (int r = 0; r < TH; r++) {
+            const int64_t p = t * TPIX + lane + TW * r;
             a += c.w[p] > 0 && c.h[p] < HINF;
-        }
+        }   // no stores: the loads pipeline
         for (int o = 16; o; o >>= 1) a += __shfl_xor_sync(0xffffffffu, a, o);
-        if ((threadIdx.x & 31) == 0 && a) atomicAdd(&c.act[gid], a);
-        if (__syncthreads_or(a) && threadIdx.x == 0) {
+        if (lane == 0 && a) {
+            atomicAdd(&c.act[c.tile_grid[t]], a);
             if (c.tfresh) c.tfresh[t] = 1;   // its heights are this relabel's exact distances
             seed_tile(c, int32_t(t));
         }
-    }
+    });
 }
 
 // Reset the worklist (sweep mode) or queue (persistent mode) state for a
@@ -386,20 +412,22 @@ __global__ void __launch_bounds__(1024) k_unspoil(Ctx c, int32_t ngrids) {
 // ---------------------------------------------------------------------------
 
 __global__ void __launch_bounds__(NT) k_lab_seed(Ctx c) {
-    for (int64_t t = blockIdx.x; t < c.ntiles; t += gridDim.x) {
-        const int32_t gid = c.tile_grid[t];
-        if (!grid_due(c, gid)) continue;
-        const GridDesc &gd = c.grids[gid];
-        if (grid_swapped(c, gd)) continue;
+    for_tiles(c, [&](int32_t g) { return grid_due(c, g) && !grid_swapped(c, c.grids[g]); }, [&](int64_t t, int lane) {
         unsigned seeds = 0;
-        for (int j = 0; j < PPT; j++) {
-            int64_t p = t * TPIX + threadIdx.x + j * NT;
-            int v = c.w[p] > 0;
-            c.lab[p] = uint8_t(v);
-            seeds |= unsigned(v) << j;
+        const int64_t p0 = t * TPIX + lane;
+#pragma unroll
+        for (int r0 = 0; r0 < TH; r0 += SCAN_ROWS) {
+            int32_t wv[SCAN_ROWS];
+#pragma unroll
+            for (int k = 0; k < SCAN_ROWS; k++) wv[k] = c.w[p0 + TW * (r0 + k)];
+#pragma unroll
+            for (int k = 0; k < SCAN_ROWS; k++) {
+                c.lab[p0 + TW * (r0 + k)] = uint8_t(wv[k] > 0);
+                seeds |= unsigned(wv[k] > 0) << (r0 + k);
+            }
         }
-        seed_with_halo(c, t, seeds);
-    }
+        seed_with_halo(c, t, seeds, lane);
+    });
 }
 
 // Label bytes in row-major order and the per-grid unused sink residual.
@@ -408,32 +436,39 @@ __global__ void __launch_bounds__(NT) k_lab_seed(Ctx c) {
 //   composite:   swapped column ? ~sink side : source side
 //                (supergraph.py:201-206)
 __global__ void __launch_bounds__(NT) k_emit(Ctx c) {
-    __shared__ int64_t red[NT / 32];
-    for (int64_t t = blockIdx.x; t < c.ntiles; t += gridDim.x) {
-        if (!grid_due(c, c.tile_grid[t])) continue;
-        TileGeo g = tile_geo(c, int32_t(t));
+    for_tiles(c, [&](int32_t g) { return grid_due(c, g); }, [&](int64_t t, int lane) {
+        const TileGeo g = tile_geo(c, int32_t(t));
         const GridDesc &gd = c.grids[g.g];
+        const bool comp = gd.kind == 1, swapped = !comp && grid_swapped(c, gd);
+        const int x = g.x0 + lane;
+        const bool cswap = comp && x < g.W && c.colswap[gd.colswap_off + x];
+        const int64_t off = comp ? gd.out_off : (int64_t(gd.prob) * c.nlam + c.cur_lam[g.g]) * (int64_t(g.W) * g.H);
         int64_t drain = 0;
-        for (int j = 0; j < PPT; j++) {
-            int i = threadIdx.x + j * NT;
-            int x = g.x0 + (i & (TW - 1)), y = g.y0 + i / TW;
-            if (x >= g.W || y >= g.H) continue;
-            int64_t p = t * TPIX + i;
-            int32_t wv = c.w[p];
-            if (wv < 0) drain -= wv;
-            uint8_t v;
-            if (gd.kind == 1) {
-                v = c.colswap[gd.colswap_off + x] ? uint8_t(c.h[p] >= HINF) : c.lab[p];
-            } else {
-                v = grid_swapped(c, gd) ? uint8_t(c.h[p] < HINF) : c.lab[p];
+        const int rows = min(TH, g.H - g.y0);
+        // h decides the side when the grid (column) is swapped, lab otherwise
+        const bool use_h = comp ? cswap : swapped;
+        const bool h_inf_side = comp;   // composite swapped column: side = h >= HINF
+        if (x < g.W)
+#pragma unroll
+            for (int r0 = 0; r0 < TH; r0 += SCAN_ROWS) {
+                int32_t wv[SCAN_ROWS];
+                uint8_t v[SCAN_ROWS];
+#pragma unroll
+                for (int k = 0; k < SCAN_ROWS; k++) {
+                    const int64_t p = t * TPIX + lane + TW * (r0 + k);
+                    const bool in = r0 + k < rows;
+                    wv[k] = in ? c.w[p] : 0;
+                    v[k] = !in ? 0 : use_h ? uint8_t((c.h[p] >= HINF) == h_inf_side) : c.lab[p];
+                }
+#pragma unroll
+                for (int k = 0; k < SCAN_ROWS; k++) {
+                    if (wv[k] < 0) drain -= wv[k];
+                    if (r0 + k < rows) c.out[off + int64_t(g.y0 + r0 + k) * g.W + x] = v[k];
+                }
             }
-            const int64_t off = gd.kind == 1 ? gd.out_off
-                                             : (int64_t(gd.prob) * c.nlam + c.cur_lam[g.g]) * (int64_t(g.W) * g.H);
-            c.out[off + int64_t(y) * g.W + x] = v;
-        }
-        int64_t s = block_sum64(drain, red);
-        if (threadIdx.x == 0 && s) atomicAdd((unsigned long long *)&c.drain[g.g], (unsigned long long)s);
-    }
+        drain = warp_sum64(drain);
+        if (lane == 0 && drain) atomicAdd((unsigned long long *)&c.drain[g.g], (unsigned long long)drain);
+    });
 }
 
 }  // namespace pmf
@@ -486,30 +521,41 @@ __global__ void k_finalize(Ctx c, int32_t ngrids) {
 // embedded swapped, of sink capacity (w -=).
 __global__ void __launch_bounds__(NT) k_advance_tiles(Ctx c, SeedArgs a) {
     const int64_t n = int64_t(a.W) * a.H;
-    for (int64_t t = blockIdx.x; t < c.ntiles; t += gridDim.x) {
-        if (!grid_due(c, c.tile_grid[t])) continue;
-        TileGeo g = tile_geo(c, int32_t(t));
+    for_tiles(c, [&](int32_t g) { return grid_due(c, g) && c.cur_lam[g] + 1 < c.grids[g].lam_end; },
+              [&](int64_t t, int lane) {
+        const TileGeo g = tile_geo(c, int32_t(t));
         const GridDesc &gd = c.grids[g.g];
         const int cur = c.cur_lam[g.g];
-        if (cur + 1 >= gd.lam_end) continue;
         const int64_t dl = a.lambdas[cur + 1] - a.lambdas[cur];
         const int sign = c.swapflag[gd.prob] ? -1 : 1;
-        const int64_t po = a.plane_off[gd.prob];
-        for (int j = 0; j < PPT; j++) {
-            int i = threadIdx.x + j * NT;
-            int x = g.x0 + (i & (TW - 1)), y = g.y0 + i / TW;
-            if (x >= g.W || y >= g.H) continue;
-            const int64_t q = int64_t(y) * a.W + x;
-            if (a.mask[int64_t(gd.prob) * n + q] == 1) continue;   // fg seed: CAP_MAX either way
-            c.w[t * TPIX + i] += int32_t(sign * dl * int64_t(a.slope[po + q]));
-        }
-    }
+        const int32_t *slope = a.slope + a.plane_off[gd.prob];
+        const uint8_t *mask = a.mask + int64_t(gd.prob) * n;
+        const int x = g.x0 + lane, rows = min(TH, g.H - g.y0);
+        if (x < g.W)
+#pragma unroll
+            for (int r0 = 0; r0 < TH; r0 += SCAN_ROWS) {
+                int32_t d[SCAN_ROWS], wv[SCAN_ROWS];
+#pragma unroll
+                for (int k = 0; k < SCAN_ROWS; k++) {
+                    const bool in = r0 + k < rows;
+                    const int64_t q = int64_t(g.y0 + r0 + k) * a.W + x;
+                    // fg seed: CAP_MAX either way (both loads issued, no load behind a load)
+                    const uint8_t m = in ? mask[q] : 1;
+                    const int32_t sv = in ? slope[q] : 0;
+                    d[k] = m != 1 ? int32_t(sign * dl * int64_t(sv)) : 0;
+                    wv[k] = in ? c.w[t * TPIX + lane + TW * (r0 + k)] : 0;
+                }
+#pragma unroll
+                for (int k = 0; k < SCAN_ROWS; k++)
+                    if (d[k]) c.w[t * TPIX + lane + TW * (r0 + k)] = wv[k] + d[k];
+            }
+    });
 }
 
 // Integrity certificate per (problem, lambda) (grid.py:159-178 cut_cost;
 // the reference checks it in split(), supergraph.py:181-186, and in the RPC
 // client, rpc.py:328-331): the cut cost of the emitted mask of the ORIGINAL
-// graph must equal the flow.  One CTA per (problem, lambda) plane.
+// graph must equal the flow.
 // One CTA per (problem, chunk of pixels): a thread loads its VPX pixels'
 // terms once per VLAM lambdas and then issues every label load of the pass
 // unconditionally (no load behind a branch on another load: the pass is
