@@ -219,7 +219,7 @@ struct pmf_solver {
     int grid_div = 1;           // use 1/grid_div of the GPU's resident CTAs (solvers sharing a GPU)
     int async_mode = -1;        // seed batches: one persistent kernel, every grid on its own phase machine
                                 // (1), step-synchronous phases (0), or -1: async up to async_max_tiles tiles
-    int async_max_tiles = 30000;
+    int async_max_tiles = 20000;
     int async_max_grid_tiles = 1024;   // ... and grids of at most this many tiles on average
     int async_cont = 1, async_prefetch = 1;
     int async_spec = 1;         // drained discharge -> speculative label closure instead of a confirming relabel
