@@ -148,6 +148,21 @@ int pmf_solve_composites(pmf_solver *s, int32_t ncomp,
                          int64_t *flow_out, uint8_t *const *labels_out);
 
 /*
+ * pmf_solve_composites with int32 planes: the wire request's capacity arrays
+ * (wire.py:19 "six i32 arrays", decoded at wire.py:180-186) are read in
+ * place, without the int64 GridGraph copies decode_request makes; same
+ * checks (PMF_ERR_RANGE outside [0, CAP_MAX]) and outputs.  Serves the
+ * GPU worker handler wire.serve_payload (rpc.py:147-162 _solve_and_reply).
+ */
+int pmf_solve_composites_i32(pmf_solver *s, int32_t ncomp,
+                             const int32_t *width, const int32_t *height,
+                             const int32_t *const *src, const int32_t *const *snk,
+                             const int32_t *const *nbr,
+                             const int32_t *nseg, const int32_t *const *seg_off,
+                             const int32_t *const *seg_w, const uint8_t *const *seg_swapped,
+                             int64_t *flow_out, uint8_t *const *labels_out);
+
+/*
  * Build and solve the lambda families of nprob SeedProblems
  * (parametric.py:80-130) sharing one width x height, over nlam lambda
  * values (strictly increasing, validated by the caller), on device.

@@ -25,7 +25,8 @@ SWAP_MODES = {"auto": 0, "on": 1, "off": 2}
 EXPORTS = ("pmf_solver_create", "pmf_solver_destroy", "pmf_solver_set", "pmf_last_error",
            "pmf_solver_stats", "pmf_solver_stream", "pmf_solve_composites", "pmf_solve_seed_batch",
            "pmf_seed_stage", "pmf_seed_run", "pmf_seed_fetch", "pmf_debug_state",
-           "pmf_debug_trace", "pmf_debug_busy", "pmf_seed_score", "pmf_debug_phases")
+           "pmf_debug_trace", "pmf_debug_busy", "pmf_seed_score", "pmf_debug_phases",
+           "pmf_solve_composites_i32")
 
 
 class NativeUnavailable(RuntimeError):
@@ -182,18 +183,20 @@ class Solver:
             pass
 
     # ---------------------------------------------------------------- solves
-    def solve_composites(self, items):
+    def solve_composites(self, items, i32: bool = False):
         """items: [(width, height, src, snk, nbr, segments)] with segments a
-        list of (offset, width, swapped) or None.  Returns [(flow, labels)]."""
+        list of (offset, width, swapped) or None.  Returns [(flow, labels)].
+        i32: the planes are int32 (wire requests) and are read in place."""
         k = len(items)
+        dt = np.int32 if i32 else np.int64
         keep = []
         widths = np.array([it[0] for it in items], np.int32)
         heights = np.array([it[1] for it in items], np.int32)
         srcs, snks, nbrs, nsegs, offs, wids, sws, labs = [], [], [], [], [], [], [], []
         for (w, h, src, snk, nbr, segs) in items:
-            srcs.append(np.ascontiguousarray(src, np.int64))
-            snks.append(np.ascontiguousarray(snk, np.int64))
-            nbrs.append(np.ascontiguousarray(nbr, np.int64))
+            srcs.append(np.ascontiguousarray(src, dt))
+            snks.append(np.ascontiguousarray(snk, dt))
+            nbrs.append(np.ascontiguousarray(nbr, dt))
             segs = list(segs or ())
             nsegs.append(len(segs))
             offs.append(np.array([s[0] for s in segs] or [0], np.int32))
@@ -204,7 +207,8 @@ class Solver:
         flows = np.zeros(k, np.int64)
         nseg = np.array(nsegs, np.int32)
         P = ctypes.POINTER
-        rc = self._lib.pmf_solve_composites(
+        fn = self._lib.pmf_solve_composites_i32 if i32 else self._lib.pmf_solve_composites
+        rc = fn(
             self._h, k, widths.ctypes.data_as(P(ctypes.c_int32)),
             heights.ctypes.data_as(P(ctypes.c_int32)), _ptrs(srcs), _ptrs(snks), _ptrs(nbrs),
             nseg.ctypes.data_as(P(ctypes.c_int32)), _ptrs(offs), _ptrs(wids), _ptrs(sws),

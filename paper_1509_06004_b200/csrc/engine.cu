@@ -1635,12 +1635,14 @@ int pmf_solver_stats(const pmf_solver *s, pmf_stats *out) {
     return 0;
 }
 
-int pmf_solve_composites(pmf_solver *s, int32_t ncomp, const int32_t *width, const int32_t *height,
-                         const int64_t *const *src, const int64_t *const *snk,
-                         const int64_t *const *nbr, const int32_t *nseg,
-                         const int32_t *const *seg_off, const int32_t *const *seg_w,
-                         const uint8_t *const *seg_swapped, int64_t *flow_out,
-                         uint8_t *const *labels_out) {
+}  // extern "C"
+
+// T = int64_t (GridGraph planes) or int32_t (wire planes, wire.py:19)
+template <class T>
+static int solve_composites_t(pmf_solver *s, int32_t ncomp, const int32_t *width, const int32_t *height,
+                              const T *const *src, const T *const *snk, const T *const *nbr,
+                              const int32_t *nseg, const int32_t *const *seg_off, const int32_t *const *seg_w,
+                              const uint8_t *const *seg_swapped, int64_t *flow_out, uint8_t *const *labels_out) {
     if (!s || ncomp < 1 || !width || !height || !src || !snk || !nbr || !flow_out || !labels_out)
         return fail(PMF_ERR_ARG, "bad arguments");
     CK(cudaSetDevice(s->device));
@@ -1679,7 +1681,7 @@ int pmf_solve_composites(pmf_solver *s, int32_t ncomp, const int32_t *width, con
         const int64_t n = int64_t(width[c]) * height[c], off = s->comp_off[c];
         const int64_t lo = (task - chunk_base[c]) * kChunk, hi = std::min(6 * n, lo + kChunk);
         for (int64_t i = lo; i < hi; i++) {   // element i of [src | snk | nbr(4n)]
-            const int64_t v = i < n ? src[c][i] : i < 2 * n ? snk[c][i - n] : nbr[c][i - 2 * n];
+            const int64_t v = int64_t(i < n ? src[c][i] : i < 2 * n ? snk[c][i - n] : nbr[c][i - 2 * n]);
             if (v < 0 || v > CAP_MAX) {
                 terr.set(PMF_ERR_RANGE, "composite capacity outside [0, CAP_MAX]");
                 return;
@@ -1720,13 +1722,11 @@ int pmf_solve_composites(pmf_solver *s, int32_t ncomp, const int32_t *width, con
     const Layout &L = s->lay;
     const int64_t G = int64_t(L.grids.size());
     const size_t lab_bytes = size_t((L.out_bytes + 7) / 8) * 8;
-    if ((rc = s->h_out.ensure(lab_bytes + size_t(G) * 16))) return rc;
+    if ((rc = s->h_out.ensure(lab_bytes + size_t(G) * 8))) return rc;
     uint8_t *ho = s->h_out.as<uint8_t>();
     int64_t *hsnk = (int64_t *)(ho + lab_bytes);
-    int64_t *hdr = hsnk + G;
     CK(cudaMemcpyAsync(ho, s->d_out.p, L.out_bytes, cudaMemcpyDeviceToHost, s->st));
     CK(cudaMemcpyAsync(hsnk, s->d_flows.p, G * 8, cudaMemcpyDeviceToHost, s->st));
-    (void)hdr;
     if ((rc = run_end(s))) return rc;
     for (int c = 0; c < ncomp; c++) {
         flow_out[c] = hsnk[c];
@@ -1735,6 +1735,28 @@ int pmf_solve_composites(pmf_solver *s, int32_t ncomp, const int32_t *width, con
     s->stats.h2d_bytes = total_px * 6 * 4;
     s->stats.d2h_bytes = L.out_bytes + G * 16;
     return 0;
+}
+
+extern "C" {
+
+int pmf_solve_composites(pmf_solver *s, int32_t ncomp, const int32_t *width, const int32_t *height,
+                         const int64_t *const *src, const int64_t *const *snk,
+                         const int64_t *const *nbr, const int32_t *nseg,
+                         const int32_t *const *seg_off, const int32_t *const *seg_w,
+                         const uint8_t *const *seg_swapped, int64_t *flow_out,
+                         uint8_t *const *labels_out) {
+    return solve_composites_t<int64_t>(s, ncomp, width, height, src, snk, nbr, nseg, seg_off, seg_w,
+                                       seg_swapped, flow_out, labels_out);
+}
+
+int pmf_solve_composites_i32(pmf_solver *s, int32_t ncomp, const int32_t *width, const int32_t *height,
+                             const int32_t *const *src, const int32_t *const *snk,
+                             const int32_t *const *nbr, const int32_t *nseg,
+                             const int32_t *const *seg_off, const int32_t *const *seg_w,
+                             const uint8_t *const *seg_swapped, int64_t *flow_out,
+                             uint8_t *const *labels_out) {
+    return solve_composites_t<int32_t>(s, ncomp, width, height, src, snk, nbr, nseg, seg_off, seg_w,
+                                       seg_swapped, flow_out, labels_out);
 }
 
 // CTA-busy milliseconds of the last asynchronous run, summed over CTAs:
