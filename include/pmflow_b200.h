@@ -112,6 +112,8 @@ int pmf_solver_destroy(pmf_solver *s);
  * "verify" (device cut-cost == flow certificate, default on; 2 = test hook
  *   that corrupts one emitted label first, so the check must fail),
  * "verify_vec" (4-pixel-group certificate kernel for W % 4 == 0, default on),
+ * "comp_split" (composites: one grid per segment span that no arc leaves,
+ *   default on; otherwise one grid per composite),
  * "fresh_skip" (skip the no-op local relabel of a first pass on exact
  * heights), "push_budget_add", "push_mode", "push_flush", "push_minb",
  * "grid_div", "relax_cap", "bfs_multi", "phase_log" (diagnostics).

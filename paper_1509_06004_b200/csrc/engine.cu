@@ -153,6 +153,8 @@ struct Layout {
         g.prob = prob;
         g.lam = lam;
         g.lam_end = lam_end;
+        g.pitch = W;
+        g.xoff = 0;
         int64_t nt = int64_t(g.ntx) * g.nty;
         tile_grid.insert(tile_grid.end(), size_t(nt), int32_t(grids.size()));
         for (int32_t ty = 0; ty < g.nty; ty++)
@@ -165,6 +167,18 @@ struct Layout {
         out_bytes += int64_t(W) * H;
         pixels += int64_t(W) * H;
         grids.push_back(g);
+    }
+    // One column span [xoff, xoff + W) of a pitch x H composite whose output
+    // starts at out_base (reserved by the caller): a grid of its own.
+    void add_span(int32_t W, int32_t H, int32_t colswap_off, int32_t comp, int64_t out_base, int32_t pitch,
+                  int32_t xoff) {
+        const int64_t ob = out_bytes, px = pixels;
+        add(W, H, 1, colswap_off, comp, 0, 1);
+        out_bytes = ob;
+        pixels = px + int64_t(W) * H;
+        grids.back().out_off = out_base;
+        grids.back().pitch = pitch;
+        grids.back().xoff = xoff;
     }
 };
 
@@ -239,7 +253,9 @@ struct pmf_solver {
     Layout lay;
     std::vector<int32_t> ones, curlam0;
     std::vector<uint8_t> colswap;
-    std::vector<int64_t> comp_off;
+    std::vector<int64_t> comp_off, grid_off;
+    int comp_any_split = 0;
+    int comp_split = 1;         // composites: one grid per isolated segment span
     SeedStage stage;
     Ctx ctx{};
     std::vector<cudaEvent_t> ev_pool;
@@ -1512,11 +1528,15 @@ int comp_run_t(pmf_solver *s, int ncomp, int64_t total_px) {
     CK(cudaMemcpyAsync(s->d_colswap.p, s->colswap.data(), s->colswap.size(), cudaMemcpyHostToDevice, s->st));
     const Ctx &c = s->ctx;
     s->tmark(C_H2D);
-    if ((rc = s->d_in32.ensure(size_t(total_px) * 6 * 4)) || (rc = s->d_off.ensure(size_t(ncomp) * 8)))
-        return rc;
+    const size_t G = s->lay.grids.size();
+    if ((rc = s->d_in32.ensure(size_t(total_px) * 6 * 4)) || (rc = s->d_off.ensure(G * 8))) return rc;
     int32_t *din = s->d_in32.as<int32_t>();
     CK(cudaMemcpyAsync(din, s->h_in32.p, size_t(total_px) * 6 * 4, cudaMemcpyHostToDevice, s->st));
-    CK(cudaMemcpyAsync(s->d_off.p, s->comp_off.data(), size_t(ncomp) * 8, cudaMemcpyHostToDevice, s->st));
+    s->grid_off.resize(G);   // per grid: its composite's plane offset
+    for (size_t g = 0; g < G; g++) s->grid_off[g] = s->comp_off[size_t(s->lay.grids[g].prob)];
+    CK(cudaMemcpyAsync(s->d_off.p, s->grid_off.data(), G * 8, cudaMemcpyHostToDevice, s->st));
+    // split composites: bridge / uncovered columns belong to no grid and stay 0
+    if (s->comp_any_split) CK(cudaMemsetAsync(s->d_out.p, 0, size_t(s->lay.out_bytes), s->st));
     s->tmark(C_BUILD);
     CompArgs a{din, din + total_px, din + 2 * total_px, s->d_off.as<int64_t>()};
     LAUNCH(s, (k_load_comp<E><<<s->grid_full, NT, 0, s->st>>>(c, a)));
@@ -1599,6 +1619,7 @@ int pmf_solver_set(pmf_solver *s, const char *name, int64_t v) {
     else if (k == "push_budget_add" && v >= 0 && v < (int64_t(1) << 30)) s->push_budget_add = int(v);
     else if (k == "verify" && v >= 0 && v <= 2) s->verify = int(v);
     else if (k == "verify_vec") s->verify_vec = v != 0;
+    else if (k == "comp_split") s->comp_split = v != 0;
     else if (k == "rolling") s->rolling = v != 0;
     else if (k == "push_minb" && (v == 1 || v == 2)) s->push_minb = int(v);
     else if (k == "grid_div" && v >= 1 && v <= 64) s->grid_div = int(v);
@@ -1650,20 +1671,22 @@ static int solve_composites_t(pmf_solver *s, int32_t ncomp, const int32_t *width
     s->lay.clear();
     s->colswap.clear();
     s->comp_off.assign(size_t(ncomp), 0);
+    std::vector<int32_t> cs_off(size_t(ncomp), 0);
     int64_t total_px = 0;
     for (int c = 0; c < ncomp; c++) {
         if (width[c] < 1 || height[c] < 1) return fail(PMF_ERR_ARG, "composite %d: bad shape", c);
-        int32_t cs_off = int32_t(s->colswap.size());
+        cs_off[c] = int32_t(s->colswap.size());
         s->colswap.resize(s->colswap.size() + width[c], 0);
         int ns = nseg ? nseg[c] : 0;
         for (int k = 0; k < ns; k++) {
             int o = seg_off[c][k], w = seg_w[c][k];
             if (o < 0 || w < 0 || o + w > width[c])
                 return fail(PMF_ERR_ARG, "composite %d: segment %d outside the grid", c, k);
+            if (k > 0 && o < seg_off[c][k - 1] + seg_w[c][k - 1])
+                return fail(PMF_ERR_ARG, "composite %d: segment %d overlaps its predecessor", c, k);
             if (seg_swapped[c][k])
-                for (int x = o; x < o + w; x++) s->colswap[cs_off + x] = 1;
+                for (int x = o; x < o + w; x++) s->colswap[cs_off[c] + x] = 1;
         }
-        s->lay.add(width[c], height[c], 1, cs_off, c, 0, 1);
         s->comp_off[c] = total_px;
         total_px += int64_t(width[c]) * height[c];
     }
@@ -1692,35 +1715,106 @@ static int solve_composites_t(pmf_solver *s, int32_t ncomp, const int32_t *width
         }
     });
     if ((rc = terr.raise())) return rc;
-    std::vector<int64_t> mp(ncomp, 0), mx(ncomp, 0);
-    s->pool->run(ncomp, [&](int64_t c) {
-        const int64_t n = int64_t(width[c]) * height[c], off = s->comp_off[c];
+    // per (composite, band of rows) task: largest arc pair and the bound on
+    // any pixel's excess (its positive terminal plus all arc pairs); bands
+    // keep one large composite (a wire request) on every host thread
+    constexpr int32_t kBand = 64;
+    std::vector<int64_t> band_base(size_t(ncomp) + 1, 0);
+    for (int c = 0; c < ncomp; c++) band_base[size_t(c) + 1] = band_base[size_t(c)] + cdiv(height[c], kBand);
+    std::vector<int64_t> mp(size_t(band_base[size_t(ncomp)]), 0), mx(mp.size(), 0);
+    s->pool->run(band_base[size_t(ncomp)], [&](int64_t task) {
+        const int c = int(std::upper_bound(band_base.begin(), band_base.end(), task) - band_base.begin()) - 1;
+        const int32_t W = width[c], H = height[c];
+        const int32_t y0 = int32_t(task - band_base[size_t(c)]) * kBand, y1 = std::min(H, y0 + kBand);
+        const int64_t n = int64_t(W) * H, off = s->comp_off[c];
         const int32_t *nb = hin + 2 * total_px + 4 * off;
-        mp[c] = max_pair(nb, width[c], height[c]);
-        // bound on any pixel's excess: its positive terminal plus all arc pairs
+        mp[size_t(task)] = max_pair(nb, W, H, y0, y1);
         int64_t m = 0;
-        for (int64_t p = 0; p < n; p++) {
+        for (int64_t p = int64_t(y0) * W; p < int64_t(y1) * W; p++) {
             int64_t e = std::max<int64_t>(0, int64_t(hin[off + p]) - hin[total_px + off + p]);
             for (int d = 0; d < 4; d++) e += 2 * int64_t(nb[d * n + p]);
             m = std::max(m, e);
         }
-        mx[c] = m;
+        mx[size_t(task)] = m;
     });
     int64_t maxpair = 0, maxexcess = 0;
-    for (int c = 0; c < ncomp; c++) {
-        maxpair = std::max(maxpair, mp[c]);
-        maxexcess = std::max(maxexcess, mx[c]);
+    for (size_t k = 0; k < mp.size(); k++) {
+        maxpair = std::max(maxpair, mp[k]);
+        maxexcess = std::max(maxexcess, mx[k]);
     }
     if (maxexcess >= (int64_t(1) << 31) - 1)
         return fail(PMF_ERR_RANGE, "capacities too large for the int32 device state");
-    if ((rc = s->d_flows.ensure(size_t(ncomp) * 8))) return rc;
+    // Segments whose spans no arc leaves (bridge / uncovered columns all
+    // zero, no LEFT arc on a span's first column, no RIGHT arc on its last)
+    // are independent max-flow problems: each becomes a grid of its own
+    // (knob comp_split), solved and relabelled separately, writing its
+    // columns of the composite's output; the composite's flow is the sum.
+    // The reference's join() builds exactly such composites (zero bridge
+    // columns, supergraph.py:95-154).
+    // column -> segment of every composite (at cs_off), -1: bridge / uncovered
+    std::vector<int32_t> colseg(s->colswap.size(), -1);
+    std::vector<uint8_t> cand(size_t(ncomp), 0), leak(size_t(band_base[size_t(ncomp)]), 0);
+    for (int c = 0; c < ncomp; c++) {
+        const int ns = nseg ? nseg[c] : 0;
+        if (!s->comp_split || ns < 2) continue;
+        cand[size_t(c)] = 1;
+        for (int k = 0; k < ns; k++)
+            for (int x = seg_off[c][k]; x < seg_off[c][k] + seg_w[c][k]; x++) colseg[size_t(cs_off[c] + x)] = k;
+    }
+    s->pool->run(band_base[size_t(ncomp)], [&](int64_t task) {
+        const int c = int(std::upper_bound(band_base.begin(), band_base.end(), task) - band_base.begin()) - 1;
+        if (!cand[size_t(c)]) return;
+        const int32_t *sc = colseg.data() + cs_off[c];
+        const int32_t W = width[c], H = height[c];
+        const int32_t y0 = int32_t(task - band_base[size_t(c)]) * kBand, y1 = std::min(H, y0 + kBand);
+        const int64_t n = int64_t(W) * H, off = s->comp_off[c];
+        const int32_t *sp = hin + off, *kp = hin + total_px + off, *nb = hin + 2 * total_px + 4 * off;
+        for (int32_t x = 0; x < W; x++) {
+            const bool bridge = sc[x] < 0;
+            const bool ledge = x > 0 && sc[x - 1] != sc[x];
+            const bool redge = x + 1 < W && sc[x + 1] != sc[x];
+            if (!bridge && !ledge && !redge) continue;
+            for (int32_t y = y0; y < y1; y++) {
+                const int64_t q = int64_t(y) * W + x;
+                if (bridge ? (sp[q] | kp[q] | nb[q] | nb[n + q] | nb[2 * n + q] | nb[3 * n + q]) != 0
+                           : (ledge && nb[q]) || (redge && nb[n + q])) {
+                    leak[size_t(task)] = 1;
+                    return;
+                }
+            }
+        }
+    });
+    std::vector<uint8_t> split(size_t(ncomp), 0);
+    for (int c = 0; c < ncomp; c++) {
+        if (!cand[size_t(c)]) continue;
+        split[size_t(c)] = 1;
+        for (int64_t k = band_base[size_t(c)]; k < band_base[size_t(c) + 1]; k++)
+            if (leak[size_t(k)]) split[size_t(c)] = 0;
+    }
+    int any_split = 0;
+    std::vector<int64_t> comp_out(size_t(ncomp), 0);   // output offset per composite
+    for (int c = 0; c < ncomp; c++) {
+        comp_out[size_t(c)] = s->lay.out_bytes;
+        if (split[size_t(c)]) {
+            any_split = 1;
+            const int64_t base = s->lay.out_bytes;
+            s->lay.out_bytes += int64_t(width[c]) * height[c];
+            for (int k = 0; k < nseg[c]; k++)
+                s->lay.add_span(seg_w[c][k], height[c], cs_off[c] + seg_off[c][k], c, base, width[c],
+                                seg_off[c][k]);
+        } else {
+            s->lay.add(width[c], height[c], 1, cs_off[c], c, 0, 1);
+        }
+    }
+    s->comp_any_split = any_split;
+    const int64_t G = int64_t(s->lay.grids.size());
+    if ((rc = s->d_flows.ensure(size_t(G) * 8))) return rc;
     if ((rc = run_begin(s))) return rc;
     rc = maxpair <= 255 ? comp_run_t<EdgeU8>(s, ncomp, total_px) : comp_run_t<EdgeI32>(s, ncomp, total_px);
     if (rc) return rc;
     // outputs
     s->tmark(C_D2H);
     const Layout &L = s->lay;
-    const int64_t G = int64_t(L.grids.size());
     const size_t lab_bytes = size_t((L.out_bytes + 7) / 8) * 8;
     if ((rc = s->h_out.ensure(lab_bytes + size_t(G) * 8))) return rc;
     uint8_t *ho = s->h_out.as<uint8_t>();
@@ -1728,10 +1822,10 @@ static int solve_composites_t(pmf_solver *s, int32_t ncomp, const int32_t *width
     CK(cudaMemcpyAsync(ho, s->d_out.p, L.out_bytes, cudaMemcpyDeviceToHost, s->st));
     CK(cudaMemcpyAsync(hsnk, s->d_flows.p, G * 8, cudaMemcpyDeviceToHost, s->st));
     if ((rc = run_end(s))) return rc;
-    for (int c = 0; c < ncomp; c++) {
-        flow_out[c] = hsnk[c];
-        memcpy(labels_out[c], ho + L.grids[c].out_off, size_t(width[c]) * height[c]);
-    }
+    for (int c = 0; c < ncomp; c++) flow_out[c] = 0;
+    for (int64_t g = 0; g < G; g++) flow_out[L.grids[size_t(g)].prob] += hsnk[g];
+    for (int c = 0; c < ncomp; c++)
+        memcpy(labels_out[c], ho + comp_out[size_t(c)], size_t(width[c]) * height[c]);
     s->stats.h2d_bytes = total_px * 6 * 4;
     s->stats.d2h_bytes = L.out_bytes + G * 16;
     return 0;

@@ -103,6 +103,8 @@ struct GridDesc {
     int32_t colswap_off;    // composite: offset of its per-column swap flags
     int32_t prob, lam;      // builder: problem / first lambda index of the grid's chain
     int32_t lam_end;        // one past the last lambda index of the chain (warm start)
+    int32_t pitch, xoff;    // composite span grids: row pitch of the composite's planes and
+                            // output, and the span's first column (W and 0 otherwise)
 };
 
 struct Ctx {

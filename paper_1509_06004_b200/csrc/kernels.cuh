@@ -151,8 +151,9 @@ __global__ void __launch_bounds__(NT) k_load_comp(Ctx c, CompArgs a) {
     __shared__ int64_t red[NT / 32];
     for (int64_t t = blockIdx.x; t < c.ntiles; t += gridDim.x) {
         TileGeo g = tile_geo(c, int32_t(t));
+        const GridDesc &gd = c.grids[g.g];
         const int64_t off = a.plane_off[g.g];
-        const int64_t n = int64_t(g.W) * g.H;
+        const int64_t n = int64_t(gd.pitch) * g.H;   // the composite's plane size
         int64_t snk_acc = 0;
         for (int j = 0; j < PPT; j++) {
             int i = threadIdx.x + j * NT;
@@ -161,7 +162,7 @@ __global__ void __launch_bounds__(NT) k_load_comp(Ctx c, CompArgs a) {
             int32_t wv = 0;
             int e[4] = {0, 0, 0, 0};
             if (x < g.W && y < g.H) {
-                int64_t q = int64_t(y) * g.W + x;
+                int64_t q = int64_t(y) * gd.pitch + gd.xoff + x;
                 int32_t s = a.src[off + q], k = a.snk[off + q];
                 wv = s - k;
                 snk_acc += k;
@@ -442,7 +443,7 @@ __global__ void __launch_bounds__(NT) k_emit(Ctx c) {
         const bool comp = gd.kind == 1, swapped = !comp && grid_swapped(c, gd);
         const int x = g.x0 + lane;
         const bool cswap = comp && x < g.W && c.colswap[gd.colswap_off + x];
-        const int64_t off = comp ? gd.out_off : (int64_t(gd.prob) * c.nlam + c.cur_lam[g.g]) * (int64_t(g.W) * g.H);
+        const int64_t off = comp ? gd.out_off + gd.xoff : (int64_t(gd.prob) * c.nlam + c.cur_lam[g.g]) * (int64_t(g.W) * g.H);
         int64_t drain = 0;
         const int rows = min(TH, g.H - g.y0);
         // h decides the side when the grid (column) is swapped, lab otherwise
@@ -463,7 +464,7 @@ __global__ void __launch_bounds__(NT) k_emit(Ctx c) {
 #pragma unroll
                 for (int k = 0; k < SCAN_ROWS; k++) {
                     if (wv[k] < 0) drain -= wv[k];
-                    if (r0 + k < rows) c.out[off + int64_t(g.y0 + r0 + k) * g.W + x] = v[k];
+                    if (r0 + k < rows) c.out[off + int64_t(g.y0 + r0 + k) * gd.pitch + x] = v[k];
                 }
             }
         drain = warp_sum64(drain);

@@ -513,3 +513,46 @@ def test_integrity_check_catches_a_corrupted_cut(engine, mode, vec):
                     s.solve_seed_batch(500, 375, probs, synth.L20, "auto")
         finally:
             s.close()
+
+
+@pytest.mark.parametrize("split", [1, 0])
+def test_composite_span_split_vs_oracle(engine, split):
+    """Composites as one grid per isolated segment span (knob comp_split=1)
+    or one grid per composite: flows and labels equal the oracle's
+    (supergraph.py:190-207 semantics), for join()-built composites (zero
+    bridges: split) and for leaky ones -- a bridge pixel with a terminal
+    capacity, an arc across a span boundary -- which must not be split."""
+    from paper_1509_06004_b200 import _native
+    rng = np.random.default_rng(91)
+    items, ref = [], []
+    for case in range(10):
+        h = int(rng.integers(3, 40))
+        graphs = []
+        for _ in range(int(rng.integers(2, 5))):
+            w = int(rng.integers(1, 40))
+            nb = rng.integers(0, 30, (4, h, w))
+            nb[0][:, 0] = 0
+            nb[1][:, -1] = 0
+            nb[2][0, :] = 0
+            nb[3][-1, :] = 0
+            graphs.append(grid(w, h, rng.integers(0, 60, w * h), rng.integers(0, 60, w * h), nb.reshape(4, -1)))
+        flags = [bool(rng.integers(0, 2)) for _ in graphs]
+        comp, lay = join([apply_swap(g) if f else g for g, f in zip(graphs, flags)], swapped=flags)
+        src, snk = comp.src_cap.copy(), comp.snk_cap.copy()
+        nbr = comp.nbr_cap.copy().reshape(4, comp.height, comp.width)
+        seg0 = lay.segments[0]
+        if case % 3 == 1 and lay.bridge_columns:     # a bridge pixel with a source arc
+            src.reshape(comp.height, comp.width)[h // 2, lay.bridge_columns[0]] = 7
+        if case % 3 == 2:                            # an arc leaving the first span
+            nbr[1][h // 2, seg0.offset + seg0.width - 1] = 9
+        segs = [(s.offset, s.width, s.swapped) for s in lay.segments]
+        items.append((comp.width, comp.height, src, snk, nbr.reshape(4, -1), segs))
+        ref.append(oracle.solve(comp.width, comp.height, src, snk, nbr.reshape(4, -1), segs))
+    s = _native.Solver(0, comp_split=split)
+    try:
+        got = s.solve_composites(items)
+    finally:
+        s.close()
+    for (f, lab), (rf, rlab, _) in zip(got, ref):
+        assert f == rf
+        assert np.array_equal(lab, rlab)
