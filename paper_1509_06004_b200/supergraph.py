@@ -19,6 +19,7 @@ returns, bit for bit.
 
 from __future__ import annotations
 
+import threading
 from dataclasses import dataclass
 
 import numpy as np
@@ -230,19 +231,32 @@ def build_seed_supergraph(problems, schedule: LambdaSchedule, swap_mode: str = "
     return composite, layout, originals
 
 
-def seed_layout(problems, schedule: LambdaSchedule, swapped) -> SupergraphLayout:
-    """The layout build_seed_supergraph would produce for these problems."""
+def _layout_skeleton(problems, schedule: LambdaSchedule):
+    """Segments (all unswapped for now), bridge columns and height of the
+    layout build_seed_supergraph would produce."""
     widths = [p.width for p in problems for _ in schedule]
     offsets, bridges, height, _ = _plan(widths, [p.height for p in problems for _ in schedule],
                                         False)
-    flags = [bool(swapped[i]) for i in range(len(problems)) for _ in schedule]
     new = object.__new__
     segs = []
-    for i, (o, w, f) in enumerate(zip(offsets, widths, flags)):
+    for i, (o, w) in enumerate(zip(offsets, widths)):
         seg = new(Segment)                     # frozen dataclass, fields set directly
-        seg.__dict__.update(constituent=i, offset=o, width=w, swapped=f)
+        seg.__dict__.update(constituent=i, offset=o, width=w, swapped=False)
         segs.append(seg)
+    return segs, bridges, height
+
+
+def _finish_layout(skeleton, swapped, k: int) -> SupergraphLayout:
+    segs, bridges, height = skeleton
+    for i in np.flatnonzero(np.asarray(swapped, bool)):   # a swapped family: its k segments
+        for seg in segs[i * k:(i + 1) * k]:
+            seg.__dict__["swapped"] = True
     return SupergraphLayout(tuple(segs), tuple(bridges), height)
+
+
+def seed_layout(problems, schedule: LambdaSchedule, swapped) -> SupergraphLayout:
+    """The layout build_seed_supergraph would produce for these problems."""
+    return _finish_layout(_layout_skeleton(problems, schedule), swapped, len(schedule))
 
 
 @dataclass(frozen=True, eq=False)
@@ -283,9 +297,20 @@ def solve_seed_supergraph(problems, schedule: LambdaSchedule, swap_mode: str = "
     shapes = {(p.width, p.height) for p in problems}
     solver = _native.solver_for_thread(device)
     scores = ()
+    skeleton = None
     if len(shapes) == 1:
         W, H = shapes.pop()
-        swapped, flows, labels = solver.solve_seed_batch(W, H, problems, schedule.values, swap_mode)
+        # the layout's Segment objects (~3 us each in Python; 8,000 for a C5
+        # batch) are built on a host thread while the device solves (the
+        # engine's ctypes calls release the GIL); swap flags are set after
+        box = {}
+        th = threading.Thread(target=lambda: box.update(sk=_layout_skeleton(problems, schedule)))
+        th.start()
+        try:
+            swapped, flows, labels = solver.solve_seed_batch(W, H, problems, schedule.values, swap_mode)
+        finally:
+            th.join()
+        skeleton = box.get("sk")
         if truths is not None:
             from .scoring import score_cuts
             scores = score_cuts(solver, truths)
@@ -304,4 +329,6 @@ def solve_seed_supergraph(problems, schedule: LambdaSchedule, swap_mode: str = "
     fl = [[int(f) for f in row] for row in flows]
     cuts = tuple(CutResult._trusted(fl[i][j], labels[i][j])
                  for i in range(len(problems)) for j in range(len(schedule)))
-    return SeedSupergraphResult(seed_layout(problems, schedule, swapped), cuts, scores)
+    layout = (_finish_layout(skeleton, swapped, len(schedule)) if skeleton is not None
+              else seed_layout(problems, schedule, swapped))
+    return SeedSupergraphResult(layout, cuts, scores)
