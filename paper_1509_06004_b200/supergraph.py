@@ -304,12 +304,15 @@ def solve_seed_supergraph(problems, schedule: LambdaSchedule, swap_mode: str = "
         # batch) are built on a host thread while the device solves (the
         # engine's ctypes calls release the GIL); swap flags are set after
         box = {}
-        th = threading.Thread(target=lambda: box.update(sk=_layout_skeleton(problems, schedule)))
-        th.start()
+        th = None
+        if len(problems) * len(schedule) >= 512:   # small layouts: not worth a thread
+            th = threading.Thread(target=lambda: box.update(sk=_layout_skeleton(problems, schedule)))
+            th.start()
         try:
             swapped, flows, labels = solver.solve_seed_batch(W, H, problems, schedule.values, swap_mode)
         finally:
-            th.join()
+            if th is not None:
+                th.join()
         skeleton = box.get("sk")
         if truths is not None:
             from .scoring import score_cuts
