@@ -165,6 +165,15 @@ int pmf_solve_composites_i32(pmf_solver *s, int32_t ncomp,
                              int64_t *flow_out, uint8_t *const *labels_out);
 
 /*
+ * Both composite entry points accept a null labels_out[c]: that
+ * composite's labels stay on the device, and pmf_composite_bits packs them
+ * there into the wire's LSB-first bit order (wire.py:26, bit i of byte k =
+ * pixel 8k + i) and copies ceil(n / 8) bytes to out -- the GPU worker's
+ * response body without a host-side pack.  c indexes the last solve.
+ */
+int pmf_composite_bits(pmf_solver *s, int32_t c, uint8_t *out, int64_t out_bytes);
+
+/*
  * Build and solve the lambda families of nprob SeedProblems
  * (parametric.py:80-130) sharing one width x height, over nlam lambda
  * values (strictly increasing, validated by the caller), on device.

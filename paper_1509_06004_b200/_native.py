@@ -26,7 +26,7 @@ EXPORTS = ("pmf_solver_create", "pmf_solver_destroy", "pmf_solver_set", "pmf_las
            "pmf_solver_stats", "pmf_solver_stream", "pmf_solve_composites", "pmf_solve_seed_batch",
            "pmf_seed_stage", "pmf_seed_run", "pmf_seed_fetch", "pmf_debug_state",
            "pmf_debug_trace", "pmf_debug_busy", "pmf_seed_score", "pmf_debug_phases",
-           "pmf_solve_composites_i32")
+           "pmf_solve_composites_i32", "pmf_composite_bits")
 
 
 class NativeUnavailable(RuntimeError):
@@ -75,6 +75,8 @@ def load_library(path: str = LIB_PATH):
         lib.pmf_solve_composites.argtypes = [
             vp, i32, P(i32), P(i32), P(vp), P(vp), P(vp), P(i32), P(vp), P(vp), P(vp),
             P(i64), P(vp)]
+        lib.pmf_solve_composites_i32.argtypes = lib.pmf_solve_composites.argtypes
+        lib.pmf_composite_bits.argtypes = [vp, i32, P(u8), i64]
         lib.pmf_solve_seed_batch.argtypes = [
             vp, i32, i32, i32, P(vp), P(vp), P(vp), P(vp), P(vp), P(i32), P(vp), P(i32),
             i32, P(i64), i32, P(u8), P(i64), P(u8)]
@@ -112,7 +114,7 @@ def _raise_for(rc: int):
 
 
 def _ptrs(arrays, ctype=ctypes.c_void_p):
-    return (ctype * len(arrays))(*[a.ctypes.data for a in arrays])
+    return (ctype * len(arrays))(*[None if a is None else a.ctypes.data for a in arrays])
 
 
 class _LabelBuffers:
@@ -183,10 +185,12 @@ class Solver:
             pass
 
     # ---------------------------------------------------------------- solves
-    def solve_composites(self, items, i32: bool = False):
+    def solve_composites(self, items, i32: bool = False, labels: bool = True):
         """items: [(width, height, src, snk, nbr, segments)] with segments a
         list of (offset, width, swapped) or None.  Returns [(flow, labels)].
-        i32: the planes are int32 (wire requests) and are read in place."""
+        i32: the planes are int32 (wire requests) and are read in place.
+        labels=False: labels stay on the device (None returned; see
+        composite_bits)."""
         k = len(items)
         dt = np.int32 if i32 else np.int64
         keep = []
@@ -202,7 +206,7 @@ class Solver:
             offs.append(np.array([s[0] for s in segs] or [0], np.int32))
             wids.append(np.array([s[1] for s in segs] or [0], np.int32))
             sws.append(np.array([1 if s[2] else 0 for s in segs] or [0], np.uint8))
-            labs.append(np.empty(w * h, np.uint8))
+            labs.append(np.empty(w * h, np.uint8) if labels else None)
         keep += [srcs, snks, nbrs, offs, wids, sws, labs]
         flows = np.zeros(k, np.int64)
         nseg = np.array(nsegs, np.int32)
@@ -216,6 +220,16 @@ class Solver:
         if rc:
             _raise_for(rc)
         return [(int(f), l) for f, l in zip(flows, labs)]
+
+    def composite_bits(self, c: int, n: int) -> bytes:
+        """Labels of composite c of the last composite solve (n pixels) as
+        LSB-first bits (the wire's response body), packed on the device."""
+        out = np.empty((n + 7) // 8, np.uint8)
+        rc = self._lib.pmf_composite_bits(self._h, c, out.ctypes.data_as(ctypes.POINTER(ctypes.c_uint8)),
+                                          ctypes.c_int64(out.size))
+        if rc:
+            _raise_for(rc)
+        return out.tobytes()
 
     def debug_state(self):
         """(w, h, r, lab) tile-major arrays of the last run (diagnostics)."""

@@ -253,7 +253,7 @@ struct pmf_solver {
     Layout lay;
     std::vector<int32_t> ones, curlam0;
     std::vector<uint8_t> colswap;
-    std::vector<int64_t> comp_off, grid_off;
+    std::vector<int64_t> comp_off, grid_off, comp_out, comp_n;
     int comp_any_split = 0;
     int comp_split = 1;         // composites: one grid per isolated segment span
     SeedStage stage;
@@ -1792,9 +1792,13 @@ static int solve_composites_t(pmf_solver *s, int32_t ncomp, const int32_t *width
             if (leak[size_t(k)]) split[size_t(c)] = 0;
     }
     int any_split = 0;
-    std::vector<int64_t> comp_out(size_t(ncomp), 0);   // output offset per composite
+    std::vector<int64_t> &comp_out = s->comp_out;   // output offset per composite (16-byte aligned,
+    comp_out.assign(size_t(ncomp), 0);              // so pmf_composite_bits can pack it in place)
+    s->comp_n.assign(size_t(ncomp), 0);
     for (int c = 0; c < ncomp; c++) {
+        s->lay.out_bytes = (s->lay.out_bytes + 15) / 16 * 16;
         comp_out[size_t(c)] = s->lay.out_bytes;
+        s->comp_n[size_t(c)] = int64_t(width[c]) * height[c];
         if (split[size_t(c)]) {
             any_split = 1;
             const int64_t base = s->lay.out_bytes;
@@ -1819,15 +1823,17 @@ static int solve_composites_t(pmf_solver *s, int32_t ncomp, const int32_t *width
     if ((rc = s->h_out.ensure(lab_bytes + size_t(G) * 8))) return rc;
     uint8_t *ho = s->h_out.as<uint8_t>();
     int64_t *hsnk = (int64_t *)(ho + lab_bytes);
-    CK(cudaMemcpyAsync(ho, s->d_out.p, L.out_bytes, cudaMemcpyDeviceToHost, s->st));
+    bool any_labels = false;   // a null labels_out[c]: labels stay on the device (pmf_composite_bits)
+    for (int c = 0; c < ncomp; c++) any_labels |= labels_out[c] != nullptr;
+    if (any_labels) CK(cudaMemcpyAsync(ho, s->d_out.p, L.out_bytes, cudaMemcpyDeviceToHost, s->st));
     CK(cudaMemcpyAsync(hsnk, s->d_flows.p, G * 8, cudaMemcpyDeviceToHost, s->st));
     if ((rc = run_end(s))) return rc;
     for (int c = 0; c < ncomp; c++) flow_out[c] = 0;
     for (int64_t g = 0; g < G; g++) flow_out[L.grids[size_t(g)].prob] += hsnk[g];
     for (int c = 0; c < ncomp; c++)
-        memcpy(labels_out[c], ho + comp_out[size_t(c)], size_t(width[c]) * height[c]);
+        if (labels_out[c]) memcpy(labels_out[c], ho + comp_out[size_t(c)], size_t(width[c]) * height[c]);
     s->stats.h2d_bytes = total_px * 6 * 4;
-    s->stats.d2h_bytes = L.out_bytes + G * 16;
+    s->stats.d2h_bytes = (any_labels ? L.out_bytes : 0) + G * 8;
     return 0;
 }
 
@@ -1851,6 +1857,26 @@ int pmf_solve_composites_i32(pmf_solver *s, int32_t ncomp, const int32_t *width,
                              uint8_t *const *labels_out) {
     return solve_composites_t<int32_t>(s, ncomp, width, height, src, snk, nbr, nseg, seg_off, seg_w,
                                        seg_swapped, flow_out, labels_out);
+}
+
+// Labels of composite c of the last composite solve as LSB-first bits
+// (bit i of byte k = pixel 8k + i; the wire's response order, wire.py:26),
+// packed on the device: ceil(n / 8) bytes into out.
+int pmf_composite_bits(pmf_solver *s, int32_t c, uint8_t *out, int64_t out_bytes) {
+    if (!s || !out) return fail(PMF_ERR_ARG, "null argument");
+    if (c < 0 || size_t(c) >= s->comp_n.size()) return fail(PMF_ERR_ARG, "no composite %d in the last solve", c);
+    const int64_t n = s->comp_n[size_t(c)], need = (n + 7) / 8;
+    if (out_bytes < need) return fail(PMF_ERR_ARG, "%lld bytes needed for %lld labels", (long long)need, (long long)n);
+    CK(cudaSetDevice(s->device));
+    int rc;
+    if ((rc = s->d_bits.ensure(size_t(cdiv(n, 32)) * 4))) return rc;
+    const int grid = int(std::max<int64_t>(1, std::min<int64_t>(cdiv(n, 32 * 256), 16 * s->sms)));
+    LAUNCH(s, (k_pack_bits<<<grid, 256, 0, s->st>>>(s->d_out.as<uint8_t>() + s->comp_out[size_t(c)],
+                                                     s->d_bits.as<uint32_t>(), n)));
+    CK(cudaGetLastError());
+    CK(cudaMemcpyAsync(out, s->d_bits.p, size_t(need), cudaMemcpyDeviceToHost, s->st));
+    CK(cudaStreamSynchronize(s->st));
+    return 0;
 }
 
 // CTA-busy milliseconds of the last asynchronous run, summed over CTAs:

@@ -556,3 +556,30 @@ def test_composite_span_split_vs_oracle(engine, split):
     for (f, lab), (rf, rlab, _) in zip(got, ref):
         assert f == rf
         assert np.array_equal(lab, rlab)
+
+
+def test_composite_bits_from_device(engine):
+    """pmf_composite_bits: the labels of each composite of the last solve,
+    packed on the device in the wire's LSB-first order, equal the packed
+    byte labels; composites solved with labels left on the device still
+    report their flows."""
+    from paper_1509_06004_b200 import _native
+    from paper_1509_06004_b200.wire import pack_bits
+    rng = np.random.default_rng(5)
+    items = []
+    for (w, h) in [(7, 5), (33, 17), (64, 40), (3, 1)]:
+        nb = rng.integers(0, 20, (4, h, w))
+        nb[0][:, 0] = 0
+        nb[1][:, -1] = 0
+        nb[2][0, :] = 0
+        nb[3][-1, :] = 0
+        items.append((w, h, rng.integers(0, 40, w * h), rng.integers(0, 40, w * h), nb.reshape(4, -1), None))
+    s = _native.Solver(0)
+    try:
+        ref = s.solve_composites(items)
+        got = s.solve_composites(items, labels=False)
+        assert [f for f, _ in got] == [f for f, _ in ref] and all(l is None for _, l in got)
+        for c, (w, h, *_ ) in enumerate(items):
+            assert s.composite_bits(c, w * h) == pack_bits(ref[c][1])
+    finally:
+        s.close()
