@@ -1233,6 +1233,7 @@ int seed_stage(pmf_solver *s, int32_t nprob, int32_t W, int32_t H, const int64_t
                const int64_t *const *us, const int64_t *const *sb, const int64_t *const *pw,
                const int64_t *const *fg_idx, const int32_t *n_fg, const int64_t *const *bg_idx,
                const int32_t *n_bg, int32_t nlam, const int64_t *lambdas, int32_t swap_mode) {
+    s->comp_n.clear();   // a seed batch reuses the output buffer: no composite labels to pack
     SeedStage &S = s->stage;
     S.valid = false;
     if (nprob < 1 || nlam < 1 || W < 1 || H < 1 || !ub || !us || !sb || !pw || !lambdas ||
