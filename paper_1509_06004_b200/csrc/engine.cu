@@ -1482,34 +1482,58 @@ int seed_fetch(pmf_solver *s, uint8_t *swapped_out, int64_t *flows_out, uint8_t 
         LAUNCH(s, (k_pack_bits<<<std::max(grid, 1), 256, 0, s->st>>>(s->d_out.as<uint8_t>(), s->d_bits.as<uint32_t>(),
                                                                      out_bytes)));
         CK(cudaGetLastError());
-        CK(cudaMemcpyAsync(ho, s->d_bits.p, size_t(bit_bytes), cudaMemcpyDeviceToHost, s->st));
+    }
+    // the bits cross in pieces of >= 4 MB, each unpacked on the host pool
+    // while the next one is in flight (the unpack writes 8x the bytes)
+    const int64_t full = labels_out ? out_bytes / 8 : 0;   // whole bit bytes = 8 labels each
+    const int npiece = int(std::min<int64_t>(8, std::max<int64_t>(1, full >> 22)));
+    const int64_t piece = cdiv(std::max<int64_t>(full, 1), npiece);
+    cudaEvent_t ev[8];
+    if (labels_out) {
+        for (int i = 0; i < npiece; i++) {
+            const int64_t lo = i * piece, hi = i + 1 == npiece ? int64_t(bit_bytes) : std::min(full, lo + piece);
+            if (hi > lo)
+                CK(cudaMemcpyAsync(ho + lo, s->d_bits.as<uint8_t>() + lo, size_t(hi - lo), cudaMemcpyDeviceToHost, s->st));
+            CK(cudaEventCreateWithFlags(&ev[i], cudaEventDisableTiming));
+            CK(cudaEventRecord(ev[i], s->st));
+        }
     }
     CK(cudaMemcpyAsync(hfl, s->d_flows.p, nf * 8, cudaMemcpyDeviceToHost, s->st));
     CK(cudaMemcpyAsync(hsw, s->d_swapflag.p, size_t(S.nprob) * 4, cudaMemcpyDeviceToHost, s->st));
-    CK(cudaStreamSynchronize(s->st));
-    memcpy(flows_out, hfl, size_t(nf) * 8);
-    if (swapped_out)
-        for (int p = 0; p < S.nprob; p++) swapped_out[p] = uint8_t(hsw[p] != 0);
     if (labels_out) {
-        // large outputs are fresh memory: ask for huge pages so first touch
-        // costs one fault per 2 MiB instead of per 4 KiB
+        // large outputs: huge pages, so first touch costs one fault per 2 MiB
         if (out_bytes >= (int64_t(64) << 20)) {
             const uintptr_t a = (reinterpret_cast<uintptr_t>(labels_out) + 0x1fffff) & ~uintptr_t(0x1fffff);
             const uintptr_t e = (reinterpret_cast<uintptr_t>(labels_out) + uintptr_t(out_bytes)) & ~uintptr_t(0x1fffff);
             if (e > a) madvise(reinterpret_cast<void *>(a), e - a, MADV_HUGEPAGE);
         }
         // parallel unpack straight into the caller's buffer (64 KiB of bits per task)
-        const int64_t per = int64_t(64) << 10, full = out_bytes / 8, chunks = cdiv(full, per);
-        s->pool->run(chunks, [&](int64_t i) {
-            const int64_t lo = i * per, hi = std::min(full, lo + per);
-            uint64_t *dst = reinterpret_cast<uint64_t *>(labels_out) + lo;
-            for (int64_t k = lo; k < hi; k++) {
-                const uint64_t v = lut.v[ho[k]];
-                memcpy(dst + (k - lo), &v, 8);
+        const int64_t per = int64_t(64) << 10;
+        for (int i = 0; i < npiece; i++) {
+            const cudaError_t e = cudaEventSynchronize(ev[i]);
+            cudaEventDestroy(ev[i]);
+            if (e != cudaSuccess) {
+                for (int j = i + 1; j < npiece; j++) cudaEventDestroy(ev[j]);
+                return fail(PMF_ERR_CUDA, "label transfer: %s", cudaGetErrorString(e));
             }
-        });
-        for (int64_t i = full * 8; i < out_bytes; i++) labels_out[i] = uint8_t((ho[i >> 3] >> (i & 7)) & 1);
+            const int64_t lo = i * piece, hi = std::min(full, lo + piece);
+            if (hi <= lo) continue;
+            s->pool->run(cdiv(hi - lo, per), [&](int64_t t) {
+                const int64_t a = lo + t * per, b = std::min(hi, a + per);
+                uint64_t *dst = reinterpret_cast<uint64_t *>(labels_out) + a;
+                for (int64_t k = a; k < b; k++) {
+                    const uint64_t v = lut.v[ho[k]];
+                    memcpy(dst + (k - a), &v, 8);
+                }
+            });
+        }
     }
+    CK(cudaStreamSynchronize(s->st));
+    memcpy(flows_out, hfl, size_t(nf) * 8);
+    if (swapped_out)
+        for (int p = 0; p < S.nprob; p++) swapped_out[p] = uint8_t(hsw[p] != 0);
+    if (labels_out)
+        for (int64_t i = full * 8; i < out_bytes; i++) labels_out[i] = uint8_t((ho[i >> 3] >> (i & 7)) & 1);
     s->stats.d2h_bytes = (labels_out ? bit_bytes : 0) + nf * 8 + int64_t(S.nprob) * 4;
     return 0;
 }
