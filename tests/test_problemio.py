@@ -81,3 +81,15 @@ def test_file_problems_solved_on_gpu_match_oracle(engine):
             cut = res.cuts[pi * K + j]
             assert cut.flow == f
             assert np.array_equal(np.asarray(cut.labels, np.uint8).reshape(-1), lab)
+
+
+def test_writer_rejects_mismatched_truths(tmp_path):
+    meta, probs, truths = problemio.read_problem_file(PMF)
+    with pytest.raises(problemio.ProblemFileError, match="one truth mask per problem"):
+        problemio.write_problem_file(tmp_path / "x.pmf", probs, truths[:-1])
+    # no truths at all is fine, and reads back with an empty list
+    problemio.write_problem_file(tmp_path / "y.pmf", probs)
+    m2, p2, t2 = problemio.read_problem_file(tmp_path / "y.pmf")
+    assert t2 == [] and m2["truths"] == 0 and len(p2) == len(probs)
+    assert all(np.array_equal(a.pairwise, b.pairwise) and a.fg_seeds == b.fg_seeds
+               for a, b in zip(p2, probs))

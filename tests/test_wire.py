@@ -110,3 +110,17 @@ def test_gpu_solve_fn_matches_the_wire_answer():
     r = wire.decode_response(bytes.fromhex(f["response"]), req.graph.n)
     assert cut.flow == r.flow
     assert np.array_equal(np.asarray(cut.labels, np.uint8).reshape(-1), r.labels)
+
+
+def test_encoder_rejects_capacities_the_wire_cannot_carry():
+    """encode_request refuses planes outside [0, CAP_MAX] (wire.py:131-134)."""
+    from paper_1509_06004_b200.grid import CAP_MAX, GridGraph
+    f = next(f for f in FRAMES if f["name"] == "whole_6x9")
+    req = wire.decode_request(bytes.fromhex(f["request"]))
+    g = req.graph
+    for bad in (-1, CAP_MAX + 1):
+        src = g.src_cap.copy()
+        src[3] = bad
+        g2 = GridGraph(g.width, g.height, src, g.snk_cap, g.nbr_cap)
+        with pytest.raises(wire.CapacityRangeError):
+            wire.encode_request(wire.WireRequest(1, g2, None))
