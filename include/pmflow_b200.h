@@ -81,7 +81,7 @@ typedef struct pmf_stats {
     int64_t scan_tile_passes;   /* async: init / seed / label-init / emit tile passes */
     double ms_async;            /* async: span of the persistent solve kernel (device clock) */
     int32_t async_mode;         /* 1: the last run used the asynchronous solver */
-    int32_t reserved;
+    int32_t wide_mode;          /* 1: the last run used the int64 state variant */
     int64_t binit_tile_passes;  /* async scan phases, tiles each: relabel init, */
     int64_t seed_tile_passes;   /*   active-tile seeding, label init,           */
     int64_t linit_tile_passes;  /*   emit (+ warm-start advance)                */

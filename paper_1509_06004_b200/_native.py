@@ -42,7 +42,7 @@ class PmfStats(ctypes.Structure):
                                        "ms_seed", "ms_h2d", "ms_d2h", "ms_device")] + [
         (k, ctypes.c_int64) for k in ("launches", "h2d_bytes", "d2h_bytes", "graph_builds",
                                        "kernels", "steps", "scan_tile_passes")] + [
-        ("ms_async", ctypes.c_double), ("async_mode", ctypes.c_int32), ("reserved", ctypes.c_int32)] + [
+        ("ms_async", ctypes.c_double), ("async_mode", ctypes.c_int32), ("wide_mode", ctypes.c_int32)] + [
         (k, ctypes.c_int64) for k in ("binit_tile_passes", "seed_tile_passes", "linit_tile_passes",
                                        "emit_tile_passes")]
 
@@ -192,6 +192,7 @@ class Solver:
         labels=False: labels stay on the device (None returned; see
         composite_bits)."""
         k = len(items)
+        self._staged = None   # a composite solve replaces the staged seed batch on the device
         dt = np.int32 if i32 else np.int64
         keep = []
         widths = np.array([it[0] for it in items], np.int32)
@@ -326,6 +327,8 @@ class Solver:
 
     def seed_fetch(self, labels=True):
         """(swapped (P,), flows (P, K), labels (P, K, n) uint8 or None)."""
+        if getattr(self, "_staged", None) is None:
+            raise ValueError("no staged seed batch (a composite solve replaced it)")
         n, P_, K = self._staged
         Pt = ctypes.POINTER
         swapped = np.zeros(P_, np.uint8)

@@ -26,6 +26,7 @@
 #include "tile.cuh"
 #include "warp.cuh"
 #include "async.cuh"
+#include "wide.cuh"
 
 using namespace pmf;
 
@@ -192,6 +193,7 @@ struct SeedStage {
     std::vector<int64_t> lambdas;
     std::vector<int64_t> slope_sum; // per problem: sum of unary_slope over non-fg pixels
     int32_t chain = 1;              // lambdas per warm-start chain
+    bool wide = false;              // excess bound past int32: int64 state variant (wide.cuh)
 };
 
 }  // namespace
@@ -245,10 +247,15 @@ struct pmf_solver {
     int bfs_chunk = 8;
     int timing = 0;
     int64_t max_cycles = 50000;
+    int force_wide = 0;         // select the int64 state variant even when int32 bounds hold (tests)
+    cudaEvent_t fetch_ev[8] = {};   // seed_fetch: label pieces in flight (created once)
+    int wide_pulses = 64;       // int64 variant: lock-step pulses between exact global relabels
+    int64_t wide_cycles = 0, wide_pulses_run = 0, wide_relax_launches = 0;   // ... of the last wide run
     // device workspace
     DevBuf d_w, d_h, d_r, d_lab, d_tile_grid, d_tnb, d_fin, d_gpend, d_specg, d_keeph, d_seeds, d_sofs, d_gr, d_tflag, d_vacc, d_truth, d_score, d_plog, d_tfresh, d_grids, d_live, d_act, d_list, d_inq, d_cnt,
         d_snk, d_drain, d_err, d_stat, d_colswap, d_out, d_bits, d_in32, d_pw, d_mask, d_off, d_lam,
-        d_swapcnt, d_swapflag, d_ring, d_qstate, d_qctr, d_ctl, d_curlam, d_flows, d_slopesum;
+        d_swapcnt, d_swapflag, d_ring, d_qstate, d_qctr, d_ctl, d_curlam, d_flows, d_slopesum,
+        d_we, d_wr, d_wgrid, d_wtile, d_wchg, d_wcnt;   // int64 state variant (wide.cuh)
     HostBuf h_in32, h_pw, h_mask, h_out, h_small, h_seeds;
     Layout lay;
     std::vector<int32_t> ones, curlam0;
@@ -1161,18 +1168,10 @@ int async_solve(pmf_solver *s, const Ctx &c0, const SeedArgs &sa) {
     return 0;
 }
 
-template <class E>
-int seed_run_t(pmf_solver *s) {
-    SeedStage &S = s->stage;
-    int rc = grids_for<E>(s);
-    if (rc) return rc;
-    if ((rc = setup_state(s, E::kBytes))) return rc;
-    if ((rc = s->d_swapflag.ensure(size_t(S.nprob) * 4))) return rc;
-    s->ctx.swapflag = s->d_swapflag.as<int32_t>();
-    const Ctx &c = s->ctx;
+// Kernel arguments of the staged seed batch (planes, offsets, lambdas).
+SeedArgs seed_args(pmf_solver *s) {
+    const SeedStage &S = s->stage;
     const int64_t n = int64_t(S.W) * S.H;
-    s->tmark(C_BUILD);
-    CK(cudaMemsetAsync(s->d_swapcnt.p, 0, size_t(S.nprob) * 8, s->st));
     const int32_t *b32 = s->d_in32.as<int32_t>();
     SeedArgs a{};
     a.base = b32;
@@ -1191,6 +1190,14 @@ int seed_run_t(pmf_solver *s) {
     a.swap_cnt = s->d_swapcnt.as<int32_t>();
     a.swapped = s->d_swapflag.as<int32_t>();
     a.mask = s->d_mask.as<uint8_t>();
+    return a;
+}
+
+// Swap decision per problem (supergraph.py:210-212, 85-92) into d_swapflag.
+int seed_swap_flags(pmf_solver *s, const SeedArgs &a) {
+    const SeedStage &S = s->stage;
+    const int64_t n = int64_t(S.W) * S.H;
+    CK(cudaMemsetAsync(s->d_swapcnt.p, 0, size_t(S.nprob) * 8, s->st));
     if (S.swap_mode == PMF_SWAP_AUTO) {
         if (n >= (int64_t(1) << 31)) return fail(PMF_ERR_ARG, "image too large (%lld pixels)", (long long)n);
         const int chunks = int(std::max<int64_t>(1, std::min<int64_t>(cdiv(n, 256 * 4), cdiv(8 * s->sms, S.nprob))));
@@ -1198,6 +1205,22 @@ int seed_run_t(pmf_solver *s) {
                        a, chunks)));
     }
     LAUNCH(s, (k_swap_decide<<<int(cdiv(S.nprob, 128)), 128, 0, s->st>>>(a)));
+    CK(cudaGetLastError());
+    return 0;
+}
+
+template <class E>
+int seed_run_t(pmf_solver *s) {
+    SeedStage &S = s->stage;
+    int rc = grids_for<E>(s);
+    if (rc) return rc;
+    if ((rc = setup_state(s, E::kBytes))) return rc;
+    if ((rc = s->d_swapflag.ensure(size_t(S.nprob) * 4))) return rc;
+    s->ctx.swapflag = s->d_swapflag.as<int32_t>();
+    const Ctx &c = s->ctx;
+    s->tmark(C_BUILD);
+    const SeedArgs a = seed_args(s);
+    if ((rc = seed_swap_flags(s, a))) return rc;
     LAUNCH(s, (k_build_seed<E><<<s->grid_full, NT, 0, s->st>>>(c, a)));
     CK(cudaGetLastError());
     s->stats.full_passes++;
@@ -1376,8 +1399,9 @@ int seed_stage(pmf_solver *s, int32_t nprob, int32_t W, int32_t H, const int64_t
     });
     if ((rc = terr.raise())) return rc;
     S.u8 = maxpair <= 255;
-    if (!S.u8 && CAP_MAX + 8 * maxpair >= (int64_t(1) << 31) - 1)
-        return fail(PMF_ERR_RANGE, "pairwise capacities too large for the int32 device state");
+    // a pixel's excess is bounded by its source term plus its incoming arc
+    // pairs; past int32 the batch runs on the int64 state variant
+    S.wide = s->force_wide || (!S.u8 && CAP_MAX + 8 * maxpair >= (int64_t(1) << 31) - 1);
     S.lambdas.assign(lambdas, lambdas + nlam);
     const int64_t nu = int64_t(uniq.size());
     const size_t bytes_b = size_t(nu) * n * 3 * 4, bytes_pw = pw_list.size() * size_t(4 * n) * 4;
@@ -1488,13 +1512,13 @@ int seed_fetch(pmf_solver *s, uint8_t *swapped_out, int64_t *flows_out, uint8_t 
     const int64_t full = labels_out ? out_bytes / 8 : 0;   // whole bit bytes = 8 labels each
     const int npiece = int(std::min<int64_t>(8, std::max<int64_t>(1, full >> 22)));
     const int64_t piece = cdiv(std::max<int64_t>(full, 1), npiece);
-    cudaEvent_t ev[8];
+    cudaEvent_t *ev = s->fetch_ev;   // created once per solver, reused by every fetch
     if (labels_out) {
         for (int i = 0; i < npiece; i++) {
             const int64_t lo = i * piece, hi = i + 1 == npiece ? int64_t(bit_bytes) : std::min(full, lo + piece);
             if (hi > lo)
                 CK(cudaMemcpyAsync(ho + lo, s->d_bits.as<uint8_t>() + lo, size_t(hi - lo), cudaMemcpyDeviceToHost, s->st));
-            CK(cudaEventCreateWithFlags(&ev[i], cudaEventDisableTiming));
+            if (!ev[i]) CK(cudaEventCreateWithFlags(&ev[i], cudaEventDisableTiming));
             CK(cudaEventRecord(ev[i], s->st));
         }
     }
@@ -1511,11 +1535,7 @@ int seed_fetch(pmf_solver *s, uint8_t *swapped_out, int64_t *flows_out, uint8_t 
         const int64_t per = int64_t(64) << 10;
         for (int i = 0; i < npiece; i++) {
             const cudaError_t e = cudaEventSynchronize(ev[i]);
-            cudaEventDestroy(ev[i]);
-            if (e != cudaSuccess) {
-                for (int j = i + 1; j < npiece; j++) cudaEventDestroy(ev[j]);
-                return fail(PMF_ERR_CUDA, "label transfer: %s", cudaGetErrorString(e));
-            }
+            if (e != cudaSuccess) return fail(PMF_ERR_CUDA, "label transfer: %s", cudaGetErrorString(e));
             const int64_t lo = i * piece, hi = std::min(full, lo + piece);
             if (hi <= lo) continue;
             s->pool->run(cdiv(hi - lo, per), [&](int64_t t) {
@@ -1536,6 +1556,204 @@ int seed_fetch(pmf_solver *s, uint8_t *swapped_out, int64_t *flows_out, uint8_t 
         for (int64_t i = full * 8; i < out_bytes; i++) labels_out[i] = uint8_t((ho[i >> 3] >> (i & 7)) & 1);
     s->stats.d2h_bytes = (labels_out ? bit_bytes : 0) + nf * 8 + int64_t(S.nprob) * 4;
     return 0;
+}
+
+// --------------------------------------------------------------------------
+// int64 state variant (wide.cuh): graphs whose excess bound leaves int32
+// --------------------------------------------------------------------------
+
+struct WideBatch {
+    std::vector<WGrid> grids;
+    std::vector<WTile> tiles;
+    int64_t P = 0;
+    void add(int32_t W, int32_t H, int64_t out_off, int32_t pitch, int32_t xoff, int32_t cs_off, int32_t flow_idx,
+             int32_t prob, int32_t lam) {
+        WGrid g{};
+        g.base = P;
+        g.W = W;
+        g.H = H;
+        g.out_off = out_off;
+        g.pitch = pitch;
+        g.xoff = xoff;
+        g.cs_off = cs_off;
+        g.flow_idx = flow_idx;
+        g.prob = prob;
+        g.lam = lam;
+        const int32_t gi = int32_t(grids.size());
+        for (int32_t y = 0; y < H; y += WT)
+            for (int32_t x = 0; x < W; x += WT) tiles.push_back(WTile{gi, x, y, 0});
+        P += int64_t(W) * H;
+        grids.push_back(g);
+    }
+};
+
+// device state + tables of batch B; returns the kernel context in *c
+int wide_setup(pmf_solver *s, const WideBatch &B, WCtx *c) {
+    const int64_t P = B.P, G = int64_t(B.grids.size()), T = int64_t(B.tiles.size());
+    if (T >= (int64_t(1) << 31)) return fail(PMF_ERR_ARG, "batch too large (%lld tiles)", (long long)T);
+    int rc;
+    if ((rc = s->d_we.ensure(size_t(P) * 8)) || (rc = s->d_wr.ensure(size_t(P) * 32)) ||
+        (rc = s->d_h.ensure(size_t(P) * 4)) || (rc = s->d_lab.ensure(size_t(P))) ||
+        (rc = s->d_wgrid.ensure(size_t(G) * sizeof(WGrid))) || (rc = s->d_wtile.ensure(size_t(T) * sizeof(WTile))) ||
+        (rc = s->d_snk.ensure(size_t(G) * 8)) || (rc = s->d_drain.ensure(size_t(G) * 8)) ||
+        (rc = s->d_wchg.ensure(64)) || (rc = s->d_wcnt.ensure(64)) || (rc = s->d_err.ensure(64)) ||
+        (rc = s->d_stat.ensure(ST_NSTAT * 8)) || (rc = s->d_ctl.ensure(sizeof(Ctl))) || (rc = s->d_colswap.ensure(64)))
+        return rc;
+    CK(cudaMemcpyAsync(s->d_wgrid.p, B.grids.data(), size_t(G) * sizeof(WGrid), cudaMemcpyHostToDevice, s->st));
+    CK(cudaMemcpyAsync(s->d_wtile.p, B.tiles.data(), size_t(T) * sizeof(WTile), cudaMemcpyHostToDevice, s->st));
+    CK(cudaMemsetAsync(s->d_snk.p, 0, size_t(G) * 8, s->st));
+    CK(cudaMemsetAsync(s->d_drain.p, 0, size_t(G) * 8, s->st));
+    WCtx x{};
+    x.e = s->d_we.as<int64_t>();
+    x.r = s->d_wr.as<int64_t>();
+    x.h = s->d_h.as<int32_t>();
+    x.lab = s->d_lab.as<uint8_t>();
+    x.P = P;
+    x.grids = s->d_wgrid.as<WGrid>();
+    x.tiles = s->d_wtile.as<WTile>();
+    x.ntiles = int32_t(T);
+    x.snk_sum = s->d_snk.as<int64_t>();
+    x.drain = s->d_drain.as<int64_t>();
+    x.err = s->d_err.as<int32_t>();
+    x.colswap = s->d_colswap.as<uint8_t>();
+    x.out = s->d_out.as<uint8_t>();
+    x.flows = s->d_flows.as<int64_t>();
+    x.count = s->d_wcnt.as<unsigned long long>();
+    *c = x;
+    return 0;
+}
+
+// run bracket state of a wide run: no tile-engine counters, no error yet
+int wide_bracket(pmf_solver *s) {
+    int rc;
+    if ((rc = s->d_err.ensure(64)) || (rc = s->d_stat.ensure(ST_NSTAT * 8)) || (rc = s->d_ctl.ensure(sizeof(Ctl))))
+        return rc;
+    CK(cudaMemsetAsync(s->d_err.p, 0, 64, s->st));
+    CK(cudaMemsetAsync(s->d_stat.p, 0, ST_NSTAT * 8, s->st));
+    CK(cudaMemsetAsync(s->d_ctl.p, 0, sizeof(Ctl), s->st));
+    s->wide_cycles = s->wide_pulses_run = s->wide_relax_launches = 0;
+    return 0;
+}
+
+inline int wide_grid(const pmf_solver *s, const WCtx &c) {
+    return int(std::max<int64_t>(1, std::min<int64_t>(c.ntiles, 2 * int64_t(s->sms))));
+}
+
+// relaxation launches until one changes nothing (a fixpoint stays one)
+int wide_relax(pmf_solver *s, const WCtx &c, int sink) {
+    const int grid = wide_grid(s, c);
+    LAUNCH(s, (k_wide_init<<<grid, 1024, 0, s->st>>>(c, sink)));
+    int32_t *chg = s->d_wchg.as<int32_t>(), *hp = s->h_small.as<int32_t>();
+    for (;;) {
+        CK(cudaMemsetAsync(chg, 0, 8 * 4, s->st));
+        for (int k = 0; k < 8; k++) LAUNCH(s, (k_wide_relax<<<grid, 1024, 0, s->st>>>(c, sink, chg + k)));
+        CK(cudaGetLastError());
+        s->wide_relax_launches += 8;
+        CK(cudaMemcpyAsync(hp, chg + 7, 4, cudaMemcpyDeviceToHost, s->st));
+        CK(cudaStreamSynchronize(s->st));
+        if (!*hp) return 0;
+    }
+}
+
+// phase 1 to a maximum preflow, then labels, flows (per grid into flows[flow_idx])
+int wide_solve(pmf_solver *s, const WCtx &c, int32_t ngrids) {
+    const int grid = wide_grid(s, c);
+    unsigned long long *hc = s->h_small.as<unsigned long long>();
+    int rc;
+    for (;;) {
+        // exact global relabel (solvers.py:54-85) ...
+        if ((rc = wide_relax(s, c, 1))) return rc;
+        // ... then stop when no pixel that can reach the sink holds excess
+        CK(cudaMemsetAsync(c.count, 0, 8, s->st));
+        LAUNCH(s, (k_wide_count<<<grid, 1024, 0, s->st>>>(c)));
+        CK(cudaMemcpyAsync(hc, c.count, 8, cudaMemcpyDeviceToHost, s->st));
+        CK(cudaStreamSynchronize(s->st));
+        if (*hc == 0) break;
+        if (++s->wide_cycles > s->max_cycles)
+            return fail(PMF_ERR_NOCONV, "push-relabel failed to converge within %lld cycles", (long long)s->max_cycles);
+        for (int k = 0; k < s->wide_pulses; k++) {
+            LAUNCH(s, (k_wide_push<<<grid, 1024, 0, s->st>>>(c)));
+            LAUNCH(s, (k_wide_relabel<<<grid, 1024, 0, s->st>>>(c)));
+        }
+        CK(cudaGetLastError());
+        s->wide_pulses_run += s->wide_pulses;
+    }
+    if ((rc = wide_relax(s, c, 0))) return rc;   // source-side closure
+    LAUNCH(s, (k_wide_emit<<<grid, 1024, 0, s->st>>>(c)));
+    LAUNCH(s, (k_wide_finalize<<<int(cdiv(ngrids, 256)), 256, 0, s->st>>>(c, ngrids)));
+    CK(cudaGetLastError());
+    return 0;
+}
+
+// seed batch on the int64 state: every (problem, lambda) graph built in
+// its original orientation, in chunks that bound the device state
+int wide_seed_run(pmf_solver *s) {
+    const SeedStage &S = s->stage;
+    const int64_t n = int64_t(S.W) * S.H, NG = int64_t(S.nprob) * S.nlam;
+    int rc;
+    if ((rc = wide_bracket(s))) return rc;
+    if ((rc = s->d_swapflag.ensure(size_t(S.nprob) * 4)) || (rc = s->d_out.ensure(size_t(NG * n))) ||
+        (rc = s->d_flows.ensure(size_t(NG) * 8)))
+        return rc;
+    s->tmark(C_BUILD);
+    const SeedArgs a = seed_args(s);
+    if ((rc = seed_swap_flags(s, a))) return rc;
+    const int64_t per = std::max<int64_t>(1, (int64_t(24) << 30) / (45 * n));   // <= ~24 GB of state per chunk
+    for (int64_t g0 = 0; g0 < NG; g0 += per) {
+        const int64_t g1 = std::min(NG, g0 + per);
+        WideBatch B;
+        for (int64_t g = g0; g < g1; g++)
+            B.add(S.W, S.H, g * n, S.W, 0, -1, int32_t(g), int32_t(g / S.nlam), int32_t(g % S.nlam));
+        WCtx c;
+        if ((rc = wide_setup(s, B, &c))) return rc;
+        LAUNCH(s, (k_wide_build_seed<<<wide_grid(s, c), 1024, 0, s->st>>>(c, a.base, a.slope, a.sink, a.pw, a.mask,
+                                                                          a.plane_off, a.pw_off, a.lambdas)));
+        CK(cudaGetLastError());
+        if ((rc = wide_solve(s, c, int32_t(B.grids.size())))) return rc;
+    }
+    if (s->verify) {
+        Ctx x{};
+        x.out = s->d_out.as<uint8_t>();
+        x.flows = s->d_flows.as<int64_t>();
+        x.err = s->d_err.as<int32_t>();
+        if ((rc = launch_verify<EdgeI32>(s, x, a))) return rc;
+    }
+    return 0;
+}
+
+// stats of a wide run (after run_end): cycles, pulses, relaxation launches
+void wide_stats(pmf_solver *s) {
+    s->stats.cycles = s->wide_cycles;
+    s->stats.push_sweeps = s->wide_pulses_run;
+    s->stats.bfs_sweeps = s->wide_relax_launches;
+    s->stats.wide_mode = 1;
+    s->stats.edge_bytes = 32;
+}
+
+// composites on the int64 state: one grid per composite, planes from the
+// int32 staging (src | snk | nbr per composite at comp_off)
+int wide_comp_run(pmf_solver *s, int32_t ncomp, const int32_t *width, const int32_t *height,
+                  const std::vector<int32_t> &cs_off, int64_t total_px) {
+    int rc;
+    if ((rc = wide_bracket(s))) return rc;
+    if ((rc = s->d_colswap.ensure(s->colswap.size() + 1)) || (rc = s->d_in32.ensure(size_t(total_px) * 6 * 4)) ||
+        (rc = s->d_off.ensure(size_t(ncomp) * 8)) || (rc = s->d_out.ensure(size_t(std::max<int64_t>(s->lay.out_bytes, 1)))))
+        return rc;
+    s->tmark(C_H2D);
+    CK(cudaMemcpyAsync(s->d_colswap.p, s->colswap.data(), s->colswap.size(), cudaMemcpyHostToDevice, s->st));
+    CK(cudaMemcpyAsync(s->d_in32.p, s->h_in32.p, size_t(total_px) * 6 * 4, cudaMemcpyHostToDevice, s->st));
+    CK(cudaMemcpyAsync(s->d_off.p, s->comp_off.data(), size_t(ncomp) * 8, cudaMemcpyHostToDevice, s->st));
+    s->tmark(C_BUILD);
+    WideBatch B;
+    for (int32_t c = 0; c < ncomp; c++)
+        B.add(width[c], height[c], s->comp_out[size_t(c)], width[c], 0, cs_off[size_t(c)], c, c, 0);
+    WCtx c;
+    if ((rc = wide_setup(s, B, &c))) return rc;
+    const int32_t *din = s->d_in32.as<int32_t>();
+    LAUNCH(s, (k_wide_load_comp<<<wide_grid(s, c), 1024, 0, s->st>>>(c, din, din + total_px, din + 2 * total_px,
+                                                                     s->d_off.as<int64_t>())));
+    CK(cudaGetLastError());
+    return wide_solve(s, c, ncomp);
 }
 
 // --------------------------------------------------------------------------
@@ -1618,6 +1836,8 @@ int pmf_solver_destroy(pmf_solver *s) {
     cudaSetDevice(s->device);
     if (s->st) cudaStreamSynchronize(s->st);
     for (auto e : s->ev_pool) cudaEventDestroy(e);
+    for (auto e : s->fetch_ev)
+        if (e) cudaEventDestroy(e);
     if (s->gexec) cudaGraphExecDestroy(s->gexec);
     delete s->pool;
     for (auto e : s->ev_run)
@@ -1665,6 +1885,8 @@ int pmf_solver_set(pmf_solver *s, const char *name, int64_t v) {
     else if (k == "push_budget" && v >= 0) s->push_budget = int(v);
     else if (k == "timing") s->timing = v != 0;
     else if (k == "max_cycles" && v >= 1) s->max_cycles = v;
+    else if (k == "force_wide") s->force_wide = v != 0;
+    else if (k == "wide_pulses" && v >= 1 && v <= 100000) s->wide_pulses = int(v);
     else return fail(PMF_ERR_ARG, "unknown knob or bad value: %s=%lld", name, (long long)v);
     return 0;
 }
@@ -1693,6 +1915,11 @@ static int solve_composites_t(pmf_solver *s, int32_t ncomp, const int32_t *width
         return fail(PMF_ERR_ARG, "bad arguments");
     CK(cudaSetDevice(s->device));
     CK(cudaStreamSynchronize(s->st));   // staging buffers are reused below
+    // a composite solve overwrites the staged seed batch's layout, planes,
+    // offsets, labels and flows (pmf_seed_run/fetch/score refuse until the
+    // next pmf_seed_stage), and the previous composites' labels
+    s->stage.valid = false;
+    s->comp_n.clear();
     s->lay.clear();
     s->colswap.clear();
     s->comp_off.assign(size_t(ncomp), 0);
@@ -1767,8 +1994,9 @@ static int solve_composites_t(pmf_solver *s, int32_t ncomp, const int32_t *width
         maxpair = std::max(maxpair, mp[k]);
         maxexcess = std::max(maxexcess, mx[k]);
     }
-    if (maxexcess >= (int64_t(1) << 31) - 1)
-        return fail(PMF_ERR_RANGE, "capacities too large for the int32 device state");
+    // past int32 the composites run on the int64 state variant (wide.cuh),
+    // one grid per composite
+    const bool wide = s->force_wide || maxexcess >= (int64_t(1) << 31) - 1;
     // Segments whose spans no arc leaves (bridge / uncovered columns all
     // zero, no LEFT arc on a span's first column, no RIGHT arc on its last)
     // are independent max-flow problems: each becomes a grid of its own
@@ -1781,7 +2009,7 @@ static int solve_composites_t(pmf_solver *s, int32_t ncomp, const int32_t *width
     std::vector<uint8_t> cand(size_t(ncomp), 0), leak(size_t(band_base[size_t(ncomp)]), 0);
     for (int c = 0; c < ncomp; c++) {
         const int ns = nseg ? nseg[c] : 0;
-        if (!s->comp_split || ns < 2) continue;
+        if (!s->comp_split || ns < 2 || wide) continue;
         cand[size_t(c)] = 1;
         for (int k = 0; k < ns; k++)
             for (int x = seg_off[c][k]; x < seg_off[c][k] + seg_w[c][k]; x++) colseg[size_t(cs_off[c] + x)] = k;
@@ -1819,11 +2047,11 @@ static int solve_composites_t(pmf_solver *s, int32_t ncomp, const int32_t *width
     int any_split = 0;
     std::vector<int64_t> &comp_out = s->comp_out;   // output offset per composite (16-byte aligned,
     comp_out.assign(size_t(ncomp), 0);              // so pmf_composite_bits can pack it in place)
-    s->comp_n.assign(size_t(ncomp), 0);
+    std::vector<int64_t> comp_n(size_t(ncomp), 0);  // published once the solve succeeded
     for (int c = 0; c < ncomp; c++) {
         s->lay.out_bytes = (s->lay.out_bytes + 15) / 16 * 16;
         comp_out[size_t(c)] = s->lay.out_bytes;
-        s->comp_n[size_t(c)] = int64_t(width[c]) * height[c];
+        comp_n[size_t(c)] = int64_t(width[c]) * height[c];
         if (split[size_t(c)]) {
             any_split = 1;
             const int64_t base = s->lay.out_bytes;
@@ -1839,7 +2067,8 @@ static int solve_composites_t(pmf_solver *s, int32_t ncomp, const int32_t *width
     const int64_t G = int64_t(s->lay.grids.size());
     if ((rc = s->d_flows.ensure(size_t(G) * 8))) return rc;
     if ((rc = run_begin(s))) return rc;
-    rc = maxpair <= 255 ? comp_run_t<EdgeU8>(s, ncomp, total_px) : comp_run_t<EdgeI32>(s, ncomp, total_px);
+    rc = wide ? wide_comp_run(s, ncomp, width, height, cs_off, total_px)
+              : maxpair <= 255 ? comp_run_t<EdgeU8>(s, ncomp, total_px) : comp_run_t<EdgeI32>(s, ncomp, total_px);
     if (rc) return rc;
     // outputs
     s->tmark(C_D2H);
@@ -1853,6 +2082,8 @@ static int solve_composites_t(pmf_solver *s, int32_t ncomp, const int32_t *width
     if (any_labels) CK(cudaMemcpyAsync(ho, s->d_out.p, L.out_bytes, cudaMemcpyDeviceToHost, s->st));
     CK(cudaMemcpyAsync(hsnk, s->d_flows.p, G * 8, cudaMemcpyDeviceToHost, s->st));
     if ((rc = run_end(s))) return rc;
+    if (wide) wide_stats(s);
+    s->comp_n = std::move(comp_n);
     for (int c = 0; c < ncomp; c++) flow_out[c] = 0;
     for (int64_t g = 0; g < G; g++) flow_out[L.grids[size_t(g)].prob] += hsnk[g];
     for (int c = 0; c < ncomp; c++)
@@ -1975,9 +2206,10 @@ int pmf_seed_run(pmf_solver *s) {
     int64_t h2d = s->stats.h2d_bytes;
     int rc = run_begin(s);
     if (rc) return rc;
-    rc = s->stage.u8 ? seed_run_t<EdgeU8>(s) : seed_run_t<EdgeI32>(s);
+    rc = s->stage.wide ? wide_seed_run(s) : s->stage.u8 ? seed_run_t<EdgeU8>(s) : seed_run_t<EdgeI32>(s);
     if (rc) return rc;
     rc = run_end(s);
+    if (s->stage.wide) wide_stats(s);
     s->stats.h2d_bytes = h2d;
     return rc;
 }

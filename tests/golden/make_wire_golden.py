@@ -32,6 +32,26 @@ from pmflow.supergraph import apply_swap, join, solve_composite  # noqa: E402
 OUT = os.path.join(os.path.dirname(os.path.abspath(__file__)), "wire_frames.json")
 
 
+def wide_grid(rng, w, h):
+    """Random admitted grid with capacities drawn from {0, small, up to
+    CAP_MAX, CAP_MAX}: most pixels' excess bound is far past 2**31."""
+    cap = 1 << 30
+
+    def draw(shape):
+        kind = rng.integers(0, 4, shape)
+        v = np.where(kind == 0, 0, np.where(kind == 1, rng.integers(1, 100, shape),
+                                            np.where(kind == 2, rng.integers(1, cap + 1, shape), cap)))
+        return v.astype(np.int64)
+
+    src, snk, nbr = draw(w * h), draw(w * h), draw((4, w * h)).reshape(4, h, w)
+    nbr[0][:, 0] = 0
+    nbr[1][:, -1] = 0
+    nbr[2][0, :] = 0
+    nbr[3][-1, :] = 0
+    from pmflow.grid import GridGraph
+    return admit(GridGraph(w, h, src, snk, nbr.reshape(4, w * h)))
+
+
 def served(payload: bytes) -> bytes:
     """What the reference worker answers for one payload (rpc.py:147-195)."""
     try:
@@ -58,6 +78,13 @@ def main():
     for k, (w, h) in enumerate([(1, 1), (8, 1), (6, 9), (13, 11)]):
         g = random_grid(rng, w, h, cap_hi=50)
         frames.append((f"whole_{w}x{h}", wire.encode_request(wire.WireRequest(1000 + k, g, None))))
+    # graphs the reference admits whose excess leaves int32 (CAP_MAX arc
+    # pairs and CAP_MAX terminals next to them): the engine's int64 variant
+    for k, (w, h) in enumerate([(7, 5), (12, 9)]):
+        frames.append((f"wide_{w}x{h}", wire.encode_request(wire.WireRequest(2000 + k, wide_grid(rng, w, h), None))))
+    wparts = [wide_grid(rng, 6, 5), wide_grid(rng, 4, 5)]
+    wcomp, wlay = join([wparts[0], apply_swap(wparts[1])], swapped=[False, True])
+    frames.append(("wide_composite_2seg", wire.encode_request(wire.WireRequest(2100, wcomp, wlay))))
     good = frames[0][1]
     # malformed payloads, one per failure class
     bad = {
@@ -79,6 +106,11 @@ def main():
     border = bytearray(good)
     border[planes_at + 8 * n: planes_at + 8 * n + 4] = struct.pack("<i", 5)   # LEFT arc of pixel 0
     bad["border_arc"] = bytes(border)
+    # a range error together with a framing error: the reference's decode
+    # reports the range error when the planes are complete and the framing
+    # error when they are not (decode_request's order, wire.py:189-228)
+    bad["range_and_trailing"] = bytes(big) + b"\0"
+    bad["range_and_truncated"] = bytes(neg)[:-3]
     frames += sorted(bad.items())
     out = []
     for name, payload in frames:

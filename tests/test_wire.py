@@ -124,3 +124,17 @@ def test_encoder_rejects_capacities_the_wire_cannot_carry():
         g2 = GridGraph(g.width, g.height, src, g.snk_cap, g.nbr_cap)
         with pytest.raises(wire.CapacityRangeError):
             wire.encode_request(wire.WireRequest(1, g2, None))
+
+
+@pytest.mark.parametrize("f", [f for f in GOOD if f["name"].startswith("wide_")], ids=lambda f: f["name"])
+def test_oracle_pinned_on_wide_frames(f):
+    """The oracle (the GPU tests' checker) reproduces the reference worker's
+    answers on requests whose excess leaves int32 (CAP_MAX arc pairs)."""
+    import oracle
+    req = wire.decode_request(bytes.fromhex(f["request"]))
+    g = req.graph
+    segs = [(s.offset, s.width, s.swapped) for s in req.layout.segments]
+    flow, labels, _ = oracle.solve(g.width, g.height, g.src_cap, g.snk_cap, g.nbr_cap, segs)
+    r = wire.decode_response(bytes.fromhex(f["response"]), g.n)
+    assert flow == r.flow
+    assert np.array_equal(labels, r.labels)
