@@ -255,7 +255,7 @@ struct pmf_solver {
     DevBuf d_w, d_h, d_r, d_lab, d_tile_grid, d_tnb, d_fin, d_gpend, d_specg, d_keeph, d_seeds, d_sofs, d_gr, d_tflag, d_vacc, d_truth, d_score, d_plog, d_tfresh, d_grids, d_live, d_act, d_list, d_inq, d_cnt,
         d_snk, d_drain, d_err, d_stat, d_colswap, d_out, d_bits, d_in32, d_pw, d_mask, d_off, d_lam,
         d_swapcnt, d_swapflag, d_ring, d_qstate, d_qctr, d_ctl, d_curlam, d_flows, d_slopesum,
-        d_we, d_wr, d_wgrid, d_wtile, d_wchg, d_wcnt;   // int64 state variant (wide.cuh)
+        d_we, d_wr, d_wgrid, d_wtile, d_wchg, d_wcnt, d_cv;   // int64 state variant (wide.cuh)
     HostBuf h_in32, h_pw, h_mask, h_out, h_small, h_seeds;
     Layout lay;
     std::vector<int32_t> ones, curlam0;
@@ -2047,7 +2047,7 @@ static int solve_composites_t(pmf_solver *s, int32_t ncomp, const int32_t *width
     int any_split = 0;
     std::vector<int64_t> &comp_out = s->comp_out;   // output offset per composite (16-byte aligned,
     comp_out.assign(size_t(ncomp), 0);              // so pmf_composite_bits can pack it in place)
-    std::vector<int64_t> comp_n(size_t(ncomp), 0);  // published once the solve succeeded
+    std::vector<int64_t> comp_n(static_cast<size_t>(ncomp), 0);  // published once the solve succeeded
     for (int c = 0; c < ncomp; c++) {
         s->lay.out_bytes = (s->lay.out_bytes + 15) / 16 * 16;
         comp_out[size_t(c)] = s->lay.out_bytes;
@@ -2070,13 +2070,49 @@ static int solve_composites_t(pmf_solver *s, int32_t ncomp, const int32_t *width
     rc = wide ? wide_comp_run(s, ncomp, width, height, cs_off, total_px)
               : maxpair <= 255 ? comp_run_t<EdgeU8>(s, ncomp, total_px) : comp_run_t<EdgeI32>(s, ncomp, total_px);
     if (rc) return rc;
+    // integrity certificate: cut cost of every composite's labels == its flow
+    if (s->verify) {
+        std::vector<CompV> vdesc(static_cast<size_t>(ncomp));
+        int64_t cmax = 0;
+        for (int c = 0; c < ncomp; c++) {
+            CompV &v = vdesc[size_t(c)];
+            v.off = s->comp_off[size_t(c)];
+            v.out_off = comp_out[size_t(c)];
+            v.W = width[c];
+            v.H = height[c];
+            cmax = std::max(cmax, int64_t(width[c]) * height[c]);
+        }
+        if ((rc = s->d_cv.ensure(size_t(ncomp) * sizeof(CompV))) || (rc = s->d_vacc.ensure(size_t(ncomp) * 8)))
+            return rc;
+        CK(cudaMemcpyAsync(s->d_cv.p, vdesc.data(), size_t(ncomp) * sizeof(CompV), cudaMemcpyHostToDevice, s->st));
+        CK(cudaMemsetAsync(s->d_vacc.p, 0, size_t(ncomp) * 8, s->st));
+        // verify=2 (test hook): flip the first label of composite 0 whose
+        // pixel has src != snk, so the check must fail
+        if (s->verify == 2) {
+            const int32_t *hin = s->h_in32.as<int32_t>();
+            const int64_t n0 = int64_t(width[0]) * height[0];
+            for (int64_t q = 0; q < n0; q++)
+                if (hin[q] != hin[total_px + q]) {
+                    LAUNCH(s, (k_flip_label<<<1, 1, 0, s->st>>>(s->d_out.as<uint8_t>() + comp_out[0], q)));
+                    break;
+                }
+        }
+        const int chunks = int(std::max<int64_t>(1, std::min<int64_t>(cdiv(cmax, 8 * NT), 4096)));
+        LAUNCH(s, (k_comp_verify<<<int(std::max<int64_t>(1, std::min<int64_t>(int64_t(ncomp) * chunks, 32 * s->sms))),
+                                    NT, 0, s->st>>>(s->d_in32.as<int32_t>(), total_px, s->d_cv.as<CompV>(),
+                                                    s->d_out.as<uint8_t>(), ncomp, chunks,
+                                                    s->d_vacc.as<unsigned long long>())));
+        CK(cudaGetLastError());
+    }
     // outputs
     s->tmark(C_D2H);
     const Layout &L = s->lay;
     const size_t lab_bytes = size_t((L.out_bytes + 7) / 8) * 8;
-    if ((rc = s->h_out.ensure(lab_bytes + size_t(G) * 8))) return rc;
+    if ((rc = s->h_out.ensure(lab_bytes + size_t(G) * 8 + size_t(ncomp) * 8))) return rc;
     uint8_t *ho = s->h_out.as<uint8_t>();
     int64_t *hsnk = (int64_t *)(ho + lab_bytes);
+    int64_t *hcost = hsnk + G;
+    if (s->verify) CK(cudaMemcpyAsync(hcost, s->d_vacc.p, size_t(ncomp) * 8, cudaMemcpyDeviceToHost, s->st));
     bool any_labels = false;   // a null labels_out[c]: labels stay on the device (pmf_composite_bits)
     for (int c = 0; c < ncomp; c++) any_labels |= labels_out[c] != nullptr;
     if (any_labels) CK(cudaMemcpyAsync(ho, s->d_out.p, L.out_bytes, cudaMemcpyDeviceToHost, s->st));
@@ -2086,6 +2122,13 @@ static int solve_composites_t(pmf_solver *s, int32_t ncomp, const int32_t *width
     s->comp_n = std::move(comp_n);
     for (int c = 0; c < ncomp; c++) flow_out[c] = 0;
     for (int64_t g = 0; g < G; g++) flow_out[L.grids[size_t(g)].prob] += hsnk[g];
+    if (s->verify)
+        for (int c = 0; c < ncomp; c++)
+            if (hcost[c] != flow_out[c]) {
+                s->comp_n.clear();
+                return fail(PMF_ERR_NONMAX, "composite %d: cut cost %lld differs from its flow %lld (integrity check)",
+                            c, (long long)hcost[c], (long long)flow_out[c]);
+            }
     for (int c = 0; c < ncomp; c++)
         if (labels_out[c]) memcpy(labels_out[c], ho + comp_out[size_t(c)], size_t(width[c]) * height[c]);
     s->stats.h2d_bytes = total_px * 6 * 4;

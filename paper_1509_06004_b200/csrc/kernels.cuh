@@ -766,6 +766,48 @@ __global__ void __launch_bounds__(NT, 3) k_verify4(Ctx c, SeedArgs a, unsigned l
 
 __global__ void k_flip_label(uint8_t *out, int64_t q) { out[q] ^= 1; }
 
+// Integrity certificate of a composite solve (supergraph.py:181-186 split's
+// sum check, rpc.py:328-331 the client's check): the cut cost of every
+// composite's emitted labels on its own (admitted) planes, summed into
+// acc[c] and compared with its flow on the host.  Swapped spans carry the
+// maximal source side of their segment (supergraph.py:201-206), also a
+// minimum cut, so the cost equals the flow there as well.  One CTA per
+// (composite, pixel chunk); planes row-major int32 as staged
+// (src | snk | nbr(4n) per composite at off).
+struct CompV {
+    int64_t off, out_off;
+    int32_t W, H;
+};
+__global__ void __launch_bounds__(NT) k_comp_verify(const int32_t *__restrict__ in, int64_t total_px,
+                                                    const CompV *__restrict__ cv, const uint8_t *__restrict__ out,
+                                                    int32_t ncomp, int chunks, unsigned long long *acc) {
+    __shared__ int64_t red[NT / 32];
+    for (int64_t blk = blockIdx.x; blk < int64_t(ncomp) * chunks; blk += gridDim.x) {
+        const int c = int(blk / chunks);
+        const CompV v = cv[c];
+        const int64_t n = int64_t(v.W) * v.H, per = (n + chunks - 1) / chunks;
+        const int64_t lo = (blk % chunks) * per, hi = min(n, lo + per);
+        const int32_t *src = in + v.off, *snk = in + total_px + v.off, *nb = in + 2 * total_px + 4 * v.off;
+        const uint8_t *l = out + v.out_off;
+        int64_t cost = 0;
+        for (int64_t q = lo + threadIdx.x; q < hi; q += NT) {
+            if (!l[q]) {
+                cost += src[q];
+                continue;
+            }
+            const int32_t x = int32_t(q % v.W), y = int32_t(q / v.W);
+            cost += snk[q];
+            if (x > 0 && !l[q - 1]) cost += nb[q];
+            if (x + 1 < v.W && !l[q + 1]) cost += nb[n + q];
+            if (y > 0 && !l[q - v.W]) cost += nb[2 * n + q];
+            if (y + 1 < v.H && !l[q + v.W]) cost += nb[3 * n + q];
+        }
+        cost = block_sum64(cost, red);
+        if (threadIdx.x == 0 && cost) atomicAdd(acc + c, (unsigned long long)cost);
+    }
+}
+
+
 __global__ void k_verify_check(Ctx c, int64_t nplanes, const unsigned long long *acc) {
     for (int64_t plane = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; plane < nplanes;
          plane += int64_t(gridDim.x) * blockDim.x)

@@ -199,7 +199,20 @@ class GpuBackend:
                 results = self._run_batch([t for t, _ in batch], dev)
                 errs = [None] * len(batch)
             except Exception as exc:  # noqa: BLE001
-                results, errs = [None] * len(batch), [_wrap(exc)] * len(batch)
+                if len(batch) == 1:
+                    results, errs = [None], [_wrap(exc)]
+                else:
+                    # a coalesced batch failed: solve its tasks one at a time so
+                    # the failure is charged to the task that caused it (the
+                    # reference charges only the failing task, scheduler.py:270-279)
+                    results, errs = [], []
+                    for t, _ in batch:
+                        try:
+                            results.append(self._run_batch([t], dev)[0])
+                            errs.append(None)
+                        except Exception as exc1:  # noqa: BLE001
+                            results.append(None)
+                            errs.append(_wrap(exc1))
             fin = self._now()
             for (task, attempt), res, err in zip(batch, results, errs):
                 self._done.put(Completion(task, worker, attempt, start, fin, res, err))

@@ -183,3 +183,28 @@ def test_composite_solve_invalidates_the_staged_seed_batch(engine):
             s.seed_fetch()
     finally:
         s.close()
+
+
+@pytest.mark.parametrize("wide", [0, 1])
+def test_composite_certificate_catches_a_corrupted_cut(engine, wide):
+    """Composite solves carry the device certificate too (cut cost of the
+    emitted labels == flow, supergraph.py:181-186, rpc.py:328-331): with the
+    verify=2 hook corrupting one label the solve raises; without it the same
+    composites pass."""
+    from paper_1509_06004_b200 import NonMaximalFlowError
+    rng = np.random.default_rng(40 + wide)
+    parts = [wide_graph(rng, 12, 9) if wide else
+             admit(GridGraph(12, 9, rng.integers(0, 50, 108), rng.integers(0, 50, 108),
+                             zero_border(rng.integers(1, 30, (4, 9, 12))).reshape(4, -1)))
+             for _ in range(3)]
+    comp, lay = join([parts[0], apply_swap(parts[1]), parts[2]], swapped=[False, True, False])
+    s = _native.solver_for_thread(0)
+    good = solve_composites([(comp, lay)])[0]
+    assert s.stats()["wide_mode"] == wide
+    assert cut_cost(comp, good.labels) == good.flow
+    s.set("verify", 2)
+    try:
+        with pytest.raises(NonMaximalFlowError):
+            solve_composites([(comp, lay)])
+    finally:
+        s.set("verify", 1)

@@ -262,6 +262,60 @@ def test_run_dynamic_retries_once_then_aborts():
         backend.close()
 
 
+def test_gpu_backend_two_devices_dynamic_placement_and_retry():
+    """GpuBackend over two (fake) devices through its solver= hook: tasks go
+    FIFO to both devices; device 1 fails, is retired, and every task it had
+    is retried once on device 0 (scheduler.py:253-292)."""
+    import threading
+    from paper_1509_06004_b200 import GpuBackend, gpu_workers
+    seen = {0: [], 1: []}
+    lock = threading.Lock()
+
+    def fake(tasks, dev):
+        with lock:
+            seen[dev] += [t.id for t in tasks]
+        if dev == 1:
+            raise RuntimeError("device 1 lost")
+        return [CutResult(t.id * 10 + dev, np.zeros(1, np.uint8)) for t in tasks]
+
+    tasks = [Task(id=i) for i in range(12)]
+    backend = GpuBackend(max_batch=4, solver=fake)
+    try:
+        sched, cuts = run_dynamic(tasks, gpu_workers([0, 1], slots=2), backend)
+    finally:
+        backend.close()
+    assert sorted(cuts) == list(range(12))
+    assert all(cuts[i].flow == 10 * i for i in range(12))          # all solved on device 0
+    assert seen[1], "device 1 never received work"
+    for tid in set(seen[1]):
+        rec = sched.record_for(tid)
+        assert rec.worker_id == 0 and rec.attempt == 2              # retried once, elsewhere
+    assert all(sched.record_for(t).attempt == 1 for t in range(12) if t not in seen[1])
+
+
+def test_gpu_backend_charges_a_failure_to_its_task():
+    """A coalesced device batch that fails is re-solved task by task, so the
+    innocent tasks complete and the abort names the task that failed twice."""
+    import threading
+    from paper_1509_06004_b200 import GpuBackend, gpu_workers
+    gate = threading.Event()
+
+    def fake(tasks, dev):
+        gate.wait(5)   # let the queue fill so tasks coalesce
+        if any(t.id == 3 for t in tasks):
+            raise RuntimeError("bad task")
+        return [CutResult(t.id, np.zeros(1, np.uint8)) for t in tasks]
+
+    backend = GpuBackend(max_batch=8, solver=fake)
+    threading.Timer(0.2, gate.set).start()
+    try:
+        with pytest.raises(BatchAborted, match="task 3 failed twice"):
+            run_dynamic([Task(id=i) for i in range(6)], gpu_workers([0, 1], slots=6), backend)
+    finally:
+        gate.set()
+        backend.close()
+
+
 # ------------------------------------------------------------- synth
 
 def test_quantize_weights_rounds_half_up():
