@@ -9,6 +9,7 @@ scheduler.  Solves run on hand-written sm_100a CUDA kernels
 fallback.
 """
 
+from .floatcap import FloatCutResult, maxflow_float, maxflow_float_many, quantize_graph
 from .grid import (CAP_MAX, BorderEdgeError, CapacityOverflowError, CutResult, GraphError,
                    GridGraph, NegativeCapacityError, ShapeError, admit, cut_cost)
 from .parametric import (DEFAULT_LAMBDA_VALUES, HALVED_LAMBDA_VALUES, LambdaSchedule,
@@ -25,7 +26,7 @@ from .supergraph import (SeedSupergraphResult, Segment, SupergraphError, Supergr
 __version__ = "0.1.0"
 
 __all__ = [
-    "CAP_MAX", "BatchAborted", "BorderEdgeError", "CapacityOverflowError", "CutResult",
+    "CAP_MAX", "BatchAborted", "FloatCutResult", "maxflow_float", "maxflow_float_many", "quantize_graph", "BorderEdgeError", "CapacityOverflowError", "CutResult",
     "DEFAULT_LAMBDA_VALUES", "GpuBackend", "GraphError", "GridGraph", "HALVED_LAMBDA_VALUES",
     "LambdaSchedule", "NegativeCapacityError", "NonMaximalFlowError", "ParametricResult",
     "ProblemError", "ScheduleError", "SchedulerError", "SeedProblem", "SeedSupergraphResult",

@@ -316,6 +316,35 @@ def test_c3_cpmc_image_rolling_vs_cold_vs_reference(engine):
         assert np.array_equal(lw[pi, li].reshape(-1), labels)
 
 
+def test_c5_batch_sampled_cuts_vs_oracle(engine):
+    """C5's unit of work -- 8 distinct CPMC images (rng_seed 0..7) in one
+    device batch, 400 warm-start chains, the step-synchronous rolling engine
+    the bench runs -- against the oracle on 50 sampled (image, problem,
+    lambda) cuts: bit-exact flows and masks.  Every cut also passed the
+    device certificate (cut cost == flow) inside the solve."""
+    from paper_1509_06004_b200 import _native
+    probs = []
+    for i in range(8):
+        probs += synth.generate(500, 375, 5, 5, rng_seed=i, types=("A", "B")).problems
+    s = _native.Solver(0)
+    try:
+        _, fl, lab = s.solve_seed_batch(500, 375, probs, synth.L20, "auto")
+        assert s.stats()["async_mode"] == 0   # 8 images: the step-synchronous engine
+    finally:
+        s.close()
+    rng = np.random.default_rng(2026)
+    picks = [(int(rng.integers(0, len(probs))), int(rng.integers(0, len(synth.L20)))) for _ in range(50)]
+    jobs = []
+    for pi, li in picks:
+        p = probs[pi]
+        src, snk, nbr = oracle.instantiate(p.unary_base, p.unary_slope, p.sink_base, p.pairwise,
+                                           p.fg_seeds, p.bg_seeds, synth.L20[li])
+        jobs.append((500, 375, src, snk, nbr, None))
+    for (pi, li), (flow, labels, _) in zip(picks, oracle.solve_many(jobs)):
+        assert int(fl[pi, li]) == flow, (pi // 50, pi % 50, li)
+        assert np.array_equal(lab[pi, li].reshape(-1), labels), (pi // 50, pi % 50, li)
+
+
 def test_staging_shares_equal_planes_but_checks_each_mask(engine):
     """Problems with equal unary/sink planes are staged once (pointer-equal
     or content-equal arrays); results stay per problem, and each problem's

@@ -85,3 +85,23 @@ def test_c2_generator_digest():
     g = load_synth("c2_500x375.npz")
     assert problem_digest(synth.generate(500, 375, rng_seed=0).problems[0]) == g["sha"]
     assert sum(g["flows"]) == 90475333
+
+
+def test_fp64_checker_pinned_on_integer_vectors():
+    """The fp64 Dinic checker of the float mode (oracle/maxflow_f64.c)
+    reproduces the reference's flows and minimal source sides exactly on
+    integer-valued graphs (integers are exact in double): the KATs, the 500
+    random 8x8 grids and the C1 per-lambda cuts."""
+    for name, k in load_kat().items():
+        f, lab = oracle.maxflow_f64(k["width"], k["height"], k["src"], k["snk"], k["nbr"])
+        assert f == k["flow"], name
+        assert lab.tolist() == k["labels"], name
+    for (w, h, s, t, nb, flow, labels) in load_random("random_8x8_seed101.npz"):
+        f, lab = oracle.maxflow_f64(w, h, s, t, nb)
+        assert f == flow and np.array_equal(lab, labels)
+    gold = load_synth("c1_160x120.npz")
+    p = oracle.synth_problems(160, 120, 1, 1, rng_seed=0)[0]
+    for k in (0, 4, 19):
+        src, snk, nbr = oracle.instantiate(*p[2:], gold["lambdas"][k])
+        f, lab = oracle.maxflow_f64(160, 120, src, snk, nbr)
+        assert f == gold["flows"][k] and np.array_equal(lab, gold["labels"][k])
