@@ -1,24 +1,30 @@
 """Benchmark: lambda-graph min-cuts/sec of the supergraph path on B200.
 
-    python bench.py [--gpus N] [--steps K] [--warmup W] [--config c2]
-                    [--impl b200|reference] [--no-cpu-baseline] [--no-cpmc]
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config c5]
+                    [--impl b200|reference] [--no-cpu-baseline] [--no-secondary]
 
-One step = one pass of the hot path over one batch: the seed supergraph of
-BASELINE.json config 2 (synthetic 500x375 image, 1 seed, 20-lambda ladder,
-integer capacities) built, solved and decoded on one GPU = 20 lambda-cuts.
-Under torchrun (N > 1) every rank solves its own supergraph per step (weak
-scaling, independent supergraphs, no data-path collective); ranks only
-meet in barriers and a max-reduction of their times.
+Default workload (BASELINE.json config 5, the multi-GPU headline; its unit
+of work is config 3's CPMC image): a pool of 256 distinct synthetic CPMC
+images (500x375, rng_seed 0..255; 25 seeds x 2 seed types x 20 lambdas =
+1,000 lambda-graphs each), cut into 32 batches of 8 images.  One step of a
+rank = one batch, CLAIMED DYNAMICALLY: the rank takes the next batch of the
+shared FIFO (a counter on the process group's store, the torchrun
+analogue of run_dynamic's token queue, scheduler.py:253-292) and solves it
+as one device batch (8,000 lambda-cuts).  Per-GPU work per step is fixed,
+so scaling is weak; no data-path collective exists (ranks share only the
+claim counter, barriers and a max-reduction, over gloo -- no NCCL).
 
-value : whole-job lambda-cuts/s with the seed planes already resident in
-        HBM (pmf_seed_run), device time from CUDA events on the engine's
-        stream, L2 flushed (256 MiB memset) between steps, max over ranks.
-e2e   : the same metric through the public API (solve_seed_supergraph)
-        from host SeedProblem objects: conversion + H2D + solve + D2H of
-        every label mask + CutResult construction, wall clock per step.
+value : whole-job lambda-cuts/s with the batch's seed planes already
+        resident in HBM (pmf_seed_stage before the timed events), device
+        time of pmf_seed_run from CUDA events on the engine's stream, L2
+        flushed between steps, max over ranks.
+e2e   : the same metric through the public API (solve_seed_supergraph) on
+        FRESH SeedProblem objects (admission checks, int64 -> int32
+        narrowing, H2D, solve, D2H of every label mask, CutResult
+        construction), wall clock, max over ranks.
 --impl reference : the reference solver's algorithm (oracle/, a C
         restatement of pmflow's push-relabel) on the host cores, same
-        config, same metric.
+        workload, a bounded sample per step, same metric.
 """
 
 from __future__ import annotations
@@ -37,25 +43,26 @@ sys.path.insert(0, ROOT)
 
 METRIC = "lambda-graph min-cuts/sec"
 UNIT = "lambda-cuts/s"
+POOL_IMAGES = 256            # C5: rng_seed 0..255
 CONFIGS = {
-    "c1": dict(w=160, h=120, rows=1, cols=1, types=("A",), lams="default",
-               desc="C1: synthetic 160x120, 1 seed, DEFAULT 20-lambda ladder, one supergraph"),
-    "c2": dict(w=500, h=375, rows=1, cols=1, types=("A",), lams="L20",
+    "c1": dict(w=160, h=120, rows=1, cols=1, types=("A",), lams="default", images=1,
+               desc="C1: synthetic 160x120, 1 seed, DEFAULT 20-lambda ladder, one supergraph per step"),
+    "c2": dict(w=500, h=375, rows=1, cols=1, types=("A",), lams="L20", images=1,
                desc="C2: synthetic 500x375 (VOC-sized), 1 seed, 20-lambda ladder L20, "
                     "one supergraph (20 lambda-graphs) per GPU per step"),
-    "c3": dict(w=500, h=375, rows=5, cols=5, types=("A", "B"), lams="L20",
+    "c3": dict(w=500, h=375, rows=5, cols=5, types=("A", "B"), lams="L20", images=1,
                desc="C3: one CPMC-style image per GPU per step -- synthetic 500x375, 25 seeds x "
-                    "2 seed types x 20 lambdas = 1000 lambda-graphs in one device batch "
-                    "(warm-start chains along the schedule)"),
-    "c4": dict(w=1920, h=1080, rows=1, cols=1, types=("A",), lams="C4",
+                    "2 seed types x 20 lambdas = 1000 lambda-graphs in one device batch"),
+    "c4": dict(w=1920, h=1080, rows=1, cols=1, types=("A",), lams="C4", images=1,
                desc="C4: synthetic 1920x1080, 1 seed, 8 lambdas per supergraph"),
     "c5": dict(w=500, h=375, rows=5, cols=5, types=("A", "B"), lams="L20", images=8,
-               desc="C5: batch throughput -- 8 synthetic CPMC images (500x375, 25 seeds x 2 types "
-                    "x 20 lambdas) per GPU per step, images independent across GPUs"),
+               desc="C5: batch throughput over 256 distinct CPMC images (500x375, 25 seeds x 2 types "
+                    "x 20 lambdas; rng_seed 0..255) in batches of 8 images claimed dynamically "
+                    "(FIFO) by the GPUs; one batch per GPU per step"),
 }
 # CPU reference sample per step for the big configs (the full C3 image is
 # ~3,400 CPU-s on the reference algorithm): the first problems' lambda graphs
-REF_SAMPLE_PROBLEMS = {"c3": 2, "c5": 2, "c4": 1}
+REF_SAMPLE_PROBLEMS = {"c3": 1, "c5": 1, "c4": 1}
 BYTES_PER_PIXEL_PASS = {4: 24, 16: 48}   # load+store of w, h and the residual word(s)
 # algorithmic bytes per pixel of one tile pass of each kind of the
 # asynchronous solver, by residual word size 4 / 16:
@@ -75,31 +82,50 @@ def dist_env():
             int(os.environ.get("WORLD_SIZE", 1)))
 
 
-def shard(n_units: int, rank: int, world: int):
-    """Contiguous block of unit indices owned by ``rank`` (independent
-    supergraphs; no exchange between ranks)."""
-    base, extra = divmod(n_units, world)
-    start = rank * base + min(rank, extra)
-    return list(range(start, start + base + (1 if rank < extra else 0)))
-
-
-def reduce_max(value: float, device=None) -> float:
+def reduce_max(value: float) -> float:
     import torch
     import torch.distributed as dist
     if not (dist.is_available() and dist.is_initialized()):
         return value
-    t = torch.tensor([value], dtype=torch.float64, device=device)
+    t = torch.tensor([value], dtype=torch.float64)
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
     return float(t.item())
 
 
-def barrier(device=None):
+def barrier():
     import torch.distributed as dist
     if dist.is_available() and dist.is_initialized():
-        if device is not None and dist.get_backend() == "nccl":
-            dist.barrier(device_ids=[device])
-        else:
-            dist.barrier()
+        dist.barrier()
+
+
+class Claims:
+    """Shared FIFO of batch ids: rank r takes the next id with one atomic
+    add on the process group's store (torchrun), or a local counter."""
+
+    KEY = "pmf_bench_claims"
+
+    def __init__(self, shared: bool):
+        self.store, self.k = None, 0
+        if shared:
+            import torch.distributed as dist
+            self.store = dist.distributed_c10d._get_default_store()
+
+    def next(self) -> int:
+        if self.store is None:
+            self.k += 1
+            return self.k - 1
+        return int(self.store.add(self.KEY, 1)) - 1
+
+
+def cpu_model() -> str:
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
 
 
 def lambdas_for(name):
@@ -206,19 +232,32 @@ class ClockSampler:
                 "samples": len(self.rows), "source": "nvml" if self.nvml else "nvidia-smi"}
 
 
+
+
+# ------------------------------------------------------------- workload
+
+def batch_problems(cfg, b: int, sched):
+    """Fresh SeedProblem objects of batch b (images b*k .. b*k + k - 1 of
+    the pool, rng_seed = image index); generated on the host, untimed."""
+    from paper_1509_06004_b200 import synth
+    k = cfg["images"]
+    probs = []
+    for i in range(b * k, b * k + k):
+        probs += synth.generate(cfg["w"], cfg["h"], cfg["rows"], cfg["cols"], rng_seed=i % POOL_IMAGES,
+                                types=cfg["types"]).problems
+    return probs
+
+
 # ------------------------------------------------------------- CPU baseline
 
-def cpu_solve_config(cfg, rng_seed, threads, max_problems=None):
+def cpu_solve(cfg, problems, threads):
     """The reference's solver (C restatement in oracle/) on every lambda graph
-    of one supergraph (or of the first ``max_problems`` problems), per lambda
-    as solve_schedule_sequential does; returns (n_cuts, seconds, total_flow)."""
+    of the given problems, per lambda as solve_schedule_sequential does;
+    returns (n_cuts, seconds, flows)."""
     import oracle
-    from paper_1509_06004_b200 import synth
     lams = lambdas_for(cfg["lams"])
-    batch = synth.generate(cfg["w"], cfg["h"], cfg["rows"], cfg["cols"], rng_seed=rng_seed,
-                           types=cfg["types"])
     jobs = []
-    for p in batch.problems[:max_problems]:
+    for p in problems:
         for lam in lams:
             s, t, nb = oracle.instantiate(p.unary_base, p.unary_slope, p.sink_base, p.pairwise,
                                           p.fg_seeds, p.bg_seeds, lam)
@@ -226,7 +265,24 @@ def cpu_solve_config(cfg, rng_seed, threads, max_problems=None):
     t0 = time.perf_counter()
     res = oracle.solve_many(jobs, threads=threads)
     dt = time.perf_counter() - t0
-    return len(jobs), dt, sum(r[0] for r in res)
+    return len(jobs), dt, [r[0] for r in res]
+
+
+def ref_sample(cfg, step: int):
+    """Bounded CPU sample of one step: the problems of one seed supergraph
+    (C1/C2/C4), or REF_SAMPLE_PROBLEMS of them, rotating through the pool."""
+    from paper_1509_06004_b200 import synth
+    img = step % POOL_IMAGES
+    b = synth.generate(cfg["w"], cfg["h"], cfg["rows"], cfg["cols"], rng_seed=img, types=cfg["types"])
+    mp = REF_SAMPLE_PROBLEMS.get(args_config(cfg))
+    if mp is None:
+        return b.problems, img
+    k = (step * mp) % len(b.problems)
+    return (b.problems + b.problems)[k:k + mp], img
+
+
+def args_config(cfg):
+    return next(k for k, v in CONFIGS.items() if v is cfg)
 
 
 def run_reference(args, cfg):
@@ -236,194 +292,213 @@ def run_reference(args, cfg):
     import oracle
     oracle.build()
     threads = os.cpu_count() or 1
-    mp = REF_SAMPLE_PROBLEMS.get(args.config)
-    for _ in range(args.warmup):
-        cpu_solve_config(cfg, 0, threads, mp)
+    for i in range(args.warmup):
+        cpu_solve(cfg, ref_sample(cfg, i)[0], threads)
     tot_cuts, tot_s = 0, 0.0
-    for _ in range(args.steps):
-        n, dt, _ = cpu_solve_config(cfg, 0, threads, mp)
+    for i in range(args.steps):
+        n, dt, _ = cpu_solve(cfg, ref_sample(cfg, args.warmup + i)[0], threads)
         tot_cuts += n
         tot_s += dt
     value = tot_cuts / tot_s
-    what = (f"the lambda-graphs of the first {mp} seed problems" if mp else
+    mp = REF_SAMPLE_PROBLEMS.get(args.config)
+    what = (f"the lambda-graphs of {mp} seed problem(s) of one pool image, rotating" if mp else
             "all lambda-graphs of one supergraph")
     sample = (f"{cfg['desc']}: {what} per step ({tot_cuts // args.steps} graphs), solved with the "
               f"reference push-relabel restated in C (oracle/pmflow_oracle.c), per lambda as "
-              f"solve_schedule_sequential, {threads} host threads")
+              f"solve_schedule_sequential, {threads} host threads ({cpu_model()})")
     print(json.dumps({
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * tot_s / args.steps,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "int32",
         "data": "synthetic", "config": {"workload": cfg["desc"]},
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "port",
-                         "sample": sample},
+                         "cpu_model": cpu_model(), "sample": sample},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }), flush=True)
 
 
 # ---------------------------------------------------------------- GPU arm
 
-def run_b200(args, cfg):
-    import torch
-    import torch.distributed as dist
-
-    from paper_1509_06004_b200 import LambdaSchedule, _native, solve_seed_supergraph, synth
-    from paper_1509_06004_b200.supergraph import check_seed_supergraph
-
-    rank, local, world = dist_env()
-    ndev = torch.cuda.device_count()
-    dev = local % ndev          # one GPU per rank (shared only when testing N > #GPUs)
-    torch.cuda.set_device(dev)
-    if world > 1:
-        if ndev >= world:
-            dist.init_process_group("nccl", device_id=torch.device("cuda", dev))
-        else:   # NCCL cannot put two ranks on one GPU: plumbing-only test mode
-            dist.init_process_group("gloo")
-    sched = LambdaSchedule(lambdas_for(cfg["lams"]))
-    # weak scaling with fixed per-GPU work: every rank solves the same
-    # synthetic image(s) (rng_seed = i), so the max over ranks measures the
-    # system, not the spread of data-dependent difficulty between images
-    nimg = cfg.get("images", 1)
-    problems = []
-    for i in range(nimg):
-        batch = synth.generate(cfg["w"], cfg["h"], cfg["rows"], cfg["cols"],
-                               rng_seed=i, types=cfg["types"])
-        problems += check_seed_supergraph(batch.problems, sched, "auto")
-    cuts_per_step = len(problems) * len(sched)
-
-    solver = _native.solver_for_thread(dev)
-    stream = torch.cuda.ExternalStream(solver.stream_handle(), device=dev)
-    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
-    solver.seed_stage(cfg["w"], cfg["h"], problems, sched.values, "auto")
-    for _ in range(args.warmup):
-        solver.seed_run()
-    _, ref_flows, _ = solver.seed_fetch(labels=False)
-
-    # ---- device-resident timed region
-    barrier(dev)
-    torch.cuda.synchronize()
-    steps_ms, stats = [], []
-    with ClockSampler(dev) as clk:
-        for _ in range(args.steps):
-            with torch.cuda.stream(stream):
-                flush.zero_()                      # L2 flush, outside the timed events
-                e0 = torch.cuda.Event(enable_timing=True)
-                e1 = torch.cuda.Event(enable_timing=True)
-                e0.record(stream)
-            solver.seed_run()
-            with torch.cuda.stream(stream):
-                e1.record(stream)
-            e1.synchronize()
-            steps_ms.append(e0.elapsed_time(e1))
-            stats.append(solver.stats())
-    torch.cuda.synchronize()
-    barrier(dev)
-    _, flows, _ = solver.seed_fetch(labels=False)
-    assert (flows == ref_flows).all(), "flows changed between runs"
-    dev_s = sum(steps_ms) / 1e3
-    dev_s_max = reduce_max(dev_s, torch.device("cuda", dev))
-    value = world * cuts_per_step * args.steps / dev_s_max
-
-    # roofline of the dominant kernel: the asynchronous solve kernel (every
-    # phase of every grid, one launch per step) or, step-synchronous, the
-    # push-relabel discharge
+def roofline_of(stats, steps, config):
+    """Roofline of the dominant kernel: the asynchronous solve kernel (one
+    launch per step: every phase of every grid) or, step-synchronous, the
+    push-relabel discharge k_push.  achieved = algorithmic bytes per launch
+    (declared layout) / average launch time; the
+    SURVEY section 8(d) canonical 64 B push / 24 B BFS pixel-pass figure and
+    the layout-independent pixel-passes/s are reported beside it."""
     peak, peak_kind = measured_peaks()
     edge_bytes = stats[-1]["edge_bytes"]
     total_ms = sum(s["ms_device"] for s in stats)
     if stats[-1]["async_mode"]:
         col = 0 if edge_bytes == 4 else 1
         kern_ms = sum(s["ms_async"] for s in stats)
-        alg_bytes = sum(s[k] * 1024 * v[col] for s in stats for k, v in ASYNC_BYTES.items())
-        achieved = alg_bytes / args.steps / (kern_ms / 1e3 / args.steps) / 1e9 if kern_ms else 0.0
-        roofline = {"bound": "hbm", "kernel": "k_async (asynchronous solve: relabel, discharge, labels, "
-                                              "emit of every grid in one persistent launch)",
-                    "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
-                    "traffic": committed_traffic("k_async", args.config), "peak_kind": peak_kind,
-                    "bytes_per_pixel_pass": {k.replace("_tile_passes", ""): v[col] for k, v in ASYNC_BYTES.items()},
-                    "tile_passes_per_step": {k.replace("_tile_passes", ""): stats[-1][k] for k in ASYNC_BYTES},
-                    "avg_launch_us": kern_ms * 1e3 / args.steps,
-                    "time_share": {"k_async": round(kern_ms / total_ms, 4) if total_ms else None}}
-    else:
-        push_ms = sum(s["ms_push"] for s in stats)
-        push_launches = sum(s["push_sweeps"] for s in stats)
-        tile_passes = sum(s["push_tile_passes"] for s in stats)
-        bpp = BYTES_PER_PIXEL_PASS[edge_bytes]
-        alg_bytes_per_launch = tile_passes * 1024 * bpp / max(push_launches, 1)
-        avg_launch_s = push_ms / 1e3 / max(push_launches, 1)
-        achieved = alg_bytes_per_launch / avg_launch_s / 1e9 if avg_launch_s else 0.0
-        share = {k: round(sum(s[k] for s in stats) / total_ms, 4) for k in
-                 ("ms_push", "ms_bfs", "ms_labels")} if total_ms else {}
-        roofline = {"bound": "hbm", "kernel": "k_push (push-relabel tile discharge)",
-                    "achieved": achieved, "peak": peak, "unit": "GB/s",
-                    "frac": achieved / peak, "traffic": committed_traffic("k_push", args.config), "peak_kind": peak_kind,
-                    "bytes_per_pixel_pass": bpp,
-                    "pixel_passes_per_s": tile_passes * 1024 / (push_ms / 1e3) if push_ms else 0,
-                    "avg_launch_us": avg_launch_s * 1e6,
-                    "time_share": share}
+        alg = sum(s[k] * 1024 * v[col] for s in stats for k, v in ASYNC_BYTES.items())
+        canon = sum(s["push_tile_passes"] * 1024 * 64 + (s["bfs_tile_passes"] + s["label_tile_passes"]) * 1024 * 24
+                    for s in stats)
+        pp = sum((s["push_tile_passes"] + s["bfs_tile_passes"] + s["label_tile_passes"]) * 1024 for s in stats)
+        sec = kern_ms / 1e3 if kern_ms else float("inf")
+        achieved = alg / sec / 1e9
+        return {"bound": "hbm", "kernel": "k_async (asynchronous solve: relabel, discharge, labels, "
+                                          "emit of every grid in one persistent launch)",
+                "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
+                "traffic": committed_traffic("k_async", config), "peak_kind": peak_kind,
+                "frac_canonical_64_24": canon / sec / 1e9 / peak,
+                "pixel_passes_per_s": pp / sec,
+                "bytes_per_pixel_pass": {k.replace("_tile_passes", ""): v[col] for k, v in ASYNC_BYTES.items()},
+                "tile_passes_per_step": {k.replace("_tile_passes", ""): stats[-1][k] for k in ASYNC_BYTES},
+                "avg_launch_us": kern_ms * 1e3 / steps,
+                "time_share": {"k_async": round(kern_ms / total_ms, 4) if total_ms else None}}
+    push_ms = sum(s["ms_push"] for s in stats)
+    launches = max(1, sum(s["push_sweeps"] for s in stats))
+    passes = sum(s["push_tile_passes"] for s in stats)
+    bpp = BYTES_PER_PIXEL_PASS[edge_bytes]
+    sec = push_ms / 1e3 if push_ms else float("inf")
+    achieved = passes * 1024 * bpp / launches / (sec / launches) / 1e9
+    share = {k: round(sum(s[k] for s in stats) / total_ms, 4) for k in ("ms_push", "ms_bfs", "ms_labels")} \
+        if total_ms else {}
+    return {"bound": "hbm", "kernel": "k_push (push-relabel tile discharge)",
+            "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
+            "traffic": committed_traffic("k_push", config), "peak_kind": peak_kind,
+            "frac_canonical_64_24": passes * 1024 * 64 / sec / 1e9 / peak,
+            "bytes_per_pixel_pass": bpp, "pixel_passes_per_s": passes * 1024 / sec,
+            "avg_launch_us": sec / launches * 1e6, "launches_per_step": launches / steps,
+            "time_share": share}
 
-    # ---- end to end through the public API (host SeedProblems in, CutResults out)
-    e2e_s, h2d, d2h = 0.0, 0, 0
-    barrier(dev)
-    for i in range(args.warmup + args.steps):
+
+def measure(cfg, steps, warmup, dev, claims, sampler=None):
+    """Run warmup + steps batches claimed from the shared FIFO; per step the
+    e2e call on fresh problems (wall clock) and the device-resident run
+    (CUDA events).  Returns the per-rank sums and the last batch's data."""
+    import torch
+
+    from paper_1509_06004_b200 import LambdaSchedule, _native, solve_seed_supergraph
+
+    sched = LambdaSchedule(lambdas_for(cfg["lams"]))
+    nbatch = POOL_IMAGES // cfg["images"]
+    solver = _native.solver_for_thread(dev)
+    stream = torch.cuda.ExternalStream(solver.stream_handle(), device=dev)
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+    out = dict(dev_ms=0.0, e2e_s=0.0, h2d=0, d2h=0, cuts=0, stats=[], batches=[])
+
+    def one(timed):
+        b = claims.next() % nbatch
+        probs = batch_problems(cfg, b, sched)
+        # end to end through the public API, fresh objects (admission included)
         t0 = time.perf_counter()
-        res = solve_seed_supergraph(problems, sched, "auto", device=dev)
+        res = solve_seed_supergraph(probs, sched, "auto", device=dev)
         dt = time.perf_counter() - t0
-        if i >= args.warmup:
-            e2e_s += dt
-            st = solver.stats()
-            h2d += st["h2d_bytes"]
-            d2h += st["d2h_bytes"]
-    assert [c.flow for c in res.cuts] == [int(f) for f in ref_flows.reshape(-1)]
-    e2e_s_max = reduce_max(e2e_s, torch.device("cuda", dev))
-    e2e_value = world * cuts_per_step * args.steps / e2e_s_max
+        st_e2e = solver.stats()
+        # device-resident: stage (untimed), L2 flush, timed run
+        solver.seed_stage(cfg["w"], cfg["h"], probs, sched.values, "auto")
+        with torch.cuda.stream(stream):
+            flush.zero_()
+            e0 = torch.cuda.Event(enable_timing=True)
+            e1 = torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+        solver.seed_run()
+        with torch.cuda.stream(stream):
+            e1.record(stream)
+        e1.synchronize()
+        st = solver.stats()
+        _, flows, _ = solver.seed_fetch(labels=False)
+        assert [c.flow for c in res.cuts] == [int(f) for f in flows.reshape(-1)], "e2e and device runs disagree"
+        if timed:
+            out["dev_ms"] += e0.elapsed_time(e1)
+            out["e2e_s"] += dt
+            out["h2d"] += st_e2e["h2d_bytes"]
+            out["d2h"] += st_e2e["d2h_bytes"]
+            out["cuts"] += len(res.cuts)
+            out["stats"].append(st)
+            out["batches"].append(b)
+            out["last"] = (probs, flows)
 
-    # ---- CPMC image (C3) device time, reported beside the headline
-    cpmc = None
-    if args.cpmc and rank == 0 and args.config not in ("c3", "c5"):
-        c3 = synth.generate(500, 375, 5, 5, rng_seed=0, types=("A", "B"))
-        s3sched = LambdaSchedule(synth.L20)      # C3's ladder, whatever the headline config
-        c3p = check_seed_supergraph(c3.problems, s3sched, "auto")
-        s3 = _native.Solver(dev)
-        s3.seed_stage(500, 375, c3p, s3sched.values, "auto")
-        s3.seed_run()
-        s3.seed_run()
-        st3 = s3.stats()
-        cpmc = {"ms_per_image": round(st3["ms_device"], 3), "lambda_cuts": len(c3p) * len(s3sched),
-                "lambda_cuts_per_s": round(len(c3p) * len(s3sched) / st3["ms_device"] * 1e3, 1),
-                "image": "500x375, 25 seeds x 2 types x 20 lambdas, one device batch"}
-        s3.close()
+    for _ in range(warmup):
+        one(False)
+    barrier()
+    torch.cuda.synchronize()
+    if sampler is not None:
+        with sampler:
+            for _ in range(steps):
+                one(True)
+    else:
+        for _ in range(steps):
+            one(True)
+    torch.cuda.synchronize()
+    barrier()
+    return out
 
-    # ---- CPU baseline (rank 0, N == 1 only)
+
+def run_b200(args, cfg):
+    import torch
+    import torch.distributed as dist
+
+    rank, local, world = dist_env()
+    ndev = torch.cuda.device_count()
+    dev = local % ndev          # one GPU per rank (shared only when testing N > #GPUs)
+    torch.cuda.set_device(dev)
+    if world > 1:
+        dist.init_process_group("gloo")   # plumbing only: claims, barriers, max-reduce
+    clk = ClockSampler(dev)
+    m = measure(cfg, args.steps, args.warmup, dev, Claims(world > 1), clk)
+    dev_s_max = reduce_max(m["dev_ms"] / 1e3)
+    e2e_s_max = reduce_max(m["e2e_s"])
+    cuts_all = int(reduce_sum(m["cuts"]))
+    value = cuts_all / dev_s_max
+    e2e_value = cuts_all / e2e_s_max
+    stats = m["stats"]
+    nimg = cfg["images"]
+
+    # ---- CPU baseline (rank 0, N == 1 only): the oracle on a bounded
+    # sample of the last timed batch, checked against the device flows
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         import oracle
         oracle.build()
         threads = os.cpu_count() or 1
-        mp = REF_SAMPLE_PROBLEMS.get(args.config)
-        n, dt, flow = cpu_solve_config(cfg, 0, threads, mp)
-        if mp is None:
-            assert flow == int(ref_flows.sum()), "oracle and engine disagree on the flow"
-        else:
-            assert flow == int(ref_flows.reshape(-1)[:n].sum()), "oracle and engine disagree"
-        cpu = {"value": n / dt, "unit": UNIT, "cores": threads, "kind": "port",
-               "sample": f"{n} lambda-graphs of the rank-0 batch ({cfg['desc'].split(':')[0]}"
-                         f"{', first %d problems' % mp if mp else ''}), "
-                         "reference push-relabel restated in C (oracle/pmflow_oracle.c), "
-                         f"per lambda, {threads} threads; took {dt:.2f} s"}
+        probs, flows = m["last"]
+        mp = REF_SAMPLE_PROBLEMS.get(args.config) or len(probs)
+        n, dt, fl = cpu_solve(cfg, probs[:mp], threads)
+        assert fl == [int(f) for f in flows[:mp].reshape(-1)], "oracle and engine disagree"
+        cpu = {"value": n / dt, "unit": UNIT, "cores": threads, "kind": "port", "cpu_model": cpu_model(),
+               "sample": f"{n} lambda-graphs ({mp} seed problem(s) of the last timed batch, "
+                         f"{cfg['desc'].split(':')[0]}), reference push-relabel restated in C "
+                         f"(oracle/pmflow_oracle.c), per lambda, {threads} threads; took {dt:.2f} s"}
+
+    # ---- secondary workloads (N == 1): C3 (ms per CPMC image) and C2
+    secondary = None
+    if rank == 0 and world == 1 and args.secondary and args.config == "c5":
+        secondary = {}
+        for name, st_, wu in (("c3", 5, 3), ("c2", 10, 3)):
+            c = CONFIGS[name]
+            s2 = measure(c, st_, wu, dev, Claims(False))
+            k = s2["cuts"]
+            secondary[name] = {
+                "workload": c["desc"], "steps": st_, "value": k / (s2["dev_ms"] / 1e3), "unit": UNIT,
+                "ms_per_image": s2["dev_ms"] / st_ / c["images"],
+                "e2e": {"value": k / s2["e2e_s"], "ms_per_image": 1e3 * s2["e2e_s"] / st_ / c["images"],
+                        "h2d_bytes_per_step": s2["h2d"] // st_, "d2h_bytes_per_step": s2["d2h"] // st_},
+                "roofline": roofline_of(s2["stats"], st_, name)}
 
     if rank == 0:
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup,
-            "ms_per_step": 1e3 * dev_s_max / args.steps, "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "int32", "data": "synthetic",
-            "config": {"workload": cfg["desc"], "lambda_cuts_per_step_per_gpu": cuts_per_step,
-                       "image": f"{cfg['w']}x{cfg['h']}", "rng_seed": "0.. per image, the same on every rank",
-                       "l2": "flushed between steps (256 MiB memset, outside the timed events)",
-                       "parallelism": f"{world} GPU(s), independent supergraphs, no collectives"},
-            "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": h2d // args.steps,
-                    "d2h_bytes_per_step": d2h // args.steps},
-            "roofline": roofline,
+            "ms_per_step": 1e3 * dev_s_max / args.steps,
+            "ms_per_image": 1e3 * dev_s_max / args.steps / nimg,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "int32",
+            "data": "synthetic",
+            "config": {"workload": cfg["desc"], "images_per_step_per_gpu": nimg,
+                       "lambda_cuts_per_step_per_gpu": cuts_all // world // args.steps,
+                       "image": f"{cfg['w']}x{cfg['h']}",
+                       "pool": f"{POOL_IMAGES} distinct images (rng_seed 0..{POOL_IMAGES - 1}), "
+                               f"batches of {nimg} claimed FIFO across ranks",
+                       "l2": "flushed between steps (256 MiB memset, outside the timed events); "
+                             "each step also stages a new batch",
+                       "parallelism": f"{world} GPU(s), one process each, dynamic batch claims "
+                                      "(store counter), no data-path collective, gloo plumbing"},
+            "e2e": {"value": e2e_value, "unit": UNIT, "ms_per_image": 1e3 * e2e_s_max / args.steps / nimg,
+                    "h2d_bytes_per_step": m["h2d"] // args.steps, "d2h_bytes_per_step": m["d2h"] // args.steps},
+            "roofline": roofline_of(stats, args.steps, args.config),
             "cpu_baseline": cpu,
             "clocks": clk.summary(),
             "gpu_launches": int(sum(s["kernels"] for s in stats)),
@@ -431,14 +506,22 @@ def run_b200(args, cfg):
                                                   "push_tile_passes", "bfs_sweeps", "bfs_tile_passes",
                                                   "label_tile_passes", "scan_tile_passes", "tiles",
                                                   "edge_bytes", "grids")},
-            "cpmc": cpmc,
+            "batches_rank0": m["batches"],
+            "secondary": secondary,
         }
-        if args.config in ("c3", "c5"):
-            line["ms_per_image"] = 1e3 * dev_s_max / args.steps / nimg
-            line["e2e"]["ms_per_image"] = 1e3 * e2e_s_max / args.steps / nimg
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()
+
+
+def reduce_sum(value: float) -> float:
+    import torch
+    import torch.distributed as dist
+    if not (dist.is_available() and dist.is_initialized()):
+        return value
+    t = torch.tensor([value], dtype=torch.float64)
+    dist.all_reduce(t, op=dist.ReduceOp.SUM)
+    return float(t.item())
 
 
 def main():
@@ -446,10 +529,10 @@ def main():
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
-    ap.add_argument("--config", default="c2", choices=sorted(CONFIGS))
+    ap.add_argument("--config", default="c5", choices=sorted(CONFIGS))
     ap.add_argument("--impl", default="b200", choices=("b200", "reference"))
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--no-cpmc", dest="cpmc", action="store_false")
+    ap.add_argument("--no-secondary", dest="secondary", action="store_false")
     args = ap.parse_args()
     if args.warmup < 3 and args.impl == "b200":
         print("warning: fewer than 3 warm-up steps", file=sys.stderr)

@@ -15,6 +15,8 @@ builder only ever sees admissible problems.
 
 from __future__ import annotations
 
+import threading
+import weakref
 from dataclasses import dataclass, field
 
 import numpy as np
@@ -122,37 +124,76 @@ class SeedProblem:
         return self.width * self.height
 
     def _family_stats(self):
-        """Lambda-independent reductions used by check_family (cached)."""
+        """Lambda-independent reductions used by check_family (cached).
+
+        Whole-plane reductions come from a cache keyed by the plane's memory
+        (``_plane_stats``): the problems of one image share its pairwise
+        plane and the seed types of one seed share their unary / sink planes,
+        so a CPMC image's 50 problems reduce 26 distinct planes, not 200.
+        The seed pixels are then taken out exactly (sums) or bounded (the
+        extrema only gate exact fallbacks, _check_lambda)."""
         if self._stats is None:
-            n = self.n
-            nonfg = np.ones(n, bool)
-            nonfg[self._fg_idx] = False
-            nonbg = np.ones(n, bool)
-            nonbg[self._bg_idx] = False
-            b, s = self.unary_base, self.unary_slope
-            sink = self.sink_base[nonbg]
-            pw = self.pairwise
-            arcs = pw.reshape(4, self.height, self.width)
+            fg, bg = self._fg_idx, self._bg_idx
+            b, s, sink, pw = self.unary_base, self.unary_slope, self.sink_base, self.pairwise
+            sb, ss, sk = _plane_stats(b), _plane_stats(s), _plane_stats(sink)
+            sp = _plane_stats(pw, self.height, self.width)
+            kb = sink[bg]
             st = dict(
-                max_slope=int(s.max(initial=0)),
-                max_base=int(b.max(initial=0)),
-                min_base_nonfg=int(b[nonfg].min(initial=0)),
-                sum_base_nonfg=int(b[nonfg].sum()),
-                sum_slope_nonfg=int(s[nonfg].sum()),
-                max_slope_nonfg=int(s[nonfg].max(initial=0)),
-                max_base_nonfg=int(b[nonfg].max(initial=0)),
-                n_fg=int(self._fg_idx.size), n_bg=int(self._bg_idx.size),
-                min_sink=int(sink.min(initial=0)), max_sink=int(sink.max(initial=0)),
-                sum_sink=int(sink.sum()), sum_sink_fin=int(sink[sink < CAP_MAX].sum()),
-                min_pw=int(pw.min(initial=0)), max_pw=int(pw.max(initial=0)),
-                sum_pw=int(pw.sum()), sum_pw_fin=int(pw[pw < CAP_MAX].sum()),
-                border=[(d, int(row.max(initial=0))) for d, row in (
-                    (0, arcs[0][:, 0]), (1, arcs[1][:, -1]), (2, arcs[2][0, :]),
-                    (3, arcs[3][-1, :]))],
-                nonfg=nonfg,
+                max_slope=ss["max"], max_base=sb["max"],
+                # bounds over all pixels (>= the non-seed extrema): a bound that
+                # passes implies the exact value passes; otherwise exact below
+                min_base_nonfg=sb["min"] if sb["min"] >= 0 else
+                int(b[self._nonfg()].min(initial=0)),
+                sum_base_nonfg=sb["sum"] - int(b[fg].sum()),
+                sum_slope_nonfg=ss["sum"] - int(s[fg].sum()),
+                max_slope_nonfg=ss["max"], max_base_nonfg=sb["max"],
+                n_fg=int(fg.size), n_bg=int(bg.size),
+                min_sink=sk["min"] if sk["min"] >= 0 else int(sink[self._nonbg()].min(initial=0)),
+                max_sink=sk["max"] if sk["max"] <= CAP_MAX else int(sink[self._nonbg()].max(initial=0)),
+                sum_sink=sk["sum"] - int(kb.sum()),
+                sum_sink_fin=sk["sum_fin"] - int(kb[kb < CAP_MAX].sum()),
+                min_pw=sp["min"], max_pw=sp["max"], sum_pw=sp["sum"], sum_pw_fin=sp["sum_fin"],
+                border=sp["border"],
             )
             object.__setattr__(self, "_stats", st)
         return self._stats
+
+    def _nonfg(self):
+        m = np.ones(self.n, bool)
+        m[self._fg_idx] = False
+        return m
+
+    def _nonbg(self):
+        m = np.ones(self.n, bool)
+        m[self._bg_idx] = False
+        return m
+
+
+_PLANE_STATS = {}
+_PLANE_LOCK = threading.Lock()
+
+
+def _plane_stats(a: np.ndarray, height: int = 0, width: int = 0) -> dict:
+    """min / max / sum / sum below CAP_MAX of a plane (and, for a (4, n)
+    pairwise plane with height/width, the largest arc on each image border),
+    cached by the plane's memory while an array viewing it is alive."""
+    key = (a.__array_interface__["data"][0], a.shape, a.dtype.str, height, width)
+    with _PLANE_LOCK:
+        ent = _PLANE_STATS.get(key)
+        if ent is not None and ent[0]() is not None:
+            return ent[1]
+    st = dict(min=int(a.min(initial=0)), max=int(a.max(initial=0)), sum=int(a.sum()))
+    st["sum_fin"] = st["sum"] if st["max"] < CAP_MAX else int(a[a < CAP_MAX].sum())
+    if height:
+        arcs = a.reshape(4, height, width)
+        st["border"] = [(d, int(row.max(initial=0))) for d, row in (
+            (0, arcs[0][:, 0]), (1, arcs[1][:, -1]), (2, arcs[2][0, :]), (3, arcs[3][-1, :]))]
+    with _PLANE_LOCK:
+        if len(_PLANE_STATS) > 4096:
+            for k in [k for k, (r, _) in _PLANE_STATS.items() if r() is None]:
+                del _PLANE_STATS[k]
+        _PLANE_STATS[key] = (weakref.ref(a), st)
+    return st
 
 
 def _check_lambda(p: SeedProblem, lam: int) -> None:
@@ -175,7 +216,8 @@ def _check_lambda(p: SeedProblem, lam: int) -> None:
                 f"(lambda={lam})")
     # admit on the instantiated graph: src (fg pixels are CAP_MAX)
     if st["min_base_nonfg"] < 0:
-        src_nf = p.unary_base[st["nonfg"]] + lam * p.unary_slope[st["nonfg"]]
+        nonfg = p._nonfg()
+        src_nf = p.unary_base[nonfg] + lam * p.unary_slope[nonfg]
         if src_nf.size and int(src_nf.min()) < 0:
             raise NegativeCapacityError("src_cap has a negative capacity")
     if st["min_sink"] < 0:
@@ -198,7 +240,8 @@ def _check_lambda(p: SeedProblem, lam: int) -> None:
     if st["max_base_nonfg"] + lam * st["max_slope_nonfg"] < CAP_MAX:
         src_fin = st["sum_base_nonfg"] + lam * st["sum_slope_nonfg"]
     else:
-        s_nf = p.unary_base[st["nonfg"]] + lam * p.unary_slope[st["nonfg"]]
+        nonfg = p._nonfg()
+        s_nf = p.unary_base[nonfg] + lam * p.unary_slope[nonfg]
         src_fin = int(s_nf[s_nf < CAP_MAX].sum())
     finite = src_fin + st["sum_sink_fin"] + st["sum_pw_fin"]
     if finite >= CAP_MAX:

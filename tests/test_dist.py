@@ -1,10 +1,10 @@
-"""The N > 1 path of bench.py on CPU: world_size-2 gloo process group,
-weak-scaling shard assignment and the max-over-ranks timing reduction."""
+"""The N > 1 path of bench.py on CPU: world_size-2 gloo process group, the
+shared FIFO of batch claims (dynamic placement of the 256-image pool over
+the ranks), and the max/sum-over-ranks reductions of the timing."""
 
 import os
 import socket
 
-import pytest
 import torch.multiprocessing as mp
 
 from conftest import ROOT
@@ -17,22 +17,31 @@ def _free_port():
 
 
 def _worker(rank, world, port, out):
+    import random
     import sys
+    import time
     sys.path.insert(0, ROOT)
     import torch.distributed as dist
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), RANK=str(rank),
                       WORLD_SIZE=str(world), LOCAL_RANK=str(rank))
     dist.init_process_group("gloo", rank=rank, world_size=world)
     import bench
-    mine = bench.shard(25, rank, world)
-    t = 1.0 + rank * 0.5           # pretend per-rank device seconds
-    tmax = bench.reduce_max(t)
+    claims = bench.Claims(True)
     bench.barrier()
-    out.put((rank, mine, tmax, bench.dist_env()))
+    mine = []
+    rng = random.Random(rank)
+    for _ in range(10):                 # rank 1 is slower: it should claim later ids
+        mine.append(claims.next())
+        time.sleep(rng.random() * 0.002 * (1 + 3 * rank))
+    t = 1.0 + rank * 0.5                # pretend per-rank device seconds
+    tmax = bench.reduce_max(t)
+    tsum = bench.reduce_sum(len(mine))
+    bench.barrier()
+    out.put((rank, mine, tmax, tsum, bench.dist_env()))
     dist.destroy_process_group()
 
 
-def test_gloo_world2_shards_and_max_reduce():
+def test_gloo_world2_dynamic_claims_and_reductions():
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
@@ -43,18 +52,19 @@ def test_gloo_world2_shards_and_max_reduce():
     for p in procs:
         p.join(timeout=60)
         assert p.exitcode == 0
-    (r0, s0, m0, e0), (r1, s1, m1, e1) = res
-    assert s0 + s1 == list(range(25)) and not set(s0) & set(s1)
-    assert m0 == m1 == 1.5
+    (r0, c0, m0, s0, e0), (r1, c1, m1, s1, e1) = res
+    # every claim distinct, together exactly the FIFO prefix 0..19
+    assert sorted(c0 + c1) == list(range(20))
+    assert c0 == sorted(c0) and c1 == sorted(c1)          # each rank's claims in FIFO order
+    assert m0 == m1 == 1.5 and s0 == s1 == 20
     assert e0 == (0, 0, 2) and e1 == (1, 1, 2)
 
 
-@pytest.mark.parametrize("n,world", [(25, 1), (25, 2), (25, 8), (3, 8), (1000, 7)])
-def test_shard_partitions(n, world):
+def test_local_claims_and_batches():
     import sys
     sys.path.insert(0, ROOT)
     import bench
-    parts = [bench.shard(n, r, world) for r in range(world)]
-    flat = [i for p in parts for i in p]
-    assert flat == list(range(n))
-    assert max(map(len, parts)) - min(map(len, parts)) <= 1
+    c = bench.Claims(False)
+    assert [c.next() for _ in range(5)] == [0, 1, 2, 3, 4]
+    cfg = bench.CONFIGS["c5"]
+    assert bench.POOL_IMAGES // cfg["images"] == 32      # 256 images in batches of 8
