@@ -124,6 +124,13 @@ int pmf_solver_set(pmf_solver *s, const char *name, int64_t value);
  * own events or order their own work against the engine. */
 int pmf_solver_stream(const pmf_solver *s, void **stream_out);
 
+/* Host-only helper (no device needed): per int64 plane k of sizes[k]
+ * entries, out[4k .. 4k+3] = min, max, sum, sum of entries below CAP_MAX
+ * (min / max include 0, numpy's initial=0).  The reductions of the seed
+ * family admission checks (parametric.py:141-165), over many planes on all
+ * host cores. */
+int pmf_plane_stats(int32_t nplanes, const int64_t *const *planes, const int64_t *sizes, int64_t *out);
+
 /* Thread-local message describing the last error on this thread. */
 const char *pmf_last_error(void);
 

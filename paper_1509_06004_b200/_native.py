@@ -26,7 +26,7 @@ EXPORTS = ("pmf_solver_create", "pmf_solver_destroy", "pmf_solver_set", "pmf_las
            "pmf_solver_stats", "pmf_solver_stream", "pmf_solve_composites", "pmf_solve_seed_batch",
            "pmf_seed_stage", "pmf_seed_run", "pmf_seed_fetch", "pmf_debug_state",
            "pmf_debug_trace", "pmf_debug_busy", "pmf_seed_score", "pmf_debug_phases",
-           "pmf_solve_composites_i32", "pmf_composite_bits")
+           "pmf_solve_composites_i32", "pmf_composite_bits", "pmf_plane_stats")
 
 
 class NativeUnavailable(RuntimeError):
@@ -91,6 +91,7 @@ def load_library(path: str = LIB_PATH):
         lib.pmf_debug_busy.argtypes = [vp, P(ctypes.c_double)]
         lib.pmf_debug_phases.argtypes = [vp, i64, P(ctypes.c_uint64), P(i32)]
         lib.pmf_seed_score.argtypes = [vp, P(vp), P(i64), P(i64), P(i64)]
+        lib.pmf_plane_stats.argtypes = [i32, P(vp), P(i64), P(i64)]
         for name in EXPORTS:
             if name != "pmf_last_error":
                 getattr(lib, name).restype = ctypes.c_int
@@ -392,3 +393,18 @@ def solver_for_thread(device: int = 0) -> Solver:
     if s is None:
         s = pool[device] = Solver(device, **_knobs)
     return s
+
+
+def plane_stats(planes):
+    """[(min, max, sum, sum below CAP_MAX)] of int64 planes, reduced on all
+    host cores by the native library (pmf_plane_stats)."""
+    lib = load_library()
+    arrs = [np.ascontiguousarray(a, np.int64).reshape(-1) for a in planes]
+    sizes = np.array([a.size for a in arrs], np.int64)
+    out = np.zeros((len(arrs), 4), np.int64)
+    P = ctypes.POINTER
+    rc = lib.pmf_plane_stats(len(arrs), _ptrs(arrs), sizes.ctypes.data_as(P(ctypes.c_int64)),
+                             out.ctypes.data_as(P(ctypes.c_int64)))
+    if rc:
+        _raise_for(rc)
+    return [tuple(int(v) for v in row) for row in out]

@@ -14,7 +14,7 @@ CSRC = os.path.join(HERE, "csrc")
 OUT = os.path.join(HERE, "libpmflow_b200.so")
 SOURCES = ["engine.cu"]
 NVCC_FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
-              "-Xcompiler", "-fPIC,-O2,-fopenmp", "-shared", "--expt-relaxed-constexpr", "-lgomp"]
+              "-Xcompiler", "-fPIC,-O3,-fopenmp", "-shared", "--expt-relaxed-constexpr", "-lgomp"]
 
 
 def nvcc():

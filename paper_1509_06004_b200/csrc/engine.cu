@@ -1891,6 +1891,32 @@ int pmf_solver_set(pmf_solver *s, const char *name, int64_t v) {
     return 0;
 }
 
+// Host-side admission statistics of many int64 planes at once (OpenMP over
+// planes): min, max, sum and the sum of the entries below CAP_MAX per plane
+// (parametric.py _plane_stats; the reductions instantiate's checks need,
+// parametric.py:141-165 / grid.py:102-130).
+int pmf_plane_stats(int32_t nplanes, const int64_t *const *planes, const int64_t *sizes, int64_t *out) {
+    if (nplanes < 0 || (nplanes && (!planes || !sizes || !out))) return fail(PMF_ERR_ARG, "bad arguments");
+    int nt = int(std::max(1u, std::min(std::thread::hardware_concurrency(), 16u)));
+#pragma omp parallel for schedule(dynamic, 1) num_threads(nt)
+    for (int32_t k = 0; k < nplanes; k++) {
+        const int64_t *a = planes[k];
+        int64_t mn = 0, mx = 0, sum = 0, fin = 0;   // initial=0 semantics of numpy min/max
+        for (int64_t i = 0; i < sizes[k]; i++) {
+            const int64_t v = a[i];
+            mn = std::min(mn, v);
+            mx = std::max(mx, v);
+            sum += v;
+            fin += v < CAP_MAX ? v : 0;
+        }
+        out[4 * k + 0] = mn;
+        out[4 * k + 1] = mx;
+        out[4 * k + 2] = sum;
+        out[4 * k + 3] = fin;
+    }
+    return 0;
+}
+
 int pmf_solver_stream(const pmf_solver *s, void **stream_out) {
     if (!s || !stream_out) return fail(PMF_ERR_ARG, "null argument");
     *stream_out = (void *)s->st;

@@ -25,7 +25,7 @@ from dataclasses import dataclass
 import numpy as np
 
 from .grid import CutResult, GridGraph, admit, cut_cost
-from .parametric import LambdaSchedule, SeedProblem, check_family, instantiate
+from .parametric import prefetch_family_stats, LambdaSchedule, SeedProblem, check_family, instantiate
 
 
 class SupergraphError(ValueError):
@@ -277,6 +277,7 @@ def check_seed_supergraph(problems, schedule: LambdaSchedule, swap_mode: str = "
     """Raise whatever build_seed_supergraph would raise, in the same order."""
     problems = _check_seed_args(problems, swap_mode)
     shapes = {(p.width, p.height) for p in problems}
+    prefetch_family_stats(problems)
     for p in problems:
         if swap_mode == "auto":
             check_family(p, (schedule[schedule.mid_index],))
