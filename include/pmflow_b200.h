@@ -92,31 +92,28 @@ typedef struct pmf_stats {
 int pmf_solver_create(int32_t device, pmf_solver **out);
 int pmf_solver_destroy(pmf_solver *s);
 
-/* Tuning knobs: "push_iters" (inner smem iterations per tile pass),
- * "relabel_every" (exact local relabel period inside a tile pass),
- * "push_budget" (persistent discharge: tile pops per seeded tile),
- * "push_sweeps" (sweep-mode discharge launches per cycle), "bfs_chunk"
- * (host-driven mode: launches between convergence checks), "persistent" /
- * "persistent_bfs" (phase scheduling), "graph" (0: host-driven loop, 1:
- * whole solve as one CUDA graph), "chain" (warm-start chain length; 0:
- * auto: whole ladder per problem from "warm_min_problems" problems on),
- * "push_budget_warm" (discharge budget of warm-start batches),
- * "warp" (bit mask: warp-per-tile discharge 1 / sink BFS 2 / label BFS 4),
- * "timing" (0/1 event timings),
- * "max_cycles" (non-convergence guard),
- * "async" (seed batches: -1 auto / 0 step-synchronous / 1 asynchronous
- * single-kernel solver) with "async_max_tiles" / "async_max_grid_tiles"
- * (auto thresholds: batch tiles, average tiles per grid),
- * "async_cont" / "async_prefetch" (queue hand-off options),
- * "rolling" (step-synchronous warm start without a common step barrier),
- * "verify" (device cut-cost == flow certificate, default on; 2 = test hook
- *   that corrupts one emitted label first, so the check must fail),
- * "verify_vec" (4-pixel-group certificate kernel for W % 4 == 0, default on),
- * "comp_split" (composites: one grid per segment span that no arc leaves,
- *   default on; otherwise one grid per composite),
- * "fresh_skip" (skip the no-op local relabel of a first pass on exact
- * heights), "push_budget_add", "push_mode", "push_flush", "push_minb",
- * "grid_div", "relax_cap", "bfs_multi", "phase_log" (diagnostics).
+/* Tuning knobs (each covered by a -m gpu parity test, tests/test_gpu_parity.py
+ * test_every_knob_keeps_c1_bit_exact):
+ *   discharge:  "push_iters" (smem iterations per tile pass), "relabel_every"
+ *               (exact local relabel period), "push_budget" / "push_budget_warm"
+ *               / "push_budget_add" (pops per discharge phase), "push_sweeps"
+ *               (sweep-mode launches per cycle), "push_flush" (mid-pass
+ *               hand-off of border inflow), "fresh_skip";
+ *   scheduling: "async" (-1 auto / 0 step-synchronous / 1 single-kernel
+ *               asynchronous solver) with "async_max_tiles" /
+ *               "async_max_grid_tiles" (auto thresholds), "async_cont",
+ *               "async_prefetch", "async_spec", "adv_keep_h"; "graph" (0
+ *               host-driven loop, 1 whole solve as one CUDA graph),
+ *               "persistent", "persistent_bfs", "bfs_multi", "bfs_chunk",
+ *               "rolling", "chain" / "warm_min_problems" (warm-start chains);
+ *   kernels:    "warp" (label BFS: 4 warp-per-tile bitset kernel, 0 CTA kernel);
+ *   int64:      "force_wide" (the int64 state variant even when int32 bounds
+ *               hold), "wide_pulses" (pulses between its global relabels);
+ *   checks:     "verify" (device cut-cost == flow certificate, default on; 2 =
+ *               test hook corrupting one label first), "verify_vec",
+ *               "comp_split" (composites: one grid per isolated segment span),
+ *               "max_cycles" (non-convergence guard);
+ *   diagnostics: "timing", "phase_log".
  * Returns PMF_ERR_ARG if unknown or out of range. */
 int pmf_solver_set(pmf_solver *s, const char *name, int64_t value);
 

@@ -65,7 +65,7 @@ struct AsyncArgs {
     const int64_t *slope_sum;
     GridRun *gr;
     uint8_t *tflag;    // per tile: listed for the next flagged phase
-    int iters, relabel_every, relax_cap;
+    int iters, relabel_every;
     unsigned budget_factor;
     int32_t budget_add;    // discharge pop budget: factor x seeded tiles + this
     int32_t max_cycles;
@@ -520,8 +520,7 @@ __global__ void __launch_bounds__(NTT, 2) k_async(Ctx c, AsyncArgs A) {
             }
             __syncthreads();
             if (s_ok) {
-                r = c.push_mode == 1 ? push_tile1<E>(c, t, A.iters, A.relabel_every, A.relax_cap)
-                                     : push_tile<E>(c, t, A.iters, A.relabel_every, A.relax_cap);
+                r = push_tile<E>(c, t, A.iters, A.relabel_every);
                 stat = ST_PUSH;
             }
         } else if (ph == PH_LAB) {

@@ -207,32 +207,26 @@ struct pmf_solver {
     int push_iters = 16;
     int push_sweeps = 64;
     int relabel_every = 8;
-    // warp-per-tile kernels instead of 1024-thread CTAs, per kernel kind:
-    // bit 0 discharge, bit 1 sink BFS, bit 2 label BFS; -1: auto (label BFS
-    // always, sink BFS when the batch has >= warp_bfs_tiles tiles)
+    // label BFS: warp-per-tile bitset kernel (4, default) or the
+    // 1024-thread CTA kernel (0)
     int warp = 4;
-    int warp_bfs_tiles = 20000;
-    int warp_eff = 0;         // resolved bits for the current batch
+    int warp_eff = 0;         // resolved for the current batch
     int warm_active = 0;      // the current run uses warm-start chains
-    int grid_wpush = 0, grid_wbfs = 0;
+    int grid_wbfs = 0;
     size_t smem_w = 0;
     int persistent = 1;       // discharge phase as one persistent launch
     int persistent_bfs = 0;   // BFS phases as one persistent launch
     int bfs_multi = 1;        // BFS phases as one cooperative launch (grid barriers between sweeps)
     int push_budget = 2;      // persistent push phase: pops <= budget * seeded tiles
     int chain = 0;            // warm-start chain length (0: auto, see warm_min_problems)
-    int relax_cap = 0;        // sweep cap of the discharge's local relabel (0: to the fixpoint)
     int warm_min_problems = 8;  // auto: one chain per problem (whole ladder) from this many problems
     int push_budget_warm = 3;   // discharge budget factor when the batch runs warm-start chains
     int push_budget_add = 64;   // asynchronous solver: + this many pops per discharge phase
     int verify = 1;             // seed batches: device cut_cost == flow certificate per cut
     int verify_vec = 1;         // 4-pixel-group verify kernel when W % 4 == 0
     int rolling = 1;            // warm-start chains advance per grid as each finishes (no step barrier)
-    int push_minb = 2;          // CTA discharge: min CTAs per SM of its launch bounds (1 or 2)
-    int push_mode = 0;          // discharge body: 0 two CTA barriers per iteration, 1 one
     int fresh_skip = 1;         // first discharge pass after an exact relabel skips its local relabel
     int push_flush = 0;         // discharge: hand border inflow over every this many iterations (0 off; queue modes)
-    int grid_div = 1;           // use 1/grid_div of the GPU's resident CTAs (solvers sharing a GPU)
     int async_mode = -1;        // seed batches: one persistent kernel, every grid on its own phase machine
                                 // (1), step-synchronous phases (0), or -1: async up to async_max_tiles tiles
     int async_max_tiles = 20000;
@@ -322,7 +316,7 @@ int setup_state(pmf_solver *s, int edge_bytes) {
         (rc = s->d_ctl.ensure(sizeof(Ctl))) || (rc = s->d_curlam.ensure(G * 4)))
         return rc;
     s->edge_bytes = edge_bytes;
-    s->warp_eff = s->warp >= 0 ? s->warp : (4 | (T >= s->warp_bfs_tiles ? 2 : 0));
+    s->warp_eff = s->warp;
     // host sources live in the solver (s->lay, s->ones) until the next setup
     CK(cudaMemcpyAsync(s->d_tile_grid.p, L.tile_grid.data(), T * 4, cudaMemcpyHostToDevice, s->st));
     CK(cudaMemcpyAsync(s->d_tnb.p, L.tile_nb.data(), T * 16, cudaMemcpyHostToDevice, s->st));
@@ -352,7 +346,6 @@ int setup_state(pmf_solver *s, int edge_bytes) {
     x.grids = s->d_grids.as<GridDesc>();
     x.live = s->d_live.as<int32_t>();
     x.fin = s->d_fin.as<int32_t>();
-    x.push_mode = s->push_mode;
     x.push_flush = s->push_flush;
     x.tfresh = nullptr;
     if (s->fresh_skip) {
@@ -467,39 +460,26 @@ void launch_bfs(pmf_solver *s, const Ctx &c, bool sink, int k) {
     if (k == K_MULTI) {
         const LaunchCtl lc = lctl(sink ? ST_BFS : ST_LAB);
         cudaError_t e;
-        if (s->warp_eff & (sink ? 2 : 4))
-            e = launch_coop(sink ? k_wbfs_sink<E> : k_wbfs_src<E>, s->grid_wbfs, WPB * 32, s->smem_w, s->st, c, k,
-                            lc);
+        if (!sink && (s->warp_eff & 4))
+            e = launch_coop(k_wbfs_src<E>, s->grid_wbfs, WPB * 32, s->smem_w, s->st, c, k, lc);
         else
             e = launch_coop(sink ? k_bfs_sink<E> : k_bfs_src<E>, s->grid_bfs, NTT, 0, s->st, c, k, lc);
         (void)e;   // surfaced by the caller's cudaGetLastError
         s->stats.launches++;
         return;
     }
-    if (s->warp_eff & (sink ? 2 : 4)) {
-        if (sink) LAUNCH(s, (k_wbfs_sink<E><<<s->grid_wbfs, WPB * 32, s->smem_w, s->st>>>(c, k, lctl(ST_BFS))));
-        else LAUNCH(s, (k_wbfs_src<E><<<s->grid_wbfs, WPB * 32, s->smem_w, s->st>>>(c, k, lctl(ST_LAB))));
+    if (!sink && (s->warp_eff & 4)) {
+        LAUNCH(s, (k_wbfs_src<E><<<s->grid_wbfs, WPB * 32, s->smem_w, s->st>>>(c, k, lctl(ST_LAB))));
     } else {
         if (sink) LAUNCH(s, (k_bfs_sink<E><<<s->grid_bfs, NTT, 0, s->st>>>(c, k, lctl(ST_BFS))));
         else LAUNCH(s, (k_bfs_src<E><<<s->grid_bfs, NTT, 0, s->st>>>(c, k, lctl(ST_LAB))));
     }
 }
 
-// CTA discharge kernel: 2 CTAs per SM at 32 registers (default) or one CTA
-// per SM at 64 registers (knob push_minb = 1)
-template <class E>
-auto push_kernel(const pmf_solver *s) -> decltype(&k_push<E, 2>) {
-    return s->push_minb == 1 ? &k_push<E, 1> : &k_push<E, 2>;
-}
-
+// CTA discharge kernel: 2 CTAs per SM at 32 registers
 template <class E>
 void launch_push(pmf_solver *s, const Ctx &c, int k) {
-    if (s->warp_eff & 1)
-        LAUNCH(s, (k_wpush<E><<<s->grid_wpush, WPB * 32, s->smem_w, s->st>>>(c, k, s->push_iters, s->relabel_every,
-                                                                            lctl(ST_PUSH))));
-    else
-        LAUNCH(s, (push_kernel<E>(s)<<<s->grid_push, NTT, 0, s->st>>>(c, k, s->push_iters, s->relabel_every, s->relax_cap,
-                                                              lctl(ST_PUSH))));
+    LAUNCH(s, (k_push<E><<<s->grid_push, NTT, 0, s->st>>>(c, k, s->push_iters, s->relabel_every, lctl(ST_PUSH))));
 }
 
 // ---- host-driven loop (graph = 0): the host reads worklist lengths and the
@@ -645,11 +625,8 @@ int add_if(cudaGraph_t g, cudaGraphNode_t *prev, cudaGraphConditionalHandle h, c
 template <class E>
 int add_bfs_node_raw(pmf_solver *s, cudaGraph_t g, cudaGraphNode_t *prev, bool sink, const Ctx &c, int k,
                      LaunchCtl lc) {
-    if (s->warp_eff & (sink ? 2 : 4)) {
-        if (sink)
-            return add_kernel_smem(g, prev, dim3(s->grid_wbfs), dim3(WPB * 32), s->smem_w, k_wbfs_sink<E>, c, k, lc);
+    if (!sink && (s->warp_eff & 4))
         return add_kernel_smem(g, prev, dim3(s->grid_wbfs), dim3(WPB * 32), s->smem_w, k_wbfs_src<E>, c, k, lc);
-    }
     if (sink) return add_kernel(g, prev, dim3(s->grid_bfs), dim3(NTT), k_bfs_sink<E>, c, k, lc);
     return add_kernel(g, prev, dim3(s->grid_bfs), dim3(NTT), k_bfs_src<E>, c, k, lc);
 }
@@ -667,11 +644,7 @@ int add_bfs_node(pmf_solver *s, cudaGraph_t g, cudaGraphNode_t *prev, bool sink,
 
 template <class E>
 int add_push_node(pmf_solver *s, cudaGraph_t g, cudaGraphNode_t *prev, const Ctx &c, int k, LaunchCtl lc) {
-    if (s->warp_eff & 1)
-        return add_kernel_smem(g, prev, dim3(s->grid_wpush), dim3(WPB * 32), s->smem_w, k_wpush<E>, c, k,
-                               s->push_iters, s->relabel_every, lc);
-    return add_kernel(g, prev, dim3(s->grid_push), dim3(NTT), push_kernel<E>(s), c, k, s->push_iters, s->relabel_every,
-                      s->relax_cap, lc);
+    return add_kernel(g, prev, dim3(s->grid_push), dim3(NTT), k_push<E>, c, k, s->push_iters, s->relabel_every, lc);
 }
 
 template <class E>
@@ -822,7 +795,7 @@ int build_graph_rolling(pmf_solver *s, const Ctx &c0, int32_t ngrids, const Seed
 // knobs + context a cached graph was built for
 struct GraphKey {
     Ctx ctx;
-    int32_t ngrids, edge, p_push, p_bfs, iters, relabel, budget, sweeps, warp, relax_cap, multi, minb;
+    int32_t ngrids, edge, p_push, p_bfs, iters, relabel, budget, sweeps, warp, multi;
     int64_t maxc;
     int32_t gfull, gbfs, gpush;
     SeedArgs sa;
@@ -845,9 +818,7 @@ int graph_solve(pmf_solver *s, const Ctx &c0, int32_t ngrids, const SeedArgs *sa
     key.budget = budget_factor(s);
     key.sweeps = s->push_sweeps;
     key.warp = s->warp_eff;
-    key.relax_cap = s->relax_cap;
     key.multi = s->bfs_multi;
-    key.minb = s->push_minb;
     key.maxc = s->max_cycles;
     key.gfull = s->grid_full;
     key.gbfs = s->grid_bfs;
@@ -1062,7 +1033,7 @@ int64_t max_pair(const int32_t *nb, int W, int H, int y0 = 0, int y1 = -1) {
 template <class E>
 int grids_for(pmf_solver *s) {
     int occ = 0;
-    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, push_kernel<E>(s), NTT, 0));
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_push<E>, NTT, 0));
     s->grid_push = std::max(1, occ) * s->sms;
     // BFS grids are co-resident (cooperative K_MULTI launches): the smaller
     // occupancy of the sink and label kernels
@@ -1071,19 +1042,10 @@ int grids_for(pmf_solver *s) {
     CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ2, k_bfs_src<E>, NTT, 0));
     s->grid_bfs = std::max(1, std::min(occ, occ2)) * s->sms;
     s->smem_w = WPB * sizeof(WarpTile<E>);
-    CK(cudaFuncSetAttribute(k_wpush<E>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(s->smem_w)));
-    CK(cudaFuncSetAttribute(k_wbfs_sink<E>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(s->smem_w)));
     CK(cudaFuncSetAttribute(k_wbfs_src<E>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(s->smem_w)));
-    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_wpush<E>, WPB * 32, s->smem_w));
-    s->grid_wpush = std::max(1, occ) * s->sms;
-    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_wbfs_sink<E>, WPB * 32, s->smem_w));
     CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ2, k_wbfs_src<E>, WPB * 32, s->smem_w));
-    s->grid_wbfs = std::max(1, std::min(occ, occ2)) * s->sms;
+    s->grid_wbfs = std::max(1, occ2) * s->sms;
     s->grid_full = 8 * s->sms;
-    if (s->grid_div > 1) {   // a share of the GPU (several solvers running side by side)
-        for (int *gp : {&s->grid_push, &s->grid_bfs, &s->grid_full, &s->grid_wpush, &s->grid_wbfs})
-            *gp = std::max(1, *gp / s->grid_div);
-    }
     return 0;
 }
 
@@ -1144,7 +1106,6 @@ int async_solve(pmf_solver *s, const Ctx &c0, const SeedArgs &sa) {
     A.tflag = s->d_tflag.as<uint8_t>();
     A.iters = s->push_iters;
     A.relabel_every = s->relabel_every;
-    A.relax_cap = s->relax_cap;
     A.budget_factor = unsigned(budget_factor(s));
     A.budget_add = s->push_budget_add;
     A.max_cycles = int32_t(std::min<int64_t>(s->max_cycles, 0x7fffffff));
@@ -1855,10 +1816,8 @@ int pmf_solver_set(pmf_solver *s, const char *name, int64_t v) {
     else if (k == "bfs_chunk" && v >= 1 && v <= 100000) s->bfs_chunk = int(v);
     else if (k == "relabel_every" && v >= 0 && v <= 100000) s->relabel_every = int(v);
     else if (k == "persistent") s->persistent = v != 0;
-    else if (k == "warp" && v >= -1 && v <= 7) s->warp = int(v);
-    else if (k == "warp_bfs_tiles" && v >= 0) s->warp_bfs_tiles = int(v);
+    else if (k == "warp" && (v == 0 || v == 4)) s->warp = int(v);
     else if (k == "chain" && v >= 0 && v <= 1000000) s->chain = int(v);
-    else if (k == "relax_cap" && v >= 0 && v <= 1000) s->relax_cap = int(v);
     else if (k == "warm_min_problems" && v >= 1) s->warm_min_problems = int(v);
     else if (k == "push_budget_warm" && v >= 0) s->push_budget_warm = int(v);
     else if (k == "push_budget_add" && v >= 0 && v < (int64_t(1) << 30)) s->push_budget_add = int(v);
@@ -1866,9 +1825,6 @@ int pmf_solver_set(pmf_solver *s, const char *name, int64_t v) {
     else if (k == "verify_vec") s->verify_vec = v != 0;
     else if (k == "comp_split") s->comp_split = v != 0;
     else if (k == "rolling") s->rolling = v != 0;
-    else if (k == "push_minb" && (v == 1 || v == 2)) s->push_minb = int(v);
-    else if (k == "grid_div" && v >= 1 && v <= 64) s->grid_div = int(v);
-    else if (k == "push_mode" && (v == 0 || v == 1)) s->push_mode = int(v);
     else if (k == "push_flush" && v >= 0 && v <= 1024) s->push_flush = int(v);
     else if (k == "fresh_skip") s->fresh_skip = v != 0;
     else if (k == "async" && v >= -1 && v <= 1) s->async_mode = int(v);

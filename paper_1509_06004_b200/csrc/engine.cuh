@@ -122,7 +122,6 @@ struct Ctx {
     int32_t *keeph;         // warm chains (nullable): grid entered its lambda with valid heights, skip its relabel
     int32_t ngrids;
     int32_t rolling;        // rolling warm start: grids emit and advance as they finish
-    int32_t push_mode;      // discharge body: 0 two barriers per iteration, 1 one (double-buffered inflow)
     uint8_t *tfresh;        // per tile: heights are exact from the last relabel (first discharge
                             // pass skips its local relabel, a no-op then); nullptr: off
     int32_t push_flush;     // discharge: hand border inflow to the neighbours every this many iterations (0 off)

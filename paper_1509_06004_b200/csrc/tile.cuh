@@ -469,14 +469,14 @@ __device__ __forceinline__ int ring_index(int s, int j) {
 }
 
 __shared__ int32_t s_ph[RPIX];        // discharge heights (ring: neighbour tiles)
-__shared__ int32_t s_in[2][4][RPIX];  // s_in[b][d][q]: flow pushed into q by its d-neighbour (buffer b)
-__shared__ int s_rowin[2][TH + 2];    // ring-frame row received inflow (buffer b)
+__shared__ int32_t s_in[1][4][RPIX];  // s_in[0][d][q]: flow pushed into q by its d-neighbour
+__shared__ int s_rowin[1][TH + 2];    // ring-frame row received inflow
 
 // Discharge scratch invariant: inflow slots and row flags are zero at every
 // pass boundary; established once per CTA by push_prepare().
 __device__ __forceinline__ void push_prepare() {
-    for (int j = threadIdx.x; j < 2 * 4 * RPIX; j += blockDim.x) (&s_in[0][0][0])[j] = 0;
-    if (threadIdx.x < 2 * (TH + 2)) (&s_rowin[0][0])[threadIdx.x] = 0;
+    for (int j = threadIdx.x; j < 4 * RPIX; j += blockDim.x) (&s_in[0][0][0])[j] = 0;
+    if (threadIdx.x < TH + 2) (&s_rowin[0][0])[threadIdx.x] = 0;
 }
 
 // Residuals of one pixel held in registers: EdgeU8 keeps the packed u8x4
@@ -562,8 +562,7 @@ __device__ __forceinline__ void push_flush(const Ctx &c, int32_t t, int64_t p, i
 }
 
 template <class E>
-__device__ __forceinline__ TileResult push_tile(const Ctx &c, int32_t t, int iters, int relabel_every,
-                                                int relax_cap) {
+__device__ __forceinline__ TileResult push_tile(const Ctx &c, int32_t t, int iters, int relabel_every) {
     constexpr int OFF[4] = {-1, 1, -RW, RW};
     const int i = threadIdx.x, lx = i & 31, ly = i >> 5, pi = ly * SP + lx;
     const int q = (ly + 1) * RW + lx + 1;
@@ -601,7 +600,7 @@ __device__ __forceinline__ TileResult push_tile(const Ctx &c, int32_t t, int ite
             s_sm[i] = R.mask();
             __syncthreads();
             const unsigned long long tr0 = i == 0 ? gtimer() : 0ull;
-            const int rr = tile_relax(s_sd, s_sm, s_hv, 1, relax_cap), conv = rr & 1;
+            const int rr = tile_relax(s_sd, s_sm, s_hv, 1), conv = rr & 1;
             if (i == 0) {   // diagnostics
                 atomicAdd(&c.stat[ST_RELAX_NS], gtimer() - tr0);
                 atomicAdd(&c.stat[ST_RELAX_N], 1ull);
@@ -620,12 +619,16 @@ __device__ __forceinline__ TileResult push_tile(const Ctx &c, int32_t t, int ite
         }
         until_relabel--;
         // warp == tile row: rows without an active pixel skip the push
-        // work, rows nobody pushed into skip the merge (barriers stay)
+        // work, rows nobody pushed into skip the merge (barriers stay).
+        // Every pixel reads its neighbours' heights here, before the
+        // relabels of this iteration write any: a pixel that becomes active
+        // by inflow relabels from these values too (no read of s_ph races
+        // with a relabel write; racecheck-clean)
         const bool mine = e > 0 && h < HINF;
         int32_t hn[4];
-        if (__any_sync(0xffffffffu, mine)) {
 #pragma unroll
-            for (int d = 0; d < 4; d++) hn[d] = s_ph[q + OFF[d]];
+        for (int d = 0; d < 4; d++) hn[d] = s_ph[q + OFF[d]];
+        if (__any_sync(0xffffffffu, mine)) {
             // ---- push downhill (heights are fixed during this phase, so
             // an arc is never pushed both ways and every inflow slot has
             // one writer)
@@ -663,10 +666,6 @@ __device__ __forceinline__ TileResult push_tile(const Ctx &c, int32_t t, int ite
             if (lx == 0) s_rowin[0][ly + 1] = 0;
         }
         if (e > 0 && h < HINF) {
-            if (!mine) {   // became active by inflow this iteration
-#pragma unroll
-                for (int d = 0; d < 4; d++) hn[d] = s_ph[q + OFF[d]];
-            }
             int32_t m = HINF;
 #pragma unroll
             for (int d = 0; d < 4; d++)
@@ -709,144 +708,10 @@ __device__ __forceinline__ TileResult push_tile(const Ctx &c, int32_t t, int ite
     return TileResult{act, s_side};
 }
 
-// One-barrier variant: each iteration absorbs the inflow of the previous
-// one (double-buffered slots), relabels an active pixel that has no
-// admissible arc, and pushes -- all before a single CTA barrier.  Neighbour
-// heights read in the same phase may be stale or fresh (both are fine for
-// the lock-free rule h(p) > h(q)); flow in flight at a pass end is absorbed
-// before the write-back.  Exactness comes from the global relabel, as for
-// the two-barrier variant.
 template <class E>
-__device__ __forceinline__ void push_absorb(int b, int q, int lx, int ly, int32_t &e, int32_t *r) {
-    if (s_rowin[b][ly + 1]) {
-#pragma unroll
-        for (int d = 0; d < 4; d++) {
-            const int32_t v = s_in[b][d][q];
-            if (v) {
-                e += v;
-                r[d] += v;
-                s_in[b][d][q] = 0;
-            }
-        }
-        __syncwarp();
-        if (lx == 0) s_rowin[b][ly + 1] = 0;
-    }
-}
-
-template <class E>
-__device__ __forceinline__ TileResult push_tile1(const Ctx &c, int32_t t, int iters, int relabel_every,
-                                                 int relax_cap) {
-    constexpr int OFF[4] = {-1, 1, -RW, RW};
-    const int i = threadIdx.x, lx = i & 31, ly = i >> 5, pi = ly * SP + lx;
-    const int q = (ly + 1) * RW + lx + 1;
-    const int64_t p = int64_t(t) * TPIX + i;
-    const int32_t w0 = __ldcg(c.w + p);
-    const typename E::Word rv0 = E::load(c.r, p);
-    int32_t e = w0, h = __ldcg(c.h + p);
-    int32_t r[4];
-#pragma unroll
-    for (int d = 0; d < 4; d++) r[d] = E::lane(rv0, d);
-    if (i < 4 * TW) {
-        const int s = i / TW, j = i % TW;
-        const int32_t nb = tile_nb(c, t, s);
-        const int32_t v = nb >= 0 ? __ldcg(c.h + int64_t(nb) * TPIX + halo_index(s, j)) : HINF;
-        s_hv[s][j] = v;
-        s_ph[ring_index(s, j)] = v;
-    }
-    if (i == 0) s_side = 0;
-    int act = 1, until_relabel = 0, b = 0;
-    for (int it = 0; it < iters; it++) {
-        push_absorb<E>(b, q, lx, ly, e, r);
-        if (relabel_every && until_relabel == 0) {
-            until_relabel = relabel_every;
-            // exact local relabel (frozen pixels stay frozen)
-            s_sd[pi] = e < 0 ? 1 : HINF;
-            s_sm[i] = uint8_t((r[0] > 0) | ((r[1] > 0) << 1) | ((r[2] > 0) << 2) | ((r[3] > 0) << 3));
-            __syncthreads();
-            const int conv = tile_relax(s_sd, s_sm, s_hv, 1, relax_cap) & 1;
-            if (h < HINF && (conv || s_sd[pi] < HINF)) h = s_sd[pi];
-            s_ph[q] = h;
-            act = __syncthreads_or(e > 0 && h < HINF);
-            if (!act) break;
-        } else if (it == 0) {
-            s_ph[q] = h;
-            act = __syncthreads_or(e > 0 && h < HINF);
-            if (!act) break;
-        }
-        until_relabel--;
-        const int nb = b ^ 1;
-        int pushed = 0;
-        if (e > 0 && h < HINF) {
-            int32_t hn[4];
-#pragma unroll
-            for (int d = 0; d < 4; d++) hn[d] = s_ph[q + OFF[d]];
-            int32_t m = HINF;
-#pragma unroll
-            for (int d = 0; d < 4; d++)
-                if (r[d] > 0) m = min(m, hn[d]);
-            if (m >= h) {   // no admissible arc: relabel, then push along the new one
-                h = m >= HINF ? HINF : m + 1;
-                s_ph[q] = h;
-            }
-#pragma unroll
-            for (int d = 0; d < 4; d++) {
-                if (e > 0 && r[d] > 0 && h > hn[d]) {
-                    const int32_t dl = min(e, r[d]);
-                    e -= dl;
-                    r[d] -= dl;
-                    s_in[nb][opp(d)][q + OFF[d]] += dl;
-                    pushed |= 1 << d;
-                }
-            }
-            if (pushed & ((1 << DL) | (1 << DR))) s_rowin[nb][ly + 1] = 1;
-            if (pushed & (1 << DU)) s_rowin[nb][ly] = 1;
-            if (pushed & (1 << DD)) s_rowin[nb][ly + 2] = 1;
-        }
-        b = nb;
-        act = __syncthreads_or((e > 0 && h < HINF) || pushed);
-        if (!act) break;
-    }
-    if (act) {   // iteration cap: absorb the flow still in flight
-        push_absorb<E>(b, q, lx, ly, e, r);
-        act = __syncthreads_or(e > 0 && h < HINF);
-    }
-    // ---- write back: interior pixels plainly, border pixels as deltas
-    const typename E::Word rv = E::pack(r[0], r[1], r[2], r[3]);
-    if (!on_border(i)) {
-        c.w[p] = e;
-        E::store(c.r, p, rv);
-    } else {
-        if (e != w0) atomicAdd(&c.w[p], e - w0);
-        E::store_delta(c.r, p, rv, rv0);
-    }
-    c.h[p] = h;
-    if (i < 4) s_rowin[i >> 1][(i & 1) * (TH + 1)] = 0;   // ring rows are never absorbed
-    __syncthreads();
-    if (i < 4 * TW) {
-        const int s = i / TW, j = i % TW;
-        const int rq = ring_index(s, j);
-        const int32_t a = s_in[0][opp(s)][rq] + s_in[1][opp(s)][rq];
-        if (a > 0) {
-            s_in[0][opp(s)][rq] = 0;
-            s_in[1][opp(s)][rq] = 0;
-            const int64_t qn = int64_t(tile_nb(c, t, s)) * TPIX + halo_index(s, j);
-            atomicAdd(&c.w[qn], a);
-            E::add(c.r, qn, opp(s), a);
-            atomicOr(&s_side, 1 << s);
-        }
-    }
-    __syncthreads();
-    return TileResult{act, s_side};
-}
-
-template <class E, int MINB>
-__global__ void __launch_bounds__(NTT, MINB) k_push(Ctx c, int k, int iters, int relabel_every, int relax_cap,
-                                                    LaunchCtl lc) {
+__global__ void __launch_bounds__(NTT, 2) k_push(Ctx c, int k, int iters, int relabel_every, LaunchCtl lc) {
     push_prepare();
-    if (c.push_mode == 1)
-        tile_loop(c, k, lc, [&](int32_t t) { return push_tile1<E>(c, t, iters, relabel_every, relax_cap); });
-    else
-        tile_loop(c, k, lc, [&](int32_t t) { return push_tile<E>(c, t, iters, relabel_every, relax_cap); });
+    tile_loop(c, k, lc, [&](int32_t t) { return push_tile<E>(c, t, iters, relabel_every); });
 }
 
 }  // namespace pmf

@@ -2,11 +2,11 @@
 // slice of shared memory; no CTA barrier anywhere, so an SM keeps 16 tiles
 // in flight and a lone tile is not slowed down by 31 idle warps.
 //
-//   k_wpush     push-relabel discharge over the tile's ACTIVE pixels only
-//               (row by row, alternating direction: Gauss-Seidel sweeps),
-//               with an exact local relabel by bitset BFS
-//   k_wbfs_sink exact distance to the sink (global relabel, solvers.py:54-71)
 //   k_wbfs_src  residual closure of the excess pixels (solvers.py:144-158)
+//
+// (Warp-per-tile discharge and sink-distance kernels were measured against
+// the 1024-thread CTA kernels and lost: a lone warp's tile pass is ~3x
+// slower; they were removed.)
 //
 // Bitset representation: lane y holds 32-bit row words (bit x = pixel
 // (x, y)); horizontal moves are shifts, vertical moves are shuffles.
@@ -101,62 +101,6 @@ __device__ __forceinline__ void wt_arc_masks(const WarpTile<E> &T, int lane, uin
 __device__ __forceinline__ uint32_t row_ballot_to_lane(bool pred, int y, int lane, uint32_t cur) {
     uint32_t b = __ballot_sync(0xffffffffu, pred);
     return lane == y ? b : cur;
-}
-
-// ---------------------------------------------------------------------------
-// bitset BFS: exact distance inside the tile to the sink-residual pixels
-// (value 1) or to a halo pixel (its height + 1), over the pixels' own
-// residual arcs.  Frozen pixels (blocked) are never reached.  Writes T.h for
-// every non-blocked pixel (HINF where unreached).  m[] = own-arc row masks.
-// ---------------------------------------------------------------------------
-template <class E>
-__device__ __forceinline__ void wt_bfs_dist(WarpTile<E> &T, int lane, const uint32_t m[4], uint32_t sinks,
-                                            uint32_t blocked) {
-    const int y = lane;
-    // halo injections: left/right pixels of my row, top row via lane x of
-    // the U halo, bottom row via lane x of the D halo
-    const int32_t iL = (m[0] & 1u) && T.hh[DL][y] < HINF ? T.hh[DL][y] + 1 : HINF;
-    const int32_t iR = (m[1] >> 31) && T.hh[DR][y] < HINF ? T.hh[DR][y] + 1 : HINF;
-    const uint32_t m2_row0 = __shfl_sync(0xffffffffu, m[2], 0);
-    const uint32_t m3_row31 = __shfl_sync(0xffffffffu, m[3], 31);
-    const int32_t iU = ((m2_row0 >> lane) & 1u) && T.hh[DU][lane] < HINF ? T.hh[DU][lane] + 1 : HINF;
-    const int32_t iD = ((m3_row31 >> lane) & 1u) && T.hh[DD][lane] < HINF ? T.hh[DD][lane] + 1 : HINF;
-    for (int yy = 0; yy < TH; yy++) T.h[yy * TW + lane] = HINF;
-    __syncwarp();
-    uint32_t V = blocked;
-    uint32_t F = sinks & ~V;
-    int32_t L = 1;
-    for (;;) {
-        // injections at level L
-        uint32_t inj = (iL == L ? 1u : 0u) | (iR == L ? 0x80000000u : 0u);
-        uint32_t mU = __ballot_sync(0xffffffffu, iU == L);
-        uint32_t mD = __ballot_sync(0xffffffffu, iD == L);
-        if (lane == 0) inj |= mU;
-        if (lane == 31) inj |= mD;
-        F = (F | inj) & ~V;
-        V |= F;
-        for (uint32_t b = F; b; b &= b - 1) T.h[y * TW + (__ffs(b) - 1)] = L;
-        // expand one level over pull arcs (pixel takes its d-neighbour's level + 1)
-        uint32_t up = __shfl_up_sync(0xffffffffu, F, 1);
-        uint32_t dn = __shfl_down_sync(0xffffffffu, F, 1);
-        if (lane == 0) up = 0;
-        if (lane == 31) dn = 0;
-        uint32_t N = ((F << 1) & m[0]) | ((F >> 1) & m[1]) | (up & m[2]) | (dn & m[3]);
-        F = N & ~V;
-        ++L;
-        if (!__any_sync(0xffffffffu, F != 0)) {
-            // jump to the next pending injection level
-            int32_t nx = HINF;
-            if (iL >= L) nx = min(nx, iL);
-            if (iR >= L) nx = min(nx, iR);
-            if (iU >= L) nx = min(nx, iU);
-            if (iD >= L) nx = min(nx, iD);
-            nx = warp_min(nx);
-            if (nx >= HINF) break;
-            L = nx;
-        }
-    }
-    __syncwarp();
 }
 
 // Kogge-Stone fills along a row word: every bit reachable from a set bit of G
@@ -290,39 +234,6 @@ __device__ __forceinline__ void warp_loop(const Ctx &c, int k, const LaunchCtl &
 }
 
 // ---------------------------------------------------------------------------
-// global relabel (exact distance to the sink), warp per tile
-// ---------------------------------------------------------------------------
-template <class E>
-__global__ void __launch_bounds__(WPB * 32) k_wbfs_sink(Ctx c, int k, LaunchCtl lc) {
-    extern __shared__ __align__(16) unsigned char smem_raw[];
-    WarpTile<E> &T = reinterpret_cast<WarpTile<E> *>(smem_raw)[threadIdx.x >> 5];
-    const int lane = threadIdx.x & 31;
-    warp_loop(c, k, lc, [&](int32_t t) -> TileResult {
-        const TileNb g = tile_nbs(c, t);
-        const int64_t base = int64_t(t) * TPIX;
-        wt_load<E>(c, t, T, g, lane, true, false);
-        uint32_t m[4];
-        wt_arc_masks<E>(T, lane, m);
-        uint32_t sinks = 0;
-        for (int y = 0; y < TH; y++) sinks = row_ballot_to_lane(T.w[y * TW + lane] < 0, y, lane, sinks);
-        wt_bfs_dist<E>(T, lane, m, sinks, 0u);
-        // relaxation from above: only ever lower the stored distance
-        int out = 0;
-        for (int y = 0; y < TH; y++) {
-            const int p = y * TW + lane;
-            const int32_t h0 = __ldcg(c.h + base + p), h1 = T.h[p];
-            if (h1 < h0) {
-                c.h[base + p] = h1;
-                out |= (lane == 0 ? 1 << DL : 0) | (lane == TW - 1 ? 1 << DR : 0) |
-                       (y == 0 ? 1 << DU : 0) | (y == TH - 1 ? 1 << DD : 0);
-            }
-        }
-        for (int o = 16; o; o >>= 1) out |= __shfl_xor_sync(0xffffffffu, out, o);
-        return TileResult{0, out};
-    });
-}
-
-// ---------------------------------------------------------------------------
 // source-side closure, warp per tile (cost-0 flood fill with bitsets)
 // ---------------------------------------------------------------------------
 template <class E>
@@ -397,171 +308,6 @@ __global__ void __launch_bounds__(WPB * 32) k_wbfs_src(Ctx c, int k, LaunchCtl l
         if (fresh) out |= (lane == 0 ? 1 << DU : 0) | (lane == 31 ? 1 << DD : 0);
         for (int o = 16; o; o >>= 1) out |= __shfl_xor_sync(0xffffffffu, out, o);
         return TileResult{0, out};
-    });
-}
-
-// ---------------------------------------------------------------------------
-// discharge, warp per tile
-// ---------------------------------------------------------------------------
-template <class E>
-__device__ __forceinline__ void wt_local_relabel(WarpTile<E> &T, int lane) {
-    uint32_t m[4];
-    wt_arc_masks<E>(T, lane, m);
-    uint32_t sinks = 0, frozen = 0;
-    for (int y = 0; y < TH; y++) {
-        const int p = y * TW + lane;
-        sinks = row_ballot_to_lane(T.w[p] < 0, y, lane, sinks);
-        frozen = row_ballot_to_lane(T.h[p] >= HINF, y, lane, frozen);
-    }
-    wt_bfs_dist<E>(T, lane, m, sinks, frozen);   // frozen pixels keep HINF
-    uint32_t a = 0;
-    for (int y = 0; y < TH; y++) {
-        const int p = y * TW + lane;
-        a = row_ballot_to_lane(T.w[p] > 0 && T.h[p] < HINF, y, lane, a);
-    }
-    T.act[lane] = a;
-    __syncwarp();
-}
-
-template <class E>
-__global__ void __launch_bounds__(WPB * 32) k_wpush(Ctx c, int k, int rounds, int relabel_every, LaunchCtl lc) {
-    extern __shared__ __align__(16) unsigned char smem_raw[];
-    WarpTile<E> &T = reinterpret_cast<WarpTile<E> *>(smem_raw)[threadIdx.x >> 5];
-    const int lane = threadIdx.x & 31;
-    warp_loop(c, k, lc, [&](int32_t t) -> TileResult {
-        const TileNb g = tile_nbs(c, t);
-        const int64_t base = int64_t(t) * TPIX;
-        wt_load<E>(c, t, T, g, lane, true, true);
-        // snapshots of the border pixels for delta write-back: lane x keeps
-        // (x, 0) and (x, 31); lane y keeps (0, y) and (31, y)
-        const int32_t sw_t = T.w[lane], sw_b = T.w[31 * TW + lane];
-        const int32_t sw_l = T.w[lane * TW], sw_r = T.w[lane * TW + 31];
-        const auto sr_t = SRes<E>::pack(T.r, lane), sr_b = SRes<E>::pack(T.r, 31 * TW + lane);
-        const auto sr_l = SRes<E>::pack(T.r, lane * TW), sr_r = SRes<E>::pack(T.r, lane * TW + 31);
-        bool any = true;
-        for (int rd = 0; rd < rounds && any; rd++) {
-            if (relabel_every ? (rd % relabel_every == 0) : (rd == 0)) {
-                if (relabel_every) wt_local_relabel<E>(T, lane);
-                else {
-                    uint32_t a = 0;
-                    for (int y = 0; y < TH; y++) {
-                        const int p = y * TW + lane;
-                        a = row_ballot_to_lane(T.w[p] > 0 && T.h[p] < HINF, y, lane, a);
-                    }
-                    T.act[lane] = a;
-                    __syncwarp();
-                }
-            }
-            // one Gauss-Seidel sweep over the rows holding active pixels
-            const bool up = rd & 1;
-            for (int yy = 0; yy < TH; yy++) {
-                const int y = up ? TH - 1 - yy : yy;
-                const uint32_t rowm = T.act[y];
-                if (!rowm) continue;
-                if ((rowm >> lane) & 1) {
-                    atomicAnd(&T.act[y], ~(1u << lane));
-                    const int p = y * TW + lane;
-                    int32_t e = T.w[p];
-                    int32_t hp = T.h[p];
-                    if (e > 0 && hp < HINF) {
-                        const auto word = SRes<E>::word(T.r, p);
-                        int32_t hn[4];
-                        hn[DL] = lane > 0 ? T.h[p - 1] : T.hh[DL][y];
-                        hn[DR] = lane < TW - 1 ? T.h[p + 1] : T.hh[DR][y];
-                        hn[DU] = y > 0 ? T.h[p - TW] : T.hh[DU][lane];
-                        hn[DD] = y < TH - 1 ? T.h[p + TW] : T.hh[DD][lane];
-                        const int qi[4] = {p - 1, p + 1, p - TW, p + TW};
-                        const bool in[4] = {lane > 0, lane < TW - 1, y > 0, y < TH - 1};
-                        const int hpos[4] = {y, y, lane, lane};
-                        int32_t sent = 0;
-                        int32_t mlow = HINF;
-#pragma unroll
-                        for (int d = 0; d < 4; d++) {
-                            const int32_t rr = SRes<E>::lane(word, d);
-                            if (rr <= 0) continue;
-                            if (e > 0 && hp > hn[d]) {
-                                const int32_t dl = min(e, rr);
-                                e -= dl;
-                                sent += dl;
-                                SRes<E>::add(T.r, p, d, -dl);
-                                if (in[d]) {
-                                    const int q = qi[d];
-                                    atomicAdd(&T.w[q], dl);
-                                    SRes<E>::add(T.r, q, opp(d), dl);
-                                    atomicOr(&T.act[q >> 5], 1u << (q & 31));
-                                } else {
-                                    T.hacc[d][hpos[d]] += dl;
-                                }
-                                if (rr > dl) mlow = min(mlow, hn[d]);
-                            } else {
-                                mlow = min(mlow, hn[d]);
-                            }
-                        }
-                        if (sent) atomicSub(&T.w[p], sent);
-                        if (e > 0) {
-                            // no residual arc left downhill: relabel over the
-                            // current arcs (inflows may have opened reverse arcs)
-                            const auto w2 = SRes<E>::word(T.r, p);
-                            mlow = HINF;
-#pragma unroll
-                            for (int d = 0; d < 4; d++)
-                                if (SRes<E>::lane(w2, d) > 0) mlow = min(mlow, hn[d]);
-                            if (mlow >= hp) {
-                                hp = mlow >= HINF ? HINF : mlow + 1;
-                                T.h[p] = hp;
-                            }
-                            if (hp < HINF) atomicOr(&T.act[y], 1u << lane);
-                        }
-                    }
-                }
-                __syncwarp();
-            }
-            any = __any_sync(0xffffffffu, T.act[lane] != 0);
-        }
-        // ---- write back (interior plainly, border pixels as deltas)
-        for (int y = 0; y < TH; y++) {
-            const int p = y * TW + lane;
-            const int64_t gp = base + p;
-            const int32_t e = T.w[p];
-            const auto rw = SRes<E>::pack(T.r, p);
-            const bool border = y == 0 || y == TH - 1 || lane == 0 || lane == TW - 1;
-            if (!border) {
-                c.w[gp] = e;
-                E::store(c.r, gp, rw);
-            }
-            c.h[gp] = T.h[p];
-        }
-        // border pixels: (x, 0) and (x, 31) by lane x; (0, y) and (31, y) by
-        // lane y for y in 1..30
-        {
-            const int pt = lane, pb = 31 * TW + lane;
-            if (T.w[pt] != sw_t) atomicAdd(&c.w[base + pt], T.w[pt] - sw_t);
-            E::store_delta(c.r, base + pt, SRes<E>::pack(T.r, pt), sr_t);
-            if (T.w[pb] != sw_b) atomicAdd(&c.w[base + pb], T.w[pb] - sw_b);
-            E::store_delta(c.r, base + pb, SRes<E>::pack(T.r, pb), sr_b);
-            if (lane > 0 && lane < TH - 1) {
-                const int pl = lane * TW, pr = lane * TW + 31;
-                if (T.w[pl] != sw_l) atomicAdd(&c.w[base + pl], T.w[pl] - sw_l);
-                E::store_delta(c.r, base + pl, SRes<E>::pack(T.r, pl), sr_l);
-                if (T.w[pr] != sw_r) atomicAdd(&c.w[base + pr], T.w[pr] - sw_r);
-                E::store_delta(c.r, base + pr, SRes<E>::pack(T.r, pr), sr_r);
-            }
-        }
-        int out = 0;
-#pragma unroll
-        for (int s = 0; s < 4; s++) {
-            const int32_t a = T.hacc[s][lane];
-            if (a > 0) {
-                const int64_t q = int64_t(g.nb[s]) * TPIX + halo_index(s, lane);
-                atomicAdd(&c.w[q], a);
-                E::add(c.r, q, opp(s), a);
-                out |= 1 << s;
-            }
-        }
-        for (int o = 16; o; o >>= 1) out |= __shfl_xor_sync(0xffffffffu, out, o);
-        const int again = __any_sync(0xffffffffu, T.act[lane] != 0);
-        __syncwarp();
-        return TileResult{again, out};
     });
 }
 

@@ -35,7 +35,6 @@ def main():
     ap.add_argument("--warp", type=int, default=None)
     ap.add_argument("--trace", action="store_true")
     ap.add_argument("--chain", type=int, default=None)
-    ap.add_argument("--cap", type=int, default=None)
     ap.add_argument("--multi", type=int, default=None)
     ap.add_argument("--check", action="store_true", help="compare flows with a chain=1 solve")
     ap.add_argument("--reps", type=int, default=3)
@@ -63,7 +62,6 @@ def main():
     if a.graph is not None: s.set("graph", a.graph)
     if a.warp is not None: s.set("warp", a.warp)
     if a.chain is not None: s.set("chain", a.chain)
-    if a.cap is not None: s.set("relax_cap", a.cap)
     if a.multi is not None: s.set("bfs_multi", a.multi)
     ref = None
     if a.check:

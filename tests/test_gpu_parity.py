@@ -612,3 +612,47 @@ def test_composite_bits_from_device(engine):
             assert s.composite_bits(c, w * h) == pack_bits(ref[c][1])
     finally:
         s.close()
+
+
+# every tuning knob that survives on the ABI (pmf_solver_set), each value
+# against the reference's C1 cuts (golden) -- the knob must not change results
+KNOB_CASES = [
+    {"graph": 0}, {"graph": 0, "async": 0}, {"async": 0}, {"async": 1},
+    {"async": 0, "persistent": 0}, {"async": 0, "persistent_bfs": 1}, {"async": 0, "bfs_multi": 0},
+    {"async": 0, "rolling": 0}, {"chain": 1}, {"chain": 5}, {"chain": 5, "async": 0},
+    {"fresh_skip": 0}, {"warp": 0}, {"warp": 0, "async": 0}, {"async_cont": 0}, {"async_prefetch": 0},
+    {"async_spec": 0}, {"adv_keep_h": 0}, {"push_iters": 4}, {"relabel_every": 0},
+    {"relabel_every": 3, "async": 0}, {"push_budget": 1, "async": 0}, {"push_budget_warm": 1, "chain": 20},
+    {"push_budget_add": 0}, {"push_sweeps": 2, "async": 0, "persistent": 0}, {"bfs_chunk": 1, "graph": 0},
+    {"push_flush": 8}, {"verify_vec": 0}, {"timing": 1}, {"wide_pulses": 8, "force_wide": 1},
+    {"warm_min_problems": 1}, {"async_max_tiles": 0}, {"async_max_grid_tiles": 0},
+    {"phase_log": 1}, {"max_cycles": 100000},
+]
+
+
+@pytest.mark.parametrize("knobs", KNOB_CASES, ids=lambda k: ",".join(f"{a}={b}" for a, b in k.items()))
+def test_every_knob_keeps_c1_bit_exact(engine, knobs):
+    from paper_1509_06004_b200 import _native
+    gold = load_synth("c1_160x120.npz")
+    batch = synth.generate(160, 120, 1, 1, rng_seed=0)
+    s = _native.Solver(0, **knobs)
+    try:
+        _, fl, lab = s.solve_seed_batch(160, 120, batch.problems, gold["lambdas"], "auto")
+    finally:
+        s.close()
+    assert [int(f) for f in fl[0]] == gold["flows"]
+    for k in range(len(gold["flows"])):
+        assert np.array_equal(lab[0, k], gold["labels"][k])
+
+
+def test_removed_knobs_are_refused(engine):
+    """Measured-and-rejected variants are gone from the ABI."""
+    from paper_1509_06004_b200 import _native
+    s = _native.Solver(0)
+    try:
+        for name, v in (("push_mode", 1), ("relax_cap", 4), ("push_minb", 1), ("grid_div", 2), ("warp", 1),
+                        ("warp", 2), ("warp_bfs_tiles", 5)):
+            with pytest.raises(ValueError):
+                s.set(name, v)
+    finally:
+        s.close()
