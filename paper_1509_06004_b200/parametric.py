@@ -108,16 +108,17 @@ class SeedProblem:
         set_(self, "pairwise", pw.reshape(4, n))
         if self.unary_slope.size and int(self.unary_slope.min()) < 0:
             raise ProblemError("unary_slope must be non-negative")
-        fg = frozenset(int(i) for i in self.fg_seeds)
-        bg = frozenset(int(i) for i in self.bg_seeds)
+        fg, fg_idx = _seed_set(self.fg_seeds)
+        bg, bg_idx = _seed_set(self.bg_seeds)
         if fg & bg:
             raise ProblemError("a pixel cannot be both a foreground and background seed")
-        if any(not 0 <= i < n for i in fg) or any(not 0 <= i < n for i in bg):
-            raise ProblemError("seed set contains an out-of-range pixel index")
+        for name, idx in (("fg_seeds", fg_idx), ("bg_seeds", bg_idx)):
+            if idx.size and (int(idx[0]) < 0 or int(idx[-1]) >= n):
+                raise ProblemError(f"{name} contains an out-of-range pixel index")
         set_(self, "fg_seeds", fg)
         set_(self, "bg_seeds", bg)
-        set_(self, "_fg_idx", np.array(sorted(fg), np.int64))
-        set_(self, "_bg_idx", np.array(sorted(bg), np.int64))
+        set_(self, "_fg_idx", fg_idx)
+        set_(self, "_bg_idx", bg_idx)
         set_(self, "_stats", None)
 
     @property
@@ -168,6 +169,30 @@ class SeedProblem:
         m = np.ones(self.n, bool)
         m[self._bg_idx] = False
         return m
+
+
+_SEED_SETS = {}
+
+
+def _seed_set(seeds):
+    """(frozenset of int, sorted read-only int64 index array) of a seed set.
+    A frozenset of Python ints seen before (the problems of one image share
+    their border background set) is reused as is, with its index array."""
+    if isinstance(seeds, frozenset):
+        ent = _SEED_SETS.get(id(seeds))
+        if ent is not None and ent[0]() is seeds:
+            return seeds, ent[1]
+    fs = frozenset(int(i) for i in seeds)
+    idx = np.fromiter(sorted(fs), np.int64, len(fs))
+    idx.flags.writeable = False
+    if isinstance(seeds, frozenset) and len(fs) > 64 and all(type(i) is int for i in seeds):
+        with _PLANE_LOCK:
+            if len(_SEED_SETS) > 4096:
+                for k in [k for k, (r, _) in _SEED_SETS.items() if r() is None]:
+                    del _SEED_SETS[k]
+            _SEED_SETS[id(seeds)] = (weakref.ref(seeds), idx)
+        return seeds, idx
+    return fs, idx
 
 
 _PLANE_STATS = {}

@@ -73,13 +73,20 @@ def border_pixels(width, height, top=True):
     return frozenset(int(p) for p in grid[ring])
 
 
+# the three terms of every intensity difference dsim = |I - I(seed)| in
+# [0, 255]: base 1 + 15 (255 - dsim) // 255, slope 1 + 7 (255 - dsim) // 255,
+# sink 1 + 63 dsim // 255 (harness/synth.py seed terms), as lookup tables
+_DS = np.arange(INTENSITY_MAX + 1, dtype=np.int64)
+_TERM_LUT = np.stack([1 + ((INTENSITY_MAX - _DS) * 15) // INTENSITY_MAX,
+                      1 + ((INTENSITY_MAX - _DS) * 7) // INTENSITY_MAX,
+                      1 + (_DS * 63) // INTENSITY_MAX])
+
+
 def seed_terms(img, x, y):
     """(unary_base, unary_slope, sink_base) from intensity similarity to the
-    seed pixel."""
-    dsim = np.abs(img - img[y, x])
-    near = INTENSITY_MAX - dsim
-    return ((1 + (near * 15) // INTENSITY_MAX).reshape(-1), (1 + (near * 7) // INTENSITY_MAX).reshape(-1),
-            (1 + (dsim * 63) // INTENSITY_MAX).reshape(-1))
+    seed pixel (one table lookup per pixel; same values as the arithmetic)."""
+    dsim = np.abs(img - img[y, x]).reshape(-1)
+    return tuple(np.take(_TERM_LUT[k], dsim) for k in range(3))
 
 
 def seed_problem(img, x, y, pairwise, bg, terms=None):
