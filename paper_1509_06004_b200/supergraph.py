@@ -294,13 +294,34 @@ def solve_seed_supergraph(problems, schedule: LambdaSchedule, swap_mode: str = "
     With ``truths`` (one 0/1 mask per problem) every cut is also scored on
     the device (foreground count, exact overlap; harness/bench.py:95-113)."""
     from . import _native
-    problems = check_seed_supergraph(problems, schedule, swap_mode)
+    problems = _check_seed_args(problems, swap_mode)
     shapes = {(p.width, p.height) for p in problems}
     solver = _native.solver_for_thread(device)
     scores = ()
     skeleton = None
+    if len(shapes) != 1:
+        check_seed_supergraph(problems, schedule, swap_mode)
     if len(shapes) == 1:
-        W, H = shapes.pop()
+        W, H = next(iter(shapes))
+        # the admission checks (Python, the reference's errors in order) run
+        # while the engine stages the planes on a host thread (its ctypes
+        # call releases the GIL); a check error wins over a staging error
+        staged = {}
+
+        def stage():
+            try:
+                solver.seed_stage(W, H, problems, schedule.values, swap_mode)
+            except BaseException as exc:  # noqa: BLE001 -- re-raised below
+                staged["err"] = exc
+
+        sth = threading.Thread(target=stage)
+        sth.start()
+        try:
+            check_seed_supergraph(problems, schedule, swap_mode)
+        finally:
+            sth.join()
+        if "err" in staged:
+            raise staged["err"]
         # the layout's Segment objects (~3 us each in Python; 8,000 for a C5
         # batch) are built on a host thread while the device solves (the
         # engine's ctypes calls release the GIL); swap flags are set after
@@ -310,7 +331,8 @@ def solve_seed_supergraph(problems, schedule: LambdaSchedule, swap_mode: str = "
             th = threading.Thread(target=lambda: box.update(sk=_layout_skeleton(problems, schedule)))
             th.start()
         try:
-            swapped, flows, labels = solver.solve_seed_batch(W, H, problems, schedule.values, swap_mode)
+            solver.seed_run()
+            swapped, flows, labels = solver.seed_fetch(True)
         finally:
             if th is not None:
                 th.join()
