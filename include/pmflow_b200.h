@@ -208,6 +208,14 @@ int pmf_solve_seed_batch(pmf_solver *s, int32_t nprob, int32_t width, int32_t he
  *   pmf_seed_run    build + solve the staged batch; results stay on device;
  *   pmf_seed_fetch  copy swapped flags, flows and (if labels_out != NULL)
  *                   label masks of the last run to the host.
+ * pmf_seed_run = pmf_seed_launch(s, NULL) + pmf_seed_wait(s).  The split
+ * lets a batch stream keep the device busy while the host works: launch
+ * enqueues the whole run on the solver's stream and returns; with `after`
+ * non-NULL (another solver of the same device) the run starts only when
+ * `after`'s last launched run has finished, so runs never share the GPU
+ * while the next batch is staged and the previous one fetched (staging
+ * enqueues copies only).  wait blocks until the run is done and reports
+ * its device errors (supergraph.solve_seed_supergraphs).
  */
 int pmf_seed_stage(pmf_solver *s, int32_t nprob, int32_t width, int32_t height,
                    const int64_t *const *unary_base, const int64_t *const *unary_slope,
@@ -216,6 +224,8 @@ int pmf_seed_stage(pmf_solver *s, int32_t nprob, int32_t width, int32_t height,
                    const int64_t *const *bg_idx, const int32_t *n_bg,
                    int32_t nlam, const int64_t *lambdas, int32_t swap_mode);
 int pmf_seed_run(pmf_solver *s);
+int pmf_seed_launch(pmf_solver *s, pmf_solver *after);
+int pmf_seed_wait(pmf_solver *s);
 int pmf_seed_fetch(pmf_solver *s, uint8_t *swapped_out, int64_t *flows_out, uint8_t *labels_out);
 
 /* Scores of the last seed run on the device (replaces the per-cut host

@@ -21,7 +21,8 @@ from .solvers import NonMaximalFlowError, SolverError, maxflow_many, maxflow_pus
 from .supergraph import (SeedSupergraphResult, Segment, SupergraphError, SupergraphLayout,
                          apply_swap, build_lambda_supergraph, build_seed_supergraph,
                          family_swap_decision, join, solve_composite, solve_composites,
-                         solve_seed_supergraph, split, swap_decision, terminal_balance)
+                         solve_seed_supergraph, solve_seed_supergraphs, split, swap_decision,
+                         terminal_balance)
 
 __version__ = "0.1.0"
 
@@ -35,6 +36,6 @@ __all__ = [
     "build_lambda_supergraph", "build_seed_supergraph", "check_nested", "cut_cost", "energy",
     "family_swap_decision", "gpu_workers", "instantiate", "join", "maxflow_many",
     "maxflow_pushrelabel", "run_dynamic", "solve_composite", "solve_composites",
-    "solve_schedule_sequential", "solve_seed_supergraph", "split", "swap_decision",
+    "solve_schedule_sequential", "solve_seed_supergraph", "solve_seed_supergraphs", "split", "swap_decision",
     "terminal_balance", "__version__",
 ]

@@ -24,7 +24,8 @@ SWAP_MODES = {"auto": 0, "on": 1, "off": 2}
 
 EXPORTS = ("pmf_solver_create", "pmf_solver_destroy", "pmf_solver_set", "pmf_last_error",
            "pmf_solver_stats", "pmf_solver_stream", "pmf_solve_composites", "pmf_solve_seed_batch",
-           "pmf_seed_stage", "pmf_seed_run", "pmf_seed_fetch", "pmf_debug_state",
+           "pmf_seed_stage", "pmf_seed_run", "pmf_seed_launch", "pmf_seed_wait", "pmf_seed_fetch",
+           "pmf_debug_state",
            "pmf_debug_trace", "pmf_debug_busy", "pmf_seed_score", "pmf_debug_phases",
            "pmf_solve_composites_i32", "pmf_composite_bits", "pmf_plane_stats")
 
@@ -84,6 +85,8 @@ def load_library(path: str = LIB_PATH):
             vp, i32, i32, i32, P(vp), P(vp), P(vp), P(vp), P(vp), P(i32), P(vp), P(i32),
             i32, P(i64), i32]
         lib.pmf_seed_run.argtypes = [vp]
+        lib.pmf_seed_launch.argtypes = [vp, vp]
+        lib.pmf_seed_wait.argtypes = [vp]
         lib.pmf_seed_fetch.argtypes = [vp, P(u8), P(i64), P(u8)]
         lib.pmf_solver_stream.argtypes = [vp, P(vp)]
         lib.pmf_debug_state.argtypes = [vp, vp, vp, vp, vp, P(i64)]
@@ -326,6 +329,30 @@ class Solver:
         if rc:
             _raise_for(rc)
 
+    def seed_launch(self, after=None):
+        """Enqueue the run of the staged batch and return at once; with
+        ``after`` (another Solver of the device) the run starts when that
+        solver's last launched run has finished."""
+        rc = self._lib.pmf_seed_launch(self._h, after._h if after is not None else None)
+        if rc:
+            _raise_for(rc)
+        self._launched = True
+
+    def seed_wait(self):
+        """Block until the launched run is done (device errors raised here)."""
+        self._launched = False
+        rc = self._lib.pmf_seed_wait(self._h)
+        if rc:
+            _raise_for(rc)
+
+    def abandon(self):
+        """Wait for a launched run nobody will fetch (errors dropped)."""
+        if getattr(self, "_launched", False):
+            try:
+                self.seed_wait()
+            except Exception:  # noqa: BLE001 -- the stream that launched it has ended
+                pass
+
     def seed_fetch(self, labels=True):
         """(swapped (P,), flows (P, K), labels (P, K, n) uint8 or None)."""
         if getattr(self, "_staged", None) is None:
@@ -393,6 +420,33 @@ def solver_for_thread(device: int = 0) -> Solver:
     if s is None:
         s = pool[device] = Solver(device, **_knobs)
     return s
+
+
+def pipeline_solvers(device: int, depth: int):
+    """The calling thread's ``depth`` solvers for ``device`` used by the
+    batch stream (supergraph.solve_seed_supergraphs), created on first use."""
+    pool = getattr(_tls, "pipes", None)
+    if pool is None:
+        pool = _tls.pipes = {}
+    lst = pool.setdefault(device, [])
+    while len(lst) < depth:
+        lst.append(Solver(device, **_knobs))
+    return lst[:depth]
+
+
+_dev_locks = {}
+_dev_locks_mu = threading.Lock()
+
+
+def device_lock(device: int) -> threading.Lock:
+    """Process-wide lock serialising device solves of one GPU: solvers of
+    different threads may stage and fetch concurrently, but their persistent
+    and cooperative kernels never share the device."""
+    with _dev_locks_mu:
+        lk = _dev_locks.get(device)
+        if lk is None:
+            lk = _dev_locks[device] = threading.Lock()
+        return lk
 
 
 def plane_stats(planes):

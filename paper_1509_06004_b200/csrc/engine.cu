@@ -263,6 +263,9 @@ struct pmf_solver {
     std::vector<std::pair<int, int>> ev_marks;  // (category, event index of start)
     size_t ev_used = 0;
     cudaEvent_t ev_run[2] = {nullptr, nullptr};
+    cudaEvent_t ev_tail = nullptr;     // end of the last launched seed run (pmf_seed_launch's `after`)
+    bool launched = false;             // a seed run was launched and not yet waited for
+    int64_t launch_h2d = 0;
     pmf_stats stats{};
     int edge_bytes = 4;
     Pool *pool = nullptr;
@@ -1374,10 +1377,8 @@ int seed_stage(pmf_solver *s, int32_t nprob, int32_t W, int32_t H, const int64_t
     if ((rc = s->d_seeds.ensure(size_t(nseeds + 1) * 4)) || (rc = s->d_sofs.ensure(sofs.size() * 8))) return rc;
     CK(cudaMemcpyAsync(s->d_seeds.p, hs, size_t(nseeds) * 4, cudaMemcpyHostToDevice, s->st));
     CK(cudaMemcpyAsync(s->d_sofs.p, sofs.data(), sofs.size() * 8, cudaMemcpyHostToDevice, s->st));
-    CK(cudaMemsetAsync(s->d_mask.p, 0, size_t(nprob) * n, s->st));
-    LAUNCH(s, (k_seed_masks<<<std::max(1, std::min(nprob, 4 * s->sms)), 256, 0, s->st>>>(
-                   s->d_mask.as<uint8_t>(), s->d_seeds.as<int32_t>(), s->d_sofs.as<int64_t>(), nprob, n)));
-    CK(cudaGetLastError());
+    // (the device seed masks are built at the start of the run, k_seed_masks:
+    // staging enqueues copies only, so it overlaps another solver's run)
     // distinct planes: check + narrow in one pass, group by group, each
     // group's H2D overlapping the conversion of the next
     const int64_t group = std::max<int64_t>(1, cdiv(nu, 8));
@@ -1461,13 +1462,7 @@ int seed_fetch(pmf_solver *s, uint8_t *swapped_out, int64_t *flows_out, uint8_t 
     uint8_t *ho = s->h_out.as<uint8_t>();
     int64_t *hfl = (int64_t *)(ho + lab_bytes);
     int32_t *hsw = (int32_t *)(hfl + nf);
-    if (labels_out) {
-        if ((rc = s->d_bits.ensure(size_t(bit_bytes)))) return rc;
-        const int grid = int(std::min<int64_t>(cdiv(out_bytes, 32 * 256), 16 * s->sms));
-        LAUNCH(s, (k_pack_bits<<<std::max(grid, 1), 256, 0, s->st>>>(s->d_out.as<uint8_t>(), s->d_bits.as<uint32_t>(),
-                                                                     out_bytes)));
-        CK(cudaGetLastError());
-    }
+    // (the run packed the labels into d_bits, pmf_seed_launch)
     // the bits cross in pieces of >= 4 MB, each unpacked on the host pool
     // while the next one is in flight (the unpack writes 8x the bytes)
     const int64_t full = labels_out ? out_bytes / 8 : 0;   // whole bit bytes = 8 labels each
@@ -1803,6 +1798,7 @@ int pmf_solver_destroy(pmf_solver *s) {
     delete s->pool;
     for (auto e : s->ev_run)
         if (e) cudaEventDestroy(e);
+    if (s->ev_tail) cudaEventDestroy(s->ev_tail);
     if (s->st) cudaStreamDestroy(s->st);
     delete s;
     return 0;
@@ -2225,18 +2221,56 @@ int pmf_seed_stage(pmf_solver *s, int32_t nprob, int32_t W, int32_t H, const int
     return seed_stage(s, nprob, W, H, ub, us, sb, pw, fg_idx, n_fg, bg_idx, n_bg, nlam, lambdas, swap_mode);
 }
 
-int pmf_seed_run(pmf_solver *s) {
+// Enqueue the whole run of the staged batch on the solver's stream: seed
+// masks, build, solve, certificate, label bit packing.  `after` (nullable):
+// a solver whose last launched run must finish first (device runs of a
+// batch stream stay serialised while the host stages and fetches).
+int pmf_seed_launch(pmf_solver *s, pmf_solver *after) {
     if (!s || !s->stage.valid) return fail(PMF_ERR_ARG, "no staged seed batch");
+    if (after == s) return fail(PMF_ERR_ARG, "a solver cannot wait for itself");
     CK(cudaSetDevice(s->device));
-    int64_t h2d = s->stats.h2d_bytes;
+    s->launch_h2d = s->stats.h2d_bytes;
+    if (after) {   // before run_begin: the run's device time excludes the wait
+        if (after->device != s->device) return fail(PMF_ERR_ARG, "solvers on different devices");
+        if (after->ev_tail) CK(cudaStreamWaitEvent(s->st, after->ev_tail, 0));
+    }
     int rc = run_begin(s);
     if (rc) return rc;
-    rc = s->stage.wide ? wide_seed_run(s) : s->stage.u8 ? seed_run_t<EdgeU8>(s) : seed_run_t<EdgeI32>(s);
+    const SeedStage &S = s->stage;
+    const int64_t n = int64_t(S.W) * S.H, out_bytes = int64_t(S.nprob) * S.nlam * n;
+    CK(cudaMemsetAsync(s->d_mask.p, 0, size_t(S.nprob) * n, s->st));
+    LAUNCH(s, (k_seed_masks<<<std::max(1, std::min(S.nprob, 4 * s->sms)), 256, 0, s->st>>>(
+                   s->d_mask.as<uint8_t>(), s->d_seeds.as<int32_t>(), s->d_sofs.as<int64_t>(), S.nprob, n)));
+    CK(cudaGetLastError());
+    rc = S.wide ? wide_seed_run(s) : S.u8 ? seed_run_t<EdgeU8>(s) : seed_run_t<EdgeI32>(s);
     if (rc) return rc;
-    rc = run_end(s);
+    // labels leave the device as bits (unpacked on the host by pmf_seed_fetch)
+    if ((rc = s->d_bits.ensure(size_t(cdiv(out_bytes, 32)) * 4))) return rc;
+    const int grid = int(std::min<int64_t>(cdiv(out_bytes, 32 * 256), 16 * s->sms));
+    LAUNCH(s, (k_pack_bits<<<std::max(grid, 1), 256, 0, s->st>>>(s->d_out.as<uint8_t>(), s->d_bits.as<uint32_t>(),
+                                                                 out_bytes)));
+    CK(cudaGetLastError());
+    if (!s->ev_tail) CK(cudaEventCreateWithFlags(&s->ev_tail, cudaEventDisableTiming));
+    CK(cudaEventRecord(s->ev_tail, s->st));
+    s->launched = true;
+    return 0;
+}
+
+// Wait for the launched run; device errors, statistics.
+int pmf_seed_wait(pmf_solver *s) {
+    if (!s || !s->launched) return fail(PMF_ERR_ARG, "no launched seed run");
+    CK(cudaSetDevice(s->device));
+    s->launched = false;
+    int rc = run_end(s);
     if (s->stage.wide) wide_stats(s);
-    s->stats.h2d_bytes = h2d;
+    s->stats.h2d_bytes = s->launch_h2d;
     return rc;
+}
+
+int pmf_seed_run(pmf_solver *s) {
+    int rc = pmf_seed_launch(s, nullptr);
+    if (rc) return rc;
+    return pmf_seed_wait(s);
 }
 
 // Device scoring of the last seed run against ground-truth masks (one n-byte

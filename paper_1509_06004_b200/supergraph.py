@@ -288,6 +288,72 @@ def check_seed_supergraph(problems, schedule: LambdaSchedule, swap_mode: str = "
     return problems
 
 
+def _stage_checked(solver, problems, schedule: LambdaSchedule, swap_mode: str) -> None:
+    """Stage one same-shape seed batch on ``solver``: the admission checks
+    (Python, the reference's errors in order) run while the engine narrows
+    and copies the planes on a host thread (its ctypes call releases the
+    GIL); a check error wins over a staging error."""
+    W, H = problems[0].width, problems[0].height
+    staged = {}
+
+    def stage():
+        try:
+            solver.seed_stage(W, H, problems, schedule.values, swap_mode)
+        except BaseException as exc:  # noqa: BLE001 -- re-raised below
+            staged["err"] = exc
+
+    sth = threading.Thread(target=stage)
+    sth.start()
+    try:
+        check_seed_supergraph(problems, schedule, swap_mode)
+    finally:
+        sth.join()
+    if "err" in staged:
+        raise staged["err"]
+
+
+def _collect(solver, problems, schedule: LambdaSchedule, skeleton, truths) -> SeedSupergraphResult:
+    """Results of the batch the solver last ran: D2H of flows and label bits
+    (unpacked on the host cores), device scores, CutResults and layout."""
+    swapped, flows, labels = solver.seed_fetch(True)
+    scores = ()
+    if truths is not None:
+        from .scoring import score_cuts
+        scores = score_cuts(solver, truths)
+    return _result(problems, schedule, skeleton, swapped, flows, labels, scores)
+
+
+def _result(problems, schedule, skeleton, swapped, flows, labels, scores) -> SeedSupergraphResult:
+    fl = [[int(f) for f in row] for row in flows]
+    cuts = tuple(CutResult._trusted(fl[i][j], labels[i][j])
+                 for i in range(len(problems)) for j in range(len(schedule)))
+    layout = (_finish_layout(skeleton, swapped, len(schedule)) if skeleton is not None
+              else seed_layout(problems, schedule, swapped))
+    return SeedSupergraphResult(layout, cuts, scores)
+
+
+def _solve_mixed(solver, problems, schedule: LambdaSchedule, swap_mode: str, truths, after=None):
+    """Problems of one height and several widths: one device batch per
+    width (the first run waits for ``after``'s last launched run)."""
+    check_seed_supergraph(problems, schedule, swap_mode)
+    if truths is not None:
+        raise SupergraphError("device scoring needs problems of one shape")
+    shapes = {(p.width, p.height) for p in problems}
+    swapped = np.zeros(len(problems), bool)
+    flows = [None] * len(problems)
+    labels = [None] * len(problems)
+    for (W, H) in sorted(shapes):
+        idx = [i for i, p in enumerate(problems) if (p.width, p.height) == (W, H)]
+        solver.seed_stage(W, H, [problems[i] for i in idx], schedule.values, swap_mode)
+        solver.seed_launch(after)
+        solver.seed_wait()
+        after = None
+        sw, fl, lb = solver.seed_fetch(True)
+        for k, i in enumerate(idx):
+            swapped[i], flows[i], labels[i] = sw[k], fl[k], lb[k]
+    return _result(problems, schedule, None, swapped, flows, labels, ())
+
+
 def solve_seed_supergraph(problems, schedule: LambdaSchedule, swap_mode: str = "auto",
                           device: int = 0, truths=None) -> SeedSupergraphResult:
     """Build + solve + decode a seed supergraph entirely on the device.
@@ -295,66 +361,129 @@ def solve_seed_supergraph(problems, schedule: LambdaSchedule, swap_mode: str = "
     the device (foreground count, exact overlap; harness/bench.py:95-113)."""
     from . import _native
     problems = _check_seed_args(problems, swap_mode)
-    shapes = {(p.width, p.height) for p in problems}
     solver = _native.solver_for_thread(device)
-    scores = ()
-    skeleton = None
-    if len(shapes) != 1:
-        check_seed_supergraph(problems, schedule, swap_mode)
-    if len(shapes) == 1:
-        W, H = next(iter(shapes))
-        # the admission checks (Python, the reference's errors in order) run
-        # while the engine stages the planes on a host thread (its ctypes
-        # call releases the GIL); a check error wins over a staging error
-        staged = {}
-
-        def stage():
-            try:
-                solver.seed_stage(W, H, problems, schedule.values, swap_mode)
-            except BaseException as exc:  # noqa: BLE001 -- re-raised below
-                staged["err"] = exc
-
-        sth = threading.Thread(target=stage)
-        sth.start()
-        try:
-            check_seed_supergraph(problems, schedule, swap_mode)
-        finally:
-            sth.join()
-        if "err" in staged:
-            raise staged["err"]
-        # the layout's Segment objects (~3 us each in Python; 8,000 for a C5
-        # batch) are built on a host thread while the device solves (the
-        # engine's ctypes calls release the GIL); swap flags are set after
-        box = {}
-        th = None
-        if len(problems) * len(schedule) >= 512:   # small layouts: not worth a thread
-            th = threading.Thread(target=lambda: box.update(sk=_layout_skeleton(problems, schedule)))
-            th.start()
-        try:
+    if len({(p.width, p.height) for p in problems}) != 1:
+        with _native.device_lock(device):
+            return _solve_mixed(solver, problems, schedule, swap_mode, truths)
+    _stage_checked(solver, problems, schedule, swap_mode)
+    # the layout's Segment objects (~3 us each in Python; 8,000 for a C5
+    # batch) are built on a host thread while the device solves (the
+    # engine's ctypes calls release the GIL); swap flags are set after
+    box = {}
+    th = None
+    if len(problems) * len(schedule) >= 512:   # small layouts: not worth a thread
+        th = threading.Thread(target=lambda: box.update(sk=_layout_skeleton(problems, schedule)))
+        th.start()
+    try:
+        with _native.device_lock(device):
             solver.seed_run()
-            swapped, flows, labels = solver.seed_fetch(True)
-        finally:
-            if th is not None:
-                th.join()
-        skeleton = box.get("sk")
-        if truths is not None:
-            from .scoring import score_cuts
-            scores = score_cuts(solver, truths)
-    else:  # same height, different widths: one device batch per width
-        if truths is not None:
-            raise SupergraphError("device scoring needs problems of one shape")
-        swapped = np.zeros(len(problems), bool)
-        flows = [None] * len(problems)
-        labels = [None] * len(problems)
-        for (W, H) in sorted(shapes):
-            idx = [i for i, p in enumerate(problems) if (p.width, p.height) == (W, H)]
-            sw, fl, lb = solver.solve_seed_batch(W, H, [problems[i] for i in idx],
-                                                 schedule.values, swap_mode)
-            for k, i in enumerate(idx):
-                swapped[i], flows[i], labels[i] = sw[k], fl[k], lb[k]
-    fl = [[int(f) for f in row] for row in flows]
-    cuts = tuple(CutResult._trusted(fl[i][j], labels[i][j])
-                 for i in range(len(problems)) for j in range(len(schedule)))
-    layout = (_finish_layout(skeleton, swapped, len(schedule)) if skeleton is not None
-              else seed_layout(problems, schedule, swapped))
-    return SeedSupergraphResult(layout, cuts, scores)
+    finally:
+        if th is not None:
+            th.join()
+    return _collect(solver, problems, schedule, box.get("sk"), truths)
+
+
+def solve_seed_supergraphs(batches, schedule: LambdaSchedule, swap_mode: str = "auto",
+                           device: int = 0, truths=None, depth: int = 2):
+    """Stream of seed supergraphs through one device: yields, in order, what
+    ``solve_seed_supergraph(batch, schedule, swap_mode, device, truths_k)``
+    returns for each batch (a list of problems) of ``batches`` -- same
+    values, same errors.  ``truths`` is None or an iterable with one list of
+    truth masks (or None) per batch.
+
+    The host work of neighbouring batches overlaps the device: a stager
+    thread admits and stages batch k + 1 (narrowing, H2D) on the next of
+    ``depth`` solvers of the device while batch k runs; a launcher thread
+    enqueues each staged run behind the previous one (pmf_seed_launch with
+    `after`: runs never share the GPU and start back to back, without a host
+    round trip); the caller's thread waits for batch k, fetches and decodes
+    it (D2H, label unpack, CutResults) while batch k + 1 runs.  An error of
+    batch k is raised when its result is due; the stream ends there.  The
+    serving analogue of run_dynamic's per-worker slots
+    (scheduler.py:253-292, harness/bench.py:79-93); a stream owns its device
+    (no concurrent solves on it from other threads)."""
+    import queue
+
+    from . import _native
+    if depth < 2:
+        raise ValueError("depth must be >= 2")
+    solvers = _native.pipeline_solvers(device, depth + 1)
+    mixed = solvers[depth]   # mixed-width batches, solved by the launcher
+    free = [threading.Semaphore(1) for _ in range(depth)]
+    to_run, to_fetch = queue.Queue(), queue.Queue()
+    stop = threading.Event()
+
+    def stager():
+        try:
+            tr_iter = iter(truths) if truths is not None else None
+            for k, probs in enumerate(batches):
+                tr = next(tr_iter) if tr_iter is not None else None
+                slot = k % depth
+                free[slot].acquire()   # the slot's previous batch has been fetched
+                if stop.is_set():
+                    return
+                try:
+                    probs = _check_seed_args(probs, swap_mode)
+                    if len({(p.width, p.height) for p in probs}) != 1:
+                        item = ("mixed", probs, tr)
+                    else:
+                        _stage_checked(solvers[slot], probs, schedule, swap_mode)
+                        item = ("ok", (probs, _layout_skeleton(probs, schedule)), tr)
+                except BaseException as exc:  # noqa: BLE001 -- raised by the consumer
+                    item = ("err", exc, None)
+                to_run.put((slot, item))
+        except BaseException as exc:  # noqa: BLE001 -- batches / truths iterables raised
+            to_run.put((None, ("err", exc, None)))
+        to_run.put(None)
+
+    def launcher():
+        prev = None   # solver of the last launched run
+        while True:
+            x = to_run.get()
+            if x is None or stop.is_set():
+                to_fetch.put(None)
+                return
+            slot, item = x
+            try:
+                if item[0] == "ok":
+                    solvers[slot].seed_launch(prev)
+                    prev = solvers[slot]
+                elif item[0] == "mixed":
+                    item = ("done", _solve_mixed(mixed, item[1], schedule, swap_mode, item[2], prev), None)
+                    prev = mixed
+            except BaseException as exc:  # noqa: BLE001
+                item = ("err", exc, None)
+            to_fetch.put((slot, item))
+
+    threads = [threading.Thread(target=stager, daemon=True), threading.Thread(target=launcher, daemon=True)]
+    for t in threads:
+        t.start()
+    try:
+        while True:
+            x = to_fetch.get()
+            if x is None:
+                return
+            slot, (kind, a, tr) = x
+            try:
+                if kind == "err":
+                    raise a
+                if kind == "done":
+                    res = a
+                else:
+                    s = solvers[slot]
+                    s.seed_wait()
+                    res = _collect(s, a[0], schedule, a[1], tr)
+            finally:
+                if slot is not None:
+                    free[slot].release()
+            yield res
+    finally:
+        stop.set()
+        for f in free:
+            f.release()
+        while threads[1].is_alive():   # unblock the launcher, then wait for both
+            to_run.put(None)
+            threads[1].join(timeout=0.05)
+        threads[0].join()
+        for s in solvers:   # a run launched but never waited for (stream closed early)
+            s.abandon()

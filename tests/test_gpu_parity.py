@@ -431,6 +431,34 @@ def test_device_scoring_matches_reference():
             assert sc.overlap == Fraction(*rec["overlap"][j]) == overlap(cut.labels, b.truths[pi])
 
 
+def test_seed_supergraph_stream_matches_single_calls():
+    """solve_seed_supergraphs (stager / runner / fetch overlap over two
+    solvers) returns exactly what solve_seed_supergraph returns per batch --
+    flows, label masks, layouts, device scores -- including a mixed-width
+    batch (solved inline) and a failing batch (raised at its position)."""
+    from paper_1509_06004_b200 import solve_seed_supergraphs
+    from paper_1509_06004_b200.supergraph import SupergraphError
+    sched = LambdaSchedule(synth.L20[:6])
+    imgs = [synth.generate(160, 120, 2, 2, rng_seed=s, types=("A", "B")) for s in range(4)]
+    batches = [b.problems for b in imgs[:3]]
+    mixed = synth.generate(96, 120, 1, 1, rng_seed=9).problems + imgs[3].problems[:2]
+    batches.append(mixed)
+    truths = [b.truths for b in imgs[:3]] + [None]
+    want = [solve_seed_supergraph(b, sched, "auto", truths=t) for b, t in zip(batches, truths)]
+    got = list(solve_seed_supergraphs(batches, sched, "auto", truths=truths))
+    assert len(got) == len(want)
+    for g, w in zip(got, want):
+        assert g.layout == w.layout
+        assert [c.flow for c in g.cuts] == [c.flow for c in w.cuts]
+        assert all(np.array_equal(a.labels, b.labels) for a, b in zip(g.cuts, w.cuts))
+        assert g.scores == w.scores
+    out = []
+    with pytest.raises(SupergraphError):
+        for r in solve_seed_supergraphs([batches[0], [], batches[1]], sched):
+            out.append(r)
+    assert len(out) == 1 and [c.flow for c in out[0].cuts] == [c.flow for c in want[0].cuts]
+
+
 def test_run_dynamic_on_gpu_backend():
     """scheduler.py:253-292 policy over the GPU backend (one executor per
     device, queued tasks coalesced into device batches): composite tasks and
