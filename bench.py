@@ -6,13 +6,16 @@
 Default workload (BASELINE.json config 5, the multi-GPU headline; its unit
 of work is config 3's CPMC image): a pool of 256 distinct synthetic CPMC
 images (500x375, rng_seed 0..255; 25 seeds x 2 seed types x 20 lambdas =
-1,000 lambda-graphs each), cut into 32 batches of 8 images.  One step of a
+1,000 lambda-graphs each), cut into 16 batches of 16 images.  One step of a
 rank = one batch, CLAIMED DYNAMICALLY: the rank takes the next batch of the
 shared FIFO (a counter on the process group's store, the torchrun
 analogue of run_dynamic's token queue, scheduler.py:253-292) and solves it
-as one device batch (8,000 lambda-cuts).  Per-GPU work per step is fixed,
-so scaling is weak; no data-path collective exists (ranks share only the
-claim counter, barriers and a max-reduction, over gloo -- no NCCL).
+as one device batch (16,000 lambda-cuts; a larger batch amortises the
+latency-bound tail of its slowest chains: 24.3 / 22.5 / 19.9 ms per image
+at 8 / 16 / 32 images, while 16 batches keep the claims dynamic at
+N = 8).  Per-GPU work per step is fixed, so scaling is weak; no
+data-path collective exists (ranks share only the claim counter, barriers
+and a max-reduction, over gloo -- no NCCL).
 
 value : whole-job lambda-cuts/s with the batch's seed planes already
         resident in HBM (pmf_seed_stage before the timed events), device
@@ -60,9 +63,9 @@ CONFIGS = {
                     "2 seed types x 20 lambdas = 1000 lambda-graphs in one device batch"),
     "c4": dict(w=1920, h=1080, rows=1, cols=1, types=("A",), lams="C4", images=1,
                desc="C4: synthetic 1920x1080, 1 seed, 8 lambdas per supergraph"),
-    "c5": dict(w=500, h=375, rows=5, cols=5, types=("A", "B"), lams="L20", images=8,
+    "c5": dict(w=500, h=375, rows=5, cols=5, types=("A", "B"), lams="L20", images=16,
                desc="C5: batch throughput over 256 distinct CPMC images (500x375, 25 seeds x 2 types "
-                    "x 20 lambdas; rng_seed 0..255) in batches of 8 images claimed dynamically "
+                    "x 20 lambdas; rng_seed 0..255) in batches of 16 images claimed dynamically "
                     "(FIFO) by the GPUs; one batch per GPU per step"),
 }
 # CPU reference sample per step for the big configs (the full C3 image is
@@ -471,6 +474,36 @@ def measure_stream(cfg, steps, warmup, dev, claims, sampler=None, ids=None):
     return dict(e2e_s=dt, cuts=cuts, h2d=st["h2d_bytes"], d2h=st["d2h_bytes"], batches=ids)
 
 
+def measure_stream_synth(cfg, steps, warmup, dev, ids):
+    """Harness path with on-device synthesis (synth_device): per batch the
+    host draws the images from their rng seeds (the reference generator's
+    stream, inside the timed region, on the stager thread), the device
+    derives every plane, solves, and the host receives every flow and label
+    mask -- generate_batch + solve + split of harness/bench.py:79-120."""
+    from paper_1509_06004_b200 import LambdaSchedule, solve_seed_supergraphs
+    from paper_1509_06004_b200.synth_device import generate_images
+
+    sched = LambdaSchedule(lambdas_for(cfg["lams"]))
+    k = cfg["images"]
+
+    def gen(bids):
+        for b in bids:
+            yield generate_images(cfg["w"], cfg["h"], cfg["rows"], cfg["cols"],
+                                  [(b * k + i) % POOL_IMAGES for i in range(k)], cfg["types"])
+
+    for _ in solve_seed_supergraphs(gen(ids[:max(2, warmup)]), sched, "auto", device=dev):
+        pass
+    barrier()
+    cuts = 0
+    t0 = time.perf_counter()
+    for res in solve_seed_supergraphs(gen(ids), sched, "auto", device=dev):
+        cuts += len(res.cuts)
+        del res
+    dt = time.perf_counter() - t0
+    barrier()
+    return dict(e2e_s=dt, cuts=cuts)
+
+
 class _Null:
     def __enter__(self):
         return self
@@ -493,6 +526,9 @@ def run_b200(args, cfg):
     claims = Claims(world > 1)
     m = measure(cfg, args.steps, args.warmup, dev, claims, clk)
     sm = measure_stream(cfg, args.steps, args.warmup, dev, claims, clk, ids=m["batches"])
+    sy = measure_stream_synth(cfg, args.steps, args.warmup, dev, m["batches"])
+    synth_s_max = reduce_max(sy["e2e_s"])
+    synth_cuts_all = int(reduce_sum(sy["cuts"]))
     dev_s_max = reduce_max(m["dev_ms"] / 1e3)
     single_s_max = reduce_max(m["e2e_s"])
     e2e_s_max = reduce_max(sm["e2e_s"])
@@ -561,6 +597,12 @@ def run_b200(args, cfg):
                     "api": "solve_seed_supergraphs (batch stream: staging of batch k+1 and the fetch of "
                            "batch k-1 overlap the solve of batch k; fresh problems of the device loop's "
                            "batches, generated untimed)",
+                    "synthetic_path": {
+                        "value": synth_cuts_all / synth_s_max,
+                        "ms_per_image": 1e3 * synth_s_max / args.steps / nimg,
+                        "api": "solve_seed_supergraphs over synth_device.ImageBatch: images drawn from "
+                               "their rng seeds on the host inside the timed region, planes derived on "
+                               "the device (pmf_synth_stage), every flow and label mask to the host"},
                     "single_call": {"value": cuts_all / single_s_max,
                                     "ms_per_image": 1e3 * single_s_max / args.steps / nimg,
                                     "api": "solve_seed_supergraph, one batch per call",

@@ -224,6 +224,30 @@ int pmf_seed_stage(pmf_solver *s, int32_t nprob, int32_t width, int32_t height,
                    const int64_t *const *bg_idx, const int32_t *n_bg,
                    int32_t nlam, const int64_t *lambdas, int32_t swap_mode);
 int pmf_seed_run(pmf_solver *s);
+
+/*
+ * On-device synthesis (replaces generate_batch's planes,
+ * harness/synth.py:52-136): stage a seed batch of `nimg` synthetic CPMC
+ * images whose planes are derived on the GPU at the start of the run.
+ * images: nimg * width * height intensities (0..255, row-major); seed_xy:
+ * `nseed` interior seed pixels (x, y) shared by every image; types[ntypes]:
+ * 0 = background = the image border (problem_for_seed, synth.py:67-100),
+ * 1 = the border minus its top row.  Problems are image-major, seed,
+ * type-minor, with exactly the planes problem_for_seed derives (unary_base
+ * 1 + 15(255-d)/255, unary_slope 1 + 7(255-d)/255, sink_base 1 + 63d/255,
+ * d = |I - I(seed)|; pairwise 1 + 63(255-|dI|)/255).  Then pmf_seed_run /
+ * launch / wait / fetch / score as for pmf_seed_stage.  The admission
+ * checks (instantiate's errors) are the caller's.
+ */
+int pmf_synth_stage(pmf_solver *s, int32_t nimg, int32_t width, int32_t height, const uint8_t *images,
+                    int32_t nseed, const int32_t *seed_xy, int32_t ntypes, const int32_t *types,
+                    int32_t nlam, const int64_t *lambdas, int32_t swap_mode);
+/* Diagnostics: copy the staged planes of the current seed batch off the
+ * device (after a run for pmf_synth_stage batches): three int32 planes
+ * (unary_base, unary_slope, sink_base) per distinct problem, then four
+ * pairwise planes per distinct pairwise plane; pass NULL / too-small
+ * buffers to read the sizes (*n_planes, *n_pw, in int32 elements). */
+int pmf_debug_planes(pmf_solver *s, int32_t *planes_out, int64_t *n_planes, int32_t *pw_out, int64_t *n_pw);
 int pmf_seed_launch(pmf_solver *s, pmf_solver *after);
 int pmf_seed_wait(pmf_solver *s);
 int pmf_seed_fetch(pmf_solver *s, uint8_t *swapped_out, int64_t *flows_out, uint8_t *labels_out);

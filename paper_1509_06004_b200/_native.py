@@ -25,6 +25,7 @@ SWAP_MODES = {"auto": 0, "on": 1, "off": 2}
 EXPORTS = ("pmf_solver_create", "pmf_solver_destroy", "pmf_solver_set", "pmf_last_error",
            "pmf_solver_stats", "pmf_solver_stream", "pmf_solve_composites", "pmf_solve_seed_batch",
            "pmf_seed_stage", "pmf_seed_run", "pmf_seed_launch", "pmf_seed_wait", "pmf_seed_fetch",
+           "pmf_synth_stage", "pmf_debug_planes",
            "pmf_debug_state",
            "pmf_debug_trace", "pmf_debug_busy", "pmf_seed_score", "pmf_debug_phases",
            "pmf_solve_composites_i32", "pmf_composite_bits", "pmf_plane_stats")
@@ -86,6 +87,8 @@ def load_library(path: str = LIB_PATH):
             i32, P(i64), i32]
         lib.pmf_seed_run.argtypes = [vp]
         lib.pmf_seed_launch.argtypes = [vp, vp]
+        lib.pmf_debug_planes.argtypes = [vp, P(i32), P(i64), P(i32), P(i64)]
+        lib.pmf_synth_stage.argtypes = [vp, i32, i32, i32, P(u8), i32, P(i32), i32, P(i32), i32, P(i64), i32]
         lib.pmf_seed_wait.argtypes = [vp]
         lib.pmf_seed_fetch.argtypes = [vp, P(u8), P(i64), P(u8)]
         lib.pmf_solver_stream.argtypes = [vp, P(vp)]
@@ -322,6 +325,39 @@ class Solver:
         if rc:
             _raise_for(rc)
         self._staged = (width * height, len(problems), lam.size)
+
+    def synth_stage(self, images, coords, types, lambdas, swap_mode="auto"):
+        """Stage synthetic CPMC images (k, H, W) whose planes the device
+        derives (pmf_synth_stage); coords: seed (x, y) pixels; types: "A" /
+        "B" seed types.  Problems image-major, seed, type-minor."""
+        imgs = np.ascontiguousarray(images, np.uint8)
+        k, H, W = imgs.shape
+        xy = np.ascontiguousarray(np.asarray(coords, np.int32).reshape(-1))
+        ty = np.array([{"A": 0, "B": 1}[t] for t in types], np.int32)
+        lam = np.ascontiguousarray(lambdas, np.int64)
+        P = ctypes.POINTER
+        rc = self._lib.pmf_synth_stage(self._h, k, W, H, imgs.ctypes.data_as(P(ctypes.c_uint8)), xy.size // 2,
+                                       xy.ctypes.data_as(P(ctypes.c_int32)), ty.size,
+                                       ty.ctypes.data_as(P(ctypes.c_int32)), lam.size,
+                                       lam.ctypes.data_as(P(ctypes.c_int64)), SWAP_MODES[swap_mode])
+        if rc:
+            _raise_for(rc)
+        self._staged = (W * H, k * (xy.size // 2) * ty.size, lam.size)
+
+    def debug_planes(self):
+        """(planes, pairwise) int32 arrays of the staged batch on the device
+        (diagnostics; synthetic batches: valid after a run)."""
+        P = ctypes.POINTER
+        a, b = ctypes.c_int64(0), ctypes.c_int64(0)
+        rc = self._lib.pmf_debug_planes(self._h, None, ctypes.byref(a), None, ctypes.byref(b))
+        if rc:
+            _raise_for(rc)
+        pl, pw = np.empty(a.value, np.int32), np.empty(b.value, np.int32)
+        rc = self._lib.pmf_debug_planes(self._h, pl.ctypes.data_as(P(ctypes.c_int32)), ctypes.byref(a),
+                                        pw.ctypes.data_as(P(ctypes.c_int32)), ctypes.byref(b))
+        if rc:
+            _raise_for(rc)
+        return pl, pw
 
     def seed_run(self):
         """Build + solve the staged batch; results stay on the device."""

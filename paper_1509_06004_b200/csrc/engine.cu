@@ -194,6 +194,8 @@ struct SeedStage {
     std::vector<int64_t> slope_sum; // per problem: sum of unary_slope over non-fg pixels
     int32_t chain = 1;              // lambdas per warm-start chain
     bool wide = false;              // excess bound past int32: int64 state variant (wide.cuh)
+    bool synth = false;             // planes derived on the device from 8-bit images (pmf_synth_stage)
+    int32_t nimg = 0, nseed = 0;    // ... images and seeds per image of such a batch
 };
 
 }  // namespace
@@ -249,7 +251,8 @@ struct pmf_solver {
     DevBuf d_w, d_h, d_r, d_lab, d_tile_grid, d_tnb, d_fin, d_gpend, d_specg, d_keeph, d_seeds, d_sofs, d_gr, d_tflag, d_vacc, d_truth, d_score, d_plog, d_tfresh, d_grids, d_live, d_act, d_list, d_inq, d_cnt,
         d_snk, d_drain, d_err, d_stat, d_colswap, d_out, d_bits, d_in32, d_pw, d_mask, d_off, d_lam,
         d_swapcnt, d_swapflag, d_ring, d_qstate, d_qctr, d_ctl, d_curlam, d_flows, d_slopesum,
-        d_we, d_wr, d_wgrid, d_wtile, d_wchg, d_wcnt, d_cv;   // int64 state variant (wide.cuh)
+        d_we, d_wr, d_wgrid, d_wtile, d_wchg, d_wcnt, d_cv,   // int64 state variant (wide.cuh)
+        d_img, d_spix;   // on-device synthesis: images, seed pixel per (image, seed)
     HostBuf h_in32, h_pw, h_mask, h_out, h_small, h_seeds;
     Layout lay;
     std::vector<int32_t> ones, curlam0;
@@ -265,6 +268,11 @@ struct pmf_solver {
     cudaEvent_t ev_run[2] = {nullptr, nullptr};
     cudaEvent_t ev_tail = nullptr;     // end of the last launched seed run (pmf_seed_launch's `after`)
     bool launched = false;             // a seed run was launched and not yet waited for
+    bool prepped = false;              // seed_prep_t ran for the run being launched
+    struct Geom {
+        int grid_push = 0, grid_bfs = 0, grid_wbfs = 0;
+        size_t smem_w = 0;
+    } geom[2];                         // launch geometry per residual policy (U8, I32), computed once
     int64_t launch_h2d = 0;
     pmf_stats stats{};
     int edge_bytes = 4;
@@ -1035,6 +1043,18 @@ int64_t max_pair(const int32_t *nb, int W, int H, int y0 = 0, int y1 = -1) {
 
 template <class E>
 int grids_for(pmf_solver *s) {
+    // once per solver and residual policy: the occupancy queries and
+    // cudaFuncSetAttribute wait for kernels running on the device, which
+    // would block a batch stream's launch behind the previous run
+    constexpr int kind = E::kBytes == 4 ? 0 : 1;
+    if (s->geom[kind].grid_push) {
+        s->grid_push = s->geom[kind].grid_push;
+        s->grid_bfs = s->geom[kind].grid_bfs;
+        s->grid_wbfs = s->geom[kind].grid_wbfs;
+        s->smem_w = s->geom[kind].smem_w;
+        s->grid_full = 8 * s->sms;
+        return 0;
+    }
     int occ = 0;
     CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_push<E>, NTT, 0));
     s->grid_push = std::max(1, occ) * s->sms;
@@ -1049,6 +1069,7 @@ int grids_for(pmf_solver *s) {
     CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ2, k_wbfs_src<E>, WPB * 32, s->smem_w));
     s->grid_wbfs = std::max(1, occ2) * s->sms;
     s->grid_full = 8 * s->sms;
+    s->geom[kind] = {s->grid_push, s->grid_bfs, s->grid_wbfs, s->smem_w};
     return 0;
 }
 
@@ -1173,14 +1194,26 @@ int seed_swap_flags(pmf_solver *s, const SeedArgs &a) {
     return 0;
 }
 
+// Host-side preparation of a run: launch geometry, device state and the
+// layout uploads (pageable copies: issued before a batch stream's wait on
+// the previous run, so the launch does not block on it)
 template <class E>
-int seed_run_t(pmf_solver *s) {
-    SeedStage &S = s->stage;
+int seed_prep_t(pmf_solver *s) {
     int rc = grids_for<E>(s);
     if (rc) return rc;
     if ((rc = setup_state(s, E::kBytes))) return rc;
-    if ((rc = s->d_swapflag.ensure(size_t(S.nprob) * 4))) return rc;
+    if ((rc = s->d_swapflag.ensure(size_t(s->stage.nprob) * 4))) return rc;
     s->ctx.swapflag = s->d_swapflag.as<int32_t>();
+    s->prepped = true;
+    return 0;
+}
+
+template <class E>
+int seed_run_t(pmf_solver *s) {
+    SeedStage &S = s->stage;
+    int rc;
+    if (!s->prepped && (rc = seed_prep_t<E>(s))) return rc;
+    s->prepped = false;
     const Ctx &c = s->ctx;
     s->tmark(C_BUILD);
     const SeedArgs a = seed_args(s);
@@ -1213,6 +1246,41 @@ int seed_run_t(pmf_solver *s) {
     if (s->verify) {
         if ((rc = launch_verify<E>(s, c, a))) return rc;
     }
+    return 0;
+}
+
+// Common end of the staging paths: offsets, lambdas, chains and the grid
+// layout, per-problem slope sums (S.slope_sum, filled by the caller).
+int stage_tail(pmf_solver *s, int32_t nprob, int32_t W, int32_t H, int32_t nlam, int32_t swap_mode) {
+    SeedStage &S = s->stage;
+    const int64_t n = int64_t(W) * H;
+    int rc;
+    if ((rc = s->d_off.ensure(size_t(nprob) * 16)) || (rc = s->d_lam.ensure(size_t(nlam) * 8)) ||
+        (rc = s->d_swapcnt.ensure(size_t(nprob) * 8)) || (rc = s->d_mask.ensure(size_t(nprob) * n)) ||
+        (rc = s->d_slopesum.ensure(size_t(nprob) * 8)) || (rc = s->d_flows.ensure(size_t(nprob) * nlam * 8)))
+        return rc;
+    CK(cudaMemcpyAsync(s->d_off.p, S.offs.data(), S.offs.size() * 8, cudaMemcpyHostToDevice, s->st));
+    CK(cudaMemcpyAsync(s->d_lam.p, S.lambdas.data(), size_t(nlam) * 8, cudaMemcpyHostToDevice, s->st));
+    // warm-start chains: nlam lambdas split into chains of S.chain
+    // consecutive values; each chain is one grid solved step by step
+    // auto: enough problems keep the GPU busy with one grid per problem, so
+    // each solves its whole ladder warm; few problems are latency-bound and
+    // solve every lambda cold and in parallel
+    int32_t chain = s->chain;
+    if (chain <= 0) chain = nprob >= s->warm_min_problems ? nlam : 1;
+    chain = std::max(1, std::min(chain, nlam));
+    S.chain = chain;
+    s->lay.clear();
+    for (int p = 0; p < nprob; p++)
+        for (int j = 0; j < nlam; j += chain) s->lay.add(W, H, 0, 0, p, j, std::min(nlam, j + chain));
+    s->lay.out_bytes = int64_t(nprob) * nlam * n;   // one label plane per (problem, lambda)
+    CK(cudaMemcpyAsync(s->d_slopesum.p, S.slope_sum.data(), size_t(nprob) * 8, cudaMemcpyHostToDevice, s->st));
+    S.nprob = nprob;
+    S.nlam = nlam;
+    S.W = W;
+    S.H = H;
+    S.swap_mode = swap_mode;
+    S.valid = true;
     return 0;
 }
 
@@ -1399,21 +1467,6 @@ int seed_stage(pmf_solver *s, int32_t nprob, int32_t W, int32_t H, const int64_t
         CK(cudaMemcpyAsync(s->d_in32.as<int32_t>() + 3 * g0 * n, hb + 3 * g0 * n, size_t(g1 - g0) * 3 * n * 4,
                            cudaMemcpyHostToDevice, s->st));
     }
-    CK(cudaMemcpyAsync(s->d_off.p, S.offs.data(), S.offs.size() * 8, cudaMemcpyHostToDevice, s->st));
-    CK(cudaMemcpyAsync(s->d_lam.p, S.lambdas.data(), size_t(nlam) * 8, cudaMemcpyHostToDevice, s->st));
-    // warm-start chains: nlam lambdas split into chains of S.chain
-    // consecutive values; each chain is one grid solved step by step
-    // auto: enough problems keep the GPU busy with one grid per problem, so
-    // each solves its whole ladder warm; few problems are latency-bound and
-    // solve every lambda cold and in parallel
-    int32_t chain = s->chain;
-    if (chain <= 0) chain = nprob >= s->warm_min_problems ? nlam : 1;
-    chain = std::max(1, std::min(chain, nlam));
-    S.chain = chain;
-    s->lay.clear();
-    for (int p = 0; p < nprob; p++)
-        for (int j = 0; j < nlam; j += chain) s->lay.add(W, H, 0, 0, p, j, std::min(nlam, j + chain));
-    s->lay.out_bytes = int64_t(nprob) * nlam * n;   // one label plane per (problem, lambda)
     // sums of unary_slope over non-fg pixels (sink capacity growth of swapped grids)
     S.slope_sum.assign(size_t(nprob), 0);
     s->pool->run(nprob, [&](int64_t p) {
@@ -1424,16 +1477,113 @@ int seed_stage(pmf_solver *s, int32_t nprob, int32_t W, int32_t H, const int64_t
             if (m[q] != 1) acc += sl[q];
         S.slope_sum[p] = acc;
     });
-    if ((rc = s->d_slopesum.ensure(size_t(nprob) * 8)) || (rc = s->d_flows.ensure(size_t(nprob) * nlam * 8)))
-        return rc;
-    CK(cudaMemcpyAsync(s->d_slopesum.p, S.slope_sum.data(), size_t(nprob) * 8, cudaMemcpyHostToDevice, s->st));
-    S.nprob = nprob;
-    S.nlam = nlam;
-    S.W = W;
-    S.H = H;
-    S.swap_mode = swap_mode;
-    S.valid = true;
+    S.synth = false;
+    if ((rc = stage_tail(s, nprob, W, H, nlam, swap_mode))) return rc;
     s->stats.h2d_bytes = int64_t(bytes_b + bytes_pw) + nseeds * 4 + int64_t(sofs.size()) * 8 + int64_t(nlam) * 8;
+    return 0;
+}
+
+// Seed batch of synthetic CPMC images whose planes are derived on the
+// device (k_synth_planes / k_synth_pw at the start of the run): problems
+// image-major, seed, type-minor; type 0 = border background (reference
+// problem_for_seed, harness/synth.py:67-100), 1 = border minus the top row.
+// Only the 8-bit images, the seed pixels and the seed index lists cross the
+// host link.  The admission checks are the caller's (synth_device.py runs
+// the reference's checks on image histograms).
+int synth_stage(pmf_solver *s, int32_t nimg, int32_t W, int32_t H, const uint8_t *images, int32_t nseed,
+                const int32_t *seed_xy, int32_t ntypes, const int32_t *types, int32_t nlam, const int64_t *lambdas,
+                int32_t swap_mode) {
+    s->comp_n.clear();
+    SeedStage &S = s->stage;
+    S.valid = false;
+    if (nimg < 1 || nseed < 1 || ntypes < 1 || W < 1 || H < 1 || nlam < 1 || !images || !seed_xy || !types ||
+        !lambdas || swap_mode < 0 || swap_mode > 2)
+        return fail(PMF_ERR_ARG, "bad arguments");
+    for (int t = 0; t < ntypes; t++)
+        if (types[t] != 0 && types[t] != 1) return fail(PMF_ERR_ARG, "seed type must be 0 (A) or 1 (B)");
+    for (int j = 0; j < nlam; j++)
+        if (lambdas[j] < 0 || (j && lambdas[j] <= lambdas[j - 1]))
+            return fail(PMF_ERR_ARG, "lambda values must be non-negative and strictly increasing");
+    const int64_t n = int64_t(W) * H;
+    const int64_t nprob64 = int64_t(nimg) * nseed * ntypes;
+    if (nprob64 > (int64_t(1) << 30)) return fail(PMF_ERR_ARG, "too many problems");
+    const int32_t nprob = int32_t(nprob64);
+    // background sets per type (row-major ring; type 1 without the top row)
+    std::vector<int32_t> ring[2];
+    for (int y = 0; y < H; y++)
+        for (int x = 0; x < W; x++)
+            if (x == 0 || y == 0 || x == W - 1 || y == H - 1) {
+                ring[0].push_back(y * W + x);
+                if (y != 0) ring[1].push_back(y * W + x);
+            }
+    std::vector<int32_t> spix(size_t(nimg) * nseed);
+    for (int k = 0; k < nseed; k++) {
+        const int32_t x = seed_xy[2 * k], y = seed_xy[2 * k + 1];
+        if (x < 0 || x >= W || y < 0 || y >= H) return fail(PMF_ERR_ARG, "seed (%d, %d) outside the image", x, y);
+        const bool ring_px = x == 0 || x == W - 1 || y == 0 || y == H - 1;
+        for (int t = 0; t < ntypes; t++)
+            if (ring_px && (types[t] == 0 || y != 0))
+                return fail(PMF_ERR_ARG, "seed (%d, %d) sits on the background border", x, y);
+        for (int i = 0; i < nimg; i++) spix[size_t(i) * nseed + k] = y * W + x;
+    }
+    int rc;
+    CK(cudaStreamSynchronize(s->st));   // the previous run may still read the staging buffers
+    // seed index lists [fg of p0 | bg of p0 | fg of p1 | ...]
+    std::vector<int64_t> sofs(size_t(2 * nprob + 1), 0);
+    for (int p = 0; p < nprob; p++) {
+        sofs[2 * p + 1] = sofs[2 * p] + 1;
+        sofs[2 * p + 2] = sofs[2 * p + 1] + int64_t(ring[types[p % ntypes]].size());
+    }
+    const int64_t nseeds = sofs.back();
+    if ((rc = s->h_seeds.ensure(size_t(nseeds + 1) * 4))) return rc;
+    int32_t *hs = s->h_seeds.as<int32_t>();
+    s->pool->run(nprob, [&](int64_t p) {
+        const std::vector<int32_t> &r = ring[types[p % ntypes]];
+        hs[sofs[2 * p]] = spix[size_t(p / ntypes)];
+        memcpy(hs + sofs[2 * p + 1], r.data(), r.size() * 4);
+    });
+    // slope sums over non-fg pixels from one intensity histogram per image
+    std::vector<int64_t> hist(size_t(nimg) * 256, 0);
+    s->pool->run(nimg, [&](int64_t i) {
+        const uint8_t *im = images + i * n;
+        int64_t *h = hist.data() + i * 256;
+        for (int64_t q = 0; q < n; q++) h[im[q]]++;
+    });
+    S.slope_sum.assign(size_t(nprob), 0);
+    for (int p = 0; p < nprob; p++) {
+        const int64_t u = p / ntypes, i = u / nseed;
+        const int sv = images[i * n + spix[size_t(u)]];
+        int64_t acc = 0;
+        for (int v = 0; v < 256; v++) acc += hist[size_t(i) * 256 + v] * (1 + ((255 - std::abs(v - sv)) * 7) / 255);
+        S.slope_sum[p] = acc - (1 + (255 * 7) / 255);   // the fg seed (dsim 0)
+    }
+    S.offs.assign(2 * size_t(nprob), 0);
+    for (int p = 0; p < nprob; p++) {
+        S.offs[p] = 3 * int64_t(p / ntypes) * n;
+        S.offs[nprob + p] = 4 * int64_t(p / (int64_t(nseed) * ntypes)) * n;
+    }
+    const int64_t nu = int64_t(nimg) * nseed;
+    if ((rc = s->d_in32.ensure(size_t(nu) * n * 3 * 4)) || (rc = s->d_pw.ensure(size_t(nimg) * n * 4 * 4)) ||
+        (rc = s->d_img.ensure(size_t(nimg) * n)) || (rc = s->d_spix.ensure(spix.size() * 4)) ||
+        (rc = s->d_seeds.ensure(size_t(nseeds + 1) * 4)) || (rc = s->d_sofs.ensure(sofs.size() * 8)) ||
+        (rc = s->h_mask.ensure(size_t(nimg) * n)) || (rc = s->h_small.ensure(spix.size() * 4 + 64)))
+        return rc;
+    // images and seed pixels through pinned staging (async copies)
+    memcpy(s->h_mask.p, images, size_t(nimg) * n);
+    memcpy(s->h_small.p, spix.data(), spix.size() * 4);
+    CK(cudaMemcpyAsync(s->d_img.p, s->h_mask.p, size_t(nimg) * n, cudaMemcpyHostToDevice, s->st));
+    CK(cudaMemcpyAsync(s->d_spix.p, s->h_small.p, spix.size() * 4, cudaMemcpyHostToDevice, s->st));
+    CK(cudaMemcpyAsync(s->d_seeds.p, hs, size_t(nseeds) * 4, cudaMemcpyHostToDevice, s->st));
+    CK(cudaMemcpyAsync(s->d_sofs.p, sofs.data(), sofs.size() * 8, cudaMemcpyHostToDevice, s->st));
+    S.lambdas.assign(lambdas, lambdas + nlam);
+    S.u8 = true;                 // arc pairs <= 2 * 64
+    S.wide = s->force_wide;
+    S.synth = true;
+    S.nimg = nimg;
+    S.nseed = nseed;
+    if ((rc = stage_tail(s, nprob, W, H, nlam, swap_mode))) return rc;
+    s->stats.h2d_bytes = int64_t(nimg) * n + int64_t(spix.size()) * 4 + nseeds * 4 + int64_t(sofs.size()) * 8 +
+                         int64_t(nlam) * 8;
     return 0;
 }
 
@@ -2230,6 +2380,11 @@ int pmf_seed_launch(pmf_solver *s, pmf_solver *after) {
     if (after == s) return fail(PMF_ERR_ARG, "a solver cannot wait for itself");
     CK(cudaSetDevice(s->device));
     s->launch_h2d = s->stats.h2d_bytes;
+    s->prepped = false;
+    if (!s->stage.wide) {
+        const int rp = s->stage.u8 ? seed_prep_t<EdgeU8>(s) : seed_prep_t<EdgeI32>(s);
+        if (rp) return rp;
+    }
     if (after) {   // before run_begin: the run's device time excludes the wait
         if (after->device != s->device) return fail(PMF_ERR_ARG, "solvers on different devices");
         if (after->ev_tail) CK(cudaStreamWaitEvent(s->st, after->ev_tail, 0));
@@ -2238,6 +2393,15 @@ int pmf_seed_launch(pmf_solver *s, pmf_solver *after) {
     if (rc) return rc;
     const SeedStage &S = s->stage;
     const int64_t n = int64_t(S.W) * S.H, out_bytes = int64_t(S.nprob) * S.nlam * n;
+    if (S.synth) {   // planes of a synthetic image batch, derived on the device
+        const int64_t nu = int64_t(S.nimg) * S.nseed;
+        LAUNCH(s, (k_synth_planes<<<int(std::min<int64_t>(cdiv(nu * cdiv(n, 4), 256), 64 * s->sms)), 256, 0,
+                                    s->st>>>(s->d_img.as<uint8_t>(), n, S.nseed, s->d_spix.as<int32_t>(), nu,
+                                             s->d_in32.as<int32_t>())));
+        LAUNCH(s, (k_synth_pw<<<int(std::min<int64_t>(cdiv(int64_t(S.nimg) * n, 256), 64 * s->sms)), 256, 0,
+                                s->st>>>(s->d_img.as<uint8_t>(), S.W, S.H, S.nimg, s->d_pw.as<int32_t>())));
+        CK(cudaGetLastError());
+    }
     CK(cudaMemsetAsync(s->d_mask.p, 0, size_t(S.nprob) * n, s->st));
     LAUNCH(s, (k_seed_masks<<<std::max(1, std::min(S.nprob, 4 * s->sms)), 256, 0, s->st>>>(
                    s->d_mask.as<uint8_t>(), s->d_seeds.as<int32_t>(), s->d_sofs.as<int64_t>(), S.nprob, n)));
@@ -2265,6 +2429,36 @@ int pmf_seed_wait(pmf_solver *s) {
     if (s->stage.wide) wide_stats(s);
     s->stats.h2d_bytes = s->launch_h2d;
     return rc;
+}
+
+// Diagnostics: the staged planes of the current seed batch as the solver
+// holds them on the device (unary / slope / sink per distinct problem, then
+// the pairwise planes); sizes in int32 elements, *n_* receive the totals.
+int pmf_debug_planes(pmf_solver *s, int32_t *planes_out, int64_t *n_planes, int32_t *pw_out, int64_t *n_pw) {
+    if (!s || !s->stage.valid || !n_planes || !n_pw) return fail(PMF_ERR_ARG, "bad arguments");
+    CK(cudaSetDevice(s->device));
+    const SeedStage &S = s->stage;
+    const int64_t n = int64_t(S.W) * S.H;
+    int64_t np_ = 0, nw = 0;
+    for (int p = 0; p < S.nprob; p++) {
+        np_ = std::max(np_, S.offs[p] + 3 * n);
+        nw = std::max(nw, S.offs[S.nprob + p] + 4 * n);
+    }
+    if (planes_out && *n_planes >= np_)
+        CK(cudaMemcpyAsync(planes_out, s->d_in32.p, size_t(np_) * 4, cudaMemcpyDeviceToHost, s->st));
+    if (pw_out && *n_pw >= nw) CK(cudaMemcpyAsync(pw_out, s->d_pw.p, size_t(nw) * 4, cudaMemcpyDeviceToHost, s->st));
+    CK(cudaStreamSynchronize(s->st));
+    *n_planes = np_;
+    *n_pw = nw;
+    return 0;
+}
+
+int pmf_synth_stage(pmf_solver *s, int32_t nimg, int32_t width, int32_t height, const uint8_t *images,
+                    int32_t nseed, const int32_t *seed_xy, int32_t ntypes, const int32_t *types, int32_t nlam,
+                    const int64_t *lambdas, int32_t swap_mode) {
+    if (!s) return fail(PMF_ERR_ARG, "null solver");
+    CK(cudaSetDevice(s->device));
+    return synth_stage(s, nimg, width, height, images, nseed, seed_xy, ntypes, types, nlam, lambdas, swap_mode);
 }
 
 int pmf_seed_run(pmf_solver *s) {

@@ -45,6 +45,64 @@ __global__ void k_seed_masks(uint8_t *mask, const int32_t *seeds, const int64_t 
     }
 }
 
+// ---------------------------------------------------------------------------
+// On-device synthesis of CPMC seed batches (harness/synth.py:52-100): the
+// planes of every (image, seed) problem are derived from the 8-bit images
+// instead of crossing the host link (pmf_synth_stage).  Same integer
+// arithmetic as the reference (INTENSITY_MAX = 255):
+//   dsim = |I - I(seed)|          (problem_for_seed, synth.py:82)
+//   unary_base  = 1 + (255 - dsim) * 15 / 255
+//   unary_slope = 1 + (255 - dsim) *  7 / 255
+//   sink_base   = 1 +        dsim  * 63 / 255
+//   pairwise    = 1 + (255 - |dI|) * 63 / 255 on both arcs of an edge,
+//                 0 on arcs leaving the image        (_pairwise_weights :52-64)
+// Planes row-major, laid out as pmf_seed_stage stages them: three int32
+// planes per (image, seed) (the seed types of a seed share them) and four
+// pairwise planes per image.
+// ---------------------------------------------------------------------------
+constexpr int kIntensityMax = 255;
+
+// one thread per 4 pixels of one (image, seed) problem; grid-stride
+__global__ void __launch_bounds__(256) k_synth_planes(const uint8_t *img, int64_t n, int32_t nseed,
+                                                      const int32_t *seed_pix, int64_t nu, int32_t *planes) {
+    const int64_t n4 = (n + 3) / 4;
+    const int64_t stride = int64_t(gridDim.x) * blockDim.x;
+    for (int64_t t = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; t < nu * n4; t += stride) {
+        const int64_t u = t / n4, q0 = (t % n4) * 4;
+        const uint8_t *im = img + (u / nseed) * n;
+        const int s = im[seed_pix[u]];
+        int32_t *pb = planes + 3 * u * n;
+#pragma unroll
+        for (int k = 0; k < 4; k++) {
+            const int64_t q = q0 + k;
+            if (q >= n) break;
+            const int d = abs(int(im[q]) - s);
+            pb[q] = 1 + ((kIntensityMax - d) * 15) / kIntensityMax;
+            pb[n + q] = 1 + ((kIntensityMax - d) * 7) / kIntensityMax;
+            pb[2 * n + q] = 1 + (d * 63) / kIntensityMax;
+        }
+    }
+}
+
+// one thread per pixel of one image: its four arcs (L, R, U, D)
+__global__ void __launch_bounds__(256) k_synth_pw(const uint8_t *img, int32_t W, int32_t H, int32_t nimg,
+                                                  int32_t *pw) {
+    const int64_t n = int64_t(W) * H;
+    const int64_t stride = int64_t(gridDim.x) * blockDim.x;
+    auto w = [](int a, int b) { return 1 + ((kIntensityMax - abs(a - b)) * 63) / kIntensityMax; };
+    for (int64_t t = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; t < int64_t(nimg) * n; t += stride) {
+        const int64_t i = t / n, q = t % n;
+        const int x = int(q % W), y = int(q / W);
+        const uint8_t *im = img + i * n;
+        const int v = im[q];
+        int32_t *o = pw + 4 * i * n;
+        o[q] = x > 0 ? w(v, im[q - 1]) : 0;
+        o[n + q] = x < W - 1 ? w(v, im[q + 1]) : 0;
+        o[2 * n + q] = y > 0 ? w(v, im[q - W]) : 0;
+        o[3 * n + q] = y < H - 1 ? w(v, im[q + W]) : 0;
+    }
+}
+
 // Terminal balance at the mid-schedule lambda (supergraph.py:77-92, 210-212).
 __device__ __forceinline__ int64_t block_sum64(int64_t v, int64_t *red) {
     for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);

@@ -172,6 +172,19 @@ class SeedProblem:
 
 
 _SEED_SETS = {}
+_PRUNE_AT = {}
+
+
+def _prune(cache: dict) -> None:
+    """Drop the entries whose object died, once the cache has doubled since
+    the last pass (amortised O(1) per insertion even when every cached
+    object is still alive, e.g. many batches of problems held at once)."""
+    limit = _PRUNE_AT.get(id(cache), 4096)
+    if len(cache) <= limit:
+        return
+    for k in [k for k, (r, _) in cache.items() if r() is None]:
+        del cache[k]
+    _PRUNE_AT[id(cache)] = max(4096, 2 * len(cache))
 
 
 def _seed_set(seeds):
@@ -187,9 +200,7 @@ def _seed_set(seeds):
     idx.flags.writeable = False
     if isinstance(seeds, frozenset) and len(fs) > 64 and all(type(i) is int for i in seeds):
         with _PLANE_LOCK:
-            if len(_SEED_SETS) > 4096:
-                for k in [k for k, (r, _) in _SEED_SETS.items() if r() is None]:
-                    del _SEED_SETS[k]
+            _prune(_SEED_SETS)
             _SEED_SETS[id(seeds)] = (weakref.ref(seeds), idx)
         return seeds, idx
     return fs, idx
@@ -218,9 +229,7 @@ def _plane_stats(a: np.ndarray, height: int = 0, width: int = 0, pre: dict | Non
         st["border"] = [(d, int(row.max(initial=0))) for d, row in (
             (0, arcs[0][:, 0]), (1, arcs[1][:, -1]), (2, arcs[2][0, :]), (3, arcs[3][-1, :]))]
     with _PLANE_LOCK:
-        if len(_PLANE_STATS) > 4096:
-            for k in [k for k, (r, _) in _PLANE_STATS.items() if r() is None]:
-                del _PLANE_STATS[k]
+        _prune(_PLANE_STATS)
         _PLANE_STATS[key] = (weakref.ref(a), st)
     return st
 

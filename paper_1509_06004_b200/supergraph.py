@@ -231,27 +231,50 @@ def build_seed_supergraph(problems, schedule: LambdaSchedule, swap_mode: str = "
     return composite, layout, originals
 
 
+_SKELETONS = {}
+_SKEL_LOCK = threading.Lock()
+
+
 def _layout_skeleton(problems, schedule: LambdaSchedule):
-    """Segments (all unswapped for now), bridge columns and height of the
-    layout build_seed_supergraph would produce."""
-    widths = [p.width for p in problems for _ in schedule]
-    offsets, bridges, height, _ = _plan(widths, [p.height for p in problems for _ in schedule],
-                                        False)
+    """Segments -- unswapped and swapped instances of every one -- bridge
+    columns and height of the layout build_seed_supergraph would produce.
+    Segment is immutable, so the instances are cached per batch shape and
+    shared by every layout of that shape (a C5 batch has 16,000 segments)."""
+    k = len(schedule)
+    shapes = [(p.width, p.height) for p in problems]
+    key = (shapes[0], len(shapes), k) if len(set(shapes)) == 1 else (tuple(shapes), k)
+    with _SKEL_LOCK:
+        hit = _SKELETONS.get(key)
+    if hit is not None:
+        return hit
+    widths = [w for (w, _) in shapes for _ in range(k)]
+    offsets, bridges, height, _ = _plan(widths, [h for (_, h) in shapes for _ in range(k)], False)
     new = object.__new__
-    segs = []
-    for i, (o, w) in enumerate(zip(offsets, widths)):
-        seg = new(Segment)                     # frozen dataclass, fields set directly
-        seg.__dict__.update(constituent=i, offset=o, width=w, swapped=False)
-        segs.append(seg)
-    return segs, bridges, height
+    variants = []
+    for sw in (False, True):
+        segs = []
+        for i, (o, w) in enumerate(zip(offsets, widths)):
+            seg = new(Segment)                     # frozen dataclass, fields set directly
+            seg.__dict__.update(constituent=i, offset=o, width=w, swapped=sw)
+            segs.append(seg)
+        variants.append(tuple(segs))
+    sk = (variants[0], variants[1], tuple(bridges), height)
+    with _SKEL_LOCK:
+        if len(_SKELETONS) >= 16:
+            _SKELETONS.pop(next(iter(_SKELETONS)))
+        _SKELETONS[key] = sk
+    return sk
 
 
 def _finish_layout(skeleton, swapped, k: int) -> SupergraphLayout:
-    segs, bridges, height = skeleton
-    for i in np.flatnonzero(np.asarray(swapped, bool)):   # a swapped family: its k segments
-        for seg in segs[i * k:(i + 1) * k]:
-            seg.__dict__["swapped"] = True
-    return SupergraphLayout(tuple(segs), tuple(bridges), height)
+    plain, swapped_segs, bridges, height = skeleton
+    flags = np.asarray(swapped, bool)
+    if not flags.any():
+        return SupergraphLayout(plain, bridges, height)
+    segs = list(plain)
+    for i in np.flatnonzero(flags):   # a swapped family: its k segments
+        segs[i * k:(i + 1) * k] = swapped_segs[i * k:(i + 1) * k]
+    return SupergraphLayout(tuple(segs), bridges, height)
 
 
 def seed_layout(problems, schedule: LambdaSchedule, swapped) -> SupergraphLayout:
@@ -324,7 +347,7 @@ def _collect(solver, problems, schedule: LambdaSchedule, skeleton, truths) -> Se
 
 
 def _result(problems, schedule, skeleton, swapped, flows, labels, scores) -> SeedSupergraphResult:
-    fl = [[int(f) for f in row] for row in flows]
+    fl = np.asarray(flows).tolist() if isinstance(flows, np.ndarray) else [[int(f) for f in r] for r in flows]
     cuts = tuple(CutResult._trusted(fl[i][j], labels[i][j])
                  for i in range(len(problems)) for j in range(len(schedule)))
     layout = (_finish_layout(skeleton, swapped, len(schedule)) if skeleton is not None
@@ -384,20 +407,21 @@ def solve_seed_supergraph(problems, schedule: LambdaSchedule, swap_mode: str = "
 
 
 def solve_seed_supergraphs(batches, schedule: LambdaSchedule, swap_mode: str = "auto",
-                           device: int = 0, truths=None, depth: int = 2):
+                           device: int = 0, truths=None, depth: int = 3):
     """Stream of seed supergraphs through one device: yields, in order, what
     ``solve_seed_supergraph(batch, schedule, swap_mode, device, truths_k)``
-    returns for each batch (a list of problems) of ``batches`` -- same
-    values, same errors.  ``truths`` is None or an iterable with one list of
+    returns for each batch (a list of problems, or a synth_device.ImageBatch
+    whose planes the device derives) of ``batches`` -- same values, same
+    errors.  ``truths`` is None or an iterable with one list of
     truth masks (or None) per batch.
 
     The host work of neighbouring batches overlaps the device: a stager
     thread admits and stages batch k + 1 (narrowing, H2D) on the next of
-    ``depth`` solvers of the device while batch k runs; a launcher thread
-    enqueues each staged run behind the previous one (pmf_seed_launch with
-    `after`: runs never share the GPU and start back to back, without a host
-    round trip); the caller's thread waits for batch k, fetches and decodes
-    it (D2H, label unpack, CutResults) while batch k + 1 runs.  An error of
+    ``depth`` solvers of the device while batch k runs, and launches it at
+    once behind the previous run (pmf_seed_launch with `after`: runs never
+    share the GPU and start back to back with no host round trip in
+    between); the caller's thread waits for batch k, fetches and decodes it
+    (D2H, label unpack, CutResults) while batch k + 1 runs.  An error of
     batch k is raised when its result is due; the stream ends there.  The
     serving analogue of run_dynamic's per-worker slots
     (scheduler.py:253-292, harness/bench.py:79-93); a stream owns its device
@@ -405,15 +429,17 @@ def solve_seed_supergraphs(batches, schedule: LambdaSchedule, swap_mode: str = "
     import queue
 
     from . import _native
+    from .synth_device import ImageBatch, stage_image_batch
     if depth < 2:
         raise ValueError("depth must be >= 2")
     solvers = _native.pipeline_solvers(device, depth + 1)
-    mixed = solvers[depth]   # mixed-width batches, solved by the launcher
+    mixed = solvers[depth]   # mixed-width batches, solved synchronously by the stager
     free = [threading.Semaphore(1) for _ in range(depth)]
-    to_run, to_fetch = queue.Queue(), queue.Queue()
+    to_fetch = queue.Queue()
     stop = threading.Event()
 
     def stager():
+        prev = None   # solver of the last launched run
         try:
             tr_iter = iter(truths) if truths is not None else None
             for k, probs in enumerate(batches):
@@ -422,42 +448,31 @@ def solve_seed_supergraphs(batches, schedule: LambdaSchedule, swap_mode: str = "
                 free[slot].acquire()   # the slot's previous batch has been fetched
                 if stop.is_set():
                     return
+                sv = solvers[slot]
                 try:
-                    probs = _check_seed_args(probs, swap_mode)
-                    if len({(p.width, p.height) for p in probs}) != 1:
-                        item = ("mixed", probs, tr)
+                    if isinstance(probs, ImageBatch):   # planes derived on the device
+                        fams = stage_image_batch(sv, probs, schedule, swap_mode)
+                        item = ("ok", (fams, _layout_skeleton(fams, schedule)), tr)
                     else:
-                        _stage_checked(solvers[slot], probs, schedule, swap_mode)
-                        item = ("ok", (probs, _layout_skeleton(probs, schedule)), tr)
+                        probs = _check_seed_args(probs, swap_mode)
+                        if len({(p.width, p.height) for p in probs}) != 1:
+                            item = ("done", _solve_mixed(mixed, probs, schedule, swap_mode, tr, prev), None)
+                            prev = mixed
+                        else:
+                            _stage_checked(sv, probs, schedule, swap_mode)
+                            item = ("ok", (probs, _layout_skeleton(probs, schedule)), tr)
+                    if item[0] == "ok":
+                        sv.seed_launch(prev)
+                        prev = sv
                 except BaseException as exc:  # noqa: BLE001 -- raised by the consumer
                     item = ("err", exc, None)
-                to_run.put((slot, item))
+                to_fetch.put((slot, item))
         except BaseException as exc:  # noqa: BLE001 -- batches / truths iterables raised
-            to_run.put((None, ("err", exc, None)))
-        to_run.put(None)
+            to_fetch.put((None, ("err", exc, None)))
+        to_fetch.put(None)
 
-    def launcher():
-        prev = None   # solver of the last launched run
-        while True:
-            x = to_run.get()
-            if x is None or stop.is_set():
-                to_fetch.put(None)
-                return
-            slot, item = x
-            try:
-                if item[0] == "ok":
-                    solvers[slot].seed_launch(prev)
-                    prev = solvers[slot]
-                elif item[0] == "mixed":
-                    item = ("done", _solve_mixed(mixed, item[1], schedule, swap_mode, item[2], prev), None)
-                    prev = mixed
-            except BaseException as exc:  # noqa: BLE001
-                item = ("err", exc, None)
-            to_fetch.put((slot, item))
-
-    threads = [threading.Thread(target=stager, daemon=True), threading.Thread(target=launcher, daemon=True)]
-    for t in threads:
-        t.start()
+    th = threading.Thread(target=stager, daemon=True)
+    th.start()
     try:
         while True:
             x = to_fetch.get()
@@ -477,13 +492,11 @@ def solve_seed_supergraphs(batches, schedule: LambdaSchedule, swap_mode: str = "
                 if slot is not None:
                     free[slot].release()
             yield res
+            del res
     finally:
         stop.set()
         for f in free:
             f.release()
-        while threads[1].is_alive():   # unblock the launcher, then wait for both
-            to_run.put(None)
-            threads[1].join(timeout=0.05)
-        threads[0].join()
+        th.join()
         for s in solvers:   # a run launched but never waited for (stream closed early)
             s.abandon()
