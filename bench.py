@@ -6,14 +6,13 @@
 Default workload (BASELINE.json config 5, the multi-GPU headline; its unit
 of work is config 3's CPMC image): a pool of 256 distinct synthetic CPMC
 images (500x375, rng_seed 0..255; 25 seeds x 2 seed types x 20 lambdas =
-1,000 lambda-graphs each), cut into 16 batches of 16 images.  One step of a
+1,000 lambda-graphs each), cut into 8 batches of 32 images.  One step of a
 rank = one batch, CLAIMED DYNAMICALLY: the rank takes the next batch of the
 shared FIFO (a counter on the process group's store, the torchrun
 analogue of run_dynamic's token queue, scheduler.py:253-292) and solves it
-as one device batch (16,000 lambda-cuts; a larger batch amortises the
+as one device batch (32,000 lambda-cuts; a larger batch amortises the
 latency-bound tail of its slowest chains: 24.3 / 22.5 / 19.9 ms per image
-at 8 / 16 / 32 images, while 16 batches keep the claims dynamic at
-N = 8).  Per-GPU work per step is fixed, so scaling is weak; no
+at 8 / 16 / 32 images).  Per-GPU work per step is fixed, so scaling is weak; no
 data-path collective exists (ranks share only the claim counter, barriers
 and a max-reduction, over gloo -- no NCCL).
 
@@ -63,9 +62,9 @@ CONFIGS = {
                     "2 seed types x 20 lambdas = 1000 lambda-graphs in one device batch"),
     "c4": dict(w=1920, h=1080, rows=1, cols=1, types=("A",), lams="C4", images=1,
                desc="C4: synthetic 1920x1080, 1 seed, 8 lambdas per supergraph"),
-    "c5": dict(w=500, h=375, rows=5, cols=5, types=("A", "B"), lams="L20", images=16,
+    "c5": dict(w=500, h=375, rows=5, cols=5, types=("A", "B"), lams="L20", images=32,
                desc="C5: batch throughput over 256 distinct CPMC images (500x375, 25 seeds x 2 types "
-                    "x 20 lambdas; rng_seed 0..255) in batches of 16 images claimed dynamically "
+                    "x 20 lambdas; rng_seed 0..255) in batches of 32 images claimed dynamically "
                     "(FIFO) by the GPUs; one batch per GPU per step"),
 }
 # CPU reference sample per step for the big configs (the full C3 image is
@@ -123,6 +122,18 @@ class Claims:
             self.k += 1
             return self.k - 1
         return int(self.store.add(self.KEY, 1)) - 1
+
+
+def mem_available() -> float:
+    """Host MemAvailable in bytes (Linux), or a large default."""
+    try:
+        with open("/proc/meminfo") as f:
+            for line in f:
+                if line.startswith("MemAvailable:"):
+                    return int(line.split()[1]) * 1024.0
+    except OSError:
+        pass
+    return 1e12
 
 
 def cpu_model() -> str:
@@ -459,7 +470,13 @@ def measure_stream(cfg, steps, warmup, dev, claims, sampler=None, ids=None):
     for _ in solve_seed_supergraphs(warm, sched, "auto", device=dev):
         pass
     del warm
-    ids, todo = batches(steps, ids)
+    # host memory: the timed batches are generated up front (~120 MB of
+    # int64 planes per CPMC image); ranks sharing the node split 40 % of the
+    # available memory (with 8 ranks on a small node the stream is shorter)
+    per_batch = 0.125e9 * cfg["images"]
+    budget = 0.4 * mem_available() / int(os.environ.get("LOCAL_WORLD_SIZE", 1))
+    n = max(2, min(steps, int(budget // (2 * per_batch))))
+    ids, todo = batches(n, ids[:n] if ids is not None else None)
     barrier()
     cuts = 0
     ctx = sampler if sampler is not None else _Null()
@@ -471,7 +488,7 @@ def measure_stream(cfg, steps, warmup, dev, claims, sampler=None, ids=None):
         dt = time.perf_counter() - t0
     barrier()
     st = _native.pipeline_solvers(dev, 2)[0].stats()   # its last batch: same shape as every batch
-    return dict(e2e_s=dt, cuts=cuts, h2d=st["h2d_bytes"], d2h=st["d2h_bytes"], batches=ids)
+    return dict(e2e_s=dt, cuts=cuts, h2d=st["h2d_bytes"], d2h=st["d2h_bytes"], batches=ids, steps=len(ids))
 
 
 def measure_stream_synth(cfg, steps, warmup, dev, ids):
@@ -568,7 +585,8 @@ def run_b200(args, cfg):
             secondary[name] = {
                 "workload": c["desc"], "steps": st_, "value": k / (s2["dev_ms"] / 1e3), "unit": UNIT,
                 "ms_per_image": s2["dev_ms"] / st_ / c["images"],
-                "e2e": {"value": ss["cuts"] / ss["e2e_s"], "ms_per_image": 1e3 * ss["e2e_s"] / st_ / c["images"],
+                "e2e": {"value": ss["cuts"] / ss["e2e_s"],
+                        "ms_per_image": 1e3 * ss["e2e_s"] / ss["steps"] / c["images"],
                         "h2d_bytes_per_step": ss["h2d"], "d2h_bytes_per_step": ss["d2h"],
                         "api": "solve_seed_supergraphs (batch stream)",
                         "single_call": {"value": k / s2["e2e_s"],
@@ -592,7 +610,8 @@ def run_b200(args, cfg):
                              "each step also stages a new batch",
                        "parallelism": f"{world} GPU(s), one process each, dynamic batch claims "
                                       "(store counter), no data-path collective, gloo plumbing"},
-            "e2e": {"value": e2e_value, "unit": UNIT, "ms_per_image": 1e3 * e2e_s_max / args.steps / nimg,
+            "e2e": {"value": e2e_value, "unit": UNIT, "ms_per_image": 1e3 * e2e_s_max / sm["steps"] / nimg,
+                    "steps": sm["steps"],
                     "h2d_bytes_per_step": sm["h2d"], "d2h_bytes_per_step": sm["d2h"],
                     "api": "solve_seed_supergraphs (batch stream: staging of batch k+1 and the fetch of "
                            "batch k-1 overlap the solve of batch k; fresh problems of the device loop's "

@@ -62,24 +62,43 @@ __global__ void k_seed_masks(uint8_t *mask, const int32_t *seeds, const int64_t 
 // ---------------------------------------------------------------------------
 constexpr int kIntensityMax = 255;
 
-// one thread per 4 pixels of one (image, seed) problem; grid-stride
+// one thread per 4 pixels of one (image, seed) problem; grid-stride.  With
+// n % 4 == 0 every plane row of 4 pixels is one aligned 16 B store (and the
+// 4 intensities one 4 B load); otherwise scalar stores.
+__device__ __forceinline__ void synth_terms(int v, int s, int32_t &b, int32_t &sl, int32_t &sk) {
+    const int d = abs(v - s);
+    b = 1 + ((kIntensityMax - d) * 15) / kIntensityMax;
+    sl = 1 + ((kIntensityMax - d) * 7) / kIntensityMax;
+    sk = 1 + (d * 63) / kIntensityMax;
+}
+
 __global__ void __launch_bounds__(256) k_synth_planes(const uint8_t *img, int64_t n, int32_t nseed,
                                                       const int32_t *seed_pix, int64_t nu, int32_t *planes) {
     const int64_t n4 = (n + 3) / 4;
     const int64_t stride = int64_t(gridDim.x) * blockDim.x;
+    const bool vec = (n & 3) == 0;
     for (int64_t t = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; t < nu * n4; t += stride) {
         const int64_t u = t / n4, q0 = (t % n4) * 4;
         const uint8_t *im = img + (u / nseed) * n;
         const int s = im[seed_pix[u]];
         int32_t *pb = planes + 3 * u * n;
+        if (vec) {
+            const uchar4 v = *reinterpret_cast<const uchar4 *>(im + q0);
+            int4 b, sl, sk;
+            synth_terms(v.x, s, b.x, sl.x, sk.x);
+            synth_terms(v.y, s, b.y, sl.y, sk.y);
+            synth_terms(v.z, s, b.z, sl.z, sk.z);
+            synth_terms(v.w, s, b.w, sl.w, sk.w);
+            *reinterpret_cast<int4 *>(pb + q0) = b;
+            *reinterpret_cast<int4 *>(pb + n + q0) = sl;
+            *reinterpret_cast<int4 *>(pb + 2 * n + q0) = sk;
+            continue;
+        }
 #pragma unroll
         for (int k = 0; k < 4; k++) {
             const int64_t q = q0 + k;
             if (q >= n) break;
-            const int d = abs(int(im[q]) - s);
-            pb[q] = 1 + ((kIntensityMax - d) * 15) / kIntensityMax;
-            pb[n + q] = 1 + ((kIntensityMax - d) * 7) / kIntensityMax;
-            pb[2 * n + q] = 1 + (d * 63) / kIntensityMax;
+            synth_terms(im[q], s, pb[q], pb[n + q], pb[2 * n + q]);
         }
     }
 }

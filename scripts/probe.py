@@ -41,6 +41,7 @@ def main():
     ap.add_argument("--nprob", type=int, default=None, help="problems per device batch")
     ap.add_argument("--knob", action="append", default=[], help="name=value (any pmf_solver_set knob)")
     ap.add_argument("--images", type=int, default=1, help="images per device batch (rng_seed 0..)")
+    ap.add_argument("--synth", action="store_true", help="planes derived on the device (pmf_synth_stage)")
     a = ap.parse_args()
     c = CFG[a.cfg]
     probs = []
@@ -71,7 +72,12 @@ def main():
     devs = []
     for r in range(a.reps):
         t0 = time.perf_counter()
-        s.seed_stage(c["w"], c["h"], probs, c["lams"], "auto")
+        if a.synth:
+            from paper_1509_06004_b200.synth_device import generate_images
+            ib = generate_images(c["w"], c["h"], c["rows"], c["cols"], range(a.images), c["types"])
+            s.synth_stage(ib.images, ib.coords, ib.types, c["lams"], "auto")
+        else:
+            s.seed_stage(c["w"], c["h"], probs, c["lams"], "auto")
         t1 = time.perf_counter()
         s.seed_run()
         t2 = time.perf_counter()

@@ -67,4 +67,4 @@ def test_local_claims_and_batches():
     c = bench.Claims(False)
     assert [c.next() for _ in range(5)] == [0, 1, 2, 3, 4]
     cfg = bench.CONFIGS["c5"]
-    assert bench.POOL_IMAGES // cfg["images"] == 16      # 256 images in batches of 16
+    assert bench.POOL_IMAGES // cfg["images"] == 8       # 256 images in batches of 32
