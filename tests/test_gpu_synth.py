@@ -93,3 +93,48 @@ def test_synth_stage_rejects_bad_arguments():
     with pytest.raises(ValueError):
         s.synth_stage(img, [(3, 3)], ("A",), (2, 1))          # lambdas not increasing
     s.synth_stage(img, [(3, 0)], ("B",), (1, 2))              # type B: the top row is not background
+
+
+def test_synthetic_batch_on_the_int64_state_variant():
+    """force_wide: the int64 state variant (wide.cuh) reads the device-built
+    planes exactly like staged ones."""
+    sched = LambdaSchedule(synth.L20[:5])
+    b = sd.generate_images(96, 64, 2, 1, rng_seeds=(8,), types=("A", "B"))
+    want = sd.solve_image_batch(b, sched)
+    s = _native.solver_for_thread(0)
+    s.set("force_wide", 1)
+    try:
+        got = sd.solve_image_batch(b, sched)
+        assert s.stats()["wide_mode"] == 1
+    finally:
+        s.set("force_wide", 0)
+    _same(got, want)
+
+
+def test_launch_wait_contract():
+    """pmf_seed_launch / pmf_seed_wait: launch behind another solver's run,
+    wait reports the run; misuse is an argument error, not a hang."""
+    sched = LambdaSchedule(synth.L20[:4])
+    probs = synth.generate(96, 64, 1, 2, rng_seed=3).problems
+    a, b = _native.Solver(0), _native.Solver(0)
+    try:
+        with pytest.raises(ValueError):
+            a.seed_wait()                          # nothing launched
+        with pytest.raises(ValueError):
+            a.seed_launch()                        # nothing staged
+        a.seed_stage(96, 64, probs, sched.values)
+        b.seed_stage(96, 64, probs[::-1], sched.values)
+        with pytest.raises(ValueError):
+            a.seed_launch(a)                       # cannot wait for itself
+        a.seed_launch()
+        b.seed_launch(a)                           # runs after a's run
+        b.seed_wait()
+        a.seed_wait()
+        _, fa, _ = a.seed_fetch(False)
+        _, fb, _ = b.seed_fetch(False)
+        assert np.array_equal(fa, fb[::-1])
+        want = solve_seed_supergraph(probs, sched)
+        assert [c.flow for c in want.cuts] == [int(f) for f in fa.reshape(-1)]
+    finally:
+        a.close()
+        b.close()
