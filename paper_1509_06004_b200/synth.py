@@ -5,8 +5,8 @@ box (which has no reference checkout) generates the same problems from the
 same ``rng_seed``: one image of random constant rectangles plus clipped
 noise (synth.py:22-41), contrast-gated pairwise weights (:52-64), and one
 seed problem per interior lattice point with the border as background
-(:44-49, :73-100).  ``tests/test_synth.py`` pins the planes against the
-reference generator.
+(:44-49, :73-100).  ``tests/test_oracle.py`` and ``tests/test_host.py`` pin
+the planes against digests of the reference generator's problems.
 
 CPMC seed "type B" (BASELINE.json config 3): the same
 foreground seed with the border minus its top row as background -- not in

@@ -71,6 +71,7 @@ def load_synth(name):
 
 
 def problem_digest(p) -> str:
+    """sha256 of a SeedProblem's planes and seeds (make_golden.problem_digest)."""
     import hashlib
     h = hashlib.sha256()
     for a in (p.unary_base, p.unary_slope, p.sink_base, p.pairwise):
@@ -100,14 +101,3 @@ def load_scores():
     batch: per problem flows, foreground counts, exact overlaps."""
     with open(os.path.join(GOLDEN, "scores_96x72_2x2.json")) as f:
         return json.load(f)
-
-
-def problem_digest(p):
-    """sha256 of a SeedProblem's planes and seeds (make_golden.problem_digest)."""
-    import hashlib
-    h = hashlib.sha256()
-    for a in (p.unary_base, p.unary_slope, p.sink_base, p.pairwise):
-        h.update(np.ascontiguousarray(a, np.int64).tobytes())
-    h.update(np.array(sorted(p.fg_seeds), np.int64).tobytes())
-    h.update(np.array(sorted(p.bg_seeds), np.int64).tobytes())
-    return h.hexdigest()
