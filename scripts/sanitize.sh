@@ -10,10 +10,12 @@ run() {   # tool case limit
     tail -4 "gpurun_out/san_$1_$2.txt" >> gpurun_out/san_summary.txt
 }
 : > gpurun_out/san_summary.txt
-for c in c1-async c1-sync c1-sync-host comp comp-host wide; do
+for c in ${CASES:-c1-async c1-sync c1-sync-host comp comp-host wide synth synth-sync stream}; do
     run memcheck $c 300
     run synccheck $c 300
     run racecheck $c 400
 done
+if [ -z "$CASES" ]; then
 run memcheck c3-async 600
 run synccheck c3-async 600
+fi

@@ -9,6 +9,8 @@ c3-async  one C3 CPMC image (50 warm-start chains) through k_async
 comp      a composite with a swapped span (k_load_comp path + certificate)
 *-host    the same case with the host-driven loop (graph=0)
 wide      the int64 state variant on a CAP_MAX-heavy graph
+synth     a synthetic image batch, planes built on the device (async; -sync: step mode)
+stream    the batch stream: runs launched behind each other on three solvers
 Each case checks its result against the oracle, so a sanitizer run that
 perturbs scheduling still has to produce the reference's cuts.
 """
@@ -77,6 +79,26 @@ def main(case):
         assert s.stats()["wide_mode"] == 1
         f, lab, _ = oracle.solve(w, h, g.src_cap, g.snk_cap, g.nbr_cap)
         assert cut.flow == f and np.array_equal(cut.labels, lab)
+    elif case in ("synth", "synth-sync"):
+        # on-device synthesis: k_synth_planes (ragged 53x37 images: the
+        # scalar store path) and k_synth_pw at the start of the run
+        from paper_1509_06004_b200.synth_device import generate_images, solve_image_batch
+        s.set("async", 1 if case == "synth" else 0)
+        b = generate_images(53, 37, 1, 2, rng_seeds=(4, 5), types=("A", "B"))
+        sched = LambdaSchedule(synth.L20[:6])
+        res = solve_image_batch(b, sched)
+        check_seed(b.problems(), sched, res, k=4)
+    elif case == "stream":
+        # batch stream: three solvers, each run launched behind the previous
+        # one (pmf_seed_launch with `after`), an image batch in the middle
+        from paper_1509_06004_b200 import solve_seed_supergraphs
+        from paper_1509_06004_b200.synth_device import generate_images
+        sched = LambdaSchedule(synth.L20[:6])
+        p0 = synth.generate(96, 64, 1, 2, rng_seed=1, types=("A", "B")).problems
+        b1 = generate_images(96, 64, 1, 2, rng_seeds=(2,), types=("A", "B"))
+        p2 = synth.generate(96, 64, 1, 2, rng_seed=3, types=("A", "B")).problems
+        for probs, res in zip((p0, b1.problems(), p2), solve_seed_supergraphs([p0, b1, p2], sched)):
+            check_seed(probs, sched, res, k=4)
     else:
         raise SystemExit(f"unknown case {case}")
     print(case, "ok")
