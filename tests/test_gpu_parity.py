@@ -307,29 +307,34 @@ def test_c3_cpmc_image_rolling_vs_cold_vs_reference(engine):
     per = fw.sum(axis=1)
     assert int(per[0::2].sum()) == 2408913070 and int(per[1::2].sum()) == 2293473574
     assert int(per[0]) == 101007728 and int(per[1]) == 99225144
-    for pi, li in ((0, 0), (17, 9), (49, 19)):
+    rng = np.random.default_rng(303)
+    picks = [(0, 0), (17, 9), (49, 19)] + [(int(rng.integers(0, 50)), int(rng.integers(0, 20)))
+                                           for _ in range(37)]
+    jobs = []
+    for pi, li in picks:
         p = b.problems[pi]
         src, snk, nbr = oracle.instantiate(p.unary_base, p.unary_slope, p.sink_base, p.pairwise,
                                            p.fg_seeds, p.bg_seeds, lams[li])
-        flow, labels, _ = oracle.solve(500, 375, src, snk, nbr)
-        assert int(fw[pi, li]) == flow
-        assert np.array_equal(lw[pi, li].reshape(-1), labels)
+        jobs.append((500, 375, src, snk, nbr, None))
+    for (pi, li), (flow, labels, _) in zip(picks, oracle.solve_many(jobs)):
+        assert int(fw[pi, li]) == flow, (pi, li)
+        assert np.array_equal(lw[pi, li].reshape(-1), labels), (pi, li)
 
 
 def test_c5_batch_sampled_cuts_vs_oracle(engine):
-    """C5's unit of work -- 8 distinct CPMC images (rng_seed 0..7) in one
-    device batch, 400 warm-start chains, the step-synchronous rolling engine
-    the bench runs -- against the oracle on 50 sampled (image, problem,
-    lambda) cuts: bit-exact flows and masks.  Every cut also passed the
-    device certificate (cut cost == flow) inside the solve."""
+    """C5's unit of work -- 32 distinct CPMC images (rng_seed 0..31) in one
+    device batch, 1,600 warm-start chains, the step-synchronous rolling
+    engine the bench runs -- against the oracle on 50 sampled (image,
+    problem, lambda) cuts: bit-exact flows and masks.  Every cut also passed
+    the device certificate (cut cost == flow) inside the solve."""
     from paper_1509_06004_b200 import _native
     probs = []
-    for i in range(8):
+    for i in range(32):
         probs += synth.generate(500, 375, 5, 5, rng_seed=i, types=("A", "B")).problems
     s = _native.Solver(0)
     try:
         _, fl, lab = s.solve_seed_batch(500, 375, probs, synth.L20, "auto")
-        assert s.stats()["async_mode"] == 0   # 8 images: the step-synchronous engine
+        assert s.stats()["async_mode"] == 0   # 32 images: the step-synchronous engine
     finally:
         s.close()
     rng = np.random.default_rng(2026)
