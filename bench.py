@@ -487,7 +487,7 @@ def measure_stream(cfg, steps, warmup, dev, claims, sampler=None, ids=None):
             del res
         dt = time.perf_counter() - t0
     barrier()
-    st = _native.pipeline_solvers(dev, 2)[0].stats()   # its last batch: same shape as every batch
+    st = _native.pipeline_solvers(dev, 1)[0].stats()   # the last stream's solver: same shape as every batch
     return dict(e2e_s=dt, cuts=cuts, h2d=st["h2d_bytes"], d2h=st["d2h_bytes"], batches=ids, steps=len(ids))
 
 

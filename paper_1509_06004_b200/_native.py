@@ -458,16 +458,38 @@ def solver_for_thread(device: int = 0) -> Solver:
     return s
 
 
-def pipeline_solvers(device: int, depth: int):
-    """The calling thread's ``depth`` solvers for ``device`` used by the
-    batch stream (supergraph.solve_seed_supergraphs), created on first use."""
+def pipeline_solvers(device: int, depth: int, lease: bool = False):
+    """``depth`` solvers for ``device`` from the calling thread's pool, used
+    by the batch stream (supergraph.solve_seed_supergraphs) and created on
+    first use.  lease=True hands out a set no running stream of this thread
+    holds (nested streams get their own solvers; give it back with
+    release_solvers); without it, the most recent set (its statistics)."""
     pool = getattr(_tls, "pipes", None)
     if pool is None:
         pool = _tls.pipes = {}
-    lst = pool.setdefault(device, [])
-    while len(lst) < depth:
-        lst.append(Solver(device, **_knobs))
-    return lst[:depth]
+    sets = pool.setdefault(device, [])
+    if not lease:
+        return sets[-1][1][:depth] if sets else []
+    for ent in sets:
+        if not ent[0]:
+            break
+    else:
+        ent = [False, []]
+        sets.append(ent)
+    while len(ent[1]) < depth:
+        ent[1].append(Solver(device, **_knobs))
+    ent[0] = True
+    sets.remove(ent)
+    sets.append(ent)   # most recent last
+    return ent[1][:depth]
+
+
+def release_solvers(device: int, solvers) -> None:
+    """Give a leased solver set back to the calling thread's pool."""
+    for ent in getattr(_tls, "pipes", {}).get(device, []):
+        if ent[1][:len(solvers)] == list(solvers):
+            ent[0] = False
+            return
 
 
 _dev_locks = {}

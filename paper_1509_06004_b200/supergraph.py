@@ -424,15 +424,16 @@ def solve_seed_supergraphs(batches, schedule: LambdaSchedule, swap_mode: str = "
     (D2H, label unpack, CutResults) while batch k + 1 runs.  An error of
     batch k is raised when its result is due; the stream ends there.  The
     serving analogue of run_dynamic's per-worker slots
-    (scheduler.py:253-292, harness/bench.py:79-93); a stream owns its device
-    (no concurrent solves on it from other threads)."""
+    (scheduler.py:253-292, harness/bench.py:79-93).  A stream owns its
+    solvers (nested streams of one thread lease separate ones) and expects
+    no concurrent solves on its device from other threads."""
     import queue
 
     from . import _native
     from .synth_device import ImageBatch, stage_image_batch
     if depth < 2:
         raise ValueError("depth must be >= 2")
-    solvers = _native.pipeline_solvers(device, depth + 1)
+    solvers = _native.pipeline_solvers(device, depth + 1, lease=True)
     mixed = solvers[depth]   # mixed-width batches, solved synchronously by the stager
     free = [threading.Semaphore(1) for _ in range(depth)]
     to_fetch = queue.Queue()
@@ -500,3 +501,4 @@ def solve_seed_supergraphs(batches, schedule: LambdaSchedule, swap_mode: str = "
         th.join()
         for s in solvers:   # a run launched but never waited for (stream closed early)
             s.abandon()
+        _native.release_solvers(device, solvers)

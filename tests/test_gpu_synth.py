@@ -138,3 +138,17 @@ def test_launch_wait_contract():
     finally:
         a.close()
         b.close()
+
+
+def test_nested_streams_use_separate_solvers():
+    """A stream consumed inside another stream's loop (same thread) leases
+    its own solvers: both yield what the single calls return."""
+    sched = LambdaSchedule(synth.L20[:4])
+    outer = [_host(96, 64, 1, 2, (s,), ("A",)) for s in (1, 2)]
+    inner = [sd.generate_images(96, 64, 1, 2, rng_seeds=(s,)) for s in (3, 4)]
+    want_o = [solve_seed_supergraph(b, sched) for b in outer]
+    want_i = [sd.solve_image_batch(b, sched) for b in inner]
+    for k, ro in enumerate(solve_seed_supergraphs(outer, sched)):
+        _same(ro, want_o[k])
+        for j, ri in enumerate(solve_seed_supergraphs(inner, sched)):
+            _same(ri, want_i[j])

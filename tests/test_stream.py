@@ -63,7 +63,8 @@ def _batch(tag):
 def fake_engine(monkeypatch):
     FakeSolver.log = []
     solvers = [FakeSolver(i) for i in range(4)]
-    monkeypatch.setattr(_native, "pipeline_solvers", lambda device, depth: solvers[:depth])
+    monkeypatch.setattr(_native, "pipeline_solvers", lambda device, depth, lease=False: solvers[:depth])
+    monkeypatch.setattr(_native, "release_solvers", lambda device, s: None)
     return solvers
 
 
