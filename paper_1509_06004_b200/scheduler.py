@@ -13,7 +13,9 @@ the device ordinal).  ``GpuBackend`` gives each device one executor thread
 with its own solver/stream; tasks dispatched to a device while it is busy
 are coalesced into the next device batch (every grid of every coalesced
 supergraph is discharged by the same kernel launches), so ``slots`` tokens
-per GPU become batch depth instead of idle threads.  CUDA errors surface as
+per GPU become batch depth instead of idle threads (composite tasks share
+one device batch; seed-supergraph tasks run as a batch stream whose host
+staging and decoding overlap the device).  CUDA errors surface as
 ``WorkerFailure`` and go through the reference's retry path.
 """
 
@@ -27,7 +29,8 @@ from concurrent.futures import FIRST_COMPLETED, ThreadPoolExecutor, wait as futu
 from dataclasses import dataclass
 
 from .grid import CutResult, GridGraph
-from .supergraph import SupergraphLayout, solve_composite, solve_composites, solve_seed_supergraph
+from .supergraph import (SupergraphLayout, solve_composite, solve_composites, solve_seed_supergraph,
+                         solve_seed_supergraphs)
 
 
 class SchedulerError(RuntimeError):
@@ -226,9 +229,22 @@ class GpuBackend:
             for i, r in zip(comp, solve_composites([(tasks[i].graph, tasks[i].layout)
                                                     for i in comp], device=dev)):
                 out[i] = r
+        # seed supergraphs: one batch stream per (schedule, swap mode), so the
+        # admission / staging of task k+1 and the decode of task k-1 overlap
+        # the device solve of task k (an error fails the coalesced batch,
+        # which _loop then re-solves task by task)
+        groups = {}
         for i, t in enumerate(tasks):
             if t.problems is not None:
-                out[i] = _solve_one(t, dev)
+                groups.setdefault((tuple(t.schedule.values), t.swap_mode), []).append(i)
+        for idx in groups.values():
+            if len(idx) == 1:
+                out[idx[0]] = _solve_one(tasks[idx[0]], dev)
+                continue
+            t0 = tasks[idx[0]]
+            for i, res in zip(idx, solve_seed_supergraphs([tasks[i].problems for i in idx], t0.schedule,
+                                                          t0.swap_mode, device=dev)):
+                out[i] = res
         return out
 
     def submit(self, worker: WorkerHandle, task: Task, attempt: int = 1) -> None:

@@ -493,6 +493,28 @@ def test_run_dynamic_on_gpu_backend():
         assert all(np.array_equal(a.labels, c.labels) for a, c in zip(dev.cuts, parts))
 
 
+def test_run_dynamic_streams_coalesced_seed_tasks():
+    """Seed-supergraph tasks coalesced on one GPU run as a batch stream
+    (GpuBackend._run_batch -> solve_seed_supergraphs); every task's result
+    equals the direct call, a task with another schedule forms its own group."""
+    from paper_1509_06004_b200 import GpuBackend, Task, gpu_workers, run_dynamic
+    sched, other = LambdaSchedule(synth.L20[:5]), LambdaSchedule(synth.L20[2:6])
+    probs = [synth.generate(120, 90, 1, 2, rng_seed=s, types=("A", "B")).problems for s in range(6)]
+    tasks = [Task(id=i, problems=tuple(p), schedule=sched if i != 4 else other) for i, p in enumerate(probs)]
+    backend = GpuBackend(max_batch=6)
+    try:
+        schedule, cuts = run_dynamic(tasks, gpu_workers([0], slots=6), backend)
+    finally:
+        backend.close()
+    assert sorted(r.task_id for r in schedule.records) == list(range(6))
+    for t in tasks:
+        want = solve_seed_supergraph(list(t.problems), t.schedule)
+        got = cuts[t.id]
+        assert got.layout == want.layout
+        assert [c.flow for c in got.cuts] == [c.flow for c in want.cuts]
+        assert all(np.array_equal(a.labels, b.labels) for a, b in zip(got.cuts, want.cuts))
+
+
 @pytest.mark.parametrize("mode", [1, 0])
 def test_seed_batches_on_edge_shapes(engine, mode):
     """Seed batches through the device builder on odd shapes (1xN, Nx1,
