@@ -7,7 +7,6 @@ gpurun_out/ (and copy the bench lines gpurun_out/<tag>_bench*.json).
 import csv
 import json
 import os
-import shutil
 import subprocess
 import sys
 
@@ -49,8 +48,8 @@ lt = [f"# {TAG} launch lists (ncu --metrics gpu__time_duration.sum,dram__bytes_r
       f"Command: scripts/ncu_r02c.sh {TAG} (scripts/probe.py; step-synchronous batches with --graph 0 so "
       "every kernel is a separate launch).\n"]
 lists = {}
-for f, desc in (("c5", "C5 batch: 16 CPMC images (rng_seed 0..15), host-staged planes, step-synchronous"),
-                ("c5s", "C5 batch: the same 16 images, planes derived on the device (pmf_synth_stage)"),
+for f, desc in (("c5", "C5 batch: 32 CPMC images (rng_seed 0..31), host-staged planes, step-synchronous"),
+                ("c5s", "C5 batch: the same 32 images, planes derived on the device (pmf_synth_stage)"),
                 ("c3", "C3: one CPMC image (rng_seed 0), asynchronous solver"),
                 ("c2", "C2: 500x375, 20 lambdas, asynchronous solver")):
     path = os.path.join(G, f"{TAG}_launches_{f}.csv")
@@ -79,7 +78,7 @@ open(os.path.join(P, f"{TAG}_launches.md"), "w").write("\n".join(lt) + "\n")
 out = {}
 for f, k, desc in (("c2", "k_async", "C2 (500x375, 20 lambdas, one supergraph)"),
                    ("c3", "k_async", "C3 (one CPMC image, 1000 lambda-graphs)"),
-                   ("c5", "k_push", "C5 batch (16 images, step-synchronous mode)")):
+                   ("c5", "k_push", "C5 batch (32 images, step-synchronous mode)")):
     if f in lists:
         b, n, _ = per_kernel(lists[f], k)
         out.setdefault(k, {})[f] = {"dram_bytes_per_launch": b, "launches": n, "workload": desc}
@@ -101,10 +100,10 @@ lines = [f"# {TAG} ncu --set full captures (--clock-control none --import-source
          "(C5), `k_bfs_sink` = exact global relabel, `k_async` = the asynchronous solve kernel (one launch "
          "solves the batch, C2/C3), `k_synth_*` / `k_pack_bits` = on-device synthesis and output packing "
          "(plain streaming kernels: their DRAM throughput is the HBM roofline).\n"]
-for f, desc in ((f"{TAG}_k_push_c5", "k_push (9th launch), C5 batch of 16 images"),
-                (f"{TAG}_k_bfs_c5", "k_bfs_sink (41st launch), C5 batch of 16 images"),
+for f, desc in ((f"{TAG}_k_push_c5", "k_push (9th launch), C5 batch of 32 images"),
+                (f"{TAG}_k_bfs_c5", "k_bfs_sink (41st launch), C5 batch of 32 images"),
                 (f"{TAG}_k_async_c3", "k_async, C3 (one CPMC image: 50 warm-start chains x 20 lambdas)"),
-                (f"{TAG}_k_synth_c5", "on-device synthesis + packing, C5 batch of 16 images")):
+                (f"{TAG}_k_synth_c5", "on-device synthesis + packing, C5 batch of 32 images")):
     rep = os.path.join(G, f + ".ncu-rep")
     if not os.path.exists(rep):
         continue
@@ -127,9 +126,9 @@ for f, desc in ((f"{TAG}_k_push_c5", "k_push (9th launch), C5 batch of 16 images
         if row:
             d = dict(zip(rr[0], row))
             try:
-                b = float(d["dram__bytes_read.sum"]) * 1e0 + float(d["dram__bytes_write.sum"])
-                u = rr[1][rr[0].index("dram__bytes_read.sum")]
-                lines.append(f"| dram bytes (read + write) | {b:.3f} {u} |")
+                b = sum(float(d[m].replace(",", "")) * SCALE.get(rr[1][rr[0].index(m)], 1)
+                        for m in ("dram__bytes_read.sum", "dram__bytes_write.sum"))
+                lines.append(f"| dram bytes (read + write) | {b / 1e6:.3f} MB |")
             except (KeyError, ValueError):
                 pass
             st = {}
