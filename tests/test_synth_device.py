@@ -78,3 +78,32 @@ def test_image_batch_validation():
         sd.ImageBatch(np.zeros((1, 4, 4), np.uint8), [(0, 1)]).families()
     # type B: the top row is not background
     assert len(sd.ImageBatch(np.zeros((1, 4, 4), np.uint8), [(1, 0)], types=("B",)).families()) == 1
+
+
+def test_admission_order_across_images_and_types():
+    """The first failing (image, seed, type) problem decides the error, as
+    check_seed_supergraph on the host problems in the same order."""
+    sched = LambdaSchedule((1, 700, 140000))
+    b = sd.generate_images(64, 48, 2, 2, rng_seeds=(5, 6, 7), types=("B", "A"))
+    host = []
+    for s in (5, 6, 7):
+        host += synth.generate(64, 48, 2, 2, rng_seed=s, types=("B", "A")).problems
+    outcome = []
+    for probs in (host, b.families()):
+        try:
+            check_seed_supergraph(probs, sched, "auto")
+            outcome.append(None)
+        except Exception as exc:  # noqa: BLE001
+            outcome.append((type(exc), str(exc)))
+    assert outcome[0] == outcome[1]
+
+
+def test_tiny_images():
+    """3x3 images: one interior pixel, the seed; the border is background
+    (type A) or the ring minus its top row (type B)."""
+    b = sd.ImageBatch(np.array([[[0, 9, 2], [3, 40, 5], [6, 7, 255]]], np.uint8), [(1, 1)], ("A", "B"))
+    fa, fb = b.families()
+    assert fa.n == 9 and len(fa.bg_seeds) == 8 and len(fb.bg_seeds) == 5
+    for f in (fa, fb):
+        p = f.problem()
+        assert f._family_stats() == p._family_stats()
