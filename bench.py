@@ -529,6 +529,27 @@ class _Null:
         return False
 
 
+def c2_per_lambda(dev):
+    """Critical path of C2 (one supergraph, 20 cold lambda-graphs solved in
+    parallel by the asynchronous solver): per lambda-graph the exact global
+    relabels and discharge phases it needed and when it finished (device
+    phase log of one untimed solve of pool image 0)."""
+    from paper_1509_06004_b200 import LambdaSchedule, _native
+    cfg = CONFIGS["c2"]
+    sched = LambdaSchedule(lambdas_for(cfg["lams"]))
+    s = _native.Solver(dev, phase_log=1)
+    try:
+        s.solve_seed_batch(cfg["w"], cfg["h"], batch_problems(cfg, 0, sched), sched.values, "auto")
+        out = []
+        for g, lam in enumerate(sched.values):
+            ph = s.phases(g)
+            out.append({"lambda": int(lam), "global_relabels": sum(1 for n, _ in ph if n == "bfs"),
+                        "discharges": sum(1 for n, _ in ph if n == "push"), "finish_us": ph[-1][1]})
+        return {"device_ms": round(s.stats()["ms_device"], 3), "image": 0, "lambdas": out}
+    finally:
+        s.close()
+
+
 def run_b200(args, cfg):
     import torch
     import torch.distributed as dist
@@ -592,6 +613,7 @@ def run_b200(args, cfg):
                         "single_call": {"value": k / s2["e2e_s"],
                                         "ms_per_image": 1e3 * s2["e2e_s"] / st_ / c["images"]}},
                 "roofline": roofline_of(s2["stats"], st_, name)}
+        secondary["c2"]["per_lambda"] = c2_per_lambda(dev)
 
     if rank == 0:
         line = {

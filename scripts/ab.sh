@@ -10,7 +10,7 @@ for arm in "$@"; do
   ks=""; for kv in $arm; do ks="$ks --knob $kv"; done
   for cfg in "${CL[@]}"; do
     echo "== [$arm] $cfg"
-    timeout 300 python scripts/probe.py $cfg --reps 5 $ks 2>&1 | tail -1 | python -c "
+    timeout 300 python scripts/probe.py $cfg --reps ${REPS:-5} $ks 2>&1 | tail -1 | python -c "
 import json,sys
 d=json.loads(sys.stdin.read()); print({k:d[k] for k in ('med_dev_ms','flow','cycles','push_tile_passes','bfs_tile_passes','label_tile_passes','ms_push','ms_bfs','ms_labels','ms_async')})"
   done
