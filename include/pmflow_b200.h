@@ -249,6 +249,14 @@ int pmf_synth_stage(pmf_solver *s, int32_t nimg, int32_t width, int32_t height, 
  * buffers to read the sizes (*n_planes, *n_pw, in int32 elements). */
 int pmf_debug_planes(pmf_solver *s, int32_t *planes_out, int64_t *n_planes, int32_t *pw_out, int64_t *n_pw);
 int pmf_seed_launch(pmf_solver *s, pmf_solver *after);
+/* Extra ordering for a batch stream: the next run of s starts only after
+ * `on`'s last launched run (any number of calls before pmf_seed_launch). */
+int pmf_solver_depend(pmf_solver *s, pmf_solver *on);
+/* Kind of the staged batch's run and of the solver's last launched run:
+ * 1 = asynchronous solver (one non-cooperative persistent kernel whose idle
+ * CTAs may leave its tail to a concurrent run, knob async_yield_us), 0 =
+ * step-synchronous graph (cooperative launches: must not share the GPU). */
+int pmf_seed_kind(pmf_solver *s, int32_t *staged_async, int32_t *last_async);
 int pmf_seed_wait(pmf_solver *s);
 int pmf_seed_fetch(pmf_solver *s, uint8_t *swapped_out, int64_t *flows_out, uint8_t *labels_out);
 

@@ -25,7 +25,7 @@ SWAP_MODES = {"auto": 0, "on": 1, "off": 2}
 EXPORTS = ("pmf_solver_create", "pmf_solver_destroy", "pmf_solver_set", "pmf_last_error",
            "pmf_solver_stats", "pmf_solver_stream", "pmf_solve_composites", "pmf_solve_seed_batch",
            "pmf_seed_stage", "pmf_seed_run", "pmf_seed_launch", "pmf_seed_wait", "pmf_seed_fetch",
-           "pmf_synth_stage", "pmf_debug_planes",
+           "pmf_synth_stage", "pmf_debug_planes", "pmf_solver_depend", "pmf_seed_kind",
            "pmf_debug_state",
            "pmf_debug_trace", "pmf_debug_busy", "pmf_seed_score", "pmf_debug_phases",
            "pmf_solve_composites_i32", "pmf_composite_bits", "pmf_plane_stats")
@@ -87,6 +87,8 @@ def load_library(path: str = LIB_PATH):
             i32, P(i64), i32]
         lib.pmf_seed_run.argtypes = [vp]
         lib.pmf_seed_launch.argtypes = [vp, vp]
+        lib.pmf_solver_depend.argtypes = [vp, vp]
+        lib.pmf_seed_kind.argtypes = [vp, P(i32), P(i32)]
         lib.pmf_debug_planes.argtypes = [vp, P(i32), P(i64), P(i32), P(i64)]
         lib.pmf_synth_stage.argtypes = [vp, i32, i32, i32, P(u8), i32, P(i32), i32, P(i32), i32, P(i64), i32]
         lib.pmf_seed_wait.argtypes = [vp]
@@ -373,6 +375,20 @@ class Solver:
         if rc:
             _raise_for(rc)
         self._launched = True
+
+    def depend(self, other):
+        """The next launched run starts after ``other``'s last launched run."""
+        rc = self._lib.pmf_solver_depend(self._h, other._h)
+        if rc:
+            _raise_for(rc)
+
+    def seed_kind(self):
+        """(staged batch runs asynchronously, last launched run was asynchronous)."""
+        a, b = ctypes.c_int32(), ctypes.c_int32()
+        rc = self._lib.pmf_seed_kind(self._h, ctypes.byref(a), ctypes.byref(b))
+        if rc:
+            _raise_for(rc)
+        return bool(a.value), bool(b.value)
 
     def seed_wait(self):
         """Block until the launched run is done (device errors raised here)."""

@@ -40,7 +40,8 @@ __host__ __device__ constexpr bool scan_phase(int ph) {
 }
 // extra pass counters (Ctx::stat) of the scan phases
 enum { ST_BINIT = 9, ST_SEED = 10, ST_LINIT = 11, ST_EMIT = 12, ST_LAMS = 13, ST_ASYNC_NS = 14,
-       ST_SPEC = 32, ST_SPOILED = 33 };   // speculative label closures tried / spoiled
+       ST_SPEC = 32, ST_SPOILED = 33,    // speculative label closures tried / spoiled
+       ST_YIELDED = 37 };                // CTAs that left an idle tail early
 // CTA-busy nanoseconds per phase kind (ST_BUSY + PH_*), then queue wait,
 // hand-off (requests + retire) and grid transitions
 constexpr int ST_BUSY = 16;
@@ -73,6 +74,11 @@ struct AsyncArgs {
     int32_t prefetch;  // take the next ticket while the queue is deep
     int32_t spec;      // a drained discharge goes straight to a speculative label closure
     int32_t keep_h;    // unswapped grids enter the next lambda with their current heights
+    // CTAs with blockIdx >= yield_keep leave the kernel after yield_ns of an
+    // empty queue (no ticket held), so a concurrent run gets their SM slots
+    // in this run's latency-bound tail (0: never)
+    unsigned long long yield_ns;
+    int32_t yield_keep;
     unsigned long long *plog;   // diagnostics (nullable): per grid PLOG entries (phase << 56 | globaltimer)
 };
 constexpr int PLOG = 512;
@@ -477,7 +483,23 @@ __global__ void __launch_bounds__(NTT, 2) k_async(Ctx c, AsyncArgs A) {
             const unsigned long long tw = gtimer();
             int32_t t = s_cont;
             s_cont = -1;
-            if (t < 0) {
+            if (t < 0 && pre == ~0u && A.yield_ns && int(blockIdx.x) >= A.yield_keep) {
+                // idle without a ticket: wait for queued work without taking
+                // one; after yield_ns leave the SM to a concurrent run
+                const unsigned long long t_idle = gtimer();
+                for (;;) {
+                    if (ld_volatile(&c.qctr[QC_TAIL]) > ld_volatile(&c.qctr[QC_HEAD])) break;
+                    if (ld_volatile(&c.qctr[QC_PENDING]) == 0) break;
+                    if (gtimer() - t_idle > A.yield_ns) {
+                        t = -2;
+                        break;
+                    }
+                    __nanosleep(256);
+                }
+            }
+            if (t == -2) {
+                atomicAdd(&c.stat[ST_YIELDED], 1ull);
+            } else if (t < 0) {
                 t = pre != ~0u ? q_wait(c, pre) : q_next(c);
                 pre = ~0u;
             }

@@ -234,6 +234,9 @@ struct pmf_solver {
     int async_max_tiles = 20000;
     int async_max_grid_tiles = 1024;   // ... and grids of at most this many tiles on average
     int async_cont = 1, async_prefetch = 1;
+    int async_yield_us = 0;     // asynchronous solver: idle CTAs leave an empty-queue tail after this (0 never)
+    int async_yield_keep = 0;   // ... except the first this many CTAs (0: a quarter of the grid)
+    bool last_async = false;    // the last launched seed run was asynchronous (no cooperative kernels)
     int async_spec = 1;         // drained discharge -> speculative label closure instead of a confirming relabel
     int adv_keep_h = 1;         // async: unswapped grids enter the next lambda without a relabel
     int phase_log = 0;          // diagnostics: record every grid's phase timeline (async)
@@ -1137,6 +1140,8 @@ int async_solve(pmf_solver *s, const Ctx &c0, const SeedArgs &sa) {
     A.prefetch = s->async_prefetch;
     A.spec = s->async_spec;
     A.keep_h = s->adv_keep_h && s->async_spec;   // kept heights need the speculative closure
+    A.yield_ns = (unsigned long long)s->async_yield_us * 1000ull;
+    A.yield_keep = s->async_yield_keep ? s->async_yield_keep : std::max(1, s->grid_push / 4);
     if (s->phase_log) {
         if ((rc = s->d_plog.ensure(size_t(G) * PLOG * 8))) return rc;
         CK(cudaMemsetAsync(s->d_plog.p, 0, size_t(G) * PLOG * 8, s->st));
@@ -1194,6 +1199,15 @@ int seed_swap_flags(pmf_solver *s, const SeedArgs &a) {
     return 0;
 }
 
+// The staged seed batch runs on the asynchronous solver (one persistent,
+// non-cooperative kernel) rather than the step-synchronous graph.
+bool seed_uses_async(const pmf_solver *s) {
+    if (s->stage.wide) return false;
+    const int64_t ngr = std::max<int64_t>(1, int64_t(s->lay.grids.size()));
+    return s->async_mode == 1 || (s->async_mode < 0 && s->lay.ntiles <= s->async_max_tiles &&
+                                  s->lay.ntiles <= int64_t(s->async_max_grid_tiles) * ngr);
+}
+
 // Host-side preparation of a run: launch geometry, device state and the
 // layout uploads (pageable copies: issued before a batch stream's wait on
 // the previous run, so the launch does not block on it)
@@ -1226,11 +1240,7 @@ int seed_run_t(pmf_solver *s) {
     // asynchronous solver for latency-bound batches; large batches keep the
     // GPU full with step-synchronous phases, whose wide scan kernels and
     // multi-sweep relabels cost less per tile than queued tile tasks
-    const int64_t ngr = std::max<int64_t>(1, int64_t(s->lay.grids.size()));
-    const bool use_async = s->async_mode == 1 ||
-                           (s->async_mode < 0 && s->lay.ntiles <= s->async_max_tiles &&
-                            s->lay.ntiles <= int64_t(s->async_max_grid_tiles) * ngr);
-    if (use_async) {
+    if (seed_uses_async(s)) {
         if ((rc = async_solve<E>(s, c, a))) return rc;
         if (s->verify && (rc = launch_verify<E>(s, c, a))) return rc;
         return 0;
@@ -1972,6 +1982,8 @@ int pmf_solver_set(pmf_solver *s, const char *name, int64_t v) {
     else if (k == "comp_split") s->comp_split = v != 0;
     else if (k == "rolling") s->rolling = v != 0;
     else if (k == "push_flush" && v >= 0 && v <= 1024) s->push_flush = int(v);
+    else if (k == "async_yield_us" && v >= 0 && v <= 1000000) s->async_yield_us = int(v);
+    else if (k == "async_yield_keep" && v >= 0 && v <= 100000) s->async_yield_keep = int(v);
     else if (k == "fresh_skip") s->fresh_skip = v != 0;
     else if (k == "async" && v >= -1 && v <= 1) s->async_mode = int(v);
     else if (k == "async_max_tiles" && v >= 0) s->async_max_tiles = int(std::min<int64_t>(v, 1 << 30));
@@ -2417,6 +2429,28 @@ int pmf_seed_launch(pmf_solver *s, pmf_solver *after) {
     if (!s->ev_tail) CK(cudaEventCreateWithFlags(&s->ev_tail, cudaEventDisableTiming));
     CK(cudaEventRecord(s->ev_tail, s->st));
     s->launched = true;
+    s->last_async = seed_uses_async(s);
+    return 0;
+}
+
+// The next run of s starts only after `on`'s last launched run (recorded
+// before pmf_seed_launch; any number of calls).
+int pmf_solver_depend(pmf_solver *s, pmf_solver *on) {
+    if (!s || !on || on == s) return fail(PMF_ERR_ARG, "bad arguments");
+    if (on->device != s->device) return fail(PMF_ERR_ARG, "solvers on different devices");
+    CK(cudaSetDevice(s->device));
+    if (on->ev_tail) CK(cudaStreamWaitEvent(s->st, on->ev_tail, 0));
+    return 0;
+}
+
+// Run kind of the staged batch (1: asynchronous solver, a single
+// non-cooperative persistent kernel that may share the device with another
+// such run; 0: step-synchronous graph with cooperative launches) and of the
+// solver's last launched run.
+int pmf_seed_kind(pmf_solver *s, int32_t *staged_async, int32_t *last_async) {
+    if (!s || !s->stage.valid) return fail(PMF_ERR_ARG, "no staged seed batch");
+    if (staged_async) *staged_async = seed_uses_async(s) ? 1 : 0;
+    if (last_async) *last_async = s->last_async ? 1 : 0;
     return 0;
 }
 

@@ -407,7 +407,7 @@ def solve_seed_supergraph(problems, schedule: LambdaSchedule, swap_mode: str = "
 
 
 def solve_seed_supergraphs(batches, schedule: LambdaSchedule, swap_mode: str = "auto",
-                           device: int = 0, truths=None, depth: int = 3):
+                           device: int = 0, truths=None, depth: int = 3, overlap_us: int = 20):
     """Stream of seed supergraphs through one device: yields, in order, what
     ``solve_seed_supergraph(batch, schedule, swap_mode, device, truths_k)``
     returns for each batch (a list of problems, or a synth_device.ImageBatch
@@ -424,7 +424,14 @@ def solve_seed_supergraphs(batches, schedule: LambdaSchedule, swap_mode: str = "
     (D2H, label unpack, CutResults) while batch k + 1 runs.  An error of
     batch k is raised when its result is due; the stream ends there.  The
     serving analogue of run_dynamic's per-worker slots
-    (scheduler.py:253-292, harness/bench.py:79-93).  A stream owns its
+    (scheduler.py:253-292, harness/bench.py:79-93).
+
+    ``overlap_us`` (0: off): two consecutive batches that both run on the
+    asynchronous solver (small batches, C1-C3) may share the device -- the
+    later run starts once the one before the previous has finished, and the
+    idle CTAs of a run's latency-bound tail leave the SM to it after that
+    many microseconds of an empty queue (knob async_yield_us).  Step-
+    synchronous runs (cooperative launches) never share the device.  A stream owns its
     solvers (nested streams of one thread lease separate ones) and expects
     no concurrent solves on its device from other threads."""
     import queue
@@ -435,6 +442,19 @@ def solve_seed_supergraphs(batches, schedule: LambdaSchedule, swap_mode: str = "
         raise ValueError("depth must be >= 2")
     solvers = _native.pipeline_solvers(device, depth + 1, lease=True)
     mixed = solvers[depth]   # mixed-width batches, solved synchronously by the stager
+    for sv in solvers:
+        sv.set("async_yield_us", overlap_us)
+
+    def launch(sv, prev):
+        """Launch sv's staged run behind every other solver's last run --
+        except the previous one when both runs are asynchronous (they may
+        share the device)."""
+        share = (overlap_us > 0 and prev is not None and prev is not sv and sv.seed_kind()[0]
+                 and prev.seed_kind()[1])
+        for o in solvers:
+            if o is not sv and not (share and o is prev):
+                sv.depend(o)
+        sv.seed_launch(None)
     free = [threading.Semaphore(1) for _ in range(depth)]
     to_fetch = queue.Queue()
     stop = threading.Event()
@@ -463,7 +483,7 @@ def solve_seed_supergraphs(batches, schedule: LambdaSchedule, swap_mode: str = "
                             _stage_checked(sv, probs, schedule, swap_mode)
                             item = ("ok", (probs, _layout_skeleton(probs, schedule)), tr)
                     if item[0] == "ok":
-                        sv.seed_launch(prev)
+                        launch(sv, prev)
                         prev = sv
                 except BaseException as exc:  # noqa: BLE001 -- raised by the consumer
                     item = ("err", exc, None)

@@ -54,7 +54,7 @@ for rep in range(2):
     log.clear()
     t0 = time.perf_counter()
     ys = []
-    for r in solve_seed_supergraphs(bs, sched):
+    for r in solve_seed_supergraphs(bs, sched, overlap_us=int(os.environ.get("OVERLAP", 20))):
         ys.append(time.perf_counter())
         del r
     T = time.perf_counter() - t0

@@ -152,3 +152,16 @@ def test_nested_streams_use_separate_solvers():
         _same(ro, want_o[k])
         for j, ri in enumerate(solve_seed_supergraphs(inner, sched)):
             _same(ri, want_i[j])
+
+
+def test_overlapping_async_runs_in_a_stream():
+    """Consecutive asynchronous runs share the device (overlap_us: idle CTAs
+    of a run's tail leave their SM to the next run; 1 us = aggressive
+    yielding): every batch still equals its single call, and overlap off
+    gives the same results."""
+    sched = LambdaSchedule(synth.L20[:8])
+    batches = [_host(160, 120, 1, 2, (s,), ("A", "B")) for s in range(10)]
+    want = [solve_seed_supergraph(b, sched) for b in batches]
+    for ov in (1, 20, 0):
+        for g, w in zip(solve_seed_supergraphs(batches, sched, overlap_us=ov), want):
+            _same(g, w)

@@ -27,13 +27,25 @@ class FakeSolver:
         self.slot = slot
         self.staged = None
         self.end = 0.0
+        self.deps = []
 
     def seed_stage(self, W, H, problems, lambdas, swap_mode):
         FakeSolver.log.append(("stage", problems[0].tag, time.perf_counter(), None))
         self.staged = (W * H, problems, len(lambdas))
 
+    def set(self, name, value):
+        pass
+
+    def seed_kind(self):
+        return False, False   # step-synchronous runs: never share the device
+
+    def depend(self, other):
+        self.deps.append(other)
+
     def seed_launch(self, after=None):
-        start = max(time.perf_counter(), after.end if after is not None else 0.0)
+        deps = self.deps + ([after] if after is not None else [])
+        self.deps = []
+        start = max([time.perf_counter()] + [d.end for d in deps])
         self.end = start + FakeSolver.RUN_S
         FakeSolver.log.append(("run", self.staged[1][0].tag, start, self.end))
 
