@@ -2012,16 +2012,43 @@ int pmf_solver_set(pmf_solver *s, const char *name, int64_t v) {
 int pmf_plane_stats(int32_t nplanes, const int64_t *const *planes, const int64_t *sizes, int64_t *out) {
     if (nplanes < 0 || (nplanes && (!planes || !sizes || !out))) return fail(PMF_ERR_ARG, "bad arguments");
     int nt = int(std::max(1u, std::min(std::thread::hardware_concurrency(), 16u)));
+    if (const char *lw = getenv("LOCAL_WORLD_SIZE")) {   // host cores shared by the local ranks
+        const int n = atoi(lw);
+        if (n > 1) nt = std::max(1, nt / n);
+    }
+    // tasks of <= 2^20 elements (a few large planes still use every thread)
+    constexpr int64_t kStat = int64_t(1) << 20;
+    std::vector<int64_t> first(size_t(nplanes) + 1, 0);
+    for (int32_t k = 0; k < nplanes; k++) first[k + 1] = first[k] + std::max<int64_t>(1, cdiv(sizes[k], kStat));
+    const int64_t ntask = first[nplanes];
+    std::vector<int64_t> part(size_t(ntask) * 4);
 #pragma omp parallel for schedule(dynamic, 1) num_threads(nt)
-    for (int32_t k = 0; k < nplanes; k++) {
+    for (int64_t task = 0; task < ntask; task++) {
+        const int32_t k = int32_t(std::upper_bound(first.begin(), first.end(), task) - first.begin() - 1);
+        const int64_t lo = (task - first[k]) * kStat, hi = std::min(sizes[k], lo + kStat);
         const int64_t *a = planes[k];
         int64_t mn = 0, mx = 0, sum = 0, fin = 0;   // initial=0 semantics of numpy min/max
-        for (int64_t i = 0; i < sizes[k]; i++) {
+        for (int64_t i = lo; i < hi; i++) {
             const int64_t v = a[i];
             mn = std::min(mn, v);
             mx = std::max(mx, v);
             sum += v;
             fin += v < CAP_MAX ? v : 0;
+        }
+        int64_t *o = part.data() + 4 * task;
+        o[0] = mn;
+        o[1] = mx;
+        o[2] = sum;
+        o[3] = fin;
+    }
+    for (int32_t k = 0; k < nplanes; k++) {
+        int64_t mn = 0, mx = 0, sum = 0, fin = 0;
+        for (int64_t t = first[k]; t < first[k + 1]; t++) {
+            const int64_t *o = part.data() + 4 * t;
+            mn = std::min(mn, o[0]);
+            mx = std::max(mx, o[1]);
+            sum += o[2];
+            fin += o[3];
         }
         out[4 * k + 0] = mn;
         out[4 * k + 1] = mx;

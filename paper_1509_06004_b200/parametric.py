@@ -248,8 +248,8 @@ def prefetch_family_stats(problems) -> None:
             if key not in seen:
                 seen.add(key)
                 todo.append((a, hw))
-    if len(todo) < 8:
-        return
+    if len(todo) < 8 and sum(a.size for a, _ in todo) < (1 << 20):
+        return   # a few small planes: numpy is quicker than a native pool round trip
     try:
         from ._native import plane_stats
         red = plane_stats([a for a, _ in todo])

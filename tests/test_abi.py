@@ -76,3 +76,17 @@ def _check_missing(native, tmp_path):
         native.load_library(str(tmp_path / "nope.so"))
     finally:
         native._lib = saved
+
+
+def test_plane_stats_host_reduction(lib):
+    """pmf_plane_stats (host only, no GPU): chunked OpenMP reductions equal
+    numpy's min / max (initial=0) / sum / sum below CAP_MAX, across chunk
+    boundaries and for empty planes."""
+    import numpy as np
+    from paper_1509_06004_b200 import _native
+    rng = np.random.default_rng(0)
+    planes = [rng.integers(-5, 1 << 31, size=n) for n in (0, 1, 1000, (1 << 20) + 7, 3 * (1 << 20))]
+    planes[3][5] = 1 << 30
+    for a, (mn, mx, sm, fin) in zip(planes, _native.plane_stats(planes)):
+        assert (mn, mx, sm) == (int(a.min(initial=0)), int(a.max(initial=0)), int(a.sum()))
+        assert fin == int(a[a < (1 << 30)].sum())
