@@ -26,6 +26,9 @@ def batch(b):
     return out
 
 
+for kv in filter(None, os.environ.get("KNOBS", "").split(",")):   # e.g. KNOBS=async=1
+    k_, v_ = kv.split("=")
+    _native.configure(**{k_: int(v_)})
 log = []
 for name in ("seed_stage", "synth_stage", "seed_launch", "seed_wait", "seed_fetch") if os.environ.get("TRACE") else ():
     orig = getattr(_native.Solver, name)
