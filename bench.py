@@ -369,7 +369,7 @@ def roofline_of(stats, steps, config):
                 "avg_launch_us": kern_ms * 1e3 / steps,
                 "time_share": {"k_async": round(kern_ms / total_ms, 4) if total_ms else None},
                 "limiter": "latency / issue, not HBM: working set L2-resident (profiles/r02f_ncu_full.md: "
-                           "k_async C3 DRAM 0.9 %, issue slots 44 %, 36 % of stall samples idle CTAs "
+                           "k_async C3 DRAM 0.9 %, issue slots 46 %, barrier 52 % of stall samples, most of it idle CTAs "
                            "waiting for work in the single-image tail)"}
     push_ms = sum(s["ms_push"] for s in stats)
     launches = max(1, sum(s["push_sweeps"] for s in stats))
