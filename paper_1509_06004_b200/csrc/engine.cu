@@ -234,6 +234,7 @@ struct pmf_solver {
     int async_max_tiles = 20000;
     int async_max_grid_tiles = 1024;   // ... and grids of at most this many tiles on average
     int async_cont = 1, async_prefetch = 1;
+    int nested_lab = 1;         // rolling step mode: seed label closures with the previous lambda's source side
     int async_yield_us = 0;     // asynchronous solver: idle CTAs leave an empty-queue tail after this (0 never)
     int async_yield_keep = 0;   // ... except the first this many CTAs (0: a quarter of the grid)
     bool last_async = false;    // the last launched seed run was asynchronous (no cooperative kernels)
@@ -251,7 +252,7 @@ struct pmf_solver {
     int wide_pulses = 64;       // int64 variant: lock-step pulses between exact global relabels
     int64_t wide_cycles = 0, wide_pulses_run = 0, wide_relax_launches = 0;   // ... of the last wide run
     // device workspace
-    DevBuf d_w, d_h, d_r, d_lab, d_tile_grid, d_tnb, d_fin, d_gpend, d_specg, d_keeph, d_seeds, d_sofs, d_gr, d_tflag, d_vacc, d_truth, d_score, d_plog, d_tfresh, d_grids, d_live, d_act, d_list, d_inq, d_cnt,
+    DevBuf d_w, d_h, d_r, d_lab, d_tile_grid, d_tnb, d_fin, d_gpend, d_specg, d_keeph, d_labok, d_seeds, d_sofs, d_gr, d_tflag, d_vacc, d_truth, d_score, d_plog, d_tfresh, d_grids, d_live, d_act, d_list, d_inq, d_cnt,
         d_snk, d_drain, d_err, d_stat, d_colswap, d_out, d_bits, d_in32, d_pw, d_mask, d_off, d_lam,
         d_swapcnt, d_swapflag, d_ring, d_qstate, d_qctr, d_ctl, d_curlam, d_flows, d_slopesum,
         d_we, d_wr, d_wgrid, d_wtile, d_wchg, d_wcnt, d_cv,   // int64 state variant (wide.cuh)
@@ -320,7 +321,7 @@ int setup_state(pmf_solver *s, int edge_bytes) {
     if ((rc = s->d_w.ensure(P * 4)) || (rc = s->d_h.ensure(P * 4)) ||
         (rc = s->d_r.ensure(P * size_t(edge_bytes))) || (rc = s->d_lab.ensure(P)) ||
         (rc = s->d_tile_grid.ensure(T * 4)) || (rc = s->d_tnb.ensure(T * 16)) || (rc = s->d_grids.ensure(G * sizeof(GridDesc))) ||
-        (rc = s->d_live.ensure(G * 4)) || (rc = s->d_fin.ensure(G * 4)) || (rc = s->d_gpend.ensure(G * 4)) || (rc = s->d_specg.ensure(G * 4)) || (rc = s->d_keeph.ensure(G * 4)) || (rc = s->d_act.ensure(G * 4)) ||
+        (rc = s->d_live.ensure(G * 4)) || (rc = s->d_fin.ensure(G * 4)) || (rc = s->d_gpend.ensure(G * 4)) || (rc = s->d_specg.ensure(G * 4)) || (rc = s->d_keeph.ensure(G * 4)) || (rc = s->d_labok.ensure(G * 4)) || (rc = s->d_act.ensure(G * 4)) ||
         (rc = s->d_list.ensure(2 * T * 4)) || (rc = s->d_inq.ensure(2 * T * 4)) ||
         (rc = s->d_cnt.ensure(64)) || (rc = s->d_snk.ensure(G * 8)) || (rc = s->d_drain.ensure(G * 8)) ||
         (rc = s->d_err.ensure(64)) || (rc = s->d_stat.ensure(ST_NSTAT * 8)) ||
@@ -345,6 +346,7 @@ int setup_state(pmf_solver *s, int edge_bytes) {
     CK(cudaMemsetAsync(s->d_gpend.p, 0, G * 4, s->st));
     CK(cudaMemsetAsync(s->d_specg.p, 0, G * 4, s->st));
     CK(cudaMemsetAsync(s->d_keeph.p, 0, G * 4, s->st));
+    CK(cudaMemsetAsync(s->d_labok.p, 0, G * 4, s->st));
     CK(cudaMemsetAsync(s->d_snk.p, 0, G * 8, s->st));
     CK(cudaMemsetAsync(s->d_drain.p, 0, G * 8, s->st));
     CK(cudaMemsetAsync(s->d_err.p, 0, 64, s->st));
@@ -370,6 +372,7 @@ int setup_state(pmf_solver *s, int edge_bytes) {
     x.gpend = s->d_gpend.as<int32_t>();
     x.specg = nullptr;   // set by seed_run_t in rolling mode
     x.keeph = nullptr;   // set by seed_run_t for warm chains
+    x.labok = nullptr;   // ... as is the nested label seeding
     x.ngrids = int32_t(G);
     x.rolling = 0;
     x.act = s->d_act.as<int32_t>();
@@ -1250,6 +1253,9 @@ int seed_run_t(pmf_solver *s) {
     s->ctx.specg = s->ctx.rolling && s->async_spec ? s->d_specg.as<int32_t>() : nullptr;
     // kept heights need the speculative closure as their safety net
     s->ctx.keeph = s->ctx.specg && s->adv_keep_h ? s->d_keeph.as<int32_t>() : nullptr;
+    // minimal source sides are nested along the schedule: a chain's next
+    // label closure is seeded with the previous lambda's (knob nested_lab)
+    s->ctx.labok = s->ctx.rolling && s->nested_lab ? s->d_labok.as<int32_t>() : nullptr;
     int rc2 = run_solve<E>(s, c, int32_t(s->lay.grids.size()), chains ? &a : nullptr,
                            chains ? s->d_slopesum.as<int64_t>() : nullptr);
     if (rc2) return rc2;
@@ -1982,6 +1988,7 @@ int pmf_solver_set(pmf_solver *s, const char *name, int64_t v) {
     else if (k == "comp_split") s->comp_split = v != 0;
     else if (k == "rolling") s->rolling = v != 0;
     else if (k == "push_flush" && v >= 0 && v <= 1024) s->push_flush = int(v);
+    else if (k == "nested_lab") s->nested_lab = v != 0;
     else if (k == "async_yield_us" && v >= 0 && v <= 1000000) s->async_yield_us = int(v);
     else if (k == "async_yield_keep" && v >= 0 && v <= 100000) s->async_yield_keep = int(v);
     else if (k == "fresh_skip") s->fresh_skip = v != 0;

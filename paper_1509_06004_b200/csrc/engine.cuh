@@ -120,6 +120,8 @@ struct Ctx {
     int32_t *gpend;         // per grid: its tiles queued or running in the current persistent phase
     int32_t *specg;         // rolling mode (nullable): 1 label closure speculative, 2 spoiled
     int32_t *keeph;         // warm chains (nullable): grid entered its lambda with valid heights, skip its relabel
+    int32_t *labok;         // warm chains (nullable): lab holds the grid's previous lambda's minimal
+                            // source side (nested seeding of the next label closure)
     int32_t ngrids;
     int32_t rolling;        // rolling warm start: grids emit and advance as they finish
     uint8_t *tfresh;        // per tile: heights are exact from the last relabel (first discharge

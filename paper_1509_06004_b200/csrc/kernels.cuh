@@ -291,14 +291,18 @@ __device__ __forceinline__ void for_tiles(const Ctx &c, Pred pred, F f) {
 // and every neighbour facing a seed on t's border -- a seed never
 // "changes", so the relaxation of t alone would never hand it across the
 // tile boundary.  `seeds` bit r = pixel (lane, row r) is a seed.
-__device__ __forceinline__ void seed_with_halo(const Ctx &c, int64_t t, unsigned seeds, int lane) {
+// need_open: a tile whose every pixel is a seed is not listed itself (its
+// relaxation could add nothing), only the neighbours facing its border.
+__device__ __forceinline__ void seed_with_halo(const Ctx &c, int64_t t, unsigned seeds, int lane,
+                                               bool need_open = false) {
     const unsigned cols = __ballot_sync(0xffffffffu, seeds != 0);
     const unsigned top = __ballot_sync(0xffffffffu, seeds & 1u), bottom = __ballot_sync(0xffffffffu, seeds >> (TH - 1));
+    const bool open = !need_open || __any_sync(0xffffffffu, seeds != 0xffffffffu);
     if (lane == 0 && cols) {
         const int sides = (cols & 1u ? 1 << DL : 0) | (cols >> 31 ? 1 << DR : 0) | (top ? 1 << DU : 0) |
                           (bottom ? 1 << DD : 0);
         TileGeo g = tile_geo(c, int32_t(t));
-        seed_tile(c, int32_t(t));
+        if (open) seed_tile(c, int32_t(t));
         for (int s = 0; s < 4; s++)
             if (((sides >> s) & 1) && g.nb[s] >= 0) seed_tile(c, g.nb[s]);
     }
@@ -477,6 +481,7 @@ __global__ void __launch_bounds__(1024) k_unspoil(Ctx c, int32_t ngrids) {
         if (sp == 2) {
             c.fin[g] = 0;
             c.live[g] = 1;
+            if (c.labok) c.labok[g] = 0;   // lab holds a spoiled closure
             n++;
         }
         if (sp) c.specg[g] = 0;
@@ -489,22 +494,34 @@ __global__ void __launch_bounds__(1024) k_unspoil(Ctx c, int32_t ngrids) {
 // then per-grid label bytes and flows.
 // ---------------------------------------------------------------------------
 
+// Seeds of the label closure: the excess pixels, plus -- chain grids whose
+// previous lambda's labels are final (c.labok) -- that lambda's minimal
+// source side, still in lab: minimal source sides are nested along a
+// monotone schedule (parametric.py:191-201), and its pixels never regain a
+// sink residual (w >= 0 stays >= 0), so the closure is unchanged and only
+// travels the new ring.  Tiles already inside it are not relaxed.
 __global__ void __launch_bounds__(NT) k_lab_seed(Ctx c) {
     for_tiles(c, [&](int32_t g) { return grid_due(c, g) && !grid_swapped(c, c.grids[g]); }, [&](int64_t t, int lane) {
+        const bool nested = c.labok && c.labok[c.tile_grid[t]];
         unsigned seeds = 0;
         const int64_t p0 = t * TPIX + lane;
 #pragma unroll
         for (int r0 = 0; r0 < TH; r0 += SCAN_ROWS) {
             int32_t wv[SCAN_ROWS];
-#pragma unroll
-            for (int k = 0; k < SCAN_ROWS; k++) wv[k] = c.w[p0 + TW * (r0 + k)];
+            uint8_t lv[SCAN_ROWS];
 #pragma unroll
             for (int k = 0; k < SCAN_ROWS; k++) {
-                c.lab[p0 + TW * (r0 + k)] = uint8_t(wv[k] > 0);
-                seeds |= unsigned(wv[k] > 0) << (r0 + k);
+                wv[k] = c.w[p0 + TW * (r0 + k)];
+                lv[k] = nested ? c.lab[p0 + TW * (r0 + k)] : 0;
+            }
+#pragma unroll
+            for (int k = 0; k < SCAN_ROWS; k++) {
+                const bool v = wv[k] > 0 || lv[k];
+                c.lab[p0 + TW * (r0 + k)] = uint8_t(v);
+                seeds |= unsigned(v) << (r0 + k);
             }
         }
-        seed_with_halo(c, t, seeds, lane);
+        seed_with_halo(c, t, seeds, lane, nested);
     });
 }
 
@@ -912,6 +929,7 @@ __global__ void __launch_bounds__(1024) k_advance_grids(Ctx c, SeedArgs a, const
         if (c.swapflag[gd.prob]) c.snk_sum[g] += (a.lambdas[cur + 1] - a.lambdas[cur]) * slope_sum[gd.prob];
         c.cur_lam[g] = cur + 1;
         c.live[g] = 1;
+        if (c.labok) c.labok[g] = !c.swapflag[gd.prob];   // lab holds this lambda's source side
         // unswapped: lambda_{i+1} only lowers sink residuals, the exact
         // heights of lambda_i stay a valid labelling -- skip one relabel
         if (c.keeph && !c.swapflag[gd.prob]) c.keeph[g] = 1;

@@ -244,6 +244,12 @@ __global__ void __launch_bounds__(WPB * 32) k_wbfs_src(Ctx c, int k, LaunchCtl l
     warp_loop(c, k, lc, [&](int32_t t) -> TileResult {
         const TileNb g = tile_nbs(c, t);
         const int64_t base = int64_t(t) * TPIX;
+        if (c.labok) {   // nested seeding: a tile already inside the closure cannot change
+            bool full = true;
+#pragma unroll 8
+            for (int y = 0; y < TH; y++) full &= __ldcg(c.lab + base + y * TW + lane) != 0;
+            if (__all_sync(0xffffffffu, full)) return TileResult{0, 0};
+        }
         wt_load<E>(c, t, T, g, lane, true, false);
         uint32_t m[4];   // own arcs: bit x of m[d] = r_d(x, y) > 0
         wt_arc_masks<E>(T, lane, m);
