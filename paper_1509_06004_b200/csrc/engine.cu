@@ -800,10 +800,10 @@ int build_graph_rolling(pmf_solver *s, const Ctx &c0, int32_t ngrids, const Seed
     if ((rc = add_kernel(lab, &l, gfull, dim3(NT), k_lab_seed, P.bfs))) return rc;
     if ((rc = add_bfs_node<E>(s, lab, &l, false, P.bfs, bfs_k, lctl(ST_LAB)))) return rc;
     if (c0.specg && (rc = add_kernel(lab, &l, dim3(1), dim3(1024), k_unspoil, P.base, ngrids))) return rc;
-    if ((rc = add_kernel(lab, &l, gfull, dim3(NT), k_emit, P.base))) return rc;
+    // label bytes + warm-start advance of the finished grids in one pass
+    if ((rc = add_kernel(lab, &l, gfull, dim3(NT), k_emit_advance, P.base, *sa))) return rc;
     if ((rc = add_kernel(lab, &l, dim3(std::max(1, int(cdiv(ngrids, 256)))), dim3(256), k_finalize, P.base, ngrids)))
         return rc;
-    if ((rc = add_kernel(lab, &l, gfull, dim3(NT), k_advance_tiles, P.base, *sa))) return rc;
     if ((rc = add_kernel(lab, &l, dim3(1), dim3(1024), k_advance_grids, P.base, *sa, slope_sum, ngrids, h_cycle, 1)))
         return rc;
     return 0;
@@ -903,9 +903,8 @@ int host_solve_rolling(pmf_solver *s, const Ctx &c0, int32_t ngrids, const SeedA
         LAUNCH(s, (k_lab_seed<<<s->grid_full, NT, 0, s->st>>>(P.bfs)));
         if ((rc = host_bfs<E>(s, P.bfs, false))) return rc;
         if (c0.specg) LAUNCH(s, (k_unspoil<<<1, 1024, 0, s->st>>>(c0, ngrids)));
-        LAUNCH(s, (k_emit<<<s->grid_full, NT, 0, s->st>>>(P.base)));
+        LAUNCH(s, (k_emit_advance<<<s->grid_full, NT, 0, s->st>>>(P.base, sa)));
         LAUNCH(s, (k_finalize<<<gfin, 256, 0, s->st>>>(c0, ngrids)));
-        LAUNCH(s, (k_advance_tiles<<<s->grid_full, NT, 0, s->st>>>(c0, sa)));
         LAUNCH(s, (k_advance_grids<<<1, 1024, 0, s->st>>>(c0, sa, slope_sum, ngrids, 0, 0)));
         CK(cudaGetLastError());
         if ((rc = read_ctl(s, c0, &ctl))) return rc;

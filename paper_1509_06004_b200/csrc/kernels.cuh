@@ -614,6 +614,56 @@ __global__ void k_finalize(Ctx c, int32_t ngrids) {
 // swapped ones, parametric.py:147) -- so the next solve starts from it.
 // Non-fg pixels gain (lambda_{i+1} - lambda_i) * slope of source (w +=) or,
 // embedded swapped, of sink capacity (w -=).
+// Rolling warm start, fused k_emit + k_advance_tiles for seed-batch grids
+// (one pass over w instead of two): label bytes and unused sink residual of
+// the finished lambda, then -- when the chain has a next lambda -- its
+// terminal advance w += sign * (lambda_{i+1} - lambda_i) * slope.
+__global__ void __launch_bounds__(NT) k_emit_advance(Ctx c, SeedArgs a) {
+    const int64_t n = int64_t(a.W) * a.H;
+    for_tiles(c, [&](int32_t g) { return grid_due(c, g); }, [&](int64_t t, int lane) {
+        const TileGeo g = tile_geo(c, int32_t(t));
+        const GridDesc &gd = c.grids[g.g];
+        const bool swapped = grid_swapped(c, gd);
+        const int cur = c.cur_lam[g.g];
+        const bool next = cur + 1 < gd.lam_end;
+        const int64_t dl = next ? a.lambdas[cur + 1] - a.lambdas[cur] : 0;
+        const int sign = c.swapflag[gd.prob] ? -1 : 1;
+        const int32_t *slope = a.slope + a.plane_off[gd.prob];
+        const uint8_t *mask = a.mask + int64_t(gd.prob) * n;
+        const int64_t off = (int64_t(gd.prob) * c.nlam + cur) * n;
+        int64_t drain = 0;
+        const int x = g.x0 + lane, rows = min(TH, g.H - g.y0);
+        if (x < g.W)
+#pragma unroll
+            for (int r0 = 0; r0 < TH; r0 += SCAN_ROWS) {
+                int32_t wv[SCAN_ROWS], d[SCAN_ROWS];
+                uint8_t v[SCAN_ROWS];
+#pragma unroll
+                for (int k = 0; k < SCAN_ROWS; k++) {
+                    const int64_t p = t * TPIX + lane + TW * (r0 + k);
+                    const bool in = r0 + k < rows;
+                    const int64_t q = int64_t(g.y0 + r0 + k) * a.W + x;
+                    wv[k] = in ? c.w[p] : 0;
+                    // swapped grid: its sink side {h < HINF}; else the source-side closure
+                    v[k] = !in ? 0 : swapped ? uint8_t(c.h[p] < HINF) : c.lab[p];
+                    const uint8_t m = in && next ? mask[q] : 1;   // fg seed: CAP_MAX either way
+                    const int32_t sv = in && next ? slope[q] : 0;
+                    d[k] = m != 1 ? int32_t(sign * dl * int64_t(sv)) : 0;
+                }
+#pragma unroll
+                for (int k = 0; k < SCAN_ROWS; k++) {
+                    if (wv[k] < 0) drain -= wv[k];
+                    if (r0 + k < rows) {
+                        c.out[off + int64_t(g.y0 + r0 + k) * g.W + x] = v[k];
+                        if (d[k]) c.w[t * TPIX + lane + TW * (r0 + k)] = wv[k] + d[k];
+                    }
+                }
+            }
+        drain = warp_sum64(drain);
+        if (lane == 0 && drain) atomicAdd((unsigned long long *)&c.drain[g.g], (unsigned long long)drain);
+    });
+}
+
 __global__ void __launch_bounds__(NT) k_advance_tiles(Ctx c, SeedArgs a) {
     const int64_t n = int64_t(a.W) * a.H;
     for_tiles(c, [&](int32_t g) { return grid_due(c, g) && c.cur_lam[g] + 1 < c.grids[g].lam_end; },
