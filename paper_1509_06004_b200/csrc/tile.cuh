@@ -346,14 +346,32 @@ __device__ __forceinline__ TileResult bfs_sink_tile(const Ctx &c, int32_t t) {
     const int32_t h0 = __ldcg(c.h + p);
     typename E::Word wd = E::load(c.r, p);
     s_sd[ly * SP + lx] = h0;
-    s_sm[i] = uint8_t((E::lane(wd, 0) > 0) | ((E::lane(wd, 1) > 0) << 1) | ((E::lane(wd, 2) > 0) << 2) |
-                      ((E::lane(wd, 3) > 0) << 3));
+    const int mk = (E::lane(wd, 0) > 0) | ((E::lane(wd, 1) > 0) << 1) | ((E::lane(wd, 2) > 0) << 2) |
+                   ((E::lane(wd, 3) > 0) << 3);
+    s_sm[i] = uint8_t(mk);
     if (i < 4 * TW) {
         int s = i / TW, j = i % TW;
         s_hv[s][j] = g.nb[s] >= 0 ? __ldcg(c.h + int64_t(g.nb[s]) * TPIX + halo_index(s, j)) : HINF;
     }
     if (i == 0) s_side = 0;
     __syncthreads();
+    // Most passes of a relabel revisit a tile whose heights are already a
+    // fixpoint for its new halo (59 % at C5: the neighbour's improvement
+    // does not reach it).  One test of every pull arc p <- q -- h(p) <=
+    // h(q) + 1 -- proves it and skips the relaxation (exactly the pass the
+    // relaxation would have found unchanged).
+    {
+        int open = 0;
+        if (h0 > 1) {
+            const int32_t hl = lx > 0 ? s_sd[ly * SP + lx - 1] : s_hv[DL][ly];
+            const int32_t hr = lx < TW - 1 ? s_sd[ly * SP + lx + 1] : s_hv[DR][ly];
+            const int32_t hu = ly > 0 ? s_sd[(ly - 1) * SP + lx] : s_hv[DU][lx];
+            const int32_t hd = ly < TH - 1 ? s_sd[(ly + 1) * SP + lx] : s_hv[DD][lx];
+            open = ((mk & 1) && hl + 1 < h0) | ((mk & 2) && hr + 1 < h0) | ((mk & 4) && hu + 1 < h0) |
+                   ((mk & 8) && hd + 1 < h0);
+        }
+        if (!__syncthreads_or(open)) return TileResult{0, 0};
+    }
     tile_relax(s_sd, s_sm, s_hv, 1);
     const int32_t h1 = s_sd[ly * SP + lx];
     if (h1 != h0) {
