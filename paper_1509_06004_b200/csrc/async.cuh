@@ -83,6 +83,14 @@ struct AsyncArgs {
 };
 constexpr int PLOG = 512;
 
+// A grid reports its sink side: a swapped seed-batch grid, or a composite
+// grid whose columns are all swapped (the asynchronous solver runs only
+// composites whose every grid is uniform: one grid per segment span, or no
+// swapped column at all).
+__device__ __forceinline__ bool async_swapped(const Ctx &c, const GridDesc &gd) {
+    return gd.kind == 1 ? c.colswap[gd.colswap_off] != 0 : grid_swapped(c, gd);
+}
+
 // ---- scan phases: one task = up to SCAN_GROUP consecutive tiles of a grid,
 // all processed at once (SCAN_GROUP pixels per thread, loads issued
 // together), with per-tile flags / counts gathered in shared memory.
@@ -212,13 +220,17 @@ __device__ __forceinline__ void emit_group(const Ctx &c, const AsyncArgs &A, int
     const int i = threadIdx.x;
     const int cur = __ldcg(c.cur_lam + g);   // advanced by other CTAs' transitions
     const bool next = cur + 1 < gd.lam_end;
-    const bool swapped = grid_swapped(c, gd);
+    const bool swapped = async_swapped(c, gd);
+    const bool comp = gd.kind == 1;
     const int64_t n = int64_t(gd.W) * gd.H;
     const int64_t dl = next ? a.lambdas[cur + 1] - a.lambdas[cur] : 0;
-    const int sign = c.swapflag[gd.prob] ? -1 : 1;
-    uint8_t *out = c.out + (int64_t(gd.prob) * c.nlam + cur) * n;
-    const uint8_t *mask = a.mask + int64_t(gd.prob) * n;
-    const int32_t *slope = a.slope + a.plane_off[gd.prob];
+    const int sign = !comp && c.swapflag[gd.prob] ? -1 : 1;
+    // composites (no next lambda): the span's columns of the composite's
+    // output, swapped columns as ~sink side (supergraph.py:201-206, k_emit)
+    uint8_t *out = comp ? c.out + gd.out_off + gd.xoff : c.out + (int64_t(gd.prob) * c.nlam + cur) * n;
+    const int64_t pitch = comp ? gd.pitch : gd.W;
+    const uint8_t *mask = next ? a.mask + int64_t(gd.prob) * n : nullptr;
+    const int32_t *slope = next ? a.slope + a.plane_off[gd.prob] : nullptr;
     // unswapped grids may keep their heights into the next lambda (knob
     // adv_keep_h, see the EMIT transition); swapped ones get that lambda's
     // BINIT fused in here
@@ -238,7 +250,8 @@ __device__ __forceinline__ void emit_group(const Ctx &c, const AsyncArgs &A, int
         if (x < gd.W && y < gd.H) {
             if (wv < 0) drain -= wv;
             const int64_t q = int64_t(y) * gd.W + x;
-            out[q] = swapped ? uint8_t(__ldcg(c.h + p) < HINF) : __ldcg(c.lab + p);
+            out[int64_t(y) * pitch + x] =
+                swapped ? uint8_t((__ldcg(c.h + p) < HINF) != comp) : __ldcg(c.lab + p);
             if (next && mask[q] != 1) {   // fg seed: CAP_MAX either way
                 wv += int32_t(sign * dl * int64_t(slope[q]));
                 c.w[p] = wv;
@@ -279,7 +292,7 @@ __device__ void grid_transition(const Ctx &c, const AsyncArgs &A, int32_t g, int
     for (;;) {
         if (threadIdx.x == 0) {
             int next = PH_DONE;
-            const bool swapped = grid_swapped(c, gd);
+            const bool swapped = async_swapped(c, gd);
             switch (ph) {
             case PH_BINIT: next = PH_BFS; break;
             case PH_BFS:
@@ -336,7 +349,7 @@ __device__ void grid_transition(const Ctx &c, const AsyncArgs &A, int32_t g, int
             case PH_EMIT: {
                 const int cur = __ldcg(c.cur_lam + g);
                 const int64_t snk = int64_t(__ldcg((const unsigned long long *)(c.snk_sum + g)));
-                c.flows[int64_t(gd.prob) * c.nlam + cur] =
+                c.flows[gd.kind == 1 ? int64_t(g) : int64_t(gd.prob) * c.nlam + cur] =
                     snk - int64_t(__ldcg((const unsigned long long *)&R.drain));
                 R.drain = 0;
                 atomicAdd(&c.stat[ST_LAMS], 1ull);
@@ -526,7 +539,7 @@ __global__ void __launch_bounds__(NTT, 2) k_async(Ctx c, AsyncArgs A) {
             switch (ph) {
             case PH_BINIT: binit_group(c, A, t, ntl); break;
             case PH_SEED: seed_group(c, A, t, ntl, g); break;
-            case PH_LINIT: linit_group(c, A, t, ntl, g, grid_swapped(c, gd)); break;
+            case PH_LINIT: linit_group(c, A, t, ntl, g, async_swapped(c, gd)); break;
             default: emit_group(c, A, t, ntl, g); break;
             }
             stat = ph == PH_BINIT ? ST_BINIT : ph == PH_SEED ? ST_SEED : ph == PH_LINIT ? ST_LINIT : ST_EMIT;

@@ -234,7 +234,8 @@ struct pmf_solver {
     int async_max_tiles = 20000;
     int async_max_grid_tiles = 1024;   // ... and grids of at most this many tiles on average
     int async_cont = 1, async_prefetch = 1;
-    int nested_lab = 1;         // rolling step mode: seed label closures with the previous lambda's source side
+    int nested_lab = 1;
+    int comp_async = 1;         // latency-bound composites on the asynchronous solver         // rolling step mode: seed label closures with the previous lambda's source side
     int async_yield_us = 0;     // asynchronous solver: idle CTAs leave an empty-queue tail after this (0 never)
     int async_yield_keep = 0;   // ... except the first this many CTAs (0: a quarter of the grid)
     bool last_async = false;    // the last launched seed run was asynchronous (no cooperative kernels)
@@ -1906,6 +1907,19 @@ int comp_run_t(pmf_solver *s, int ncomp, int64_t total_px) {
     LAUNCH(s, (k_load_comp<E><<<s->grid_full, NT, 0, s->st>>>(c, a)));
     CK(cudaGetLastError());
     s->stats.full_passes++;
+    // latency-bound composites (a wire request, a small join()) run on the
+    // asynchronous solver when every grid reports one side: a segment span,
+    // or a composite with no swapped column (or only swapped ones)
+    bool uniform = true;
+    for (const GridDesc &gd : s->lay.grids) {
+        const uint8_t *cs = s->colswap.data() + gd.colswap_off;
+        for (int32_t x = 1; x < gd.W && uniform; x++) uniform = cs[x] == cs[0];
+    }
+    const int64_t ngr = std::max<int64_t>(1, int64_t(G));
+    const bool use_async = uniform && (s->async_mode == 1 ||
+                                       (s->async_mode < 0 && s->lay.ntiles <= s->async_max_tiles &&
+                                        s->lay.ntiles <= int64_t(s->async_max_grid_tiles) * ngr));
+    if (use_async && s->comp_async) return async_solve<E>(s, c, SeedArgs{});
     return run_solve<E>(s, c, int32_t(s->lay.grids.size()));
 }
 
@@ -1988,6 +2002,7 @@ int pmf_solver_set(pmf_solver *s, const char *name, int64_t v) {
     else if (k == "rolling") s->rolling = v != 0;
     else if (k == "push_flush" && v >= 0 && v <= 1024) s->push_flush = int(v);
     else if (k == "nested_lab") s->nested_lab = v != 0;
+    else if (k == "comp_async") s->comp_async = v != 0;
     else if (k == "async_yield_us" && v >= 0 && v <= 1000000) s->async_yield_us = int(v);
     else if (k == "async_yield_keep" && v >= 0 && v <= 100000) s->async_yield_keep = int(v);
     else if (k == "fresh_skip") s->fresh_skip = v != 0;
