@@ -1853,7 +1853,8 @@ void wide_stats(pmf_solver *s) {
 }
 
 // composites on the int64 state: one grid per composite, planes from the
-// int32 staging (src | snk | nbr per composite at comp_off)
+// int32 staging (src | snk | nbr per composite at comp_off), already on the
+// device (solve_composites_t)
 int wide_comp_run(pmf_solver *s, int32_t ncomp, const int32_t *width, const int32_t *height,
                   const std::vector<int32_t> &cs_off, int64_t total_px) {
     int rc;
@@ -1863,7 +1864,6 @@ int wide_comp_run(pmf_solver *s, int32_t ncomp, const int32_t *width, const int3
         return rc;
     s->tmark(C_H2D);
     CK(cudaMemcpyAsync(s->d_colswap.p, s->colswap.data(), s->colswap.size(), cudaMemcpyHostToDevice, s->st));
-    CK(cudaMemcpyAsync(s->d_in32.p, s->h_in32.p, size_t(total_px) * 6 * 4, cudaMemcpyHostToDevice, s->st));
     CK(cudaMemcpyAsync(s->d_off.p, s->comp_off.data(), size_t(ncomp) * 8, cudaMemcpyHostToDevice, s->st));
     s->tmark(C_BUILD);
     WideBatch B;
@@ -1894,9 +1894,8 @@ int comp_run_t(pmf_solver *s, int ncomp, int64_t total_px) {
     const Ctx &c = s->ctx;
     s->tmark(C_H2D);
     const size_t G = s->lay.grids.size();
-    if ((rc = s->d_in32.ensure(size_t(total_px) * 6 * 4)) || (rc = s->d_off.ensure(G * 8))) return rc;
-    int32_t *din = s->d_in32.as<int32_t>();
-    CK(cudaMemcpyAsync(din, s->h_in32.p, size_t(total_px) * 6 * 4, cudaMemcpyHostToDevice, s->st));
+    if ((rc = s->d_off.ensure(G * 8))) return rc;
+    int32_t *din = s->d_in32.as<int32_t>();   // planes staged by solve_composites_t
     s->grid_off.resize(G);   // per grid: its composite's plane offset
     for (size_t g = 0; g < G; g++) s->grid_off[g] = s->comp_off[size_t(s->lay.grids[g].prob)];
     CK(cudaMemcpyAsync(s->d_off.p, s->grid_off.data(), G * 8, cudaMemcpyHostToDevice, s->st));
@@ -2135,26 +2134,45 @@ static int solve_composites_t(pmf_solver *s, int32_t ncomp, const int32_t *width
     if (rc) return rc;
     int32_t *hin = s->h_in32.as<int32_t>();
     TaskErr terr;
-    // range check + narrow every plane, chunked over all composites
-    std::vector<int64_t> chunk_base(ncomp + 1, 0);
-    for (int c = 0; c < ncomp; c++)
-        chunk_base[c + 1] = chunk_base[c] + cdiv(int64_t(width[c]) * height[c] * 6, kChunk);
-    s->pool->run(chunk_base[ncomp], [&](int64_t task) {
-        int c = int(std::upper_bound(chunk_base.begin(), chunk_base.end(), task) - chunk_base.begin()) - 1;
-        const int64_t n = int64_t(width[c]) * height[c], off = s->comp_off[c];
-        const int64_t lo = (task - chunk_base[c]) * kChunk, hi = std::min(6 * n, lo + kChunk);
-        for (int64_t i = lo; i < hi; i++) {   // element i of [src | snk | nbr(4n)]
-            const int64_t v = int64_t(i < n ? src[c][i] : i < 2 * n ? snk[c][i - n] : nbr[c][i - 2 * n]);
-            if (v < 0 || v > CAP_MAX) {
-                terr.set(PMF_ERR_RANGE, "composite capacity outside [0, CAP_MAX]");
-                return;
+    // range check + narrow every plane into the pinned staging buffer
+    // [src | snk | nbr (4 planes per composite)], in 6 pieces of total_px
+    // elements each; a piece's H2D overlaps the narrowing of the next
+    // (comp_run_t finds the planes on the device)
+    if ((rc = s->d_in32.ensure(size_t(total_px) * 6 * 4))) return rc;
+    std::vector<int64_t> off4(size_t(ncomp) + 1, 0);   // 4 * comp_off, plus the end
+    for (int c = 0; c < ncomp; c++) off4[size_t(c)] = 4 * s->comp_off[size_t(c)];
+    off4[size_t(ncomp)] = 4 * total_px;
+    for (int piece = 0; piece < 6; piece++) {
+        const int64_t base = int64_t(piece) * total_px, ntask = cdiv(total_px, kChunk);
+        s->pool->run(ntask, [&](int64_t task) {
+            const int64_t lo = task * kChunk, hi = std::min(total_px, lo + kChunk);
+            // element j of this piece: pixel j (src / snk), or element j of
+            // the 4-plane neighbour blocks; composite boundaries from `bnd`
+            const bool term = piece < 2;
+            const int64_t j0 = (term ? 0 : (piece - 2) * total_px) + lo, j1 = j0 + (hi - lo);
+            const std::vector<int64_t> &bnd = term ? s->comp_off : off4;
+            int c = int(std::upper_bound(bnd.begin(), bnd.begin() + ncomp, j0) - bnd.begin()) - 1;
+            for (int64_t j = j0; j < j1;) {
+                const int64_t cend = std::min(j1, c + 1 < ncomp ? bnd[size_t(c) + 1] : (term ? total_px : 4 * total_px));
+                const int64_t cb = bnd[size_t(c)];
+                const T *srcp = term ? (piece == 0 ? src[c] : snk[c]) : nbr[c];
+                int32_t *dst = hin + base + (j - j0) + lo;
+                for (int64_t k = j; k < cend; k++) {
+                    const int64_t v = int64_t(srcp[k - cb]);
+                    if (v < 0 || v > CAP_MAX) {
+                        terr.set(PMF_ERR_RANGE, "composite capacity outside [0, CAP_MAX]");
+                        return;
+                    }
+                    dst[k - j] = int32_t(v);
+                }
+                j = cend;
+                c++;
             }
-            int32_t *dst = i < n ? hin + off + i : i < 2 * n ? hin + total_px + off + (i - n)
-                                                             : hin + 2 * total_px + 4 * off + (i - 2 * n);
-            *dst = int32_t(v);
-        }
-    });
-    if ((rc = terr.raise())) return rc;
+        });
+        if ((rc = terr.raise())) return rc;
+        CK(cudaMemcpyAsync(s->d_in32.as<int32_t>() + base, hin + base, size_t(total_px) * 4, cudaMemcpyHostToDevice,
+                           s->st));
+    }
     // per (composite, band of rows) task: largest arc pair and the bound on
     // any pixel's excess (its positive terminal plus all arc pairs); bands
     // keep one large composite (a wire request) on every host thread
