@@ -7,6 +7,9 @@
 // the next worklist the tiles that still / newly need work.
 #pragma once
 #include "engine.cuh"
+#ifndef PMF_BFS_SKIP
+#define PMF_BFS_SKIP false
+#endif
 
 namespace pmf {
 
@@ -61,6 +64,15 @@ __device__ __forceinline__ int32_t line_relax(int32_t v, int m, int lane, unsign
 // threads call it.  Runs to the fixpoint (bit 0 of the result set) or stops
 // after max_sweeps sweeps (> 0; bit 0 clear if it had not converged) -- a
 // capped relax only gives upper bounds.  Bits 1.. hold the sweeps run.
+//
+// A line pass leaves its line at the line's own fixpoint (the halo values
+// are constant), so after the first sweep a row needs its pass again only
+// if the column pass before it changed one of its pixels, and a column only
+// if the row pass changed one of its pixels: the passes publish their
+// change ballots (s_rchg[row] / s_cchg[column]) and clean lines skip their
+// scans.  The relax ends when a column pass changes nothing.
+__shared__ unsigned s_rchg[TH], s_cchg[TW];
+template <bool kSkip = true>
 __device__ int tile_relax(int32_t *d, const uint8_t *mk, const int32_t (*hv)[TW], int cost,
                           int max_sweeps = 0) {
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -74,22 +86,51 @@ __device__ int tile_relax(int32_t *d, const uint8_t *mk, const int32_t (*hv)[TW]
         pk = unsigned(mr) | (unsigned(mc) << 4) | (line_seg(mr, lane, 1, 2) << 8) | (line_seg(mc, lane, 4, 8) << 18);
     }
     int sweeps = 0;
+    if (!kSkip) {
+        for (;;) {
+            int changed = 0;
+            {
+                const int32_t v0 = d[warp * SP + lane];
+                const int32_t v = line_relax(v0, pk & 15, lane, pk >> 8, 1, 2, &hv[DL][warp], &hv[DR][warp], cost);
+                if (v != v0) { d[warp * SP + lane] = v; changed = 1; }
+            }
+            __syncthreads();
+            {
+                const int32_t v0 = d[lane * SP + warp];
+                const int32_t v = line_relax(v0, (pk >> 4) & 15, lane, pk >> 18, 4, 8, &hv[DU][warp],
+                                             &hv[DD][warp], cost);
+                if (v != v0) { d[lane * SP + warp] = v; changed = 1; }
+            }
+            sweeps++;
+            if (!__syncthreads_or(changed)) return 1 | (sweeps << 1);
+            if (max_sweeps && sweeps >= max_sweeps) return sweeps << 1;
+        }
+    }
     for (;;) {
-        int changed = 0;
         {
-            const int32_t v0 = d[warp * SP + lane];
-            const int32_t v = line_relax(v0, pk & 15, lane, pk >> 8, 1, 2, &hv[DL][warp], &hv[DR][warp], cost);
-            if (v != v0) { d[warp * SP + lane] = v; changed = 1; }
+            unsigned chg = 0;
+            if (sweeps == 0 || __any_sync(0xffffffffu, (s_cchg[lane] >> warp) & 1u)) {
+                const int32_t v0 = d[warp * SP + lane];
+                const int32_t v = line_relax(v0, pk & 15, lane, pk >> 8, 1, 2, &hv[DL][warp], &hv[DR][warp], cost);
+                if (v != v0) d[warp * SP + lane] = v;
+                chg = __ballot_sync(0xffffffffu, v != v0);
+            }
+            if (lane == 0) s_rchg[warp] = chg;
         }
         __syncthreads();
-        {
+        unsigned chg = 0;
+        if (sweeps == 0 || __any_sync(0xffffffffu, (s_rchg[lane] >> warp) & 1u)) {
             const int32_t v0 = d[lane * SP + warp];
             const int32_t v = line_relax(v0, (pk >> 4) & 15, lane, pk >> 18, 4, 8, &hv[DU][warp], &hv[DD][warp],
                                          cost);
-            if (v != v0) { d[lane * SP + warp] = v; changed = 1; }
+            if (v != v0) d[lane * SP + warp] = v;
+            chg = __ballot_sync(0xffffffffu, v != v0);
         }
+        if (lane == 0) s_cchg[warp] = chg;
         sweeps++;
-        if (!__syncthreads_or(changed)) return 1 | (sweeps << 1);
+        // done when a column pass changes nothing: the rows are then at
+        // their fixpoint too
+        if (!__syncthreads_or(chg != 0)) return 1 | (sweeps << 1);
         if (max_sweeps && sweeps >= max_sweeps) return sweeps << 1;
     }
 }
@@ -372,11 +413,12 @@ __device__ __forceinline__ TileResult bfs_sink_tile(const Ctx &c, int32_t t) {
         }
         if (!__syncthreads_or(open)) return TileResult{0, 0};
     }
-    tile_relax(s_sd, s_sm, s_hv, 1);
-    const int32_t h1 = s_sd[ly * SP + lx];
+    tile_relax<PMF_BFS_SKIP>(s_sd, s_sm, s_hv, 1);
+    // (positions recomputed after the relax: fewer registers live across it)
+    const int j = threadIdx.x, h1 = s_sd[(j >> 5) * SP + (j & 31)];
     if (h1 != h0) {
-        c.h[p] = h1;
-        if (int b = border_sides(lx, ly)) atomicOr(&s_side, b);
+        c.h[int64_t(t) * TPIX + j] = h1;
+        if (int b = border_sides(j & 31, j >> 5)) atomicOr(&s_side, b);
     }
     __syncthreads();
     return TileResult{0, s_side};
