@@ -212,6 +212,43 @@ def test_random_composites_vs_oracle(engine):
         assert r.flow == f and np.array_equal(r.labels, lab)
 
 
+@pytest.mark.parametrize("i32", [False, True])
+@pytest.mark.parametrize("plane,where", [("src", 0), ("snk", -1), ("nbr", 0), ("nbr", -1)])
+def test_composite_staging_range_errors_leave_solver_usable(engine, i32, plane, where):
+    """pmf_solve_composites(_i32) narrows and uploads the planes in pieces
+    (src, snk, four neighbour quarters); a value outside [0, CAP_MAX] in any
+    piece -- first or last composite, first or last plane -- is the
+    reference's CapacityOverflowError, and the same solver then solves a valid
+    request bit-exactly (oracle)."""
+    from paper_1509_06004_b200 import CapacityOverflowError
+    rng = np.random.default_rng(5)
+    items = []
+    for k in range(3):
+        w, h = int(rng.integers(3, 40)), int(rng.integers(3, 40))
+        nb = rng.integers(0, 25, (4, h, w))
+        nb[0][:, 0] = 0
+        nb[1][:, -1] = 0
+        nb[2][0, :] = 0
+        nb[3][-1, :] = 0
+        items.append([w, h, rng.integers(0, 50, w * h), rng.integers(0, 50, w * h), nb.reshape(4, -1), None])
+    bad = [list(it) for it in items]
+    idx = {"src": 2, "snk": 3, "nbr": 4}[plane]
+    c = 0 if where == 0 else len(bad) - 1
+    arr = np.array(bad[c][idx], np.int64, copy=True)
+    arr.reshape(-1)[where] = -1 if plane == "snk" else CAP_MAX + 1
+    bad[c][idx] = arr
+    if i32:
+        arr = arr.astype(np.int32)
+        bad[c][idx] = arr
+    with pytest.raises(CapacityOverflowError):
+        engine.solve_composites([tuple(b) for b in bad], i32=i32)
+    got = engine.solve_composites([tuple(it) for it in items], i32=i32)
+    for (w, h, src, snk, nbr, _), (flow, lab) in zip(items, got):
+        f, want, _ = oracle.solve(w, h, np.asarray(src, np.int64), np.asarray(snk, np.int64),
+                                  np.asarray(nbr, np.int64).reshape(-1), [])
+        assert flow == f and np.array_equal(lab, want)
+
+
 def test_large_grid_properties(engine):
     """C4-shaped single lambda (1920x1080): certificate checks that do not
     need the reference -- the labels' cut cost equals the flow, and the
