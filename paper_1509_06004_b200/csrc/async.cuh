@@ -108,7 +108,7 @@ __device__ __forceinline__ void scan_reset() {
 // thread k < ntl: flag tile t0 + k for the next flagged phase when it holds a
 // flagged pixel, plus each neighbour facing a flagged border pixel (a seed
 // never changes, so the tile alone would never hand it across the border;
-// seed_with_halo() of the worklist kernels)
+// halo_seed_mask() of the worklist kernels)
 // (bit 4 of sides, when `need_open` is set: the tile also has an unflagged
 // pixel -- a tile whose every pixel is flagged is not listed itself, only
 // the neighbours facing its border)

@@ -287,25 +287,54 @@ __device__ __forceinline__ void for_tiles(const Ctx &c, Pred pred, F f) {
     }
 }
 
-// Seed a BFS phase (warp per tile): list tile t if it holds a seed pixel,
-// and every neighbour facing a seed on t's border -- a seed never
-// "changes", so the relaxation of t alone would never hand it across the
-// tile boundary.  `seeds` bit r = pixel (lane, row r) is a seed.
+// Worklist / queue insertions of a seeding scan, as a mask per tile: bit 0
+// the tile itself, bit 1 + s its neighbour on side s.
+__device__ __forceinline__ void seed_mask(const Ctx &c, int32_t t, unsigned mask) {
+    if (mask & 1u) seed_tile(c, t);
+    for (int s = 0; s < 4; s++)
+        if ((mask >> (s + 1)) & 1u) {
+            const int32_t nb = tile_nb(c, t, s);
+            if (nb >= 0) seed_tile(c, nb);
+        }
+}
+
+// for_tiles for seeding scans: f returns the tile's seed mask (warp-
+// uniform); the insertions -- dependent atomics on the worklist or queue
+// state -- run after the warp's round of up to 32 tiles, each lane doing
+// those of its own tile, so they overlap instead of stalling the warp tile
+// after tile.  (A worklist's order does not matter.)
+template <class Pred, class F>
+__device__ __forceinline__ void for_tiles_seed(const Ctx &c, Pred pred, F f) {
+    const int lane = threadIdx.x & 31;
+    const int64_t w0 = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+    const int64_t G = (int64_t(gridDim.x) * blockDim.x) >> 5;
+    for (int64_t r = 0; w0 + r * G < c.ntiles; r += 32) {
+        const int64_t t = w0 + (r + lane) * G;
+        unsigned m = __ballot_sync(0xffffffffu, t < c.ntiles && pred(c.tile_grid[t]));
+        unsigned mine = 0;
+        while (m) {
+            const int k = __ffs(m) - 1;
+            m &= m - 1;
+            const unsigned sm = f(w0 + (r + k) * G, lane);
+            if (lane == k) mine = sm;
+        }
+        if (mine) seed_mask(c, int32_t(t), mine);
+    }
+}
+
+// Seed mask of a BFS phase (warp per tile): the tile if it holds a seed
+// pixel, and every neighbour facing a seed on its border -- a seed never
+// "changes", so the relaxation of the tile alone would never hand it
+// across the tile boundary.  `seeds` bit r = pixel (lane, row r) is a seed.
 // need_open: a tile whose every pixel is a seed is not listed itself (its
 // relaxation could add nothing), only the neighbours facing its border.
-__device__ __forceinline__ void seed_with_halo(const Ctx &c, int64_t t, unsigned seeds, int lane,
-                                               bool need_open = false) {
+__device__ __forceinline__ unsigned halo_seed_mask(unsigned seeds, bool need_open = false) {
     const unsigned cols = __ballot_sync(0xffffffffu, seeds != 0);
     const unsigned top = __ballot_sync(0xffffffffu, seeds & 1u), bottom = __ballot_sync(0xffffffffu, seeds >> (TH - 1));
     const bool open = !need_open || __any_sync(0xffffffffu, seeds != 0xffffffffu);
-    if (lane == 0 && cols) {
-        const int sides = (cols & 1u ? 1 << DL : 0) | (cols >> 31 ? 1 << DR : 0) | (top ? 1 << DU : 0) |
-                          (bottom ? 1 << DD : 0);
-        TileGeo g = tile_geo(c, int32_t(t));
-        if (open) seed_tile(c, int32_t(t));
-        for (int s = 0; s < 4; s++)
-            if (((sides >> s) & 1) && g.nb[s] >= 0) seed_tile(c, g.nb[s]);
-    }
+    if (!cols) return 0u;
+    return (open ? 1u : 0u) | (cols & 1u ? 2u << DL : 0u) | (cols >> 31 ? 2u << DR : 0u) | (top ? 2u << DU : 0u) |
+           (bottom ? 2u << DD : 0u);
 }
 
 __device__ __forceinline__ int64_t warp_sum64(int64_t v) {
@@ -317,7 +346,7 @@ __device__ __forceinline__ int64_t warp_sum64(int64_t v) {
 // tile holding such a pixel (and its neighbours facing one).  Tiles of
 // finished grids are left untouched.
 __global__ void __launch_bounds__(NT) k_gr_init(Ctx c) {
-    for_tiles(c, [&](int32_t g) { return c.live[g] && !(c.keeph && c.keeph[g]); }, [&](int64_t t, int lane) {
+    for_tiles_seed(c, [&](int32_t g) { return c.live[g] && !(c.keeph && c.keeph[g]); }, [&](int64_t t, int lane) {
         unsigned seeds = 0;
         const int64_t p0 = t * TPIX + lane;
 #pragma unroll
@@ -331,7 +360,7 @@ __global__ void __launch_bounds__(NT) k_gr_init(Ctx c) {
                 seeds |= unsigned(wv[k] < 0) << (r0 + k);
             }
         }
-        seed_with_halo(c, t, seeds, lane);
+        return halo_seed_mask(seeds);
     });
 }
 
@@ -344,7 +373,7 @@ __global__ void __launch_bounds__(NT) k_gr_init(Ctx c) {
 // Lists every tile of a live grid that holds an active pixel (w > 0,
 // h < HINF); counts active pixels per grid.
 __global__ void __launch_bounds__(NT) k_seed_push(Ctx c) {
-    for_tiles(c, [&](int32_t g) { return c.live[g] != 0; }, [&](int64_t t, int lane) {
+    for_tiles_seed(c, [&](int32_t g) { return c.live[g] != 0; }, [&](int64_t t, int lane) {
         int a = 0;
 #pragma unroll 8
         for (int r = 0; r < TH; r++) {
@@ -355,8 +384,8 @@ __global__ void __launch_bounds__(NT) k_seed_push(Ctx c) {
         if (lane == 0 && a) {
             atomicAdd(&c.act[c.tile_grid[t]], a);
             if (c.tfresh) c.tfresh[t] = 1;   // its heights are this relabel's exact distances
-            seed_tile(c, int32_t(t));
         }
+        return a ? 1u : 0u;
     });
 }
 
@@ -501,7 +530,7 @@ __global__ void __launch_bounds__(1024) k_unspoil(Ctx c, int32_t ngrids) {
 // sink residual (w >= 0 stays >= 0), so the closure is unchanged and only
 // travels the new ring.  Tiles already inside it are not relaxed.
 __global__ void __launch_bounds__(NT) k_lab_seed(Ctx c) {
-    for_tiles(c, [&](int32_t g) { return grid_due(c, g) && !grid_swapped(c, c.grids[g]); }, [&](int64_t t, int lane) {
+    for_tiles_seed(c, [&](int32_t g) { return grid_due(c, g) && !grid_swapped(c, c.grids[g]); }, [&](int64_t t, int lane) {
         const bool nested = c.labok && c.labok[c.tile_grid[t]];
         unsigned seeds = 0;
         const int64_t p0 = t * TPIX + lane;
@@ -521,7 +550,7 @@ __global__ void __launch_bounds__(NT) k_lab_seed(Ctx c) {
                 seeds |= unsigned(v) << (r0 + k);
             }
         }
-        seed_with_halo(c, t, seeds, lane, nested);
+        return halo_seed_mask(seeds, nested);
     });
 }
 
