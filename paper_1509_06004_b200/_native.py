@@ -261,11 +261,12 @@ class Solver:
         """[(kind, us, tile_passes, start_us)] of the first tile-kernel launches
         of the last run (kind: 0 discharge, 1 sink BFS, 2 label BFS; start_us
         relative to the first traced launch)."""
-        n = ctypes.c_int32(256)
-        kind = np.zeros(256, np.int32)
-        us = np.zeros(256, np.float64)
-        t0 = np.zeros(256, np.float64)
-        tiles = np.zeros(256, np.int64)
+        cap = 1 << 16   # PMF_KTRACE of diagnostics builds; the library clamps to its own
+        n = ctypes.c_int32(cap)
+        kind = np.zeros(cap, np.int32)
+        us = np.zeros(cap, np.float64)
+        t0 = np.zeros(cap, np.float64)
+        tiles = np.zeros(cap, np.int64)
         self._lib.pmf_debug_trace(self._h, kind.ctypes.data, us.ctypes.data, t0.ctypes.data,
                                   tiles.ctypes.data, ctypes.byref(n))
         return [(int(kind[i]), round(float(us[i]), 1), int(tiles[i]), round(float(t0[i]), 1))

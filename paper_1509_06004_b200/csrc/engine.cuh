@@ -46,6 +46,10 @@ constexpr int K_MULTI = -3;        // one cooperative launch runs every sweep (g
 
 // Device-side control block of a solve (graph-driven mode keeps all loop
 // state here; the host never reads it mid-solve).
+// diagnostics builds may lengthen the launch trace (-DPMF_KTRACE=...)
+#ifndef PMF_KTRACE
+#define PMF_KTRACE 256
+#endif
 struct Ctl {
     int32_t k;              // sweep index of the current list phase
     uint32_t done;          // CTAs finished in the current launch
@@ -63,12 +67,12 @@ struct Ctl {
     uint32_t bar_pad;
     // trace of the first kTrace tile-kernel launches: kind, span (ns), tile passes
     int32_t ntrace;
-    int32_t trace_kind[256];
-    unsigned long long trace_ns[256];
-    unsigned long long trace_tiles[256];
-    unsigned long long trace_t0[256];  // absolute start of the launch (ns)
+    int32_t trace_kind[PMF_KTRACE];
+    unsigned long long trace_ns[PMF_KTRACE];
+    unsigned long long trace_tiles[PMF_KTRACE];
+    unsigned long long trace_t0[PMF_KTRACE];  // absolute start of the launch (ns)
 };
-constexpr int kTrace = 256;
+constexpr int kTrace = PMF_KTRACE;
 
 // Grid-wide barrier for cooperative launches (every CTA co-resident): a
 // monotonic arrival counter; barrier `round` (0, 1, ...) of the launch
