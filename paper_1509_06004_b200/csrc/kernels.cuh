@@ -647,7 +647,17 @@ __global__ void k_finalize(Ctx c, int32_t ngrids) {
 // (one pass over w instead of two): label bytes and unused sink residual of
 // the finished lambda, then -- when the chain has a next lambda -- its
 // terminal advance w += sign * (lambda_{i+1} - lambda_i) * slope.
-__global__ void __launch_bounds__(NT) k_emit_advance(Ctx c, SeedArgs a) {
+#ifndef EMIT_ROWS
+#define EMIT_ROWS 1
+#endif
+#ifndef EMIT_MINB
+#define EMIT_MINB 8
+#endif
+// One row per step, per-tile base pointers advanced per row: 32 registers,
+// full occupancy (the unrolled 8-row form needed 76 registers -- a third of
+// the SM's warps in flight, 2.6 TB/s; this form: C5 step -1.2 %).
+__global__ void __launch_bounds__(NT, EMIT_MINB) k_emit_advance(Ctx c, SeedArgs a) {
+    constexpr int ER = EMIT_ROWS;
     const int64_t n = int64_t(a.W) * a.H;
     for_tiles(c, [&](int32_t g) { return grid_due(c, g); }, [&](int64_t t, int lane) {
         const TileGeo g = tile_geo(c, int32_t(t));
@@ -655,39 +665,51 @@ __global__ void __launch_bounds__(NT) k_emit_advance(Ctx c, SeedArgs a) {
         const bool swapped = grid_swapped(c, gd);
         const int cur = c.cur_lam[g.g];
         const bool next = cur + 1 < gd.lam_end;
-        const int64_t dl = next ? a.lambdas[cur + 1] - a.lambdas[cur] : 0;
-        const int sign = c.swapflag[gd.prob] ? -1 : 1;
-        const int32_t *slope = a.slope + a.plane_off[gd.prob];
-        const uint8_t *mask = a.mask + int64_t(gd.prob) * n;
-        const int64_t off = (int64_t(gd.prob) * c.nlam + cur) * n;
+        const int64_t mul = next ? int64_t(c.swapflag[gd.prob] ? -1 : 1) * (a.lambdas[cur + 1] - a.lambdas[cur]) : 0;
         int64_t drain = 0;
         const int x = g.x0 + lane, rows = min(TH, g.H - g.y0);
-        if (x < g.W)
+        if (x < g.W) {
+            // row pointers advanced per chunk; rows inside a chunk at
+            // constant (tile) or one-multiply (image) offsets, so no
+            // per-row 64-bit induction variables stay live
+            int32_t *wp = c.w + t * TPIX + lane;
+            const int32_t *hp = c.h + t * TPIX + lane;
+            const uint8_t *lp = c.lab + t * TPIX + lane;
+            const int64_t q0 = int64_t(g.y0) * a.W + x;
+            const uint8_t *mp = a.mask + int64_t(gd.prob) * n + q0;
+            const int32_t *sp = a.slope + a.plane_off[gd.prob] + q0;
+            uint8_t *op = c.out + (int64_t(gd.prob) * c.nlam + cur) * n + int64_t(g.y0) * g.W + x;
+            const int aw = a.W, gw = g.W;
+#pragma unroll 1
+            for (int r0 = 0; r0 < rows; r0 += ER) {
+                int32_t wv[ER], d[ER];
+                uint8_t v[ER];
 #pragma unroll
-            for (int r0 = 0; r0 < TH; r0 += SCAN_ROWS) {
-                int32_t wv[SCAN_ROWS], d[SCAN_ROWS];
-                uint8_t v[SCAN_ROWS];
-#pragma unroll
-                for (int k = 0; k < SCAN_ROWS; k++) {
-                    const int64_t p = t * TPIX + lane + TW * (r0 + k);
+                for (int k = 0; k < ER; k++) {
                     const bool in = r0 + k < rows;
-                    const int64_t q = int64_t(g.y0 + r0 + k) * a.W + x;
-                    wv[k] = in ? c.w[p] : 0;
+                    wv[k] = in ? wp[TW * k] : 0;
                     // swapped grid: its sink side {h < HINF}; else the source-side closure
-                    v[k] = !in ? 0 : swapped ? uint8_t(c.h[p] < HINF) : c.lab[p];
-                    const uint8_t m = in && next ? mask[q] : 1;   // fg seed: CAP_MAX either way
-                    const int32_t sv = in && next ? slope[q] : 0;
-                    d[k] = m != 1 ? int32_t(sign * dl * int64_t(sv)) : 0;
+                    v[k] = !in ? 0 : swapped ? uint8_t(hp[TW * k] < HINF) : lp[TW * k];
+                    const uint8_t m = in && next ? mp[k * aw] : 1;   // fg seed: CAP_MAX either way
+                    const int32_t sv = in && next ? sp[k * aw] : 0;
+                    d[k] = m != 1 ? int32_t(mul * int64_t(sv)) : 0;
                 }
 #pragma unroll
-                for (int k = 0; k < SCAN_ROWS; k++) {
+                for (int k = 0; k < ER; k++) {
                     if (wv[k] < 0) drain -= wv[k];
                     if (r0 + k < rows) {
-                        c.out[off + int64_t(g.y0 + r0 + k) * g.W + x] = v[k];
-                        if (d[k]) c.w[t * TPIX + lane + TW * (r0 + k)] = wv[k] + d[k];
+                        op[k * gw] = v[k];
+                        if (d[k]) wp[TW * k] = wv[k] + d[k];
                     }
                 }
+                wp += ER * TW;
+                hp += ER * TW;
+                lp += ER * TW;
+                mp += ER * aw;
+                sp += ER * aw;
+                op += ER * gw;
             }
+        }
         drain = warp_sum64(drain);
         if (lane == 0 && drain) atomicAdd((unsigned long long *)&c.drain[g.g], (unsigned long long)drain);
     });
@@ -852,7 +874,13 @@ __global__ void __launch_bounds__(NT) k_score(const uint8_t *__restrict__ out, c
 // three 4-byte loads plus two predicated edge bytes (5 loads per 4 pixels
 // instead of 20), and its terms are 16-byte loads.  Every offset (plane_off,
 // pw_off, label planes) is a multiple of n, hence of 4.
-constexpr int VLAM4 = 8;
+// lambdas per pass over the problem planes: 10 (C5's 20-lambda ladder in
+// two passes instead of three, 80 registers without spills; 8 -> 10 measured
+// -0.5 % of the C5 step, 20 spills)
+#ifndef PMF_VLAM4
+#define PMF_VLAM4 10
+#endif
+constexpr int VLAM4 = PMF_VLAM4;
 template <bool NARROW>
 __global__ void __launch_bounds__(NT, 3) k_verify4(Ctx c, SeedArgs a, unsigned long long *acc, int chunks) {
     using SS = typename std::conditional<NARROW, int32_t, int64_t>::type;
