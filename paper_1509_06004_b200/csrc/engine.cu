@@ -1070,8 +1070,7 @@ int grids_for(pmf_solver *s) {
     CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_bfs_sink<E>, NTT, 0));
     CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ2, k_bfs_src<E>, NTT, 0));
     s->grid_bfs = std::max(1, std::min(occ, occ2)) * s->sms;
-    s->smem_w = WPB * sizeof(WarpTile<E>);
-    CK(cudaFuncSetAttribute(k_wbfs_src<E>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(s->smem_w)));
+    s->smem_w = 0;   // the label closure holds its tile in registers
     CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ2, k_wbfs_src<E>, WPB * 32, s->smem_w));
     s->grid_wbfs = std::max(1, occ2) * s->sms;
     s->grid_full = 8 * s->sms;
