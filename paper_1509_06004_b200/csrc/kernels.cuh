@@ -882,7 +882,10 @@ __global__ void __launch_bounds__(NT) k_score(const uint8_t *__restrict__ out, c
 #endif
 constexpr int VLAM4 = PMF_VLAM4;
 template <bool NARROW>
-__global__ void __launch_bounds__(NT, 3) k_verify4(Ctx c, SeedArgs a, unsigned long long *acc, int chunks) {
+#ifndef PMF_VMINB
+#define PMF_VMINB 4
+#endif
+__global__ void __launch_bounds__(NT, PMF_VMINB) k_verify4(Ctx c, SeedArgs a, unsigned long long *acc, int chunks) {
     using SS = typename std::conditional<NARROW, int32_t, int64_t>::type;
     __shared__ unsigned long long s_acc[VLAM4];
     const int32_t n = a.W * a.H, n4 = n / 4, W = a.W;
