@@ -377,21 +377,43 @@ __shared__ uint8_t s_bits[TPIX];      // label BFS: own outgoing-arc bits
 __shared__ int32_t s_hv[4][TW];       // halo values per side
 __shared__ int s_side;                // sides whose neighbour needs work
 
+// A thread's inputs of a sink-BFS tile pass: its pixel's height and
+// residual word, and (threads < 4 * TW) one halo height -- each halo
+// thread reads only its own side's neighbour id (C5 sink BFS -3 % against
+// every thread reading all four; issuing the next tile's loads ahead of
+// the current relaxation measured no better and was dropped).
 template <class E>
-__device__ __forceinline__ TileResult bfs_sink_tile(const Ctx &c, int32_t t) {
-    const int i = threadIdx.x, lx = i & 31, ly = i >> 5;
-    const TileNb g = tile_nbs(c, t);
+struct BfsIn {
+    int32_t h0;
+    typename E::Word wd;
+    int32_t hv;
+};
+template <class E>
+__device__ __forceinline__ BfsIn<E> bfs_sink_load(const Ctx &c, int32_t t) {
+    const int i = threadIdx.x;
     const int64_t p = int64_t(t) * TPIX + i;
-    const int32_t h0 = __ldcg(c.h + p);
-    typename E::Word wd = E::load(c.r, p);
+    BfsIn<E> in;
+    in.h0 = __ldcg(c.h + p);
+    in.wd = E::load(c.r, p);
+    in.hv = HINF;
+    if (i < 4 * TW) {
+        const int s = i / TW, j = i % TW;
+        const int32_t nb = tile_nb(c, t, s);
+        if (nb >= 0) in.hv = __ldcg(c.h + int64_t(nb) * TPIX + halo_index(s, j));
+    }
+    return in;
+}
+
+template <class E>
+__device__ __forceinline__ TileResult bfs_sink_tile(const Ctx &c, int32_t t, const BfsIn<E> &in) {
+    const int i = threadIdx.x, lx = i & 31, ly = i >> 5;
+    const int32_t h0 = in.h0;
+    const typename E::Word wd = in.wd;
     s_sd[ly * SP + lx] = h0;
     const int mk = (E::lane(wd, 0) > 0) | ((E::lane(wd, 1) > 0) << 1) | ((E::lane(wd, 2) > 0) << 2) |
                    ((E::lane(wd, 3) > 0) << 3);
     s_sm[i] = uint8_t(mk);
-    if (i < 4 * TW) {
-        int s = i / TW, j = i % TW;
-        s_hv[s][j] = g.nb[s] >= 0 ? __ldcg(c.h + int64_t(g.nb[s]) * TPIX + halo_index(s, j)) : HINF;
-    }
+    if (i < 4 * TW) s_hv[i / TW][i % TW] = in.hv;
     if (i == 0) s_side = 0;
     __syncthreads();
     // Most passes of a relabel revisit a tile whose heights are already a
@@ -425,6 +447,11 @@ __device__ __forceinline__ TileResult bfs_sink_tile(const Ctx &c, int32_t t) {
 }
 
 template <class E>
+__device__ __forceinline__ TileResult bfs_sink_tile(const Ctx &c, int32_t t) {
+    return bfs_sink_tile<E>(c, t, bfs_sink_load<E>(c, t));
+}
+
+template <class E>
 __global__ void __launch_bounds__(NTT, 2) k_bfs_sink(Ctx c, int k, LaunchCtl lc) {
     tile_loop(c, k, lc, [&](int32_t t) { return bfs_sink_tile<E>(c, t); });
 }
@@ -440,7 +467,6 @@ __global__ void __launch_bounds__(NTT, 2) k_bfs_sink(Ctx c, int k, LaunchCtl lc)
 template <class E>
 __device__ __forceinline__ TileResult bfs_src_tile(const Ctx &c, int32_t t, int32_t *spoil = nullptr) {
     const int i = threadIdx.x, lx = i & 31, ly = i >> 5;
-    const TileNb g = tile_nbs(c, t);
     const int64_t p = int64_t(t) * TPIX + i;
     const uint8_t l0 = __ldcg(c.lab + p);
     // a tile whose every pixel is already in the closure cannot change
@@ -452,7 +478,8 @@ __device__ __forceinline__ TileResult bfs_src_tile(const Ctx &c, int32_t t, int3
     if (i < 4 * TW) {
         int s = i / TW, j = i % TW;
         int32_t v = HINF;
-        if (g.nb[s] >= 0 && __ldcg(c.lab + int64_t(g.nb[s]) * TPIX + halo_index(s, j))) v = 0;
+        const int32_t nb = tile_nb(c, t, s);   // (own side's id only, as in bfs_sink_load)
+        if (nb >= 0 && __ldcg(c.lab + int64_t(nb) * TPIX + halo_index(s, j))) v = 0;
         s_hv[s][j] = v;
     }
     if (i == 0) s_side = 0;
@@ -463,14 +490,24 @@ __device__ __forceinline__ TileResult bfs_src_tile(const Ctx &c, int32_t t, int3
     if (lx < TW - 1) mk |= ((s_bits[i + 1] >> DL) & 1) << 1;
     if (ly > 0) mk |= ((s_bits[i - TW] >> DD) & 1) << 2;
     if (ly < TH - 1) mk |= ((s_bits[i + TW] >> DU) & 1) << 3;
-    if (lx == 0 && g.nb[DL] >= 0)
-        mk |= (E::lane(E::load(c.r, int64_t(g.nb[DL]) * TPIX + halo_index(DL, ly)), DR) > 0) << 0;
-    if (lx == TW - 1 && g.nb[DR] >= 0)
-        mk |= (E::lane(E::load(c.r, int64_t(g.nb[DR]) * TPIX + halo_index(DR, ly)), DL) > 0) << 1;
-    if (ly == 0 && g.nb[DU] >= 0)
-        mk |= (E::lane(E::load(c.r, int64_t(g.nb[DU]) * TPIX + halo_index(DU, lx)), DD) > 0) << 2;
-    if (ly == TH - 1 && g.nb[DD] >= 0)
-        mk |= (E::lane(E::load(c.r, int64_t(g.nb[DD]) * TPIX + halo_index(DD, lx)), DU) > 0) << 3;
+    // border pixels: the facing neighbour's arc into us (its id read by the
+    // border threads of that side only)
+    if (lx == 0) {
+        const int32_t nb = tile_nb(c, t, DL);
+        if (nb >= 0) mk |= (E::lane(E::load(c.r, int64_t(nb) * TPIX + halo_index(DL, ly)), DR) > 0) << 0;
+    }
+    if (lx == TW - 1) {
+        const int32_t nb = tile_nb(c, t, DR);
+        if (nb >= 0) mk |= (E::lane(E::load(c.r, int64_t(nb) * TPIX + halo_index(DR, ly)), DL) > 0) << 1;
+    }
+    if (ly == 0) {
+        const int32_t nb = tile_nb(c, t, DU);
+        if (nb >= 0) mk |= (E::lane(E::load(c.r, int64_t(nb) * TPIX + halo_index(DU, lx)), DD) > 0) << 2;
+    }
+    if (ly == TH - 1) {
+        const int32_t nb = tile_nb(c, t, DD);
+        if (nb >= 0) mk |= (E::lane(E::load(c.r, int64_t(nb) * TPIX + halo_index(DD, lx)), DU) > 0) << 3;
+    }
     s_sm[i] = uint8_t(mk);
     __syncthreads();
     tile_relax(s_sd, s_sm, s_hv, 0);
