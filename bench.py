@@ -368,8 +368,8 @@ def roofline_of(stats, steps, config):
                 "tile_passes_per_step": {k.replace("_tile_passes", ""): stats[-1][k] for k in ASYNC_BYTES},
                 "avg_launch_us": kern_ms * 1e3 / steps,
                 "time_share": {"k_async": round(kern_ms / total_ms, 4) if total_ms else None},
-                "limiter": "latency / issue, not HBM: working set L2-resident (profiles/r02l_ncu_full.md: "
-                           "k_async C3 DRAM 0.9 %, issue slots 40 %, barrier 58 % of stall samples, most of it idle CTAs "
+                "limiter": "latency / issue, not HBM: working set L2-resident (profiles/r02n_ncu_full.md: "
+                           "k_async C3 DRAM 0.9 %, issue slots 42 %, barrier 58 % of stall samples, most of it idle CTAs "
                            "waiting for work in the single-image tail)"}
     push_ms = sum(s["ms_push"] for s in stats)
     launches = max(1, sum(s["push_sweeps"] for s in stats))
@@ -386,7 +386,7 @@ def roofline_of(stats, steps, config):
             "bytes_per_pixel_pass": bpp, "pixel_passes_per_s": passes * 1024 / sec,
             "avg_launch_us": sec / launches * 1e6, "launches_per_step": launches / steps,
             "time_share": share,
-            "limiter": "instruction issue, not HBM (profiles/r02l_ncu_full.md: k_push C5 issue slots 64 %, "
+            "limiter": "instruction issue, not HBM (profiles/r02n_ncu_full.md: k_push C5 issue slots 64 %, "
                        "IPC 2.6, DRAM 3.9 %, barrier 42 % of stall samples): up to 16 shared-memory "
                        "push-relabel iterations per pixel-pass"}
 
